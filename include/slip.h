@@ -1,0 +1,298 @@
+/* slip.h — C ABI of libslip.so, the B200-native hot path of SlipStream
+ * (arXiv 2405.14009): a per-stage transformer training step whose backward is
+ * split into B (input gradients, on the critical path) and W (weight
+ * gradients, deferred into pipeline bubbles), followed by the per-stage DP
+ * all-reduce and a staggered per-stage AdamW step; the micro-batches of failed
+ * (masked) workers are re-routed to their data-parallel peers by a
+ * deterministic CPU planner.
+ *
+ * Citations are PAPER.md lines (section / equation / figure):
+ *   §3.1 Adaptive Pipelining ........... lines 197-229, Figs. 2 and 5
+ *   §3.2 Decoupled BackProp ............ lines 250-292, Figs. 3, 4 and 6
+ *   §3.3 Staggered Optimizer ........... lines 294-305, Fig. 7
+ *   §3.4 Multiple failures ............. lines 309-345, Fig. 8
+ *   §4.2 Planner (5-tuple, S, Eqs. 1-6)  lines 372-549
+ *   §4.3 Implementation (ReRouteAct/Grad, WeightGradStore, AdamW) lines 550-583
+ *
+ * Conventions (all entry points):
+ *   - extern "C"; no C++ or torch types cross the boundary; no exceptions.
+ *   - Every pointer is caller-owned.  "device" pointers are CUDA global memory
+ *     of the context's device; "host" pointers are CPU memory.
+ *   - GPU work is enqueued asynchronously on the stream argument (a
+ *     cudaStream_t passed as slip_stream; NULL = legacy default stream).  Input
+ *     buffers must stay valid until that work completes.
+ *   - The library never allocates device memory on the hot path: the caller
+ *     allocates parameters, the stash arena and the workspace after querying
+ *     their sizes.  (NCCL allocates its own buffers in slip_comm_*.)
+ *   - Errors: a non-zero slip_status; slip_last_error() returns a thread-local
+ *     message for the last failing call.  Device faults surface at the next
+ *     synchronising call.  There is no CPU fallback: a call that cannot run
+ *     on the GPU fails with SLIP_ECUDA / SLIP_EUNSUPPORTED.
+ *
+ * Numerics (readings R1, R10, R23): bf16 storage (RNE), fp32
+ * accumulation in tensor memory (tcgen05), fp32 LayerNorm statistics, fp32
+ * softmax, attention scores S and dP as fp32 transients, fp32 master weights,
+ * gradients and Adam moments.
+ */
+#ifndef SLIP_H
+#define SLIP_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct CUstream_st* slip_stream; /* == cudaStream_t */
+typedef struct slip_ctx slip_ctx;
+typedef struct slip_comm slip_comm;
+
+typedef enum {
+  SLIP_OK = 0,
+  SLIP_EINVAL = 1,              /* bad argument / shape / pointer */
+  SLIP_EUNRECOVERABLE = 2,      /* some stage lost every worker (§3.4) */
+  SLIP_EINFEASIBLE_MEMORY = 3,  /* m_limit admits no schedule (Eq. 6) */
+  SLIP_ESTATE = 4,              /* slot state machine violated (e.g. B before F) */
+  SLIP_ECUDA = 5,
+  SLIP_ENCCL = 6,
+  SLIP_ENONFINITE = 7,
+  SLIP_EUNSUPPORTED = 8         /* shape outside the kernels' envelope */
+} slip_status;
+
+/* Op phases of the plan (§4.2 5-tuple c ∈ {F, B_input, B_weight};
+ * BC = coupled backward; OPT = optimizer step of one worker; AR = the stage's
+ * DP all-reduce, which runs on the communication stream). */
+typedef enum { SLIP_F = 0, SLIP_B = 1, SLIP_W = 2, SLIP_BC = 3, SLIP_OPT = 4, SLIP_AR = 5 } slip_phase;
+
+/* GPT-shaped stage.  Layer architecture (reading R1, PAPER.md line 607 names
+ * only "Megatron implementation of GPT-3"): pre-LN, biased-variance
+ * LayerNorm(eps), causal softmax attention with head dim hidden/heads, tanh-GeLU
+ * FFN of width ffn, biases on every linear.  T = seq * micro_batch tokens per
+ * micro-batch; token t = b*seq + position. */
+typedef struct {
+  int32_t hidden, heads, ffn, seq, micro_batch;
+  float ln_eps;
+} slip_model;
+
+/* Cluster (SPEC core_model.ClusterConfig): N stages x DP pipelines, m
+ * micro-batches per pipeline per iteration, live[i*DP + k] = 1 if worker
+ * W_{k_i} (stage i, pipeline k) is functional.
+ * Rank of worker (i, k) is k*N + i. */
+typedef struct {
+  int32_t num_stages, num_pipelines, num_microbatches;
+  const uint8_t* live; /* host, [N*DP] */
+} slip_cluster;
+
+/* Profiled integer costs (§4.2 "Inputs": T_F, T_Binput, T_Bweight,
+ * T_comm; A_B, A_Binput, A_Bweight, M_limit).  a_f = bytes stashed by F,
+ * a_w = bytes still held after B for the deferred W (reading R18).
+ * m_limit <= 0: unlimited. */
+typedef struct {
+  int64_t t_f, t_b, t_w, t_comm, t_ar, t_opt;
+  int64_t a_f, a_w, m_limit;
+} slip_costs;
+
+/* Planner options: decoupled = Decoupled BackProp (§3.2), staggered =
+ * Staggered Optimizer (§3.3), horizon = iterations planned (>= 1; the period
+ * is measured between the last two). */
+typedef struct {
+  int32_t decoupled, staggered, horizon;
+} slip_plan_opts;
+
+typedef struct {
+  float lr, beta1, beta2, eps, weight_decay;
+} slip_adam;
+
+/* One planned op (SPEC baseline_schedule JSON-lines schema): stage i,
+ * micro-batch j, origin pipeline k, phase, executing pipeline k_s, iteration,
+ * integer start/end.  OPT: mb = origin = -1.  AR: mb = origin = exec = -1. */
+typedef struct {
+  int32_t stage, mb, origin, phase, exec, iter;
+  int64_t start, end;
+} slip_op;
+
+/* ------------------------------------------------------------------ misc */
+int32_t slip_version(void);
+const char* slip_last_error(void);
+const char* slip_status_str(slip_status s);
+
+/* ------------------------------------------------------------- planner (CPU)
+ * Deterministic; identical on every rank; bit-exact with the Python oracle
+ * planner (oracle/planner.py) — DESIGN.md "Planner reading". */
+
+/* RECOVERABLE (1) iff every stage keeps a live worker (§3.4 lines
+ * 311-314); *out = 0 otherwise. */
+slip_status slip_recoverable(const slip_cluster* c, int32_t* out);
+
+/* Assignment S^{k_s}_{i,j,k}: out_exec[(i*m + j)*DP
+ * + k] = k_s.  Live workers keep their own micro-batches; the failed workers'
+ * micro-batches, enumerated in (k, j) order, go round-robin to the ascending
+ * list of live peers starting at the lowest (PAPER.md lines 203, 211-214,
+ * 554; reading R14).  SLIP_EUNRECOVERABLE if a stage has no live worker. */
+slip_status slip_assign(const slip_cluster* c, int32_t* out_exec);
+
+/* Heuristic list schedule (reading in DESIGN.md).
+ * Writes at most cap ops to out_ops (host) in canonical order: compute ops
+ * sorted by (stage, exec, start), then AR ops by (iter, stage).  *n_ops gets
+ * the total count (call with cap = 0 to size the buffer).  out_makespans
+ * (host, [horizon], may be NULL) gets the per-iteration makespan, *out_period
+ * (may be NULL) the steady-state period. */
+slip_status slip_plan_schedule(const slip_cluster* c, const slip_costs* costs, const slip_plan_opts* opts,
+                               slip_op* out_ops, int64_t cap, int64_t* n_ops, int64_t* out_makespans,
+                               int64_t* out_period);
+
+/* FNV-1a 64 over the op fields (int64 little-endian, list order). */
+uint64_t slip_plan_hash(const slip_op* ops, int64_t n);
+
+/* ------------------------------------------------------------------ sizes
+ * Parameter layout (flat, per layer, row-major, layers consecutive):
+ *   Wqkv[3h,h] bqkv[3h] Wo[h,h] bo[h] g1[h] b1n[h] g2[h] b2n[h]
+ *   W1[f,h] b1[f] W2[h,f] b2[h]                        (12h^2+13h for f = 4h)
+ * QKV rows are the [Q; K; V] blocks; head n uses rows n*d .. (n+1)*d - 1 of
+ * each block.  Linear weights are [out, in]. */
+slip_status slip_param_count(const slip_model* m, int32_t n_layers, int64_t* out);
+
+/* Bytes of the stash arena for n_slots in-flight micro-batches (F-stash +
+ * W-stash, the WeightGradStore of PAPER.md line 558), and of the shared
+ * workspace (attention score / dP transients, reduction partials). */
+slip_status slip_stash_bytes(const slip_model* m, int32_t n_layers, int32_t n_slots, size_t* out);
+slip_status slip_workspace_bytes(const slip_model* m, size_t* out);
+
+/* ------------------------------------------------------------ stage context
+ * One per rank: a stage of n_layers layers on the current CUDA device. */
+slip_status slip_ctx_create(slip_ctx** out, const slip_model* m, int32_t n_layers, int32_t n_slots);
+slip_status slip_ctx_destroy(slip_ctx* ctx);
+
+/* Bind caller-owned device buffers.  w_bf16: [n_params] bf16 weights read by
+ * F/B; master, grad, adam_m, adam_v: [n_params] fp32; arena/workspace sized
+ * by the queries above.  All device pointers, 256-byte aligned.  Resets every
+ * slot to FREE. */
+slip_status slip_stage_bind(slip_ctx* ctx, void* w_bf16, float* master, float* grad, float* adam_m, float* adam_v,
+                            int64_t n_params, void* arena, size_t arena_bytes, void* workspace, size_t ws_bytes);
+
+/* Device address inside the arena of a slot's stage input (which = 0, [T,h]
+ * bf16) or stage-output gradient (which = 1, [T,h] bf16), so that a receiver
+ * can ncclRecv straight into the slot (then pass that pointer as x_in / dy). */
+slip_status slip_slot_ptr(slip_ctx* ctx, int32_t slot, int32_t which, void** out);
+
+/* ------------------------------------------------------------------ hot path
+ * Slot state machine (per slot): FREE -F-> F_DONE -B-> B_DONE -W-> FREE.
+ * Violations return SLIP_ESTATE without enqueuing work. */
+
+/* F (§4.2 c = F): x_in [T,h] bf16 device -> y_out [T,h] bf16
+ * device, through all layers of the stage; writes the slot's F-stash.  x_in
+ * is copied into the slot unless it already is the slot's input buffer. */
+slip_status slip_stage_forward(slip_ctx* ctx, int32_t slot, const void* x_in, void* y_out, slip_stream s);
+
+/* B = B_input (§3.2): dy [T,h] bf16 = dL/d(stage
+ * output) -> dx [T,h] bf16 = dL/d(stage input) (dx may be NULL on stage 0).
+ * Also produces the bias and LayerNorm gamma/beta gradients (reading R9),
+ * added to (accumulate = 1) or written over (accumulate = 0) the fp32 grad
+ * buffer, and converts the F-stash into the W-stash. */
+slip_status slip_backward_input(slip_ctx* ctx, int32_t slot, const void* dy, void* dx, int32_t accumulate,
+                                slip_stream s);
+
+/* W = B_weight (§3.2; WeightBackwardPass line 558): for every layer
+ * dW2 (+)= dOut^T G, dW1 (+)= dH^T Y2, dWo (+)= dX2^T O, dWqkv (+)= dQKV^T Y1
+ * into the fp32 grad buffer, fused in the tcgen05 GEMM epilogue.  Frees the
+ * slot. */
+slip_status slip_backward_weight(slip_ctx* ctx, int32_t slot, int32_t accumulate, slip_stream s);
+
+/* Coupled backward (the conventional baseline): B then W
+ * of the same slot back to back. */
+slip_status slip_backward_coupled(slip_ctx* ctx, int32_t slot, const void* dy, void* dx, int32_t accumulate,
+                                  slip_stream s);
+
+/* AdamW on the whole stage (§4.3; reading R11):
+ * g <- grad_scale*g; m, v moments; bias correction with step (>= 1); decay
+ * on the 2-D weights only; refresh w_bf16 = RNE(master).  d_nonfinite
+ * (device int32, may be NULL) is OR-ed with 1 if any gradient element is not
+ * finite (local post-step validation). */
+slip_status slip_optimizer_step(slip_ctx* ctx, const slip_adam* a, int64_t step, float grad_scale,
+                                int32_t* d_nonfinite, slip_stream s);
+
+/* Last-stage loss head: l = 1/2 ||y - target||^2 / (T h),
+ * dy = (y - target) / (T h) as bf16; *d_loss (device fp32) = l. */
+slip_status slip_loss_mse(slip_ctx* ctx, const void* y, const void* target, void* dy, float* d_loss,
+                          slip_stream s);
+
+/* Stage-0 synthetic input for throughput runs: n bf16 values ~ N(0,1) from a
+ * counter-based generator keyed by (seed, k, j), so a re-routed micro-batch
+ * sees the same data on whichever peer runs it. */
+slip_status slip_synth_normal(void* out_bf16, int64_t n, uint64_t seed, uint64_t k, uint64_t j, slip_stream s);
+
+/* w_bf16 <- RNE(master) (after loading master weights). */
+slip_status slip_weights_from_master(slip_ctx* ctx, slip_stream s);
+
+/* Diagnostic entry to one GEMM of the tcgen05 family, for kernel-level parity
+ * tests: D[M,N] = sum_k A(m,k) B(k,n), bf16 operands, fp32 accumulation.
+ * A(m,k) = a[m*lda + k] (a_mn = 0) or a[k*lda + m] (a_mn = 1);
+ * B(k,n) = b[n*ldb + k] (b_mn = 0) or b[k*ldb + n] (b_mn = 1) (a_mn = 1 needs
+ * b_mn = 1).  mode 0: c bf16 = alpha*D; 3: c fp32 = alpha*D; 4: c fp32 (+)= D
+ * (accumulate).  bn: N tile, one of 32, 64, 80, 128, 256.  Device pointers,
+ * 16-byte aligned rows. */
+slip_status slip_gemm(int32_t M, int32_t N, int32_t K, const void* a, int64_t lda, int32_t a_mn, const void* b,
+                      int64_t ldb, int32_t b_mn, void* c, int64_t ldc, int32_t mode, int32_t bn, int32_t accumulate,
+                      float alpha, slip_stream s);
+
+/* --------------------------------------------------------------- NCCL comms
+ * rank r of world; the 128-byte id is created by rank 0 with
+ * slip_nccl_unique_id and broadcast by the caller (torch.distributed). */
+slip_status slip_nccl_unique_id(uint8_t out_id[128]);
+slip_status slip_comm_create(slip_comm** out, int32_t rank, int32_t world, const uint8_t id[128]);
+/* Collective over the world: builds the stage communicator over the live peers
+ * of every stage (failed ranks are left out) and one communicator per directed
+ * worker pair that the plan can use for activations / gradients
+ * (ReRouteAct / ReRouteGrad). */
+slip_status slip_comm_setup(slip_comm* comm, const slip_cluster* c);
+slip_status slip_comm_destroy(slip_comm* comm);
+
+/* In-place fp32 sum of the stage gradient over the live peers of the caller's
+ * stage ("all-reduce collective"; reading R13).  A
+ * singleton group returns without communicating. */
+slip_status slip_grad_allreduce(slip_ctx* ctx, slip_comm* comm, slip_stream s);
+
+/* ------------------------------------------------------------------ executor
+ * Host buffers for an end-to-end run (may be NULL: inputs are then generated
+ * on the device by slip_synth_normal with (seed, k, j) and targets with
+ * (seed + 1, k, j)).  x_host[k*m + j] / target_host[k*m + j]: pinned host
+ * [T,h] bf16; loss_host[k*m + j] receives each micro-batch's loss. */
+typedef struct {
+  const void* const* x_host;
+  const void* const* target_host;
+  float* loss_host;
+} slip_io;
+
+typedef struct {
+  double period_ms;          /* measured wall period per iteration (CUDA events) */
+  double total_ms;           /* all timed iterations */
+  int64_t predicted_period;  /* planner units */
+  int64_t n_ops;             /* ops executed by this rank per iteration */
+  int64_t n_kernels;         /* kernels launched by this rank in the timed iterations */
+  uint64_t plan_hash;
+  float last_loss;           /* mean loss of the micro-batches whose last stage ran here */
+  int32_t nonfinite;
+  /* per-phase device time summed over the timed iterations (CUDA events on the
+   * compute stream around each op; includes waits on incoming transfers) and op
+   * counts: index = slip_phase (F, B, W, BC, OPT, AR) */
+  double phase_ms[6];
+  int64_t phase_ops[6];
+  int64_t w_gemm_launches;   /* tcgen05 GEMM launches issued by the W / BC ops */
+} slip_report;
+
+/* Runs `iterations` training iterations of the plan on this rank (worker
+ * (i, k) with rank = k*N + i, stage = the ctx's stage): F / B / W / BC ops in
+ * planned order on the compute stream, activation / gradient P2P on per-pair
+ * streams, the stage all-reduce after the stage's last W, then the staggered
+ * AdamW step.  Masked ranks return immediately.  warmup iterations are run
+ * first and not timed. */
+slip_status slip_execute_schedule(slip_ctx* ctx, slip_comm* comm, const slip_cluster* c, const slip_costs* costs,
+                                  const slip_plan_opts* opts, const slip_adam* adam, int32_t warmup,
+                                  int32_t iterations, uint64_t seed, const slip_io* io, slip_stream s,
+                                  slip_report* out);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SLIP_H */

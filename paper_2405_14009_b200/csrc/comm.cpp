@@ -1,0 +1,144 @@
+// comm.cpp — NCCL bootstrap, per-stage and per-pair communicators, the stage gradient
+// all-reduce (slip_grad_allreduce).
+#include "comm.h"
+
+#include <cstring>
+#include <set>
+#include <string>
+
+#include "common.h"
+#include "stage.h"
+
+namespace slip {
+slip_status nccl_status(ncclResult_t r, const char* where) {
+  if (r == ncclSuccess) return SLIP_OK;
+  set_error(std::string(where) + ": " + ncclGetErrorString(r));
+  return SLIP_ENCCL;
+}
+}  // namespace slip
+
+#define SLIP_NCCL(expr)                                        \
+  do {                                                         \
+    ncclResult_t _r = (expr);                                  \
+    if (_r != ncclSuccess) return ::slip::nccl_status(_r, #expr); \
+  } while (0)
+
+using namespace slip;
+
+namespace {
+
+void destroy_setup(slip_comm* c) {
+  for (auto& kv : c->pair_comm)
+    if (kv.second) ncclCommDestroy(kv.second);
+  for (auto& kv : c->pair_stream)
+    if (kv.second) cudaStreamDestroy(kv.second);
+  c->pair_comm.clear();
+  c->pair_stream.clear();
+  if (c->stage_comm) ncclCommDestroy(c->stage_comm);
+  c->stage_comm = nullptr;
+  if (c->ar_stream) cudaStreamDestroy(c->ar_stream);
+  c->ar_stream = nullptr;
+  c->ready = false;
+}
+
+}  // namespace
+
+extern "C" {
+
+slip_status slip_nccl_unique_id(uint8_t out_id[128]) {
+  SLIP_CHECK(out_id, SLIP_EINVAL, "nccl_unique_id: out is NULL");
+  static_assert(sizeof(ncclUniqueId) == 128, "ncclUniqueId size");
+  ncclUniqueId id;
+  SLIP_NCCL(ncclGetUniqueId(&id));
+  std::memcpy(out_id, &id, 128);
+  return SLIP_OK;
+}
+
+slip_status slip_comm_create(slip_comm** out, int32_t rank, int32_t world, const uint8_t id[128]) {
+  SLIP_CHECK(out && id && world >= 1 && rank >= 0 && rank < world, SLIP_EINVAL, "comm_create: bad arguments");
+  ncclUniqueId uid;
+  std::memcpy(&uid, id, 128);
+  slip_comm* c = new slip_comm();
+  c->rank = rank;
+  c->world = world;
+  ncclResult_t r = ncclCommInitRank(&c->world_comm, world, uid, rank);
+  if (r != ncclSuccess) {
+    delete c;
+    return nccl_status(r, "ncclCommInitRank");
+  }
+  *out = c;
+  return SLIP_OK;
+}
+
+slip_status slip_comm_setup(slip_comm* c, const slip_cluster* cl) {
+  SLIP_CHECK(c && c->world_comm, SLIP_EINVAL, "comm_setup: comm not created");
+  Cluster cc;
+  SLIP_TRY(read_cluster(cl, cc));
+  SLIP_CHECK(cc.N * cc.DP == c->world, SLIP_EINVAL, "comm_setup: world size must equal N * DP");
+  std::vector<int> ex;
+  if (!assign(cc, ex)) {
+    set_error("comm_setup: unrecoverable failure set");
+    return SLIP_EUNRECOVERABLE;
+  }
+  destroy_setup(c);
+  c->cl = cc;
+  c->my_stage = c->rank % cc.N;
+  c->my_pipe = c->rank / cc.N;
+  c->my_live = cc.is_live(c->my_stage, c->my_pipe);
+  SLIP_CUDA(cudaStreamCreateWithFlags(&c->ar_stream, cudaStreamNonBlocking));
+  // stage communicator over the live peers (color = stage), failed ranks excluded
+  int n_live = 0;
+  for (int k = 0; k < cc.DP; ++k) n_live += cc.is_live(c->my_stage, k);
+  ncclComm_t sc = nullptr;
+  SLIP_NCCL(ncclCommSplit(c->world_comm, c->my_live ? c->my_stage : NCCL_SPLIT_NOCOLOR, c->my_pipe, &sc, nullptr));
+  c->stage_size = c->my_live ? n_live : 0;
+  if (sc && n_live <= 1) {
+    ncclCommDestroy(sc);
+    sc = nullptr;
+  }
+  c->stage_comm = sc;
+  // directed pairs used by the assignment (ACT i -> i+1, GRAD i+1 -> i), in a fixed order
+  std::set<std::pair<int, int>> pairs;
+  for (int k = 0; k < cc.DP; ++k)
+    for (int j = 0; j < cc.m; ++j)
+      for (int i = 0; i + 1 < cc.N; ++i) {
+        const int a = rank_of(cc.N, i, ex[(static_cast<size_t>(i) * cc.m + j) * cc.DP + k]);
+        const int b = rank_of(cc.N, i + 1, ex[(static_cast<size_t>(i + 1) * cc.m + j) * cc.DP + k]);
+        pairs.insert({a, b});
+        pairs.insert({b, a});
+      }
+  int color = 0;
+  for (const auto& pr : pairs) {
+    const bool member = c->rank == pr.first || c->rank == pr.second;
+    ncclComm_t pc = nullptr;
+    SLIP_NCCL(ncclCommSplit(c->world_comm, member ? color : NCCL_SPLIT_NOCOLOR, c->rank == pr.first ? 0 : 1, &pc,
+                            nullptr));
+    if (member) {
+      c->pair_comm[pr] = pc;
+      cudaStream_t st;
+      SLIP_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+      c->pair_stream[pr] = st;
+    }
+    ++color;
+  }
+  c->ready = true;
+  return SLIP_OK;
+}
+
+slip_status slip_comm_destroy(slip_comm* c) {
+  if (!c) return SLIP_OK;
+  destroy_setup(c);
+  if (c->world_comm) ncclCommDestroy(c->world_comm);
+  delete c;
+  return SLIP_OK;
+}
+
+slip_status slip_grad_allreduce(slip_ctx* ctx, slip_comm* c, slip_stream s) {
+  SLIP_CHECK(ctx && ctx->bound && c && c->ready, SLIP_EINVAL, "grad_allreduce: ctx not bound or comm not set up");
+  if (!c->my_live || !c->stage_comm) return SLIP_OK;  // failed rank or singleton group
+  SLIP_NCCL(ncclAllReduce(ctx->grad, ctx->grad, static_cast<size_t>(ctx->n_params), ncclFloat32, ncclSum,
+                          c->stage_comm, reinterpret_cast<cudaStream_t>(s)));
+  return SLIP_OK;
+}
+
+}  // extern "C"

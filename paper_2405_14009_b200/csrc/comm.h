@@ -1,0 +1,33 @@
+// comm.h — NCCL communicators of one rank: world, per-stage live-peer group (DP
+// all-reduce) and one communicator + stream per directed worker pair
+// that the plan uses (ReRouteAct / ReRouteGrad).
+#pragma once
+#include <cuda_runtime.h>
+#include <nccl.h>
+
+#include <map>
+#include <utility>
+#include <vector>
+
+#include "planner.h"
+
+struct slip_comm {
+  int rank = 0, world = 1;
+  ncclComm_t world_comm = nullptr;
+  bool ready = false;
+  slip::Cluster cl;
+  int my_stage = 0, my_pipe = 0;
+  bool my_live = true;
+  ncclComm_t stage_comm = nullptr;  // live peers of my stage (nullptr if singleton / failed)
+  int stage_size = 1;
+  cudaStream_t ar_stream = nullptr;
+  // directed pair (src rank, dst rank) -> communicator in which src is rank 0, dst rank 1
+  std::map<std::pair<int, int>, ncclComm_t> pair_comm;
+  std::map<std::pair<int, int>, cudaStream_t> pair_stream;
+};
+
+namespace slip {
+// worker (stage i, pipeline k) <-> rank k*N + i
+inline int rank_of(int N, int i, int k) { return k * N + i; }
+slip_status nccl_status(ncclResult_t r, const char* where);
+}  // namespace slip

@@ -1,0 +1,500 @@
+// gemm.cu — warp-specialised persistent tcgen05 GEMM for sm_100a.
+//
+// One kernel family serves every dense contraction of the stage step (F, B and W
+// linears; S = QK^T, PV, dP, dV, dQ, dK of attention):
+//   warp 0      : TMA producer (one lane) — A/B tiles into a STAGES-deep smem ring
+//   warp 1      : MMA issuer  (one lane) — tcgen05.mma.cta_group::1.kind::f16, M=128, N=BN, K=16
+//   warp 2      : TMEM allocator (2 x ACC_COLS fp32 accumulators = double buffer)
+//   warps 4..7  : epilogue — tcgen05.ld 32x32b, then bias / GeLU / GeLU' / residual and bf16
+//                 stores, or fp32 TMA store / TMA reduce-add (W: dW += dY^T X fused here).
+// Tiles are 128 x BN x 64 (K), statically scheduled round-robin over a grid of
+// min(#tiles, #SMs) CTAs; the epilogue of tile i overlaps the mainloop of tile i+1.
+#include <cudaTypedefs.h>
+
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+
+#include "gemm.cuh"
+#include "ptx.cuh"
+
+namespace slip {
+namespace {
+
+constexpr int BM = 128;
+constexpr int BK = 64;
+constexpr int NUM_THREADS = 256;
+constexpr int EPI_WARP0 = 4;
+
+template <int BN, bool A_MN, bool B_MN>
+struct Cfg {
+  static_assert(BN % 16 == 0 && BN >= 16 && BN <= 256, "UMMA N for M=128");
+  static constexpr int A_BYTES = BM * BK * 2;
+  static constexpr int B_ATOMS = (BN + 63) / 64;
+  static constexpr int B_BYTES = B_MN ? B_ATOMS * 8192 : BN * 128;
+  static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+  static constexpr int STAGES = (196608 / STAGE_BYTES) > 8 ? 8 : (196608 / STAGE_BYTES);
+  static constexpr int ACC_COLS = (BN + 31) / 32 * 32;
+  static constexpr int TMEM_COLS = 2 * ACC_COLS <= 32    ? 32
+                                   : 2 * ACC_COLS <= 64  ? 64
+                                   : 2 * ACC_COLS <= 128 ? 128
+                                   : 2 * ACC_COLS <= 256 ? 256
+                                                         : 512;
+  static constexpr int EPI_BYTES = 4 * 32 * 128;  // one 32x32 fp32 staging tile per epilogue warp
+  static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + EPI_BYTES + 1024 + 1024;
+  static constexpr uint32_t IDESC = ptx::idesc_bf16_f32(BM, BN, A_MN, B_MN);
+  static constexpr uint32_t A_KSTEP = A_MN ? 2048 : 32;  // bytes per UMMA_K = 16
+  static constexpr uint32_t B_KSTEP = B_MN ? 2048 : 32;
+  static constexpr uint32_t A_LBO = A_MN ? 8192 : 16;
+  static constexpr uint32_t B_LBO = B_MN ? 8192 : 16;
+  static_assert(SMEM_BYTES <= 232448, "smem budget");
+};
+
+struct KParams {
+  int M, N, K;
+  int zi_count;
+  int mt, nt, nkb;
+  int per_z, total;
+  int causal;
+  int mode;
+  void* c;
+  int64_t ldc, c_zi, c_zo;
+  const __nv_bfloat16* bias;
+  const __nv_bfloat16* resid;
+  __nv_bfloat16* aux;
+  float alpha;
+  int accumulate;
+};
+
+struct Tile {
+  int zi, zo, m0, n0, kb0, kb1;
+};
+
+template <int BN>
+__device__ __forceinline__ Tile decode_tile(int t, const KParams& p) {
+  Tile r;
+  const int z = t / p.per_z;
+  const int q = t - z * p.per_z;
+  int mb, nb;
+  if (p.causal == CAUSAL_TILES) {
+    mb = static_cast<int>((sqrtf(8.0f * q + 1.0f) - 1.0f) * 0.5f);
+    while ((mb + 1) * (mb + 2) / 2 <= q) ++mb;
+    while (mb * (mb + 1) / 2 > q) --mb;
+    nb = q - mb * (mb + 1) / 2;
+  } else {
+    mb = q % p.mt;
+    nb = q / p.mt;
+  }
+  r.zi = z % p.zi_count;
+  r.zo = z / p.zi_count;
+  r.m0 = mb * BM;
+  r.n0 = nb * BN;
+  r.kb0 = 0;
+  r.kb1 = p.nkb;
+  if (p.causal == CAUSAL_K_UPPER) {
+    const int lim = (r.m0 + BM + BK - 1) / BK;
+    r.kb1 = lim < p.nkb ? lim : p.nkb;
+  } else if (p.causal == CAUSAL_K_LOWER) {
+    r.kb0 = r.m0 / BK;
+  }
+  return r;
+}
+
+__device__ __forceinline__ float gelu_f(float x) {
+  const float c = 0.7978845608028654f, a = 0.044715f;
+  return 0.5f * x * (1.0f + ptx::tanh_fast(c * (x + a * x * x * x)));
+}
+__device__ __forceinline__ float gelu_grad_f(float x) {
+  const float c = 0.7978845608028654f, a = 0.044715f;
+  const float t = ptx::tanh_fast(c * (x + a * x * x * x));
+  return 0.5f * (1.0f + t) + 0.5f * x * (1.0f - t * t) * c * (1.0f + 3.0f * a * x * x);
+}
+
+__device__ __forceinline__ void unpack8(const uint4& u, float (&f)[8]) {
+  const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&u);
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    float2 v = __bfloat1622float2(h[i]);
+    f[2 * i] = v.x;
+    f[2 * i + 1] = v.y;
+  }
+}
+__device__ __forceinline__ uint4 pack8(const float (&f)[8]) {
+  uint4 u;
+  __nv_bfloat162* h = reinterpret_cast<__nv_bfloat162*>(&u);
+#pragma unroll
+  for (int i = 0; i < 4; ++i) h[i] = __floats2bfloat162_rn(f[2 * i], f[2 * i + 1]);
+  return u;
+}
+
+template <int BN, bool A_MN, bool B_MN>
+__global__ void __launch_bounds__(NUM_THREADS, 1)
+    gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                   const __grid_constant__ CUtensorMap tmC, const KParams p) {
+  using C = Cfg<BN, A_MN, B_MN>;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* ring = smem;
+  float* epi = reinterpret_cast<float*>(smem + C::STAGES * C::STAGE_BYTES);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::STAGES * C::STAGE_BYTES + C::EPI_BYTES);
+  uint64_t* full = bars;
+  uint64_t* empty = bars + C::STAGES;
+  uint64_t* tfull = bars + 2 * C::STAGES;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(tempty + 2);
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < C::STAGES; ++s) {
+      ptx::mbar_init(&full[s], 1);
+      ptx::mbar_init(&empty[s], 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      ptx::mbar_init(&tfull[a], 1);
+      ptx::mbar_init(&tempty[a], 4);
+    }
+    ptx::fence_mbar_init();
+  }
+  if (warp == 0 && lane == 0) {
+    ptx::prefetch_tmap(&tmA);
+    ptx::prefetch_tmap(&tmB);
+    if (p.mode >= EPI_F32_STORE) ptx::prefetch_tmap(&tmC);
+  }
+  if (warp == 2) ptx::tmem_alloc<C::TMEM_COLS>(tmem_holder);
+  ptx::tc_fence_before();
+  __syncthreads();
+  ptx::tc_fence_after();
+  const uint32_t tmem_base = *tmem_holder;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      // ---------------------------------------------------------------- TMA producer
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int t = blockIdx.x; t < p.total; t += gridDim.x) {
+        const Tile tl = decode_tile<BN>(t, p);
+        for (int kb = tl.kb0; kb < tl.kb1; ++kb) {
+          ptx::mbar_wait(&empty[stage], phase ^ 1);
+          uint8_t* sa = ring + stage * C::STAGE_BYTES;
+          uint8_t* sb = sa + C::A_BYTES;
+          ptx::mbar_arrive_expect_tx(&full[stage], C::STAGE_BYTES);
+          if (!A_MN) {
+            ptx::tma_load_4d(&tmA, sa, &full[stage], kb * BK, tl.m0, tl.zi, tl.zo);
+          } else {
+            ptx::tma_load_4d(&tmA, sa, &full[stage], tl.m0, kb * BK, tl.zi, tl.zo);
+            ptx::tma_load_4d(&tmA, sa + 8192, &full[stage], tl.m0 + 64, kb * BK, tl.zi, tl.zo);
+          }
+          if (!B_MN) {
+            ptx::tma_load_4d(&tmB, sb, &full[stage], kb * BK, tl.n0, tl.zi, tl.zo);
+          } else {
+#pragma unroll
+            for (int a = 0; a < C::B_ATOMS; ++a)
+              ptx::tma_load_4d(&tmB, sb + a * 8192, &full[stage], tl.n0 + a * 64, kb * BK, tl.zi, tl.zo);
+          }
+          if (++stage == C::STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      // ---------------------------------------------------------------- MMA issuer
+      int stage = 0;
+      uint32_t phase = 0;
+      int acc = 0;
+      uint32_t acc_phase = 0;
+      for (int t = blockIdx.x; t < p.total; t += gridDim.x) {
+        const Tile tl = decode_tile<BN>(t, p);
+        ptx::mbar_wait(&tempty[acc], acc_phase ^ 1);
+        ptx::tc_fence_after();
+        const uint32_t d_tmem = tmem_base + acc * C::ACC_COLS;
+        for (int kb = tl.kb0; kb < tl.kb1; ++kb) {
+          ptx::mbar_wait(&full[stage], phase);
+          ptx::tc_fence_after();
+          const uint32_t a_base = ptx::smem_u32(ring + stage * C::STAGE_BYTES);
+          const uint32_t b_base = a_base + C::A_BYTES;
+#pragma unroll
+          for (int k = 0; k < BK / 16; ++k) {
+            const uint64_t ad = ptx::smem_desc_sw128(a_base + k * C::A_KSTEP, C::A_LBO, 1024);
+            const uint64_t bd = ptx::smem_desc_sw128(b_base + k * C::B_KSTEP, C::B_LBO, 1024);
+            ptx::tc_mma_f16(d_tmem, ad, bd, C::IDESC, (kb > tl.kb0 || k > 0) ? 1u : 0u);
+          }
+          ptx::tc_commit(&empty[stage]);
+          if (++stage == C::STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+        ptx::tc_commit(&tfull[acc]);
+        if (++acc == 2) {
+          acc = 0;
+          acc_phase ^= 1;
+        }
+      }
+    }
+  } else if (warp >= EPI_WARP0) {
+    // ------------------------------------------------------------------ epilogue
+    const int ew = warp - EPI_WARP0;  // == warp % 4: TMEM lanes 32*ew .. 32*ew+31
+    float* buf = epi + ew * 32 * 32;
+    int acc = 0;
+    uint32_t acc_phase = 0;
+    for (int t = blockIdx.x; t < p.total; t += gridDim.x) {
+      const Tile tl = decode_tile<BN>(t, p);
+      ptx::mbar_wait(&tfull[acc], acc_phase);
+      ptx::tc_fence_after();
+      const int row0 = tl.m0 + ew * 32;
+      const int m = row0 + lane;
+#pragma unroll 1
+      for (int ch = 0; ch < C::ACC_COLS / 32; ++ch) {
+        uint32_t r[32];
+        ptx::tmem_ld_32x32b_x32(tmem_base + (static_cast<uint32_t>(ew * 32) << 16) + acc * C::ACC_COLS + ch * 32, r);
+        ptx::tmem_ld_wait();
+        const int n = tl.n0 + ch * 32;
+        if (n >= p.N || row0 >= p.M) continue;
+        if (p.mode >= EPI_F32_STORE) {
+          if (lane == 0) ptx::bulk_wait_read0();
+          __syncwarp();
+          float4* rowp = reinterpret_cast<float4*>(buf + lane * 32);
+          const float al = (p.mode == EPI_F32_STORE) ? p.alpha : 1.0f;
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            rowp[j ^ (lane & 7)] = make_float4(al * __uint_as_float(r[4 * j]), al * __uint_as_float(r[4 * j + 1]),
+                                               al * __uint_as_float(r[4 * j + 2]), al * __uint_as_float(r[4 * j + 3]));
+          }
+          ptx::fence_proxy_async_smem();
+          __syncwarp();
+          if (lane == 0) {
+            if (p.mode == EPI_F32_ACC && p.accumulate)
+              ptx::tma_reduce_add_4d(&tmC, buf, n, row0, tl.zi, tl.zo);
+            else
+              ptx::tma_store_4d(&tmC, buf, n, row0, tl.zi, tl.zo);
+            ptx::bulk_commit();
+          }
+        } else if (m < p.M) {
+          const int64_t off = tl.zo * p.c_zo + tl.zi * p.c_zi + static_cast<int64_t>(m) * p.ldc + n;
+          __nv_bfloat16* cp = reinterpret_cast<__nv_bfloat16*>(p.c) + off;
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            const int nn = n + q * 8;
+            if (nn >= p.N) break;
+            float x[8];
+#pragma unroll
+            for (int e = 0; e < 8; ++e) x[e] = __uint_as_float(r[q * 8 + e]) * p.alpha;
+            if (p.bias) {
+              float b[8];
+              unpack8(*reinterpret_cast<const uint4*>(p.bias + nn), b);
+#pragma unroll
+              for (int e = 0; e < 8; ++e) x[e] += b[e];
+            }
+            if (p.mode == EPI_BF16_GELU) {
+              *reinterpret_cast<uint4*>(p.aux + off + q * 8) = pack8(x);
+#pragma unroll
+              for (int e = 0; e < 8; ++e) x[e] = gelu_f(x[e]);
+            } else if (p.mode == EPI_BF16_DGELU) {
+              float hv[8];
+              unpack8(*reinterpret_cast<const uint4*>(p.aux + off + q * 8), hv);
+#pragma unroll
+              for (int e = 0; e < 8; ++e) x[e] *= gelu_grad_f(hv[e]);
+            }
+            if (p.resid) {
+              float rv[8];
+              unpack8(*reinterpret_cast<const uint4*>(p.resid + off + q * 8), rv);
+#pragma unroll
+              for (int e = 0; e < 8; ++e) x[e] += rv[e];
+            }
+            *reinterpret_cast<uint4*>(cp + q * 8) = pack8(x);
+          }
+        }
+      }
+      ptx::tc_fence_before();
+      __syncwarp();
+      if (lane == 0) ptx::mbar_arrive(&tempty[acc]);
+      if (++acc == 2) {
+        acc = 0;
+        acc_phase ^= 1;
+      }
+    }
+    if (lane == 0) ptx::bulk_wait0();
+  }
+  __syncthreads();
+  if (warp == 2) {
+    ptx::tc_fence_after();
+    ptx::tmem_dealloc<C::TMEM_COLS>(tmem_base);
+  }
+}
+
+// ------------------------------------------------------------------ host side
+thread_local std::string g_msg;
+
+PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* f = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(f);
+  });
+  return fn;
+}
+
+// 4-D view: dims (inner, outer, zi, zo); strides in elements for dims 1..3.
+bool encode4d(CUtensorMap* map, CUtensorMapDataType dt, int esize, const void* base, uint64_t d0, uint64_t d1,
+              uint64_t d2, uint64_t d3, int64_t s1, int64_t s2, int64_t s3, uint32_t b0, uint32_t b1) {
+  auto fn = encode_fn();
+  if (!fn) {
+    g_msg = "cuTensorMapEncodeTiled unavailable (driver entry point)";
+    return false;
+  }
+  cuuint64_t dims[4] = {d0, d1, d2 ? d2 : 1, d3 ? d3 : 1};
+  auto fix = [](int64_t st, int64_t fallback) -> cuuint64_t {
+    int64_t v = st > 0 ? st : fallback;
+    return static_cast<cuuint64_t>(v);
+  };
+  const int64_t s1b = s1 * esize;
+  const int64_t s2b = (dims[2] > 1 ? s2 * esize : s1b * static_cast<int64_t>(d1));
+  const int64_t s3b = (dims[3] > 1 ? s3 * esize : s2b * static_cast<int64_t>(dims[2]));
+  cuuint64_t strides[3] = {fix(s1b, 16), fix(s2b, 16), fix(s3b, 16)};
+  for (int i = 0; i < 3; ++i) {
+    if (strides[i] % 16 != 0) {
+      char b[160];
+      snprintf(b, sizeof b, "TMA stride %d = %llu bytes is not a multiple of 16", i + 1,
+               static_cast<unsigned long long>(strides[i]));
+      g_msg = b;
+      return false;
+    }
+  }
+  if (reinterpret_cast<uintptr_t>(base) % 16 != 0) {
+    g_msg = "TMA base address not 16-byte aligned";
+    return false;
+  }
+  cuuint32_t box[4] = {b0, b1, 1, 1};
+  cuuint32_t est[4] = {1, 1, 1, 1};
+  CUresult r = fn(map, dt, 4, const_cast<void*>(base), dims, strides, box, est, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                  CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) {
+    char b[200];
+    snprintf(b, sizeof b, "cuTensorMapEncodeTiled failed (%d): dims %llu %llu %llu %llu box %u %u", static_cast<int>(r),
+             (unsigned long long)dims[0], (unsigned long long)dims[1], (unsigned long long)dims[2],
+             (unsigned long long)dims[3], b0, b1);
+    g_msg = b;
+    return false;
+  }
+  return true;
+}
+
+// operand view for A (rows = M) or B (rows = N)
+bool encode_operand(CUtensorMap* map, const Operand& o, int rows, int K, int zi, int zo, uint32_t box_rows) {
+  if (!o.mn_major)
+    return encode4d(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, o.ptr, K, rows, zi, zo, o.ld, o.zi_stride, o.zo_stride,
+                    64, box_rows);
+  return encode4d(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, o.ptr, rows, K, zi, zo, o.ld, o.zi_stride, o.zo_stride, 64,
+                  64);
+}
+
+template <int BN, bool A_MN, bool B_MN>
+cudaError_t launch_t(const GemmDesc& d, cudaStream_t s) {
+  using C = Cfg<BN, A_MN, B_MN>;
+  static std::once_flag once;
+  static cudaError_t attr_err = cudaSuccess;
+  std::call_once(once, [] {
+    attr_err = cudaFuncSetAttribute(gemm_tc_kernel<BN, A_MN, B_MN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    C::SMEM_BYTES);
+  });
+  if (attr_err != cudaSuccess) return attr_err;
+  CUtensorMap ta, tb, tc;
+  std::memset(&tc, 0, sizeof tc);
+  if (!encode_operand(&ta, d.a, d.M, d.K, d.zi_count, d.zo_count, BM)) return cudaErrorInvalidValue;
+  if (!encode_operand(&tb, d.b, d.N, d.K, d.zi_count, d.zo_count, BN)) return cudaErrorInvalidValue;
+  if (d.mode >= EPI_F32_STORE) {
+    if (!encode4d(&tc, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, d.c, d.N, d.M, d.zi_count, d.zo_count, d.ldc, d.c_zi,
+                  d.c_zo, 32, 32))
+      return cudaErrorInvalidValue;
+  }
+  KParams p{};
+  p.M = d.M;
+  p.N = d.N;
+  p.K = d.K;
+  p.zi_count = d.zi_count;
+  p.mt = (d.M + BM - 1) / BM;
+  p.nt = (d.N + BN - 1) / BN;
+  p.nkb = (d.K + BK - 1) / BK;
+  p.causal = d.causal;
+  p.per_z = d.causal == CAUSAL_TILES ? p.mt * (p.mt + 1) / 2 : p.mt * p.nt;
+  p.total = p.per_z * d.zi_count * d.zo_count;
+  p.mode = d.mode;
+  p.c = d.c;
+  p.ldc = d.ldc;
+  p.c_zi = d.c_zi;
+  p.c_zo = d.c_zo;
+  p.bias = static_cast<const __nv_bfloat16*>(d.bias);
+  p.resid = static_cast<const __nv_bfloat16*>(d.resid);
+  p.aux = static_cast<__nv_bfloat16*>(d.aux);
+  p.alpha = d.alpha;
+  p.accumulate = d.accumulate;
+  if (p.total == 0) return cudaSuccess;
+  const int grid = p.total < num_sms() ? p.total : num_sms();
+  gemm_tc_kernel<BN, A_MN, B_MN><<<grid, NUM_THREADS, C::SMEM_BYTES, s>>>(ta, tb, tc, p);
+  return cudaGetLastError();
+}
+
+template <int BN>
+cudaError_t launch_bn(const GemmDesc& d, cudaStream_t s) {
+  const bool am = d.a.mn_major, bm = d.b.mn_major;
+  if (!am && !bm) return launch_t<BN, false, false>(d, s);
+  if (!am && bm) return launch_t<BN, false, true>(d, s);
+  if (am && bm) return launch_t<BN, true, true>(d, s);
+  g_msg = "unsupported operand majorness (A MN-major with B K-major)";
+  return cudaErrorInvalidValue;
+}
+
+}  // namespace
+
+int num_sms() {
+  static int n = 0;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    if (n <= 0) n = 148;
+  });
+  return n;
+}
+
+const char* gemm_last_message() { return g_msg.c_str(); }
+
+cudaError_t gemm_launch(const GemmDesc& d, cudaStream_t s) {
+  g_msg.clear();
+  if (d.M <= 0 || d.N <= 0 || d.K <= 0 || d.zi_count <= 0 || d.zo_count <= 0) {
+    g_msg = "gemm: non-positive shape";
+    return cudaErrorInvalidValue;
+  }
+  if (d.mode < EPI_F32_STORE && (d.N % 8 != 0 || d.ldc % 8 != 0)) {
+    g_msg = "gemm: bf16 epilogue needs N and ldc multiples of 8";
+    return cudaErrorInvalidValue;
+  }
+  if (d.causal == CAUSAL_TILES && (d.bn != 128 || d.M != d.N)) {
+    g_msg = "gemm: causal tile skipping needs BN = 128 and M = N";
+    return cudaErrorInvalidValue;
+  }
+  switch (d.bn) {
+    case 32: return launch_bn<32>(d, s);
+    case 64: return launch_bn<64>(d, s);
+    case 80: return launch_bn<80>(d, s);
+    case 128: return launch_bn<128>(d, s);
+    case 256: return launch_bn<256>(d, s);
+    default:
+      g_msg = "gemm: unsupported BN (32, 64, 80, 128, 256)";
+      return cudaErrorInvalidValue;
+  }
+}
+
+}  // namespace slip

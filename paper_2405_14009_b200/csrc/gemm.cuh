@@ -1,0 +1,60 @@
+// gemm.cuh — host interface of the tcgen05/TMEM/TMA GEMM family used by F, B and W.
+//
+//   D[z](M x N) = sum_k A[z](m, k) * B[z](k, n)       (bf16 operands, fp32 accumulate in TMEM)
+//
+// Each operand is described by a strided view; "K-major" means k is the contiguous
+// index, "MN-major" means m (or n) is.  A batch index z = zo * zi_count + zi selects
+// (zi, zo) offsets, which covers per-(batch, head) attention views of the QKV buffer.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace slip {
+
+enum EpiMode : int {
+  EPI_BF16 = 0,        // C = bf16(alpha*acc + bias[n] + resid[m,n])
+  EPI_BF16_GELU = 1,   // H = alpha*acc + bias[n]; aux = bf16(H); C = bf16(gelu(H))
+  EPI_BF16_DGELU = 2,  // C = bf16(acc * gelu'(aux[m,n]))
+  EPI_F32_STORE = 3,   // C(f32) = alpha*acc                  (TMA store)
+  EPI_F32_ACC = 4      // C(f32) += acc, or = acc if !accumulate (TMA reduce-add / store)
+};
+
+enum Causal : int {
+  CAUSAL_NONE = 0,
+  CAUSAL_TILES = 1,    // skip tiles strictly above the diagonal (S = QK^T, dP = dO V^T); BN == 128
+  CAUSAL_K_UPPER = 2,  // k ranges over [0, m0 + 128)   (P V, dS K)
+  CAUSAL_K_LOWER = 3   // k ranges over [m0, K)          (P^T dO, dS^T Q)
+};
+
+struct Operand {
+  const void* ptr = nullptr;  // element (0,0) of batch (0,0)
+  int64_t ld = 0;             // stride (elements) of the non-contiguous index
+  int64_t zi_stride = 0;      // elements
+  int64_t zo_stride = 0;      // elements
+  bool mn_major = false;      // true: the M (or N) index is contiguous
+};
+
+struct GemmDesc {
+  int M = 0, N = 0, K = 0;
+  int zi_count = 1, zo_count = 1;
+  int bn = 256;               // N tile: 32, 80, 128 or 256
+  int causal = CAUSAL_NONE;
+  Operand a, b;
+  // epilogue
+  int mode = EPI_BF16;
+  void* c = nullptr;          // output base (bf16 or f32)
+  int64_t ldc = 0, c_zi = 0, c_zo = 0;  // element strides
+  const void* bias = nullptr;     // bf16 [N]
+  const void* resid = nullptr;    // bf16, indexed like C
+  void* aux = nullptr;            // bf16, indexed like C
+  float alpha = 1.0f;
+  int accumulate = 0;
+};
+
+// Enqueue on `s`.  Returns cudaSuccess or the launch / encode error; shape errors
+// return cudaErrorInvalidValue with a message retrievable by gemm_last_message().
+cudaError_t gemm_launch(const GemmDesc& d, cudaStream_t s);
+const char* gemm_last_message();
+int num_sms();
+
+}  // namespace slip

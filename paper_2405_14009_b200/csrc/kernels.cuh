@@ -1,0 +1,56 @@
+// kernels.cuh — memory-bound kernels of the stage step (coalesced, 16-byte vectorised,
+// warp-shuffle reductions; column reductions are two-stage and deterministic).
+#pragma once
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+namespace slip {
+
+using bf16 = __nv_bfloat16;
+
+constexpr int kRedChunks = 64;  // row chunks of the deterministic column reductions
+
+// LayerNorm forward over rows of x [T, h]: y = xhat*gamma + beta; mean, rstd fp32 [T].
+cudaError_t ln_fwd(const bf16* x, const bf16* gamma, const bf16* beta, bf16* y, float* mean, float* rstd, int T,
+                   int h, float eps, cudaStream_t s);
+
+// LayerNorm backward.  dx = resid + rstd*(g - mean_h(g) - xhat*mean_h(g*xhat)), g = dy*gamma
+// (dx may be null).  Column partials [kRedChunks, h] of dgamma = sum dy*xhat, dbeta = sum dy
+// and, if part_dxsum != null, of sum_t dx.
+cudaError_t ln_bwd(const bf16* dy, const bf16* x, const float* mean, const float* rstd, const bf16* gamma,
+                   const bf16* resid, bf16* dx, float* part_dgamma, float* part_dbeta, float* part_dxsum, int T, int h,
+                   cudaStream_t s);
+
+// Column-sum partials of a bf16 matrix [T, N] (row stride ld): part [kRedChunks, N].
+cudaError_t colsum_partial(const bf16* a, int T, int N, int64_t ld, float* part, cudaStream_t s);
+
+// out[n] (+)= sum_c part[c, n]  (fixed order over c).
+cudaError_t colsum_finalize(const float* part, int N, float* out, int accumulate, cudaStream_t s);
+
+// Causal softmax over rows of S [z, s, s] fp32 (row t uses columns 0..t):
+// P[z, t, u] = softmax for u <= t, 0 for t < u < ceil128(t+1).
+cudaError_t softmax_fwd(const float* S, bf16* P, int z, int s, cudaStream_t s_);
+
+// dS = scale * P (dP - rowsum(dP P)) on the same causal extents.
+cudaError_t softmax_bwd(const float* dP, const bf16* P, bf16* dS, int z, int s, float scale, cudaStream_t s_);
+
+// MSE head: dy = (y - r)/n (bf16), loss partials per block; loss = 0.5*sum/n.
+cudaError_t mse_loss(const bf16* y, const bf16* r, bf16* dy, float* part, int nparts, float* loss, int64_t n,
+                     cudaStream_t s);
+
+// AdamW over flat fp32 arrays (reading R11).  Weight decay applies
+// to the 2-D weights: layer-local offsets in [0, 3h^2), [3h^2+3h, 4h^2+3h),
+// [4h^2+8h, 4h^2+8h+fh), [4h^2+8h+fh+f, 4h^2+8h+2fh+f).
+cudaError_t adamw(float* p, float* m, float* v, const float* g, bf16* w, int64_t n, int64_t per_layer, int h, int f,
+                  float lr, float b1, float b2, float eps, float wd, float bc1, float bc2, float grad_scale,
+                  int32_t* nonfinite, cudaStream_t s);
+
+// bf16 <- RNE(fp32)
+cudaError_t f32_to_bf16(const float* src, bf16* dst, int64_t n, cudaStream_t s);
+
+// Counter-based N(0,1) -> bf16 (Philox4x32-10 + Box-Muller), key (seed), counter (k, j, i).
+cudaError_t synth_normal(bf16* out, int64_t n, uint64_t seed, uint64_t k, uint64_t j, cudaStream_t s);
+
+}  // namespace slip

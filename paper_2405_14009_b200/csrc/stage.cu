@@ -1,0 +1,636 @@
+// stage.cu — F (slip_stage_forward), B (slip_backward_input), W (slip_backward_weight),
+// AdamW (slip_optimizer_step) and the loss head, composed from the tcgen05 GEMM family
+// (gemm.cu) and the HBM-bound kernels (kernels.cu).  Formulas: DESIGN.md "Stage step",
+// following PAPER.md §3.2 (B_input / B_weight split, lines 250-255) with the layer of
+// reading R1 and the W set of reading R9.
+#include <cmath>
+#include <cstring>
+#include <string>
+
+#include "common.h"
+#include "gemm.cuh"
+#include "kernels.cuh"
+#include "stage.h"
+
+namespace slip {
+
+ParamOffsets param_offsets(int h, int f) {
+  const int64_t H = h, F = f;
+  ParamOffsets o;
+  o.wqkv = 0;
+  o.bqkv = 3 * H * H;
+  o.wo = o.bqkv + 3 * H;
+  o.bo = o.wo + H * H;
+  o.g1 = o.bo + H;
+  o.b1n = o.g1 + H;
+  o.g2 = o.b1n + H;
+  o.b2n = o.g2 + H;
+  o.w1 = o.b2n + H;
+  o.b1 = o.w1 + F * H;
+  o.w2 = o.b1 + F;
+  o.b2 = o.w2 + H * F;
+  o.per_layer = o.b2 + H;
+  return o;
+}
+
+slip_status check_model(const slip_model* m) {
+  SLIP_CHECK(m, SLIP_EINVAL, "model is NULL");
+  SLIP_CHECK(m->hidden > 0 && m->heads > 0 && m->ffn > 0 && m->seq > 0 && m->micro_batch > 0, SLIP_EINVAL,
+             "model: non-positive dimension");
+  SLIP_CHECK(m->hidden % m->heads == 0, SLIP_EINVAL, "model: hidden % heads != 0");
+  const int d = m->hidden / m->heads;
+  SLIP_CHECK(d == 32 || d == 64 || d == 80 || d == 128, SLIP_EUNSUPPORTED, "model: head dim must be 32, 64, 80 or 128");
+  SLIP_CHECK(m->hidden % 64 == 0 && m->ffn % 64 == 0, SLIP_EUNSUPPORTED, "model: hidden and ffn must be multiples of 64");
+  SLIP_CHECK(m->hidden <= 4096, SLIP_EUNSUPPORTED, "model: hidden > 4096");
+  SLIP_CHECK(m->seq % 8 == 0 && m->seq <= 2048, SLIP_EUNSUPPORTED, "model: seq must be a multiple of 8 and <= 2048");
+  SLIP_CHECK(m->ln_eps > 0.f, SLIP_EINVAL, "model: ln_eps must be > 0");
+  return SLIP_OK;
+}
+
+Dims make_dims(const slip_model& m) {
+  Dims d;
+  d.h = m.hidden;
+  d.a = m.heads;
+  d.d = m.hidden / m.heads;
+  d.f = m.ffn;
+  d.s = m.seq;
+  d.b = m.micro_batch;
+  d.T = m.seq * m.micro_batch;
+  d.z = m.heads * m.micro_batch;
+  d.eps = m.ln_eps;
+  return d;
+}
+
+namespace {
+
+constexpr size_t kAlign = 256;
+inline size_t al(size_t x) { return (x + kAlign - 1) / kAlign * kAlign; }
+
+// Walks the slot layout; with base == nullptr only sizes are computed.
+struct Carver {
+  uint8_t* base;
+  size_t off = 0;
+  template <class T>
+  T* take(size_t n) {
+    T* p = base ? reinterpret_cast<T*>(base + off) : nullptr;
+    off += al(n * sizeof(T));
+    return p;
+  }
+};
+
+void carve_slot(Carver& cv, const Dims& d, int L, SlotBufs* out) {
+  const size_t Th = static_cast<size_t>(d.T) * d.h, Tf = static_cast<size_t>(d.T) * d.f;
+  const size_t zss = static_cast<size_t>(d.z) * d.s * d.s;
+  SlotBufs sb;
+  sb.x = cv.take<bf16>(Th);
+  sb.dy = cv.take<bf16>(Th);
+  sb.layer.resize(L);
+  for (int l = 0; l < L; ++l) {
+    LayerStash& ls = sb.layer[l];
+    ls.xin = l == 0 ? sb.x : cv.take<bf16>(Th);
+    ls.y1 = cv.take<bf16>(Th);
+    ls.qkv = cv.take<bf16>(3 * Th);
+    ls.p = cv.take<bf16>(zss);
+    ls.o = cv.take<bf16>(Th);
+    ls.x2 = cv.take<bf16>(Th);
+    ls.y2 = cv.take<bf16>(Th);
+    ls.hpre = cv.take<bf16>(Tf);
+    ls.g = cv.take<bf16>(Tf);
+    ls.mean1 = cv.take<float>(d.T);
+    ls.rstd1 = cv.take<float>(d.T);
+    ls.mean2 = cv.take<float>(d.T);
+    ls.rstd2 = cv.take<float>(d.T);
+    ls.dout = l == L - 1 ? sb.dy : cv.take<bf16>(Th);
+    ls.dh = cv.take<bf16>(Tf);
+    ls.dx2 = cv.take<bf16>(Th);
+    ls.dqkv = cv.take<bf16>(3 * Th);
+  }
+  if (out) *out = sb;
+}
+
+void carve_ws(Carver& cv, const Dims& d, Workspace* out) {
+  const size_t Th = static_cast<size_t>(d.T) * d.h;
+  const size_t zss = static_cast<size_t>(d.z) * d.s * d.s;
+  const size_t red = static_cast<size_t>(kRedChunks) * (d.f > 3 * d.h ? d.f : 3 * d.h);
+  Workspace w;
+  w.s = cv.take<float>(zss);
+  w.ds = cv.take<bf16>(zss);
+  w.dy2 = cv.take<bf16>(Th);
+  w.dO = cv.take<bf16>(Th);
+  w.dy1 = cv.take<bf16>(Th);
+  w.part0 = cv.take<float>(red);
+  w.part1 = cv.take<float>(red);
+  w.part2 = cv.take<float>(red);
+  w.loss_part = cv.take<float>(256);
+  w.losses = cv.take<float>(1024);
+  w.nonfinite = cv.take<int32_t>(64);
+  if (out) *out = w;
+}
+
+}  // namespace
+
+size_t stash_bytes_per_slot(const Dims& d, int L) {
+  Carver cv{nullptr};
+  carve_slot(cv, d, L, nullptr);
+  return cv.off;
+}
+
+size_t workspace_bytes(const Dims& d) {
+  Carver cv{nullptr};
+  carve_ws(cv, d, nullptr);
+  return cv.off;
+}
+
+}  // namespace slip
+
+using namespace slip;
+
+namespace {
+
+// ---------------------------------------------------------------- GEMM helpers
+slip_status run_gemm(slip_ctx* c, const GemmDesc& d, cudaStream_t s, const char* what) {
+  cudaError_t e = gemm_launch(d, s);
+  if (e != cudaSuccess) {
+    std::string m = std::string(what) + ": " + cudaGetErrorString(e);
+    if (gemm_last_message()[0]) m += std::string(" (") + gemm_last_message() + ")";
+    set_error(m);
+    return e == cudaErrorInvalidValue ? SLIP_EUNSUPPORTED : SLIP_ECUDA;
+  }
+  c->launches += 1;
+  return SLIP_OK;
+}
+
+Operand op(const void* p, int64_t ld, bool mn, int64_t zi = 0, int64_t zo = 0) {
+  Operand o;
+  o.ptr = p;
+  o.ld = ld;
+  o.mn_major = mn;
+  o.zi_stride = zi;
+  o.zo_stride = zo;
+  return o;
+}
+
+// out[T, N] = X[T, K] W[N, K]^T (+ bias, resid / GeLU)
+slip_status linear_fwd(slip_ctx* c, const bf16* X, const bf16* W, int N, int K, bf16* out, const bf16* bias,
+                       const bf16* resid, int mode, bf16* aux, cudaStream_t s) {
+  GemmDesc d;
+  d.M = c->dm.T;
+  d.N = N;
+  d.K = K;
+  d.bn = 256;
+  d.a = op(X, K, false);
+  d.b = op(W, K, false);
+  d.mode = mode;
+  d.c = out;
+  d.ldc = N;
+  d.bias = bias;
+  d.resid = resid;
+  d.aux = aux;
+  return run_gemm(c, d, s, "linear_fwd");
+}
+
+// dX[T, K] = dY[T, N] W[N, K]   (mode: EPI_BF16 or EPI_BF16_DGELU with aux = H)
+slip_status linear_dx(slip_ctx* c, const bf16* dY, const bf16* W, int N, int K, bf16* dX, int mode, bf16* aux,
+                      cudaStream_t s) {
+  GemmDesc d;
+  d.M = c->dm.T;
+  d.N = K;
+  d.K = N;
+  d.bn = 256;
+  d.a = op(dY, N, false);
+  d.b = op(W, K, true);
+  d.mode = mode;
+  d.c = dX;
+  d.ldc = K;
+  d.aux = aux;
+  return run_gemm(c, d, s, "linear_dx");
+}
+
+// dW[N, K] (+)= dY[T, N]^T X[T, K]   (fp32, fused in the epilogue: TMA store / reduce-add)
+slip_status linear_dw(slip_ctx* c, const bf16* dY, const bf16* X, int N, int K, float* dW, int accumulate,
+                      cudaStream_t s) {
+  GemmDesc d;
+  d.M = N;
+  d.N = K;
+  d.K = c->dm.T;
+  d.bn = 256;
+  d.a = op(dY, N, true);
+  d.b = op(X, K, true);
+  d.mode = EPI_F32_ACC;
+  d.c = dW;
+  d.ldc = K;
+  d.accumulate = accumulate;
+  return run_gemm(c, d, s, "linear_dw");
+}
+
+struct LayerW {
+  const bf16 *wqkv, *bqkv, *wo, *bo, *g1, *b1n, *g2, *b2n, *w1, *b1, *w2, *b2;
+};
+struct LayerG {
+  float *wqkv, *bqkv, *wo, *bo, *g1, *b1n, *g2, *b2n, *w1, *b1, *w2, *b2;
+};
+
+LayerW layer_w(slip_ctx* c, int l) {
+  const bf16* b = c->w + l * c->po.per_layer;
+  const ParamOffsets& o = c->po;
+  return {b + o.wqkv, b + o.bqkv, b + o.wo, b + o.bo, b + o.g1, b + o.b1n,
+          b + o.g2,   b + o.b2n,  b + o.w1, b + o.b1, b + o.w2, b + o.b2};
+}
+LayerG layer_g(slip_ctx* c, int l) {
+  float* b = c->grad + l * c->po.per_layer;
+  const ParamOffsets& o = c->po;
+  return {b + o.wqkv, b + o.bqkv, b + o.wo, b + o.bo, b + o.g1, b + o.b1n,
+          b + o.g2,   b + o.b2n,  b + o.w1, b + o.b1, b + o.w2, b + o.b2};
+}
+
+slip_status kcheck(slip_ctx* c, cudaError_t e, const char* what, int n_launch = 1) {
+  if (e != cudaSuccess) return cuda_status(e, what);
+  c->launches += n_launch;
+  return SLIP_OK;
+}
+
+// ---------------------------------------------------------------- attention
+slip_status attention_fwd(slip_ctx* c, LayerStash& ls, cudaStream_t s) {
+  const Dims& D = c->dm;
+  const int64_t h3 = 3LL * D.h;
+  // S = Q K^T / sqrt(d), causal tiles only, fp32 transient
+  GemmDesc g;
+  g.M = D.s;
+  g.N = D.s;
+  g.K = D.d;
+  g.zi_count = D.a;
+  g.zo_count = D.b;
+  g.bn = 128;
+  g.causal = CAUSAL_TILES;
+  g.a = op(ls.qkv, h3, false, D.d, D.s * h3);
+  g.b = op(ls.qkv + D.h, h3, false, D.d, D.s * h3);
+  g.mode = EPI_F32_STORE;
+  g.alpha = 1.0f / std::sqrt(static_cast<float>(D.d));
+  g.c = c->ws.s;
+  g.ldc = D.s;
+  g.c_zi = static_cast<int64_t>(D.s) * D.s;
+  g.c_zo = static_cast<int64_t>(D.a) * D.s * D.s;
+  SLIP_TRY(run_gemm(c, g, s, "attn S"));
+  SLIP_TRY(kcheck(c, softmax_fwd(c->ws.s, ls.p, D.z, D.s, s), "softmax_fwd"));
+  // O = P V  (k < m0 + 128)
+  GemmDesc o;
+  o.M = D.s;
+  o.N = D.d;
+  o.K = D.s;
+  o.zi_count = D.a;
+  o.zo_count = D.b;
+  o.bn = D.d;
+  o.causal = CAUSAL_K_UPPER;
+  o.a = op(ls.p, D.s, false, static_cast<int64_t>(D.s) * D.s, static_cast<int64_t>(D.a) * D.s * D.s);
+  o.b = op(ls.qkv + 2 * D.h, h3, true, D.d, D.s * h3);
+  o.mode = EPI_BF16;
+  o.c = ls.o;
+  o.ldc = D.h;
+  o.c_zi = D.d;
+  o.c_zo = static_cast<int64_t>(D.s) * D.h;
+  return run_gemm(c, o, s, "attn PV");
+}
+
+slip_status attention_bwd(slip_ctx* c, LayerStash& ls, cudaStream_t s) {
+  const Dims& D = c->dm;
+  const int64_t h3 = 3LL * D.h;
+  const int64_t zss_i = static_cast<int64_t>(D.s) * D.s, zss_o = static_cast<int64_t>(D.a) * D.s * D.s;
+  // dP = dO V^T (fp32, causal tiles)
+  GemmDesc g;
+  g.M = D.s;
+  g.N = D.s;
+  g.K = D.d;
+  g.zi_count = D.a;
+  g.zo_count = D.b;
+  g.bn = 128;
+  g.causal = CAUSAL_TILES;
+  g.a = op(c->ws.dO, D.h, false, D.d, static_cast<int64_t>(D.s) * D.h);
+  g.b = op(ls.qkv + 2 * D.h, h3, false, D.d, D.s * h3);
+  g.mode = EPI_F32_STORE;
+  g.alpha = 1.0f;
+  g.c = c->ws.s;
+  g.ldc = D.s;
+  g.c_zi = zss_i;
+  g.c_zo = zss_o;
+  SLIP_TRY(run_gemm(c, g, s, "attn dP"));
+  // dS = P (dP - rowsum(dP P)) / sqrt(d)
+  SLIP_TRY(kcheck(c, softmax_bwd(c->ws.s, ls.p, c->ws.ds, D.z, D.s, 1.0f / std::sqrt(static_cast<float>(D.d)), s),
+                  "softmax_bwd"));
+  auto base = [&](int which) {
+    GemmDesc x;
+    x.M = D.s;
+    x.N = D.d;
+    x.K = D.s;
+    x.zi_count = D.a;
+    x.zo_count = D.b;
+    x.bn = D.d;
+    x.mode = EPI_BF16;
+    x.c = ls.dqkv + which * D.h;
+    x.ldc = h3;
+    x.c_zi = D.d;
+    x.c_zo = D.s * h3;
+    return x;
+  };
+  // dV = P^T dO  (queries >= key tile start)
+  GemmDesc dv = base(2);
+  dv.causal = CAUSAL_K_LOWER;
+  dv.a = op(ls.p, D.s, true, zss_i, zss_o);
+  dv.b = op(c->ws.dO, D.h, true, D.d, static_cast<int64_t>(D.s) * D.h);
+  SLIP_TRY(run_gemm(c, dv, s, "attn dV"));
+  // dQ = dS K
+  GemmDesc dq = base(0);
+  dq.causal = CAUSAL_K_UPPER;
+  dq.a = op(c->ws.ds, D.s, false, zss_i, zss_o);
+  dq.b = op(ls.qkv + D.h, h3, true, D.d, D.s * h3);
+  SLIP_TRY(run_gemm(c, dq, s, "attn dQ"));
+  // dK = dS^T Q
+  GemmDesc dk = base(1);
+  dk.causal = CAUSAL_K_LOWER;
+  dk.a = op(c->ws.ds, D.s, true, zss_i, zss_o);
+  dk.b = op(ls.qkv, h3, true, D.d, D.s * h3);
+  return run_gemm(c, dk, s, "attn dK");
+}
+
+// colsum(a[T, N]) -> out (fp32, overwrite or accumulate)
+slip_status bias_grad(slip_ctx* c, const bf16* a, int N, int64_t ld, float* out, int accumulate, cudaStream_t s) {
+  SLIP_TRY(kcheck(c, colsum_partial(a, c->dm.T, N, ld, c->ws.part0, s), "colsum_partial"));
+  return kcheck(c, colsum_finalize(c->ws.part0, N, out, accumulate, s), "colsum_finalize");
+}
+
+slip_status slot_check(slip_ctx* c, int slot, int want) {
+  SLIP_CHECK(c, SLIP_EINVAL, "ctx is NULL");
+  SLIP_CHECK(c->bound, SLIP_ESTATE, "stage buffers not bound (slip_stage_bind)");
+  SLIP_CHECK(slot >= 0 && slot < c->n_slots, SLIP_EINVAL, "slot out of range");
+  if (c->state[slot] != want) {
+    static const char* names[] = {"FREE", "F_DONE", "B_DONE"};
+    set_error(std::string("slot ") + std::to_string(slot) + " is " + names[c->state[slot]] + ", expected " +
+              names[want]);
+    return SLIP_ESTATE;
+  }
+  return SLIP_OK;
+}
+
+slip_status backward_weight_impl(slip_ctx* c, int slot, int accumulate, cudaStream_t s) {
+  const Dims& D = c->dm;
+  SlotBufs& sb = c->slots[slot];
+  for (int l = c->L - 1; l >= 0; --l) {
+    LayerStash& ls = sb.layer[l];
+    LayerG G = layer_g(c, l);
+    SLIP_TRY(linear_dw(c, ls.dout, ls.g, D.h, D.f, G.w2, accumulate, s));
+    SLIP_TRY(linear_dw(c, ls.dh, ls.y2, D.f, D.h, G.w1, accumulate, s));
+    SLIP_TRY(linear_dw(c, ls.dx2, ls.o, D.h, D.h, G.wo, accumulate, s));
+    SLIP_TRY(linear_dw(c, ls.dqkv, ls.y1, 3 * D.h, D.h, G.wqkv, accumulate, s));
+  }
+  return SLIP_OK;
+}
+
+slip_status backward_input_impl(slip_ctx* c, int slot, const void* dy, void* dx, int accumulate, cudaStream_t s) {
+  const Dims& D = c->dm;
+  SlotBufs& sb = c->slots[slot];
+  const size_t Th = static_cast<size_t>(D.T) * D.h;
+  if (dy != sb.dy) SLIP_CUDA(cudaMemcpyAsync(sb.dy, dy, Th * sizeof(bf16), cudaMemcpyDeviceToDevice, s));
+  // db2 of the top layer = colsum(dy)
+  SLIP_TRY(bias_grad(c, sb.dy, D.h, D.h, layer_g(c, c->L - 1).b2, accumulate, s));
+  for (int l = c->L - 1; l >= 0; --l) {
+    LayerStash& ls = sb.layer[l];
+    LayerW Wt = layer_w(c, l);
+    LayerG G = layer_g(c, l);
+    // dH = (dOut W2) * gelu'(H)   (GeLU backward fused in the epilogue)
+    SLIP_TRY(linear_dx(c, ls.dout, Wt.w2, D.h, D.f, ls.dh, EPI_BF16_DGELU, ls.hpre, s));
+    SLIP_TRY(bias_grad(c, ls.dh, D.f, D.f, G.b1, accumulate, s));
+    // dY2 = dH W1
+    SLIP_TRY(linear_dx(c, ls.dh, Wt.w1, D.f, D.h, c->ws.dy2, EPI_BF16, nullptr, s));
+    // LN2 backward + residual: dX2 = dOut + LN2'(dY2); dgamma2, dbeta2, dbo = colsum(dX2)
+    SLIP_TRY(kcheck(c,
+                    ln_bwd(c->ws.dy2, ls.x2, ls.mean2, ls.rstd2, Wt.g2, ls.dout, ls.dx2, c->ws.part0, c->ws.part1,
+                           c->ws.part2, D.T, D.h, s),
+                    "ln_bwd 2", 3));
+    SLIP_TRY(kcheck(c, colsum_finalize(c->ws.part0, D.h, G.g2, accumulate, s), "fin g2"));
+    SLIP_TRY(kcheck(c, colsum_finalize(c->ws.part1, D.h, G.b2n, accumulate, s), "fin b2n"));
+    SLIP_TRY(kcheck(c, colsum_finalize(c->ws.part2, D.h, G.bo, accumulate, s), "fin bo"));
+    // dO = dX2 Wo
+    SLIP_TRY(linear_dx(c, ls.dx2, Wt.wo, D.h, D.h, c->ws.dO, EPI_BF16, nullptr, s));
+    SLIP_TRY(attention_bwd(c, ls, s));
+    SLIP_TRY(bias_grad(c, ls.dqkv, 3 * D.h, 3 * D.h, G.bqkv, accumulate, s));
+    // dY1 = dQKV Wqkv
+    SLIP_TRY(linear_dx(c, ls.dqkv, Wt.wqkv, 3 * D.h, D.h, c->ws.dy1, EPI_BF16, nullptr, s));
+    // LN1 backward + residual: dX = dX2 + LN1'(dY1); db2 of the layer below = colsum(dX)
+    bf16* dxl = l > 0 ? sb.layer[l - 1].dout : static_cast<bf16*>(dx);
+    float* dxsum = l > 0 ? c->ws.part2 : nullptr;
+    if (dxl) {
+      SLIP_TRY(kcheck(c,
+                      ln_bwd(c->ws.dy1, ls.xin, ls.mean1, ls.rstd1, Wt.g1, ls.dx2, dxl, c->ws.part0, c->ws.part1,
+                             dxsum, D.T, D.h, s),
+                      "ln_bwd 1", dxsum ? 3 : 2));
+    } else {
+      SLIP_TRY(kcheck(c,
+                      ln_bwd(c->ws.dy1, ls.xin, ls.mean1, ls.rstd1, Wt.g1, nullptr, nullptr, c->ws.part0,
+                             c->ws.part1, nullptr, D.T, D.h, s),
+                      "ln_bwd 1", 1));
+    }
+    SLIP_TRY(kcheck(c, colsum_finalize(c->ws.part0, D.h, G.g1, accumulate, s), "fin g1"));
+    SLIP_TRY(kcheck(c, colsum_finalize(c->ws.part1, D.h, G.b1n, accumulate, s), "fin b1n"));
+    if (l > 0)
+      SLIP_TRY(kcheck(c, colsum_finalize(c->ws.part2, D.h, layer_g(c, l - 1).b2, accumulate, s), "fin b2"));
+  }
+  return SLIP_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+slip_status slip_param_count(const slip_model* m, int32_t n_layers, int64_t* out) {
+  SLIP_TRY(check_model(m));
+  SLIP_CHECK(n_layers > 0 && out, SLIP_EINVAL, "param_count: bad arguments");
+  *out = param_offsets(m->hidden, m->ffn).per_layer * n_layers;
+  return SLIP_OK;
+}
+
+slip_status slip_stash_bytes(const slip_model* m, int32_t n_layers, int32_t n_slots, size_t* out) {
+  SLIP_TRY(check_model(m));
+  SLIP_CHECK(n_layers > 0 && n_slots > 0 && out, SLIP_EINVAL, "stash_bytes: bad arguments");
+  *out = stash_bytes_per_slot(make_dims(*m), n_layers) * n_slots;
+  return SLIP_OK;
+}
+
+slip_status slip_workspace_bytes(const slip_model* m, size_t* out) {
+  SLIP_TRY(check_model(m));
+  SLIP_CHECK(out, SLIP_EINVAL, "workspace_bytes: out is NULL");
+  *out = workspace_bytes(make_dims(*m));
+  return SLIP_OK;
+}
+
+slip_status slip_ctx_create(slip_ctx** out, const slip_model* m, int32_t n_layers, int32_t n_slots) {
+  SLIP_CHECK(out, SLIP_EINVAL, "ctx_create: out is NULL");
+  SLIP_TRY(check_model(m));
+  SLIP_CHECK(n_layers > 0 && n_slots > 0, SLIP_EINVAL, "ctx_create: n_layers and n_slots must be > 0");
+  int dev = 0;
+  SLIP_CUDA(cudaGetDevice(&dev));
+  int major = 0, minor = 0;
+  SLIP_CUDA(cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev));
+  SLIP_CUDA(cudaDeviceGetAttribute(&minor, cudaDevAttrComputeCapabilityMinor, dev));
+  SLIP_CHECK(major == 10 && minor == 0, SLIP_EUNSUPPORTED, "libslip is built for sm_100a (B200) only");
+  slip_ctx* c = new slip_ctx();
+  c->model = *m;
+  c->dm = make_dims(*m);
+  c->L = n_layers;
+  c->n_slots = n_slots;
+  c->po = param_offsets(m->hidden, m->ffn);
+  c->n_params = c->po.per_layer * n_layers;
+  c->state.assign(n_slots, SLOT_FREE);
+  *out = c;
+  return SLIP_OK;
+}
+
+slip_status slip_ctx_destroy(slip_ctx* ctx) {
+  delete ctx;
+  return SLIP_OK;
+}
+
+slip_status slip_stage_bind(slip_ctx* c, void* w_bf16, float* master, float* grad, float* adam_m, float* adam_v,
+                            int64_t n_params, void* arena, size_t arena_bytes, void* workspace, size_t ws_bytes) {
+  SLIP_CHECK(c, SLIP_EINVAL, "ctx is NULL");
+  SLIP_CHECK(n_params == c->n_params, SLIP_EINVAL, "stage_bind: n_params does not match the model");
+  SLIP_CHECK(w_bf16 && master && grad && adam_m && adam_v && arena && workspace, SLIP_EINVAL,
+             "stage_bind: NULL buffer");
+  auto aligned = [](const void* p) { return reinterpret_cast<uintptr_t>(p) % 256 == 0; };
+  SLIP_CHECK(aligned(w_bf16) && aligned(master) && aligned(grad) && aligned(adam_m) && aligned(adam_v) &&
+                 aligned(arena) && aligned(workspace),
+             SLIP_EINVAL, "stage_bind: buffers must be 256-byte aligned");
+  const size_t per = stash_bytes_per_slot(c->dm, c->L);
+  SLIP_CHECK(arena_bytes >= per * c->n_slots, SLIP_EINVAL, "stage_bind: arena too small");
+  SLIP_CHECK(ws_bytes >= workspace_bytes(c->dm), SLIP_EINVAL, "stage_bind: workspace too small");
+  c->w = static_cast<bf16*>(w_bf16);
+  c->master = master;
+  c->grad = grad;
+  c->adam_m = adam_m;
+  c->adam_v = adam_v;
+  c->arena = static_cast<uint8_t*>(arena);
+  c->arena_bytes = arena_bytes;
+  c->ws_base = static_cast<uint8_t*>(workspace);
+  c->ws_bytes = ws_bytes;
+  c->slots.resize(c->n_slots);
+  for (int i = 0; i < c->n_slots; ++i) {
+    Carver cv{c->arena + per * i};
+    carve_slot(cv, c->dm, c->L, &c->slots[i]);
+  }
+  Carver wv{c->ws_base};
+  carve_ws(wv, c->dm, &c->ws);
+  c->state.assign(c->n_slots, SLOT_FREE);
+  c->bound = true;
+  return SLIP_OK;
+}
+
+slip_status slip_slot_ptr(slip_ctx* c, int32_t slot, int32_t which, void** out) {
+  SLIP_CHECK(c && c->bound && out, SLIP_EINVAL, "slot_ptr: bad arguments");
+  SLIP_CHECK(slot >= 0 && slot < c->n_slots && (which == 0 || which == 1), SLIP_EINVAL, "slot_ptr: bad slot / which");
+  *out = which == 0 ? static_cast<void*>(c->slots[slot].x) : static_cast<void*>(c->slots[slot].dy);
+  return SLIP_OK;
+}
+
+slip_status slip_stage_forward(slip_ctx* c, int32_t slot, const void* x_in, void* y_out, slip_stream st) {
+  SLIP_TRY(slot_check(c, slot, SLOT_FREE));
+  SLIP_CHECK(x_in && y_out, SLIP_EINVAL, "stage_forward: NULL x_in / y_out");
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(st);
+  const Dims& D = c->dm;
+  SlotBufs& sb = c->slots[slot];
+  const size_t Th = static_cast<size_t>(D.T) * D.h;
+  if (x_in != sb.x) SLIP_CUDA(cudaMemcpyAsync(sb.x, x_in, Th * sizeof(bf16), cudaMemcpyDeviceToDevice, s));
+  for (int l = 0; l < c->L; ++l) {
+    LayerStash& ls = sb.layer[l];
+    LayerW Wt = layer_w(c, l);
+    bf16* out = l + 1 < c->L ? sb.layer[l + 1].xin : static_cast<bf16*>(y_out);
+    SLIP_TRY(kcheck(c, ln_fwd(ls.xin, Wt.g1, Wt.b1n, ls.y1, ls.mean1, ls.rstd1, D.T, D.h, D.eps, s), "ln_fwd 1"));
+    SLIP_TRY(linear_fwd(c, ls.y1, Wt.wqkv, 3 * D.h, D.h, ls.qkv, Wt.bqkv, nullptr, EPI_BF16, nullptr, s));
+    SLIP_TRY(attention_fwd(c, ls, s));
+    SLIP_TRY(linear_fwd(c, ls.o, Wt.wo, D.h, D.h, ls.x2, Wt.bo, ls.xin, EPI_BF16, nullptr, s));
+    SLIP_TRY(kcheck(c, ln_fwd(ls.x2, Wt.g2, Wt.b2n, ls.y2, ls.mean2, ls.rstd2, D.T, D.h, D.eps, s), "ln_fwd 2"));
+    SLIP_TRY(linear_fwd(c, ls.y2, Wt.w1, D.f, D.h, ls.g, Wt.b1, nullptr, EPI_BF16_GELU, ls.hpre, s));
+    SLIP_TRY(linear_fwd(c, ls.g, Wt.w2, D.h, D.f, out, Wt.b2, ls.x2, EPI_BF16, nullptr, s));
+  }
+  c->state[slot] = SLOT_F_DONE;
+  return SLIP_OK;
+}
+
+slip_status slip_backward_input(slip_ctx* c, int32_t slot, const void* dy, void* dx, int32_t accumulate,
+                                slip_stream st) {
+  SLIP_TRY(slot_check(c, slot, SLOT_F_DONE));
+  SLIP_CHECK(dy, SLIP_EINVAL, "backward_input: NULL dy");
+  SLIP_TRY(backward_input_impl(c, slot, dy, dx, accumulate, reinterpret_cast<cudaStream_t>(st)));
+  c->state[slot] = SLOT_B_DONE;
+  return SLIP_OK;
+}
+
+slip_status slip_backward_weight(slip_ctx* c, int32_t slot, int32_t accumulate, slip_stream st) {
+  SLIP_TRY(slot_check(c, slot, SLOT_B_DONE));
+  SLIP_TRY(backward_weight_impl(c, slot, accumulate, reinterpret_cast<cudaStream_t>(st)));
+  c->state[slot] = SLOT_FREE;
+  return SLIP_OK;
+}
+
+slip_status slip_backward_coupled(slip_ctx* c, int32_t slot, const void* dy, void* dx, int32_t accumulate,
+                                  slip_stream st) {
+  SLIP_TRY(slip_backward_input(c, slot, dy, dx, accumulate, st));
+  return slip_backward_weight(c, slot, accumulate, st);
+}
+
+slip_status slip_optimizer_step(slip_ctx* c, const slip_adam* a, int64_t step, float grad_scale, int32_t* d_nonfinite,
+                                slip_stream st) {
+  SLIP_CHECK(c && c->bound && a, SLIP_EINVAL, "optimizer_step: bad arguments");
+  SLIP_CHECK(step >= 1, SLIP_EINVAL, "optimizer_step: step must be >= 1");
+  const double bc1 = 1.0 - std::pow(static_cast<double>(a->beta1), static_cast<double>(step));
+  const double bc2 = 1.0 - std::pow(static_cast<double>(a->beta2), static_cast<double>(step));
+  return kcheck(c,
+                adamw(c->master, c->adam_m, c->adam_v, c->grad, c->w, c->n_params, c->po.per_layer, c->dm.h, c->dm.f,
+                      a->lr, a->beta1, a->beta2, a->eps, a->weight_decay, static_cast<float>(bc1),
+                      static_cast<float>(bc2), grad_scale, d_nonfinite, reinterpret_cast<cudaStream_t>(st)),
+                "adamw");
+}
+
+slip_status slip_loss_mse(slip_ctx* c, const void* y, const void* target, void* dy, float* d_loss, slip_stream st) {
+  SLIP_CHECK(c && c->bound && y && target && dy && d_loss, SLIP_EINVAL, "loss_mse: bad arguments");
+  const int64_t n = static_cast<int64_t>(c->dm.T) * c->dm.h;
+  return kcheck(c,
+                mse_loss(static_cast<const bf16*>(y), static_cast<const bf16*>(target), static_cast<bf16*>(dy),
+                         c->ws.loss_part, 256, d_loss, n, reinterpret_cast<cudaStream_t>(st)),
+                "mse_loss", 2);
+}
+
+slip_status slip_synth_normal(void* out_bf16, int64_t n, uint64_t seed, uint64_t k, uint64_t j, slip_stream st) {
+  SLIP_CHECK(out_bf16 && n > 0, SLIP_EINVAL, "synth_normal: bad arguments");
+  SLIP_CUDA(synth_normal(static_cast<bf16*>(out_bf16), n, seed, k, j, reinterpret_cast<cudaStream_t>(st)));
+  return SLIP_OK;
+}
+
+slip_status slip_gemm(int32_t M, int32_t N, int32_t K, const void* a, int64_t lda, int32_t a_mn, const void* b,
+                      int64_t ldb, int32_t b_mn, void* c, int64_t ldc, int32_t mode, int32_t bn, int32_t accumulate,
+                      float alpha, slip_stream st) {
+  SLIP_CHECK(a && b && c, SLIP_EINVAL, "gemm: NULL operand");
+  SLIP_CHECK(mode == EPI_BF16 || mode == EPI_F32_STORE || mode == EPI_F32_ACC, SLIP_EINVAL, "gemm: mode");
+  GemmDesc d;
+  d.M = M;
+  d.N = N;
+  d.K = K;
+  d.bn = bn;
+  d.a = op(a, lda, a_mn != 0);
+  d.b = op(b, ldb, b_mn != 0);
+  d.mode = mode;
+  d.c = c;
+  d.ldc = ldc;
+  d.alpha = alpha;
+  d.accumulate = accumulate;
+  cudaError_t e = gemm_launch(d, reinterpret_cast<cudaStream_t>(st));
+  if (e != cudaSuccess) {
+    set_error(std::string("gemm: ") + cudaGetErrorString(e) + " " + gemm_last_message());
+    return e == cudaErrorInvalidValue ? SLIP_EUNSUPPORTED : SLIP_ECUDA;
+  }
+  return SLIP_OK;
+}
+
+slip_status slip_weights_from_master(slip_ctx* c, slip_stream st) {
+  SLIP_CHECK(c && c->bound, SLIP_EINVAL, "weights_from_master: not bound");
+  return kcheck(c, f32_to_bf16(c->master, c->w, c->n_params, reinterpret_cast<cudaStream_t>(st)), "f32_to_bf16");
+}
+
+}  // extern "C"

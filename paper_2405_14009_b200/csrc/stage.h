@@ -1,0 +1,80 @@
+// stage.h — per-rank stage context: bound buffers, arena layout (F-stash + W-stash per
+// slot = the WeightGradStore of PAPER.md line 558), workspace, slot state machine.
+#pragma once
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <vector>
+
+#include "../../include/slip.h"
+
+namespace slip {
+
+using bf16 = __nv_bfloat16;
+
+// Offsets (elements) of one layer's tensors inside the flat parameter vector
+// (include/slip.h "Parameter layout").
+struct ParamOffsets {
+  int64_t wqkv, bqkv, wo, bo, g1, b1n, g2, b2n, w1, b1, w2, b2, per_layer;
+};
+ParamOffsets param_offsets(int h, int f);
+
+struct LayerStash {
+  bf16 *xin, *y1, *qkv, *p, *o, *x2, *y2, *hpre, *g;  // F-stash
+  float *mean1, *rstd1, *mean2, *rstd2;
+  bf16 *dout, *dh, *dx2, *dqkv;                          // W-stash (with y1, o, y2, g)
+};
+
+struct SlotBufs {
+  bf16* x;   // stage input   [T, h]
+  bf16* dy;  // stage output gradient [T, h]
+  std::vector<LayerStash> layer;
+};
+
+struct Workspace {
+  float* s;          // S and dP  [z, s, s] fp32
+  bf16* ds;          // dS        [z, s, s]
+  bf16 *dy2, *dO, *dy1;  // [T, h]
+  float *part0, *part1, *part2;  // [kRedChunks, max(f, 3h)]
+  float* loss_part;  // [256] MSE partials
+  float* losses;     // [1024] per-micro-batch losses (executor)
+  int32_t* nonfinite;  // [1] post-step validation flag (executor)
+};
+
+enum SlotState : int { SLOT_FREE = 0, SLOT_F_DONE = 1, SLOT_B_DONE = 2 };
+
+struct Dims {
+  int h, a, d, f, s, b, T, z;
+  float eps;
+};
+
+}  // namespace slip
+
+struct slip_ctx {
+  slip_model model;
+  slip::Dims dm;
+  int L = 0;
+  int n_slots = 0;
+  slip::ParamOffsets po;
+  int64_t n_params = 0;
+  slip::bf16* w = nullptr;
+  float *master = nullptr, *grad = nullptr, *adam_m = nullptr, *adam_v = nullptr;
+  uint8_t* arena = nullptr;
+  size_t arena_bytes = 0;
+  uint8_t* ws_base = nullptr;
+  size_t ws_bytes = 0;
+  bool bound = false;
+  std::vector<slip::SlotBufs> slots;
+  slip::Workspace ws{};
+  std::vector<int> state;
+  int64_t launches = 0;  // kernels enqueued through this context
+  int64_t opt_step = 0;  // AdamW steps taken by the executor
+};
+
+namespace slip {
+slip_status check_model(const slip_model* m);
+Dims make_dims(const slip_model& m);
+size_t stash_bytes_per_slot(const Dims& d, int L);
+size_t workspace_bytes(const Dims& d);
+}  // namespace slip

@@ -1,0 +1,222 @@
+"""Thin Python runtime over libslip: torch allocates device memory and provides
+streams / process groups; the library does all compute.  Names follow
+include/slip.h."""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+
+from ._binding import (SlipError, call, lib, slip_adam, slip_cluster, slip_costs, slip_io, slip_model, slip_op,
+                       slip_plan_opts, slip_report)
+
+
+def _ptr(t) -> C.c_void_p:
+    return C.c_void_p(t.data_ptr())
+
+
+def _stream(stream=None) -> C.c_void_p:
+    import torch
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return C.c_void_p(s.cuda_stream)
+
+
+def make_model(cfg) -> slip_model:
+    return slip_model(cfg.hidden, cfg.heads, cfg.ffn, cfg.seq, cfg.micro_batch, cfg.ln_eps)
+
+
+def make_cluster(N: int, DP: int, m: int, live=None):
+    """live: iterable over stages of iterables over pipelines (1 = functional)."""
+    flat = [1] * (N * DP) if live is None else [int(bool(x)) for row in live for x in row]
+    arr = (C.c_uint8 * (N * DP))(*flat)
+    cl = slip_cluster(N, DP, m, C.cast(arr, C.POINTER(C.c_uint8)))
+    cl._keep = arr  # keep the buffer alive with the struct
+    return cl
+
+
+def make_costs(t_f=1, t_b=1, t_w=1, t_comm=0, t_ar=0, t_opt=0, a_f=0, a_w=0, m_limit=0) -> slip_costs:
+    return slip_costs(t_f, t_b, t_w, t_comm, t_ar, t_opt, a_f, a_w, m_limit)
+
+
+@dataclass
+class PlanResult:
+    ops: list          # list of op tuples (stage, mb, origin, phase, exec, iter, start, end)
+    makespans: list
+    period: int
+    hash: int
+
+
+def plan_schedule(N, DP, m, live, costs: slip_costs, decoupled=True, staggered=True, horizon=3) -> PlanResult:
+    cl = make_cluster(N, DP, m, live)
+    opts = slip_plan_opts(int(decoupled), int(staggered), int(horizon))
+    n = C.c_int64(0)
+    call("slip_plan_schedule", C.byref(cl), C.byref(costs), C.byref(opts), None, 0, C.byref(n), None, None)
+    ops = (slip_op * max(1, n.value))()
+    mk = (C.c_int64 * max(1, horizon))()
+    per = C.c_int64(0)
+    call("slip_plan_schedule", C.byref(cl), C.byref(costs), C.byref(opts), ops, n.value, C.byref(n), mk,
+         C.byref(per))
+    h = lib().slip_plan_hash(ops, n.value)
+    return PlanResult([ops[i].key() for i in range(n.value)], [mk[i] for i in range(horizon)], per.value, h)
+
+
+def assign(N, DP, m, live):
+    cl = make_cluster(N, DP, m, live)
+    out = (C.c_int32 * (N * m * DP))()
+    call("slip_assign", C.byref(cl), out)
+    return {(i, j, k): out[(i * m + j) * DP + k] for i in range(N) for j in range(m) for k in range(DP)}
+
+
+def recoverable(N, DP, live) -> bool:
+    cl = make_cluster(N, DP, 1, live)
+    r = C.c_int32(0)
+    call("slip_recoverable", C.byref(cl), C.byref(r))
+    return bool(r.value)
+
+
+class Stage:
+    """One stage of `n_layers` layers on the current CUDA device, with `n_slots`
+    in-flight micro-batch slots (F-stash + W-stash each)."""
+
+    def __init__(self, cfg, n_layers: int, n_slots: int, device="cuda"):
+        import torch
+        self.cfg, self.L, self.n_slots = cfg, n_layers, n_slots
+        self.model = make_model(cfg)
+        np_ = C.c_int64(0)
+        call("slip_param_count", C.byref(self.model), n_layers, C.byref(np_))
+        self.n_params = np_.value
+        sb, wb = C.c_size_t(0), C.c_size_t(0)
+        call("slip_stash_bytes", C.byref(self.model), n_layers, n_slots, C.byref(sb))
+        call("slip_workspace_bytes", C.byref(self.model), C.byref(wb))
+        dev = torch.device(device)
+        self.w = torch.zeros(self.n_params, dtype=torch.bfloat16, device=dev)
+        self.master = torch.zeros(self.n_params, dtype=torch.float32, device=dev)
+        self.grad = torch.zeros(self.n_params, dtype=torch.float32, device=dev)
+        self.adam_m = torch.zeros(self.n_params, dtype=torch.float32, device=dev)
+        self.adam_v = torch.zeros(self.n_params, dtype=torch.float32, device=dev)
+        self.arena = torch.empty(sb.value, dtype=torch.uint8, device=dev)
+        self.ws = torch.zeros(wb.value, dtype=torch.uint8, device=dev)
+        self.stash_bytes, self.ws_bytes = sb.value, wb.value
+        ctx = C.c_void_p()
+        call("slip_ctx_create", C.byref(ctx), C.byref(self.model), n_layers, n_slots)
+        self.ctx = ctx
+        call("slip_stage_bind", self.ctx, _ptr(self.w), _ptr(self.master), _ptr(self.grad), _ptr(self.adam_m),
+             _ptr(self.adam_v), self.n_params, _ptr(self.arena), self.arena.numel(), _ptr(self.ws), self.ws.numel())
+
+    def close(self):
+        if self.ctx:
+            lib().slip_ctx_destroy(self.ctx)
+            self.ctx = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    # -- parameters
+    def load_master(self, flat_fp32, stream=None):
+        """Copy fp32 master weights and refresh the bf16 copy (RNE, on the device)."""
+        self.master.copy_(flat_fp32)
+        call("slip_weights_from_master", self.ctx, _stream(stream))
+
+    def slot_ptr(self, slot: int, which: int) -> int:
+        p = C.c_void_p()
+        call("slip_slot_ptr", self.ctx, slot, which, C.byref(p))
+        return p.value
+
+    # -- hot path
+    def forward(self, slot, x, y, stream=None):
+        call("slip_stage_forward", self.ctx, slot, _ptr(x), _ptr(y), _stream(stream))
+
+    def backward_input(self, slot, dy, dx=None, accumulate=False, stream=None):
+        call("slip_backward_input", self.ctx, slot, _ptr(dy), _ptr(dx) if dx is not None else None,
+             int(accumulate), _stream(stream))
+
+    def backward_weight(self, slot, accumulate=False, stream=None):
+        call("slip_backward_weight", self.ctx, slot, int(accumulate), _stream(stream))
+
+    def backward_coupled(self, slot, dy, dx=None, accumulate=False, stream=None):
+        call("slip_backward_coupled", self.ctx, slot, _ptr(dy), _ptr(dx) if dx is not None else None,
+             int(accumulate), _stream(stream))
+
+    def optimizer_step(self, step, lr=1e-3, beta1=0.9, beta2=0.95, eps=1e-8, weight_decay=0.1, grad_scale=1.0,
+                       nonfinite=None, stream=None):
+        a = slip_adam(lr, beta1, beta2, eps, weight_decay)
+        call("slip_optimizer_step", self.ctx, C.byref(a), int(step), float(grad_scale),
+             _ptr(nonfinite) if nonfinite is not None else None, _stream(stream))
+
+    def loss_mse(self, y, target, dy, d_loss, stream=None):
+        call("slip_loss_mse", self.ctx, _ptr(y), _ptr(target), _ptr(dy), _ptr(d_loss), _stream(stream))
+
+
+def synth_normal(out, seed, k, j, stream=None):
+    call("slip_synth_normal", _ptr(out), out.numel(), int(seed), int(k), int(j), _stream(stream))
+
+
+def gemm(a, b, c, M, N, K, lda, ldb, ldc, a_mn=False, b_mn=False, mode=0, bn=256, accumulate=False, alpha=1.0,
+         stream=None):
+    call("slip_gemm", M, N, K, _ptr(a), lda, int(a_mn), _ptr(b), ldb, int(b_mn), _ptr(c), ldc, mode, bn,
+         int(accumulate), float(alpha), _stream(stream))
+
+
+class Comm:
+    """NCCL communicators of this rank.  The unique id is created by rank 0 and
+    broadcast over an existing torch.distributed group (plumbing only)."""
+
+    def __init__(self, rank: int, world: int, pg=None):
+        import torch
+        import torch.distributed as dist
+        buf = (C.c_uint8 * 128)()
+        if rank == 0:
+            call("slip_nccl_unique_id", buf)
+        t = torch.tensor(list(bytes(buf)), dtype=torch.uint8)
+        if world > 1:
+            if dist.get_backend(pg) == "nccl":
+                t = t.cuda()
+            dist.broadcast(t, 0, group=pg)
+        idb = (C.c_uint8 * 128)(*t.cpu().tolist())
+        h = C.c_void_p()
+        call("slip_comm_create", C.byref(h), rank, world, idb)
+        self.h, self.rank, self.world = h, rank, world
+        self._cluster = None
+
+    def setup(self, N, DP, m, live=None):
+        self._cluster = make_cluster(N, DP, m, live)
+        call("slip_comm_setup", self.h, C.byref(self._cluster))
+
+    def close(self):
+        if self.h:
+            lib().slip_comm_destroy(self.h)
+            self.h = None
+
+
+def grad_allreduce(stage: Stage, comm: Comm, stream=None):
+    call("slip_grad_allreduce", stage.ctx, comm.h, _stream(stream))
+
+
+def execute_schedule(stage: Stage, comm: Comm, N, DP, m, live, costs: slip_costs, decoupled=True, staggered=True,
+                     adam=(1e-4, 0.9, 0.95, 1e-8, 0.1), warmup=0, iterations=1, seed=1234, io=None,
+                     stream=None) -> slip_report:
+    cl = make_cluster(N, DP, m, live)
+    opts = slip_plan_opts(int(decoupled), int(staggered), 1)
+    a = slip_adam(*adam)
+    rep = slip_report()
+    call("slip_execute_schedule", stage.ctx, comm.h, C.byref(cl), C.byref(costs), C.byref(opts), C.byref(a),
+         int(warmup), int(iterations), C.c_uint64(seed), C.byref(io) if io is not None else None, _stream(stream),
+         C.byref(rep))
+    return rep
+
+
+def make_io(x_host_list, target_host_list, loss_host):
+    """Host buffers for an end-to-end run: lists of pinned torch CPU tensors
+    indexed k*m + j, and a float32 CPU tensor for the losses."""
+    xs = (C.c_void_p * len(x_host_list))(*[t.data_ptr() for t in x_host_list])
+    rs = (C.c_void_p * len(target_host_list))(*[t.data_ptr() for t in target_host_list])
+    io = slip_io(C.cast(xs, C.POINTER(C.c_void_p)), C.cast(rs, C.POINTER(C.c_void_p)),
+                 C.cast(C.c_void_p(loss_host.data_ptr()), C.POINTER(C.c_float)))
+    io._keep = (xs, rs, x_host_list, target_host_list, loss_host)
+    return io
+
+
+__all__ = ["Stage", "Comm", "PlanResult", "SlipError", "assign", "execute_schedule", "gemm", "grad_allreduce",
+           "make_cluster", "make_costs", "make_io", "make_model", "plan_schedule", "recoverable", "synth_normal"]

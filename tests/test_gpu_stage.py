@@ -1,0 +1,203 @@
+"""Stage-level parity: the CUDA path through the C ABI (slip_stage_forward,
+slip_backward_input, slip_backward_weight, slip_optimizer_step) against the
+fp64 oracle on the same seeded bf16 inputs.
+
+Tolerances (BASELINE.json north_star):
+  * bf16 tensor-core paths: normwise relative error ||g - r||_inf / ||r||_inf <= 2e-2
+  * fp32 optimizer: <= 1e-4 (on identical fp32 inputs)
+  * decoupled B + W vs coupled backward on the GPU: bit-exact
+"""
+import numpy as np
+import pytest
+import torch
+
+import slipdata as sd
+from oracle import adam as OA
+from oracle import layer as OL
+
+pytestmark = pytest.mark.gpu
+
+GATE_A = 2e-2
+GATE_B = 1e-4
+
+
+def _rt():
+    from paper_2405_14009_b200 import runtime
+    return runtime
+
+
+def relerr(g, r):
+    g = np.asarray(g, dtype=np.float64)
+    return float(np.max(np.abs(g - r)) / max(np.max(np.abs(r)), 1e-300))
+
+
+def to_dev_bf16(x):
+    bits = sd.to_bf16_bits(x)
+    return torch.from_numpy(bits.view(np.int16)).view(torch.bfloat16).cuda()
+
+
+def to_np(t):
+    return t.float().cpu().numpy().astype(np.float64)
+
+
+def run_stage(cfg, n_layers, seed_k=0, seed_j=0):
+    rt = _rt()
+    layers = sd.stage_params(cfg, 0, n_layers, total_layers=max(n_layers, 2))
+    flat = sd.pack_stage(layers)
+    st = rt.Stage(cfg, n_layers, n_slots=2)
+    st.load_master(torch.from_numpy(flat).float().cuda())
+    x = sd.stage_input(cfg, seed_k, seed_j)
+    r = sd.stage_target(cfg, seed_k, seed_j)
+    xd, rd = to_dev_bf16(x), to_dev_bf16(r)
+    y = torch.empty_like(xd)
+    dx = torch.empty_like(xd)
+    st.forward(0, xd, y)
+    st.backward_input(0, rd, dx, accumulate=False)
+    st.backward_weight(0, accumulate=False)
+    torch.cuda.synchronize()
+    return st, layers, x, r, y, dx
+
+
+CFGS = {
+    "c1": (sd.C1_TINY, 1),
+    "c1x2": (sd.C1_TINY, 2),
+    "d80_ragged": (sd.ModelCfg(hidden=640, heads=8, ffn=2560, seq=200, micro_batch=1, layers=1), 1),
+    "d128_b2": (sd.ModelCfg(hidden=512, heads=4, ffn=2048, seq=384, micro_batch=2, layers=1), 1),
+    "d64": (sd.ModelCfg(hidden=256, heads=4, ffn=1024, seq=136, micro_batch=2, layers=1), 1),
+}
+
+
+@pytest.mark.parametrize("name", list(CFGS))
+def test_stage_step_matches_oracle(name):
+    cfg, L = CFGS[name]
+    st, layers, x, r, y, dx = run_stage(cfg, L)
+    out, caches = OL.stage_forward(layers, x, cfg)
+    dxr, grads = OL.stage_backward_coupled(layers, caches, r, cfg)
+    assert relerr(to_np(y), out) <= GATE_A
+    assert relerr(to_np(dx), dxr) <= GATE_A
+    g = sd.unpack_stage(st.grad.cpu().numpy().astype(np.float64), cfg, L)
+    for l in range(L):
+        for n in sd.PARAM_ORDER:
+            e = relerr(g[l][n], grads[l][n])
+            assert e <= GATE_A, (name, l, n, e)
+
+
+def test_decoupled_equals_coupled_on_gpu():
+    """B then W (deferred) and the coupled backward produce bit-identical grads."""
+    cfg = sd.C1_TINY
+    st, layers, x, r, y, dx = run_stage(cfg, 2)
+    g1 = st.grad.clone()
+    xd, rd = to_dev_bf16(x), to_dev_bf16(r)
+    dx2 = torch.empty_like(xd)
+    st.forward(1, xd, y)
+    st.backward_coupled(1, rd, dx2, accumulate=False)
+    torch.cuda.synchronize()
+    assert torch.equal(st.grad, g1)
+    assert torch.equal(dx, dx2)
+
+
+def test_accumulation_over_microbatches():
+    cfg = sd.C1_TINY
+    rt = _rt()
+    layers = sd.stage_params(cfg, 0, 1)
+    st = rt.Stage(cfg, 1, n_slots=2)
+    st.load_master(torch.from_numpy(sd.pack_stage(layers)).float().cuda())
+    ref = None
+    for j in range(3):
+        x, r = sd.stage_input(cfg, 0, j), sd.stage_target(cfg, 0, j)
+        y = torch.empty(cfg.tokens, cfg.hidden, dtype=torch.bfloat16, device="cuda")
+        st.forward(j % 2, to_dev_bf16(x), y)
+        st.backward_input(j % 2, to_dev_bf16(r), None, accumulate=j > 0)
+        st.backward_weight(j % 2, accumulate=j > 0)
+        out, c = OL.stage_forward(layers, x, cfg)
+        _, g = OL.stage_backward_coupled(layers, c, r, cfg)
+        ref = g if ref is None else [{n: a[n] + b[n] for n in a} for a, b in zip(ref, g)]
+    torch.cuda.synchronize()
+    got = sd.unpack_stage(st.grad.cpu().numpy().astype(np.float64), cfg, 1)
+    for n in sd.PARAM_ORDER:
+        assert relerr(got[0][n], ref[0][n]) <= GATE_A, n
+
+
+def test_slot_state_machine():
+    rt = _rt()
+    cfg = sd.C1_TINY
+    st = rt.Stage(cfg, 1, n_slots=1)
+    d = torch.zeros(cfg.tokens, cfg.hidden, dtype=torch.bfloat16, device="cuda")
+    with pytest.raises(rt.SlipError) as e:
+        st.backward_input(0, d, d)
+    assert e.value.code == 4  # SLIP_ESTATE: B before F
+    st.forward(0, d, d.clone())
+    with pytest.raises(rt.SlipError):
+        st.forward(0, d, d.clone())
+    with pytest.raises(rt.SlipError):
+        st.backward_weight(0)
+
+
+def test_adamw_matches_oracle():
+    """Fused AdamW on identical fp32 inputs (GPU gradients fed to both)."""
+    cfg = sd.C1_TINY
+    st, layers, x, r, y, dx = run_stage(cfg, 1)
+    p0 = st.master.cpu().numpy().astype(np.float64)
+    g = st.grad.cpu().numpy().astype(np.float64)
+    acfg = OA.AdamCfg(lr=1e-3, beta1=0.9, beta2=0.95, eps=1e-8, weight_decay=0.1)
+    flag = torch.zeros(1, dtype=torch.int32, device="cuda")
+    P = sd.unpack_layer(p0, cfg)
+    G = sd.unpack_layer(g, cfg)
+    Z = {n: np.zeros_like(v) for n, v in P.items()}
+    m, v = Z, Z
+    for step in (1, 2, 3):
+        st.optimizer_step(step, lr=acfg.lr, beta1=acfg.beta1, beta2=acfg.beta2, eps=acfg.eps,
+                          weight_decay=acfg.weight_decay, grad_scale=0.25, nonfinite=flag)
+        P, m, v = OA.adamw_step_layer(P, m, v, G, step, acfg, grad_scale=0.25)
+    torch.cuda.synchronize()
+    got = st.master.cpu().numpy().astype(np.float64)
+    ref = sd.pack_layer(P)
+    # compare the accumulated update p - p0 (the quantity Adam computes)
+    assert relerr(got - p0, ref - p0) <= GATE_B
+    assert relerr(st.adam_m.cpu().numpy().astype(np.float64), sd.pack_layer(m)) <= GATE_B
+    assert relerr(st.adam_v.cpu().numpy().astype(np.float64), sd.pack_layer(v)) <= GATE_B
+    assert int(flag.item()) == 0
+    # bf16 weights = RNE(master)
+    w = st.w.float().cpu().numpy().astype(np.float64)
+    assert np.array_equal(w, sd.bf16_round(got))
+    # non-finite flag
+    st.grad[5] = float("inf")
+    st.optimizer_step(4, nonfinite=flag)
+    torch.cuda.synchronize()
+    assert int(flag.item()) == 1
+
+
+def test_mse_head_and_synth():
+    rt = _rt()
+    cfg = sd.C1_TINY
+    st = rt.Stage(cfg, 1, n_slots=1)
+    y, r = sd.stage_input(cfg, 1, 2), sd.stage_target(cfg, 1, 2)
+    dy = torch.empty(cfg.tokens, cfg.hidden, dtype=torch.bfloat16, device="cuda")
+    loss = torch.zeros(1, device="cuda")
+    st.loss_mse(to_dev_bf16(y), to_dev_bf16(r), dy, loss)
+    torch.cuda.synchronize()
+    lref, dref = OL.loss_mse(y, r)
+    assert abs(loss.item() - lref) <= 1e-4 * lref
+    assert relerr(to_np(dy), dref) <= GATE_A
+    a = torch.empty(1 << 16, dtype=torch.bfloat16, device="cuda")
+    b = torch.empty_like(a)
+    rt.synth_normal(a, 7, 1, 2)
+    rt.synth_normal(b, 7, 1, 2)
+    torch.cuda.synchronize()
+    assert torch.equal(a, b)
+    af = a.float()
+    assert abs(af.mean().item()) < 0.02 and abs(af.std().item() - 1.0) < 0.02
+
+
+@pytest.mark.slow
+def test_one_layer_c2_full_size():
+    """One GPT-1.3B-shaped layer at full size (h 2048, s 2048, 16 heads), fp64 oracle on the host."""
+    cfg = sd.ModelCfg(hidden=2048, heads=16, ffn=8192, seq=2048, micro_batch=1, layers=24)
+    st, layers, x, r, y, dx = run_stage(cfg, 1)
+    out, caches = OL.stage_forward(layers, x, cfg)
+    dxr, grads = OL.stage_backward_coupled(layers, caches, r, cfg)
+    assert relerr(to_np(y), out) <= GATE_A
+    assert relerr(to_np(dx), dxr) <= GATE_A
+    g = sd.unpack_stage(st.grad.cpu().numpy().astype(np.float64), cfg, 1)
+    for n in sd.PARAM_ORDER:
+        assert relerr(g[0][n], grads[0][n]) <= GATE_A, n

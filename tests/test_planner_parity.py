@@ -1,0 +1,72 @@
+"""Bit-exact parity of the C++ planner (libslip, via the C ABI, CPU only) with
+the Python oracle planner: assignment, every op (stage, mb, origin, phase,
+exec, iter, start, end), makespans, period and the 64-bit plan hash."""
+import numpy as np
+import pytest
+
+from oracle import planner as PL
+
+
+def _rt():
+    from paper_2405_14009_b200 import runtime
+    return runtime
+
+
+def live_grid(N, DP, failed=()):
+    lv = [[1] * DP for _ in range(N)]
+    for (i, k) in failed:
+        lv[i][k] = 0
+    return lv
+
+
+def instances(n, seed=5):
+    rng = np.random.default_rng(seed)
+    out = [
+        (4, 3, 6, [], PL.Costs(1, 1, 1), False, False, 3),
+        (4, 3, 6, [(2, 1)], PL.Costs(1, 1, 1), False, False, 3),
+        (4, 3, 6, [(2, 1)], PL.Costs(1, 1, 1), True, False, 3),
+        (4, 3, 6, [(2, 1)], PL.Costs(1, 1, 1), True, True, 3),
+        (4, 2, 3, [(3, 1)], PL.Costs(10, 11, 9, 1, 3, 2, 30, 17), True, True, 4),
+        (4, 2, 3, [(2, 1), (3, 0)], PL.Costs(10, 11, 9, 1, 3, 2, 30, 17), True, True, 4),
+    ]
+    while len(out) < n:
+        N = int(rng.integers(1, 6)); DP = int(rng.integers(1, 5)); m = int(rng.integers(1, 7))
+        failed = {(int(rng.integers(0, N)), int(rng.integers(0, DP))) for _ in range(int(rng.integers(0, N * DP)))}
+        if not PL.recoverable(live_grid(N, DP, failed)):
+            continue
+        af = int(rng.integers(5, 20)); aw = int(rng.integers(1, af))
+        lim = 0 if rng.integers(0, 2) else int(af * (N + 1) * 2)
+        costs = PL.Costs(*(int(rng.integers(1, 9)) for _ in range(3)), int(rng.integers(0, 4)),
+                         int(rng.integers(0, 4)), int(rng.integers(0, 4)), af, aw, lim)
+        out.append((N, DP, m, sorted(failed), costs, bool(rng.integers(0, 2)), bool(rng.integers(0, 2)),
+                    int(rng.integers(1, 4))))
+    return out
+
+
+@pytest.mark.parametrize("inst", instances(80))
+def test_cpp_planner_matches_oracle(inst):
+    rt = _rt()
+    N, DP, m, failed, c, dec, stag, H = inst
+    lv = live_grid(N, DP, failed)
+    costs = rt.make_costs(c.t_f, c.t_b, c.t_w, c.t_comm, c.t_ar, c.t_opt, c.a_f, c.a_w, c.m_limit)
+    try:
+        ref = PL.schedule(lv, m, c, PL.Opts(dec, stag, H))
+    except RuntimeError:
+        with pytest.raises(rt.SlipError):
+            rt.plan_schedule(N, DP, m, lv, costs, dec, stag, H)
+        return
+    got = rt.plan_schedule(N, DP, m, lv, costs, dec, stag, H)
+    assert got.ops == [o.key() for o in ref.ops]
+    assert got.makespans == ref.makespans
+    assert got.period == ref.period
+    assert got.hash == PL.plan_hash(ref.ops)
+    assert rt.assign(N, DP, m, lv) == PL.assign(lv, m)
+
+
+def test_cpp_recoverable_and_unrecoverable():
+    rt = _rt()
+    assert rt.recoverable(4, 3, live_grid(4, 3, [(1, 0), (2, 2)]))
+    assert not rt.recoverable(2, 2, live_grid(2, 2, [(1, 0), (1, 1)]))
+    with pytest.raises(rt.SlipError) as e:
+        rt.plan_schedule(2, 2, 2, live_grid(2, 2, [(1, 0), (1, 1)]), rt.make_costs())
+    assert e.value.code == 2  # SLIP_EUNRECOVERABLE
