@@ -1,0 +1,357 @@
+#!/usr/bin/env python
+"""bench.py — training throughput of the SlipStream decoupled-B/W stage step on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--failures F] [--impl slip|reference]
+    torchrun --nproc-per-node N bench.py --gpus N ...      (N > 1: one rank per GPU, NCCL)
+
+Workload (BASELINE.json configs[1]): GPT-1.3B-shaped model (h 2048, 16 heads,
+ffn 8192, s 2048, b 1), bf16 with fp32 accumulation / master weights, synthetic
+data.  N = 1: the full 24-layer model on one GPU (DP1 x PP1), m = 4
+micro-batches per step.  N > 1: DP 2 x PP N/2, 24/PP layers per stage and
+m = 4*PP micro-batches per pipeline, so the per-GPU work is fixed (weak
+scaling).  A step is one training iteration of the plan: F, B (input grads),
+deferred W (weight grads), the per-stage DP all-reduce and the staggered AdamW.
+--failures F masks F ranks at the normalized positions (last stages, distinct
+peer groups); their micro-batches are re-routed to the DP peer.
+
+One JSON line on rank 0 (contract in the task statement): value = whole-job
+tokens/s over exactly K timed steps (CUDA events, max over ranks), plus e2e
+(pinned-host inputs / loss read-back every step), roofline of the dominant
+kernel family (the W GEMMs) measured live, cpu_baseline (fp64 oracle on the
+host cores, bounded sample, rank 0 at N = 1), clocks sampled during the timed
+region and the number of libslip kernels launched.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "train tokens/sec at 0/1/2 failures, 1-8 B200; B/W tensor-pipe % of peak"
+H, HEADS, FFN, SEQ, MB, LAYERS = 2048, 16, 8192, 2048, 1, 24
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="slip", choices=["slip", "reference"])
+    ap.add_argument("--failures", type=int, default=0)
+    ap.add_argument("--m", type=int, default=0, help="micro-batches per pipeline (default 4*PP)")
+    ap.add_argument("--layers", type=int, default=LAYERS)
+    ap.add_argument("--coupled", action="store_true", help="coupled backward, no staggering (1F1B baseline)")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    return ap.parse_args()
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return p.get("bf16_tflops", 1590.0), p.get("bf16_tflops_sustained", 1400.0), p.get("hbm_gbs", 6650.0), \
+            "measured"
+    except Exception:
+        return 1590.0, 1400.0, 6650.0, "fallback"
+
+
+# ---------------------------------------------------------------- clocks
+class ClockSampler:
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self):
+        self.p = None
+
+    def start(self):
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                                       "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.p = None
+
+    def stop(self):
+        if self.p is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.15)
+        self.p.terminate()
+        out, _ = self.p.communicate(timeout=10)
+        rows = []
+        for line in out.strip().splitlines():
+            f = [x.strip() for x in line.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                rows.append((int(f[0]), float(f[1]), float(f[2]), float(f[3]), f[5:9]))
+            except ValueError:
+                continue
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"]}
+        pmax = max(r[3] for r in rows)
+        load = [r for r in rows if r[3] >= 0.5 * pmax] or rows
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in load for i, v in enumerate(r[4]) if v.lower().startswith("active")})
+        return {"sm_mhz": statistics.median(r[1] for r in load), "sm_max_mhz": max(r[2] for r in rows),
+                "reasons": reasons, "samples": len(rows), "samples_under_load": len(load),
+                "power_w_max": pmax}
+
+
+# ---------------------------------------------------------------- oracle (CPU baseline)
+def oracle_sample(layers_total, m):
+    """fp64 oracle on the host: one GPT-1.3B-shaped layer x one micro-batch of F + B + W
+    plus AdamW over one layer's parameters; extrapolated to layers_total x m."""
+    import numpy as np
+
+    import slipdata as sd
+    from oracle import adam as OA
+    from oracle import layer as OL
+    cfg = sd.ModelCfg(hidden=H, heads=HEADS, ffn=FFN, seq=SEQ, micro_batch=MB, layers=layers_total)
+    P = sd.layer_params(cfg, 0, 0)
+    x, r = sd.stage_input(cfg, 0, 0), sd.stage_target(cfg, 0, 0)
+    t0 = time.perf_counter()
+    out, c = OL.layer_forward(P, x, cfg)
+    _, dout = OL.loss_mse(out, r)
+    dx, bg, st = OL.layer_backward_input(P, c, dout, cfg)
+    wg = OL.layer_backward_weight(st)
+    t1 = time.perf_counter()
+    grads = dict(**bg, **wg)
+    z = {k: np.zeros_like(v) for k, v in P.items()}
+    OA.adamw_step_layer(P, z, z, grads, 1, OA.AdamCfg(), grad_scale=1.0 / m)
+    t2 = time.perf_counter()
+    t_layer, t_adam = t1 - t0, t2 - t1
+    step_s = layers_total * (m * t_layer + t_adam)
+    tokens = m * MB * SEQ
+    return tokens / step_s, t_layer, t_adam
+
+
+def cpu_cores():
+    try:
+        return len(os.sched_getaffinity(0))
+    except Exception:
+        return os.cpu_count() or 1
+
+
+def run_reference(args, rank, world):
+    """--impl reference: the fp64 oracle, as it stands, on the host cores (rank 0 only)."""
+    if rank != 0:
+        return
+    m = args.m or 4
+    vals = []
+    samples = []
+    for step in range(args.warmup + args.steps):
+        v, tl, ta = oracle_sample(args.layers, m)
+        if step >= args.warmup:
+            vals.append(v)
+            samples.append(tl + ta)
+    value = statistics.median(vals)
+    ms = 1000.0 * (m * MB * SEQ) / value
+    cores = cpu_cores()
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": "gpt-1.3B-shape (h2048 s2048 16 heads ffn8192) %d layers, m=%d, DP1xPP1" % (
+            args.layers, m), "model": "gpt-1.3b-shape", "global_batch": m * MB, "seq_len": SEQ,
+            "parallelism": "host"},
+        "cpu_baseline": {"value": value, "unit": "tokens/s", "cores": cores, "kind": "oracle",
+                         "sample": "per step: 1 layer x 1 micro-batch F+B+W (T=2048, h=2048) + AdamW over 1 layer,"
+                                   " fp64 numpy, extrapolated to %d layers x %d micro-batches" % (args.layers, m)},
+        "e2e": {"value": value, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------- GPU arm
+def main():
+    args = parse()
+    rank = int(os.environ.get("RANK", 0))
+    world = int(os.environ.get("WORLD_SIZE", 1))
+    local = int(os.environ.get("LOCAL_RANK", 0))
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+        return
+    import torch
+    import torch.distributed as dist
+
+    import slipdata as sd
+    from paper_2405_14009_b200 import runtime as rt
+    if world != args.gpus:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE {world}")
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    DP = 1 if world == 1 else 2
+    PP = world // DP
+    assert DP * PP == world and args.layers % PP == 0
+    L = args.layers // PP
+    m = args.m or 4 * PP
+    cfg = sd.ModelCfg(hidden=H, heads=HEADS, ffn=FFN, seq=SEQ, micro_batch=MB, layers=args.layers)
+    T = cfg.tokens
+    # failures at normalized positions: last stages, distinct peer groups (R20)
+    failed = [(PP - 1 - q, (q + 1) % DP) for q in range(args.failures)]
+    live = [[1] * DP for _ in range(PP)]
+    for (i, k) in failed:
+        live[i][k] = 0
+    if not rt.recoverable(PP, DP, live):
+        if rank == 0:
+            print(json.dumps({"metric": METRIC, "value": None, "unit": "tokens/s", "n_gpus": world,
+                              "error": "unrecoverable failure set %s (a stage lost every worker)" % failed}))
+        return
+    decoupled, staggered = (not args.coupled), (not args.coupled)
+    # nominal integer costs ~ FLOP ratios of F : B : W, refined by profiling below
+    costs = rt.make_costs(t_f=108, t_b=117, t_w=100, t_comm=1, t_ar=10, t_opt=10)
+    # slots = max in-flight micro-batches (F started, W not finished) of any worker in the plan
+    plan = rt.plan_schedule(PP, DP, m, live, costs, decoupled, staggered, horizon=2)
+    n_slots = 1
+    for i in range(PP):
+        for k in range(DP):
+            cur = mx = 0
+            for o in sorted((o for o in plan.ops if o[0] == i and o[4] == k and o[3] in (0, 2, 3)),
+                            key=lambda o: o[6]):
+                cur += 1 if o[3] == 0 else -1
+                mx = max(mx, cur)
+            n_slots = max(n_slots, mx)
+    stage = rt.Stage(cfg, L, n_slots)
+    rt.init_master_(stage.master, cfg, L, args.layers, seed=rank % PP)
+    rt.call("slip_weights_from_master", stage.ctx, rt._stream())
+    comm = rt.Comm(rank, world)
+    comm.setup(PP, DP, m, live)
+    stream = torch.cuda.current_stream()
+
+    def allreduce_max(v):
+        if world == 1:
+            return v
+        t = torch.tensor([v], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return t.item()
+
+    def barrier():
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+
+    def execute(iters, io=None):
+        return rt.execute_schedule(stage, comm, PP, DP, m, live, costs, decoupled, staggered, warmup=0,
+                                   iterations=iters, seed=1234, io=io)
+
+    # profile pass (§4.1 Profiler): measured per-op times -> integer planner costs (10 us units)
+    rep = execute(max(1, args.warmup))
+    per = []
+    for ph in (0, 1, 2, 3, 4):
+        n = rep.phase_ops[ph]
+        per.append(allreduce_max(rep.phase_ms[ph] / n if n else 0.0))
+    q = lambda ms: max(1, int(round(ms * 100)))  # noqa: E731
+    costs = rt.make_costs(t_f=q(per[0]), t_b=q(per[1] or per[3]), t_w=q(per[2] or 0.01), t_comm=1,
+                          t_ar=q(per[4] * 0.5 if per[4] else 0.01), t_opt=q(per[4] or 0.01))
+    # warm-up steps with the profiled plan
+    execute(args.warmup)
+    barrier()
+    clocks = ClockSampler() if rank == 0 else None
+    if clocks:
+        clocks.start()
+        time.sleep(0.3)
+    barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    rep = execute(args.steps)
+    e1.record(stream)
+    barrier()
+    ms_total = allreduce_max(e0.elapsed_time(e1))
+    clk = clocks.stop() if clocks else None
+    tokens_per_step = DP * m * T
+    value = tokens_per_step * args.steps / (ms_total / 1000.0)
+    # roofline of the dominant kernel family: the W GEMMs (dW += dY^T X, fp32 epilogue)
+    w_ops = rep.phase_ops[2] + rep.phase_ops[3]
+    w_ms = rep.phase_ms[2] if rep.phase_ops[2] else rep.phase_ms[3]
+    flops_w_op = 2.0 * T * (4 * H * H + 2 * FFN * H) * L  # 4 products per layer
+    w_launches = rep.w_gemm_launches
+    ach = flops_w_op * rep.phase_ops[2] / (rep.phase_ms[2] / 1e3) / 1e12 if rep.phase_ops[2] else None
+    p_burst, p_sus, hbm, peak_src = peaks()
+    traffic = None
+    try:
+        with open(os.path.join(ROOT, "profiles", "w_gemm_traffic.json")) as f:
+            traffic = json.load(f).get("dram_bytes_per_launch")
+    except Exception:
+        pass
+    kern =torch.tensor([rep.n_kernels], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(kern)
+    gpu_launches = int(kern.item())
+    # e2e through the C ABI with pinned host buffers: every step copies its inputs H2D and
+    # reads the losses back D2H (one executor call per step)
+    e2e = None
+    if not args.no_e2e:
+        xs = [torch.empty(T, H, dtype=torch.bfloat16).pin_memory() for _ in range(DP * m)]
+        rs = [torch.empty(T, H, dtype=torch.bfloat16).pin_memory() for _ in range(DP * m)]
+        g = torch.Generator().manual_seed(7)
+        for a in xs + rs:
+            a.copy_(torch.randn(T, H, generator=g).to(torch.bfloat16))
+        loss_host = torch.zeros(DP * m, dtype=torch.float32).pin_memory()
+        io = rt.make_io(xs, rs, loss_host)
+        execute(1, io)
+        barrier()
+        f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        f0.record(stream)
+        for _ in range(args.steps):
+            r = execute(1, io)
+        f1.record(stream)
+        barrier()
+        e2e_ms = allreduce_max(f0.elapsed_time(f1))
+        # bytes per step over the whole job: X for every stage-0 F, targets for every last-stage B
+        h2d = 2 * DP * m * T * H * 2
+        e2e = {"value": tokens_per_step * args.steps / (e2e_ms / 1000.0), "unit": "tokens/s",
+               "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": 4 * DP * m,
+               "last_loss": float(r.last_loss) if (rank % PP) == PP - 1 else None}
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        v, tl, ta = oracle_sample(args.layers, m)
+        cpu = {"value": v, "unit": "tokens/s", "cores": cpu_cores(), "kind": "oracle",
+               "sample": "1 layer x 1 micro-batch F+B+W (T=2048, h=2048) %.1f s + AdamW over 1 layer %.1f s, fp64"
+                         " numpy, extrapolated to %d layers x %d micro-batches" % (tl, ta, args.layers, m)}
+    if rank != 0:
+        return
+    ms_step = ms_total / args.steps
+    line = {
+        "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
+        "config": {"workload": "gpt-1.3B-shape (h2048, 16 heads, ffn 8192, s2048, b1) %d layers, DP%dxPP%d, "
+                               "m=%d micro-batches/pipeline, %s, failures=%d" % (
+                                   args.layers, DP, PP, m,
+                                   "coupled 1F1B" if args.coupled else "decoupled B/W + staggered AdamW",
+                                   args.failures),
+                   "model": "gpt-1.3b-shape", "global_batch": DP * m * MB, "seq_len": SEQ,
+                   "parallelism": "dp%dxpp%d" % (DP, PP), "failed_workers": failed,
+                   "l2": "inputs larger than L2 (2.4 GB bf16 weights + GBs of stash per step)"},
+        "clocks": clk,
+        "e2e": e2e,
+        "gpu_launches": gpu_launches,
+        "roofline": {"bound": "tensor", "kernel": "W GEMMs (tcgen05, dW += dY^T X fused fp32 TMA reduce-add)",
+                     "achieved": ach, "peak": p_sus, "peak_kind": "bf16_tflops_sustained (%s)" % peak_src,
+                     "unit": "TFLOP/s", "frac": (ach / p_sus) if ach else None, "traffic": traffic,
+                     "flops_per_launch": flops_w_op / (4 * L), "launches": w_launches,
+                     "avg_launch_ms": (rep.phase_ms[2] / w_launches) if w_launches else None},
+        "phases_ms_per_step": {n: rep.phase_ms[i] / args.steps for i, n in enumerate(("F", "B", "W", "BC", "OPT"))},
+        "predicted_period_units": rep.predicted_period,
+        "planner_costs_10us": [costs.t_f, costs.t_b, costs.t_w, costs.t_opt],
+    }
+    if cpu:
+        line["cpu_baseline"] = cpu
+    print(json.dumps(line), flush=True)
+    comm.close()
+    stage.close()
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

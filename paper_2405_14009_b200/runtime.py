@@ -33,6 +33,40 @@ def make_cluster(N: int, DP: int, m: int, live=None):
     return cl
 
 
+def param_offsets(h: int, f: int) -> dict:
+    """Element offsets of one layer's tensors in the flat parameter vector
+    (include/slip.h "Parameter layout")."""
+    names = [("wqkv", 3 * h * h), ("bqkv", 3 * h), ("wo", h * h), ("bo", h), ("g1", h), ("b1n", h), ("g2", h),
+             ("b2n", h), ("w1", f * h), ("b1", f), ("w2", h * f), ("b2", h)]
+    out, off = {}, 0
+    for n, sz in names:
+        out[n] = (off, sz)
+        off += sz
+    out["per_layer"] = off
+    return out
+
+
+def init_master_(master, cfg, n_layers, total_layers, seed=0):
+    """Synthetic random init on the device (throughput runs): matrices ~ N(0, 0.02^2)
+    (Wo, W2 scaled by 1/sqrt(2L)), biases 0, LayerNorm gamma 1, beta 0."""
+    import math
+
+    import torch
+    g = torch.Generator(device=master.device).manual_seed(seed)
+    po = param_offsets(cfg.hidden, cfg.ffn)
+    P = po["per_layer"]
+    master.zero_()
+    for l in range(n_layers):
+        base = l * P
+        for n in ("wqkv", "wo", "w1", "w2"):
+            off, sz = po[n]
+            std = 0.02 / math.sqrt(2.0 * total_layers) if n in ("wo", "w2") else 0.02
+            master[base + off: base + off + sz].normal_(0.0, std, generator=g)
+        for n in ("g1", "g2"):
+            off, sz = po[n]
+            master[base + off: base + off + sz].fill_(1.0)
+
+
 def make_costs(t_f=1, t_b=1, t_w=1, t_comm=0, t_ar=0, t_opt=0, a_f=0, a_w=0, m_limit=0) -> slip_costs:
     return slip_costs(t_f, t_b, t_w, t_comm, t_ar, t_opt, a_f, a_w, m_limit)
 
