@@ -253,6 +253,39 @@ slip_status slip_comm_destroy(slip_comm* comm);
  * singleton group returns without communicating. */
 slip_status slip_grad_allreduce(slip_ctx* ctx, slip_comm* comm, slip_stream s);
 
+/* ------------------------------------------------------------- rank programs
+ * The executor interprets a per-rank program derived from the plan (host
+ * logic only, no GPU): for every op of worker (i, k) in planned order, the
+ * receive / load that feeds it, the compute, and the send that follows it.
+ * Slots are allocated at F (lowest free index) and released after W / BC. */
+typedef enum {
+  SLIP_ACT_LOAD_X = 0,   /* stage 0: input of micro-batch (origin, mb) into slot.x */
+  SLIP_ACT_RECV_X = 1,   /* ncclRecv activation from rank `peer` into slot.x (ReRouteAct) */
+  SLIP_ACT_F = 2,        /* slip_stage_forward(slot), output -> slot.dy */
+  SLIP_ACT_SEND_Y = 3,   /* ncclSend slot.dy (the activation) to rank `peer` */
+  SLIP_ACT_LOSS = 4,     /* last stage: MSE head, target of (origin, mb); dy -> slot.dy */
+  SLIP_ACT_RECV_DY = 5,  /* ncclRecv output gradient from rank `peer` into slot.dy (ReRouteGrad) */
+  SLIP_ACT_B = 6,        /* slip_backward_input(slot), dx -> slot.x (stage > 0) */
+  SLIP_ACT_SEND_DX = 7,  /* ncclSend slot.x (the input gradient) to rank `peer` */
+  SLIP_ACT_W = 8,        /* slip_backward_weight(slot); slot released */
+  SLIP_ACT_BC = 9,       /* coupled backward (B then W); slot released */
+  SLIP_ACT_AR = 10,      /* stage DP all-reduce of iteration `iter` */
+  SLIP_ACT_OPT = 11      /* AdamW step of iteration `iter` */
+} slip_action_kind;
+
+typedef struct {
+  int32_t kind, iter, mb, origin;
+  int32_t peer;        /* rank, or -1 */
+  int32_t slot;        /* or -1 */
+  int32_t accumulate;  /* B / W: 0 = first of the iteration on this worker (overwrite) */
+} slip_action;
+
+/* Program of `rank` (worker (rank % N, rank / N)) for a plan of opts->horizon
+ * iterations.  *n = number of actions (call with cap = 0 to size), *n_slots =
+ * slots the program needs.  A failed rank gets an empty program. */
+slip_status slip_rank_program(const slip_cluster* c, const slip_costs* costs, const slip_plan_opts* opts,
+                              int32_t rank, slip_action* out, int64_t cap, int64_t* n, int32_t* n_slots);
+
 /* ------------------------------------------------------------------ executor
  * Host buffers for an end-to-end run (may be NULL: inputs are then generated
  * on the device by slip_synth_normal with (seed, k, j) and targets with

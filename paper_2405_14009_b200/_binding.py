@@ -51,6 +51,17 @@ class slip_op(C.Structure):
         return (self.stage, self.mb, self.origin, self.phase, self.exec, self.iter, self.start, self.end)
 
 
+class slip_action(C.Structure):
+    _fields_ = [("kind", C.c_int32), ("iter", C.c_int32), ("mb", C.c_int32), ("origin", C.c_int32),
+                ("peer", C.c_int32), ("slot", C.c_int32), ("accumulate", C.c_int32)]
+
+    def key(self):
+        return (self.kind, self.iter, self.mb, self.origin, self.peer, self.slot, self.accumulate)
+
+
+ACTIONS = ("LOAD_X", "RECV_X", "F", "SEND_Y", "LOSS", "RECV_DY", "B", "SEND_DX", "W", "BC", "AR", "OPT")
+
+
 class slip_io(C.Structure):
     _fields_ = [("x_host", C.POINTER(C.c_void_p)), ("target_host", C.POINTER(C.c_void_p)),
                 ("loss_host", C.POINTER(C.c_float))]
@@ -77,6 +88,8 @@ SIGNATURES = {
     "slip_plan_schedule": (C.c_int, [C.POINTER(slip_cluster), C.POINTER(slip_costs), C.POINTER(slip_plan_opts),
                                      C.POINTER(slip_op), I64, C.POINTER(I64), C.POINTER(I64), C.POINTER(I64)]),
     "slip_plan_hash": (U64, [C.POINTER(slip_op), I64]),
+    "slip_rank_program": (C.c_int, [C.POINTER(slip_cluster), C.POINTER(slip_costs), C.POINTER(slip_plan_opts), I32,
+                                    C.POINTER(slip_action), I64, C.POINTER(I64), C.POINTER(I32)]),
     "slip_param_count": (C.c_int, [C.POINTER(slip_model), I32, C.POINTER(I64)]),
     "slip_stash_bytes": (C.c_int, [C.POINTER(slip_model), I32, I32, C.POINTER(SIZE)]),
     "slip_workspace_bytes": (C.c_int, [C.POINTER(slip_model), C.POINTER(SIZE)]),

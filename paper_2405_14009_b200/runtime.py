@@ -93,6 +93,20 @@ def plan_schedule(N, DP, m, live, costs: slip_costs, decoupled=True, staggered=T
     return PlanResult([ops[i].key() for i in range(n.value)], [mk[i] for i in range(horizon)], per.value, h)
 
 
+def rank_program(N, DP, m, live, costs: slip_costs, rank, decoupled=True, staggered=True, horizon=1):
+    """The executor's action list for `rank` (host logic only): list of
+    (kind, iter, mb, origin, peer, slot, accumulate) tuples, and slots needed."""
+    from ._binding import slip_action
+    cl = make_cluster(N, DP, m, live)
+    opts = slip_plan_opts(int(decoupled), int(staggered), int(horizon))
+    n, ns = C.c_int64(0), C.c_int32(0)
+    call("slip_rank_program", C.byref(cl), C.byref(costs), C.byref(opts), rank, None, 0, C.byref(n), C.byref(ns))
+    buf = (slip_action * max(1, n.value))()
+    call("slip_rank_program", C.byref(cl), C.byref(costs), C.byref(opts), rank, buf, n.value, C.byref(n),
+         C.byref(ns))
+    return [buf[i].key() for i in range(n.value)], ns.value
+
+
 def assign(N, DP, m, live):
     cl = make_cluster(N, DP, m, live)
     out = (C.c_int32 * (N * m * DP))()

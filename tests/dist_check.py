@@ -1,0 +1,125 @@
+"""Multi-GPU correctness of the executor (run under torchrun, one rank per GPU).
+
+    torchrun --nproc-per-node 2 tests/dist_check.py --dp 2 --pp 1
+    torchrun --nproc-per-node 4 tests/dist_check.py --dp 2 --pp 2
+
+For a fault-free run and for every recoverable failure set given by --failures
+(masked ranks at the listed (stage, pipeline) positions) it runs one training
+iteration of the plan (decoupled + staggered) on a small GPT-shaped stage and
+checks, on every live rank:
+  * per-micro-batch losses are bit-identical to the fault-free run (re-routing
+    changes no numbers);
+  * the all-reduced stage gradient equals the fault-free one within 1e-4
+    normwise (only the fp32 summation order of micro-batch contributions moves);
+  * after the AdamW step, all live peers of a stage hold bit-identical weights.
+Prints one JSON line per scenario on rank 0 and exits non-zero on failure."""
+import argparse
+import json
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+
+import torch  # noqa: E402
+import torch.distributed as dist  # noqa: E402
+
+import slipdata as sd  # noqa: E402
+from paper_2405_14009_b200 import runtime as rt  # noqa: E402
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--dp", type=int, default=2)
+    ap.add_argument("--pp", type=int, default=1)
+    ap.add_argument("--m", type=int, default=3)
+    ap.add_argument("--failures", default="auto")
+    a = ap.parse_args()
+    rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
+    local = int(os.environ.get("LOCAL_RANK", rank))
+    torch.cuda.set_device(local)
+    dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    DP, PP, m = a.dp, a.pp, a.m
+    assert DP * PP == world
+    cfg = sd.ModelCfg(hidden=256, heads=4, ffn=1024, seq=256, micro_batch=1, layers=2 * PP)
+    L = 2
+    me_i, me_k = rank % PP, rank // PP
+    if a.failures == "auto":
+        scenarios = [[(PP - 1, 1)], [(0, 0)]] + ([[(PP - 1, 1), (0, 0)]] if PP > 1 else [])
+    else:
+        scenarios = [[tuple(int(v) for v in f.split(",")) for f in s.split(";")] for s in a.failures.split("/")]
+    costs = rt.make_costs(t_f=3, t_b=3, t_w=2, t_comm=1, t_ar=1, t_opt=1)
+    stage = rt.Stage(cfg, L, n_slots=2 * m * DP)
+    comm = rt.Comm(rank, world)
+    ok = True
+
+    def run(live):
+        rt.init_master_(stage.master, cfg, L, cfg.layers, seed=100 + me_i)
+        rt.call("slip_weights_from_master", stage.ctx, rt._stream())
+        stage.adam_m.zero_()
+        stage.adam_v.zero_()
+        comm.setup(PP, DP, m, live)
+        losses = torch.zeros(DP * m, dtype=torch.float32).pin_memory()
+        g = torch.Generator().manual_seed(5)
+        xs = [torch.randn(cfg.tokens, cfg.hidden, generator=g).to(torch.bfloat16).pin_memory() for _ in range(DP * m)]
+        rs = [torch.randn(cfg.tokens, cfg.hidden, generator=g).to(torch.bfloat16).pin_memory() for _ in range(DP * m)]
+        io = rt.make_io(xs, rs, losses)
+        rep = rt.execute_schedule(stage, comm, PP, DP, m, live, costs, True, True, adam=(1e-3, 0.9, 0.95, 1e-8, 0.1),
+                                  iterations=1, io=io)
+        torch.cuda.synchronize()
+        return rep, stage.grad.clone(), stage.master.clone(), losses.clone()
+
+    live0 = [[1] * DP for _ in range(PP)]
+    rep0, g0, p0, l0 = run(live0)
+    # reference gradient of my stage from the fault-free run, shared by stage peers
+    if rank == 0:
+        print(json.dumps({"scenario": [], "ok": True, "period_ms": rep0.period_ms, "plan_hash": rep0.plan_hash}),
+              flush=True)
+    for failed in scenarios:
+        if any(k >= DP or i >= PP for (i, k) in failed):
+            continue
+        live = [[1] * DP for _ in range(PP)]
+        for (i, k) in failed:
+            live[i][k] = 0
+        if not rt.recoverable(PP, DP, live):
+            continue
+        rep, g1, p1, l1 = run(live)
+        me_live = live[me_i][me_k] == 1
+        res = {"failed": failed, "rank": rank}
+        if me_live:
+            gerr = ((g1 - g0).abs().max() / g0.abs().max()).item()
+            res["grad_relerr"] = gerr
+            ok &= gerr <= 1e-4
+            if me_i == PP - 1:
+                # losses of micro-batches whose last stage ran here; compare bitwise
+                ex = rt.assign(PP, DP, m, live)
+                for k in range(DP):
+                    for j in range(m):
+                        if ex[(PP - 1, j, k)] == me_k:
+                            ok &= bool(l1[k * m + j] == l0[k * m + j])
+                            res.setdefault("loss_equal", []).append(bool(l1[k * m + j] == l0[k * m + j]))
+        # peers of a stage hold identical weights: compare checksums across ranks
+        ck = torch.tensor([float(p1.double().sum().item()) if me_live else float("nan"), float(me_live)],
+                          dtype=torch.float64, device="cuda")
+        allck = [torch.zeros_like(ck) for _ in range(world)]
+        dist.all_gather(allck, ck)
+        for r2 in range(world):
+            if r2 % PP == me_i and allck[r2][1].item() == 1.0 and me_live:
+                same = allck[r2][0].item() == ck[0].item()
+                ok &= same
+                res.setdefault("peer_weights_equal", []).append(same)
+        flag = torch.tensor([1.0 if ok else 0.0], device="cuda")
+        dist.all_reduce(flag, op=dist.ReduceOp.MIN)
+        outs = [None] * world
+        dist.all_gather_object(outs, res)
+        if rank == 0:
+            print(json.dumps({"scenario": failed, "ok": flag.item() == 1.0, "ranks": outs,
+                              "period_ms": rep.period_ms, "fault_free_period_ms": rep0.period_ms}), flush=True)
+        ok = ok and flag.item() == 1.0
+    comm.close()
+    stage.close()
+    dist.destroy_process_group()
+    sys.exit(0 if ok else 1)
+
+
+if __name__ == "__main__":
+    main()

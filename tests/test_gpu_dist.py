@@ -1,0 +1,38 @@
+"""Multi-GPU executor checks (skipped unless >= 2 GPUs): launches
+tests/dist_check.py under torchrun (127.0.0.1 rendezvous)."""
+import os
+import subprocess
+import sys
+
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+HERE = os.path.dirname(os.path.abspath(__file__))
+
+
+def _run(n, dp, pp):
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr", "127.0.0.1", "--master-port", str(29500 + n + pp), os.path.join(HERE, "dist_check.py"),
+           "--dp", str(dp), "--pp", str(pp)]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stdout[-4000:] + r.stderr[-4000:]
+    return r.stdout
+
+
+@pytest.mark.skipif(torch.cuda.device_count() < 2, reason="needs 2 GPUs")
+def test_dp2_pp1_reroute():
+    out = _run(2, 2, 1)
+    assert '"ok": true' in out
+
+
+@pytest.mark.skipif(torch.cuda.device_count() < 2, reason="needs 2 GPUs")
+def test_dp1_pp2_pipeline():
+    out = _run(2, 1, 2)
+    assert '"ok": true' in out
+
+
+@pytest.mark.skipif(torch.cuda.device_count() < 4, reason="needs 4 GPUs")
+def test_dp2_pp2_reroute():
+    out = _run(4, 2, 2)
+    assert '"ok": true' in out
