@@ -28,12 +28,15 @@ constexpr int BK = 64;
 constexpr int NUM_THREADS = 256;
 constexpr int EPI_WARP0 = 4;
 
-template <int BN, bool A_MN, bool B_MN>
+template <int BN, bool A_MN, bool B_MN, bool PAIR = false>
 struct Cfg {
   static_assert(BN % 16 == 0 && BN >= 16 && BN <= 256, "UMMA N for M=128");
+  static_assert(!PAIR || BN == 256, "CTA-pair tiles are 256 x 256");
+  static constexpr int TILE_M = PAIR ? 2 * BM : BM;  // rows of the output tile (per CTA: BM)
+  static constexpr int B_ROWS = PAIR ? BN / 2 : BN;  // N extent of B held by each CTA
   static constexpr int A_BYTES = BM * BK * 2;
-  static constexpr int B_ATOMS = (BN + 63) / 64;
-  static constexpr int B_BYTES = B_MN ? B_ATOMS * 8192 : BN * 128;
+  static constexpr int B_ATOMS = (B_ROWS + 63) / 64;
+  static constexpr int B_BYTES = B_MN ? B_ATOMS * 8192 : B_ROWS * 128;
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
   static constexpr int STAGES = (196608 / STAGE_BYTES) > 8 ? 8 : (196608 / STAGE_BYTES);
   static constexpr int ACC_COLS = (BN + 31) / 32 * 32;
@@ -44,7 +47,7 @@ struct Cfg {
                                                          : 512;
   static constexpr int EPI_BYTES = 4 * 32 * 128;  // one 32x32 fp32 staging tile per epilogue warp
   static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + EPI_BYTES + 1024 + 1024;
-  static constexpr uint32_t IDESC = ptx::idesc_bf16_f32(BM, BN, A_MN, B_MN);
+  static constexpr uint32_t IDESC = ptx::idesc_bf16_f32(TILE_M, BN, A_MN, B_MN);
   static constexpr uint32_t A_KSTEP = A_MN ? 2048 : 32;  // bytes per UMMA_K = 16
   static constexpr uint32_t B_KSTEP = B_MN ? 2048 : 32;
   static constexpr uint32_t A_LBO = A_MN ? 8192 : 16;
@@ -66,15 +69,40 @@ struct KParams {
   __nv_bfloat16* aux;
   float alpha;
   int accumulate;
+  const GroupEntry* groups;  // grouped mode: problem table in device memory (nullptr otherwise)
+  int n_groups;
 };
 
 struct Tile {
   int zi, zo, m0, n0, kb0, kb1;
+  int g, M, N;  // problem (grouped mode) and its extent
 };
 
-template <int BN>
+template <int BN, int TM = BM>
 __device__ __forceinline__ Tile decode_tile(int t, const KParams& p) {
   Tile r;
+  if (p.groups) {
+    int lo = 0, hi = p.n_groups - 1;
+    while (lo < hi) {  // first problem whose tile range ends after t
+      const int mid = (lo + hi) >> 1;
+      if (p.groups[mid].tile_end <= t) lo = mid + 1;
+      else hi = mid;
+    }
+    const GroupEntry& ge = p.groups[lo];
+    const int q = t - ge.tile_begin;
+    r.g = lo;
+    r.M = ge.M;
+    r.N = ge.N;
+    r.zi = r.zo = 0;
+    r.m0 = (q % ge.mt) * TM;
+    r.n0 = (q / ge.mt) * BN;
+    r.kb0 = 0;
+    r.kb1 = ge.nkb;
+    return r;
+  }
+  r.g = -1;
+  r.M = p.M;
+  r.N = p.N;
   const int z = t / p.per_z;
   const int q = t - z * p.per_z;
   int mb, nb;
@@ -89,7 +117,7 @@ __device__ __forceinline__ Tile decode_tile(int t, const KParams& p) {
   }
   r.zi = z % p.zi_count;
   r.zo = z / p.zi_count;
-  r.m0 = mb * BM;
+  r.m0 = mb * TM;
   r.n0 = nb * BN;
   r.kb0 = 0;
   r.kb1 = p.nkb;
@@ -129,11 +157,11 @@ __device__ __forceinline__ uint4 pack8(const float (&f)[8]) {
   return u;
 }
 
-template <int BN, bool A_MN, bool B_MN>
+template <int BN, bool A_MN, bool B_MN, bool PAIR>
 __global__ void __launch_bounds__(NUM_THREADS, 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                    const __grid_constant__ CUtensorMap tmC, const KParams p) {
-  using C = Cfg<BN, A_MN, B_MN>;
+  using C = Cfg<BN, A_MN, B_MN, PAIR>;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* ring = smem;
@@ -147,26 +175,35 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
+  // CTA pair: rank 0 (leader) issues the MMAs for the 256-row tile; each CTA loads and
+  // drains its own 128 rows (A) and half of N (B).
+  const int cta = PAIR ? static_cast<int>(ptx::cluster_ctarank()) : 0;
+  const int t0 = PAIR ? static_cast<int>(blockIdx.x) / 2 : static_cast<int>(blockIdx.x);
+  const int tstep = PAIR ? static_cast<int>(gridDim.x) / 2 : static_cast<int>(gridDim.x);
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < C::STAGES; ++s) {
-      ptx::mbar_init(&full[s], 1);
+      ptx::mbar_init(&full[s], PAIR ? 2 : 1);
       ptx::mbar_init(&empty[s], 1);
     }
     for (int a = 0; a < 2; ++a) {
       ptx::mbar_init(&tfull[a], 1);
-      ptx::mbar_init(&tempty[a], 4);
+      ptx::mbar_init(&tempty[a], PAIR ? 8 : 4);
     }
     ptx::fence_mbar_init();
   }
-  if (warp == 0 && lane == 0) {
+  if (warp == 0 && lane == 0 && !p.groups) {
     ptx::prefetch_tmap(&tmA);
     ptx::prefetch_tmap(&tmB);
     if (p.mode >= EPI_F32_STORE) ptx::prefetch_tmap(&tmC);
   }
-  if (warp == 2) ptx::tmem_alloc<C::TMEM_COLS>(tmem_holder);
+  if (warp == 2) {
+    if (PAIR) ptx::tmem_alloc_pair<C::TMEM_COLS>(tmem_holder);
+    else ptx::tmem_alloc<C::TMEM_COLS>(tmem_holder);
+  }
   ptx::tc_fence_before();
-  __syncthreads();
+  if (PAIR) ptx::cluster_sync();
+  else __syncthreads();
   ptx::tc_fence_after();
   const uint32_t tmem_base = *tmem_holder;
 
@@ -175,25 +212,47 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       // ---------------------------------------------------------------- TMA producer
       int stage = 0;
       uint32_t phase = 0;
-      for (int t = blockIdx.x; t < p.total; t += gridDim.x) {
-        const Tile tl = decode_tile<BN>(t, p);
+      for (int t = t0; t < p.total; t += tstep) {
+        const Tile tl = decode_tile<BN, C::TILE_M>(t, p);
+        const CUtensorMap* mA = tl.g >= 0 ? &p.groups[tl.g].ta : &tmA;
+        const CUtensorMap* mB = tl.g >= 0 ? &p.groups[tl.g].tb : &tmB;
+        const int am0 = tl.m0 + cta * BM;          // this CTA's rows of A
+        const int bn0 = tl.n0 + cta * C::B_ROWS;   // this CTA's part of N
         for (int kb = tl.kb0; kb < tl.kb1; ++kb) {
           ptx::mbar_wait(&empty[stage], phase ^ 1);
           uint8_t* sa = ring + stage * C::STAGE_BYTES;
           uint8_t* sb = sa + C::A_BYTES;
-          ptx::mbar_arrive_expect_tx(&full[stage], C::STAGE_BYTES);
-          if (!A_MN) {
-            ptx::tma_load_4d(&tmA, sa, &full[stage], kb * BK, tl.m0, tl.zi, tl.zo);
-          } else {
-            ptx::tma_load_4d(&tmA, sa, &full[stage], tl.m0, kb * BK, tl.zi, tl.zo);
-            ptx::tma_load_4d(&tmA, sa + 8192, &full[stage], tl.m0 + 64, kb * BK, tl.zi, tl.zo);
-          }
-          if (!B_MN) {
-            ptx::tma_load_4d(&tmB, sb, &full[stage], kb * BK, tl.n0, tl.zi, tl.zo);
-          } else {
+          if (PAIR) {
+            if (cta == 0) ptx::mbar_arrive_expect_tx(&full[stage], 2 * C::STAGE_BYTES);
+            else ptx::mbar_arrive_leader(&full[stage]);
+            if (!A_MN) {
+              ptx::tma_load_4d_pair(mA, sa, &full[stage], kb * BK, am0, tl.zi, tl.zo);
+            } else {
+              ptx::tma_load_4d_pair(mA, sa, &full[stage], am0, kb * BK, tl.zi, tl.zo);
+              ptx::tma_load_4d_pair(mA, sa + 8192, &full[stage], am0 + 64, kb * BK, tl.zi, tl.zo);
+            }
+            if (!B_MN) {
+              ptx::tma_load_4d_pair(mB, sb, &full[stage], kb * BK, bn0, tl.zi, tl.zo);
+            } else {
 #pragma unroll
-            for (int a = 0; a < C::B_ATOMS; ++a)
-              ptx::tma_load_4d(&tmB, sb + a * 8192, &full[stage], tl.n0 + a * 64, kb * BK, tl.zi, tl.zo);
+              for (int a = 0; a < C::B_ATOMS; ++a)
+                ptx::tma_load_4d_pair(mB, sb + a * 8192, &full[stage], bn0 + a * 64, kb * BK, tl.zi, tl.zo);
+            }
+          } else {
+            ptx::mbar_arrive_expect_tx(&full[stage], C::STAGE_BYTES);
+            if (!A_MN) {
+              ptx::tma_load_4d(mA, sa, &full[stage], kb * BK, am0, tl.zi, tl.zo);
+            } else {
+              ptx::tma_load_4d(mA, sa, &full[stage], am0, kb * BK, tl.zi, tl.zo);
+              ptx::tma_load_4d(mA, sa + 8192, &full[stage], am0 + 64, kb * BK, tl.zi, tl.zo);
+            }
+            if (!B_MN) {
+              ptx::tma_load_4d(mB, sb, &full[stage], kb * BK, bn0, tl.zi, tl.zo);
+            } else {
+#pragma unroll
+              for (int a = 0; a < C::B_ATOMS; ++a)
+                ptx::tma_load_4d(mB, sb + a * 8192, &full[stage], bn0 + a * 64, kb * BK, tl.zi, tl.zo);
+            }
           }
           if (++stage == C::STAGES) {
             stage = 0;
@@ -203,14 +262,14 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       }
     }
   } else if (warp == 1) {
-    if (lane == 0) {
+    if (lane == 0 && cta == 0) {
       // ---------------------------------------------------------------- MMA issuer
       int stage = 0;
       uint32_t phase = 0;
       int acc = 0;
       uint32_t acc_phase = 0;
-      for (int t = blockIdx.x; t < p.total; t += gridDim.x) {
-        const Tile tl = decode_tile<BN>(t, p);
+      for (int t = t0; t < p.total; t += tstep) {
+        const Tile tl = decode_tile<BN, C::TILE_M>(t, p);
         ptx::mbar_wait(&tempty[acc], acc_phase ^ 1);
         ptx::tc_fence_after();
         const uint32_t d_tmem = tmem_base + acc * C::ACC_COLS;
@@ -223,15 +282,18 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           for (int k = 0; k < BK / 16; ++k) {
             const uint64_t ad = ptx::smem_desc_sw128(a_base + k * C::A_KSTEP, C::A_LBO, 1024);
             const uint64_t bd = ptx::smem_desc_sw128(b_base + k * C::B_KSTEP, C::B_LBO, 1024);
-            ptx::tc_mma_f16(d_tmem, ad, bd, C::IDESC, (kb > tl.kb0 || k > 0) ? 1u : 0u);
+            if (PAIR) ptx::tc_mma_f16_pair(d_tmem, ad, bd, C::IDESC, (kb > tl.kb0 || k > 0) ? 1u : 0u);
+            else ptx::tc_mma_f16(d_tmem, ad, bd, C::IDESC, (kb > tl.kb0 || k > 0) ? 1u : 0u);
           }
-          ptx::tc_commit(&empty[stage]);
+          if (PAIR) ptx::tc_commit_pair_mc(&empty[stage], 0x3);
+          else ptx::tc_commit(&empty[stage]);
           if (++stage == C::STAGES) {
             stage = 0;
             phase ^= 1;
           }
         }
-        ptx::tc_commit(&tfull[acc]);
+        if (PAIR) ptx::tc_commit_pair_mc(&tfull[acc], 0x3);
+        else ptx::tc_commit(&tfull[acc]);
         if (++acc == 2) {
           acc = 0;
           acc_phase ^= 1;
@@ -244,11 +306,12 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     float* buf = epi + ew * 32 * 32;
     int acc = 0;
     uint32_t acc_phase = 0;
-    for (int t = blockIdx.x; t < p.total; t += gridDim.x) {
-      const Tile tl = decode_tile<BN>(t, p);
+    for (int t = t0; t < p.total; t += tstep) {
+      const Tile tl = decode_tile<BN, C::TILE_M>(t, p);
+      const CUtensorMap* mC = tl.g >= 0 ? &p.groups[tl.g].tc : &tmC;
       ptx::mbar_wait(&tfull[acc], acc_phase);
       ptx::tc_fence_after();
-      const int row0 = tl.m0 + ew * 32;
+      const int row0 = tl.m0 + cta * BM + ew * 32;
       const int m = row0 + lane;
 #pragma unroll 1
       for (int ch = 0; ch < C::ACC_COLS / 32; ++ch) {
@@ -256,7 +319,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         ptx::tmem_ld_32x32b_x32(tmem_base + (static_cast<uint32_t>(ew * 32) << 16) + acc * C::ACC_COLS + ch * 32, r);
         ptx::tmem_ld_wait();
         const int n = tl.n0 + ch * 32;
-        if (n >= p.N || row0 >= p.M) continue;
+        if (n >= tl.N || row0 >= tl.M) continue;
         if (p.mode >= EPI_F32_STORE) {
           if (lane == 0) ptx::bulk_wait_read0();
           __syncwarp();
@@ -271,18 +334,18 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           __syncwarp();
           if (lane == 0) {
             if (p.mode == EPI_F32_ACC && p.accumulate)
-              ptx::tma_reduce_add_4d(&tmC, buf, n, row0, tl.zi, tl.zo);
+              ptx::tma_reduce_add_4d(mC, buf, n, row0, tl.zi, tl.zo);
             else
-              ptx::tma_store_4d(&tmC, buf, n, row0, tl.zi, tl.zo);
+              ptx::tma_store_4d(mC, buf, n, row0, tl.zi, tl.zo);
             ptx::bulk_commit();
           }
-        } else if (m < p.M) {
+        } else if (m < tl.M) {
           const int64_t off = tl.zo * p.c_zo + tl.zi * p.c_zi + static_cast<int64_t>(m) * p.ldc + n;
           __nv_bfloat16* cp = reinterpret_cast<__nv_bfloat16*>(p.c) + off;
 #pragma unroll
           for (int q = 0; q < 4; ++q) {
             const int nn = n + q * 8;
-            if (nn >= p.N) break;
+            if (nn >= tl.N) break;
             float x[8];
 #pragma unroll
             for (int e = 0; e < 8; ++e) x[e] = __uint_as_float(r[q * 8 + e]) * p.alpha;
@@ -314,7 +377,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       }
       ptx::tc_fence_before();
       __syncwarp();
-      if (lane == 0) ptx::mbar_arrive(&tempty[acc]);
+      if (lane == 0) {
+        if (PAIR) ptx::mbar_arrive_leader(&tempty[acc]);
+        else ptx::mbar_arrive(&tempty[acc]);
+      }
       if (++acc == 2) {
         acc = 0;
         acc_phase ^= 1;
@@ -322,10 +388,13 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     }
     if (lane == 0) ptx::bulk_wait0();
   }
-  __syncthreads();
+  ptx::tc_fence_before();
+  if (PAIR) ptx::cluster_sync();
+  else __syncthreads();
   if (warp == 2) {
     ptx::tc_fence_after();
-    ptx::tmem_dealloc<C::TMEM_COLS>(tmem_base);
+    if (PAIR) ptx::tmem_dealloc_pair<C::TMEM_COLS>(tmem_base);
+    else ptx::tmem_dealloc<C::TMEM_COLS>(tmem_base);
   }
 }
 
@@ -399,20 +468,59 @@ bool encode_operand(CUtensorMap* map, const Operand& o, int rows, int K, int zi,
                   64);
 }
 
-template <int BN, bool A_MN, bool B_MN>
-cudaError_t launch_t(const GemmDesc& d, cudaStream_t s) {
-  using C = Cfg<BN, A_MN, B_MN>;
+// Persistent launch: one CTA (or CTA pair, cluster 2x1x1) per SM, at most one per tile.
+template <int BN, bool A_MN, bool B_MN, bool PAIR>
+cudaError_t launch_kernel(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& tc, const KParams& p,
+                          cudaStream_t s) {
+  using C = Cfg<BN, A_MN, B_MN, PAIR>;
+  auto kern = gemm_tc_kernel<BN, A_MN, B_MN, PAIR>;
   static std::once_flag once;
   static cudaError_t attr_err = cudaSuccess;
-  std::call_once(once, [] {
-    attr_err = cudaFuncSetAttribute(gemm_tc_kernel<BN, A_MN, B_MN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    C::SMEM_BYTES);
+  std::call_once(once, [&] {
+    attr_err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM_BYTES);
   });
   if (attr_err != cudaSuccess) return attr_err;
+  if (p.total == 0) return cudaSuccess;
+  const int units = PAIR ? num_sms() / 2 : num_sms();
+  const int grid = (p.total < units ? p.total : units) * (PAIR ? 2 : 1);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(NUM_THREADS);
+  cfg.dynamicSmemBytes = C::SMEM_BYTES;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  if (PAIR) {
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = 2;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+  }
+  return cudaLaunchKernelEx(&cfg, kern, ta, tb, tc, p);
+}
+
+template <int BN, bool A_MN, bool B_MN, bool PAIR = false>
+cudaError_t launch_t(const GemmDesc& d, cudaStream_t s, const GroupEntry* groups = nullptr, int n_groups = 0,
+                     int group_tiles = 0) {
+  using C = Cfg<BN, A_MN, B_MN, PAIR>;
   CUtensorMap ta, tb, tc;
+  std::memset(&ta, 0, sizeof ta);
+  std::memset(&tb, 0, sizeof tb);
   std::memset(&tc, 0, sizeof tc);
+  if (groups) {
+    KParams p{};
+    p.zi_count = 1;
+    p.mode = d.mode;
+    p.alpha = d.alpha;
+    p.accumulate = d.accumulate;
+    p.groups = groups;
+    p.n_groups = n_groups;
+    p.total = group_tiles;
+    return launch_kernel<BN, A_MN, B_MN, PAIR>(ta, tb, tc, p, s);
+  }
   if (!encode_operand(&ta, d.a, d.M, d.K, d.zi_count, d.zo_count, BM)) return cudaErrorInvalidValue;
-  if (!encode_operand(&tb, d.b, d.N, d.K, d.zi_count, d.zo_count, BN)) return cudaErrorInvalidValue;
+  if (!encode_operand(&tb, d.b, d.N, d.K, d.zi_count, d.zo_count, C::B_ROWS)) return cudaErrorInvalidValue;
   if (d.mode >= EPI_F32_STORE) {
     if (!encode4d(&tc, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, d.c, d.N, d.M, d.zi_count, d.zo_count, d.ldc, d.c_zi,
                   d.c_zo, 32, 32))
@@ -423,7 +531,7 @@ cudaError_t launch_t(const GemmDesc& d, cudaStream_t s) {
   p.N = d.N;
   p.K = d.K;
   p.zi_count = d.zi_count;
-  p.mt = (d.M + BM - 1) / BM;
+  p.mt = (d.M + C::TILE_M - 1) / C::TILE_M;
   p.nt = (d.N + BN - 1) / BN;
   p.nkb = (d.K + BK - 1) / BK;
   p.causal = d.causal;
@@ -439,15 +547,19 @@ cudaError_t launch_t(const GemmDesc& d, cudaStream_t s) {
   p.aux = static_cast<__nv_bfloat16*>(d.aux);
   p.alpha = d.alpha;
   p.accumulate = d.accumulate;
-  if (p.total == 0) return cudaSuccess;
-  const int grid = p.total < num_sms() ? p.total : num_sms();
-  gemm_tc_kernel<BN, A_MN, B_MN><<<grid, NUM_THREADS, C::SMEM_BYTES, s>>>(ta, tb, tc, p);
-  return cudaGetLastError();
+  return launch_kernel<BN, A_MN, B_MN, PAIR>(ta, tb, tc, p, s);
 }
 
 template <int BN>
 cudaError_t launch_bn(const GemmDesc& d, cudaStream_t s) {
   const bool am = d.a.mn_major, bm = d.b.mn_major;
+  if constexpr (BN == 256) {
+    if (d.pair && d.causal == CAUSAL_NONE) {
+      if (!am && !bm) return launch_t<BN, false, false, true>(d, s);
+      if (!am && bm) return launch_t<BN, false, true, true>(d, s);
+      if (am && bm) return launch_t<BN, true, true, true>(d, s);
+    }
+  }
   if (!am && !bm) return launch_t<BN, false, false>(d, s);
   if (!am && bm) return launch_t<BN, false, true>(d, s);
   if (am && bm) return launch_t<BN, true, true>(d, s);
@@ -495,6 +607,48 @@ cudaError_t gemm_launch(const GemmDesc& d, cudaStream_t s) {
       g_msg = "gemm: unsupported BN (32, 64, 80, 128, 256)";
       return cudaErrorInvalidValue;
   }
+}
+
+cudaError_t gemm_group_encode(const GemmDesc* probs, int n, GroupEntry* out, int* total_tiles) {
+  g_msg.clear();
+  int tiles = 0;
+  for (int i = 0; i < n; ++i) {
+    const GemmDesc& d = probs[i];
+    if (d.bn != probs[0].bn || d.a.mn_major != probs[0].a.mn_major || d.b.mn_major != probs[0].b.mn_major ||
+        d.mode != probs[0].mode || d.mode < EPI_F32_STORE || d.zi_count != 1 || d.zo_count != 1 ||
+        d.causal != CAUSAL_NONE) {
+      g_msg = "gemm_group: problems must share BN, majorness and an fp32 epilogue, without batching";
+      return cudaErrorInvalidValue;
+    }
+    GroupEntry& g = out[i];
+    std::memset(&g, 0, sizeof g);
+    if (!encode_operand(&g.ta, d.a, d.M, d.K, 1, 1, BM)) return cudaErrorInvalidValue;
+    const uint32_t b_rows = (probs[0].pair && probs[0].bn == 256) ? 128u : static_cast<uint32_t>(d.bn);
+    if (!encode_operand(&g.tb, d.b, d.N, d.K, 1, 1, b_rows)) return cudaErrorInvalidValue;
+    if (!encode4d(&g.tc, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, d.c, d.N, d.M, 1, 1, d.ldc, 0, 0, 32, 32))
+      return cudaErrorInvalidValue;
+    const int tile_m = (probs[0].pair && probs[0].bn == 256) ? 2 * BM : BM;
+    g.M = d.M;
+    g.N = d.N;
+    g.mt = (d.M + tile_m - 1) / tile_m;
+    g.nkb = (d.K + BK - 1) / BK;
+    g.tile_begin = tiles;
+    tiles += g.mt * ((d.N + d.bn - 1) / d.bn);
+    g.tile_end = tiles;
+  }
+  *total_tiles = tiles;
+  return cudaSuccess;
+}
+
+cudaError_t gemm_group_launch(const GroupEntry* dev_table, int n, int total_tiles, const GemmDesc& proto,
+                              cudaStream_t s) {
+  g_msg.clear();
+  if (!proto.a.mn_major || !proto.b.mn_major || proto.bn != 256) {
+    g_msg = "gemm_group: instantiated for BN = 256 with MN-major A and B (the W GEMMs)";
+    return cudaErrorInvalidValue;
+  }
+  if (proto.pair) return launch_t<256, true, true, true>(proto, s, dev_table, n, total_tiles);
+  return launch_t<256, true, true>(proto, s, dev_table, n, total_tiles);
 }
 
 }  // namespace slip

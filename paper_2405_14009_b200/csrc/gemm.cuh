@@ -6,8 +6,10 @@
 // index, "MN-major" means m (or n) is.  A batch index z = zo * zi_count + zi selects
 // (zi, zo) offsets, which covers per-(batch, head) attention views of the QKV buffer.
 #pragma once
-#include <cstdint>
+#include <cuda.h>
 #include <cuda_runtime.h>
+
+#include <cstdint>
 
 namespace slip {
 
@@ -49,11 +51,24 @@ struct GemmDesc {
   void* aux = nullptr;            // bf16, indexed like C
   float alpha = 1.0f;
   int accumulate = 0;
+  bool pair = true;  // bn == 256, no causal mode: use CTA-pair (cta_group::2) 256 x 256 tiles
 };
 
 // Enqueue on `s`.  Returns cudaSuccess or the launch / encode error; shape errors
 // return cudaErrorInvalidValue with a message retrievable by gemm_last_message().
 cudaError_t gemm_launch(const GemmDesc& d, cudaStream_t s);
+
+// Grouped persistent launch: many independent problems with the same BN, operand
+// majorness and epilogue mode (the W GEMMs of a whole stage) in ONE launch, tiles of
+// all problems dealt round-robin to min(#tiles, #SMs) CTAs.  The tensor maps live in a
+// device-memory table (encoded once per slot at bind time).
+struct alignas(128) GroupEntry {
+  CUtensorMap ta, tb, tc;
+  int M, N, mt, nkb, tile_begin, tile_end;
+};
+cudaError_t gemm_group_encode(const GemmDesc* probs, int n, GroupEntry* host_out, int* total_tiles);
+cudaError_t gemm_group_launch(const GroupEntry* dev_table, int n, int total_tiles, const GemmDesc& proto,
+                              cudaStream_t s);
 const char* gemm_last_message();
 int num_sms();
 

@@ -1,9 +1,11 @@
 // kernels.cu — HBM-bound kernels of the stage step: LayerNorm fwd/bwd, causal softmax
 // fwd/bwd, deterministic column reductions (bias / gamma / beta gradients), MSE head,
 // fused AdamW, RNE weight refresh and the counter-based input generator.
-// Every kernel reads/writes with 16-byte vectors along the contiguous dimension and
-// reduces with warp shuffles; column reductions go through fixed-order partials so
-// results are bitwise reproducible run to run.
+//
+// Design rules (B200): 16-byte vectors along the contiguous dimension; one thread block
+// per row for the row kernels (high occupancy, short per-thread register arrays);
+// column reductions write fixed-order partials and the LAST block of each column strip
+// (atomic ticket) sums them in chunk order — deterministic, and one launch per reduction.
 #include <cmath>
 
 #include "kernels.cuh"
@@ -21,6 +23,39 @@ __device__ __forceinline__ float warp_max(float v) {
   for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
   return v;
 }
+// Block-wide sum of two values (blockDim.x multiple of 32, <= 1024); result broadcast.
+__device__ __forceinline__ float2 block_sum2(float a, float b, float2* red) {
+  a = warp_sum(a);
+  b = warp_sum(b);
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31, nw = blockDim.x >> 5;
+  if (l == 0) red[w] = make_float2(a, b);
+  __syncthreads();
+  if (w == 0) {
+    float2 v = l < nw ? red[l] : make_float2(0.f, 0.f);
+    v.x = warp_sum(v.x);
+    v.y = warp_sum(v.y);
+    if (l == 0) red[32] = v;
+  }
+  __syncthreads();
+  const float2 r = red[32];
+  __syncthreads();  // red reusable by the caller
+  return r;
+}
+__device__ __forceinline__ float block_max(float a, float2* red) {
+  a = warp_max(a);
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31, nw = blockDim.x >> 5;
+  if (l == 0) red[w].x = a;
+  __syncthreads();
+  if (w == 0) {
+    float v = l < nw ? red[l].x : -INFINITY;
+    v = warp_max(v);
+    if (l == 0) red[32].x = v;
+  }
+  __syncthreads();
+  const float r = red[32].x;
+  __syncthreads();
+  return r;
+}
 __device__ __forceinline__ void unpack8(const uint4& u, float (&f)[8]) {
   const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&u);
 #pragma unroll
@@ -37,34 +72,42 @@ __device__ __forceinline__ uint4 pack8(const float (&f)[8]) {
   for (int i = 0; i < 4; ++i) h[i] = __floats2bfloat162_rn(f[2 * i], f[2 * i + 1]);
   return u;
 }
+__device__ __forceinline__ uint2 pack4(float a, float b, float c, float d) {
+  __nv_bfloat162 x = __floats2bfloat162_rn(a, b);
+  __nv_bfloat162 y = __floats2bfloat162_rn(c, d);
+  uint2 u;
+  u.x = *reinterpret_cast<uint32_t*>(&x);
+  u.y = *reinterpret_cast<uint32_t*>(&y);
+  return u;
+}
 
 // ------------------------------------------------------------------ LayerNorm fwd
-template <int MAXI>
-__global__ void __launch_bounds__(128) ln_fwd_kernel(const bf16* __restrict__ x, const bf16* __restrict__ gamma,
+// One block per row; thread i owns 16-byte vectors i, i + blockDim, ... (VPT of them).
+template <int VPT>
+__global__ void __launch_bounds__(512) ln_fwd_kernel(const bf16* __restrict__ x, const bf16* __restrict__ gamma,
                                                      const bf16* __restrict__ beta, bf16* __restrict__ y,
-                                                     float* __restrict__ mean, float* __restrict__ rstd, int T, int h,
+                                                     float* __restrict__ mean, float* __restrict__ rstd, int h,
                                                      float eps) {
-  const int row = blockIdx.x * 4 + (threadIdx.x >> 5);
-  const int lane = threadIdx.x & 31;
-  if (row >= T) return;
+  __shared__ float2 red[33];
+  const int row = blockIdx.x;
   const int nv = h >> 3;
   const uint4* xr = reinterpret_cast<const uint4*>(x + static_cast<size_t>(row) * h);
-  float v[MAXI][8];
+  float v[VPT][8];
   float sum = 0.f;
 #pragma unroll
-  for (int i = 0; i < MAXI; ++i) {
-    const int idx = lane + 32 * i;
+  for (int i = 0; i < VPT; ++i) {
+    const int idx = threadIdx.x + i * blockDim.x;
     if (idx < nv) {
       unpack8(xr[idx], v[i]);
 #pragma unroll
       for (int e = 0; e < 8; ++e) sum += v[i][e];
     }
   }
-  const float mu = warp_sum(sum) / h;
+  const float mu = block_sum2(sum, 0.f, red).x / h;
   float sq = 0.f;
 #pragma unroll
-  for (int i = 0; i < MAXI; ++i) {
-    if (lane + 32 * i < nv) {
+  for (int i = 0; i < VPT; ++i) {
+    if (threadIdx.x + i * blockDim.x < nv) {
 #pragma unroll
       for (int e = 0; e < 8; ++e) {
         const float d = v[i][e] - mu;
@@ -72,11 +115,11 @@ __global__ void __launch_bounds__(128) ln_fwd_kernel(const bf16* __restrict__ x,
       }
     }
   }
-  const float rs = rsqrtf(warp_sum(sq) / h + eps);
+  const float rs = rsqrtf(block_sum2(sq, 0.f, red).x / h + eps);
   uint4* yr = reinterpret_cast<uint4*>(y + static_cast<size_t>(row) * h);
 #pragma unroll
-  for (int i = 0; i < MAXI; ++i) {
-    const int idx = lane + 32 * i;
+  for (int i = 0; i < VPT; ++i) {
+    const int idx = threadIdx.x + i * blockDim.x;
     if (idx < nv) {
       float g[8], b[8], o[8];
       unpack8(reinterpret_cast<const uint4*>(gamma)[idx], g);
@@ -86,32 +129,30 @@ __global__ void __launch_bounds__(128) ln_fwd_kernel(const bf16* __restrict__ x,
       yr[idx] = pack8(o);
     }
   }
-  if (lane == 0) {
+  if (threadIdx.x == 0) {
     mean[row] = mu;
     rstd[row] = rs;
   }
 }
 
 // ------------------------------------------------------------------ LayerNorm bwd (rows)
-template <int MAXI>
-__global__ void __launch_bounds__(128) ln_bwd_rows_kernel(const bf16* __restrict__ dy, const bf16* __restrict__ x,
+template <int VPT>
+__global__ void __launch_bounds__(512) ln_bwd_rows_kernel(const bf16* __restrict__ dy, const bf16* x,
                                                           const float* __restrict__ mean,
                                                           const float* __restrict__ rstd,
                                                           const bf16* __restrict__ gamma,
-                                                          const bf16* __restrict__ resid, bf16* __restrict__ dx,
-                                                          int T, int h) {
-  const int row = blockIdx.x * 4 + (threadIdx.x >> 5);
-  const int lane = threadIdx.x & 31;
-  if (row >= T) return;
+                                                          const bf16* __restrict__ resid, bf16* dx, int h) {
+  __shared__ float2 red[33];
+  const int row = blockIdx.x;
   const int nv = h >> 3;
   const float mu = mean[row], rs = rstd[row];
   const uint4* xr = reinterpret_cast<const uint4*>(x + static_cast<size_t>(row) * h);
   const uint4* dyr = reinterpret_cast<const uint4*>(dy + static_cast<size_t>(row) * h);
-  float g[MAXI][8], xh[MAXI][8];
+  float g[VPT][8], xh[VPT][8];
   float s1 = 0.f, s2 = 0.f;
 #pragma unroll
-  for (int i = 0; i < MAXI; ++i) {
-    const int idx = lane + 32 * i;
+  for (int i = 0; i < VPT; ++i) {
+    const int idx = threadIdx.x + i * blockDim.x;
     if (idx < nv) {
       float xv[8], dv[8], gm[8];
       unpack8(xr[idx], xv);
@@ -126,13 +167,13 @@ __global__ void __launch_bounds__(128) ln_bwd_rows_kernel(const bf16* __restrict
       }
     }
   }
-  const float mg = warp_sum(s1) / h;
-  const float mgx = warp_sum(s2) / h;
+  const float2 s = block_sum2(s1, s2, red);  // every x read completes before any dx write below
+  const float mg = s.x / h, mgx = s.y / h;
   uint4* dxr = reinterpret_cast<uint4*>(dx + static_cast<size_t>(row) * h);
   const uint4* rr = resid ? reinterpret_cast<const uint4*>(resid + static_cast<size_t>(row) * h) : nullptr;
 #pragma unroll
-  for (int i = 0; i < MAXI; ++i) {
-    const int idx = lane + 32 * i;
+  for (int i = 0; i < VPT; ++i) {
+    const int idx = threadIdx.x + i * blockDim.x;
     if (idx < nv) {
       float o[8], rv[8];
       if (rr) {
@@ -150,14 +191,18 @@ __global__ void __launch_bounds__(128) ln_bwd_rows_kernel(const bf16* __restrict
 
 // ------------------------------------------------------------------ column reductions
 // grid (ceil(N/256), kRedChunks), block 256 = 32 column-vectors x 8 row groups.
-// MODE 0: part0 = sum a.  MODE 1 (LayerNorm): part0 = sum dy*xhat, part1 = sum dy.
+// MODE 0: out0 (+)= sum_t a.   MODE 1 (LayerNorm): out0 (+)= sum dy*xhat, out1 (+)= sum dy.
+// Each block writes its chunk's partials; the last block of a column strip (atomic
+// ticket) sums the kRedChunks partials in chunk order and resets the ticket.
 template <int MODE>
 __global__ void __launch_bounds__(256) colred_kernel(const bf16* __restrict__ a, int64_t ld, const bf16* __restrict__ x,
                                                      const float* __restrict__ mean, const float* __restrict__ rstd,
-                                                     int T, int N, float* __restrict__ part0,
-                                                     float* __restrict__ part1) {
-  __shared__ float red0[8][256];
-  __shared__ float red1[MODE == 1 ? 8 : 1][256];
+                                                     int T, int N, float* part, float* __restrict__ out0,
+                                                     float* __restrict__ out1, int accumulate,
+                                                     unsigned* __restrict__ tickets) {
+  __shared__ float red0[8][257];
+  __shared__ float red1[MODE == 1 ? 8 : 1][257];
+  __shared__ bool last;
   const int cv = threadIdx.x & 31;
   const int rg = threadIdx.x >> 5;
   const int col = (blockIdx.x * 32 + cv) * 8;
@@ -193,8 +238,9 @@ __global__ void __launch_bounds__(256) colred_kernel(const bf16* __restrict__ a,
     if (MODE == 1) red1[rg][cv * 8 + e] = acc1[e];
   }
   __syncthreads();
-  const int c = threadIdx.x;  // 256 columns of this block
+  const int c = threadIdx.x;  // 256 columns of this strip
   const int gcol = blockIdx.x * 256 + c;
+  float* part1 = part + static_cast<size_t>(kRedChunks) * N;
   if (gcol < N) {
     float s0 = 0.f, s1 = 0.f;
 #pragma unroll
@@ -202,37 +248,46 @@ __global__ void __launch_bounds__(256) colred_kernel(const bf16* __restrict__ a,
       s0 += red0[g][c];
       if (MODE == 1) s1 += red1[g][c];
     }
-    part0[static_cast<size_t>(chunk) * N + gcol] = s0;
+    part[static_cast<size_t>(chunk) * N + gcol] = s0;
     if (MODE == 1) part1[static_cast<size_t>(chunk) * N + gcol] = s1;
   }
-}
-
-__global__ void colsum_finalize_kernel(const float* __restrict__ part, int N, float* __restrict__ out, int accumulate) {
-  const int n = blockIdx.x * blockDim.x + threadIdx.x;
-  if (n >= N) return;
-  float s = 0.f;
-  for (int c = 0; c < kRedChunks; ++c) s += part[static_cast<size_t>(c) * N + n];
-  out[n] = accumulate ? out[n] + s : s;
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) last = atomicAdd(&tickets[blockIdx.x], 1u) == static_cast<unsigned>(kRedChunks - 1);
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  if (gcol < N) {
+    float s0 = 0.f, s1 = 0.f;
+    for (int k = 0; k < kRedChunks; ++k) {
+      s0 += __ldcg(part + static_cast<size_t>(k) * N + gcol);
+      if (MODE == 1) s1 += __ldcg(part1 + static_cast<size_t>(k) * N + gcol);
+    }
+    out0[gcol] = accumulate ? out0[gcol] + s0 : s0;
+    if (MODE == 1) out1[gcol] = accumulate ? out1[gcol] + s1 : s1;
+  }
+  if (threadIdx.x == 0) tickets[blockIdx.x] = 0u;
 }
 
 // ------------------------------------------------------------------ causal softmax
-template <int MAXI>
-__global__ void __launch_bounds__(256) softmax_fwd_kernel(const float* __restrict__ S, bf16* __restrict__ P,
-                                                          int rows, int s) {
-  const int r = blockIdx.x * 8 + (threadIdx.x >> 5);
-  const int lane = threadIdx.x & 31;
-  if (r >= rows) return;
+// One block (128 threads) per row; thread i owns float4 columns 4i + 512j.  Row t uses
+// columns 0..t; the bf16 output is written up to E = ceil128(t+1) (zeros past t) so the
+// causal-tile GEMMs that consume it never read unwritten memory.
+template <int VPT>
+__global__ void __launch_bounds__(128) softmax_fwd_kernel(const float* __restrict__ S, bf16* __restrict__ P, int s) {
+  __shared__ float2 red[33];
+  const int r = blockIdx.x;
   const int t = r % s;
   const int E = min(s, ((t + 1 + 127) / 128) * 128);
   const float* sr = S + static_cast<size_t>(r) * s;
   const float L2E = 1.4426950408889634f;
-  float v[MAXI][4];
+  float v[VPT][4];
   float mx = -INFINITY;
 #pragma unroll
-  for (int i = 0; i < MAXI; ++i) {
-    const int c = 4 * lane + 128 * i;
+  for (int i = 0; i < VPT; ++i) {
+    const int c = 4 * threadIdx.x + 512 * i;
     if (c < E) {
-      const float4 q = *reinterpret_cast<const float4*>(sr + c);
+      const float4 q = __ldcs(reinterpret_cast<const float4*>(sr + c));
       v[i][0] = (c + 0 <= t) ? q.x : -INFINITY;
       v[i][1] = (c + 1 <= t) ? q.y : -INFINITY;
       v[i][2] = (c + 2 <= t) ? q.z : -INFINITY;
@@ -241,11 +296,11 @@ __global__ void __launch_bounds__(256) softmax_fwd_kernel(const float* __restric
       for (int e = 0; e < 4; ++e) mx = fmaxf(mx, v[i][e]);
     }
   }
-  mx = warp_max(mx);
+  mx = block_max(mx, red);
   float sum = 0.f;
 #pragma unroll
-  for (int i = 0; i < MAXI; ++i) {
-    if (4 * lane + 128 * i < E) {
+  for (int i = 0; i < VPT; ++i) {
+    if (4 * static_cast<int>(threadIdx.x) + 512 * i < E) {
 #pragma unroll
       for (int e = 0; e < 4; ++e) {
         v[i][e] = exp2f((v[i][e] - mx) * L2E);
@@ -253,39 +308,31 @@ __global__ void __launch_bounds__(256) softmax_fwd_kernel(const float* __restric
       }
     }
   }
-  const float inv = 1.0f / warp_sum(sum);
+  const float inv = 1.0f / block_sum2(sum, 0.f, red).x;
   bf16* pr = P + static_cast<size_t>(r) * s;
 #pragma unroll
-  for (int i = 0; i < MAXI; ++i) {
-    const int c = 4 * lane + 128 * i;
-    if (c < E) {
-      __nv_bfloat162 a = __floats2bfloat162_rn(v[i][0] * inv, v[i][1] * inv);
-      __nv_bfloat162 b = __floats2bfloat162_rn(v[i][2] * inv, v[i][3] * inv);
-      uint2 u;
-      u.x = *reinterpret_cast<uint32_t*>(&a);
-      u.y = *reinterpret_cast<uint32_t*>(&b);
-      *reinterpret_cast<uint2*>(pr + c) = u;
-    }
+  for (int i = 0; i < VPT; ++i) {
+    const int c = 4 * threadIdx.x + 512 * i;
+    if (c < E) *reinterpret_cast<uint2*>(pr + c) = pack4(v[i][0] * inv, v[i][1] * inv, v[i][2] * inv, v[i][3] * inv);
   }
 }
 
-template <int MAXI>
-__global__ void __launch_bounds__(256) softmax_bwd_kernel(const float* __restrict__ dP, const bf16* __restrict__ P,
-                                                          bf16* __restrict__ dS, int rows, int s, float scale) {
-  const int r = blockIdx.x * 8 + (threadIdx.x >> 5);
-  const int lane = threadIdx.x & 31;
-  if (r >= rows) return;
+template <int VPT>
+__global__ void __launch_bounds__(128) softmax_bwd_kernel(const float* __restrict__ dP, const bf16* __restrict__ P,
+                                                          bf16* __restrict__ dS, int s, float scale) {
+  __shared__ float2 red[33];
+  const int r = blockIdx.x;
   const int t = r % s;
   const int E = min(s, ((t + 1 + 127) / 128) * 128);
   const float* dr = dP + static_cast<size_t>(r) * s;
   const bf16* pr = P + static_cast<size_t>(r) * s;
-  float pv[MAXI][4], dv[MAXI][4];
+  float pv[VPT][4], dv[VPT][4];
   float dot = 0.f;
 #pragma unroll
-  for (int i = 0; i < MAXI; ++i) {
-    const int c = 4 * lane + 128 * i;
+  for (int i = 0; i < VPT; ++i) {
+    const int c = 4 * threadIdx.x + 512 * i;
     if (c < E) {
-      const float4 q = *reinterpret_cast<const float4*>(dr + c);
+      const float4 q = __ldcs(reinterpret_cast<const float4*>(dr + c));
       const uint2 u = *reinterpret_cast<const uint2*>(pr + c);
       const float2 a = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&u.x));
       const float2 b = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&u.y));
@@ -301,22 +348,15 @@ __global__ void __launch_bounds__(256) softmax_bwd_kernel(const float* __restric
       for (int e = 0; e < 4; ++e) dot += pv[i][e] * dv[i][e];
     }
   }
-  dot = warp_sum(dot);
+  dot = block_sum2(dot, 0.f, red).x;
   bf16* sr = dS + static_cast<size_t>(r) * s;
 #pragma unroll
-  for (int i = 0; i < MAXI; ++i) {
-    const int c = 4 * lane + 128 * i;
-    if (c < E) {
-      float o[4];
-#pragma unroll
-      for (int e = 0; e < 4; ++e) o[e] = scale * pv[i][e] * (dv[i][e] - dot);
-      __nv_bfloat162 a = __floats2bfloat162_rn(o[0], o[1]);
-      __nv_bfloat162 b = __floats2bfloat162_rn(o[2], o[3]);
-      uint2 u;
-      u.x = *reinterpret_cast<uint32_t*>(&a);
-      u.y = *reinterpret_cast<uint32_t*>(&b);
-      *reinterpret_cast<uint2*>(sr + c) = u;
-    }
+  for (int i = 0; i < VPT; ++i) {
+    const int c = 4 * threadIdx.x + 512 * i;
+    if (c < E)
+      *reinterpret_cast<uint2*>(sr + c) =
+          pack4(scale * pv[i][0] * (dv[i][0] - dot), scale * pv[i][1] * (dv[i][1] - dot),
+                scale * pv[i][2] * (dv[i][2] - dot), scale * pv[i][3] * (dv[i][3] - dot));
   }
 }
 
@@ -376,12 +416,11 @@ __global__ void __launch_bounds__(256) adamw_kernel(float* __restrict__ p, float
     float4 pp = reinterpret_cast<float4*>(p)[i];
     float4 mm = reinterpret_cast<float4*>(m)[i];
     float4 vv = reinterpret_cast<float4*>(v)[i];
-    const float4 gg = reinterpret_cast<const float4*>(g)[i];
+    const float4 gg = __ldcs(reinterpret_cast<const float4*>(g) + i);
     float* pa = &pp.x;
     float* ma = &mm.x;
     float* va = &vv.x;
     const float* ga = &gg.x;
-    float wo[4];
 #pragma unroll
     for (int e = 0; e < 4; ++e) {
       bad |= !isfinite(ga[e]);
@@ -391,17 +430,11 @@ __global__ void __launch_bounds__(256) adamw_kernel(float* __restrict__ p, float
       const float mh = ma[e] * inv_bc1;
       const float vh = va[e] * inv_bc2;
       pa[e] = pa[e] - lr * wdl * pa[e] - lr * mh / (sqrtf(vh) + eps);
-      wo[e] = pa[e];
     }
     reinterpret_cast<float4*>(p)[i] = pp;
     reinterpret_cast<float4*>(m)[i] = mm;
     reinterpret_cast<float4*>(v)[i] = vv;
-    __nv_bfloat162 x = __floats2bfloat162_rn(wo[0], wo[1]);
-    __nv_bfloat162 y = __floats2bfloat162_rn(wo[2], wo[3]);
-    uint2 u;
-    u.x = *reinterpret_cast<uint32_t*>(&x);
-    u.y = *reinterpret_cast<uint32_t*>(&y);
-    reinterpret_cast<uint2*>(w)[i] = u;
+    reinterpret_cast<uint2*>(w)[i] = pack4(pa[0], pa[1], pa[2], pa[3]);
   }
   if (nonfinite && __any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicOr(nonfinite, 1);
 }
@@ -409,12 +442,7 @@ __global__ void __launch_bounds__(256) adamw_kernel(float* __restrict__ p, float
 __global__ void f32_to_bf16_kernel(const float* __restrict__ src, bf16* __restrict__ dst, int64_t n4) {
   for (int64_t i = blockIdx.x * 256LL + threadIdx.x; i < n4; i += static_cast<int64_t>(gridDim.x) * 256) {
     const float4 a = reinterpret_cast<const float4*>(src)[i];
-    __nv_bfloat162 x = __floats2bfloat162_rn(a.x, a.y);
-    __nv_bfloat162 y = __floats2bfloat162_rn(a.z, a.w);
-    uint2 u;
-    u.x = *reinterpret_cast<uint32_t*>(&x);
-    u.y = *reinterpret_cast<uint32_t*>(&y);
-    reinterpret_cast<uint2*>(dst)[i] = u;
+    reinterpret_cast<uint2*>(dst)[i] = pack4(a.x, a.y, a.z, a.w);
   }
 }
 
@@ -458,68 +486,70 @@ int grid_for(int64_t work, int per_block = 256) {
   return g < 1 ? 1 : static_cast<int>(g);
 }
 
+// threads per row for the LayerNorm kernels and vectors per thread
+void ln_shape(int h, int* threads, int* vpt) {
+  const int nv = h / 8;
+  int t = nv <= 512 ? nv : 512;
+  t = (t + 31) / 32 * 32;
+  *threads = t;
+  *vpt = (nv + t - 1) / t;
+}
+
 }  // namespace
 
 cudaError_t ln_fwd(const bf16* x, const bf16* gamma, const bf16* beta, bf16* y, float* mean, float* rstd, int T, int h,
                    float eps, cudaStream_t s) {
-  if (h % 8 || h > 4096) return cudaErrorInvalidValue;
-  const int nv = h / 8, blocks = (T + 3) / 4;
-  if (nv <= 32) ln_fwd_kernel<1><<<blocks, 128, 0, s>>>(x, gamma, beta, y, mean, rstd, T, h, eps);
-  else if (nv <= 64) ln_fwd_kernel<2><<<blocks, 128, 0, s>>>(x, gamma, beta, y, mean, rstd, T, h, eps);
-  else if (nv <= 128) ln_fwd_kernel<4><<<blocks, 128, 0, s>>>(x, gamma, beta, y, mean, rstd, T, h, eps);
-  else if (nv <= 256) ln_fwd_kernel<8><<<blocks, 128, 0, s>>>(x, gamma, beta, y, mean, rstd, T, h, eps);
-  else ln_fwd_kernel<16><<<blocks, 128, 0, s>>>(x, gamma, beta, y, mean, rstd, T, h, eps);
+  if (h % 8 || h > 8192) return cudaErrorInvalidValue;
+  int nt, vpt;
+  ln_shape(h, &nt, &vpt);
+  if (vpt == 1) ln_fwd_kernel<1><<<T, nt, 0, s>>>(x, gamma, beta, y, mean, rstd, h, eps);
+  else ln_fwd_kernel<2><<<T, nt, 0, s>>>(x, gamma, beta, y, mean, rstd, h, eps);
   return cudaGetLastError();
 }
 
 cudaError_t ln_bwd(const bf16* dy, const bf16* x, const float* mean, const float* rstd, const bf16* gamma,
-                   const bf16* resid, bf16* dx, float* part_dgamma, float* part_dbeta, float* part_dxsum, int T, int h,
-                   cudaStream_t s) {
-  if (h % 8 || h > 4096) return cudaErrorInvalidValue;
-  const int nv = h / 8, blocks = (T + 3) / 4;
-  // column partials first: dx may alias x (the executor writes dx over the consumed stage input)
+                   const bf16* resid, bf16* dx, float* dgamma, float* dbeta, float* dxsum, int accumulate, float* part,
+                   unsigned* tickets, int T, int h, cudaStream_t s) {
+  if (h % 8 || h > 8192) return cudaErrorInvalidValue;
+  // gamma/beta partials first: dx may alias x (the executor writes dx over the consumed input)
   dim3 grid((h + 255) / 256, kRedChunks);
-  colred_kernel<1><<<grid, 256, 0, s>>>(dy, h, x, mean, rstd, T, h, part_dgamma, part_dbeta);
+  colred_kernel<1><<<grid, 256, 0, s>>>(dy, h, x, mean, rstd, T, h, part, dgamma, dbeta, accumulate, tickets);
   if (dx) {
-    if (nv <= 32) ln_bwd_rows_kernel<1><<<blocks, 128, 0, s>>>(dy, x, mean, rstd, gamma, resid, dx, T, h);
-    else if (nv <= 64) ln_bwd_rows_kernel<2><<<blocks, 128, 0, s>>>(dy, x, mean, rstd, gamma, resid, dx, T, h);
-    else if (nv <= 128) ln_bwd_rows_kernel<4><<<blocks, 128, 0, s>>>(dy, x, mean, rstd, gamma, resid, dx, T, h);
-    else if (nv <= 256) ln_bwd_rows_kernel<8><<<blocks, 128, 0, s>>>(dy, x, mean, rstd, gamma, resid, dx, T, h);
-    else ln_bwd_rows_kernel<16><<<blocks, 128, 0, s>>>(dy, x, mean, rstd, gamma, resid, dx, T, h);
+    int nt, vpt;
+    ln_shape(h, &nt, &vpt);
+    if (vpt == 1) ln_bwd_rows_kernel<1><<<T, nt, 0, s>>>(dy, x, mean, rstd, gamma, resid, dx, h);
+    else ln_bwd_rows_kernel<2><<<T, nt, 0, s>>>(dy, x, mean, rstd, gamma, resid, dx, h);
+    if (dxsum)
+      colred_kernel<0><<<grid, 256, 0, s>>>(dx, h, nullptr, nullptr, nullptr, T, h, part, dxsum, nullptr, accumulate,
+                                            tickets);
   }
-  if (part_dxsum && dx) colred_kernel<0><<<grid, 256, 0, s>>>(dx, h, nullptr, nullptr, nullptr, T, h, part_dxsum, nullptr);
   return cudaGetLastError();
 }
 
-cudaError_t colsum_partial(const bf16* a, int T, int N, int64_t ld, float* part, cudaStream_t s) {
-  if (N % 8 || ld % 8) return cudaErrorInvalidValue;
+cudaError_t colsum(const bf16* a, int T, int N, int64_t ld, float* out, int accumulate, float* part,
+                   unsigned* tickets, cudaStream_t s) {
+  if (N % 8 || ld % 8 || (N + 255) / 256 > kTickets) return cudaErrorInvalidValue;
   dim3 grid((N + 255) / 256, kRedChunks);
-  colred_kernel<0><<<grid, 256, 0, s>>>(a, ld, nullptr, nullptr, nullptr, T, N, part, nullptr);
-  return cudaGetLastError();
-}
-
-cudaError_t colsum_finalize(const float* part, int N, float* out, int accumulate, cudaStream_t s) {
-  colsum_finalize_kernel<<<(N + 255) / 256, 256, 0, s>>>(part, N, out, accumulate);
+  colred_kernel<0><<<grid, 256, 0, s>>>(a, ld, nullptr, nullptr, nullptr, T, N, part, out, nullptr, accumulate,
+                                        tickets);
   return cudaGetLastError();
 }
 
 cudaError_t softmax_fwd(const float* S, bf16* P, int z, int s, cudaStream_t st) {
   if (s % 4 || s > 2048) return cudaErrorInvalidValue;
-  const int rows = z * s, blocks = (rows + 7) / 8, ni = (s + 127) / 128;
-  if (ni <= 1) softmax_fwd_kernel<1><<<blocks, 256, 0, st>>>(S, P, rows, s);
-  else if (ni <= 4) softmax_fwd_kernel<4><<<blocks, 256, 0, st>>>(S, P, rows, s);
-  else if (ni <= 8) softmax_fwd_kernel<8><<<blocks, 256, 0, st>>>(S, P, rows, s);
-  else softmax_fwd_kernel<16><<<blocks, 256, 0, st>>>(S, P, rows, s);
+  const int rows = z * s, vpt = (s + 511) / 512;
+  if (vpt == 1) softmax_fwd_kernel<1><<<rows, 128, 0, st>>>(S, P, s);
+  else if (vpt == 2) softmax_fwd_kernel<2><<<rows, 128, 0, st>>>(S, P, s);
+  else softmax_fwd_kernel<4><<<rows, 128, 0, st>>>(S, P, s);
   return cudaGetLastError();
 }
 
 cudaError_t softmax_bwd(const float* dP, const bf16* P, bf16* dS, int z, int s, float scale, cudaStream_t st) {
   if (s % 4 || s > 2048) return cudaErrorInvalidValue;
-  const int rows = z * s, blocks = (rows + 7) / 8, ni = (s + 127) / 128;
-  if (ni <= 1) softmax_bwd_kernel<1><<<blocks, 256, 0, st>>>(dP, P, dS, rows, s, scale);
-  else if (ni <= 4) softmax_bwd_kernel<4><<<blocks, 256, 0, st>>>(dP, P, dS, rows, s, scale);
-  else if (ni <= 8) softmax_bwd_kernel<8><<<blocks, 256, 0, st>>>(dP, P, dS, rows, s, scale);
-  else softmax_bwd_kernel<16><<<blocks, 256, 0, st>>>(dP, P, dS, rows, s, scale);
+  const int rows = z * s, vpt = (s + 511) / 512;
+  if (vpt == 1) softmax_bwd_kernel<1><<<rows, 128, 0, st>>>(dP, P, dS, s, scale);
+  else if (vpt == 2) softmax_bwd_kernel<2><<<rows, 128, 0, st>>>(dP, P, dS, s, scale);
+  else softmax_bwd_kernel<4><<<rows, 128, 0, st>>>(dP, P, dS, s, scale);
   return cudaGetLastError();
 }
 

@@ -1,5 +1,6 @@
 // kernels.cuh — memory-bound kernels of the stage step (coalesced, 16-byte vectorised,
-// warp-shuffle reductions; column reductions are two-stage and deterministic).
+// block-per-row with warp-shuffle reductions; column reductions are deterministic and
+// finish in one launch via a last-block ticket).
 #pragma once
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
@@ -11,23 +12,23 @@ namespace slip {
 using bf16 = __nv_bfloat16;
 
 constexpr int kRedChunks = 64;  // row chunks of the deterministic column reductions
+constexpr int kTickets = 256;   // column strips (256 columns each) a reduction may use
 
 // LayerNorm forward over rows of x [T, h]: y = xhat*gamma + beta; mean, rstd fp32 [T].
 cudaError_t ln_fwd(const bf16* x, const bf16* gamma, const bf16* beta, bf16* y, float* mean, float* rstd, int T,
                    int h, float eps, cudaStream_t s);
 
 // LayerNorm backward.  dx = resid + rstd*(g - mean_h(g) - xhat*mean_h(g*xhat)), g = dy*gamma
-// (dx may be null).  Column partials [kRedChunks, h] of dgamma = sum dy*xhat, dbeta = sum dy
-// and, if part_dxsum != null, of sum_t dx.
+// (dx may be null and may alias x).  dgamma (+)= sum_t dy*xhat, dbeta (+)= sum_t dy and,
+// if dxsum != null, dxsum (+)= sum_t dx.  part: 2*kRedChunks*h floats of scratch;
+// tickets: kTickets zero-initialised counters (left zeroed).
 cudaError_t ln_bwd(const bf16* dy, const bf16* x, const float* mean, const float* rstd, const bf16* gamma,
-                   const bf16* resid, bf16* dx, float* part_dgamma, float* part_dbeta, float* part_dxsum, int T, int h,
-                   cudaStream_t s);
+                   const bf16* resid, bf16* dx, float* dgamma, float* dbeta, float* dxsum, int accumulate, float* part,
+                   unsigned* tickets, int T, int h, cudaStream_t s);
 
-// Column-sum partials of a bf16 matrix [T, N] (row stride ld): part [kRedChunks, N].
-cudaError_t colsum_partial(const bf16* a, int T, int N, int64_t ld, float* part, cudaStream_t s);
-
-// out[n] (+)= sum_c part[c, n]  (fixed order over c).
-cudaError_t colsum_finalize(const float* part, int N, float* out, int accumulate, cudaStream_t s);
+// out[n] (+)= sum_t a[t, n] for a bf16 [T, N] matrix with row stride ld (bias gradients).
+cudaError_t colsum(const bf16* a, int T, int N, int64_t ld, float* out, int accumulate, float* part,
+                   unsigned* tickets, cudaStream_t s);
 
 // Causal softmax over rows of S [z, s, s] fp32 (row t uses columns 0..t):
 // P[z, t, u] = softmax for u <= t, 0 for t < u < ceil128(t+1).

@@ -105,6 +105,8 @@ void carve_slot(Carver& cv, const Dims& d, int L, SlotBufs* out) {
     ls.dx2 = cv.take<bf16>(Th);
     ls.dqkv = cv.take<bf16>(3 * Th);
   }
+  sb.wtab = cv.take<GroupEntry>(4 * static_cast<size_t>(L));
+  sb.wtab_tiles = 0;
   if (out) *out = sb;
 }
 
@@ -118,9 +120,8 @@ void carve_ws(Carver& cv, const Dims& d, Workspace* out) {
   w.dy2 = cv.take<bf16>(Th);
   w.dO = cv.take<bf16>(Th);
   w.dy1 = cv.take<bf16>(Th);
-  w.part0 = cv.take<float>(red);
-  w.part1 = cv.take<float>(red);
-  w.part2 = cv.take<float>(red);
+  w.part = cv.take<float>(2 * red);
+  w.tickets = cv.take<unsigned>(kTickets);
   w.loss_part = cv.take<float>(256);
   w.losses = cv.take<float>(1024);
   w.nonfinite = cv.take<int32_t>(64);
@@ -351,10 +352,9 @@ slip_status attention_bwd(slip_ctx* c, LayerStash& ls, cudaStream_t s) {
   return run_gemm(c, dk, s, "attn dK");
 }
 
-// colsum(a[T, N]) -> out (fp32, overwrite or accumulate)
+// colsum(a[T, N]) -> out (fp32, overwrite or accumulate), one launch
 slip_status bias_grad(slip_ctx* c, const bf16* a, int N, int64_t ld, float* out, int accumulate, cudaStream_t s) {
-  SLIP_TRY(kcheck(c, colsum_partial(a, c->dm.T, N, ld, c->ws.part0, s), "colsum_partial"));
-  return kcheck(c, colsum_finalize(c->ws.part0, N, out, accumulate, s), "colsum_finalize");
+  return kcheck(c, colsum(a, c->dm.T, N, ld, out, accumulate, c->ws.part, c->ws.tickets, s), "colsum");
 }
 
 slip_status slot_check(slip_ctx* c, int slot, int want) {
@@ -370,17 +370,50 @@ slip_status slot_check(slip_ctx* c, int slot, int want) {
   return SLIP_OK;
 }
 
-slip_status backward_weight_impl(slip_ctx* c, int slot, int accumulate, cudaStream_t s) {
+// The four W products of every layer of a slot: dW2 += dOut^T G, dW1 += dH^T Y2,
+// dWo += dX2^T O, dWqkv += dQKV^T Y1 (reading R9).
+std::vector<GemmDesc> w_problems(slip_ctx* c, int slot) {
   const Dims& D = c->dm;
   SlotBufs& sb = c->slots[slot];
+  std::vector<GemmDesc> v;
+  auto add = [&](const bf16* dY, const bf16* X, int N, int K, float* dW) {
+    GemmDesc d;
+    d.M = N;
+    d.N = K;
+    d.K = D.T;
+    d.bn = 256;
+    d.a = op(dY, N, true);
+    d.b = op(X, K, true);
+    d.mode = EPI_F32_ACC;
+    d.c = dW;
+    d.ldc = K;
+    v.push_back(d);
+  };
   for (int l = c->L - 1; l >= 0; --l) {
     LayerStash& ls = sb.layer[l];
     LayerG G = layer_g(c, l);
-    SLIP_TRY(linear_dw(c, ls.dout, ls.g, D.h, D.f, G.w2, accumulate, s));
-    SLIP_TRY(linear_dw(c, ls.dh, ls.y2, D.f, D.h, G.w1, accumulate, s));
-    SLIP_TRY(linear_dw(c, ls.dx2, ls.o, D.h, D.h, G.wo, accumulate, s));
-    SLIP_TRY(linear_dw(c, ls.dqkv, ls.y1, 3 * D.h, D.h, G.wqkv, accumulate, s));
+    add(ls.dout, ls.g, D.h, D.f, G.w2);
+    add(ls.dh, ls.y2, D.f, D.h, G.w1);
+    add(ls.dx2, ls.o, D.h, D.h, G.wo);
+    add(ls.dqkv, ls.y1, 3 * D.h, D.h, G.wqkv);
   }
+  return v;
+}
+
+// W as ONE persistent grouped launch over all 4L products of the slot (tables encoded at bind).
+slip_status backward_weight_impl(slip_ctx* c, int slot, int accumulate, cudaStream_t s) {
+  SlotBufs& sb = c->slots[slot];
+  GemmDesc proto;
+  proto.bn = 256;
+  proto.a.mn_major = proto.b.mn_major = true;
+  proto.mode = EPI_F32_ACC;
+  proto.accumulate = accumulate;
+  cudaError_t e = gemm_group_launch(sb.wtab, 4 * c->L, sb.wtab_tiles, proto, s);
+  if (e != cudaSuccess) {
+    set_error(std::string("W grouped launch: ") + cudaGetErrorString(e) + " " + gemm_last_message());
+    return SLIP_ECUDA;
+  }
+  c->launches += 1;
   return SLIP_OK;
 }
 
@@ -402,12 +435,9 @@ slip_status backward_input_impl(slip_ctx* c, int slot, const void* dy, void* dx,
     SLIP_TRY(linear_dx(c, ls.dh, Wt.w1, D.f, D.h, c->ws.dy2, EPI_BF16, nullptr, s));
     // LN2 backward + residual: dX2 = dOut + LN2'(dY2); dgamma2, dbeta2, dbo = colsum(dX2)
     SLIP_TRY(kcheck(c,
-                    ln_bwd(c->ws.dy2, ls.x2, ls.mean2, ls.rstd2, Wt.g2, ls.dout, ls.dx2, c->ws.part0, c->ws.part1,
-                           c->ws.part2, D.T, D.h, s),
+                    ln_bwd(c->ws.dy2, ls.x2, ls.mean2, ls.rstd2, Wt.g2, ls.dout, ls.dx2, G.g2, G.b2n, G.bo, accumulate,
+                           c->ws.part, c->ws.tickets, D.T, D.h, s),
                     "ln_bwd 2", 3));
-    SLIP_TRY(kcheck(c, colsum_finalize(c->ws.part0, D.h, G.g2, accumulate, s), "fin g2"));
-    SLIP_TRY(kcheck(c, colsum_finalize(c->ws.part1, D.h, G.b2n, accumulate, s), "fin b2n"));
-    SLIP_TRY(kcheck(c, colsum_finalize(c->ws.part2, D.h, G.bo, accumulate, s), "fin bo"));
     // dO = dX2 Wo
     SLIP_TRY(linear_dx(c, ls.dx2, Wt.wo, D.h, D.h, c->ws.dO, EPI_BF16, nullptr, s));
     SLIP_TRY(attention_bwd(c, ls, s));
@@ -416,22 +446,11 @@ slip_status backward_input_impl(slip_ctx* c, int slot, const void* dy, void* dx,
     SLIP_TRY(linear_dx(c, ls.dqkv, Wt.wqkv, 3 * D.h, D.h, c->ws.dy1, EPI_BF16, nullptr, s));
     // LN1 backward + residual: dX = dX2 + LN1'(dY1); db2 of the layer below = colsum(dX)
     bf16* dxl = l > 0 ? sb.layer[l - 1].dout : static_cast<bf16*>(dx);
-    float* dxsum = l > 0 ? c->ws.part2 : nullptr;
-    if (dxl) {
-      SLIP_TRY(kcheck(c,
-                      ln_bwd(c->ws.dy1, ls.xin, ls.mean1, ls.rstd1, Wt.g1, ls.dx2, dxl, c->ws.part0, c->ws.part1,
-                             dxsum, D.T, D.h, s),
-                      "ln_bwd 1", dxsum ? 3 : 2));
-    } else {
-      SLIP_TRY(kcheck(c,
-                      ln_bwd(c->ws.dy1, ls.xin, ls.mean1, ls.rstd1, Wt.g1, nullptr, nullptr, c->ws.part0,
-                             c->ws.part1, nullptr, D.T, D.h, s),
-                      "ln_bwd 1", 1));
-    }
-    SLIP_TRY(kcheck(c, colsum_finalize(c->ws.part0, D.h, G.g1, accumulate, s), "fin g1"));
-    SLIP_TRY(kcheck(c, colsum_finalize(c->ws.part1, D.h, G.b1n, accumulate, s), "fin b1n"));
-    if (l > 0)
-      SLIP_TRY(kcheck(c, colsum_finalize(c->ws.part2, D.h, layer_g(c, l - 1).b2, accumulate, s), "fin b2"));
+    float* dxsum = l > 0 ? layer_g(c, l - 1).b2 : nullptr;
+    SLIP_TRY(kcheck(c,
+                    ln_bwd(c->ws.dy1, ls.xin, ls.mean1, ls.rstd1, Wt.g1, ls.dx2, dxl, G.g1, G.b1n, dxl ? dxsum : nullptr,
+                           accumulate, c->ws.part, c->ws.tickets, D.T, D.h, s),
+                    "ln_bwd 1", dxl ? (dxsum ? 3 : 2) : 1));
   }
   return SLIP_OK;
 }
@@ -517,6 +536,21 @@ slip_status slip_stage_bind(slip_ctx* c, void* w_bf16, float* master, float* gra
   }
   Carver wv{c->ws_base};
   carve_ws(wv, c->dm, &c->ws);
+  SLIP_CUDA(cudaMemset(c->ws.tickets, 0, kTickets * sizeof(unsigned)));
+  SLIP_CUDA(cudaMemset(c->ws.nonfinite, 0, sizeof(int32_t)));
+  // W problem tables (tensor maps of the 4L weight-gradient GEMMs) per slot
+  std::vector<GroupEntry> host(4 * static_cast<size_t>(c->L));
+  for (int i = 0; i < c->n_slots; ++i) {
+    std::vector<GemmDesc> probs = w_problems(c, i);
+    int tiles = 0;
+    cudaError_t e = gemm_group_encode(probs.data(), static_cast<int>(probs.size()), host.data(), &tiles);
+    if (e != cudaSuccess) {
+      set_error(std::string("stage_bind: W table: ") + gemm_last_message());
+      return SLIP_EUNSUPPORTED;
+    }
+    SLIP_CUDA(cudaMemcpy(c->slots[i].wtab, host.data(), host.size() * sizeof(GroupEntry), cudaMemcpyHostToDevice));
+    c->slots[i].wtab_tiles = tiles;
+  }
   c->state.assign(c->n_slots, SLOT_FREE);
   c->bound = true;
   return SLIP_OK;

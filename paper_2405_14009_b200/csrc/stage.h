@@ -26,17 +26,22 @@ struct LayerStash {
   bf16 *dout, *dh, *dx2, *dqkv;                          // W-stash (with y1, o, y2, g)
 };
 
+struct GroupEntry;
+
 struct SlotBufs {
   bf16* x;   // stage input   [T, h]
   bf16* dy;  // stage output gradient [T, h]
   std::vector<LayerStash> layer;
+  GroupEntry* wtab;  // device table of the slot's 4L W problems (grouped launch)
+  int wtab_tiles;
 };
 
 struct Workspace {
   float* s;          // S and dP  [z, s, s] fp32
   bf16* ds;          // dS        [z, s, s]
   bf16 *dy2, *dO, *dy1;  // [T, h]
-  float *part0, *part1, *part2;  // [kRedChunks, max(f, 3h)]
+  float* part;       // [2, kRedChunks, max(f, 3h)] column-reduction partials
+  unsigned* tickets;  // [kTickets] last-block tickets (zero between launches)
   float* loss_part;  // [256] MSE partials
   float* losses;     // [1024] per-micro-batch losses (executor)
   int32_t* nonfinite;  // [1] post-step validation flag (executor)
