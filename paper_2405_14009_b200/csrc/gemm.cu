@@ -583,6 +583,11 @@ int num_sms() {
 
 const char* gemm_last_message() { return g_msg.c_str(); }
 
+bool encode_bf16_4d(CUtensorMap* map, const void* base, uint64_t d0, uint64_t d1, uint64_t d2, uint64_t d3,
+                    int64_t s1, int64_t s2, int64_t s3, uint32_t b0, uint32_t b1) {
+  return encode4d(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, base, d0, d1, d2, d3, s1, s2, s3, b0, b1);
+}
+
 cudaError_t gemm_launch(const GemmDesc& d, cudaStream_t s) {
   g_msg.clear();
   if (d.M <= 0 || d.N <= 0 || d.K <= 0 || d.zi_count <= 0 || d.zo_count <= 0) {

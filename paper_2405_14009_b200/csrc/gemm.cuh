@@ -72,4 +72,9 @@ cudaError_t gemm_group_launch(const GroupEntry* dev_table, int n, int total_tile
 const char* gemm_last_message();
 int num_sms();
 
+// 4-D bf16 tensor map, 128-byte swizzle: dims (d0 inner, d1, d2, d3), strides in elements
+// of dims 1..3, box (b0, b1, 1, 1).  False (message in gemm_last_message) on failure.
+bool encode_bf16_4d(CUtensorMap* map, const void* base, uint64_t d0, uint64_t d1, uint64_t d2, uint64_t d3,
+                    int64_t s1, int64_t s2, int64_t s3, uint32_t b0, uint32_t b1);
+
 }  // namespace slip

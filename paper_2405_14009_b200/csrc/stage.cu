@@ -7,6 +7,7 @@
 #include <cstring>
 #include <string>
 
+#include "attention.cuh"
 #include "common.h"
 #include "gemm.cuh"
 #include "kernels.cuh"
@@ -80,7 +81,7 @@ struct Carver {
 
 void carve_slot(Carver& cv, const Dims& d, int L, SlotBufs* out) {
   const size_t Th = static_cast<size_t>(d.T) * d.h, Tf = static_cast<size_t>(d.T) * d.f;
-  const size_t zss = static_cast<size_t>(d.z) * d.s * d.s;
+  const size_t zs = static_cast<size_t>(d.z) * d.s;
   SlotBufs sb;
   sb.x = cv.take<bf16>(Th);
   sb.dy = cv.take<bf16>(Th);
@@ -90,7 +91,7 @@ void carve_slot(Carver& cv, const Dims& d, int L, SlotBufs* out) {
     ls.xin = l == 0 ? sb.x : cv.take<bf16>(Th);
     ls.y1 = cv.take<bf16>(Th);
     ls.qkv = cv.take<bf16>(3 * Th);
-    ls.p = cv.take<bf16>(zss);
+    ls.lse = cv.take<float>(zs);
     ls.o = cv.take<bf16>(Th);
     ls.x2 = cv.take<bf16>(Th);
     ls.y2 = cv.take<bf16>(Th);
@@ -112,11 +113,9 @@ void carve_slot(Carver& cv, const Dims& d, int L, SlotBufs* out) {
 
 void carve_ws(Carver& cv, const Dims& d, Workspace* out) {
   const size_t Th = static_cast<size_t>(d.T) * d.h;
-  const size_t zss = static_cast<size_t>(d.z) * d.s * d.s;
   const size_t red = static_cast<size_t>(kRedChunks) * (d.f > 3 * d.h ? d.f : 3 * d.h);
   Workspace w;
-  w.s = cv.take<float>(zss);
-  w.ds = cv.take<bf16>(zss);
+  w.dsum = cv.take<float>(static_cast<size_t>(d.z) * d.s);
   w.dy2 = cv.take<bf16>(Th);
   w.dO = cv.take<bf16>(Th);
   w.dy1 = cv.take<bf16>(Th);
@@ -251,105 +250,45 @@ slip_status kcheck(slip_ctx* c, cudaError_t e, const char* what, int n_launch = 
 }
 
 // ---------------------------------------------------------------- attention
-slip_status attention_fwd(slip_ctx* c, LayerStash& ls, cudaStream_t s) {
+// Fused causal attention (attention.cu): S and dP live only in TMEM; F stashes the
+// per-row log-sum-exp instead of P.  Formulas of oracle/layer.py attention_fwd / _bwd.
+AttnArgs attn_args(slip_ctx* c, LayerStash& ls) {
   const Dims& D = c->dm;
-  const int64_t h3 = 3LL * D.h;
-  // S = Q K^T / sqrt(d), causal tiles only, fp32 transient
-  GemmDesc g;
-  g.M = D.s;
-  g.N = D.s;
-  g.K = D.d;
-  g.zi_count = D.a;
-  g.zo_count = D.b;
-  g.bn = 128;
-  g.causal = CAUSAL_TILES;
-  g.a = op(ls.qkv, h3, false, D.d, D.s * h3);
-  g.b = op(ls.qkv + D.h, h3, false, D.d, D.s * h3);
-  g.mode = EPI_F32_STORE;
-  g.alpha = 1.0f / std::sqrt(static_cast<float>(D.d));
-  g.c = c->ws.s;
-  g.ldc = D.s;
-  g.c_zi = static_cast<int64_t>(D.s) * D.s;
-  g.c_zo = static_cast<int64_t>(D.a) * D.s * D.s;
-  SLIP_TRY(run_gemm(c, g, s, "attn S"));
-  SLIP_TRY(kcheck(c, softmax_fwd(c->ws.s, ls.p, D.z, D.s, s), "softmax_fwd"));
-  // O = P V  (k < m0 + 128)
-  GemmDesc o;
-  o.M = D.s;
-  o.N = D.d;
-  o.K = D.s;
-  o.zi_count = D.a;
-  o.zo_count = D.b;
-  o.bn = D.d;
-  o.causal = CAUSAL_K_UPPER;
-  o.a = op(ls.p, D.s, false, static_cast<int64_t>(D.s) * D.s, static_cast<int64_t>(D.a) * D.s * D.s);
-  o.b = op(ls.qkv + 2 * D.h, h3, true, D.d, D.s * h3);
-  o.mode = EPI_BF16;
-  o.c = ls.o;
-  o.ldc = D.h;
-  o.c_zi = D.d;
-  o.c_zo = static_cast<int64_t>(D.s) * D.h;
-  return run_gemm(c, o, s, "attn PV");
+  AttnArgs a;
+  a.s = D.s;
+  a.heads = D.a;
+  a.batch = D.b;
+  a.d = D.d;
+  a.qkv_ld = 3LL * D.h;
+  a.h = D.h;
+  a.qkv = ls.qkv;
+  a.o = ls.o;
+  a.dO = c->ws.dO;
+  a.out = nullptr;
+  a.lse = ls.lse;
+  a.dsum = c->ws.dsum;
+  return a;
+}
+
+slip_status attn_status(slip_ctx* c, cudaError_t e, const char* what, int launches) {
+  if (e == cudaSuccess) {
+    c->launches += launches;
+    return SLIP_OK;
+  }
+  set_error(std::string(what) + ": " + cudaGetErrorString(e) + " " + attn_last_message());
+  return e == cudaErrorInvalidValue ? SLIP_EUNSUPPORTED : SLIP_ECUDA;
+}
+
+slip_status attention_fwd(slip_ctx* c, LayerStash& ls, cudaStream_t s) {
+  AttnArgs a = attn_args(c, ls);
+  a.out = ls.o;
+  return attn_status(c, attn_forward(a, s), "attention forward", 2);
 }
 
 slip_status attention_bwd(slip_ctx* c, LayerStash& ls, cudaStream_t s) {
-  const Dims& D = c->dm;
-  const int64_t h3 = 3LL * D.h;
-  const int64_t zss_i = static_cast<int64_t>(D.s) * D.s, zss_o = static_cast<int64_t>(D.a) * D.s * D.s;
-  // dP = dO V^T (fp32, causal tiles)
-  GemmDesc g;
-  g.M = D.s;
-  g.N = D.s;
-  g.K = D.d;
-  g.zi_count = D.a;
-  g.zo_count = D.b;
-  g.bn = 128;
-  g.causal = CAUSAL_TILES;
-  g.a = op(c->ws.dO, D.h, false, D.d, static_cast<int64_t>(D.s) * D.h);
-  g.b = op(ls.qkv + 2 * D.h, h3, false, D.d, D.s * h3);
-  g.mode = EPI_F32_STORE;
-  g.alpha = 1.0f;
-  g.c = c->ws.s;
-  g.ldc = D.s;
-  g.c_zi = zss_i;
-  g.c_zo = zss_o;
-  SLIP_TRY(run_gemm(c, g, s, "attn dP"));
-  // dS = P (dP - rowsum(dP P)) / sqrt(d)
-  SLIP_TRY(kcheck(c, softmax_bwd(c->ws.s, ls.p, c->ws.ds, D.z, D.s, 1.0f / std::sqrt(static_cast<float>(D.d)), s),
-                  "softmax_bwd"));
-  auto base = [&](int which) {
-    GemmDesc x;
-    x.M = D.s;
-    x.N = D.d;
-    x.K = D.s;
-    x.zi_count = D.a;
-    x.zo_count = D.b;
-    x.bn = D.d;
-    x.mode = EPI_BF16;
-    x.c = ls.dqkv + which * D.h;
-    x.ldc = h3;
-    x.c_zi = D.d;
-    x.c_zo = D.s * h3;
-    return x;
-  };
-  // dV = P^T dO  (queries >= key tile start)
-  GemmDesc dv = base(2);
-  dv.causal = CAUSAL_K_LOWER;
-  dv.a = op(ls.p, D.s, true, zss_i, zss_o);
-  dv.b = op(c->ws.dO, D.h, true, D.d, static_cast<int64_t>(D.s) * D.h);
-  SLIP_TRY(run_gemm(c, dv, s, "attn dV"));
-  // dQ = dS K
-  GemmDesc dq = base(0);
-  dq.causal = CAUSAL_K_UPPER;
-  dq.a = op(c->ws.ds, D.s, false, zss_i, zss_o);
-  dq.b = op(ls.qkv + D.h, h3, true, D.d, D.s * h3);
-  SLIP_TRY(run_gemm(c, dq, s, "attn dQ"));
-  // dK = dS^T Q
-  GemmDesc dk = base(1);
-  dk.causal = CAUSAL_K_LOWER;
-  dk.a = op(c->ws.ds, D.s, true, zss_i, zss_o);
-  dk.b = op(ls.qkv, h3, true, D.d, D.s * h3);
-  return run_gemm(c, dk, s, "attn dK");
+  AttnArgs a = attn_args(c, ls);
+  a.out = ls.dqkv;
+  return attn_status(c, attn_backward(a, s), "attention backward", 3);
 }
 
 // colsum(a[T, N]) -> out (fp32, overwrite or accumulate), one launch

@@ -21,7 +21,8 @@ struct ParamOffsets {
 ParamOffsets param_offsets(int h, int f);
 
 struct LayerStash {
-  bf16 *xin, *y1, *qkv, *p, *o, *x2, *y2, *hpre, *g;  // F-stash
+  bf16 *xin, *y1, *qkv, *o, *x2, *y2, *hpre, *g;  // F-stash
+  float* lse;                                       // [z, s] attention log-sum-exp (replaces P)
   float *mean1, *rstd1, *mean2, *rstd2;
   bf16 *dout, *dh, *dx2, *dqkv;                          // W-stash (with y1, o, y2, g)
 };
@@ -37,8 +38,7 @@ struct SlotBufs {
 };
 
 struct Workspace {
-  float* s;          // S and dP  [z, s, s] fp32
-  bf16* ds;          // dS        [z, s, s]
+  float* dsum;       // [z, s] D = rowsum(dO * O) of the attention backward
   bf16 *dy2, *dO, *dy1;  // [T, h]
   float* part;       // [2, kRedChunks, max(f, 3h)] column-reduction partials
   unsigned* tickets;  // [kTickets] last-block tickets (zero between launches)

@@ -70,6 +70,10 @@ def main():
 
     live0 = [[1] * DP for _ in range(PP)]
     rep0, g0, p0, l0 = run(live0)
+    # every micro-batch's fault-free loss (each entry is written by exactly one last-stage rank)
+    l0c = l0.cuda()
+    dist.all_reduce(l0c)
+    l0 = l0c.cpu()
     # reference gradient of my stage from the fault-free run, shared by stage peers
     if rank == 0:
         print(json.dumps({"scenario": [], "ok": True, "period_ms": rep0.period_ms, "plan_hash": rep0.plan_hash}),
