@@ -269,10 +269,11 @@ def main():
     clk = clocks.stop() if clocks else None
     tokens_per_step = DP * m * T
     value = tokens_per_step * args.steps / (ms_total / 1000.0)
-    # roofline of the dominant kernel family: the W GEMMs (dW += dY^T X, fp32 epilogue)
-    w_ops = rep.phase_ops[2] + rep.phase_ops[3]
-    w_ms = rep.phase_ms[2] if rep.phase_ops[2] else rep.phase_ms[3]
-    flops_w_op = 2.0 * T * (4 * H * H + 2 * FFN * H) * L  # 4 products per layer
+    # roofline of the dominant kernel: the grouped W GEMM (all 4L products dW += dY^T X of a
+    # slot in one persistent tcgen05 launch, fp32 accumulation fused in the epilogue).
+    # achieved = algorithmic FLOP per launch (24 T h^2 L for ffn = 4h) x launches / their
+    # CUDA-event time on the compute stream inside the timed region.
+    flops_w_op = 2.0 * T * (4 * H * H + 2 * FFN * H) * L
     w_launches = rep.w_gemm_launches
     ach = flops_w_op * rep.phase_ops[2] / (rep.phase_ms[2] / 1e3) / 1e12 if rep.phase_ops[2] else None
     p_burst, p_sus, hbm, peak_src = peaks()
@@ -282,7 +283,7 @@ def main():
             traffic = json.load(f).get("dram_bytes_per_launch")
     except Exception:
         pass
-    kern =torch.tensor([rep.n_kernels], dtype=torch.float64, device="cuda")
+    kern = torch.tensor([rep.n_kernels], dtype=torch.float64, device="cuda")
     if world > 1:
         dist.all_reduce(kern)
     gpu_launches = int(kern.item())
@@ -338,7 +339,7 @@ def main():
         "roofline": {"bound": "tensor", "kernel": "W GEMMs (tcgen05, dW += dY^T X fused fp32 TMA reduce-add)",
                      "achieved": ach, "peak": p_sus, "peak_kind": "bf16_tflops_sustained (%s)" % peak_src,
                      "unit": "TFLOP/s", "frac": (ach / p_sus) if ach else None, "traffic": traffic,
-                     "flops_per_launch": flops_w_op / (4 * L), "launches": w_launches,
+                     "flops_per_launch": flops_w_op, "launches": w_launches,
                      "avg_launch_ms": (rep.phase_ms[2] / w_launches) if w_launches else None},
         "phases_ms_per_step": {n: rep.phase_ms[i] / args.steps for i, n in enumerate(("F", "B", "W", "BC", "OPT"))},
         "predicted_period_units": rep.predicted_period,

@@ -307,22 +307,22 @@ __global__ void __launch_bounds__(NT, 1)
   uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* Ks = sm;
   uint8_t* Vs = Ks + C::TB;
-  uint8_t* Qs = Vs + C::TB;
-  uint8_t* dOs = Qs + C::TB;
-  uint8_t* XP = dOs + C::TB;
-  uint8_t* XS = XP + 2 * ATOM;
-  float* lse_s = reinterpret_cast<float*>(XS + 2 * ATOM);
+  uint8_t* QD = Vs + C::TB;       // 2 stages of {Q_i, dO_i}
+  uint8_t* X = QD + 4 * C::TB;    // P^T, then (after dV consumed it) dS^T
+  float* lse_s = reinterpret_cast<float*>(X + 2 * ATOM);
   float* d_s = lse_s + TILE;
   uint64_t* bar = reinterpret_cast<uint64_t*>(d_s + TILE);
   uint64_t* kv_full = bar;
-  uint64_t* qd_full = bar + 1;
-  uint64_t* qd_empty = bar + 2;
-  uint64_t* s_full = bar + 3;
-  uint64_t* s_empty = bar + 4;
-  uint64_t* x_full = bar + 5;
-  uint64_t* x_empty = bar + 6;
-  uint64_t* acc_full = bar + 7;
-  uint32_t* tholder = reinterpret_cast<uint32_t*>(bar + 8);
+  uint64_t* qd_full = bar + 1;   // [2]
+  uint64_t* qd_empty = bar + 3;  // [2]
+  uint64_t* s_full = bar + 5;
+  uint64_t* s_empty = bar + 6;
+  uint64_t* xp_full = bar + 7;   // P^T written
+  uint64_t* xs_full = bar + 8;   // dS^T written
+  uint64_t* xp_free = bar + 9;   // dV MMA has read P^T
+  uint64_t* x_free = bar + 10;   // dK MMA has read dS^T
+  uint64_t* acc_full = bar + 11;
+  uint32_t* tholder = reinterpret_cast<uint32_t*>(bar + 12);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int z = blockIdx.x, hn = z % a.heads, bi = z / a.heads;
@@ -332,12 +332,16 @@ __global__ void __launch_bounds__(NT, 1)
 
   if (threadIdx.x == 0) {
     ptx::mbar_init(kv_full, 1);
-    ptx::mbar_init(qd_full, 1);
-    ptx::mbar_init(qd_empty, 1);
+    for (int t = 0; t < 2; ++t) {
+      ptx::mbar_init(&qd_full[t], 1);
+      ptx::mbar_init(&qd_empty[t], 1);
+    }
     ptx::mbar_init(s_full, 1);
     ptx::mbar_init(s_empty, NRW);
-    ptx::mbar_init(x_full, NRW);
-    ptx::mbar_init(x_empty, 1);
+    ptx::mbar_init(xp_full, NRW);
+    ptx::mbar_init(xs_full, NRW);
+    ptx::mbar_init(xp_free, 1);
+    ptx::mbar_init(x_free, 1);
     ptx::mbar_init(acc_full, 1);
     ptx::fence_mbar_init();
   }
@@ -356,22 +360,25 @@ __global__ void __launch_bounds__(NT, 1)
         ptx::tma_load_4d(&tmV, Vs + t * ATOM, kv_full, t * 64, k0, hn, bi);
       }
       for (int n = 0; n < ni; ++n) {
-        const int q0 = (j + n) * TILE;
-        ptx::mbar_wait(qd_empty, (n & 1) ^ 1);
-        ptx::mbar_arrive_expect_tx(qd_full, 2 * C::TB);
+        const int q0 = (j + n) * TILE, st = n & 1;
+        uint8_t* qs = QD + st * 2 * C::TB;
+        ptx::mbar_wait(&qd_empty[st], ((n >> 1) & 1) ^ 1);
+        ptx::mbar_arrive_expect_tx(&qd_full[st], 2 * C::TB);
         for (int t = 0; t < C::NA; ++t) {
-          ptx::tma_load_4d(&tmQ, Qs + t * ATOM, qd_full, t * 64, q0, hn, bi);
-          ptx::tma_load_4d(&tmdO, dOs + t * ATOM, qd_full, t * 64, q0, hn, bi);
+          ptx::tma_load_4d(&tmQ, qs + t * ATOM, &qd_full[st], t * 64, q0, hn, bi);
+          ptx::tma_load_4d(&tmdO, qs + C::TB + t * ATOM, &qd_full[st], t * 64, q0, hn, bi);
         }
       }
     }
   } else if (warp == 1) {
     if (lane == 0) {  // ------------------------------------------------ MMA issuer
-      const uint32_t kb = ptx::smem_u32(Ks), vb = ptx::smem_u32(Vs), qb = ptx::smem_u32(Qs),
-                     ob = ptx::smem_u32(dOs), xp = ptx::smem_u32(XP), xs = ptx::smem_u32(XS);
-      ptx::mbar_wait(kv_full, 0);
-      for (int n = 0; n < ni; ++n) {
-        ptx::mbar_wait(qd_full, n & 1);
+      const uint32_t kb = ptx::smem_u32(Ks), vb = ptx::smem_u32(Vs), qdb = ptx::smem_u32(QD),
+                     xb = ptx::smem_u32(X);
+      // S^T and dP^T of q-tile n (into TMEM once the row warps have read the previous ones)
+      auto issue_s = [&](int n) {
+        const int st = n & 1;
+        const uint32_t qb = qdb + st * 2 * C::TB, ob = qb + C::TB;
+        ptx::mbar_wait(&qd_full[st], (n >> 1) & 1);
         ptx::mbar_wait(s_empty, (n & 1) ^ 1);
         ptx::tc_fence_after();
 #pragma unroll
@@ -379,16 +386,26 @@ __global__ void __launch_bounds__(NT, 1)
 #pragma unroll
         for (int kk = 0; kk < C::KS; ++kk) ptx::tc_mma_f16(tP, dk(vb, kk), dk(ob, kk), C::IDESC_S, kk > 0);
         ptx::tc_commit(s_full);
-        ptx::mbar_wait(x_full, n & 1);
+      };
+      ptx::mbar_wait(kv_full, 0);
+      issue_s(0);
+      for (int n = 0; n < ni; ++n) {
+        const int st = n & 1;
+        const uint32_t qb = qdb + st * 2 * C::TB, ob = qb + C::TB;
+        ptx::mbar_wait(xp_full, n & 1);
         ptx::tc_fence_after();
 #pragma unroll
         for (int kk = 0; kk < TILE / 16; ++kk)
-          ptx::tc_mma_f16(tV, dk(xp, kk), dm(ob, kk), C::IDESC_O, (n > 0 || kk > 0) ? 1u : 0u);
+          ptx::tc_mma_f16(tV, dk(xb, kk), dm(ob, kk), C::IDESC_O, (n > 0 || kk > 0) ? 1u : 0u);
+        ptx::tc_commit(xp_free);
+        if (n + 1 < ni) issue_s(n + 1);  // overlaps the row warps' dS^T work of tile n
+        ptx::mbar_wait(xs_full, n & 1);
+        ptx::tc_fence_after();
 #pragma unroll
         for (int kk = 0; kk < TILE / 16; ++kk)
-          ptx::tc_mma_f16(tK, dk(xs, kk), dm(qb, kk), C::IDESC_O, (n > 0 || kk > 0) ? 1u : 0u);
-        ptx::tc_commit(x_empty);
-        ptx::tc_commit(qd_empty);
+          ptx::tc_mma_f16(tK, dk(xb, kk), dm(qb, kk), C::IDESC_O, (n > 0 || kk > 0) ? 1u : 0u);
+        ptx::tc_commit(x_free);
+        ptx::tc_commit(&qd_empty[st]);
       }
       ptx::tc_commit(acc_full);
     }
@@ -398,7 +415,7 @@ __global__ void __launch_bounds__(NT, 1)
     const int r = lq * 32 + lane;
     const int key = k0 + r;
     const size_t zs = static_cast<size_t>(z) * a.s;
-    const uint32_t xp = ptx::smem_u32(XP), xs = ptx::smem_u32(XS);
+    const uint32_t xb = ptx::smem_u32(X);
     const uint32_t lane_off = static_cast<uint32_t>(lq * 32) << 16;
     const uint32_t toff = lane_off + cg * 32;
     for (int n = 0; n < ni; ++n) {
@@ -419,7 +436,6 @@ __global__ void __launch_bounds__(NT, 1)
       ptx::tc_fence_before();
       __syncwarp();
       if (lane == 0) ptx::mbar_arrive(s_empty);
-      ptx::mbar_wait(x_empty, (n & 1) ^ 1);
       const bool diag = n == 0;  // key tile == query tile: causal mask inside the tile
       float pt[32], st[32];
 #pragma unroll
@@ -429,16 +445,22 @@ __global__ void __launch_bounds__(NT, 1)
         pt[e] = p;
         st[e] = p * (__uint_as_float(pv[e]) - d_s[qi]) * a.scale;
       }
+      ptx::mbar_wait(x_free, (n & 1) ^ 1);  // the previous tile's dK MMA has read X
 #pragma unroll
-      for (int g = 0; g < 4; ++g) {
-        st_shared_v4(xp + xoff(r, cg * 4 + g), pack2(pt[g * 8 + 0], pt[g * 8 + 1]), pack2(pt[g * 8 + 2], pt[g * 8 + 3]),
+      for (int g = 0; g < 4; ++g)
+        st_shared_v4(xb + xoff(r, cg * 4 + g), pack2(pt[g * 8 + 0], pt[g * 8 + 1]), pack2(pt[g * 8 + 2], pt[g * 8 + 3]),
                      pack2(pt[g * 8 + 4], pt[g * 8 + 5]), pack2(pt[g * 8 + 6], pt[g * 8 + 7]));
-        st_shared_v4(xs + xoff(r, cg * 4 + g), pack2(st[g * 8 + 0], st[g * 8 + 1]), pack2(st[g * 8 + 2], st[g * 8 + 3]),
-                     pack2(st[g * 8 + 4], st[g * 8 + 5]), pack2(st[g * 8 + 6], st[g * 8 + 7]));
-      }
       ptx::fence_proxy_async_smem();
       __syncwarp();
-      if (lane == 0) ptx::mbar_arrive(x_full);
+      if (lane == 0) ptx::mbar_arrive(xp_full);
+      ptx::mbar_wait(xp_free, n & 1);  // dV MMA has read P^T
+#pragma unroll
+      for (int g = 0; g < 4; ++g)
+        st_shared_v4(xb + xoff(r, cg * 4 + g), pack2(st[g * 8 + 0], st[g * 8 + 1]), pack2(st[g * 8 + 2], st[g * 8 + 3]),
+                     pack2(st[g * 8 + 4], st[g * 8 + 5]), pack2(st[g * 8 + 6], st[g * 8 + 7]));
+      ptx::fence_proxy_async_smem();
+      __syncwarp();
+      if (lane == 0) ptx::mbar_arrive(xs_full);
     }
     ptx::mbar_wait(acc_full, 0);
     ptx::tc_fence_after();
@@ -492,7 +514,7 @@ constexpr int row_smem(int mode) {
 }
 template <int D>
 constexpr int col_smem() {
-  return 4 * AC<D>::TB + 4 * ATOM + 2 * TILE * 4 + 1024 + 1024;
+  return 6 * AC<D>::TB + 2 * ATOM + 2 * TILE * 4 + 1024 + 1024;
 }
 
 struct Maps {

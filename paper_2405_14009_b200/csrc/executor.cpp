@@ -5,10 +5,10 @@
 // the loop — and receives are posted in the sender's order (check_fifo), so re-routed
 // traffic (§3.1, ReRouteAct / ReRouteGrad line 554) cannot deadlock.
 //
-// Buffer protocol per slot: slot.x holds the stage input (RECV_X / LOAD_X) and, after B,
-// the input gradient that SEND_DX ships; slot.dy holds the stage output that SEND_Y
-// ships and, after it, the output gradient (RECV_DY / LOSS).  Events: `freed` (W done),
-// `sent_y`, `sent_dx` guard the reuse of those buffers.
+// Buffer protocol per slot: slot.x holds the stage input (RECV_X / LOAD_X); slot.dy holds
+// the stage output that SEND_Y ships and, after it, the output gradient (RECV_DY / LOSS);
+// slot.dx holds the input gradient B produces and SEND_DX ships.  Events: `freed` (W
+// done) guards slot.x, `sent_y` guards slot.dy, `sent_dx` guards slot.dx.
 #include <algorithm>
 #include <cstring>
 #include <string>
@@ -147,7 +147,6 @@ extern "C" slip_status slip_execute_schedule(slip_ctx* ctx, slip_comm* comm, con
       switch (a.kind) {
         case SLIP_ACT_LOAD_X: {
           if (se->freed) SLIP_CUDA(cudaStreamWaitEvent(cs, se->freed, 0));
-          if (se->sent_dx) SLIP_CUDA(cudaStreamWaitEvent(cs, se->sent_dx, 0));
           if (io && io->x_host) {
             SLIP_CUDA(cudaMemcpyAsync(sb->x, io->x_host[a.origin * m + a.mb], bytes, cudaMemcpyHostToDevice, cs));
           } else {
@@ -159,7 +158,6 @@ extern "C" slip_status slip_execute_schedule(slip_ctx* ctx, slip_comm* comm, con
         case SLIP_ACT_RECV_X: {
           cudaStream_t ps = xfer_stream(a.peer, me);
           if (se->freed) SLIP_CUDA(cudaStreamWaitEvent(ps, se->freed, 0));
-          if (se->sent_dx) SLIP_CUDA(cudaStreamWaitEvent(ps, se->sent_dx, 0));
           ncclResult_t r = ncclRecv(sb->x, Th, ncclBfloat16, 0, xfer_comm(a.peer, me), ps);
           if (r != ncclSuccess) return nccl_status(r, "ncclRecv activation");
           SLIP_CUDA(chain(ps, cs));
@@ -201,20 +199,22 @@ extern "C" slip_status slip_execute_schedule(slip_ctx* ctx, slip_comm* comm, con
         }
         case SLIP_ACT_B:
         case SLIP_ACT_BC: {
-          void* dx = me_i > 0 ? static_cast<void*>(sb->x) : nullptr;  // dx overwrites the consumed input
+          // slot.dx is the send buffer of the input gradient: the previous occupant's send must be done
+          if (se->sent_dx) SLIP_CUDA(cudaStreamWaitEvent(cs, se->sent_dx, 0));
+          void* dx = me_i > 0 ? static_cast<void*>(sb->dx) : nullptr;
           SLIP_TRY(slip_backward_input(ctx, a.slot, sb->dy, dx, a.accumulate & 1, stream));
           if (a.kind == SLIP_ACT_BC) {
             SLIP_TRY(slip_backward_weight(ctx, a.slot, (a.accumulate >> 1) & 1, stream));
             SLIP_CUDA(pool.get(&se->freed));
             SLIP_CUDA(cudaEventRecord(se->freed, cs));
-            if (timed) out->w_gemm_launches += 4 * ctx->L;
+            if (timed) out->w_gemm_launches += 1;  // one grouped launch of all 4L products
           }
           break;
         }
         case SLIP_ACT_SEND_DX: {
           cudaStream_t ps = xfer_stream(me, a.peer);
           SLIP_CUDA(chain(cs, ps));
-          ncclResult_t r = ncclSend(sb->x, Th, ncclBfloat16, 1, xfer_comm(me, a.peer), ps);
+          ncclResult_t r = ncclSend(sb->dx, Th, ncclBfloat16, 1, xfer_comm(me, a.peer), ps);
           if (r != ncclSuccess) return nccl_status(r, "ncclSend gradient");
           SLIP_CUDA(pool.get(&se->sent_dx));
           SLIP_CUDA(cudaEventRecord(se->sent_dx, ps));
@@ -224,7 +224,7 @@ extern "C" slip_status slip_execute_schedule(slip_ctx* ctx, slip_comm* comm, con
           SLIP_TRY(slip_backward_weight(ctx, a.slot, a.accumulate, stream));
           SLIP_CUDA(pool.get(&se->freed));
           SLIP_CUDA(cudaEventRecord(se->freed, cs));
-          if (timed) out->w_gemm_launches += 4 * ctx->L;
+          if (timed) out->w_gemm_launches += 1;  // one grouped launch of all 4L products
           break;
         case SLIP_ACT_AR:
           if (comm->stage_comm) {

@@ -339,39 +339,53 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
               ptx::tma_store_4d(mC, buf, n, row0, tl.zi, tl.zo);
             ptx::bulk_commit();
           }
-        } else if (m < tl.M) {
-          const int64_t off = tl.zo * p.c_zo + tl.zi * p.c_zi + static_cast<int64_t>(m) * p.ldc + n;
-          __nv_bfloat16* cp = reinterpret_cast<__nv_bfloat16*>(p.c) + off;
+        } else {
+          // Transpose the 32x32 chunk through shared memory (16-byte chunks XOR-swizzled,
+          // conflict-free both ways) so that 4 lanes cover 64 contiguous bytes of a row:
+          // bias / residual / aux reads and the bf16 stores are coalesced per row.
+          (void)m;
+          __syncwarp();
+          float4* rowp = reinterpret_cast<float4*>(buf + lane * 32);
 #pragma unroll
-          for (int q = 0; q < 4; ++q) {
-            const int nn = n + q * 8;
-            if (nn >= tl.N) break;
-            float x[8];
+          for (int j = 0; j < 8; ++j)
+            rowp[j ^ (lane & 7)] =
+                make_float4(p.alpha * __uint_as_float(r[4 * j]), p.alpha * __uint_as_float(r[4 * j + 1]),
+                            p.alpha * __uint_as_float(r[4 * j + 2]), p.alpha * __uint_as_float(r[4 * j + 3]));
+          __syncwarp();
+          const int qd = lane & 3;       // 8-column group of this lane
+          const int cc = n + 8 * qd;     // its first output column
+          float bv[8];
 #pragma unroll
-            for (int e = 0; e < 8; ++e) x[e] = __uint_as_float(r[q * 8 + e]) * p.alpha;
-            if (p.bias) {
-              float b[8];
-              unpack8(*reinterpret_cast<const uint4*>(p.bias + nn), b);
+          for (int e = 0; e < 8; ++e) bv[e] = 0.f;
+          if (p.bias && cc < tl.N) unpack8(*reinterpret_cast<const uint4*>(p.bias + cc), bv);
+          const float4* sb = reinterpret_cast<const float4*>(buf);
 #pragma unroll
-              for (int e = 0; e < 8; ++e) x[e] += b[e];
-            }
+          for (int it = 0; it < 4; ++it) {
+            const int rr = 8 * it + (lane >> 2);
+            const int mm = row0 + rr;
+            const float4 u0 = sb[rr * 8 + ((2 * qd) ^ (rr & 7))];
+            const float4 u1 = sb[rr * 8 + ((2 * qd + 1) ^ (rr & 7))];
+            if (mm >= tl.M || cc >= tl.N) continue;
+            float x[8] = {u0.x + bv[0], u0.y + bv[1], u0.z + bv[2], u0.w + bv[3],
+                          u1.x + bv[4], u1.y + bv[5], u1.z + bv[6], u1.w + bv[7]};
+            const int64_t off = tl.zo * p.c_zo + tl.zi * p.c_zi + static_cast<int64_t>(mm) * p.ldc + cc;
             if (p.mode == EPI_BF16_GELU) {
-              *reinterpret_cast<uint4*>(p.aux + off + q * 8) = pack8(x);
+              *reinterpret_cast<uint4*>(p.aux + off) = pack8(x);
 #pragma unroll
               for (int e = 0; e < 8; ++e) x[e] = gelu_f(x[e]);
             } else if (p.mode == EPI_BF16_DGELU) {
               float hv[8];
-              unpack8(*reinterpret_cast<const uint4*>(p.aux + off + q * 8), hv);
+              unpack8(*reinterpret_cast<const uint4*>(p.aux + off), hv);
 #pragma unroll
               for (int e = 0; e < 8; ++e) x[e] *= gelu_grad_f(hv[e]);
             }
             if (p.resid) {
               float rv[8];
-              unpack8(*reinterpret_cast<const uint4*>(p.resid + off + q * 8), rv);
+              unpack8(*reinterpret_cast<const uint4*>(p.resid + off), rv);
 #pragma unroll
               for (int e = 0; e < 8; ++e) x[e] += rv[e];
             }
-            *reinterpret_cast<uint4*>(cp + q * 8) = pack8(x);
+            *reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(p.c) + off) = pack8(x);
           }
         }
       }

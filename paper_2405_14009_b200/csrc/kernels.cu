@@ -191,17 +191,20 @@ __global__ void __launch_bounds__(512) ln_bwd_rows_kernel(const bf16* __restrict
 
 // ------------------------------------------------------------------ column reductions
 // grid (ceil(N/256), kRedChunks), block 256 = 32 column-vectors x 8 row groups.
-// MODE 0: out0 (+)= sum_t a.   MODE 1 (LayerNorm): out0 (+)= sum dy*xhat, out1 (+)= sum dy.
+// MODE 0: out0 (+)= sum_t a.
+// MODE 1 (LayerNorm): out0 (+)= sum dy*xhat, out1 (+)= sum dy       (a = dy)
+// MODE 2 (LayerNorm + producer bias): MODE 1 and out2 (+)= sum_t dx (dx = the LN input grad)
 // Each block writes its chunk's partials; the last block of a column strip (atomic
 // ticket) sums the kRedChunks partials in chunk order and resets the ticket.
 template <int MODE>
 __global__ void __launch_bounds__(256) colred_kernel(const bf16* __restrict__ a, int64_t ld, const bf16* __restrict__ x,
                                                      const float* __restrict__ mean, const float* __restrict__ rstd,
-                                                     int T, int N, float* part, float* __restrict__ out0,
-                                                     float* __restrict__ out1, int accumulate,
+                                                     const bf16* __restrict__ dx, int T, int N, float* part,
+                                                     float* __restrict__ out0, float* __restrict__ out1,
+                                                     float* __restrict__ out2, int accumulate,
                                                      unsigned* __restrict__ tickets) {
-  __shared__ float red0[8][257];
-  __shared__ float red1[MODE == 1 ? 8 : 1][257];
+  constexpr int NO = MODE == 0 ? 1 : (MODE == 1 ? 2 : 3);  // outputs
+  __shared__ float red[NO][8][257];
   __shared__ bool last;
   const int cv = threadIdx.x & 31;
   const int rg = threadIdx.x >> 5;
@@ -210,46 +213,53 @@ __global__ void __launch_bounds__(256) colred_kernel(const bf16* __restrict__ a,
   const int rows_per = (T + kRedChunks - 1) / kRedChunks;
   const int r0 = chunk * rows_per;
   const int r1 = min(T, r0 + rows_per);
-  float acc0[8], acc1[8];
+  float acc[NO][8];
 #pragma unroll
-  for (int e = 0; e < 8; ++e) acc0[e] = acc1[e] = 0.f;
+  for (int o = 0; o < NO; ++o)
+#pragma unroll
+    for (int e = 0; e < 8; ++e) acc[o][e] = 0.f;
   if (col < N) {
+#pragma unroll 4
     for (int r = r0 + rg; r < r1; r += 8) {
       float v[8];
       unpack8(*reinterpret_cast<const uint4*>(a + static_cast<size_t>(r) * ld + col), v);
       if (MODE == 0) {
 #pragma unroll
-        for (int e = 0; e < 8; ++e) acc0[e] += v[e];
+        for (int e = 0; e < 8; ++e) acc[0][e] += v[e];
       } else {
         float xv[8];
         unpack8(*reinterpret_cast<const uint4*>(x + static_cast<size_t>(r) * N + col), xv);
         const float mu = mean[r], rs = rstd[r];
 #pragma unroll
         for (int e = 0; e < 8; ++e) {
-          acc0[e] += v[e] * ((xv[e] - mu) * rs);
-          acc1[e] += v[e];
+          acc[0][e] += v[e] * ((xv[e] - mu) * rs);
+          acc[1][e] += v[e];
+        }
+        if (MODE == 2) {
+          float gv[8];
+          unpack8(*reinterpret_cast<const uint4*>(dx + static_cast<size_t>(r) * N + col), gv);
+#pragma unroll
+          for (int e = 0; e < 8; ++e) acc[NO - 1][e] += gv[e];
         }
       }
     }
   }
 #pragma unroll
-  for (int e = 0; e < 8; ++e) {
-    red0[rg][cv * 8 + e] = acc0[e];
-    if (MODE == 1) red1[rg][cv * 8 + e] = acc1[e];
-  }
+  for (int o = 0; o < NO; ++o)
+#pragma unroll
+    for (int e = 0; e < 8; ++e) red[o][rg][cv * 8 + e] = acc[o][e];
   __syncthreads();
   const int c = threadIdx.x;  // 256 columns of this strip
   const int gcol = blockIdx.x * 256 + c;
-  float* part1 = part + static_cast<size_t>(kRedChunks) * N;
+  const size_t plane = static_cast<size_t>(kRedChunks) * N;
   if (gcol < N) {
-    float s0 = 0.f, s1 = 0.f;
 #pragma unroll
-    for (int g = 0; g < 8; ++g) {
-      s0 += red0[g][c];
-      if (MODE == 1) s1 += red1[g][c];
+    for (int o = 0; o < NO; ++o) {
+      float s = 0.f;
+#pragma unroll
+      for (int g = 0; g < 8; ++g) s += red[o][g][c];
+      part[o * plane + static_cast<size_t>(chunk) * N + gcol] = s;
     }
-    part[static_cast<size_t>(chunk) * N + gcol] = s0;
-    if (MODE == 1) part1[static_cast<size_t>(chunk) * N + gcol] = s1;
   }
   __threadfence();
   __syncthreads();
@@ -258,13 +268,14 @@ __global__ void __launch_bounds__(256) colred_kernel(const bf16* __restrict__ a,
   if (!last) return;
   __threadfence();
   if (gcol < N) {
-    float s0 = 0.f, s1 = 0.f;
-    for (int k = 0; k < kRedChunks; ++k) {
-      s0 += __ldcg(part + static_cast<size_t>(k) * N + gcol);
-      if (MODE == 1) s1 += __ldcg(part1 + static_cast<size_t>(k) * N + gcol);
+    float* outs[3] = {out0, out1, out2};
+#pragma unroll
+    for (int o = 0; o < NO; ++o) {
+      float s = 0.f;
+      for (int k = 0; k < kRedChunks; ++k) s += __ldcg(part + o * plane + static_cast<size_t>(k) * N + gcol);
+      float* out = outs[o];
+      out[gcol] = accumulate ? out[gcol] + s : s;
     }
-    out0[gcol] = accumulate ? out0[gcol] + s0 : s0;
-    if (MODE == 1) out1[gcol] = accumulate ? out1[gcol] + s1 : s1;
   }
   if (threadIdx.x == 0) tickets[blockIdx.x] = 0u;
 }
@@ -511,18 +522,20 @@ cudaError_t ln_bwd(const bf16* dy, const bf16* x, const float* mean, const float
                    const bf16* resid, bf16* dx, float* dgamma, float* dbeta, float* dxsum, int accumulate, float* part,
                    unsigned* tickets, int T, int h, cudaStream_t s) {
   if (h % 8 || h > 8192) return cudaErrorInvalidValue;
-  // gamma/beta partials first: dx may alias x (the executor writes dx over the consumed input)
-  dim3 grid((h + 255) / 256, kRedChunks);
-  colred_kernel<1><<<grid, 256, 0, s>>>(dy, h, x, mean, rstd, T, h, part, dgamma, dbeta, accumulate, tickets);
+  if ((h + 255) / 256 > kTickets || dx == x) return cudaErrorInvalidValue;
   if (dx) {
     int nt, vpt;
     ln_shape(h, &nt, &vpt);
     if (vpt == 1) ln_bwd_rows_kernel<1><<<T, nt, 0, s>>>(dy, x, mean, rstd, gamma, resid, dx, h);
     else ln_bwd_rows_kernel<2><<<T, nt, 0, s>>>(dy, x, mean, rstd, gamma, resid, dx, h);
-    if (dxsum)
-      colred_kernel<0><<<grid, 256, 0, s>>>(dx, h, nullptr, nullptr, nullptr, T, h, part, dxsum, nullptr, accumulate,
-                                            tickets);
   }
+  dim3 grid((h + 255) / 256, kRedChunks);
+  if (dx && dxsum)
+    colred_kernel<2><<<grid, 256, 0, s>>>(dy, h, x, mean, rstd, dx, T, h, part, dgamma, dbeta, dxsum, accumulate,
+                                          tickets);
+  else
+    colred_kernel<1><<<grid, 256, 0, s>>>(dy, h, x, mean, rstd, nullptr, T, h, part, dgamma, dbeta, nullptr,
+                                          accumulate, tickets);
   return cudaGetLastError();
 }
 
@@ -530,8 +543,8 @@ cudaError_t colsum(const bf16* a, int T, int N, int64_t ld, float* out, int accu
                    unsigned* tickets, cudaStream_t s) {
   if (N % 8 || ld % 8 || (N + 255) / 256 > kTickets) return cudaErrorInvalidValue;
   dim3 grid((N + 255) / 256, kRedChunks);
-  colred_kernel<0><<<grid, 256, 0, s>>>(a, ld, nullptr, nullptr, nullptr, T, N, part, out, nullptr, accumulate,
-                                        tickets);
+  colred_kernel<0><<<grid, 256, 0, s>>>(a, ld, nullptr, nullptr, nullptr, nullptr, T, N, part, out, nullptr, nullptr,
+                                        accumulate, tickets);
   return cudaGetLastError();
 }
 

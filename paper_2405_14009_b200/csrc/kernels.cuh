@@ -11,7 +11,7 @@ namespace slip {
 
 using bf16 = __nv_bfloat16;
 
-constexpr int kRedChunks = 64;  // row chunks of the deterministic column reductions
+constexpr int kRedChunks = 16;  // row chunks of the deterministic column reductions
 constexpr int kTickets = 256;   // column strips (256 columns each) a reduction may use
 
 // LayerNorm forward over rows of x [T, h]: y = xhat*gamma + beta; mean, rstd fp32 [T].
@@ -19,9 +19,9 @@ cudaError_t ln_fwd(const bf16* x, const bf16* gamma, const bf16* beta, bf16* y, 
                    int h, float eps, cudaStream_t s);
 
 // LayerNorm backward.  dx = resid + rstd*(g - mean_h(g) - xhat*mean_h(g*xhat)), g = dy*gamma
-// (dx may be null and may alias x).  dgamma (+)= sum_t dy*xhat, dbeta (+)= sum_t dy and,
-// if dxsum != null, dxsum (+)= sum_t dx.  part: 2*kRedChunks*h floats of scratch;
-// tickets: kTickets zero-initialised counters (left zeroed).
+// (dx may be null; it must not alias x).  dgamma (+)= sum_t dy*xhat, dbeta (+)= sum_t dy and,
+// if dxsum != null, dxsum (+)= sum_t dx, all three in ONE column-reduction launch.
+// part: 3*kRedChunks*h floats of scratch; tickets: kTickets zero-initialised counters.
 cudaError_t ln_bwd(const bf16* dy, const bf16* x, const float* mean, const float* rstd, const bf16* gamma,
                    const bf16* resid, bf16* dx, float* dgamma, float* dbeta, float* dxsum, int accumulate, float* part,
                    unsigned* tickets, int T, int h, cudaStream_t s);

@@ -85,6 +85,7 @@ void carve_slot(Carver& cv, const Dims& d, int L, SlotBufs* out) {
   SlotBufs sb;
   sb.x = cv.take<bf16>(Th);
   sb.dy = cv.take<bf16>(Th);
+  sb.dx = cv.take<bf16>(Th);
   sb.layer.resize(L);
   for (int l = 0; l < L; ++l) {
     LayerStash& ls = sb.layer[l];
@@ -119,7 +120,7 @@ void carve_ws(Carver& cv, const Dims& d, Workspace* out) {
   w.dy2 = cv.take<bf16>(Th);
   w.dO = cv.take<bf16>(Th);
   w.dy1 = cv.take<bf16>(Th);
-  w.part = cv.take<float>(2 * red);
+  w.part = cv.take<float>(3 * red);
   w.tickets = cv.take<unsigned>(kTickets);
   w.loss_part = cv.take<float>(256);
   w.losses = cv.take<float>(1024);
@@ -376,7 +377,7 @@ slip_status backward_input_impl(slip_ctx* c, int slot, const void* dy, void* dx,
     SLIP_TRY(kcheck(c,
                     ln_bwd(c->ws.dy2, ls.x2, ls.mean2, ls.rstd2, Wt.g2, ls.dout, ls.dx2, G.g2, G.b2n, G.bo, accumulate,
                            c->ws.part, c->ws.tickets, D.T, D.h, s),
-                    "ln_bwd 2", 3));
+                    "ln_bwd 2", 2));
     // dO = dX2 Wo
     SLIP_TRY(linear_dx(c, ls.dx2, Wt.wo, D.h, D.h, c->ws.dO, EPI_BF16, nullptr, s));
     SLIP_TRY(attention_bwd(c, ls, s));
@@ -389,7 +390,7 @@ slip_status backward_input_impl(slip_ctx* c, int slot, const void* dy, void* dx,
     SLIP_TRY(kcheck(c,
                     ln_bwd(c->ws.dy1, ls.xin, ls.mean1, ls.rstd1, Wt.g1, ls.dx2, dxl, G.g1, G.b1n, dxl ? dxsum : nullptr,
                            accumulate, c->ws.part, c->ws.tickets, D.T, D.h, s),
-                    "ln_bwd 1", dxl ? (dxsum ? 3 : 2) : 1));
+                    "ln_bwd 1", dxl ? 2 : 1));
   }
   return SLIP_OK;
 }

@@ -32,6 +32,7 @@ struct GroupEntry;
 struct SlotBufs {
   bf16* x;   // stage input   [T, h]
   bf16* dy;  // stage output gradient [T, h]
+  bf16* dx;  // stage input gradient produced by B (executor send buffer) [T, h]
   std::vector<LayerStash> layer;
   GroupEntry* wtab;  // device table of the slot's 4L W problems (grouped launch)
   int wtab_tiles;

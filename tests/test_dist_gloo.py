@@ -56,14 +56,14 @@ def simulate(progs, N, DP, live):
             sv = slot.setdefault(s, {"freed": None, "sent_y": None, "sent_dx": None})
             cs = tail.get("cs")
             if k == "LOAD_X":
-                n = add([cs, sv["freed"], sv["sent_dx"]])
+                n = add([cs, sv["freed"]])
                 tail["cs"] = n
             elif k in ("RECV_X", "RECV_DY"):
                 st = ("pair", peer, r)
                 q = chan.get((peer, r, k), 0)
                 chan[(peer, r, k)] = q + 1
                 deps = [tail.get(st)]
-                deps += [sv["freed"], sv["sent_dx"]] if k == "RECV_X" else [sv["sent_y"], cs]
+                deps += [sv["freed"]] if k == "RECV_X" else [sv["sent_y"], cs]
                 n = add(deps, rv=(peer, r, "act" if k == "RECV_X" else "grad", q))
                 tail[st] = n
                 pending_cs_dep = n
@@ -84,6 +84,8 @@ def simulate(progs, N, DP, live):
                 deps = [cs, pending_cs_dep]
                 if k == "F":
                     deps.append(sv["sent_y"])
+                if k in ("B", "BC"):
+                    deps.append(sv["sent_dx"])  # slot.dx is the previous occupant's send buffer
                 n = add(deps)
                 pending_cs_dep = None
                 tail["cs"] = n
