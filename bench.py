@@ -274,8 +274,17 @@ def main():
     # achieved = algorithmic FLOP per launch (24 T h^2 L for ffn = 4h) x launches / their
     # CUDA-event time on the compute stream inside the timed region.
     flops_w_op = 2.0 * T * (4 * H * H + 2 * FFN * H) * L
-    w_launches = rep.w_gemm_launches
-    ach = flops_w_op * rep.phase_ops[2] / (rep.phase_ms[2] / 1e3) / 1e12 if rep.phase_ops[2] else None
+    ach_local = flops_w_op * rep.phase_ops[2] / (rep.phase_ms[2] / 1e3) / 1e12 if rep.phase_ops[2] else 0.0
+    # masked ranks run nothing: take the per-phase numbers of the busiest live rank
+    stats = torch.tensor([ach_local, float(rep.w_gemm_launches), rep.phase_ms[2]] + list(rep.phase_ms[:5]),
+                         dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(stats, op=dist.ReduceOp.MAX)
+    stats = stats.tolist()
+    ach = stats[0] or None
+    w_launches = int(stats[1])
+    w_ms_total = stats[2]
+    phase_ms = stats[3:8]
     p_burst, p_sus, hbm, peak_src = peaks()
     traffic = None
     try:
@@ -340,8 +349,9 @@ def main():
                      "achieved": ach, "peak": p_sus, "peak_kind": "bf16_tflops_sustained (%s)" % peak_src,
                      "unit": "TFLOP/s", "frac": (ach / p_sus) if ach else None, "traffic": traffic,
                      "flops_per_launch": flops_w_op, "launches": w_launches,
-                     "avg_launch_ms": (rep.phase_ms[2] / w_launches) if w_launches else None},
-        "phases_ms_per_step": {n: rep.phase_ms[i] / args.steps for i, n in enumerate(("F", "B", "W", "BC", "OPT"))},
+                     "avg_launch_ms": (w_ms_total / w_launches) if w_launches else None},
+        "phases_ms_per_step_busiest_rank": {n: phase_ms[i] / args.steps
+                                            for i, n in enumerate(("F", "B", "W", "BC", "OPT"))},
         "predicted_period_units": rep.predicted_period,
         "planner_costs_10us": [costs.t_f, costs.t_b, costs.t_w, costs.t_opt],
     }

@@ -15,6 +15,7 @@
 
 #include "attention.cuh"
 #include "gemm.cuh"
+#include "launch.cuh"
 #include "ptx.cuh"
 
 namespace slip {
@@ -147,6 +148,7 @@ __global__ void __launch_bounds__(NT, 1)
   ptx::tc_fence_after();
   const uint32_t tmem = *tholder;
   const uint32_t tS = tmem, tP = tmem + 128, tA = tmem + 256;
+  ptx::grid_dep_wait();  // PDL: the prologue above overlapped the previous kernel
   // STATS: per column-group running (max, sum) of each row, merged at the end
   __shared__ float2 stats[MODE == M_STATS ? 4 : 1][MODE == M_STATS ? TILE : 1];
 
@@ -351,6 +353,7 @@ __global__ void __launch_bounds__(NT, 1)
   ptx::tc_fence_after();
   const uint32_t tmem = *tholder;
   const uint32_t tS = tmem, tP = tmem + 128, tV = tmem + 256, tK = tmem + 384;
+  ptx::grid_dep_wait();  // PDL: the prologue above overlapped the previous kernel
 
   if (warp == 0) {
     if (lane == 0) {  // ------------------------------------------------ TMA producer
@@ -487,6 +490,7 @@ __global__ void __launch_bounds__(NT, 1)
 __global__ void __launch_bounds__(256) attn_dsum_kernel(const __nv_bfloat16* __restrict__ o,
                                                         const __nv_bfloat16* __restrict__ dO, float* __restrict__ dsum,
                                                         int s, int heads, int d, int64_t h, int rows) {
+  ptx::grid_dep_wait();
   const int gw = blockIdx.x * 8 + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
   if (gw >= rows * heads) return;
@@ -556,9 +560,9 @@ cudaError_t forward_d(const AttnArgs& a, cudaStream_t st) {
     once = true;
   }
   dim3 grid(a.heads * a.batch, k.ntiles);  // z fastest: all heads' longest tiles go first
-  attn_row_kernel<D, M_STATS><<<grid, NT, s0, st>>>(mp.q, mp.k, mp.v, mp.dO, k);
-  attn_row_kernel<D, M_FWD><<<grid, NT, s1, st>>>(mp.q, mp.k, mp.v, mp.dO, k);
-  return cudaGetLastError();
+  cudaError_t e = launch_pdl(attn_row_kernel<D, M_STATS>, grid, dim3(NT), s0, st, 1, mp.q, mp.k, mp.v, mp.dO, k);
+  if (e != cudaSuccess) return e;
+  return launch_pdl(attn_row_kernel<D, M_FWD>, grid, dim3(NT), s1, st, 1, mp.q, mp.k, mp.v, mp.dO, k);
 }
 
 template <int D>
@@ -566,7 +570,9 @@ cudaError_t backward_d(const AttnArgs& a, cudaStream_t st) {
   Maps mp;
   if (!make_maps(a, mp, true)) return cudaErrorInvalidValue;
   const int rows = a.s * a.batch;
-  attn_dsum_kernel<<<(rows * a.heads + 7) / 8, 256, 0, st>>>(a.o, a.dO, a.dsum, a.s, a.heads, a.d, a.h, rows);
+  cudaError_t e = launch_pdl(attn_dsum_kernel, dim3((rows * a.heads + 7) / 8), dim3(256), 0, st, 1, a.o, a.dO,
+                             a.dsum, a.s, a.heads, a.d, a.h, rows);
+  if (e != cudaSuccess) return e;
   KArgs k{};
   k.s = a.s;
   k.heads = a.heads;
@@ -588,11 +594,11 @@ cudaError_t backward_d(const AttnArgs& a, cudaStream_t st) {
   }
   dim3 grid(a.heads * a.batch, k.ntiles);  // z fastest: all heads' longest tiles go first
   k.col0 = 0;  // dQ -> Q block
-  attn_row_kernel<D, M_DQ><<<grid, NT, s2, st>>>(mp.q, mp.k, mp.v, mp.dO, k);
+  e = launch_pdl(attn_row_kernel<D, M_DQ>, grid, dim3(NT), s2, st, 1, mp.q, mp.k, mp.v, mp.dO, k);
+  if (e != cudaSuccess) return e;
   k.col0 = a.h;      // dK -> K block
   k.col1 = 2 * a.h;  // dV -> V block
-  attn_col_kernel<D><<<grid, NT, s3, st>>>(mp.q, mp.k, mp.v, mp.dO, k);
-  return cudaGetLastError();
+  return launch_pdl(attn_col_kernel<D>, grid, dim3(NT), s3, st, 1, mp.q, mp.k, mp.v, mp.dO, k);
 }
 
 }  // namespace

@@ -18,6 +18,7 @@
 #include <string>
 
 #include "gemm.cuh"
+#include "launch.cuh"
 #include "ptx.cuh"
 
 namespace slip {
@@ -25,8 +26,9 @@ namespace {
 
 constexpr int BM = 128;
 constexpr int BK = 64;
-constexpr int NUM_THREADS = 256;
 constexpr int EPI_WARP0 = 4;
+constexpr int EPI_WARPS = 8;  // two per TMEM lane quarter, splitting the accumulator columns
+constexpr int NUM_THREADS = 32 * (EPI_WARP0 + EPI_WARPS);
 
 template <int BN, bool A_MN, bool B_MN, bool PAIR = false>
 struct Cfg {
@@ -45,7 +47,7 @@ struct Cfg {
                                    : 2 * ACC_COLS <= 128 ? 128
                                    : 2 * ACC_COLS <= 256 ? 256
                                                          : 512;
-  static constexpr int EPI_BYTES = 4 * 32 * 128;  // one 32x32 fp32 staging tile per epilogue warp
+  static constexpr int EPI_BYTES = EPI_WARPS * 32 * 128;  // one 32x32 fp32 staging tile per epilogue warp
   static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + EPI_BYTES + 1024 + 1024;
   static constexpr uint32_t IDESC = ptx::idesc_bf16_f32(TILE_M, BN, A_MN, B_MN);
   static constexpr uint32_t A_KSTEP = A_MN ? 2048 : 32;  // bytes per UMMA_K = 16
@@ -188,7 +190,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     }
     for (int a = 0; a < 2; ++a) {
       ptx::mbar_init(&tfull[a], 1);
-      ptx::mbar_init(&tempty[a], PAIR ? 8 : 4);
+      ptx::mbar_init(&tempty[a], PAIR ? 2 * EPI_WARPS : EPI_WARPS);
     }
     ptx::fence_mbar_init();
   }
@@ -206,6 +208,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   else __syncthreads();
   ptx::tc_fence_after();
   const uint32_t tmem_base = *tmem_holder;
+  ptx::grid_dep_wait();  // prologue above overlapped the previous kernel (PDL)
 
   if (warp == 0) {
     if (lane == 0) {
@@ -302,7 +305,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     }
   } else if (warp >= EPI_WARP0) {
     // ------------------------------------------------------------------ epilogue
-    const int ew = warp - EPI_WARP0;  // == warp % 4: TMEM lanes 32*ew .. 32*ew+31
+    const int ew = warp - EPI_WARP0;
+    const int lq = ew & 3;    // == warp % 4: TMEM lanes 32*lq .. 32*lq+31
+    const int half = ew >> 2;  // this warp drains the 32-column chunks half, half+2, ...
     float* buf = epi + ew * 32 * 32;
     int acc = 0;
     uint32_t acc_phase = 0;
@@ -311,12 +316,12 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       const CUtensorMap* mC = tl.g >= 0 ? &p.groups[tl.g].tc : &tmC;
       ptx::mbar_wait(&tfull[acc], acc_phase);
       ptx::tc_fence_after();
-      const int row0 = tl.m0 + cta * BM + ew * 32;
+      const int row0 = tl.m0 + cta * BM + lq * 32;
       const int m = row0 + lane;
 #pragma unroll 1
-      for (int ch = 0; ch < C::ACC_COLS / 32; ++ch) {
+      for (int ch = half; ch < C::ACC_COLS / 32; ch += 2) {
         uint32_t r[32];
-        ptx::tmem_ld_32x32b_x32(tmem_base + (static_cast<uint32_t>(ew * 32) << 16) + acc * C::ACC_COLS + ch * 32, r);
+        ptx::tmem_ld_32x32b_x32(tmem_base + (static_cast<uint32_t>(lq * 32) << 16) + acc * C::ACC_COLS + ch * 32, r);
         ptx::tmem_ld_wait();
         const int n = tl.n0 + ch * 32;
         if (n >= tl.N || row0 >= tl.M) continue;
@@ -497,21 +502,7 @@ cudaError_t launch_kernel(const CUtensorMap& ta, const CUtensorMap& tb, const CU
   if (p.total == 0) return cudaSuccess;
   const int units = PAIR ? num_sms() / 2 : num_sms();
   const int grid = (p.total < units ? p.total : units) * (PAIR ? 2 : 1);
-  cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(grid);
-  cfg.blockDim = dim3(NUM_THREADS);
-  cfg.dynamicSmemBytes = C::SMEM_BYTES;
-  cfg.stream = s;
-  cudaLaunchAttribute attr[1];
-  if (PAIR) {
-    attr[0].id = cudaLaunchAttributeClusterDimension;
-    attr[0].val.clusterDim.x = 2;
-    attr[0].val.clusterDim.y = 1;
-    attr[0].val.clusterDim.z = 1;
-    cfg.attrs = attr;
-    cfg.numAttrs = 1;
-  }
-  return cudaLaunchKernelEx(&cfg, kern, ta, tb, tc, p);
+  return launch_pdl(kern, dim3(grid), dim3(NUM_THREADS), C::SMEM_BYTES, s, PAIR ? 2 : 1, ta, tb, tc, p);
 }
 
 template <int BN, bool A_MN, bool B_MN, bool PAIR = false>

@@ -1,6 +1,6 @@
-// kernels.cu — HBM-bound kernels of the stage step: LayerNorm fwd/bwd, causal softmax
-// fwd/bwd, deterministic column reductions (bias / gamma / beta gradients), MSE head,
-// fused AdamW, RNE weight refresh and the counter-based input generator.
+// kernels.cu — HBM-bound kernels of the stage step: LayerNorm fwd/bwd, deterministic
+// column reductions (bias / gamma / beta gradients), MSE head, fused AdamW, RNE weight
+// refresh and the counter-based input generator.  All launched with PDL (launch.cuh).
 //
 // Design rules (B200): 16-byte vectors along the contiguous dimension; one thread block
 // per row for the row kernels (high occupancy, short per-thread register arrays);
@@ -9,6 +9,8 @@
 #include <cmath>
 
 #include "kernels.cuh"
+#include "launch.cuh"
+#include "ptx.cuh"
 
 namespace slip {
 namespace {
@@ -16,11 +18,6 @@ namespace {
 __device__ __forceinline__ float warp_sum(float v) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-  return v;
-}
-__device__ __forceinline__ float warp_max(float v) {
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
   return v;
 }
 // Block-wide sum of two values (blockDim.x multiple of 32, <= 1024); result broadcast.
@@ -39,21 +36,6 @@ __device__ __forceinline__ float2 block_sum2(float a, float b, float2* red) {
   __syncthreads();
   const float2 r = red[32];
   __syncthreads();  // red reusable by the caller
-  return r;
-}
-__device__ __forceinline__ float block_max(float a, float2* red) {
-  a = warp_max(a);
-  const int w = threadIdx.x >> 5, l = threadIdx.x & 31, nw = blockDim.x >> 5;
-  if (l == 0) red[w].x = a;
-  __syncthreads();
-  if (w == 0) {
-    float v = l < nw ? red[l].x : -INFINITY;
-    v = warp_max(v);
-    if (l == 0) red[32].x = v;
-  }
-  __syncthreads();
-  const float r = red[32].x;
-  __syncthreads();
   return r;
 }
 __device__ __forceinline__ void unpack8(const uint4& u, float (&f)[8]) {
@@ -89,6 +71,7 @@ __global__ void __launch_bounds__(512) ln_fwd_kernel(const bf16* __restrict__ x,
                                                      float* __restrict__ mean, float* __restrict__ rstd, int h,
                                                      float eps) {
   __shared__ float2 red[33];
+  ptx::grid_dep_wait();
   const int row = blockIdx.x;
   const int nv = h >> 3;
   const uint4* xr = reinterpret_cast<const uint4*>(x + static_cast<size_t>(row) * h);
@@ -143,6 +126,7 @@ __global__ void __launch_bounds__(512) ln_bwd_rows_kernel(const bf16* __restrict
                                                           const bf16* __restrict__ gamma,
                                                           const bf16* __restrict__ resid, bf16* dx, int h) {
   __shared__ float2 red[33];
+  ptx::grid_dep_wait();
   const int row = blockIdx.x;
   const int nv = h >> 3;
   const float mu = mean[row], rs = rstd[row];
@@ -206,6 +190,7 @@ __global__ void __launch_bounds__(256) colred_kernel(const bf16* __restrict__ a,
   constexpr int NO = MODE == 0 ? 1 : (MODE == 1 ? 2 : 3);  // outputs
   __shared__ float red[NO][8][257];
   __shared__ bool last;
+  ptx::grid_dep_wait();
   const int cv = threadIdx.x & 31;
   const int rg = threadIdx.x >> 5;
   const int col = (blockIdx.x * 32 + cv) * 8;
@@ -280,102 +265,12 @@ __global__ void __launch_bounds__(256) colred_kernel(const bf16* __restrict__ a,
   if (threadIdx.x == 0) tickets[blockIdx.x] = 0u;
 }
 
-// ------------------------------------------------------------------ causal softmax
-// One block (128 threads) per row; thread i owns float4 columns 4i + 512j.  Row t uses
-// columns 0..t; the bf16 output is written up to E = ceil128(t+1) (zeros past t) so the
-// causal-tile GEMMs that consume it never read unwritten memory.
-template <int VPT>
-__global__ void __launch_bounds__(128) softmax_fwd_kernel(const float* __restrict__ S, bf16* __restrict__ P, int s) {
-  __shared__ float2 red[33];
-  const int r = blockIdx.x;
-  const int t = r % s;
-  const int E = min(s, ((t + 1 + 127) / 128) * 128);
-  const float* sr = S + static_cast<size_t>(r) * s;
-  const float L2E = 1.4426950408889634f;
-  float v[VPT][4];
-  float mx = -INFINITY;
-#pragma unroll
-  for (int i = 0; i < VPT; ++i) {
-    const int c = 4 * threadIdx.x + 512 * i;
-    if (c < E) {
-      const float4 q = __ldcs(reinterpret_cast<const float4*>(sr + c));
-      v[i][0] = (c + 0 <= t) ? q.x : -INFINITY;
-      v[i][1] = (c + 1 <= t) ? q.y : -INFINITY;
-      v[i][2] = (c + 2 <= t) ? q.z : -INFINITY;
-      v[i][3] = (c + 3 <= t) ? q.w : -INFINITY;
-#pragma unroll
-      for (int e = 0; e < 4; ++e) mx = fmaxf(mx, v[i][e]);
-    }
-  }
-  mx = block_max(mx, red);
-  float sum = 0.f;
-#pragma unroll
-  for (int i = 0; i < VPT; ++i) {
-    if (4 * static_cast<int>(threadIdx.x) + 512 * i < E) {
-#pragma unroll
-      for (int e = 0; e < 4; ++e) {
-        v[i][e] = exp2f((v[i][e] - mx) * L2E);
-        sum += v[i][e];
-      }
-    }
-  }
-  const float inv = 1.0f / block_sum2(sum, 0.f, red).x;
-  bf16* pr = P + static_cast<size_t>(r) * s;
-#pragma unroll
-  for (int i = 0; i < VPT; ++i) {
-    const int c = 4 * threadIdx.x + 512 * i;
-    if (c < E) *reinterpret_cast<uint2*>(pr + c) = pack4(v[i][0] * inv, v[i][1] * inv, v[i][2] * inv, v[i][3] * inv);
-  }
-}
-
-template <int VPT>
-__global__ void __launch_bounds__(128) softmax_bwd_kernel(const float* __restrict__ dP, const bf16* __restrict__ P,
-                                                          bf16* __restrict__ dS, int s, float scale) {
-  __shared__ float2 red[33];
-  const int r = blockIdx.x;
-  const int t = r % s;
-  const int E = min(s, ((t + 1 + 127) / 128) * 128);
-  const float* dr = dP + static_cast<size_t>(r) * s;
-  const bf16* pr = P + static_cast<size_t>(r) * s;
-  float pv[VPT][4], dv[VPT][4];
-  float dot = 0.f;
-#pragma unroll
-  for (int i = 0; i < VPT; ++i) {
-    const int c = 4 * threadIdx.x + 512 * i;
-    if (c < E) {
-      const float4 q = __ldcs(reinterpret_cast<const float4*>(dr + c));
-      const uint2 u = *reinterpret_cast<const uint2*>(pr + c);
-      const float2 a = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&u.x));
-      const float2 b = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&u.y));
-      pv[i][0] = (c + 0 <= t) ? a.x : 0.f;
-      pv[i][1] = (c + 1 <= t) ? a.y : 0.f;
-      pv[i][2] = (c + 2 <= t) ? b.x : 0.f;
-      pv[i][3] = (c + 3 <= t) ? b.y : 0.f;
-      dv[i][0] = q.x;
-      dv[i][1] = q.y;
-      dv[i][2] = q.z;
-      dv[i][3] = q.w;
-#pragma unroll
-      for (int e = 0; e < 4; ++e) dot += pv[i][e] * dv[i][e];
-    }
-  }
-  dot = block_sum2(dot, 0.f, red).x;
-  bf16* sr = dS + static_cast<size_t>(r) * s;
-#pragma unroll
-  for (int i = 0; i < VPT; ++i) {
-    const int c = 4 * threadIdx.x + 512 * i;
-    if (c < E)
-      *reinterpret_cast<uint2*>(sr + c) =
-          pack4(scale * pv[i][0] * (dv[i][0] - dot), scale * pv[i][1] * (dv[i][1] - dot),
-                scale * pv[i][2] * (dv[i][2] - dot), scale * pv[i][3] * (dv[i][3] - dot));
-  }
-}
-
 // ------------------------------------------------------------------ MSE head
 __global__ void __launch_bounds__(256) mse_kernel(const bf16* __restrict__ y, const bf16* __restrict__ r,
                                                   bf16* __restrict__ dy, float* __restrict__ part, int64_t n8,
                                                   float inv_n) {
   __shared__ float red[8];
+  ptx::grid_dep_wait();
   float acc = 0.f;
   for (int64_t i = blockIdx.x * 256LL + threadIdx.x; i < n8; i += static_cast<int64_t>(gridDim.x) * 256) {
     float a[8], b[8], d[8];
@@ -401,6 +296,7 @@ __global__ void __launch_bounds__(256) mse_kernel(const bf16* __restrict__ y, co
 
 __global__ void mse_finalize_kernel(const float* __restrict__ part, int nparts, float* __restrict__ loss,
                                     float half_inv_n) {
+  ptx::grid_dep_wait();
   if (threadIdx.x != 0 || blockIdx.x != 0) return;
   float s = 0.f;
   for (int i = 0; i < nparts; ++i) s += part[i];
@@ -417,6 +313,7 @@ __global__ void __launch_bounds__(256) adamw_kernel(float* __restrict__ p, float
                                                     bf16* __restrict__ w, int64_t n4, int64_t per_layer, WdRanges wr,
                                                     float lr, float b1, float b2, float eps, float wd, float inv_bc1,
                                                     float inv_bc2, float grad_scale, int32_t* __restrict__ nonfinite) {
+  ptx::grid_dep_wait();
   bool bad = false;
   for (int64_t i = blockIdx.x * 256LL + threadIdx.x; i < n4; i += static_cast<int64_t>(gridDim.x) * 256) {
     const int64_t e0 = 4 * i;
@@ -451,6 +348,7 @@ __global__ void __launch_bounds__(256) adamw_kernel(float* __restrict__ p, float
 }
 
 __global__ void f32_to_bf16_kernel(const float* __restrict__ src, bf16* __restrict__ dst, int64_t n4) {
+  ptx::grid_dep_wait();
   for (int64_t i = blockIdx.x * 256LL + threadIdx.x; i < n4; i += static_cast<int64_t>(gridDim.x) * 256) {
     const float4 a = reinterpret_cast<const float4*>(src)[i];
     reinterpret_cast<uint2*>(dst)[i] = pack4(a.x, a.y, a.z, a.w);
@@ -471,6 +369,7 @@ __device__ __forceinline__ uint4 philox(uint4 c, uint2 k) {
 }
 
 __global__ void synth_normal_kernel(bf16* __restrict__ out, int64_t n, uint2 key, uint32_t kk, uint32_t jj) {
+  ptx::grid_dep_wait();
   for (int64_t i = blockIdx.x * 256LL + threadIdx.x; 4 * i < n; i += static_cast<int64_t>(gridDim.x) * 256) {
     const uint4 r = philox(make_uint4(static_cast<uint32_t>(i), static_cast<uint32_t>(i >> 32), jj, kk), key);
     const float u1 = (static_cast<float>(r.x) + 1.0f) * 2.3283064365386963e-10f;
@@ -513,9 +412,8 @@ cudaError_t ln_fwd(const bf16* x, const bf16* gamma, const bf16* beta, bf16* y, 
   if (h % 8 || h > 8192) return cudaErrorInvalidValue;
   int nt, vpt;
   ln_shape(h, &nt, &vpt);
-  if (vpt == 1) ln_fwd_kernel<1><<<T, nt, 0, s>>>(x, gamma, beta, y, mean, rstd, h, eps);
-  else ln_fwd_kernel<2><<<T, nt, 0, s>>>(x, gamma, beta, y, mean, rstd, h, eps);
-  return cudaGetLastError();
+  return launch_pdl(vpt == 1 ? ln_fwd_kernel<1> : ln_fwd_kernel<2>, dim3(T), dim3(nt), 0, s, 1, x, gamma, beta, y,
+                    mean, rstd, h, eps);
 }
 
 cudaError_t ln_bwd(const bf16* dy, const bf16* x, const float* mean, const float* rstd, const bf16* gamma,
@@ -526,52 +424,37 @@ cudaError_t ln_bwd(const bf16* dy, const bf16* x, const float* mean, const float
   if (dx) {
     int nt, vpt;
     ln_shape(h, &nt, &vpt);
-    if (vpt == 1) ln_bwd_rows_kernel<1><<<T, nt, 0, s>>>(dy, x, mean, rstd, gamma, resid, dx, h);
-    else ln_bwd_rows_kernel<2><<<T, nt, 0, s>>>(dy, x, mean, rstd, gamma, resid, dx, h);
+    cudaError_t e = launch_pdl(vpt == 1 ? ln_bwd_rows_kernel<1> : ln_bwd_rows_kernel<2>, dim3(T), dim3(nt), 0, s, 1,
+                               dy, x, mean, rstd, gamma, resid, dx, h);
+    if (e != cudaSuccess) return e;
   }
   dim3 grid((h + 255) / 256, kRedChunks);
   if (dx && dxsum)
-    colred_kernel<2><<<grid, 256, 0, s>>>(dy, h, x, mean, rstd, dx, T, h, part, dgamma, dbeta, dxsum, accumulate,
-                                          tickets);
-  else
-    colred_kernel<1><<<grid, 256, 0, s>>>(dy, h, x, mean, rstd, nullptr, T, h, part, dgamma, dbeta, nullptr,
-                                          accumulate, tickets);
-  return cudaGetLastError();
+    return launch_pdl(colred_kernel<2>, grid, dim3(256), 0, s, 1, dy, static_cast<int64_t>(h), x, mean, rstd,
+                      static_cast<const bf16*>(dx), T, h, part, dgamma, dbeta, dxsum, accumulate, tickets);
+  return launch_pdl(colred_kernel<1>, grid, dim3(256), 0, s, 1, dy, static_cast<int64_t>(h), x, mean, rstd,
+                    static_cast<const bf16*>(nullptr), T, h, part, dgamma, dbeta, static_cast<float*>(nullptr),
+                    accumulate, tickets);
 }
 
 cudaError_t colsum(const bf16* a, int T, int N, int64_t ld, float* out, int accumulate, float* part,
                    unsigned* tickets, cudaStream_t s) {
   if (N % 8 || ld % 8 || (N + 255) / 256 > kTickets) return cudaErrorInvalidValue;
   dim3 grid((N + 255) / 256, kRedChunks);
-  colred_kernel<0><<<grid, 256, 0, s>>>(a, ld, nullptr, nullptr, nullptr, nullptr, T, N, part, out, nullptr, nullptr,
-                                        accumulate, tickets);
-  return cudaGetLastError();
-}
-
-cudaError_t softmax_fwd(const float* S, bf16* P, int z, int s, cudaStream_t st) {
-  if (s % 4 || s > 2048) return cudaErrorInvalidValue;
-  const int rows = z * s, vpt = (s + 511) / 512;
-  if (vpt == 1) softmax_fwd_kernel<1><<<rows, 128, 0, st>>>(S, P, s);
-  else if (vpt == 2) softmax_fwd_kernel<2><<<rows, 128, 0, st>>>(S, P, s);
-  else softmax_fwd_kernel<4><<<rows, 128, 0, st>>>(S, P, s);
-  return cudaGetLastError();
-}
-
-cudaError_t softmax_bwd(const float* dP, const bf16* P, bf16* dS, int z, int s, float scale, cudaStream_t st) {
-  if (s % 4 || s > 2048) return cudaErrorInvalidValue;
-  const int rows = z * s, vpt = (s + 511) / 512;
-  if (vpt == 1) softmax_bwd_kernel<1><<<rows, 128, 0, st>>>(dP, P, dS, s, scale);
-  else if (vpt == 2) softmax_bwd_kernel<2><<<rows, 128, 0, st>>>(dP, P, dS, s, scale);
-  else softmax_bwd_kernel<4><<<rows, 128, 0, st>>>(dP, P, dS, s, scale);
-  return cudaGetLastError();
+  return launch_pdl(colred_kernel<0>, grid, dim3(256), 0, s, 1, a, ld, static_cast<const bf16*>(nullptr),
+                    static_cast<const float*>(nullptr), static_cast<const float*>(nullptr),
+                    static_cast<const bf16*>(nullptr), T, N, part, out, static_cast<float*>(nullptr),
+                    static_cast<float*>(nullptr), accumulate, tickets);
 }
 
 cudaError_t mse_loss(const bf16* y, const bf16* r, bf16* dy, float* part, int nparts, float* loss, int64_t n,
                      cudaStream_t s) {
   if (n % 8) return cudaErrorInvalidValue;
-  mse_kernel<<<nparts, 256, 0, s>>>(y, r, dy, part, n / 8, 1.0f / static_cast<float>(n));
-  mse_finalize_kernel<<<1, 32, 0, s>>>(part, nparts, loss, 0.5f / static_cast<float>(n));
-  return cudaGetLastError();
+  cudaError_t e = launch_pdl(mse_kernel, dim3(nparts), dim3(256), 0, s, 1, y, r, dy, part, n / 8,
+                             1.0f / static_cast<float>(n));
+  if (e != cudaSuccess) return e;
+  return launch_pdl(mse_finalize_kernel, dim3(1), dim3(32), 0, s, 1, static_cast<const float*>(part), nparts, loss,
+                    0.5f / static_cast<float>(n));
 }
 
 cudaError_t adamw(float* p, float* m, float* v, const float* g, bf16* w, int64_t n, int64_t per_layer, int h, int f,
@@ -588,22 +471,19 @@ cudaError_t adamw(float* p, float* m, float* v, const float* g, bf16* w, int64_t
   wr.c1 = wr.c0 + F * H;
   wr.d0 = wr.c1 + F;
   wr.d1 = wr.d0 + H * F;
-  adamw_kernel<<<grid_for(n / 4), 256, 0, s>>>(p, m, v, g, w, n / 4, per_layer, wr, lr, b1, b2, eps, wd, 1.0f / bc1,
-                                               1.0f / bc2, grad_scale, nonfinite);
-  return cudaGetLastError();
+  return launch_pdl(adamw_kernel, dim3(grid_for(n / 4)), dim3(256), 0, s, 1, p, m, v, g, w, n / 4, per_layer, wr, lr,
+                    b1, b2, eps, wd, 1.0f / bc1, 1.0f / bc2, grad_scale, nonfinite);
 }
 
 cudaError_t f32_to_bf16(const float* src, bf16* dst, int64_t n, cudaStream_t s) {
   if (n % 4) return cudaErrorInvalidValue;
-  f32_to_bf16_kernel<<<grid_for(n / 4), 256, 0, s>>>(src, dst, n / 4);
-  return cudaGetLastError();
+  return launch_pdl(f32_to_bf16_kernel, dim3(grid_for(n / 4)), dim3(256), 0, s, 1, src, dst, n / 4);
 }
 
 cudaError_t synth_normal(bf16* out, int64_t n, uint64_t seed, uint64_t k, uint64_t j, cudaStream_t s) {
   uint2 key = make_uint2(static_cast<uint32_t>(seed), static_cast<uint32_t>(seed >> 32));
-  synth_normal_kernel<<<grid_for((n + 3) / 4), 256, 0, s>>>(out, n, key, static_cast<uint32_t>(k),
-                                                            static_cast<uint32_t>(j));
-  return cudaGetLastError();
+  return launch_pdl(synth_normal_kernel, dim3(grid_for((n + 3) / 4)), dim3(256), 0, s, 1, out, n, key,
+                    static_cast<uint32_t>(k), static_cast<uint32_t>(j));
 }
 
 }  // namespace slip

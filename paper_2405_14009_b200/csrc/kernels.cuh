@@ -30,13 +30,6 @@ cudaError_t ln_bwd(const bf16* dy, const bf16* x, const float* mean, const float
 cudaError_t colsum(const bf16* a, int T, int N, int64_t ld, float* out, int accumulate, float* part,
                    unsigned* tickets, cudaStream_t s);
 
-// Causal softmax over rows of S [z, s, s] fp32 (row t uses columns 0..t):
-// P[z, t, u] = softmax for u <= t, 0 for t < u < ceil128(t+1).
-cudaError_t softmax_fwd(const float* S, bf16* P, int z, int s, cudaStream_t s_);
-
-// dS = scale * P (dP - rowsum(dP P)) on the same causal extents.
-cudaError_t softmax_bwd(const float* dP, const bf16* P, bf16* dS, int z, int s, float scale, cudaStream_t s_);
-
 // MSE head: dy = (y - r)/n (bf16), loss partials per block; loss = 0.5*sum/n.
 cudaError_t mse_loss(const bf16* y, const bf16* r, bf16* dy, float* part, int nparts, float* loss, int64_t n,
                      cudaStream_t s);

@@ -48,15 +48,18 @@ def main():
     else:
         scenarios = [[tuple(int(v) for v in f.split(",")) for f in s.split(";")] for s in a.failures.split("/")]
     costs = rt.make_costs(t_f=3, t_b=3, t_w=2, t_comm=1, t_ar=1, t_opt=1)
-    stage = rt.Stage(cfg, L, n_slots=2 * m * DP)
     comm = rt.Comm(rank, world)
     ok = True
+    holder = {}
 
     def run(live):
+        # a fresh stage per scenario: the AdamW step count is part of the training state,
+        # and a rank masked in an earlier scenario skipped that scenario's OPT
+        if "stage" in holder:
+            holder["stage"].close()
+        stage = holder["stage"] = rt.Stage(cfg, L, n_slots=2 * m * DP)
         rt.init_master_(stage.master, cfg, L, cfg.layers, seed=100 + me_i)
         rt.call("slip_weights_from_master", stage.ctx, rt._stream())
-        stage.adam_m.zero_()
-        stage.adam_v.zero_()
         comm.setup(PP, DP, m, live)
         losses = torch.zeros(DP * m, dtype=torch.float32).pin_memory()
         g = torch.Generator().manual_seed(5)
@@ -120,7 +123,7 @@ def main():
                               "period_ms": rep.period_ms, "fault_free_period_ms": rep0.period_ms}), flush=True)
         ok = ok and flag.item() == 1.0
     comm.close()
-    stage.close()
+    holder["stage"].close()
     dist.destroy_process_group()
     sys.exit(0 if ok else 1)
 
