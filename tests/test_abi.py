@@ -54,8 +54,9 @@ def test_sizes_and_errors_without_gpu():
     assert lib.slip_param_count(C.byref(m), 24, C.byref(n)) == 0
     assert n.value == 24 * (12 * 2048 * 2048 + 13 * 2048)
     sz = C.c_size_t(0)
-    assert lib.slip_stash_bytes(C.byref(m), 1, 1, C.byref(sz)) == 0 and sz.value > 300e6
-    assert lib.slip_workspace_bytes(C.byref(m), C.byref(sz)) == 0 and sz.value > 16 * 2048 * 2048 * 4
+    # per layer-slot: ~13 [T,h]-sized bf16 tensors (+ 4h-wide ones); no [s,s] attention matrices
+    assert lib.slip_stash_bytes(C.byref(m), 1, 1, C.byref(sz)) == 0 and 200e6 < sz.value < 260e6
+    assert lib.slip_workspace_bytes(C.byref(m), C.byref(sz)) == 0 and sz.value > 3 * 2048 * 2048 * 2
     bad = b.slip_model(2048, 7, 8192, 2048, 1, 1e-5)
     assert lib.slip_param_count(C.byref(bad), 1, C.byref(n)) == 1
     assert b"heads" in lib.slip_last_error()
