@@ -48,6 +48,7 @@ def parse():
     ap.add_argument("--m", type=int, default=0, help="micro-batches per pipeline (default 4*PP)")
     ap.add_argument("--layers", type=int, default=LAYERS)
     ap.add_argument("--coupled", action="store_true", help="coupled backward, no staggering (1F1B baseline)")
+    ap.add_argument("--no-stagger", action="store_true", help="decoupled B/W but a global optimizer barrier")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     return ap.parse_args()
@@ -206,7 +207,11 @@ def main():
             print(json.dumps({"metric": METRIC, "value": None, "unit": "tokens/s", "n_gpus": world,
                               "error": "unrecoverable failure set %s (a stage lost every worker)" % failed}))
         return
-    decoupled, staggered = (not args.coupled), (not args.coupled)
+    decoupled = not args.coupled
+    staggered = not (args.coupled or args.no_stagger)
+    plan_name = ("coupled 1F1B" if args.coupled else
+                 "decoupled B/W, global optimizer barrier" if args.no_stagger else
+                 "decoupled B/W + staggered AdamW")
     # nominal integer costs ~ FLOP ratios of F : B : W, refined by profiling below
     costs = rt.make_costs(t_f=108, t_b=117, t_w=100, t_comm=1, t_ar=10, t_opt=10)
     # slots = max in-flight micro-batches (F started, W not finished) of any worker in the plan
@@ -337,7 +342,7 @@ def main():
         "config": {"workload": "gpt-1.3B-shape (h2048, 16 heads, ffn 8192, s2048, b1) %d layers, DP%dxPP%d, "
                                "m=%d micro-batches/pipeline, %s, failures=%d" % (
                                    args.layers, DP, PP, m,
-                                   "coupled 1F1B" if args.coupled else "decoupled B/W + staggered AdamW",
+                                   plan_name,
                                    args.failures),
                    "model": "gpt-1.3b-shape", "global_batch": DP * m * MB, "seq_len": SEQ,
                    "parallelism": "dp%dxpp%d" % (DP, PP), "failed_workers": failed,
