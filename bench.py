@@ -49,6 +49,10 @@ def parse():
     ap.add_argument("--layers", type=int, default=LAYERS)
     ap.add_argument("--coupled", action="store_true", help="coupled backward, no staggering (1F1B baseline)")
     ap.add_argument("--no-stagger", action="store_true", help="decoupled B/W but a global optimizer barrier")
+    ap.add_argument("--failed-at", default="",
+                    help="actual failed workers 'i,k;i,k' (un-normalized); with --normalize they are migrated")
+    ap.add_argument("--normalize", action="store_true",
+                    help="Algorithm 1 + P2P migration swaps before the timed steps (needs --failed-at)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     return ap.parse_args()
@@ -197,8 +201,11 @@ def main():
     m = args.m or 4 * PP
     cfg = sd.ModelCfg(hidden=H, heads=HEADS, ffn=FFN, seq=SEQ, micro_batch=MB, layers=args.layers)
     T = cfg.tokens
-    # failures at normalized positions: last stages, distinct peer groups (R20)
+    # failures at normalized positions: last stages, distinct peer groups (R20),
+    # or the actual (un-normalized) set given by --failed-at
     failed = [(PP - 1 - q, (q + 1) % DP) for q in range(args.failures)]
+    if args.failed_at:
+        failed = [tuple(int(v) for v in f.split(",")) for f in args.failed_at.split(";")]
     live = [[1] * DP for _ in range(PP)]
     for (i, k) in failed:
         live[i][k] = 0
@@ -214,17 +221,32 @@ def main():
                  "decoupled B/W + staggered AdamW")
     # nominal integer costs ~ FLOP ratios of F : B : W, refined by profiling below
     costs = rt.make_costs(t_f=108, t_b=117, t_w=100, t_comm=1, t_ar=10, t_opt=10)
-    # slots = max in-flight micro-batches (F started, W not finished) of any worker in the plan
-    plan = rt.plan_schedule(PP, DP, m, live, costs, decoupled, staggered, horizon=2)
-    n_slots = 1
-    for i in range(PP):
-        for k in range(DP):
-            cur = mx = 0
-            for o in sorted((o for o in plan.ops if o[0] == i and o[4] == k and o[3] in (0, 2, 3)),
-                            key=lambda o: o[6]):
-                cur += 1 if o[3] == 0 else -1
-                mx = max(mx, cur)
-            n_slots = max(n_slots, mx)
+    def slots_for(lv, cs):
+        """max in-flight micro-batches (F started, W not finished) of any worker in the plan"""
+        plan = rt.plan_schedule(PP, DP, m, lv, cs, decoupled, staggered, horizon=2)
+        n = 1
+        for i in range(PP):
+            for k in range(DP):
+                cur = mx = 0
+                for o in sorted((o for o in plan.ops if o[0] == i and o[4] == k and o[3] in (0, 2, 3)),
+                                key=lambda o: o[6]):
+                    cur += 1 if o[3] == 0 else -1
+                    mx = max(mx, cur)
+                n = max(n, mx)
+        return n
+
+    def normalization(cs):
+        """Phase 1 of the Planner (§4.2.1): R from Algorithm 1 over the heuristic
+        cost table, then the minimum swaps from the actual failure set to R."""
+        F = len(failed)
+        tab = rt.normalize_costs(PP, DP, m, cs, F, decoupled, staggered)
+        R, _ = rt.normalize(PP, DP, F, tab)
+        swaps, after = rt.migration_plan(PP, DP, live, R)
+        return R, swaps, after, tab
+
+    n_slots = slots_for(live, costs)
+    if args.normalize:
+        n_slots = max(n_slots, slots_for(normalization(costs)[2], costs))
     stage = rt.Stage(cfg, L, n_slots)
     rt.init_master_(stage.master, cfg, L, args.layers, seed=rank % PP)
     rt.call("slip_weights_from_master", stage.ctx, rt._stream())
@@ -257,6 +279,38 @@ def main():
     q = lambda ms: max(1, int(round(ms * 100)))  # noqa: E731
     costs = rt.make_costs(t_f=q(per[0]), t_b=q(per[1] or per[3]), t_w=q(per[2] or 0.01), t_comm=1,
                           t_ar=q(per[4] * 0.5 if per[4] else 0.01), t_opt=q(per[4] or 0.01))
+    norm = None
+    if args.normalize and failed:
+        # Normalization with the profiled costs, then one P2P state copy per swap (PAPER.md
+        # lines 377-379): the GPU at the target position takes over the failed worker's role
+        R, swaps, after, tab = normalization(costs)
+        if slots_for(after, costs) > n_slots:
+            raise SystemExit("normalized plan needs more slots than allocated")
+        role = list(range(world))
+        barrier()
+        g0, g1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        g0.record(stream)
+        for (fi, fk), (ti, tk), src in swaps:
+            w_f, w_t, w_s = rt.rank_of(PP, fi, fk), rt.rank_of(PP, ti, tk), rt.rank_of(PP, fi, src)
+            # process playing the source role sends to the process playing the target role
+            p_s, p_t, p_f = role.index(w_s), role.index(w_t), role.index(w_f)
+            if rank == p_s:
+                rt.migrate_state(stage, comm, p_t, True)
+            elif rank == p_t:
+                rt.migrate_state(stage, comm, p_s, False, opt_step=0)
+            role[p_t], role[p_f] = w_f, w_t
+        g1.record(stream)
+        barrier()
+        mig_ms = allreduce_max(g0.elapsed_time(g1))
+        comm.set_role(role[rank])
+        live = after
+        comm.setup(PP, DP, m, live)
+        norm = {"actual_failed": failed, "R": R, "swaps": swaps, "migration_ms": mig_ms,
+                "state_bytes_per_swap": 12 * stage.n_params,
+                "migration_GBps": (12 * stage.n_params * len(swaps) / (mig_ms * 1e6)) if swaps and mig_ms else None,
+                "cost_table_10us": {"%d,%d" % ix: v for ix, v in tab.items()},
+                "normalized_failed": [(i, k) for i in range(PP) for k in range(DP) if not live[i][k]]}
+        failed = norm["normalized_failed"]
     # warm-up steps with the profiled plan
     execute(args.warmup)
     barrier()
@@ -343,7 +397,7 @@ def main():
                                "m=%d micro-batches/pipeline, %s, failures=%d" % (
                                    args.layers, DP, PP, m,
                                    plan_name,
-                                   args.failures),
+                                   len(failed)),
                    "model": "gpt-1.3b-shape", "global_batch": DP * m * MB, "seq_len": SEQ,
                    "parallelism": "dp%dxpp%d" % (DP, PP), "failed_workers": failed,
                    "l2": "inputs larger than L2 (2.4 GB bf16 weights + GBs of stash per step)"},
@@ -360,6 +414,8 @@ def main():
         "predicted_period_units": rep.predicted_period,
         "planner_costs_10us": [costs.t_f, costs.t_b, costs.t_w, costs.t_opt],
     }
+    if norm:
+        line["normalization"] = norm
     if cpu:
         line["cpu_baseline"] = cpu
     print(json.dumps(line), flush=True)

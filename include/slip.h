@@ -145,6 +145,45 @@ slip_status slip_plan_schedule(const slip_cluster* c, const slip_costs* costs, c
 /* FNV-1a 64 over the op fields (int64 little-endian, list order). */
 uint64_t slip_plan_hash(const slip_op* ops, int64_t n);
 
+/* ------------------------------------------------------- normalization (CPU)
+ * Phase 1 of the Planner, §4.2.1, Algorithm 1 (lines
+ * 391-414); bit-exact with oracle/normalize.py.  Readings R26-R29. */
+#define SLIP_COST_INF INT64_MAX
+
+/* The heuristic cost table: out_cost[i*(F+1) + x] = steady-state period of the
+ * plan (costs, opts) with x failures at stage i (pipelines DP-1, ..., DP-x)
+ * minus the fault-free period (reading R28), for 0 <= x <= min(F, DP-1);
+ * SLIP_COST_INF for x > DP-1.  Uses N, DP, m of c (c->live is ignored). */
+slip_status slip_normalize_costs(const slip_cluster* c, const slip_costs* costs, const slip_plan_opts* opts,
+                                 int32_t F, int64_t* out_cost);
+
+/* Algorithm 1 over a cost table cost[i*(F+1) + x] (host, N x (F+1); entries
+ * with x > DP-1 are not read): out_R[N] (host) gets R = A[N-1][F], sum F, each
+ * entry <= DP-1 (reading R26); out_C (host, N x (F+1), may be NULL) the table
+ * C with SLIP_COST_INF where no assignment exists.  Ties take the larger x at
+ * the later stage (reading R27).  SLIP_EUNRECOVERABLE if F > N (DP - 1). */
+slip_status slip_normalize(int32_t N, int32_t DP, int32_t F, const int64_t* cost, int64_t* out_C, int32_t* out_R);
+
+/* One concrete placement of R ("can be arbitrary"): stages
+ * from the last to the first, failure c (counted over all stages) at pipeline
+ * (DP-1-c) mod DP.  out_live (host, [N*DP]) as slip_cluster.live. */
+slip_status slip_normalized_live(int32_t N, int32_t DP, const int32_t* R, uint8_t* out_live);
+
+/* One swap: the live GPU at (target_stage, target_pipe) takes over the failed
+ * position (failed_stage, failed_pipe), receiving that stage's state from the
+ * live peer (failed_stage, source_pipe); the target position becomes the hole. */
+typedef struct {
+  int32_t failed_stage, failed_pipe, target_stage, target_pipe, source_pipe;
+} slip_swap;
+
+/* Minimum swaps (sum_i max(0, actual_i - R_i), reading R29) moving the failures
+ * of c->live to the per-stage counts R.  Writes at most cap swaps, *n_swaps the
+ * count (cap = 0 to size), out_live (host [N*DP], may be NULL) the live matrix
+ * after all swaps.  SLIP_EINVAL if sum R differs from the failure count,
+ * SLIP_EUNRECOVERABLE if c->live or R leaves a stage without a live worker. */
+slip_status slip_migration_plan(const slip_cluster* c, const int32_t* R, slip_swap* out, int32_t cap,
+                                int32_t* n_swaps, uint8_t* out_live);
+
 /* ------------------------------------------------------------------ sizes
  * Parameter layout (flat, per layer, row-major, layers consecutive):
  *   Wqkv[3h,h] bqkv[3h] Wo[h,h] bo[h] g1[h] b1n[h] g2[h] b2n[h]
@@ -248,6 +287,25 @@ slip_status slip_comm_create(slip_comm** out, int32_t rank, int32_t world, const
 slip_status slip_comm_setup(slip_comm* comm, const slip_cluster* c);
 slip_status slip_comm_destroy(slip_comm* comm);
 
+/* Worker position this process plays, as the role rank k*N + i of worker
+ * (stage i, pipeline k); default = its world rank.  After a normalization
+ * swap (slip_migration_plan) the GPU that sat at the target position plays the
+ * failed worker's role ("swap the location of two
+ * workers").  The roles of all processes must form a permutation; call before
+ * slip_comm_setup (it drops the current setup). */
+slip_status slip_comm_set_role(slip_comm* comm, int32_t role);
+
+/* The point-to-point copy of one normalization swap ("a
+ * point-to-point copy of model parameters"): the stage state the
+ * receiver needs to take over a role — fp32 master weights, AdamW m and v
+ * (3 x 4 B per parameter) — over the world communicator between WORLD ranks
+ * (send = 1 on the live peer of the failed worker's stage, send = 0 on the
+ * GPU taking over).  The receiver then rebuilds its bf16 weights from the
+ * master copy and sets its AdamW step count to opt_step (the coordinator's
+ * iteration count).  Both sides must call it; stream-ordered on s. */
+slip_status slip_migrate_state(slip_ctx* ctx, slip_comm* comm, int32_t peer, int32_t send, int64_t opt_step,
+                               slip_stream s);
+
 /* In-place fp32 sum of the stage gradient over the live peers of the caller's
  * stage ("all-reduce collective"; reading R13).  A
  * singleton group returns without communicating. */
@@ -265,8 +323,8 @@ typedef enum {
   SLIP_ACT_SEND_Y = 3,   /* ncclSend slot.dy (the activation) to rank `peer` */
   SLIP_ACT_LOSS = 4,     /* last stage: MSE head, target of (origin, mb); dy -> slot.dy */
   SLIP_ACT_RECV_DY = 5,  /* ncclRecv output gradient from rank `peer` into slot.dy (ReRouteGrad) */
-  SLIP_ACT_B = 6,        /* slip_backward_input(slot), dx -> slot.x (stage > 0) */
-  SLIP_ACT_SEND_DX = 7,  /* ncclSend slot.x (the input gradient) to rank `peer` */
+  SLIP_ACT_B = 6,        /* slip_backward_input(slot), dx -> slot.dx (stage > 0) */
+  SLIP_ACT_SEND_DX = 7,  /* ncclSend slot.dx (the input gradient) to rank `peer` */
   SLIP_ACT_W = 8,        /* slip_backward_weight(slot); slot released */
   SLIP_ACT_BC = 9,       /* coupled backward (B then W); slot released */
   SLIP_ACT_AR = 10,      /* stage DP all-reduce of iteration `iter` */

@@ -43,6 +43,11 @@ class slip_adam(C.Structure):
     _fields_ = [(n, C.c_float) for n in ("lr", "beta1", "beta2", "eps", "weight_decay")]
 
 
+class slip_swap(C.Structure):
+    _fields_ = [("failed_stage", C.c_int32), ("failed_pipe", C.c_int32), ("target_stage", C.c_int32),
+                ("target_pipe", C.c_int32), ("source_pipe", C.c_int32)]
+
+
 class slip_op(C.Structure):
     _fields_ = [("stage", C.c_int32), ("mb", C.c_int32), ("origin", C.c_int32), ("phase", C.c_int32),
                 ("exec", C.c_int32), ("iter", C.c_int32), ("start", C.c_int64), ("end", C.c_int64)]
@@ -88,6 +93,12 @@ SIGNATURES = {
     "slip_plan_schedule": (C.c_int, [C.POINTER(slip_cluster), C.POINTER(slip_costs), C.POINTER(slip_plan_opts),
                                      C.POINTER(slip_op), I64, C.POINTER(I64), C.POINTER(I64), C.POINTER(I64)]),
     "slip_plan_hash": (U64, [C.POINTER(slip_op), I64]),
+    "slip_normalize_costs": (C.c_int, [C.POINTER(slip_cluster), C.POINTER(slip_costs), C.POINTER(slip_plan_opts),
+                                       I32, C.POINTER(I64)]),
+    "slip_normalize": (C.c_int, [I32, I32, I32, C.POINTER(I64), C.POINTER(I64), C.POINTER(I32)]),
+    "slip_normalized_live": (C.c_int, [I32, I32, C.POINTER(I32), C.POINTER(C.c_uint8)]),
+    "slip_migration_plan": (C.c_int, [C.POINTER(slip_cluster), C.POINTER(I32), C.POINTER(slip_swap), I32,
+                                      C.POINTER(I32), C.POINTER(C.c_uint8)]),
     "slip_rank_program": (C.c_int, [C.POINTER(slip_cluster), C.POINTER(slip_costs), C.POINTER(slip_plan_opts), I32,
                                     C.POINTER(slip_action), I64, C.POINTER(I64), C.POINTER(I32)]),
     "slip_param_count": (C.c_int, [C.POINTER(slip_model), I32, C.POINTER(I64)]),
@@ -111,6 +122,8 @@ SIGNATURES = {
     "slip_comm_setup": (C.c_int, [P, C.POINTER(slip_cluster)]),
     "slip_comm_destroy": (C.c_int, [P]),
     "slip_grad_allreduce": (C.c_int, [P, P, P]),
+    "slip_comm_set_role": (C.c_int, [P, I32]),
+    "slip_migrate_state": (C.c_int, [P, P, I32, I32, I64, P]),
     "slip_execute_schedule": (C.c_int, [P, P, C.POINTER(slip_cluster), C.POINTER(slip_costs),
                                         C.POINTER(slip_plan_opts), C.POINTER(slip_adam), I32, I32, U64,
                                         C.POINTER(slip_io), P, C.POINTER(slip_report)]),

@@ -60,6 +60,7 @@ slip_status slip_comm_create(slip_comm** out, int32_t rank, int32_t world, const
   std::memcpy(&uid, id, 128);
   slip_comm* c = new slip_comm();
   c->rank = rank;
+  c->role = rank;
   c->world = world;
   ncclResult_t r = ncclCommInitRank(&c->world_comm, world, uid, rank);
   if (r != ncclSuccess) {
@@ -82,8 +83,8 @@ slip_status slip_comm_setup(slip_comm* c, const slip_cluster* cl) {
   }
   destroy_setup(c);
   c->cl = cc;
-  c->my_stage = c->rank % cc.N;
-  c->my_pipe = c->rank / cc.N;
+  c->my_stage = c->role % cc.N;
+  c->my_pipe = c->role / cc.N;
   c->my_live = cc.is_live(c->my_stage, c->my_pipe);
   SLIP_CUDA(cudaStreamCreateWithFlags(&c->ar_stream, cudaStreamNonBlocking));
   // stage communicator over the live peers (color = stage), failed ranks excluded
@@ -109,9 +110,9 @@ slip_status slip_comm_setup(slip_comm* c, const slip_cluster* cl) {
       }
   int color = 0;
   for (const auto& pr : pairs) {
-    const bool member = c->rank == pr.first || c->rank == pr.second;
+    const bool member = c->role == pr.first || c->role == pr.second;
     ncclComm_t pc = nullptr;
-    SLIP_NCCL(ncclCommSplit(c->world_comm, member ? color : NCCL_SPLIT_NOCOLOR, c->rank == pr.first ? 0 : 1, &pc,
+    SLIP_NCCL(ncclCommSplit(c->world_comm, member ? color : NCCL_SPLIT_NOCOLOR, c->role == pr.first ? 0 : 1, &pc,
                             nullptr));
     if (member) {
       c->pair_comm[pr] = pc;
@@ -130,6 +131,37 @@ slip_status slip_comm_destroy(slip_comm* c) {
   destroy_setup(c);
   if (c->world_comm) ncclCommDestroy(c->world_comm);
   delete c;
+  return SLIP_OK;
+}
+
+slip_status slip_comm_set_role(slip_comm* c, int32_t role) {
+  SLIP_CHECK(c && role >= 0 && role < c->world, SLIP_EINVAL, "comm_set_role: role out of range");
+  destroy_setup(c);
+  c->role = role;
+  return SLIP_OK;
+}
+
+slip_status slip_migrate_state(slip_ctx* ctx, slip_comm* c, int32_t peer, int32_t send, int64_t opt_step,
+                               slip_stream s) {
+  SLIP_CHECK(ctx && ctx->bound && c && c->world_comm, SLIP_EINVAL, "migrate_state: ctx not bound or comm missing");
+  SLIP_CHECK(peer >= 0 && peer < c->world && peer != c->rank, SLIP_EINVAL, "migrate_state: bad peer rank");
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(s);
+  const size_t n = static_cast<size_t>(ctx->n_params);
+  float* bufs[3] = {ctx->master, ctx->adam_m, ctx->adam_v};
+  SLIP_NCCL(ncclGroupStart());
+  for (float* b : bufs) {
+    ncclResult_t r = send ? ncclSend(b, n, ncclFloat32, peer, c->world_comm, st)
+                          : ncclRecv(b, n, ncclFloat32, peer, c->world_comm, st);
+    if (r != ncclSuccess) {
+      ncclGroupEnd();
+      return nccl_status(r, send ? "ncclSend(state)" : "ncclRecv(state)");
+    }
+  }
+  SLIP_NCCL(ncclGroupEnd());
+  if (!send) {
+    ctx->opt_step = opt_step;
+    SLIP_TRY(slip_weights_from_master(ctx, s));
+  }
   return SLIP_OK;
 }
 

@@ -13,6 +13,7 @@
 
 struct slip_comm {
   int rank = 0, world = 1;
+  int role = 0;  // worker position k*N + i this process plays (default: its world rank)
   ncclComm_t world_comm = nullptr;
   bool ready = false;
   slip::Cluster cl;

@@ -80,7 +80,7 @@ extern "C" slip_status slip_execute_schedule(slip_ctx* ctx, slip_comm* comm, con
   std::memset(out, 0, sizeof *out);
   const int N = cl.N, DP = cl.DP, m = cl.m;
   SLIP_CHECK(DP * m <= 1024, SLIP_EINVAL, "execute: DP * m must be <= 1024");
-  const int me = comm->rank, me_i = comm->my_stage, me_k = comm->my_pipe;
+  const int me = comm->role, me_i = comm->my_stage, me_k = comm->my_pipe;
   cudaStream_t cs = reinterpret_cast<cudaStream_t>(stream);
   if (!comm->my_live) return SLIP_OK;  // masked (failed) rank idles
   const Dims& D = ctx->dm;

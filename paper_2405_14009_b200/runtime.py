@@ -7,7 +7,7 @@ import ctypes as C
 from dataclasses import dataclass
 
 from ._binding import (SlipError, call, lib, slip_adam, slip_cluster, slip_costs, slip_io, slip_model, slip_op,
-                       slip_plan_opts, slip_report)
+                       slip_plan_opts, slip_report, slip_swap)
 
 
 def _ptr(t) -> C.c_void_p:
@@ -112,6 +112,55 @@ def assign(N, DP, m, live):
     out = (C.c_int32 * (N * m * DP))()
     call("slip_assign", C.byref(cl), out)
     return {(i, j, k): out[(i * m + j) * DP + k] for i in range(N) for j in range(m) for k in range(DP)}
+
+
+def rank_of(N, i, k) -> int:
+    """Role rank of worker (stage i, pipeline k) (include/slip.h slip_cluster)."""
+    return k * N + i
+
+
+def normalize_costs(N, DP, m, costs: slip_costs, F, decoupled=True, staggered=True, horizon=3):
+    """cost(i, x) table of the heuristic (reading R28): {(i, x): int or None (infinite)}."""
+    cl = make_cluster(N, DP, m, None)
+    opts = slip_plan_opts(int(decoupled), int(staggered), int(horizon))
+    out = (C.c_int64 * (N * (F + 1)))()
+    call("slip_normalize_costs", C.byref(cl), C.byref(costs), C.byref(opts), int(F), out)
+    inf = (1 << 63) - 1
+    return {(i, x): (None if out[i * (F + 1) + x] == inf else out[i * (F + 1) + x])
+            for i in range(N) for x in range(F + 1)}
+
+
+def normalize(N, DP, F, cost_table):
+    """Algorithm 1 over {(i, x): cost}; returns (R, C)
+    with C[i][f] None where no assignment exists."""
+    W = F + 1
+    inf = (1 << 63) - 1
+    tab = (C.c_int64 * (N * W))(*[inf if cost_table.get((i, x)) is None else int(cost_table[(i, x)])
+                                  for i in range(N) for x in range(W)])
+    Cout = (C.c_int64 * (N * W))()
+    R = (C.c_int32 * N)()
+    call("slip_normalize", N, DP, F, tab, Cout, R)
+    return list(R), [[None if Cout[i * W + f] == inf else Cout[i * W + f] for f in range(W)] for i in range(N)]
+
+
+def normalized_live(N, DP, R):
+    out = (C.c_uint8 * (N * DP))()
+    call("slip_normalized_live", N, DP, (C.c_int32 * N)(*R), out)
+    return [[out[i * DP + k] for k in range(DP)] for i in range(N)]
+
+
+def migration_plan(N, DP, live, R):
+    """[((i, k), (i2, k2), k_src)], live-after (see include/slip.h slip_migration_plan)."""
+    cl = make_cluster(N, DP, 1, live)
+    Rb = (C.c_int32 * N)(*R)
+    n = C.c_int32(0)
+    call("slip_migration_plan", C.byref(cl), Rb, None, 0, C.byref(n), None)
+    sw = (slip_swap * max(1, n.value))()
+    after = (C.c_uint8 * (N * DP))()
+    call("slip_migration_plan", C.byref(cl), Rb, sw, n.value, C.byref(n), after)
+    swaps = [((s.failed_stage, s.failed_pipe), (s.target_stage, s.target_pipe), s.source_pipe)
+             for s in sw[:n.value]]
+    return swaps, [[after[i * DP + k] for k in range(DP)] for i in range(N)]
 
 
 def recoverable(N, DP, live) -> bool:
@@ -228,6 +277,10 @@ class Comm:
         self.h, self.rank, self.world = h, rank, world
         self._cluster = None
 
+    def set_role(self, role: int):
+        """Play worker position `role` = k*N + i (after a normalization swap)."""
+        call("slip_comm_set_role", self.h, int(role))
+
     def setup(self, N, DP, m, live=None):
         self._cluster = make_cluster(N, DP, m, live)
         call("slip_comm_setup", self.h, C.byref(self._cluster))
@@ -236,6 +289,11 @@ class Comm:
         if self.h:
             lib().slip_comm_destroy(self.h)
             self.h = None
+
+
+def migrate_state(stage: Stage, comm: Comm, peer: int, send: bool, opt_step: int = 0, stream=None):
+    """P2P copy of the stage state of one normalization swap (world ranks)."""
+    call("slip_migrate_state", stage.ctx, comm.h, int(peer), int(bool(send)), int(opt_step), _stream(stream))
 
 
 def grad_allreduce(stage: Stage, comm: Comm, stream=None):

@@ -27,12 +27,129 @@ import slipdata as sd  # noqa: E402
 from paper_2405_14009_b200 import runtime as rt  # noqa: E402
 
 
+def migrate_scenario(a, cfg, L, comm, costs, rank, world, holder):
+    """Normalization swap on real GPUs (§4.2.1): one fault-free
+    iteration; then worker (0, 0) fails; the planner's Algorithm 1 target is taken as
+    R = [0, ..., 0, 1] (the failure belongs in the last stage); slip_migration_plan
+    names the swap; the live peer (0, k_src) copies stage 0's state (master, m, v)
+    to the GPU at the target, which takes over role (0, 0); iteration 2 runs with the
+    normalized live set.  Checked against two fault-free iterations, role by role:
+    the last-stage losses bit-identical, the gradients within 1e-4 normwise, the
+    AdamW result within 1e-5 (only the summation order of the stage all-reduce
+    moves), and all live peers of a stage bit-identical after the step."""
+    DP, PP, m = a.dp, a.pp, a.m
+    assert PP >= 2
+    g = torch.Generator().manual_seed(5)
+    xs = [torch.randn(cfg.tokens, cfg.hidden, generator=g).to(torch.bfloat16).pin_memory() for _ in range(DP * m)]
+    rs = [torch.randn(cfg.tokens, cfg.hidden, generator=g).to(torch.bfloat16).pin_memory() for _ in range(DP * m)]
+    adam = (1e-3, 0.9, 0.95, 1e-8, 0.1)
+    full = [[1] * DP for _ in range(PP)]
+
+    def fresh(role):
+        if "stage" in holder:
+            holder["stage"].close()
+        st = holder["stage"] = rt.Stage(cfg, L, n_slots=2 * m * DP)
+        rt.init_master_(st.master, cfg, L, cfg.layers, seed=100 + role % PP)
+        rt.call("slip_weights_from_master", st.ctx, rt._stream())
+        return st
+
+    def iterate(st, live):
+        comm.setup(PP, DP, m, live)
+        losses = torch.zeros(DP * m, dtype=torch.float32).pin_memory()
+        rt.execute_schedule(st, comm, PP, DP, m, live, costs, True, True, adam=adam, iterations=1,
+                            io=rt.make_io(xs, rs, losses))
+        torch.cuda.synchronize()
+        lc = losses.cuda()
+        dist.all_reduce(lc)
+        return lc.cpu()
+
+    # A: two fault-free iterations, role = rank
+    comm.set_role(rank)
+    st = fresh(rank)
+    iterate(st, full)
+    lA = iterate(st, full)
+    gA, pA = st.grad.clone(), st.master.clone()
+    # B: one fault-free iteration, then failure at (0, 0) and the normalization swap
+    st = fresh(rank)
+    iterate(st, full)
+    live = [row[:] for row in full]
+    live[0][0] = 0
+    cost = rt.normalize_costs(PP, DP, m, costs, 1)
+    R_alg1, _ = rt.normalize(PP, DP, 1, cost)
+    R = [0] * (PP - 1) + [1]
+    swaps, after = rt.migration_plan(PP, DP, live, R)
+    assert len(swaps) == 1
+    (fi, fk), (ti, tk), src = swaps[0]
+    w_failed, w_target, w_src = rt.rank_of(PP, fi, fk), rt.rank_of(PP, ti, tk), rt.rank_of(PP, fi, src)
+    role = {r: r for r in range(world)}
+    role[w_target], role[w_failed] = role[w_failed], role[w_target]
+    torch.cuda.synchronize()
+    dist.barrier()
+    t0 = torch.cuda.Event(enable_timing=True)
+    t1 = torch.cuda.Event(enable_timing=True)
+    t0.record()
+    if rank == w_src:
+        rt.migrate_state(st, comm, w_target, True)
+    elif rank == w_target:
+        rt.migrate_state(st, comm, w_src, False, opt_step=1)
+    t1.record()
+    torch.cuda.synchronize()
+    mig_ms = t0.elapsed_time(t1)
+    comm.set_role(role[rank])
+    lB = iterate(st, after)
+    gB, pB = st.grad.clone(), st.master.clone()
+    me_role = role[rank]
+    me_i, me_k = me_role % PP, me_role // PP
+    me_live = after[me_i][me_k] == 1
+    # the reference tensors of my role live on the process that played it in run A (= rank me_role)
+    refg, refp = torch.empty_like(gA), torch.empty_like(pA)
+    ops = []
+    for r in range(world):
+        if role[r] != r:  # process r plays role[r]; run A's role[r] data sits on rank role[r]
+            if rank == role[r]:
+                ops += [dist.P2POp(dist.isend, gA, r), dist.P2POp(dist.isend, pA, r)]
+            if rank == r:
+                ops += [dist.P2POp(dist.irecv, refg, role[r]), dist.P2POp(dist.irecv, refp, role[r])]
+    if ops:
+        for w in dist.batch_isend_irecv(ops):
+            w.wait()
+    if role[rank] == rank:
+        refg, refp = gA, pA
+    ok = True
+    res = {"rank": rank, "role": me_role, "live": me_live}
+    if me_live:
+        res["grad_relerr"] = ((gB - refg).abs().max() / refg.abs().max()).item()
+        res["master_relerr"] = ((pB - refp).abs().max() / refp.abs().max()).item()
+        ok &= res["grad_relerr"] <= 1e-4 and res["master_relerr"] <= 1e-5
+    # last-stage losses: every micro-batch's loss is written once in both runs
+    res["losses_equal"] = bool(torch.equal(lA, lB))
+    ok &= res["losses_equal"]
+    ck = torch.tensor([float(pB.double().sum().item()) if me_live else float("nan"), float(me_live), float(me_i)],
+                      dtype=torch.float64, device="cuda")
+    allck = [torch.zeros_like(ck) for _ in range(world)]
+    dist.all_gather(allck, ck)
+    if me_live:
+        for r2 in range(world):
+            if allck[r2][1].item() == 1.0 and int(allck[r2][2].item()) == me_i:
+                ok &= allck[r2][0].item() == ck[0].item()
+    flag = torch.tensor([1.0 if ok else 0.0], device="cuda")
+    dist.all_reduce(flag, op=dist.ReduceOp.MIN)
+    outs = [None] * world
+    dist.all_gather_object(outs, res)
+    if rank == 0:
+        print(json.dumps({"scenario": "migrate", "ok": flag.item() == 1.0, "R_alg1": R_alg1, "R": R,
+                          "swap": swaps[0], "migration_ms": mig_ms,
+                          "state_bytes": 3 * 4 * holder["stage"].n_params, "ranks": outs}), flush=True)
+    return flag.item() == 1.0
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--dp", type=int, default=2)
     ap.add_argument("--pp", type=int, default=1)
     ap.add_argument("--m", type=int, default=3)
     ap.add_argument("--failures", default="auto")
+    ap.add_argument("--migrate", action="store_true", help="normalization swap scenario (PP >= 2)")
     a = ap.parse_args()
     rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
     local = int(os.environ.get("LOCAL_RANK", rank))
@@ -70,6 +187,13 @@ def main():
                                   iterations=1, io=io)
         torch.cuda.synchronize()
         return rep, stage.grad.clone(), stage.master.clone(), losses.clone()
+
+    if a.migrate:
+        ok = migrate_scenario(a, cfg, L, comm, costs, rank, world, holder)
+        comm.close()
+        holder["stage"].close()
+        dist.destroy_process_group()
+        sys.exit(0 if ok else 1)
 
     live0 = [[1] * DP for _ in range(PP)]
     rep0, g0, p0, l0 = run(live0)

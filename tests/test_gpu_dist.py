@@ -11,10 +11,10 @@ pytestmark = pytest.mark.gpu
 HERE = os.path.dirname(os.path.abspath(__file__))
 
 
-def _run(n, dp, pp):
+def _run(n, dp, pp, *extra):
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
-           "--master-addr", "127.0.0.1", "--master-port", str(29500 + n + pp), os.path.join(HERE, "dist_check.py"),
-           "--dp", str(dp), "--pp", str(pp)]
+           "--master-addr", "127.0.0.1", "--master-port", str(29500 + n + pp + 7 * len(extra)),
+           os.path.join(HERE, "dist_check.py"), "--dp", str(dp), "--pp", str(pp), *extra]
     r = subprocess.run(cmd, capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stdout[-4000:] + r.stderr[-4000:]
     return r.stdout
@@ -36,3 +36,11 @@ def test_dp1_pp2_pipeline():
 def test_dp2_pp2_reroute():
     out = _run(4, 2, 2)
     assert '"ok": true' in out
+
+
+@pytest.mark.skipif(torch.cuda.device_count() < 4, reason="needs 4 GPUs")
+def test_dp2_pp2_normalization_swap():
+    """A failure at stage 0 migrated to the last stage by a P2P state copy; the GPU
+    that takes over the role continues training identically (dist_check --migrate)."""
+    out = _run(4, 2, 2, "--migrate")
+    assert '"scenario": "migrate", "ok": true' in out
