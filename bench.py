@@ -36,6 +36,9 @@ sys.path.insert(0, ROOT)
 
 METRIC = "train tokens/sec at 0/1/2 failures, 1-8 B200; B/W tensor-pipe % of peak"
 H, HEADS, FFN, SEQ, MB, LAYERS = 2048, 16, 8192, 2048, 1, 24
+# GPT shapes of SURVEY.md §8(a) (reading R2); the default is BASELINE.json configs[1]
+MODELS = {"1.3b": (2048, 16, 8192, 24), "2.7b": (2560, 32, 10240, 32), "6.7b": (4096, 32, 16384, 32)}
+MODEL = "1.3b"
 
 
 def parse():
@@ -45,17 +48,26 @@ def parse():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="slip", choices=["slip", "reference"])
     ap.add_argument("--failures", type=int, default=0)
-    ap.add_argument("--m", type=int, default=0, help="micro-batches per pipeline (default 4*PP)")
-    ap.add_argument("--layers", type=int, default=LAYERS)
+    ap.add_argument("--microbatches", "--m", dest="m", type=int, default=0, help="micro-batches per pipeline (default 4*PP)")
+    ap.add_argument("--layers", type=int, default=None, help="total layers (default: the model's)")
     ap.add_argument("--coupled", action="store_true", help="coupled backward, no staggering (1F1B baseline)")
     ap.add_argument("--no-stagger", action="store_true", help="decoupled B/W but a global optimizer barrier")
     ap.add_argument("--failed-at", default="",
                     help="actual failed workers 'i,k;i,k' (un-normalized); with --normalize they are migrated")
     ap.add_argument("--normalize", action="store_true",
                     help="Algorithm 1 + P2P migration swaps before the timed steps (needs --failed-at)")
+    ap.add_argument("--sm-reserve", type=int, default=-1,
+                    help="SMs kept free of persistent GEMM CTAs for NCCL kernels (default: 0 at N=1, 8 at N>1)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    return ap.parse_args()
+    ap.add_argument("--model", default="1.3b", choices=sorted(MODELS), help="GPT shape (default: BASELINE configs[1])")
+    a = ap.parse_args()
+    global H, HEADS, FFN, LAYERS, MODEL
+    MODEL = a.model
+    H, HEADS, FFN, LAYERS = MODELS[a.model]
+    if a.layers is None:
+        a.layers = LAYERS
+    return a
 
 
 def peaks():
@@ -164,8 +176,8 @@ def run_reference(args, rank, world):
         "impl": "reference", "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": "gpt-1.3B-shape (h2048 s2048 16 heads ffn8192) %d layers, m=%d, DP1xPP1" % (
-            args.layers, m), "model": "gpt-1.3b-shape", "global_batch": m * MB, "seq_len": SEQ,
+        "config": {"workload": "gpt-%s-shape (h%d s%d %d heads ffn%d) %d layers, m=%d, DP1xPP1" % (
+            MODEL, H, SEQ, HEADS, FFN, args.layers, m), "model": "gpt-%s-shape" % MODEL, "global_batch": m * MB, "seq_len": SEQ,
             "parallelism": "host"},
         "cpu_baseline": {"value": value, "unit": "tokens/s", "cores": cores, "kind": "oracle",
                          "sample": "per step: 1 layer x 1 micro-batch F+B+W (T=2048, h=2048) + AdamW over 1 layer,"
@@ -247,6 +259,8 @@ def main():
     n_slots = slots_for(live, costs)
     if args.normalize:
         n_slots = max(n_slots, slots_for(normalization(costs)[2], costs))
+    sm_reserve = args.sm_reserve if args.sm_reserve >= 0 else (0 if world == 1 else 8)
+    rt.set_sm_reserve(sm_reserve)
     stage = rt.Stage(cfg, L, n_slots)
     rt.init_master_(stage.master, cfg, L, args.layers, seed=rank % PP)
     rt.call("slip_weights_from_master", stage.ctx, rt._stream())
@@ -287,27 +301,34 @@ def main():
         if slots_for(after, costs) > n_slots:
             raise SystemExit("normalized plan needs more slots than allocated")
         role = list(range(world))
-        barrier()
-        g0, g1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        g0.record(stream)
+        pairs = []
         for (fi, fk), (ti, tk), src in swaps:
             w_f, w_t, w_s = rt.rank_of(PP, fi, fk), rt.rank_of(PP, ti, tk), rt.rank_of(PP, fi, src)
-            # process playing the source role sends to the process playing the target role
+            # the process playing the source role sends to the process playing the target role
             p_s, p_t, p_f = role.index(w_s), role.index(w_t), role.index(w_f)
-            if rank == p_s:
-                rt.migrate_state(stage, comm, p_t, True)
-            elif rank == p_t:
-                rt.migrate_state(stage, comm, p_s, False, opt_step=0)
+            pairs.append((p_s, p_t))
             role[p_t], role[p_f] = w_f, w_t
-        g1.record(stream)
-        barrier()
-        mig_ms = allreduce_max(g0.elapsed_time(g1))
+
+        def migrate():
+            barrier()
+            g0, g1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            g0.record(stream)
+            for p_s, p_t in pairs:
+                if rank == p_s:
+                    rt.migrate_state(stage, comm, p_t, True)
+                elif rank == p_t:
+                    rt.migrate_state(stage, comm, p_s, False, opt_step=0)
+            g1.record(stream)
+            barrier()
+            return allreduce_max(g0.elapsed_time(g1))
+        mig_ms = migrate()       # cold: includes NCCL's lazy P2P connection of the pair
+        mig_warm_ms = migrate()  # the same copy again: the transfer alone
         comm.set_role(role[rank])
         live = after
         comm.setup(PP, DP, m, live)
         norm = {"actual_failed": failed, "R": R, "swaps": swaps, "migration_ms": mig_ms,
-                "state_bytes_per_swap": 12 * stage.n_params,
-                "migration_GBps": (12 * stage.n_params * len(swaps) / (mig_ms * 1e6)) if swaps and mig_ms else None,
+                "migration_warm_ms": mig_warm_ms, "state_bytes_per_swap": 12 * stage.n_params,
+                "migration_GBps": (12 * stage.n_params / (mig_warm_ms * 1e6)) if swaps and mig_warm_ms else None,
                 "cost_table_10us": {"%d,%d" % ix: v for ix, v in tab.items()},
                 "normalized_failed": [(i, k) for i in range(PP) for k in range(DP) if not live[i][k]]}
         failed = norm["normalized_failed"]
@@ -393,13 +414,14 @@ def main():
         "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
-        "config": {"workload": "gpt-1.3B-shape (h2048, 16 heads, ffn 8192, s2048, b1) %d layers, DP%dxPP%d, "
+        "config": {"workload": ("gpt-%s-shape (h%d, %d heads, ffn %d, s%d, b1) " % (MODEL, H, HEADS, FFN, SEQ)) +
+                               "%d layers, DP%dxPP%d, "
                                "m=%d micro-batches/pipeline, %s, failures=%d" % (
                                    args.layers, DP, PP, m,
                                    plan_name,
                                    len(failed)),
-                   "model": "gpt-1.3b-shape", "global_batch": DP * m * MB, "seq_len": SEQ,
-                   "parallelism": "dp%dxpp%d" % (DP, PP), "failed_workers": failed,
+                   "model": "gpt-%s-shape" % MODEL, "global_batch": DP * m * MB, "seq_len": SEQ,
+                   "parallelism": "dp%dxpp%d" % (DP, PP), "failed_workers": failed, "sm_reserve": sm_reserve,
                    "l2": "inputs larger than L2 (2.4 GB bf16 weights + GBs of stash per step)"},
         "clocks": clk,
         "e2e": e2e,

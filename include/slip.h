@@ -264,6 +264,12 @@ slip_status slip_synth_normal(void* out_bf16, int64_t n, uint64_t seed, uint64_t
 /* w_bf16 <- RNE(master) (after loading master weights). */
 slip_status slip_weights_from_master(slip_ctx* ctx, slip_stream s);
 
+/* Process-wide: persistent GEMM grids fill at most (#SMs - n) SMs, leaving n
+ * SMs to kernels of other streams (the executor's NCCL transfers and stage
+ * all-reduce run concurrently with compute; a persistent CTA that finds no free
+ * SM would wait for the whole concurrent kernel).  Default 0. */
+slip_status slip_set_sm_reserve(int32_t n);
+
 /* Diagnostic entry to one GEMM of the tcgen05 family, for kernel-level parity
  * tests: D[M,N] = sum_k A(m,k) B(k,n), bf16 operands, fp32 accumulation.
  * A(m,k) = a[m*lda + k] (a_mn = 0) or a[k*lda + m] (a_mn = 1);

@@ -123,6 +123,7 @@ SIGNATURES = {
     "slip_comm_destroy": (C.c_int, [P]),
     "slip_grad_allreduce": (C.c_int, [P, P, P]),
     "slip_comm_set_role": (C.c_int, [P, I32]),
+    "slip_set_sm_reserve": (C.c_int, [I32]),
     "slip_migrate_state": (C.c_int, [P, P, I32, I32, I64, P]),
     "slip_execute_schedule": (C.c_int, [P, P, C.POINTER(slip_cluster), C.POINTER(slip_costs),
                                         C.POINTER(slip_plan_opts), C.POINTER(slip_adam), I32, I32, U64,

@@ -11,6 +11,7 @@
 // min(#tiles, #SMs) CTAs; the epilogue of tile i overlaps the mainloop of tile i+1.
 #include <cudaTypedefs.h>
 
+#include <atomic>
 #include <cmath>
 #include <cstdio>
 #include <cstring>
@@ -311,15 +312,42 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     float* buf = epi + ew * 32 * 32;
     int acc = 0;
     uint32_t acc_phase = 0;
+    constexpr int NCH = C::ACC_COLS / 32;
+    const int qd = lane & 3;  // bf16 path: 8-column group of this lane after the transpose
+    const bool ext_res = p.mode < EPI_F32_STORE && p.resid != nullptr;
+    const bool ext_aux = p.mode == EPI_BF16_DGELU;
     for (int t = t0; t < p.total; t += tstep) {
       const Tile tl = decode_tile<BN, C::TILE_M>(t, p);
       const CUtensorMap* mC = tl.g >= 0 ? &p.groups[tl.g].tc : &tmC;
+      const int row0 = tl.m0 + cta * BM + lq * 32;
+      // residual / GeLU-input operands of a chunk are read-only: their loads are issued one
+      // chunk ahead (the first before the accumulator is ready) so DRAM latency overlaps the
+      // MMA mainloop and the previous chunk instead of stalling each row group.
+      uint4 rn[4], hn[4];
+      auto prefetch = [&](int ch_) {
+        const int cc_ = tl.n0 + ch_ * 32 + 8 * qd;
+#pragma unroll
+        for (int it = 0; it < 4; ++it) {
+          const int mm = row0 + 8 * it + (lane >> 2);
+          const bool ok = mm < tl.M && cc_ < tl.N;
+          const int64_t off = tl.zo * p.c_zo + tl.zi * p.c_zi + static_cast<int64_t>(mm) * p.ldc + cc_;
+          rn[it] = (ext_res && ok) ? __ldg(reinterpret_cast<const uint4*>(p.resid + off)) : make_uint4(0, 0, 0, 0);
+          hn[it] = (ext_aux && ok) ? __ldg(reinterpret_cast<const uint4*>(p.aux + off)) : make_uint4(0, 0, 0, 0);
+        }
+      };
+      if (ext_res || ext_aux) prefetch(half);
       ptx::mbar_wait(&tfull[acc], acc_phase);
       ptx::tc_fence_after();
-      const int row0 = tl.m0 + cta * BM + lq * 32;
       const int m = row0 + lane;
 #pragma unroll 1
-      for (int ch = half; ch < C::ACC_COLS / 32; ch += 2) {
+      for (int ch = half; ch < NCH; ch += 2) {
+        uint4 rc[4], hc[4];
+#pragma unroll
+        for (int it = 0; it < 4; ++it) {
+          rc[it] = rn[it];
+          hc[it] = hn[it];
+        }
+        if ((ext_res || ext_aux) && ch + 2 < NCH) prefetch(ch + 2);
         uint32_t r[32];
         ptx::tmem_ld_32x32b_x32(tmem_base + (static_cast<uint32_t>(lq * 32) << 16) + acc * C::ACC_COLS + ch * 32, r);
         ptx::tmem_ld_wait();
@@ -357,8 +385,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                 make_float4(p.alpha * __uint_as_float(r[4 * j]), p.alpha * __uint_as_float(r[4 * j + 1]),
                             p.alpha * __uint_as_float(r[4 * j + 2]), p.alpha * __uint_as_float(r[4 * j + 3]));
           __syncwarp();
-          const int qd = lane & 3;       // 8-column group of this lane
-          const int cc = n + 8 * qd;     // its first output column
+          const int cc = n + 8 * qd;     // first output column of this lane
           float bv[8];
 #pragma unroll
           for (int e = 0; e < 8; ++e) bv[e] = 0.f;
@@ -380,13 +407,13 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
               for (int e = 0; e < 8; ++e) x[e] = gelu_f(x[e]);
             } else if (p.mode == EPI_BF16_DGELU) {
               float hv[8];
-              unpack8(*reinterpret_cast<const uint4*>(p.aux + off), hv);
+              unpack8(hc[it], hv);
 #pragma unroll
               for (int e = 0; e < 8; ++e) x[e] *= gelu_grad_f(hv[e]);
             }
             if (p.resid) {
               float rv[8];
-              unpack8(*reinterpret_cast<const uint4*>(p.resid + off), rv);
+              unpack8(rc[it], rv);
 #pragma unroll
               for (int e = 0; e < 8; ++e) x[e] += rv[e];
             }
@@ -500,7 +527,7 @@ cudaError_t launch_kernel(const CUtensorMap& ta, const CUtensorMap& tb, const CU
   });
   if (attr_err != cudaSuccess) return attr_err;
   if (p.total == 0) return cudaSuccess;
-  const int units = PAIR ? num_sms() / 2 : num_sms();
+  const int units = PAIR ? sm_budget() / 2 : sm_budget();
   const int grid = (p.total < units ? p.total : units) * (PAIR ? 2 : 1);
   return launch_pdl(kern, dim3(grid), dim3(NUM_THREADS), C::SMEM_BYTES, s, PAIR ? 2 : 1, ta, tb, tc, p);
 }
@@ -584,6 +611,15 @@ int num_sms() {
     if (n <= 0) n = 148;
   });
   return n;
+}
+
+namespace {
+std::atomic<int> g_sm_reserve{0};
+}
+void set_sm_reserve(int n) { g_sm_reserve.store(n < 0 ? 0 : n); }
+int sm_budget() {
+  const int b = num_sms() - g_sm_reserve.load();
+  return b < 2 ? 2 : b;
 }
 
 const char* gemm_last_message() { return g_msg.c_str(); }

@@ -71,6 +71,11 @@ cudaError_t gemm_group_launch(const GroupEntry* dev_table, int n, int total_tile
                               cudaStream_t s);
 const char* gemm_last_message();
 int num_sms();
+// SMs the persistent GEMM grids may fill: num_sms() minus a reserve left free for
+// kernels of other streams (NCCL P2P / all-reduce of the executor) — a persistent CTA
+// that cannot be placed waits for the whole concurrent kernel otherwise.
+int sm_budget();
+void set_sm_reserve(int n);
 
 // 4-D bf16 tensor map, 128-byte swizzle: dims (d0 inner, d1, d2, d3), strides in elements
 // of dims 1..3, box (b0, b1, 1, 1).  False (message in gemm_last_message) on failure.

@@ -577,6 +577,12 @@ slip_status slip_synth_normal(void* out_bf16, int64_t n, uint64_t seed, uint64_t
   return SLIP_OK;
 }
 
+slip_status slip_set_sm_reserve(int32_t n) {
+  SLIP_CHECK(n >= 0 && n < 1024, SLIP_EINVAL, "set_sm_reserve: n out of range");
+  set_sm_reserve(n);
+  return SLIP_OK;
+}
+
 slip_status slip_gemm(int32_t M, int32_t N, int32_t K, const void* a, int64_t lda, int32_t a_mn, const void* b,
                       int64_t ldb, int32_t b_mn, void* c, int64_t ldc, int32_t mode, int32_t bn, int32_t accumulate,
                       float alpha, slip_stream st) {

@@ -114,6 +114,11 @@ def assign(N, DP, m, live):
     return {(i, j, k): out[(i * m + j) * DP + k] for i in range(N) for j in range(m) for k in range(DP)}
 
 
+def set_sm_reserve(n: int):
+    """Leave n SMs free of persistent GEMM CTAs (for concurrent NCCL kernels)."""
+    call("slip_set_sm_reserve", int(n))
+
+
 def rank_of(N, i, k) -> int:
     """Role rank of worker (stage i, pipeline k) (include/slip.h slip_cluster)."""
     return k * N + i

@@ -18,7 +18,7 @@ for m in $MS; do
       port=$((port + 1))
       out=gpurun_out/ablation/n${N}_m${m}_f${f}_${plan}.json
       timeout 400 python -m torch.distributed.run --nnodes=1 --nproc-per-node $N --master-addr 127.0.0.1 \
-        --master-port $port bench.py --gpus $N --steps 5 --warmup 3 --m $m --failures $f $flag \
+        --master-port $port bench.py --gpus $N --steps 5 --warmup 3 --microbatches $m --failures $f $flag \
         --no-e2e --no-cpu-baseline > ${out%.json}.log 2>&1
       grep '"metric"' ${out%.json}.log > $out
       python -c "import json;d=json.load(open('$out'));print('$plan m=$m f=$f', round(d['value']), round(d['ms_per_step'],2), d['predicted_period_units'])" 2>/dev/null || echo "$plan m=$m f=$f FAILED"
