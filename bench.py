@@ -58,6 +58,7 @@ def parse():
                     help="Algorithm 1 + P2P migration swaps before the timed steps (needs --failed-at)")
     ap.add_argument("--sm-reserve", type=int, default=-1,
                     help="SMs kept free of persistent GEMM CTAs for NCCL kernels (default: 0 at N=1, 8 at N>1)")
+    ap.add_argument("--trace", default="", help="directory: dump one traced 2-iteration run per rank (JSON)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--model", default="1.3b", choices=sorted(MODELS), help="GPT shape (default: BASELINE configs[1])")
@@ -294,6 +295,7 @@ def main():
     costs = rt.make_costs(t_f=q(per[0]), t_b=q(per[1] or per[3]), t_w=q(per[2] or 0.01), t_comm=1,
                           t_ar=q(per[4] * 0.5 if per[4] else 0.01), t_opt=q(per[4] or 0.01))
     norm = None
+    my_role = rank
     if args.normalize and failed:
         # Normalization with the profiled costs, then one P2P state copy per swap (PAPER.md
         # lines 377-379): the GPU at the target position takes over the failed worker's role
@@ -324,6 +326,7 @@ def main():
         mig_ms = migrate()       # cold: includes NCCL's lazy P2P connection of the pair
         mig_warm_ms = migrate()  # the same copy again: the transfer alone
         comm.set_role(role[rank])
+        my_role = role[rank]
         live = after
         comm.setup(PP, DP, m, live)
         norm = {"actual_failed": failed, "R": R, "swaps": swaps, "migration_ms": mig_ms,
@@ -372,6 +375,19 @@ def main():
             traffic = json.load(f).get("dram_bytes_per_launch")
     except Exception:
         pass
+    if args.trace:
+        # plan-vs-execution timeline (outside the timed region)
+        rt.set_trace(stage, True)
+        execute(2)
+        barrier()
+        rt.set_trace(stage, False)
+        plan = rt.plan_schedule(PP, DP, m, live, costs, decoupled, staggered, horizon=2)
+        os.makedirs(args.trace, exist_ok=True)
+        with open(os.path.join(args.trace, "rank%d.json" % rank), "w") as f:
+            json.dump({"rank": rank, "role": my_role, "live": live, "costs_10us": [costs.t_f, costs.t_b, costs.t_w,
+                                                                                      costs.t_comm, costs.t_ar,
+                                                                                      costs.t_opt],
+                       "trace": rt.get_trace(stage), "plan_ops": plan.ops, "plan_period": plan.period}, f)
     kern = torch.tensor([rep.n_kernels], dtype=torch.float64, device="cuda")
     if world > 1:
         dist.all_reduce(kern)

@@ -389,6 +389,23 @@ slip_status slip_execute_schedule(slip_ctx* ctx, slip_comm* comm, const slip_clu
                                   int32_t iterations, uint64_t seed, const slip_io* io, slip_stream s,
                                   slip_report* out);
 
+/* ------------------------------------------------------------------ tracing
+ * Per-action timeline of the timed iterations of the last slip_execute_schedule
+ * on this ctx (off by default; costs two CUDA events per action).  Each record
+ * is one program action (slip_action_kind), timed with events on the stream it
+ * runs on (compute, pair or all-reduce stream): begin = when the stream reached
+ * the action (its waits satisfied), end = when it finished, in ms from the start
+ * of the timed region.  The planner's (start, end) of the same op make the
+ * plan-vs-execution comparison (§5.3). */
+typedef struct {
+  int32_t kind, mb, origin, iter, peer, slot;
+  float begin_ms, end_ms;
+} slip_trace_rec;
+
+slip_status slip_set_trace(slip_ctx* ctx, int32_t enable);
+/* Copies at most cap records (host) of the last traced run; *n gets the count. */
+slip_status slip_get_trace(slip_ctx* ctx, slip_trace_rec* out, int64_t cap, int64_t* n);
+
 #ifdef __cplusplus
 }
 #endif

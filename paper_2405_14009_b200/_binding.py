@@ -43,6 +43,11 @@ class slip_adam(C.Structure):
     _fields_ = [(n, C.c_float) for n in ("lr", "beta1", "beta2", "eps", "weight_decay")]
 
 
+class slip_trace_rec(C.Structure):
+    _fields_ = [("kind", C.c_int32), ("mb", C.c_int32), ("origin", C.c_int32), ("iter", C.c_int32),
+                ("peer", C.c_int32), ("slot", C.c_int32), ("begin_ms", C.c_float), ("end_ms", C.c_float)]
+
+
 class slip_swap(C.Structure):
     _fields_ = [("failed_stage", C.c_int32), ("failed_pipe", C.c_int32), ("target_stage", C.c_int32),
                 ("target_pipe", C.c_int32), ("source_pipe", C.c_int32)]
@@ -124,6 +129,8 @@ SIGNATURES = {
     "slip_grad_allreduce": (C.c_int, [P, P, P]),
     "slip_comm_set_role": (C.c_int, [P, I32]),
     "slip_set_sm_reserve": (C.c_int, [I32]),
+    "slip_set_trace": (C.c_int, [P, I32]),
+    "slip_get_trace": (C.c_int, [P, C.POINTER(slip_trace_rec), I64, C.POINTER(I64)]),
     "slip_migrate_state": (C.c_int, [P, P, I32, I32, I64, P]),
     "slip_execute_schedule": (C.c_int, [P, P, C.POINTER(slip_cluster), C.POINTER(slip_costs),
                                         C.POINTER(slip_plan_opts), C.POINTER(slip_adam), I32, I32, U64,

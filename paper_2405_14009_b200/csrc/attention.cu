@@ -27,6 +27,12 @@ constexpr int CW0 = 4;       // first row warp
 constexpr int NRW = 16;      // row warps: 4 lane quarters x 4 column groups of 32
 constexpr int NT = 32 * (CW0 + NRW);
 
+__device__ __forceinline__ float max3(float a, float b, float c) {
+  float r;
+  asm("max.f32 %0, %1, %2, %3;" : "=f"(r) : "f"(a), "f"(b), "f"(c));
+  return r;
+}
+
 __device__ __forceinline__ float ex2(float x) {
   float y;
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
@@ -295,6 +301,255 @@ __global__ void __launch_bounds__(NT, 1)
   }
 }
 
+// ====================================================================== forward kernel
+// Single pass, online softmax.  One CTA per (q-tile i, z), longest rows first.  TMEM:
+// S[0] | S[1] | O (128 columns each): S of k-tile j+1 is computed while the softmax warps
+// work on k-tile j, so the tensor core and the softmax overlap.  Warp 0 TMA (K ring of 3,
+// V ring of 2, loaded in consumption order), warp 1 MMA, warp 2 TMEM allocator, warps
+// 4-11 softmax: warp w owns TMEM lane quarter w % 4 (32 rows) and column half g =
+// (w - 4) / 4 (64 of the 128 keys of a tile).  Per k-tile: S half -> registers, row max
+// exchanged with the partner warp through shared memory, O and l rescaled only when the
+// running max grows by more than kTau (log2 units; P stays <= 2^kTau, far inside bf16 /
+// fp32 range, and the result is the exact softmax either way), P = exp2(S log2e/sqrt(d)
+// - m) written as bf16 pairs over the S columns (the MMA reads P from TMEM for O += P V).
+// Output O / l in bf16 and lse = m + log2 l (log2 domain) for the backward pass.
+constexpr int FWD_NT = 32 * 20;
+constexpr float kTau = 8.0f;
+
+// Optional cycle-stamp probe of one CTA (tools/attn_probe.cu builds with SLIP_ATTN_PROBE).
+#ifdef SLIP_ATTN_PROBE
+__device__ long long g_probe[4096];
+#define PROBE(idx)                                                                  \
+  do {                                                                              \
+    if (blockIdx.x == 0 && blockIdx.y == SLIP_ATTN_PROBE) g_probe[idx] = clock64(); \
+  } while (0)
+#else
+#define PROBE(idx) \
+  do {             \
+  } while (0)
+#endif
+
+template <int D>
+__global__ void __launch_bounds__(FWD_NT, 1)
+    attn_fwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
+                    const __grid_constant__ CUtensorMap tmV, const KArgs a) {
+  using C = AC<D>;
+  constexpr int KST = 3, VST = 2;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* Qs = sm;
+  uint8_t* Ks = Qs + C::TB;         // [KST][TB]
+  uint8_t* Vs = Ks + KST * C::TB;   // [VST][TB]
+  float* red = reinterpret_cast<float*>(Vs + VST * C::TB);  // [4][128] partial row max / sum
+  uint64_t* bar = reinterpret_cast<uint64_t*>(red + 4 * TILE);
+  uint64_t* q_full = bar;
+  uint64_t* k_full = bar + 1;                // [KST]
+  uint64_t* k_empty = k_full + KST;          // [KST]
+  uint64_t* v_full = k_empty + KST;          // [VST]
+  uint64_t* v_empty = v_full + VST;          // [VST]
+  uint64_t* s_full = v_empty + VST;          // [2] per S buffer
+  uint64_t* p_full = s_full + 2;             // P of the current k-tile written (8 warps)
+  uint64_t* o_done = p_full + 1;             // PV of a k-tile complete
+  uint32_t* tholder = reinterpret_cast<uint32_t*>(o_done + 1);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int z = blockIdx.x, hn = z % a.heads, bi = z / a.heads;
+  const int i = a.ntiles - 1 - static_cast<int>(blockIdx.y);  // longest rows first (LPT order)
+  const int nj = i + 1;
+
+  if (threadIdx.x == 0) {
+    ptx::mbar_init(q_full, 1);
+    for (int t = 0; t < KST; ++t) {
+      ptx::mbar_init(&k_full[t], 1);
+      ptx::mbar_init(&k_empty[t], 1);
+    }
+    for (int t = 0; t < VST; ++t) {
+      ptx::mbar_init(&v_full[t], 1);
+      ptx::mbar_init(&v_empty[t], 1);
+    }
+    ptx::mbar_init(&s_full[0], 1);
+    ptx::mbar_init(&s_full[1], 1);
+    ptx::mbar_init(p_full, 16);
+    ptx::mbar_init(o_done, 1);
+    ptx::fence_mbar_init();
+  }
+  if (warp == 2) ptx::tmem_alloc<512>(tholder);
+  ptx::tc_fence_before();
+  __syncthreads();
+  ptx::tc_fence_after();
+  const uint32_t tmem = *tholder;
+  ptx::grid_dep_wait();  // PDL: the prologue above overlapped the previous kernel
+  if (threadIdx.x == 0) PROBE(0);
+
+  if (warp == 0) {
+    if (lane == 0) {  // ------------------------------------------------ TMA producer
+      ptx::mbar_arrive_expect_tx(q_full, C::TB);
+      for (int t = 0; t < C::NA; ++t) ptx::tma_load_4d(&tmQ, Qs + t * ATOM, q_full, t * 64, i * TILE, hn, bi);
+      auto load_k = [&](int j) {
+        const int st = j % KST;
+        ptx::mbar_wait(&k_empty[st], ((j / KST) & 1) ^ 1);
+        ptx::mbar_arrive_expect_tx(&k_full[st], C::TB);
+        for (int t = 0; t < C::NA; ++t)
+          ptx::tma_load_4d(&tmK, Ks + st * C::TB + t * ATOM, &k_full[st], t * 64, j * TILE, hn, bi);
+      };
+      auto load_v = [&](int j) {
+        const int st = j % VST;
+        ptx::mbar_wait(&v_empty[st], ((j / VST) & 1) ^ 1);
+        ptx::mbar_arrive_expect_tx(&v_full[st], C::TB);
+        for (int t = 0; t < C::NA; ++t)
+          ptx::tma_load_4d(&tmV, Vs + st * C::TB + t * ATOM, &v_full[st], t * 64, j * TILE, hn, bi);
+      };
+      // consumption order of the MMA warp: K0 K1 V0 K2 V1 K3 V2 ...
+      load_k(0);
+      if (nj > 1) load_k(1);
+      for (int j = 0; j < nj; ++j) {
+        load_v(j);
+        if (j + 2 < nj) load_k(j + 2);
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {  // ------------------------------------------------ MMA issuer
+      ptx::mbar_wait(q_full, 0);
+      const uint32_t qb = ptx::smem_u32(Qs), kb0 = ptx::smem_u32(Ks), vb0 = ptx::smem_u32(Vs);
+      auto mma_s = [&](int j) {  // S[j % 2] = Q K_j^T
+        const int st = j % KST;
+        ptx::mbar_wait(&k_full[st], (j / KST) & 1);
+        ptx::tc_fence_after();
+        const uint32_t kb = kb0 + st * C::TB;
+#pragma unroll
+        for (int kk = 0; kk < C::KS; ++kk)
+          ptx::tc_mma_f16(tmem + (j & 1) * 128, dk(qb, kk), dk(kb, kk), C::IDESC_S, kk > 0);
+        ptx::tc_commit(&s_full[j & 1]);
+        ptx::tc_commit(&k_empty[st]);
+      };
+      mma_s(0);
+      if (nj > 1) mma_s(1);
+      for (int j = 0; j < nj; ++j) {
+        const int st = j % VST;
+        ptx::mbar_wait(p_full, j & 1);
+        ptx::mbar_wait(&v_full[st], (j / VST) & 1);
+        PROBE(100 + j);
+        ptx::tc_fence_after();
+        const uint32_t vb = vb0 + st * C::TB;
+#pragma unroll
+        for (int kk = 0; kk < TILE / 16; ++kk)  // O += P V_j, P (bf16 pairs) from TMEM
+          ptx::tc_mma_f16_ts(tmem + 256, tmem + (j & 1) * 128 + kk * 8, dm(vb, kk), C::IDESC_O,
+                             (j > 0 || kk > 0) ? 1u : 0u);
+        ptx::tc_commit(o_done);
+        ptx::tc_commit(&v_empty[st]);
+        if (j + 2 < nj) mma_s(j + 2);  // into the S buffer PV_j has just consumed (in order)
+      }
+    }
+  } else if (warp >= 4) {  // ------------------------------------------ softmax warps
+    const int lq = warp & 3, g = (warp - 4) >> 2;  // lane quarter, column group (32 keys)
+    const int r = lq * 32 + lane;
+    const int q = i * TILE + r;
+    const uint32_t lane_off = static_cast<uint32_t>(lq * 32) << 16;
+    const uint32_t tO = tmem + 256 + lane_off;
+    float m_run = -INFINITY, l = 0.f;
+    for (int j = 0; j < nj; ++j) {
+      const uint32_t tS = tmem + (j & 1) * 128 + lane_off;
+      ptx::mbar_wait(&s_full[j & 1], (j >> 1) & 1);
+      if (lq == 0 && lane == 0 && g < 2) PROBE(400 + 300 * g + j);
+      ptx::tc_fence_after();
+      const bool diag = j == i;
+      const int kb = j * TILE + g * 32;  // first key of this warp's column group
+      uint32_t v[32];
+      ptx::tmem_ld_32x32b_x32(tS + g * 32, v);
+      ptx::tmem_ld_wait();
+      float mx[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
+      if (!diag) {
+#pragma unroll
+        for (int e = 0; e < 32; e += 2)
+          mx[(e >> 1) & 3] = max3(mx[(e >> 1) & 3], __uint_as_float(v[e]), __uint_as_float(v[e + 1]));
+      } else {
+#pragma unroll
+        for (int e = 0; e < 32; ++e)
+          if (kb + e <= q) mx[e & 3] = fmaxf(mx[e & 3], __uint_as_float(v[e]));
+      }
+      // row max over the 4 column groups (the 4 warps of this lane quarter)
+      red[g * TILE + r] = fmaxf(fmaxf(mx[0], mx[1]), fmaxf(mx[2], mx[3]));
+      ptx::named_bar_sync(1 + lq, 128);
+      const float mt = fmaxf(fmaxf(red[r], red[TILE + r]), fmaxf(red[2 * TILE + r], red[3 * TILE + r])) * a.sl2;
+      ptx::named_bar_sync(1 + lq, 128);  // all read before the next tile overwrites red
+      if (lq == 0 && lane == 0 && g < 2) PROBE(500 + 300 * g + j);
+      if (__any_sync(0xffffffffu, mt > m_run + kTau)) {
+        const float mn = fmaxf(m_run, mt);
+        const float alpha = m_run == -INFINITY ? 0.f : ex2(m_run - mn);
+        if (j > 0 && g < C::OC) {  // O holds PV(0 .. j-1): wait for the last one, rescale my chunk
+          ptx::mbar_wait(o_done, (j - 1) & 1);
+          ptx::tc_fence_after();
+          uint32_t o[32];
+          ptx::tmem_ld_32x32b_x32(tO + g * 32, o);
+          ptx::tmem_ld_wait();
+#pragma unroll
+          for (int e = 0; e < 32; ++e) o[e] = __float_as_uint(__uint_as_float(o[e]) * alpha);
+          ptx::tmem_st_32x32b_x32(tO + g * 32, o);
+          ptx::tmem_st_wait();
+        }
+        l *= alpha;
+        m_run = mn;
+      }
+      const float nm = -m_run;
+      float ls[4] = {0.f, 0.f, 0.f, 0.f};
+      uint32_t pk[16];
+      if (!diag) {
+#pragma unroll
+        for (int e = 0; e < 16; ++e) {
+          const float p0 = ex2(fmaf(__uint_as_float(v[2 * e]), a.sl2, nm));
+          const float p1 = ex2(fmaf(__uint_as_float(v[2 * e + 1]), a.sl2, nm));
+          ls[(2 * e) & 3] += p0;
+          ls[(2 * e + 1) & 3] += p1;
+          pk[e] = pack2(p0, p1);
+        }
+      } else {
+#pragma unroll
+        for (int e = 0; e < 16; ++e) {
+          const int k0 = kb + 2 * e;
+          const float p0 = k0 <= q ? ex2(fmaf(__uint_as_float(v[2 * e]), a.sl2, nm)) : 0.f;
+          const float p1 = k0 + 1 <= q ? ex2(fmaf(__uint_as_float(v[2 * e + 1]), a.sl2, nm)) : 0.f;
+          ls[(2 * e) & 3] += p0;
+          ls[(2 * e + 1) & 3] += p1;
+          pk[e] = pack2(p0, p1);
+        }
+      }
+      l += (ls[0] + ls[1]) + (ls[2] + ls[3]);
+      // P of keys [32g, 32g+32) -> bf16 pairs in TMEM columns [16g, 16g+16) of this S buffer
+      // (every S value of the tile is already in registers: the exchange above ordered it)
+      ptx::tmem_st_32x32b_x16(tS + g * 16, pk);
+      ptx::tmem_st_wait();
+      ptx::tc_fence_before();
+      __syncwarp();
+      if (lane == 0) ptx::mbar_arrive(p_full);
+      if (lq == 0 && lane == 0 && g < 2) PROBE(600 + 300 * g + j);
+    }
+    // total l over the 4 column groups, then O / l and lse
+    red[g * TILE + r] = l;
+    ptx::named_bar_sync(1 + lq, 128);
+    const float lt = (red[r] + red[TILE + r]) + (red[2 * TILE + r] + red[3 * TILE + r]);
+    ptx::mbar_wait(o_done, (nj - 1) & 1);
+    ptx::tc_fence_after();
+    if (g == 0 && q < a.s) a.lse[static_cast<size_t>(z) * a.s + q] = m_run + log2f(lt);
+    if (g < C::OC) {
+      const float inv = 1.0f / lt;
+      __nv_bfloat16* orow =
+          a.out + (static_cast<int64_t>(bi) * a.s + q) * a.ldo + a.col0 + static_cast<int64_t>(hn) * a.d;
+      uint32_t o[32];
+      ptx::tmem_ld_32x32b_x32(tO + g * 32, o);
+      ptx::tmem_ld_wait();
+#pragma unroll
+      for (int e = 0; e < 32; ++e) o[e] = __float_as_uint(__uint_as_float(o[e]) * inv);
+      if (q < a.s) store_row_chunk<D>(orow, g * 32, o);
+    }
+  }
+  ptx::tc_fence_before();
+  __syncthreads();
+  if (warp == 2) {
+    ptx::tc_fence_after();
+    ptx::tmem_dealloc<512>(tmem);
+  }
+}
+
 // ====================================================================== column kernel
 // One CTA per (k-tile j, z).  Walks q-tiles i = j .. ntiles-1:
 //   S^T = K_j Q_i^T, dP^T = V_j dO_i^T (TMEM), P^T = exp(S^T - lse_q), dS^T = P^T (dP^T - D_q)/sqrt(d)
@@ -421,13 +676,22 @@ __global__ void __launch_bounds__(NT, 1)
     const uint32_t xb = ptx::smem_u32(X);
     const uint32_t lane_off = static_cast<uint32_t>(lq * 32) << 16;
     const uint32_t toff = lane_off + cg * 32;
+    // lse / D of the q-tile rows: warps 0-3 load them one tile ahead into registers (the
+    // global latency overlaps the previous tile) and publish them through shared memory
+    float lse_n = INFINITY, d_n = 0.f;
+    if (w < 4 && j * TILE + r < a.s) {
+      lse_n = a.lse[zs + j * TILE + r];
+      d_n = a.dsum[zs + j * TILE + r];
+    }
     for (int n = 0; n < ni; ++n) {
       const int q0 = (j + n) * TILE;
       ptx::named_bar_sync(1, 32 * NRW);  // previous q-tile's readers of lse_s / d_s are done
       if (w < 4) {
-        const int qq = q0 + r;
-        lse_s[r] = qq < a.s ? a.lse[zs + qq] : INFINITY;
-        d_s[r] = qq < a.s ? a.dsum[zs + qq] : 0.f;
+        lse_s[r] = lse_n;
+        d_s[r] = d_n;
+        const int qn = q0 + TILE + r;
+        lse_n = (n + 1 < ni && qn < a.s) ? a.lse[zs + qn] : INFINITY;
+        d_n = (n + 1 < ni && qn < a.s) ? a.dsum[zs + qn] : 0.f;
       }
       ptx::named_bar_sync(1, 32 * NRW);
       ptx::mbar_wait(s_full, n & 1);
@@ -517,6 +781,10 @@ constexpr int row_smem(int mode) {
          (mode == M_STATS ? 0 : 2 * ATOM) + 1024 + 1024;
 }
 template <int D>
+constexpr int fwd_smem() {
+  return 6 * AC<D>::TB + 4 * TILE * 4 + 1024 + 1024;
+}
+template <int D>
 constexpr int col_smem() {
   return 6 * AC<D>::TB + 2 * ATOM + 2 * TILE * 4 + 1024 + 1024;
 }
@@ -552,17 +820,15 @@ cudaError_t forward_d(const AttnArgs& a, cudaStream_t st) {
   k.ldo = a.h;
   k.col0 = 0;
   k.d = a.d;
+  constexpr int sf = fwd_smem<D>();
+  static_assert(fwd_smem<D>() <= 232448, "attention smem budget");
   static bool once = false;
-  constexpr int s0 = row_smem<D>(M_STATS), s1 = row_smem<D>(M_FWD);
   if (!once) {
-    cudaFuncSetAttribute(attn_row_kernel<D, M_STATS>, cudaFuncAttributeMaxDynamicSharedMemorySize, s0);
-    cudaFuncSetAttribute(attn_row_kernel<D, M_FWD>, cudaFuncAttributeMaxDynamicSharedMemorySize, s1);
+    cudaFuncSetAttribute(attn_fwd_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, sf);
     once = true;
   }
   dim3 grid(a.heads * a.batch, k.ntiles);  // z fastest: all heads' longest tiles go first
-  cudaError_t e = launch_pdl(attn_row_kernel<D, M_STATS>, grid, dim3(NT), s0, st, 1, mp.q, mp.k, mp.v, mp.dO, k);
-  if (e != cudaSuccess) return e;
-  return launch_pdl(attn_row_kernel<D, M_FWD>, grid, dim3(NT), s1, st, 1, mp.q, mp.k, mp.v, mp.dO, k);
+  return launch_pdl(attn_fwd_kernel<D>, grid, dim3(FWD_NT), sf, st, 1, mp.q, mp.k, mp.v, k);
 }
 
 template <int D>
@@ -604,6 +870,10 @@ cudaError_t backward_d(const AttnArgs& a, cudaStream_t st) {
 }  // namespace
 
 const char* attn_last_message() { return g_amsg.c_str(); }
+
+#ifdef SLIP_ATTN_PROBE
+void attn_probe_read(long long* out, int n) { cudaMemcpyFromSymbol(out, g_probe, n * sizeof(long long)); }
+#endif
 
 cudaError_t attn_forward(const AttnArgs& a, cudaStream_t s) {
   g_amsg.clear();

@@ -95,6 +95,8 @@ extern "C" slip_status slip_execute_schedule(slip_ctx* ctx, slip_comm* comm, con
   SLIP_CUDA(tpool.get(&t0));
   SLIP_CUDA(tpool.get(&t1));
   std::vector<std::pair<int, size_t>> marks;  // (phase, index of the begin event in tpool)
+  std::vector<std::pair<slip_trace_rec, size_t>> tmarks;  // trace records, begin event index
+  const bool tracing = ctx->trace_on;
   int64_t launches0 = ctx->launches;
 
   for (int run = 0; run < 2; ++run) {
@@ -135,6 +137,22 @@ extern "C" slip_status slip_execute_schedule(slip_ctx* ctx, slip_comm* comm, con
     };
     for (const slip_action& a : progs[me]) {
       const int ph = phase_of(a.kind);
+      // tracing: begin / end events on the stream the action runs on
+      cudaStream_t ts = cs;
+      if (a.kind == SLIP_ACT_RECV_X || a.kind == SLIP_ACT_RECV_DY) ts = xfer_stream(a.peer, me);
+      if (a.kind == SLIP_ACT_SEND_Y || a.kind == SLIP_ACT_SEND_DX) ts = xfer_stream(me, a.peer);
+      if (a.kind == SLIP_ACT_AR) ts = comm->ar_stream;
+      const bool tr = timed && tracing && !(a.kind == SLIP_ACT_AR && !comm->stage_comm);
+      size_t tb_idx = 0;
+      auto trace_begin = [&]() -> cudaError_t {
+        if (!tr) return cudaSuccess;
+        cudaEvent_t e0, e1;
+        cudaError_t r = tpool.get(&e0);
+        if (r == cudaSuccess) r = tpool.get(&e1);
+        if (r == cudaSuccess) r = cudaEventRecord(e0, ts);
+        tb_idx = tpool.next - 2;
+        return r;
+      };
       if (timed && ph >= 0) {
         cudaEvent_t tb, te;
         SLIP_CUDA(tpool.get(&tb));
@@ -147,6 +165,7 @@ extern "C" slip_status slip_execute_schedule(slip_ctx* ctx, slip_comm* comm, con
       switch (a.kind) {
         case SLIP_ACT_LOAD_X: {
           if (se->freed) SLIP_CUDA(cudaStreamWaitEvent(cs, se->freed, 0));
+          SLIP_CUDA(trace_begin());
           if (io && io->x_host) {
             SLIP_CUDA(cudaMemcpyAsync(sb->x, io->x_host[a.origin * m + a.mb], bytes, cudaMemcpyHostToDevice, cs));
           } else {
@@ -158,6 +177,7 @@ extern "C" slip_status slip_execute_schedule(slip_ctx* ctx, slip_comm* comm, con
         case SLIP_ACT_RECV_X: {
           cudaStream_t ps = xfer_stream(a.peer, me);
           if (se->freed) SLIP_CUDA(cudaStreamWaitEvent(ps, se->freed, 0));
+          SLIP_CUDA(trace_begin());
           ncclResult_t r = ncclRecv(sb->x, Th, ncclBfloat16, 0, xfer_comm(a.peer, me), ps);
           if (r != ncclSuccess) return nccl_status(r, "ncclRecv activation");
           SLIP_CUDA(chain(ps, cs));
@@ -165,11 +185,13 @@ extern "C" slip_status slip_execute_schedule(slip_ctx* ctx, slip_comm* comm, con
         }
         case SLIP_ACT_F:
           if (se->sent_y) SLIP_CUDA(cudaStreamWaitEvent(cs, se->sent_y, 0));
+          SLIP_CUDA(trace_begin());
           SLIP_TRY(slip_stage_forward(ctx, a.slot, sb->x, sb->dy, stream));
           break;
         case SLIP_ACT_SEND_Y: {
           cudaStream_t ps = xfer_stream(me, a.peer);
           SLIP_CUDA(chain(cs, ps));
+          SLIP_CUDA(trace_begin());
           ncclResult_t r = ncclSend(sb->dy, Th, ncclBfloat16, 1, xfer_comm(me, a.peer), ps);
           if (r != ncclSuccess) return nccl_status(r, "ncclSend activation");
           SLIP_CUDA(pool.get(&se->sent_y));
@@ -178,6 +200,7 @@ extern "C" slip_status slip_execute_schedule(slip_ctx* ctx, slip_comm* comm, con
         }
         case SLIP_ACT_LOSS: {
           bf16* target = ctx->ws.dy1;  // B's temporaries are free before the head runs
+          SLIP_CUDA(trace_begin());
           if (io && io->target_host) {
             SLIP_CUDA(
                 cudaMemcpyAsync(target, io->target_host[a.origin * m + a.mb], bytes, cudaMemcpyHostToDevice, cs));
@@ -192,6 +215,7 @@ extern "C" slip_status slip_execute_schedule(slip_ctx* ctx, slip_comm* comm, con
           cudaStream_t ps = xfer_stream(a.peer, me);
           if (se->sent_y) SLIP_CUDA(cudaStreamWaitEvent(ps, se->sent_y, 0));
           SLIP_CUDA(chain(cs, ps));  // slot.dy is no longer read by compute (F done)
+          SLIP_CUDA(trace_begin());
           ncclResult_t r = ncclRecv(sb->dy, Th, ncclBfloat16, 0, xfer_comm(a.peer, me), ps);
           if (r != ncclSuccess) return nccl_status(r, "ncclRecv gradient");
           SLIP_CUDA(chain(ps, cs));
@@ -201,6 +225,7 @@ extern "C" slip_status slip_execute_schedule(slip_ctx* ctx, slip_comm* comm, con
         case SLIP_ACT_BC: {
           // slot.dx is the send buffer of the input gradient: the previous occupant's send must be done
           if (se->sent_dx) SLIP_CUDA(cudaStreamWaitEvent(cs, se->sent_dx, 0));
+          SLIP_CUDA(trace_begin());
           void* dx = me_i > 0 ? static_cast<void*>(sb->dx) : nullptr;
           SLIP_TRY(slip_backward_input(ctx, a.slot, sb->dy, dx, a.accumulate & 1, stream));
           if (a.kind == SLIP_ACT_BC) {
@@ -214,6 +239,7 @@ extern "C" slip_status slip_execute_schedule(slip_ctx* ctx, slip_comm* comm, con
         case SLIP_ACT_SEND_DX: {
           cudaStream_t ps = xfer_stream(me, a.peer);
           SLIP_CUDA(chain(cs, ps));
+          SLIP_CUDA(trace_begin());
           ncclResult_t r = ncclSend(sb->dx, Th, ncclBfloat16, 1, xfer_comm(me, a.peer), ps);
           if (r != ncclSuccess) return nccl_status(r, "ncclSend gradient");
           SLIP_CUDA(pool.get(&se->sent_dx));
@@ -221,6 +247,7 @@ extern "C" slip_status slip_execute_schedule(slip_ctx* ctx, slip_comm* comm, con
           break;
         }
         case SLIP_ACT_W:
+          SLIP_CUDA(trace_begin());
           SLIP_TRY(slip_backward_weight(ctx, a.slot, a.accumulate, stream));
           SLIP_CUDA(pool.get(&se->freed));
           SLIP_CUDA(cudaEventRecord(se->freed, cs));
@@ -229,12 +256,14 @@ extern "C" slip_status slip_execute_schedule(slip_ctx* ctx, slip_comm* comm, con
         case SLIP_ACT_AR:
           if (comm->stage_comm) {
             SLIP_CUDA(chain(cs, comm->ar_stream));
+            SLIP_CUDA(trace_begin());
             SLIP_TRY(slip_grad_allreduce(ctx, comm, reinterpret_cast<slip_stream>(comm->ar_stream)));
             SLIP_CUDA(chain(comm->ar_stream, cs));
           }
           break;
         case SLIP_ACT_OPT:
           ctx->opt_step += 1;
+          SLIP_CUDA(trace_begin());
           SLIP_TRY(slip_optimizer_step(ctx, adam, ctx->opt_step, grad_scale, ctx->ws.nonfinite, stream));
           break;
         default:
@@ -242,6 +271,11 @@ extern "C" slip_status slip_execute_schedule(slip_ctx* ctx, slip_comm* comm, con
           return SLIP_EINVAL;
       }
       if (timed && ph >= 0) SLIP_CUDA(cudaEventRecord(tpool.ev[marks.back().second + 1], cs));
+      if (tr) {
+        SLIP_CUDA(cudaEventRecord(tpool.ev[tb_idx + 1], ts));
+        slip_trace_rec rec{a.kind, a.mb, a.origin, a.iter, a.peer, a.slot, 0.f, 0.f};
+        tmarks.push_back({rec, tb_idx});
+      }
     }
     // join every side stream back into the compute stream
     for (auto& kv : comm->pair_stream) SLIP_CUDA(chain(kv.second, cs));
@@ -259,6 +293,14 @@ extern "C" slip_status slip_execute_schedule(slip_ctx* ctx, slip_comm* comm, con
   out->total_ms = ms;
   out->period_ms = ms / iterations;
   out->n_kernels = ctx->launches - launches0;
+  if (tracing) {
+    ctx->trace.clear();
+    for (auto& tm : tmarks) {
+      SLIP_CUDA(cudaEventElapsedTime(&tm.first.begin_ms, t0, tpool.ev[tm.second]));
+      SLIP_CUDA(cudaEventElapsedTime(&tm.first.end_ms, t0, tpool.ev[tm.second + 1]));
+      ctx->trace.push_back(tm.first);
+    }
+  }
   for (const auto& mk : marks) {
     float e = 0.f;
     SLIP_CUDA(cudaEventElapsedTime(&e, tpool.ev[mk.second], tpool.ev[mk.second + 1]));
@@ -285,5 +327,19 @@ extern "C" slip_status slip_execute_schedule(slip_ctx* ctx, slip_comm* comm, con
   int32_t nf = 0;
   SLIP_CUDA(cudaMemcpy(&nf, ctx->ws.nonfinite, sizeof nf, cudaMemcpyDeviceToHost));
   out->nonfinite = nf;
+  return SLIP_OK;
+}
+
+extern "C" slip_status slip_set_trace(slip_ctx* ctx, int32_t enable) {
+  SLIP_CHECK(ctx, SLIP_EINVAL, "set_trace: ctx is NULL");
+  ctx->trace_on = enable != 0;
+  if (!ctx->trace_on) ctx->trace.clear();
+  return SLIP_OK;
+}
+
+extern "C" slip_status slip_get_trace(slip_ctx* ctx, slip_trace_rec* out, int64_t cap, int64_t* n) {
+  SLIP_CHECK(ctx && n, SLIP_EINVAL, "get_trace: NULL argument");
+  *n = static_cast<int64_t>(ctx->trace.size());
+  if (out && cap > 0) std::copy(ctx->trace.begin(), ctx->trace.begin() + std::min<int64_t>(cap, *n), out);
   return SLIP_OK;
 }

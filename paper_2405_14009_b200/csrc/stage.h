@@ -76,6 +76,8 @@ struct slip_ctx {
   std::vector<int> state;
   int64_t launches = 0;  // kernels enqueued through this context
   int64_t opt_step = 0;  // AdamW steps taken by the executor
+  bool trace_on = false;
+  std::vector<slip_trace_rec> trace;  // timeline of the last traced executor run
 };
 
 namespace slip {

@@ -7,7 +7,7 @@ import ctypes as C
 from dataclasses import dataclass
 
 from ._binding import (SlipError, call, lib, slip_adam, slip_cluster, slip_costs, slip_io, slip_model, slip_op,
-                       slip_plan_opts, slip_report, slip_swap)
+                       slip_plan_opts, slip_report, slip_swap, slip_trace_rec)
 
 
 def _ptr(t) -> C.c_void_p:
@@ -112,6 +112,20 @@ def assign(N, DP, m, live):
     out = (C.c_int32 * (N * m * DP))()
     call("slip_assign", C.byref(cl), out)
     return {(i, j, k): out[(i * m + j) * DP + k] for i in range(N) for j in range(m) for k in range(DP)}
+
+
+def set_trace(stage, enable=True):
+    call("slip_set_trace", stage.ctx, int(bool(enable)))
+
+
+def get_trace(stage):
+    """[(kind_name, mb, origin, iter, peer, slot, begin_ms, end_ms)] of the last traced run."""
+    from ._binding import ACTIONS
+    n = C.c_int64(0)
+    call("slip_get_trace", stage.ctx, None, 0, C.byref(n))
+    buf = (slip_trace_rec * max(1, n.value))()
+    call("slip_get_trace", stage.ctx, buf, n.value, C.byref(n))
+    return [(ACTIONS[r.kind], r.mb, r.origin, r.iter, r.peer, r.slot, r.begin_ms, r.end_ms) for r in buf[:n.value]]
 
 
 def set_sm_reserve(n: int):
