@@ -264,6 +264,17 @@ slip_status slip_synth_normal(void* out_bf16, int64_t n, uint64_t seed, uint64_t
 /* w_bf16 <- RNE(master) (after loading master weights). */
 slip_status slip_weights_from_master(slip_ctx* ctx, slip_stream s);
 
+/* Diagnostic entry to the fused causal attention kernels, for kernel-level parity
+ * tests (the stage step calls the same kernels).  qkv [batch*s, 3*heads*d] bf16
+ * (Q | K | V blocks, head-major columns), row-major.  backward = 0: out = O
+ * [batch*s, heads*d] bf16, lse [batch*heads, s] fp32 (log2 domain: log2 sum_k
+ * exp2(S_qk log2e / sqrt(d))).  backward = 1: o, d_o = O and dL/dO [batch*s,
+ * heads*d], lse from the forward, dsum [batch*heads, s] fp32 scratch (gets
+ * D = rowsum(dO * O)), out = dQKV [batch*s, 3*heads*d].  d in {32, 64, 80, 128};
+ * device pointers, 16-byte aligned. */
+slip_status slip_attention(int32_t s, int32_t heads, int32_t batch, int32_t d, const void* qkv, const void* o,
+                           const void* d_o, void* out, float* lse, float* dsum, int32_t backward, slip_stream st);
+
 /* Process-wide: persistent GEMM grids fill at most (#SMs - n) SMs, leaving n
  * SMs to kernels of other streams (the executor's NCCL transfers and stage
  * all-reduce run concurrently with compute; a persistent CTA that finds no free

@@ -129,6 +129,7 @@ SIGNATURES = {
     "slip_grad_allreduce": (C.c_int, [P, P, P]),
     "slip_comm_set_role": (C.c_int, [P, I32]),
     "slip_set_sm_reserve": (C.c_int, [I32]),
+    "slip_attention": (C.c_int, [I32, I32, I32, I32, P, P, P, P, P, P, I32, P]),
     "slip_set_trace": (C.c_int, [P, I32]),
     "slip_get_trace": (C.c_int, [P, C.POINTER(slip_trace_rec), I64, C.POINTER(I64)]),
     "slip_migrate_state": (C.c_int, [P, P, I32, I32, I64, P]),

@@ -23,9 +23,6 @@ namespace {
 
 constexpr int TILE = 128;
 constexpr int ATOM = 16384;  // 128 rows x 128 B (64 bf16 of the contiguous dimension)
-constexpr int CW0 = 4;       // first row warp
-constexpr int NRW = 16;      // row warps: 4 lane quarters x 4 column groups of 32
-constexpr int NT = 32 * (CW0 + NRW);
 
 __device__ __forceinline__ float max3(float a, float b, float c) {
   float r;
@@ -39,7 +36,6 @@ __device__ __forceinline__ float ex2(float x) {
   return y;
 }
 
-enum Mode : int { M_STATS = 0, M_FWD = 1, M_DQ = 2 };
 
 template <int D>
 struct AC {
@@ -62,6 +58,10 @@ struct KArgs {
   int64_t col0;  // column offset of the first output block (FWD: O; DQ: dQ; DKDV: dK)
   int64_t col1;  // DKDV: column offset of dV
   int d;
+  const __nv_bfloat16* o;   // DQ: attention output O [T, h] (for D = rowsum(dO O))
+  const __nv_bfloat16* dO;  // DQ: its gradient [T, h]
+  int64_t ldh;              // row stride of O / dO
+  float* dsum_w;            // DQ: D written here for the dK / dV kernel
 };
 
 // tile [128 rows][D] as a K-major operand (contraction over d), UMMA_K step kk
@@ -72,16 +72,9 @@ __device__ __forceinline__ uint64_t dk(uint32_t base, int kk) {
 __device__ __forceinline__ uint64_t dm(uint32_t base, int kk) {
   return ptx::smem_desc_sw128(base + kk * 2048, ATOM, 1024);
 }
-// byte offset of the 16-byte chunk `ch` (8 columns) of row r in a [128][128] K-major X tile
-__device__ __forceinline__ uint32_t xoff(int r, int ch) {
-  return (ch >> 3) * ATOM + r * 128 + (((ch & 7) ^ (r & 7)) << 4);
-}
 __device__ __forceinline__ uint32_t pack2(float a, float b) {
   __nv_bfloat162 v = __floats2bfloat162_rn(a, b);
   return *reinterpret_cast<uint32_t*>(&v);
-}
-__device__ __forceinline__ void st_shared_v4(uint32_t addr, uint32_t a, uint32_t b, uint32_t c, uint32_t d) {
-  asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "r"(a), "r"(b), "r"(c), "r"(d) : "memory");
 }
 // write 32 fp32 accumulator columns [c0, c0+32) of one output row as bf16 (cols < D)
 template <int D>
@@ -97,207 +90,6 @@ __device__ __forceinline__ void store_row_chunk(__nv_bfloat16* row, int c0, cons
       u.w = pack2(__uint_as_float(v[q * 8 + 6]), __uint_as_float(v[q * 8 + 7]));
       *reinterpret_cast<uint4*>(row + c) = u;
     }
-  }
-}
-
-// ====================================================================== row kernel
-// One CTA per (q-tile i, batch*head z).  STATS: lse; FWD: O = sum_j P_ij V_j;
-// DQ: dQ = sum_j dS_ij K_j.  j runs over the causal k-tiles 0..i.
-template <int D, int MODE>
-__global__ void __launch_bounds__(NT, 1)
-    attn_row_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
-                    const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmdO,
-                    const KArgs a) {
-  using C = AC<D>;
-  constexpr bool kV = MODE != M_STATS;     // stages carry V as well as K
-  constexpr bool kX = MODE != M_STATS;     // an X tile (P or dS) feeds a second MMA
-  constexpr int STAGE = kV ? 2 * C::TB : C::TB;
-  extern __shared__ __align__(1024) uint8_t smem_raw[];
-  uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint8_t* Qs = sm;
-  uint8_t* dOs = Qs + C::TB;
-  uint8_t* stg = dOs + (MODE == M_DQ ? C::TB : 0);
-  uint8_t* Xs = stg + 2 * STAGE;
-  uint64_t* bar = reinterpret_cast<uint64_t*>(Xs + (kX ? 2 * ATOM : 0));
-  uint64_t* q_full = bar;
-  uint64_t* kv_full = bar + 1;   // [2]
-  uint64_t* kv_empty = bar + 3;  // [2]
-  uint64_t* s_full = bar + 5;
-  uint64_t* s_empty = bar + 6;
-  uint64_t* x_full = bar + 7;
-  uint64_t* x_empty = bar + 8;
-  uint64_t* acc_full = bar + 9;
-  uint32_t* tholder = reinterpret_cast<uint32_t*>(bar + 10);
-
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int z = blockIdx.x, hn = z % a.heads, bi = z / a.heads;
-  const int i = a.ntiles - 1 - static_cast<int>(blockIdx.y);  // longest rows first (LPT order)
-  const int nj = i + 1;
-  const int q0 = i * TILE;
-
-  if (threadIdx.x == 0) {
-    ptx::mbar_init(q_full, 1);
-    for (int t = 0; t < 2; ++t) {
-      ptx::mbar_init(&kv_full[t], 1);
-      ptx::mbar_init(&kv_empty[t], 1);
-    }
-    ptx::mbar_init(s_full, 1);
-    ptx::mbar_init(s_empty, NRW);
-    ptx::mbar_init(x_full, NRW);
-    ptx::mbar_init(x_empty, 1);
-    ptx::mbar_init(acc_full, 1);
-    ptx::fence_mbar_init();
-  }
-  if (warp == 2) ptx::tmem_alloc<512>(tholder);
-  ptx::tc_fence_before();
-  __syncthreads();
-  ptx::tc_fence_after();
-  const uint32_t tmem = *tholder;
-  const uint32_t tS = tmem, tP = tmem + 128, tA = tmem + 256;
-  ptx::grid_dep_wait();  // PDL: the prologue above overlapped the previous kernel
-  // STATS: per column-group running (max, sum) of each row, merged at the end
-  __shared__ float2 stats[MODE == M_STATS ? 4 : 1][MODE == M_STATS ? TILE : 1];
-
-  if (warp == 0) {
-    if (lane == 0) {  // ------------------------------------------------ TMA producer
-      ptx::mbar_arrive_expect_tx(q_full, (MODE == M_DQ ? 2 : 1) * C::TB);
-      for (int t = 0; t < C::NA; ++t) {
-        ptx::tma_load_4d(&tmQ, Qs + t * ATOM, q_full, t * 64, q0, hn, bi);
-        if (MODE == M_DQ) ptx::tma_load_4d(&tmdO, dOs + t * ATOM, q_full, t * 64, q0, hn, bi);
-      }
-      for (int j = 0; j < nj; ++j) {
-        const int st = j & 1;
-        ptx::mbar_wait(&kv_empty[st], ((j >> 1) & 1) ^ 1);
-        uint8_t* ks = stg + st * STAGE;
-        ptx::mbar_arrive_expect_tx(&kv_full[st], STAGE);
-        for (int t = 0; t < C::NA; ++t) {
-          ptx::tma_load_4d(&tmK, ks + t * ATOM, &kv_full[st], t * 64, j * TILE, hn, bi);
-          if (kV) ptx::tma_load_4d(&tmV, ks + C::TB + t * ATOM, &kv_full[st], t * 64, j * TILE, hn, bi);
-        }
-      }
-    }
-  } else if (warp == 1) {
-    if (lane == 0) {  // ------------------------------------------------ MMA issuer
-      ptx::mbar_wait(q_full, 0);
-      ptx::tc_fence_after();
-      const uint32_t qb = ptx::smem_u32(Qs), ob = ptx::smem_u32(dOs), xb = ptx::smem_u32(Xs);
-      // software pipeline: S_j is issued before the second product of tile j-1
-      for (int j = 0; j <= nj; ++j) {
-        if (j < nj) {
-          const int st = j & 1;
-          ptx::mbar_wait(&kv_full[st], (j >> 1) & 1);
-          ptx::mbar_wait(s_empty, (j & 1) ^ 1);
-          ptx::tc_fence_after();
-          const uint32_t kb = ptx::smem_u32(stg + st * STAGE);
-#pragma unroll
-          for (int kk = 0; kk < C::KS; ++kk) ptx::tc_mma_f16(tS, dk(qb, kk), dk(kb, kk), C::IDESC_S, kk > 0);
-          if (MODE == M_DQ) {
-#pragma unroll
-            for (int kk = 0; kk < C::KS; ++kk)
-              ptx::tc_mma_f16(tP, dk(ob, kk), dk(kb + C::TB, kk), C::IDESC_S, kk > 0);
-          }
-          ptx::tc_commit(s_full);
-          if (!kX) ptx::tc_commit(&kv_empty[st]);
-        }
-        if (kX && j >= 1) {
-          const int jj = j - 1, st = jj & 1;
-          ptx::mbar_wait(x_full, jj & 1);
-          ptx::tc_fence_after();
-          const uint32_t sb = ptx::smem_u32(stg + st * STAGE);
-          const uint32_t bb = MODE == M_FWD ? sb + C::TB : sb;  // FWD: O += P V;  DQ: dQ += dS K
-#pragma unroll
-          for (int kk = 0; kk < TILE / 16; ++kk)
-            ptx::tc_mma_f16(tA, dk(xb, kk), dm(bb, kk), C::IDESC_O, (jj > 0 || kk > 0) ? 1u : 0u);
-          ptx::tc_commit(x_empty);
-          ptx::tc_commit(&kv_empty[st]);
-        }
-      }
-      if (kX) ptx::tc_commit(acc_full);
-    }
-  } else if (warp >= CW0) {  // ---------------------------------------- row warps
-    // warp w: TMEM lane quarter lq (= warp % 4, rows 32 lq .. 32 lq + 31) and column
-    // group cg (columns 32 cg .. 32 cg + 31 of every 128-wide tile)
-    const int w = warp - CW0;
-    const int lq = w & 3, cg = w >> 2;
-    const int r = lq * 32 + lane;
-    const int q = q0 + r;
-    const size_t zs = static_cast<size_t>(z) * a.s;
-    const float lrow = (MODE != M_STATS && q < a.s) ? a.lse[zs + q] : 0.f;
-    const float drow = (MODE == M_DQ && q < a.s) ? a.dsum[zs + q] : 0.f;
-    const uint32_t xb = ptx::smem_u32(Xs);
-    const uint32_t toff = (static_cast<uint32_t>(lq * 32) << 16) + cg * 32;
-    float m = -INFINITY, l = 0.f;
-    for (int j = 0; j < nj; ++j) {
-      ptx::mbar_wait(s_full, j & 1);
-      ptx::tc_fence_after();
-      uint32_t sv[32], pv[32];
-      ptx::tmem_ld_32x32b_x32(tS + toff, sv);
-      if (MODE == M_DQ) ptx::tmem_ld_32x32b_x32(tP + toff, pv);
-      ptx::tmem_ld_wait();
-      ptx::tc_fence_before();
-      __syncwarp();
-      if (lane == 0) ptx::mbar_arrive(s_empty);  // S / dP may be overwritten by the next tile's MMA
-      const int key0 = j * TILE + cg * 32;
-      const bool diag = key0 + 31 > q0;  // only the diagonal tile needs the causal mask
-      if (MODE == M_STATS) {
-        float cm = -INFINITY;
-#pragma unroll
-        for (int e = 0; e < 32; ++e)
-          if (!diag || key0 + e <= q) cm = fmaxf(cm, __uint_as_float(sv[e]) * a.sl2);
-        const float mn = fmaxf(m, cm);
-        if (mn != -INFINITY) {
-          float acc = 0.f;
-#pragma unroll
-          for (int e = 0; e < 32; ++e)
-            acc += (!diag || key0 + e <= q) ? ex2(__uint_as_float(sv[e]) * a.sl2 - mn) : 0.f;
-          l = (m == -INFINITY ? 0.f : l * ex2(m - mn)) + acc;
-          m = mn;
-        }
-      } else {
-        if (kX) ptx::mbar_wait(x_empty, (j & 1) ^ 1);
-        float x[32];
-#pragma unroll
-        for (int e = 0; e < 32; ++e) {
-          const float p = (!diag || key0 + e <= q) ? ex2(__uint_as_float(sv[e]) * a.sl2 - lrow) : 0.f;
-          x[e] = MODE == M_FWD ? p : p * (__uint_as_float(pv[e]) - drow) * a.scale;
-        }
-#pragma unroll
-        for (int g = 0; g < 4; ++g)
-          st_shared_v4(xb + xoff(r, cg * 4 + g), pack2(x[g * 8 + 0], x[g * 8 + 1]), pack2(x[g * 8 + 2], x[g * 8 + 3]),
-                       pack2(x[g * 8 + 4], x[g * 8 + 5]), pack2(x[g * 8 + 6], x[g * 8 + 7]));
-        ptx::fence_proxy_async_smem();
-        __syncwarp();
-        if (lane == 0) ptx::mbar_arrive(x_full);
-      }
-    }
-    if (MODE == M_STATS) {
-      stats[cg][r] = make_float2(m, l);
-      ptx::named_bar_sync(2, 32 * NRW);
-      if (cg == 0) {
-        float M = -INFINITY;
-        for (int g = 0; g < 4; ++g) M = fmaxf(M, stats[g][r].x);
-        float L = 0.f;
-        for (int g = 0; g < 4; ++g)
-          if (stats[g][r].x != -INFINITY) L += stats[g][r].y * ex2(stats[g][r].x - M);
-        if (q < a.s) a.lse[zs + q] = M + log2f(L);
-      }
-    } else {
-      ptx::mbar_wait(acc_full, 0);
-      ptx::tc_fence_after();
-      __nv_bfloat16* orow = a.out + (static_cast<int64_t>(bi) * a.s + q) * a.ldo + a.col0 + static_cast<int64_t>(hn) * a.d;
-      if (cg < C::OC) {
-        uint32_t v[32];
-        ptx::tmem_ld_32x32b_x32(tA + (static_cast<uint32_t>(lq * 32) << 16) + cg * 32, v);
-        ptx::tmem_ld_wait();
-        if (q < a.s) store_row_chunk<D>(orow, cg * 32, v);
-      }
-    }
-  }
-  ptx::tc_fence_before();
-  __syncthreads();
-  if (warp == 2) {
-    ptx::tc_fence_after();
-    ptx::tmem_dealloc<512>(tmem);
   }
 }
 
@@ -348,8 +140,8 @@ __global__ void __launch_bounds__(FWD_NT, 1)
   uint64_t* v_full = k_empty + KST;          // [VST]
   uint64_t* v_empty = v_full + VST;          // [VST]
   uint64_t* s_full = v_empty + VST;          // [2] per S buffer
-  uint64_t* p_full = s_full + 2;             // P of the current k-tile written (8 warps)
-  uint64_t* o_done = p_full + 1;             // PV of a k-tile complete
+  uint64_t* p_full = s_full + 2;             // [2] P of a k-tile written, per S buffer
+  uint64_t* o_done = p_full + 2;             // PV of a k-tile complete
   uint32_t* tholder = reinterpret_cast<uint32_t*>(o_done + 1);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -369,7 +161,8 @@ __global__ void __launch_bounds__(FWD_NT, 1)
     }
     ptx::mbar_init(&s_full[0], 1);
     ptx::mbar_init(&s_full[1], 1);
-    ptx::mbar_init(p_full, 16);
+    ptx::mbar_init(&p_full[0], 16);
+    ptx::mbar_init(&p_full[1], 16);
     ptx::mbar_init(o_done, 1);
     ptx::fence_mbar_init();
   }
@@ -408,7 +201,7 @@ __global__ void __launch_bounds__(FWD_NT, 1)
       }
     }
   } else if (warp == 1) {
-    if (lane == 0) {  // ------------------------------------------------ MMA issuer
+    {  // ------------------------------------------------ MMA issuer (warp-wide, elected lane issues)
       ptx::mbar_wait(q_full, 0);
       const uint32_t qb = ptx::smem_u32(Qs), kb0 = ptx::smem_u32(Ks), vb0 = ptx::smem_u32(Vs);
       auto mma_s = [&](int j) {  // S[j % 2] = Q K_j^T
@@ -418,26 +211,26 @@ __global__ void __launch_bounds__(FWD_NT, 1)
         const uint32_t kb = kb0 + st * C::TB;
 #pragma unroll
         for (int kk = 0; kk < C::KS; ++kk)
-          ptx::tc_mma_f16(tmem + (j & 1) * 128, dk(qb, kk), dk(kb, kk), C::IDESC_S, kk > 0);
-        ptx::tc_commit(&s_full[j & 1]);
-        ptx::tc_commit(&k_empty[st]);
+          ptx::tc_mma_f16_w(tmem + (j & 1) * 128, dk(qb, kk), dk(kb, kk), C::IDESC_S, kk > 0);
+        ptx::tc_commit_w(&s_full[j & 1]);
+        ptx::tc_commit_w(&k_empty[st]);
       };
       mma_s(0);
       if (nj > 1) mma_s(1);
       for (int j = 0; j < nj; ++j) {
         const int st = j % VST;
-        ptx::mbar_wait(p_full, j & 1);
+        ptx::mbar_wait(&p_full[j & 1], (j >> 1) & 1);
         ptx::mbar_wait(&v_full[st], (j / VST) & 1);
         PROBE(100 + j);
         ptx::tc_fence_after();
         const uint32_t vb = vb0 + st * C::TB;
 #pragma unroll
         for (int kk = 0; kk < TILE / 16; ++kk)  // O += P V_j, P (bf16 pairs) from TMEM
-          ptx::tc_mma_f16_ts(tmem + 256, tmem + (j & 1) * 128 + kk * 8, dm(vb, kk), C::IDESC_O,
+          ptx::tc_mma_f16_ts_w(tmem + 256, tmem + (j & 1) * 128 + kk * 8, dm(vb, kk), C::IDESC_O,
                              (j > 0 || kk > 0) ? 1u : 0u);
-        ptx::tc_commit(o_done);
-        ptx::tc_commit(&v_empty[st]);
-        if (j + 2 < nj) mma_s(j + 2);  // into the S buffer PV_j has just consumed (in order)
+        ptx::tc_commit_w(o_done);
+        ptx::tc_commit_w(&v_empty[st]);
+        if (j + 2 < nj) mma_s(j + 2);  // into the S buffer PV_j reads P from (MMAs execute in order)
       }
     }
   } else if (warp >= 4) {  // ------------------------------------------ softmax warps
@@ -520,7 +313,7 @@ __global__ void __launch_bounds__(FWD_NT, 1)
       ptx::tmem_st_wait();
       ptx::tc_fence_before();
       __syncwarp();
-      if (lane == 0) ptx::mbar_arrive(p_full);
+      if (lane == 0) ptx::mbar_arrive(&p_full[j & 1]);
       if (lq == 0 && lane == 0 && g < 2) PROBE(600 + 300 * g + j);
     }
     // total l over the 4 column groups, then O / l and lse
@@ -550,55 +343,83 @@ __global__ void __launch_bounds__(FWD_NT, 1)
   }
 }
 
-// ====================================================================== column kernel
-// One CTA per (k-tile j, z).  Walks q-tiles i = j .. ntiles-1:
-//   S^T = K_j Q_i^T, dP^T = V_j dO_i^T (TMEM), P^T = exp(S^T - lse_q), dS^T = P^T (dP^T - D_q)/sqrt(d)
-//   dV += P^T dO_i, dK += dS^T Q_i (TMEM accumulators).
+// ====================================================================== backward kernels
+// Both walk 64-wide half tiles so that S / dP of step h+1 are computed (double buffer in
+// TMEM) while the softmax warps form dS of step h; P and dS are written back to TMEM as
+// bf16 pairs over the columns they came from and read there by the next MMA (A operand).
+// Warp 0 TMA, warp 1 MMA, warp 2 TMEM allocator, warps 4-11 "softmax" warps: lane
+// quarter lq = warp % 4 (32 TMEM lanes = 32 tile rows), column group g (32 of the 64
+// columns of a half tile).  A group's bf16 pairs go to the first 16 of its own 32
+// columns, so no warp overwrites columns another warp has not read yet.
+constexpr int HT = 64;          // rows of a half tile
+constexpr int HATOM = 8192;     // 64 rows x 128 B
+constexpr int BWD_NT = 32 * 12;
+
 template <int D>
-__global__ void __launch_bounds__(NT, 1)
-    attn_col_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
-                    const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmdO,
-                    const KArgs a) {
+struct HC {
+  static constexpr int HB = AC<D>::NA * HATOM;  // bytes of one [64][D] half tile
+  static constexpr uint32_t IDESC_S = ptx::idesc_bf16_f32(128, HT, false, false);  // N = 64, K-major x2
+  static constexpr uint32_t IDESC_ACC = ptx::idesc_bf16_f32(128, D, false, true);  // A TMEM, B MN-major
+};
+// [64 rows][D] half tile as a K-major operand (contraction over d), step kk
+__device__ __forceinline__ uint64_t hk(uint32_t base, int kk) {
+  return ptx::smem_desc_sw128(base + (kk >> 2) * HATOM + (kk & 3) * 32, 16, 1024);
+}
+// [64 rows][D] half tile as an MN-major operand (contraction over its 64 rows), step kk
+__device__ __forceinline__ uint64_t hm(uint32_t base, int kk) {
+  return ptx::smem_desc_sw128(base + kk * 2048, HATOM, 1024);
+}
+// TMEM column of the bf16 A operand (64 contraction indices, 2 per column) for step kk:
+// group g = kk / 2 wrote its 32 indices to columns [32 g, 32 g + 16)
+__device__ __forceinline__ uint32_t acol(int kk) { return 32 * (kk >> 1) + (kk & 1) * 8; }
+
+// ---------------------------------------------------------------- dQ (+ D = rowsum(dO O))
+// One CTA per (q-tile i, z), longest first.  S_h = Q K_h^T, dP_h = dO V_h^T over the 64-key
+// half tiles h, dS = P (dP - D) / sqrt(d) with P = exp2(S log2e/sqrt(d) - lse), dQ += dS K_h.
+// D of the tile's rows is computed here first (and stored for the dK / dV kernel).
+template <int D>
+__global__ void __launch_bounds__(BWD_NT, 1)
+    attn_dq_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK64,
+                   const __grid_constant__ CUtensorMap tmV64, const __grid_constant__ CUtensorMap tmdO,
+                   const KArgs a) {
   using C = AC<D>;
+  using H = HC<D>;
+  constexpr int NST = 3;
+  constexpr int STG = 2 * H::HB;  // K_h | V_h
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint8_t* Ks = sm;
-  uint8_t* Vs = Ks + C::TB;
-  uint8_t* QD = Vs + C::TB;       // 2 stages of {Q_i, dO_i}
-  uint8_t* X = QD + 4 * C::TB;    // P^T, then (after dV consumed it) dS^T
-  float* lse_s = reinterpret_cast<float*>(X + 2 * ATOM);
-  float* d_s = lse_s + TILE;
-  uint64_t* bar = reinterpret_cast<uint64_t*>(d_s + TILE);
-  uint64_t* kv_full = bar;
-  uint64_t* qd_full = bar + 1;   // [2]
-  uint64_t* qd_empty = bar + 3;  // [2]
-  uint64_t* s_full = bar + 5;
-  uint64_t* s_empty = bar + 6;
-  uint64_t* xp_full = bar + 7;   // P^T written
-  uint64_t* xs_full = bar + 8;   // dS^T written
-  uint64_t* xp_free = bar + 9;   // dV MMA has read P^T
-  uint64_t* x_free = bar + 10;   // dK MMA has read dS^T
-  uint64_t* acc_full = bar + 11;
-  uint32_t* tholder = reinterpret_cast<uint32_t*>(bar + 12);
+  uint8_t* Qs = sm;
+  uint8_t* dOs = Qs + C::TB;
+  uint8_t* ring = dOs + C::TB;  // [NST][STG]
+  float* red = reinterpret_cast<float*>(ring + NST * STG);  // [2][128]
+  uint64_t* bar = reinterpret_cast<uint64_t*>(red + 2 * TILE);
+  uint64_t* q_full = bar;
+  uint64_t* kv_full = bar + 1;         // [NST]
+  uint64_t* kv_empty = kv_full + NST;  // [NST]
+  uint64_t* s_full = kv_empty + NST;   // [2]
+  uint64_t* x_full = s_full + 2;       // [2] dS of a step written (8 warps), per buffer
+  uint64_t* acc_full = x_full + 2;
+  uint32_t* tholder = reinterpret_cast<uint32_t*>(acc_full + 1);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int z = blockIdx.x, hn = z % a.heads, bi = z / a.heads;
-  const int j = blockIdx.y;  // k-tile; longest walks (small j) first (LPT order)
-  const int k0 = j * TILE;
-  const int ni = a.ntiles - j;
+  const int i = a.ntiles - 1 - static_cast<int>(blockIdx.y);  // longest rows first
+  const int q0 = i * TILE;
+  // key half tiles covering keys <= min(q0 + 127, s - 1): a box entirely past the end of
+  // the sequence is never loaded
+  const int kend = q0 + TILE < a.s ? q0 + TILE : a.s;
+  const int nh = (kend + HT - 1) / HT;
 
   if (threadIdx.x == 0) {
-    ptx::mbar_init(kv_full, 1);
-    for (int t = 0; t < 2; ++t) {
-      ptx::mbar_init(&qd_full[t], 1);
-      ptx::mbar_init(&qd_empty[t], 1);
+    ptx::mbar_init(q_full, 1);
+    for (int t = 0; t < NST; ++t) {
+      ptx::mbar_init(&kv_full[t], 1);
+      ptx::mbar_init(&kv_empty[t], 1);
     }
-    ptx::mbar_init(s_full, 1);
-    ptx::mbar_init(s_empty, NRW);
-    ptx::mbar_init(xp_full, NRW);
-    ptx::mbar_init(xs_full, NRW);
-    ptx::mbar_init(xp_free, 1);
-    ptx::mbar_init(x_free, 1);
+    ptx::mbar_init(&s_full[0], 1);
+    ptx::mbar_init(&s_full[1], 1);
+    ptx::mbar_init(&x_full[0], 8);
+    ptx::mbar_init(&x_full[1], 8);
     ptx::mbar_init(acc_full, 1);
     ptx::fence_mbar_init();
   }
@@ -607,139 +428,130 @@ __global__ void __launch_bounds__(NT, 1)
   __syncthreads();
   ptx::tc_fence_after();
   const uint32_t tmem = *tholder;
-  const uint32_t tS = tmem, tP = tmem + 128, tV = tmem + 256, tK = tmem + 384;
-  ptx::grid_dep_wait();  // PDL: the prologue above overlapped the previous kernel
+  ptx::grid_dep_wait();
+  if (threadIdx.x == 0) PROBE(1999);
 
   if (warp == 0) {
     if (lane == 0) {  // ------------------------------------------------ TMA producer
-      ptx::mbar_arrive_expect_tx(kv_full, 2 * C::TB);
+      ptx::mbar_arrive_expect_tx(q_full, 2 * C::TB);
       for (int t = 0; t < C::NA; ++t) {
-        ptx::tma_load_4d(&tmK, Ks + t * ATOM, kv_full, t * 64, k0, hn, bi);
-        ptx::tma_load_4d(&tmV, Vs + t * ATOM, kv_full, t * 64, k0, hn, bi);
+        ptx::tma_load_4d(&tmQ, Qs + t * ATOM, q_full, t * 64, q0, hn, bi);
+        ptx::tma_load_4d(&tmdO, dOs + t * ATOM, q_full, t * 64, q0, hn, bi);
       }
-      for (int n = 0; n < ni; ++n) {
-        const int q0 = (j + n) * TILE, st = n & 1;
-        uint8_t* qs = QD + st * 2 * C::TB;
-        ptx::mbar_wait(&qd_empty[st], ((n >> 1) & 1) ^ 1);
-        ptx::mbar_arrive_expect_tx(&qd_full[st], 2 * C::TB);
+      for (int h = 0; h < nh; ++h) {
+        const int st = h % NST;
+        ptx::mbar_wait(&kv_empty[st], ((h / NST) & 1) ^ 1);
+        uint8_t* kb = ring + st * STG;
+        ptx::mbar_arrive_expect_tx(&kv_full[st], STG);
         for (int t = 0; t < C::NA; ++t) {
-          ptx::tma_load_4d(&tmQ, qs + t * ATOM, &qd_full[st], t * 64, q0, hn, bi);
-          ptx::tma_load_4d(&tmdO, qs + C::TB + t * ATOM, &qd_full[st], t * 64, q0, hn, bi);
+          ptx::tma_load_4d(&tmK64, kb + t * HATOM, &kv_full[st], t * 64, h * HT, hn, bi);
+          ptx::tma_load_4d(&tmV64, kb + H::HB + t * HATOM, &kv_full[st], t * 64, h * HT, hn, bi);
         }
       }
     }
   } else if (warp == 1) {
-    if (lane == 0) {  // ------------------------------------------------ MMA issuer
-      const uint32_t kb = ptx::smem_u32(Ks), vb = ptx::smem_u32(Vs), qdb = ptx::smem_u32(QD),
-                     xb = ptx::smem_u32(X);
-      // S^T and dP^T of q-tile n (into TMEM once the row warps have read the previous ones)
-      auto issue_s = [&](int n) {
-        const int st = n & 1;
-        const uint32_t qb = qdb + st * 2 * C::TB, ob = qb + C::TB;
-        ptx::mbar_wait(&qd_full[st], (n >> 1) & 1);
-        ptx::mbar_wait(s_empty, (n & 1) ^ 1);
+    {  // ------------------------------------------------ MMA issuer (warp-wide, elected lane issues)
+      ptx::mbar_wait(q_full, 0);
+      const uint32_t qb = ptx::smem_u32(Qs), ob = ptx::smem_u32(dOs), rb = ptx::smem_u32(ring);
+      auto mma_sd = [&](int h) {  // S_b = Q K_h^T, dP_b = dO V_h^T  (b = h & 1)
+        const int st = h % NST;
+        ptx::mbar_wait(&kv_full[st], (h / NST) & 1);
         ptx::tc_fence_after();
+        const uint32_t kb = rb + st * STG, vb = kb + H::HB, tS = tmem + (h & 1) * 128;
 #pragma unroll
-        for (int kk = 0; kk < C::KS; ++kk) ptx::tc_mma_f16(tS, dk(kb, kk), dk(qb, kk), C::IDESC_S, kk > 0);
+        for (int kk = 0; kk < C::KS; ++kk) ptx::tc_mma_f16_w(tS, dk(qb, kk), hk(kb, kk), H::IDESC_S, kk > 0);
 #pragma unroll
-        for (int kk = 0; kk < C::KS; ++kk) ptx::tc_mma_f16(tP, dk(vb, kk), dk(ob, kk), C::IDESC_S, kk > 0);
-        ptx::tc_commit(s_full);
+        for (int kk = 0; kk < C::KS; ++kk) ptx::tc_mma_f16_w(tS + 64, dk(ob, kk), hk(vb, kk), H::IDESC_S, kk > 0);
+        ptx::tc_commit_w(&s_full[h & 1]);
       };
-      ptx::mbar_wait(kv_full, 0);
-      issue_s(0);
-      for (int n = 0; n < ni; ++n) {
-        const int st = n & 1;
-        const uint32_t qb = qdb + st * 2 * C::TB, ob = qb + C::TB;
-        ptx::mbar_wait(xp_full, n & 1);
+      mma_sd(0);
+      if (nh > 1) mma_sd(1);
+      for (int h = 0; h < nh; ++h) {
+        const int st = h % NST;
+        ptx::mbar_wait(&x_full[h & 1], (h >> 1) & 1);
+        PROBE(2000 + h);
         ptx::tc_fence_after();
+        const uint32_t kb = rb + st * STG, tX = tmem + (h & 1) * 128;
 #pragma unroll
-        for (int kk = 0; kk < TILE / 16; ++kk)
-          ptx::tc_mma_f16(tV, dk(xb, kk), dm(ob, kk), C::IDESC_O, (n > 0 || kk > 0) ? 1u : 0u);
-        ptx::tc_commit(xp_free);
-        if (n + 1 < ni) issue_s(n + 1);  // overlaps the row warps' dS^T work of tile n
-        ptx::mbar_wait(xs_full, n & 1);
-        ptx::tc_fence_after();
-#pragma unroll
-        for (int kk = 0; kk < TILE / 16; ++kk)
-          ptx::tc_mma_f16(tK, dk(xb, kk), dm(qb, kk), C::IDESC_O, (n > 0 || kk > 0) ? 1u : 0u);
-        ptx::tc_commit(x_free);
-        ptx::tc_commit(&qd_empty[st]);
+        for (int kk = 0; kk < HT / 16; ++kk)  // dQ += dS K_h, dS (bf16 pairs) from TMEM
+          ptx::tc_mma_f16_ts_w(tmem + 256, tX + acol(kk), hm(kb, kk), H::IDESC_ACC, (h > 0 || kk > 0) ? 1u : 0u);
+        ptx::tc_commit_w(&kv_empty[st]);
+        if (h + 2 < nh) mma_sd(h + 2);  // into the buffer dQ_h reads dS from (MMAs execute in order)
       }
-      ptx::tc_commit(acc_full);
+      ptx::tc_commit_w(acc_full);
     }
-  } else if (warp >= CW0) {  // ---------------------------------------- row warps (rows = keys)
-    const int w = warp - CW0;
-    const int lq = w & 3, cg = w >> 2;  // lane quarter (rows) and column group (q columns)
+  } else if (warp >= 4) {  // ------------------------------------------ dS warps
+    const int lq = warp & 3, g = (warp - 4) >> 2;
     const int r = lq * 32 + lane;
-    const int key = k0 + r;
+    const int q = q0 + r;
     const size_t zs = static_cast<size_t>(z) * a.s;
-    const uint32_t xb = ptx::smem_u32(X);
     const uint32_t lane_off = static_cast<uint32_t>(lq * 32) << 16;
-    const uint32_t toff = lane_off + cg * 32;
-    // lse / D of the q-tile rows: warps 0-3 load them one tile ahead into registers (the
-    // global latency overlaps the previous tile) and publish them through shared memory
-    float lse_n = INFINITY, d_n = 0.f;
-    if (w < 4 && j * TILE + r < a.s) {
-      lse_n = a.lse[zs + j * TILE + r];
-      d_n = a.dsum[zs + j * TILE + r];
-    }
-    for (int n = 0; n < ni; ++n) {
-      const int q0 = (j + n) * TILE;
-      ptx::named_bar_sync(1, 32 * NRW);  // previous q-tile's readers of lse_s / d_s are done
-      if (w < 4) {
-        lse_s[r] = lse_n;
-        d_s[r] = d_n;
-        const int qn = q0 + TILE + r;
-        lse_n = (n + 1 < ni && qn < a.s) ? a.lse[zs + qn] : INFINITY;
-        d_n = (n + 1 < ni && qn < a.s) ? a.dsum[zs + qn] : 0.f;
+    // D = rowsum(dO * O) over this head's d columns: half of them per column group
+    float dpart = 0.f;
+    if (q < a.s) {
+      const __nv_bfloat16* orow = a.o + (static_cast<int64_t>(bi) * a.s + q) * a.ldh + static_cast<int64_t>(hn) * a.d;
+      const __nv_bfloat16* grow = a.dO + (static_cast<int64_t>(bi) * a.s + q) * a.ldh + static_cast<int64_t>(hn) * a.d;
+      for (int c = g * 8; c < D; c += 16) {
+        float ov[8], gv[8];
+        const uint4 ou = *reinterpret_cast<const uint4*>(orow + c);
+        const uint4 gu = *reinterpret_cast<const uint4*>(grow + c);
+        const __nv_bfloat162* o2 = reinterpret_cast<const __nv_bfloat162*>(&ou);
+        const __nv_bfloat162* g2 = reinterpret_cast<const __nv_bfloat162*>(&gu);
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const float2 x = __bfloat1622float2(o2[e]), y = __bfloat1622float2(g2[e]);
+          ov[2 * e] = x.x, ov[2 * e + 1] = x.y, gv[2 * e] = y.x, gv[2 * e + 1] = y.y;
+        }
+#pragma unroll
+        for (int e = 0; e < 8; ++e) dpart = fmaf(ov[e], gv[e], dpart);
       }
-      ptx::named_bar_sync(1, 32 * NRW);
-      ptx::mbar_wait(s_full, n & 1);
+    }
+    red[g * TILE + r] = dpart;
+    ptx::named_bar_sync(1 + lq, 64);
+    const float drow = red[r] + red[TILE + r];
+    if (g == 0 && q < a.s) a.dsum_w[zs + q] = drow;
+    const float lrow = q < a.s ? a.lse[zs + q] : 0.f;
+    for (int h = 0; h < nh; ++h) {
+      const uint32_t tS = tmem + (h & 1) * 128 + lane_off;
+      ptx::mbar_wait(&s_full[h & 1], (h >> 1) & 1);
+      if (lq == 0 && lane == 0) PROBE(2100 + 100 * g + h);
       ptx::tc_fence_after();
       uint32_t sv[32], pv[32];
-      ptx::tmem_ld_32x32b_x32(tS + toff, sv);
-      ptx::tmem_ld_32x32b_x32(tP + toff, pv);
+      ptx::tmem_ld_32x32b_x32(tS + g * 32, sv);
+      ptx::tmem_ld_32x32b_x32(tS + 64 + g * 32, pv);
       ptx::tmem_ld_wait();
+      const int key0 = h * HT + g * 32;
+      const bool diag = key0 + 31 > q0;  // only half tiles reaching the diagonal need the mask
+      uint32_t xk[16];
+#pragma unroll
+      for (int e = 0; e < 16; ++e) {
+        float x0 = ex2(fmaf(__uint_as_float(sv[2 * e]), a.sl2, -lrow)) * (__uint_as_float(pv[2 * e]) - drow) * a.scale;
+        float x1 =
+            ex2(fmaf(__uint_as_float(sv[2 * e + 1]), a.sl2, -lrow)) * (__uint_as_float(pv[2 * e + 1]) - drow) * a.scale;
+        if (diag) {  // select after the arithmetic: nothing computed for a masked key survives
+          x0 = key0 + 2 * e <= q ? x0 : 0.f;
+          x1 = key0 + 2 * e + 1 <= q ? x1 : 0.f;
+        }
+        xk[e] = pack2(x0, x1);
+      }
+      ptx::tmem_st_32x32b_x16(tS + g * 32, xk);
+      ptx::tmem_st_wait();
       ptx::tc_fence_before();
       __syncwarp();
-      if (lane == 0) ptx::mbar_arrive(s_empty);
-      const bool diag = n == 0;  // key tile == query tile: causal mask inside the tile
-      float pt[32], st[32];
-#pragma unroll
-      for (int e = 0; e < 32; ++e) {
-        const int qi = cg * 32 + e;
-        const float p = (!diag || key <= q0 + qi) ? ex2(__uint_as_float(sv[e]) * a.sl2 - lse_s[qi]) : 0.f;
-        pt[e] = p;
-        st[e] = p * (__uint_as_float(pv[e]) - d_s[qi]) * a.scale;
-      }
-      ptx::mbar_wait(x_free, (n & 1) ^ 1);  // the previous tile's dK MMA has read X
-#pragma unroll
-      for (int g = 0; g < 4; ++g)
-        st_shared_v4(xb + xoff(r, cg * 4 + g), pack2(pt[g * 8 + 0], pt[g * 8 + 1]), pack2(pt[g * 8 + 2], pt[g * 8 + 3]),
-                     pack2(pt[g * 8 + 4], pt[g * 8 + 5]), pack2(pt[g * 8 + 6], pt[g * 8 + 7]));
-      ptx::fence_proxy_async_smem();
-      __syncwarp();
-      if (lane == 0) ptx::mbar_arrive(xp_full);
-      ptx::mbar_wait(xp_free, n & 1);  // dV MMA has read P^T
-#pragma unroll
-      for (int g = 0; g < 4; ++g)
-        st_shared_v4(xb + xoff(r, cg * 4 + g), pack2(st[g * 8 + 0], st[g * 8 + 1]), pack2(st[g * 8 + 2], st[g * 8 + 3]),
-                     pack2(st[g * 8 + 4], st[g * 8 + 5]), pack2(st[g * 8 + 6], st[g * 8 + 7]));
-      ptx::fence_proxy_async_smem();
-      __syncwarp();
-      if (lane == 0) ptx::mbar_arrive(xs_full);
+      if (lane == 0) ptx::mbar_arrive(&x_full[h & 1]);  // per buffer: a warp one step ahead
+                                                        // must not count toward this step
+      if (lq == 0 && lane == 0) PROBE(2300 + 100 * g + h);
     }
     ptx::mbar_wait(acc_full, 0);
     ptx::tc_fence_after();
-    const int64_t rowoff = (static_cast<int64_t>(bi) * a.s + key) * a.ldo + static_cast<int64_t>(hn) * a.d;
-    if (cg < C::OC) {
+    __nv_bfloat16* orow = a.out + (static_cast<int64_t>(bi) * a.s + q) * a.ldo + a.col0 + static_cast<int64_t>(hn) * a.d;
+#pragma unroll
+    for (int c = 0; c < C::OC; ++c) {
+      if ((c & 1) != g) continue;
       uint32_t v[32];
-      ptx::tmem_ld_32x32b_x32(tK + lane_off + cg * 32, v);
+      ptx::tmem_ld_32x32b_x32(tmem + 256 + lane_off + c * 32, v);
       ptx::tmem_ld_wait();
-      if (key < a.s) store_row_chunk<D>(a.out + rowoff + a.col0, cg * 32, v);
-      ptx::tmem_ld_32x32b_x32(tV + lane_off + cg * 32, v);
-      ptx::tmem_ld_wait();
-      if (key < a.s) store_row_chunk<D>(a.out + rowoff + a.col1, cg * 32, v);
+      if (q < a.s) store_row_chunk<D>(orow, c * 32, v);
     }
   }
   ptx::tc_fence_before();
@@ -750,47 +562,213 @@ __global__ void __launch_bounds__(NT, 1)
   }
 }
 
-// D[z, q] = sum_d dO[q, hn*d + dd] * O[q, hn*d + dd]; one warp per (token, head)
-__global__ void __launch_bounds__(256) attn_dsum_kernel(const __nv_bfloat16* __restrict__ o,
-                                                        const __nv_bfloat16* __restrict__ dO, float* __restrict__ dsum,
-                                                        int s, int heads, int d, int64_t h, int rows) {
-  ptx::grid_dep_wait();
-  const int gw = blockIdx.x * 8 + (threadIdx.x >> 5);
-  const int lane = threadIdx.x & 31;
-  if (gw >= rows * heads) return;
-  const int t = gw / heads, hn = gw % heads;
-  const int bi = t / s, qq = t % s;
-  const __nv_bfloat16* op = o + static_cast<int64_t>(t) * h + static_cast<int64_t>(hn) * d;
-  const __nv_bfloat16* gp = dO + static_cast<int64_t>(t) * h + static_cast<int64_t>(hn) * d;
-  float acc = 0.f;
-  for (int e = lane * 2; e < d; e += 64) {
-    const float2 a = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(op + e));
-    const float2 b = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(gp + e));
-    acc += a.x * b.x + a.y * b.y;
+// ---------------------------------------------------------------- dK, dV
+// One CTA per (k-tile j, z), longest walks first.  Over the 64-query half tiles h >= the
+// diagonal: S^T = K_j Q_h^T, dP^T = V_j dO_h^T, P^T = exp2(S^T log2e/sqrt(d) - lse_q),
+// dS^T = P^T (dP^T - D_q) / sqrt(d);  dV += P^T dO_h,  dK += dS^T Q_h.
+template <int D>
+__global__ void __launch_bounds__(BWD_NT, 1)
+    attn_dkdv_kernel(const __grid_constant__ CUtensorMap tmQ64, const __grid_constant__ CUtensorMap tmK,
+                     const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmdO64,
+                     const KArgs a) {
+  using C = AC<D>;
+  using H = HC<D>;
+  constexpr int NST = 3;
+  constexpr int STG = 2 * H::HB;  // Q_h | dO_h
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* Ks = sm;
+  uint8_t* Vs = Ks + C::TB;
+  uint8_t* ring = Vs + C::TB;  // [NST][STG]
+  float* cv = reinterpret_cast<float*>(ring + NST * STG);  // [8 warps][2][32] lse / D of the columns
+  uint64_t* bar = reinterpret_cast<uint64_t*>(cv + 8 * 64);
+  uint64_t* kv_full = bar;
+  uint64_t* qd_full = bar + 1;         // [NST]
+  uint64_t* qd_empty = qd_full + NST;  // [NST]
+  uint64_t* s_full = qd_empty + NST;   // [2]
+  uint64_t* x_full = s_full + 2;       // [2] P^T, dS^T of a step written (8 warps), per buffer
+  uint64_t* acc_full = x_full + 2;
+  uint32_t* tholder = reinterpret_cast<uint32_t*>(acc_full + 1);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int z = blockIdx.x, hn = z % a.heads, bi = z / a.heads;
+  const int j = blockIdx.y;  // k-tile; small j (longest walks) first
+  const int k0 = j * TILE;
+  const int nh = (a.s - k0 + HT - 1) / HT;  // query half tiles from the diagonal to the end
+
+  if (threadIdx.x == 0) {
+    ptx::mbar_init(kv_full, 1);
+    for (int t = 0; t < NST; ++t) {
+      ptx::mbar_init(&qd_full[t], 1);
+      ptx::mbar_init(&qd_empty[t], 1);
+    }
+    ptx::mbar_init(&s_full[0], 1);
+    ptx::mbar_init(&s_full[1], 1);
+    ptx::mbar_init(&x_full[0], 8);
+    ptx::mbar_init(&x_full[1], 8);
+    ptx::mbar_init(acc_full, 1);
+    ptx::fence_mbar_init();
   }
+  if (warp == 2) ptx::tmem_alloc<512>(tholder);
+  ptx::tc_fence_before();
+  __syncthreads();
+  ptx::tc_fence_after();
+  const uint32_t tmem = *tholder;
+  ptx::grid_dep_wait();
+
+  if (warp == 0) {
+    if (lane == 0) {  // ------------------------------------------------ TMA producer
+      ptx::mbar_arrive_expect_tx(kv_full, 2 * C::TB);
+      for (int t = 0; t < C::NA; ++t) {
+        ptx::tma_load_4d(&tmK, Ks + t * ATOM, kv_full, t * 64, k0, hn, bi);
+        ptx::tma_load_4d(&tmV, Vs + t * ATOM, kv_full, t * 64, k0, hn, bi);
+      }
+      for (int h = 0; h < nh; ++h) {
+        const int st = h % NST;
+        ptx::mbar_wait(&qd_empty[st], ((h / NST) & 1) ^ 1);
+        uint8_t* qs = ring + st * STG;
+        ptx::mbar_arrive_expect_tx(&qd_full[st], STG);
+        for (int t = 0; t < C::NA; ++t) {
+          ptx::tma_load_4d(&tmQ64, qs + t * HATOM, &qd_full[st], t * 64, k0 + h * HT, hn, bi);
+          ptx::tma_load_4d(&tmdO64, qs + H::HB + t * HATOM, &qd_full[st], t * 64, k0 + h * HT, hn, bi);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    {  // ------------------------------------------------ MMA issuer (warp-wide, elected lane issues)
+      ptx::mbar_wait(kv_full, 0);
+      const uint32_t kb = ptx::smem_u32(Ks), vb = ptx::smem_u32(Vs), rb = ptx::smem_u32(ring);
+      auto mma_sd = [&](int h) {  // S^T_b = K Q_h^T, dP^T_b = V dO_h^T  (b = h & 1)
+        const int st = h % NST;
+        ptx::mbar_wait(&qd_full[st], (h / NST) & 1);
+        ptx::tc_fence_after();
+        const uint32_t qb = rb + st * STG, ob = qb + H::HB, tS = tmem + (h & 1) * 128;
 #pragma unroll
-  for (int off = 16; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
-  if (lane == 0) dsum[(static_cast<int64_t>(bi) * heads + hn) * s + qq] = acc;
+        for (int kk = 0; kk < C::KS; ++kk) ptx::tc_mma_f16_w(tS, dk(kb, kk), hk(qb, kk), H::IDESC_S, kk > 0);
+#pragma unroll
+        for (int kk = 0; kk < C::KS; ++kk) ptx::tc_mma_f16_w(tS + 64, dk(vb, kk), hk(ob, kk), H::IDESC_S, kk > 0);
+        ptx::tc_commit_w(&s_full[h & 1]);
+      };
+      mma_sd(0);
+      if (nh > 1) mma_sd(1);
+      for (int h = 0; h < nh; ++h) {
+        const int st = h % NST;
+        ptx::mbar_wait(&x_full[h & 1], (h >> 1) & 1);
+        ptx::tc_fence_after();
+        const uint32_t qb = rb + st * STG, ob = qb + H::HB, tX = tmem + (h & 1) * 128;
+#pragma unroll
+        for (int kk = 0; kk < HT / 16; ++kk)  // dV += P^T dO_h
+          ptx::tc_mma_f16_ts_w(tmem + 256, tX + acol(kk), hm(ob, kk), H::IDESC_ACC, (h > 0 || kk > 0) ? 1u : 0u);
+#pragma unroll
+        for (int kk = 0; kk < HT / 16; ++kk)  // dK += dS^T Q_h
+          ptx::tc_mma_f16_ts_w(tmem + 384, tX + 64 + acol(kk), hm(qb, kk), H::IDESC_ACC,
+                             (h > 0 || kk > 0) ? 1u : 0u);
+        ptx::tc_commit_w(&qd_empty[st]);
+        if (h + 2 < nh) mma_sd(h + 2);  // into the buffer dV_h / dK_h read from (in order)
+      }
+      ptx::tc_commit_w(acc_full);
+    }
+  } else if (warp >= 4) {  // ------------------------------------------ P^T / dS^T warps (rows = keys)
+    const int lq = warp & 3, g = (warp - 4) >> 2;
+    const int r = lq * 32 + lane;
+    const int key = k0 + r;
+    const size_t zs = static_cast<size_t>(z) * a.s;
+    const uint32_t lane_off = static_cast<uint32_t>(lq * 32) << 16;
+    float* my = cv + (warp - 4) * 64;  // this warp's lse[32] | D[32] of its 32 query columns
+    // lse / D of the columns: lane e loads column e one half tile ahead
+    float lse_n = INFINITY, d_n = 0.f;
+    {
+      const int qq = k0 + g * 32 + lane;
+      if (qq < a.s) lse_n = a.lse[zs + qq], d_n = a.dsum[zs + qq];
+    }
+    for (int h = 0; h < nh; ++h) {
+      const int qc = k0 + h * HT + g * 32;  // first query column of this warp
+      __syncwarp();
+      my[lane] = lse_n;
+      my[32 + lane] = d_n;
+      __syncwarp();
+      {
+        const int qq = qc + HT + lane;
+        lse_n = (h + 1 < nh && qq < a.s) ? a.lse[zs + qq] : INFINITY;
+        d_n = (h + 1 < nh && qq < a.s) ? a.dsum[zs + qq] : 0.f;
+      }
+      const uint32_t tS = tmem + (h & 1) * 128 + lane_off;
+      ptx::mbar_wait(&s_full[h & 1], (h >> 1) & 1);
+      ptx::tc_fence_after();
+      uint32_t sv[32], pv[32];
+      ptx::tmem_ld_32x32b_x32(tS + g * 32, sv);
+      ptx::tmem_ld_32x32b_x32(tS + 64 + g * 32, pv);
+      ptx::tmem_ld_wait();
+      const bool diag = qc < k0 + TILE;  // the diagonal block: some columns precede some keys
+      uint32_t pk[16], dk2[16];
+#pragma unroll
+      for (int e = 0; e < 16; ++e) {
+        const float4 L = *reinterpret_cast<const float4*>(my + 4 * (e >> 1));
+        const float4 Dv = *reinterpret_cast<const float4*>(my + 32 + 4 * (e >> 1));
+        const float l0 = (e & 1) ? L.z : L.x, l1 = (e & 1) ? L.w : L.y;
+        const float d0 = (e & 1) ? Dv.z : Dv.x, d1 = (e & 1) ? Dv.w : Dv.y;
+        float p0 = ex2(fmaf(__uint_as_float(sv[2 * e]), a.sl2, -l0));
+        float p1 = ex2(fmaf(__uint_as_float(sv[2 * e + 1]), a.sl2, -l1));
+        float s0 = p0 * (__uint_as_float(pv[2 * e]) - d0) * a.scale;
+        float s1 = p1 * (__uint_as_float(pv[2 * e + 1]) - d1) * a.scale;
+        if (diag) {  // select after the arithmetic: nothing computed for a masked pair survives
+          const bool m0 = qc + 2 * e >= key, m1 = qc + 2 * e + 1 >= key;
+          p0 = m0 ? p0 : 0.f;
+          p1 = m1 ? p1 : 0.f;
+          s0 = m0 ? s0 : 0.f;
+          s1 = m1 ? s1 : 0.f;
+        }
+        pk[e] = pack2(p0, p1);
+        dk2[e] = pack2(s0, s1);
+      }
+      ptx::tmem_st_32x32b_x16(tS + g * 32, pk);
+      ptx::tmem_st_32x32b_x16(tS + 64 + g * 32, dk2);
+      ptx::tmem_st_wait();
+      ptx::tc_fence_before();
+      __syncwarp();
+      if (lane == 0) ptx::mbar_arrive(&x_full[h & 1]);  // per buffer: a warp one step ahead
+                                                        // must not count toward this step
+    }
+    ptx::mbar_wait(acc_full, 0);
+    ptx::tc_fence_after();
+    const int64_t rowoff = (static_cast<int64_t>(bi) * a.s + key) * a.ldo + static_cast<int64_t>(hn) * a.d;
+#pragma unroll
+    for (int c = 0; c < C::OC; ++c) {
+      if ((c & 1) != g) continue;
+      uint32_t v[32];
+      ptx::tmem_ld_32x32b_x32(tmem + 384 + lane_off + c * 32, v);
+      ptx::tmem_ld_wait();
+      if (key < a.s) store_row_chunk<D>(a.out + rowoff + a.col0, c * 32, v);
+      ptx::tmem_ld_32x32b_x32(tmem + 256 + lane_off + c * 32, v);
+      ptx::tmem_ld_wait();
+      if (key < a.s) store_row_chunk<D>(a.out + rowoff + a.col1, c * 32, v);
+    }
+  }
+  ptx::tc_fence_before();
+  __syncthreads();
+  if (warp == 2) {
+    ptx::tc_fence_after();
+    ptx::tmem_dealloc<512>(tmem);
+  }
 }
 
 thread_local std::string g_amsg;
 
 template <int D>
-constexpr int row_smem(int mode) {
-  return AC<D>::TB + (mode == M_DQ ? AC<D>::TB : 0) + 2 * (mode == M_STATS ? AC<D>::TB : 2 * AC<D>::TB) +
-         (mode == M_STATS ? 0 : 2 * ATOM) + 1024 + 1024;
-}
-template <int D>
 constexpr int fwd_smem() {
   return 6 * AC<D>::TB + 4 * TILE * 4 + 1024 + 1024;
 }
 template <int D>
-constexpr int col_smem() {
-  return 6 * AC<D>::TB + 2 * ATOM + 2 * TILE * 4 + 1024 + 1024;
+constexpr int dq_smem() {
+  return 2 * AC<D>::TB + 3 * 2 * HC<D>::HB + 2 * TILE * 4 + 1024 + 1024;
 }
-
+template <int D>
+constexpr int dkdv_smem() {
+  return 2 * AC<D>::TB + 3 * 2 * HC<D>::HB + 8 * 64 * 4 + 1024 + 1024;
+}
 struct Maps {
-  CUtensorMap q, k, v, dO;
+  CUtensorMap q, k, v, dO;          // 128-row boxes
+  CUtensorMap q64, k64, v64, dO64;  // 64-row boxes (backward half tiles)
 };
 
 bool make_maps(const AttnArgs& a, Maps& m, bool with_do) {
@@ -799,8 +777,15 @@ bool make_maps(const AttnArgs& a, Maps& m, bool with_do) {
   bool ok = encode_bf16_4d(&m.q, a.qkv, d, s, H, B, L, d, s * L, 64, 128) &&
             encode_bf16_4d(&m.k, a.qkv + a.h, d, s, H, B, L, d, s * L, 64, 128) &&
             encode_bf16_4d(&m.v, a.qkv + 2 * a.h, d, s, H, B, L, d, s * L, 64, 128);
-  if (with_do) ok = ok && encode_bf16_4d(&m.dO, a.dO, d, s, H, B, a.h, d, s * a.h, 64, 128);
-  else m.dO = m.q;
+  if (with_do) {
+    ok = ok && encode_bf16_4d(&m.dO, a.dO, d, s, H, B, a.h, d, s * a.h, 64, 128) &&
+         encode_bf16_4d(&m.dO64, a.dO, d, s, H, B, a.h, d, s * a.h, 64, 64) &&
+         encode_bf16_4d(&m.q64, a.qkv, d, s, H, B, L, d, s * L, 64, 64) &&
+         encode_bf16_4d(&m.k64, a.qkv + a.h, d, s, H, B, L, d, s * L, 64, 64) &&
+         encode_bf16_4d(&m.v64, a.qkv + 2 * a.h, d, s, H, B, L, d, s * L, 64, 64);
+  } else {
+    m.dO = m.q;
+  }
   if (!ok) g_amsg = std::string("attention tensor map: ") + gemm_last_message();
   return ok;
 }
@@ -835,10 +820,6 @@ template <int D>
 cudaError_t backward_d(const AttnArgs& a, cudaStream_t st) {
   Maps mp;
   if (!make_maps(a, mp, true)) return cudaErrorInvalidValue;
-  const int rows = a.s * a.batch;
-  cudaError_t e = launch_pdl(attn_dsum_kernel, dim3((rows * a.heads + 7) / 8), dim3(256), 0, st, 1, a.o, a.dO,
-                             a.dsum, a.s, a.heads, a.d, a.h, rows);
-  if (e != cudaSuccess) return e;
   KArgs k{};
   k.s = a.s;
   k.heads = a.heads;
@@ -847,24 +828,28 @@ cudaError_t backward_d(const AttnArgs& a, cudaStream_t st) {
   k.scale = 1.0f / std::sqrt(static_cast<float>(a.d));
   k.lse = a.lse;
   k.dsum = a.dsum;
+  k.dsum_w = a.dsum;
+  k.o = a.o;
+  k.dO = a.dO;
+  k.ldh = a.h;
   k.out = a.out;
   k.ldo = a.qkv_ld;
   k.d = a.d;
+  constexpr int s2 = dq_smem<D>(), s3 = dkdv_smem<D>();
+  static_assert(dq_smem<D>() <= 232448 && dkdv_smem<D>() <= 232448, "attention smem budget");
   static bool once = false;
-  constexpr int s2 = row_smem<D>(M_DQ), s3 = col_smem<D>();
-  static_assert(row_smem<D>(M_DQ) <= 232448 && col_smem<D>() <= 232448, "attention smem budget");
   if (!once) {
-    cudaFuncSetAttribute(attn_row_kernel<D, M_DQ>, cudaFuncAttributeMaxDynamicSharedMemorySize, s2);
-    cudaFuncSetAttribute(attn_col_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, s3);
+    cudaFuncSetAttribute(attn_dq_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, s2);
+    cudaFuncSetAttribute(attn_dkdv_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, s3);
     once = true;
   }
   dim3 grid(a.heads * a.batch, k.ntiles);  // z fastest: all heads' longest tiles go first
-  k.col0 = 0;  // dQ -> Q block
-  e = launch_pdl(attn_row_kernel<D, M_DQ>, grid, dim3(NT), s2, st, 1, mp.q, mp.k, mp.v, mp.dO, k);
+  k.col0 = 0;  // dQ -> Q block (and D for the next kernel)
+  cudaError_t e = launch_pdl(attn_dq_kernel<D>, grid, dim3(BWD_NT), s2, st, 1, mp.q, mp.k64, mp.v64, mp.dO, k);
   if (e != cudaSuccess) return e;
   k.col0 = a.h;      // dK -> K block
   k.col1 = 2 * a.h;  // dV -> V block
-  return launch_pdl(attn_col_kernel<D>, grid, dim3(NT), s3, st, 1, mp.q, mp.k, mp.v, mp.dO, k);
+  return launch_pdl(attn_dkdv_kernel<D>, grid, dim3(BWD_NT), s3, st, 1, mp.q64, mp.k, mp.v, mp.dO64, k);
 }
 
 }  // namespace

@@ -7,6 +7,8 @@
 #pragma once
 #include <cuda_runtime.h>
 
+#include <cstdlib>
+
 namespace slip {
 
 template <typename... KArgs, typename... Args>
@@ -20,7 +22,8 @@ cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t s
   cudaLaunchAttribute attr[2];
   int n = 0;
   attr[n].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  attr[n].val.programmaticStreamSerializationAllowed = 1;
+  static const bool no_pdl = std::getenv("SLIP_NO_PDL") != nullptr;  // debugging aid
+  attr[n].val.programmaticStreamSerializationAllowed = no_pdl ? 0 : 1;
   ++n;
   if (cluster_x > 1) {
     attr[n].id = cudaLaunchAttributeClusterDimension;

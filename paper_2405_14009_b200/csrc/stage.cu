@@ -283,13 +283,13 @@ slip_status attn_status(slip_ctx* c, cudaError_t e, const char* what, int launch
 slip_status attention_fwd(slip_ctx* c, LayerStash& ls, cudaStream_t s) {
   AttnArgs a = attn_args(c, ls);
   a.out = ls.o;
-  return attn_status(c, attn_forward(a, s), "attention forward", 2);
+  return attn_status(c, attn_forward(a, s), "attention forward", 1);
 }
 
 slip_status attention_bwd(slip_ctx* c, LayerStash& ls, cudaStream_t s) {
   AttnArgs a = attn_args(c, ls);
   a.out = ls.dqkv;
-  return attn_status(c, attn_backward(a, s), "attention backward", 3);
+  return attn_status(c, attn_backward(a, s), "attention backward", 2);
 }
 
 // colsum(a[T, N]) -> out (fp32, overwrite or accumulate), one launch
@@ -603,6 +603,32 @@ slip_status slip_gemm(int32_t M, int32_t N, int32_t K, const void* a, int64_t ld
   cudaError_t e = gemm_launch(d, reinterpret_cast<cudaStream_t>(st));
   if (e != cudaSuccess) {
     set_error(std::string("gemm: ") + cudaGetErrorString(e) + " " + gemm_last_message());
+    return e == cudaErrorInvalidValue ? SLIP_EUNSUPPORTED : SLIP_ECUDA;
+  }
+  return SLIP_OK;
+}
+
+slip_status slip_attention(int32_t s_len, int32_t heads, int32_t batch, int32_t d, const void* qkv, const void* o,
+                           const void* d_o, void* out, float* lse, float* dsum, int32_t backward, slip_stream st) {
+  SLIP_CHECK(qkv && out && lse && s_len > 0 && heads > 0 && batch > 0 && d > 0, SLIP_EINVAL, "attention: bad argument");
+  SLIP_CHECK(!backward || (o && d_o && dsum), SLIP_EINVAL, "attention: backward needs o, d_o and dsum");
+  AttnArgs a;
+  a.s = s_len;
+  a.heads = heads;
+  a.batch = batch;
+  a.d = d;
+  a.h = static_cast<int64_t>(heads) * d;
+  a.qkv_ld = 3 * a.h;
+  a.qkv = static_cast<const bf16*>(qkv);
+  a.o = static_cast<const bf16*>(o);
+  a.dO = static_cast<const bf16*>(d_o);
+  a.out = static_cast<bf16*>(out);
+  a.lse = lse;
+  a.dsum = dsum;
+  cudaStream_t cs = reinterpret_cast<cudaStream_t>(st);
+  cudaError_t e = backward ? attn_backward(a, cs) : attn_forward(a, cs);
+  if (e != cudaSuccess) {
+    set_error(std::string("attention: ") + cudaGetErrorString(e) + " " + attn_last_message());
     return e == cudaErrorInvalidValue ? SLIP_EUNSUPPORTED : SLIP_ECUDA;
   }
   return SLIP_OK;

@@ -114,6 +114,13 @@ def assign(N, DP, m, live):
     return {(i, j, k): out[(i * m + j) * DP + k] for i in range(N) for j in range(m) for k in range(DP)}
 
 
+def attention(qkv, s, heads, batch, d, out, lse, o=None, d_o=None, dsum=None, backward=False, stream=None):
+    """Diagnostic call of the fused attention kernels (see include/slip.h slip_attention)."""
+    call("slip_attention", s, heads, batch, d, _ptr(qkv), _ptr(o) if o is not None else None,
+         _ptr(d_o) if d_o is not None else None, _ptr(out), _ptr(lse), _ptr(dsum) if dsum is not None else None,
+         int(bool(backward)), _stream(stream))
+
+
 def set_trace(stage, enable=True):
     call("slip_set_trace", stage.ctx, int(bool(enable)))
 

@@ -65,5 +65,36 @@ int main() {
   show("g1: S seen", 700, nj);
   show("g1: max done", 800, nj);
   show("g1: P done", 900, nj);
+  // backward (dQ kernel probes: CTA y = SLIP_ATTN_PROBE -> q-tile 15 - y)
+  __nv_bfloat16 *dO, *dqkv;
+  float* dsum;
+  cudaMalloc(&dO, static_cast<size_t>(s) * h * 2);
+  cudaMalloc(&dqkv, hq.size() * 2);
+  cudaMalloc(&dsum, static_cast<size_t>(heads) * s * 4);
+  cudaMemcpy(dO, hq.data(), static_cast<size_t>(s) * h * 2, cudaMemcpyHostToDevice);
+  a.o = o;
+  a.dO = dO;
+  a.out = dqkv;
+  a.dsum = dsum;
+  for (int it = 0; it < 3; ++it) slip::attn_backward(a, 0);
+  cudaEventRecord(e0);
+  for (int it = 0; it < 20; ++it) slip::attn_backward(a, 0);
+  cudaEventRecord(e1);
+  cudaEventSynchronize(e1);
+  cudaEventElapsedTime(&ms, e0, e1);
+  printf("backward: %.2f us/launch (%s)\n", ms * 1000 / 20, cudaGetErrorString(cudaGetLastError()));
+  slip::attn_probe_read(p.data(), 4096);
+  const long long b0 = p[1999];
+  auto showb = [&](const char* name, int base, int n) {
+    printf("%-14s", name);
+    for (int j = 0; j < n; ++j) printf(" %7lld", p[base + j] ? p[base + j] - b0 : -1);
+    printf("\n");
+  };
+  const int nh = 2 * (16 - SLIP_ATTN_PROBE);
+  showb("dS ready@mma", 2000, nh);
+  showb("g0: S seen", 2100, nh);
+  showb("g0: dS done", 2300, nh);
+  showb("g1: S seen", 2200, nh);
+  showb("g1: dS done", 2400, nh);
   return 0;
 }
