@@ -95,7 +95,7 @@ __device__ __forceinline__ void store_row_chunk(__nv_bfloat16* row, int c0, cons
 
 // ====================================================================== forward kernel
 // Single pass, online softmax.  One CTA per (q-tile i, z), longest rows first.  TMEM:
-// S[0] | S[1] | O (128 columns each): S of k-tile j+1 is computed while the softmax warps
+// S[0] | S[1] | S[2] | O (128 columns each): S of k-tiles j+1, j+2 are computed while the softmax warps
 // work on k-tile j, so the tensor core and the softmax overlap.  Warp 0 TMA (K ring of 3,
 // V ring of 2, loaded in consumption order), warp 1 MMA, warp 2 TMEM allocator, warps
 // 4-11 softmax: warp w owns TMEM lane quarter w % 4 (32 rows) and column half g =
@@ -126,7 +126,7 @@ __global__ void __launch_bounds__(FWD_NT, 1)
     attn_fwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
                     const __grid_constant__ CUtensorMap tmV, const KArgs a) {
   using C = AC<D>;
-  constexpr int KST = 3, VST = 2;
+  constexpr int KST = 3, VST = 2, NSB = 3;  // K ring, V ring, S buffers in TMEM (O after them)
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* Qs = sm;
@@ -139,10 +139,10 @@ __global__ void __launch_bounds__(FWD_NT, 1)
   uint64_t* k_empty = k_full + KST;          // [KST]
   uint64_t* v_full = k_empty + KST;          // [VST]
   uint64_t* v_empty = v_full + VST;          // [VST]
-  uint64_t* s_full = v_empty + VST;          // [2] per S buffer
-  uint64_t* p_full = s_full + 2;             // [2] P of a k-tile written, per S buffer
-  uint64_t* o_done = p_full + 2;             // PV of a k-tile complete
-  uint32_t* tholder = reinterpret_cast<uint32_t*>(o_done + 1);
+  uint64_t* s_full = v_empty + VST;          // [NSB] per S buffer
+  uint64_t* p_full = s_full + NSB;           // [NSB] P of a k-tile written, per S buffer
+  uint64_t* o_done = p_full + NSB;           // [NSB] PV of a k-tile complete, per S buffer
+  uint32_t* tholder = reinterpret_cast<uint32_t*>(o_done + NSB);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int z = blockIdx.x, hn = z % a.heads, bi = z / a.heads;
@@ -159,11 +159,11 @@ __global__ void __launch_bounds__(FWD_NT, 1)
       ptx::mbar_init(&v_full[t], 1);
       ptx::mbar_init(&v_empty[t], 1);
     }
-    ptx::mbar_init(&s_full[0], 1);
-    ptx::mbar_init(&s_full[1], 1);
-    ptx::mbar_init(&p_full[0], 16);
-    ptx::mbar_init(&p_full[1], 16);
-    ptx::mbar_init(o_done, 1);
+    for (int t = 0; t < NSB; ++t) {
+      ptx::mbar_init(&s_full[t], 1);
+      ptx::mbar_init(&p_full[t], 16);
+      ptx::mbar_init(&o_done[t], 1);
+    }
     ptx::fence_mbar_init();
   }
   if (warp == 2) ptx::tmem_alloc<512>(tholder);
@@ -192,45 +192,43 @@ __global__ void __launch_bounds__(FWD_NT, 1)
         for (int t = 0; t < C::NA; ++t)
           ptx::tma_load_4d(&tmV, Vs + st * C::TB + t * ATOM, &v_full[st], t * 64, j * TILE, hn, bi);
       };
-      // consumption order of the MMA warp: K0 K1 V0 K2 V1 K3 V2 ...
-      load_k(0);
-      if (nj > 1) load_k(1);
+      // consumption order of the MMA warp: K0 .. K(NSB-1), then V0 K(NSB) V1 K(NSB+1) ...
+      for (int j = 0; j < NSB && j < nj; ++j) load_k(j);
       for (int j = 0; j < nj; ++j) {
         load_v(j);
-        if (j + 2 < nj) load_k(j + 2);
+        if (j + NSB < nj) load_k(j + NSB);
       }
     }
   } else if (warp == 1) {
     {  // ------------------------------------------------ MMA issuer (warp-wide, elected lane issues)
       ptx::mbar_wait(q_full, 0);
       const uint32_t qb = ptx::smem_u32(Qs), kb0 = ptx::smem_u32(Ks), vb0 = ptx::smem_u32(Vs);
-      auto mma_s = [&](int j) {  // S[j % 2] = Q K_j^T
+      auto mma_s = [&](int j) {  // S[j % NSB] = Q K_j^T
         const int st = j % KST;
         ptx::mbar_wait(&k_full[st], (j / KST) & 1);
         ptx::tc_fence_after();
         const uint32_t kb = kb0 + st * C::TB;
 #pragma unroll
         for (int kk = 0; kk < C::KS; ++kk)
-          ptx::tc_mma_f16_w(tmem + (j & 1) * 128, dk(qb, kk), dk(kb, kk), C::IDESC_S, kk > 0);
-        ptx::tc_commit_w(&s_full[j & 1]);
+          ptx::tc_mma_f16_w(tmem + (j % NSB) * 128, dk(qb, kk), dk(kb, kk), C::IDESC_S, kk > 0);
+        ptx::tc_commit_w(&s_full[j % NSB]);
         ptx::tc_commit_w(&k_empty[st]);
       };
-      mma_s(0);
-      if (nj > 1) mma_s(1);
+      for (int j = 0; j < NSB && j < nj; ++j) mma_s(j);
       for (int j = 0; j < nj; ++j) {
         const int st = j % VST;
-        ptx::mbar_wait(&p_full[j & 1], (j >> 1) & 1);
+        ptx::mbar_wait(&p_full[j % NSB], (j / NSB) & 1);
         ptx::mbar_wait(&v_full[st], (j / VST) & 1);
         PROBE(100 + j);
         ptx::tc_fence_after();
         const uint32_t vb = vb0 + st * C::TB;
 #pragma unroll
         for (int kk = 0; kk < TILE / 16; ++kk)  // O += P V_j, P (bf16 pairs) from TMEM
-          ptx::tc_mma_f16_ts_w(tmem + 256, tmem + (j & 1) * 128 + kk * 8, dm(vb, kk), C::IDESC_O,
+          ptx::tc_mma_f16_ts_w(tmem + NSB * 128, tmem + (j % NSB) * 128 + kk * 8, dm(vb, kk), C::IDESC_O,
                              (j > 0 || kk > 0) ? 1u : 0u);
-        ptx::tc_commit_w(o_done);
+        ptx::tc_commit_w(&o_done[j % NSB]);
         ptx::tc_commit_w(&v_empty[st]);
-        if (j + 2 < nj) mma_s(j + 2);  // into the S buffer PV_j reads P from (MMAs execute in order)
+        if (j + NSB < nj) mma_s(j + NSB);  // into the S buffer PV_j reads P from (MMAs execute in order)
       }
     }
   } else if (warp >= 4) {  // ------------------------------------------ softmax warps
@@ -238,11 +236,11 @@ __global__ void __launch_bounds__(FWD_NT, 1)
     const int r = lq * 32 + lane;
     const int q = i * TILE + r;
     const uint32_t lane_off = static_cast<uint32_t>(lq * 32) << 16;
-    const uint32_t tO = tmem + 256 + lane_off;
+    const uint32_t tO = tmem + NSB * 128 + lane_off;
     float m_run = -INFINITY, l = 0.f;
     for (int j = 0; j < nj; ++j) {
-      const uint32_t tS = tmem + (j & 1) * 128 + lane_off;
-      ptx::mbar_wait(&s_full[j & 1], (j >> 1) & 1);
+      const uint32_t tS = tmem + (j % NSB) * 128 + lane_off;
+      ptx::mbar_wait(&s_full[j % NSB], (j / NSB) & 1);
       if (lq == 0 && lane == 0 && g < 2) PROBE(400 + 300 * g + j);
       ptx::tc_fence_after();
       const bool diag = j == i;
@@ -270,7 +268,7 @@ __global__ void __launch_bounds__(FWD_NT, 1)
         const float mn = fmaxf(m_run, mt);
         const float alpha = m_run == -INFINITY ? 0.f : ex2(m_run - mn);
         if (j > 0 && g < C::OC) {  // O holds PV(0 .. j-1): wait for the last one, rescale my chunk
-          ptx::mbar_wait(o_done, (j - 1) & 1);
+          ptx::mbar_wait(&o_done[(j - 1) % NSB], ((j - 1) / NSB) & 1);
           ptx::tc_fence_after();
           uint32_t o[32];
           ptx::tmem_ld_32x32b_x32(tO + g * 32, o);
@@ -313,14 +311,14 @@ __global__ void __launch_bounds__(FWD_NT, 1)
       ptx::tmem_st_wait();
       ptx::tc_fence_before();
       __syncwarp();
-      if (lane == 0) ptx::mbar_arrive(&p_full[j & 1]);
+      if (lane == 0) ptx::mbar_arrive(&p_full[j % NSB]);
       if (lq == 0 && lane == 0 && g < 2) PROBE(600 + 300 * g + j);
     }
     // total l over the 4 column groups, then O / l and lse
     red[g * TILE + r] = l;
     ptx::named_bar_sync(1 + lq, 128);
     const float lt = (red[r] + red[TILE + r]) + (red[2 * TILE + r] + red[3 * TILE + r]);
-    ptx::mbar_wait(o_done, (nj - 1) & 1);
+    ptx::mbar_wait(&o_done[(nj - 1) % NSB], ((nj - 1) / NSB) & 1);
     ptx::tc_fence_after();
     if (g == 0 && q < a.s) a.lse[static_cast<size_t>(z) * a.s + q] = m_run + log2f(lt);
     if (g < C::OC) {
@@ -384,7 +382,7 @@ __global__ void __launch_bounds__(BWD_NT, 1)
                    const KArgs a) {
   using C = AC<D>;
   using H = HC<D>;
-  constexpr int NST = 3;
+  constexpr int NST = 3, NSB = 2;  // K/V ring stages, S|dP buffers in TMEM (dQ after them)
   constexpr int STG = 2 * H::HB;  // K_h | V_h
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -396,9 +394,9 @@ __global__ void __launch_bounds__(BWD_NT, 1)
   uint64_t* q_full = bar;
   uint64_t* kv_full = bar + 1;         // [NST]
   uint64_t* kv_empty = kv_full + NST;  // [NST]
-  uint64_t* s_full = kv_empty + NST;   // [2]
-  uint64_t* x_full = s_full + 2;       // [2] dS of a step written (8 warps), per buffer
-  uint64_t* acc_full = x_full + 2;
+  uint64_t* s_full = kv_empty + NST;   // [NSB]
+  uint64_t* x_full = s_full + NSB;     // [NSB] dS of a step written (8 warps), per buffer
+  uint64_t* acc_full = x_full + NSB;
   uint32_t* tholder = reinterpret_cast<uint32_t*>(acc_full + 1);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -416,10 +414,10 @@ __global__ void __launch_bounds__(BWD_NT, 1)
       ptx::mbar_init(&kv_full[t], 1);
       ptx::mbar_init(&kv_empty[t], 1);
     }
-    ptx::mbar_init(&s_full[0], 1);
-    ptx::mbar_init(&s_full[1], 1);
-    ptx::mbar_init(&x_full[0], 8);
-    ptx::mbar_init(&x_full[1], 8);
+    for (int t = 0; t < NSB; ++t) {
+      ptx::mbar_init(&s_full[t], 1);
+      ptx::mbar_init(&x_full[t], 8);
+    }
     ptx::mbar_init(acc_full, 1);
     ptx::fence_mbar_init();
   }
@@ -453,30 +451,29 @@ __global__ void __launch_bounds__(BWD_NT, 1)
     {  // ------------------------------------------------ MMA issuer (warp-wide, elected lane issues)
       ptx::mbar_wait(q_full, 0);
       const uint32_t qb = ptx::smem_u32(Qs), ob = ptx::smem_u32(dOs), rb = ptx::smem_u32(ring);
-      auto mma_sd = [&](int h) {  // S_b = Q K_h^T, dP_b = dO V_h^T  (b = h & 1)
+      auto mma_sd = [&](int h) {  // S_b = Q K_h^T, dP_b = dO V_h^T  (b = h % NSB)
         const int st = h % NST;
         ptx::mbar_wait(&kv_full[st], (h / NST) & 1);
         ptx::tc_fence_after();
-        const uint32_t kb = rb + st * STG, vb = kb + H::HB, tS = tmem + (h & 1) * 128;
+        const uint32_t kb = rb + st * STG, vb = kb + H::HB, tS = tmem + (h % NSB) * 128;
 #pragma unroll
         for (int kk = 0; kk < C::KS; ++kk) ptx::tc_mma_f16_w(tS, dk(qb, kk), hk(kb, kk), H::IDESC_S, kk > 0);
 #pragma unroll
         for (int kk = 0; kk < C::KS; ++kk) ptx::tc_mma_f16_w(tS + 64, dk(ob, kk), hk(vb, kk), H::IDESC_S, kk > 0);
-        ptx::tc_commit_w(&s_full[h & 1]);
+        ptx::tc_commit_w(&s_full[h % NSB]);
       };
-      mma_sd(0);
-      if (nh > 1) mma_sd(1);
+      for (int h = 0; h < NSB && h < nh; ++h) mma_sd(h);
       for (int h = 0; h < nh; ++h) {
         const int st = h % NST;
-        ptx::mbar_wait(&x_full[h & 1], (h >> 1) & 1);
+        ptx::mbar_wait(&x_full[h % NSB], (h / NSB) & 1);
         PROBE(2000 + h);
         ptx::tc_fence_after();
-        const uint32_t kb = rb + st * STG, tX = tmem + (h & 1) * 128;
+        const uint32_t kb = rb + st * STG, tX = tmem + (h % NSB) * 128;
 #pragma unroll
         for (int kk = 0; kk < HT / 16; ++kk)  // dQ += dS K_h, dS (bf16 pairs) from TMEM
-          ptx::tc_mma_f16_ts_w(tmem + 256, tX + acol(kk), hm(kb, kk), H::IDESC_ACC, (h > 0 || kk > 0) ? 1u : 0u);
+          ptx::tc_mma_f16_ts_w(tmem + NSB * 128, tX + acol(kk), hm(kb, kk), H::IDESC_ACC, (h > 0 || kk > 0) ? 1u : 0u);
         ptx::tc_commit_w(&kv_empty[st]);
-        if (h + 2 < nh) mma_sd(h + 2);  // into the buffer dQ_h reads dS from (MMAs execute in order)
+        if (h + NSB < nh) mma_sd(h + NSB);  // into the buffer dQ_h reads dS from (MMAs execute in order)
       }
       ptx::tc_commit_w(acc_full);
     }
@@ -512,8 +509,8 @@ __global__ void __launch_bounds__(BWD_NT, 1)
     if (g == 0 && q < a.s) a.dsum_w[zs + q] = drow;
     const float lrow = q < a.s ? a.lse[zs + q] : 0.f;
     for (int h = 0; h < nh; ++h) {
-      const uint32_t tS = tmem + (h & 1) * 128 + lane_off;
-      ptx::mbar_wait(&s_full[h & 1], (h >> 1) & 1);
+      const uint32_t tS = tmem + (h % NSB) * 128 + lane_off;
+      ptx::mbar_wait(&s_full[h % NSB], (h / NSB) & 1);
       if (lq == 0 && lane == 0) PROBE(2100 + 100 * g + h);
       ptx::tc_fence_after();
       uint32_t sv[32], pv[32];
@@ -538,7 +535,7 @@ __global__ void __launch_bounds__(BWD_NT, 1)
       ptx::tmem_st_wait();
       ptx::tc_fence_before();
       __syncwarp();
-      if (lane == 0) ptx::mbar_arrive(&x_full[h & 1]);  // per buffer: a warp one step ahead
+      if (lane == 0) ptx::mbar_arrive(&x_full[h % NSB]);  // per buffer: a warp one step ahead
                                                         // must not count toward this step
       if (lq == 0 && lane == 0) PROBE(2300 + 100 * g + h);
     }
@@ -549,7 +546,7 @@ __global__ void __launch_bounds__(BWD_NT, 1)
     for (int c = 0; c < C::OC; ++c) {
       if ((c & 1) != g) continue;
       uint32_t v[32];
-      ptx::tmem_ld_32x32b_x32(tmem + 256 + lane_off + c * 32, v);
+      ptx::tmem_ld_32x32b_x32(tmem + NSB * 128 + lane_off + c * 32, v);
       ptx::tmem_ld_wait();
       if (q < a.s) store_row_chunk<D>(orow, c * 32, v);
     }
