@@ -234,10 +234,10 @@ def main():
                  "decoupled B/W + staggered AdamW")
     # nominal integer costs ~ FLOP ratios of F : B : W, refined by profiling below
     costs = rt.make_costs(t_f=108, t_b=117, t_w=100, t_comm=1, t_ar=10, t_opt=10)
-    def slots_for(lv, cs):
-        """max in-flight micro-batches (F started, W not finished) of any worker in the plan"""
+    def inflight(lv, cs):
+        """{(i, k): max in-flight micro-batches (F started, W / BC not finished)} of the plan"""
         plan = rt.plan_schedule(PP, DP, m, lv, cs, decoupled, staggered, horizon=2)
-        n = 1
+        out = {}
         for i in range(PP):
             for k in range(DP):
                 cur = mx = 0
@@ -245,8 +245,11 @@ def main():
                                 key=lambda o: o[6]):
                     cur += 1 if o[3] == 0 else -1
                     mx = max(mx, cur)
-                n = max(n, mx)
-        return n
+                out[(i, k)] = mx
+        return out
+
+    def slots_for(lv, cs):
+        return max(1, max(inflight(lv, cs).values()))
 
     def normalization(cs):
         """Phase 1 of the Planner (§4.2.1): R from Algorithm 1 over the heuristic
@@ -380,6 +383,7 @@ def main():
         rt.set_trace(stage, True)
         execute(2)
         barrier()
+        trace = rt.get_trace(stage)
         rt.set_trace(stage, False)
         plan = rt.plan_schedule(PP, DP, m, live, costs, decoupled, staggered, horizon=2)
         os.makedirs(args.trace, exist_ok=True)
@@ -387,7 +391,24 @@ def main():
             json.dump({"rank": rank, "role": my_role, "live": live, "costs_10us": [costs.t_f, costs.t_b, costs.t_w,
                                                                                       costs.t_comm, costs.t_ar,
                                                                                       costs.t_opt],
-                       "trace": rt.get_trace(stage), "plan_ops": plan.ops, "plan_period": plan.period}, f)
+                       "trace": trace, "plan_ops": plan.ops, "plan_period": plan.period}, f)
+    # per-stage peak memory (Fig. 12): the plan's peak in-flight
+    # micro-batches per worker x the stash bytes of one slot, plus parameters / optimizer state
+    # (bf16 w + fp32 master, grad, m, v = 18 B/param); and the bytes this process allocated
+    peak = inflight(live, costs)
+    alloc = torch.tensor([float(torch.cuda.max_memory_allocated())], dtype=torch.float64, device="cuda")
+    alloc_all = [torch.zeros_like(alloc) for _ in range(world)]
+    if world > 1:
+        dist.all_gather(alloc_all, alloc)
+    else:
+        alloc_all = [alloc]
+    slot_bytes = stage.stash_bytes / max(1, stage.n_slots)
+    memory = {"stash_bytes_per_microbatch": slot_bytes, "param_state_bytes": 18 * stage.n_params,
+              "workspace_bytes": stage.ws_bytes,
+              "plan_peak_inflight": {"%d,%d" % ik: v for ik, v in sorted(peak.items())},
+              "plan_peak_bytes_per_stage": [max(peak[(i, k)] for k in range(DP)) * slot_bytes + 18 * stage.n_params
+                                            for i in range(PP)],
+              "allocated_bytes_per_rank": [a.item() for a in alloc_all]}
     kern = torch.tensor([rep.n_kernels], dtype=torch.float64, device="cuda")
     if world > 1:
         dist.all_reduce(kern)
@@ -452,6 +473,7 @@ def main():
         "predicted_period_units": rep.predicted_period,
         "planner_costs_10us": [costs.t_f, costs.t_b, costs.t_w, costs.t_opt],
     }
+    line["memory"] = memory
     if norm:
         line["normalization"] = norm
     if cpu:

@@ -93,9 +93,10 @@ typedef struct {
   int64_t a_f, a_w, m_limit;
 } slip_costs;
 
-/* Planner options: decoupled = Decoupled BackProp (§3.2), staggered =
- * Staggered Optimizer (§3.3), horizon = iterations planned (>= 1; the period
- * is measured between the last two). */
+/* Planner options: decoupled = Decoupled BackProp (§3.2; 2 = selective: plan
+ * with and without it and keep the shorter period, PAPER.md lines 289-292,
+ * reading R32), staggered = Staggered Optimizer (§3.3), horizon = iterations
+ * planned (>= 1; the period is measured between the last two). */
 typedef struct {
   int32_t decoupled, staggered, horizon;
 } slip_plan_opts;
@@ -387,6 +388,7 @@ typedef struct {
   double phase_ms[6];
   int64_t phase_ops[6];
   int64_t w_gemm_launches;   /* tcgen05 GEMM launches issued by the W / BC ops */
+  int64_t rollbacks;         /* validated mode: optimizer steps this rank rolled back */
 } slip_report;
 
 /* Runs `iterations` training iterations of the plan on this rank (worker
@@ -399,6 +401,26 @@ slip_status slip_execute_schedule(slip_ctx* ctx, slip_comm* comm, const slip_clu
                                   const slip_plan_opts* opts, const slip_adam* adam, int32_t warmup,
                                   int32_t iterations, uint64_t seed, const slip_io* io, slip_stream s,
                                   slip_report* out);
+
+/* ------------------------------------------------------ validation / rollback
+ * PAPER.md §4.3 lines 580-583 ("Bypassing Optimizer Synchronizations"), reading
+ * R31.  With validation on, the executor's OPT of iteration t on each live worker
+ * (1) checks the stage's all-reduced gradients for non-finite values (local
+ * validation), (2) takes the AdamW step only if they are finite, and (3) starts an
+ * all-reduce (MAX) of its flag over the live ranks on the all-reduce stream — no
+ * stage waits for another before stepping.  Before the first W of iteration t+1
+ * (the last moment the gradients of t are intact) or at the end of the call, the
+ * compute stream waits for that flag and, if some stage failed while this one
+ * stepped, applies the arithmetic reversal of the step (adamw_rollback, no saved
+ * copy).  All decisions are taken on the device (no host round trip). */
+slip_status slip_set_validation(slip_ctx* ctx, int32_t enable);
+/* Fault injection for tests: kind 1 makes the next validation on this ctx report
+ * non-finite gradients (the data is untouched); kind 0 clears it. */
+slip_status slip_inject_fault(slip_ctx* ctx, int32_t kind);
+/* The reversal of one slip_optimizer_step with the same (step, grad_scale) and the
+ * gradient still in the ctx's grad buffer: p, m, v restored to rounding (v clamped at
+ * 0), bf16 weights refreshed. */
+slip_status slip_optimizer_rollback(slip_ctx* ctx, const slip_adam* a, int64_t step, float grad_scale, slip_stream s);
 
 /* ------------------------------------------------------------------ tracing
  * Per-action timeline of the timed iterations of the last slip_execute_schedule

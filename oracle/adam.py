@@ -53,3 +53,20 @@ def nonfinite(grads) -> bool:
     """Local post-step validation flag (§4.3): any non-finite
     gradient element in this stage."""
     return any(not np.all(np.isfinite(g)) for g in grads.values())
+
+
+def adamw_inverse(p1, m1, v1, g, step, cfg: AdamCfg, grad_scale=1.0, decay=True):
+    """The arithmetic reversal of adamw_step (§4.3: AdamW rollbacks
+    "do not entail additional memory costs because the operations involved are
+    arithmetically reversible"), given the post-step state and the same gradient:
+        m0 = (m1 - (1 - b1) g) / b1,   v0 = (v1 - (1 - b2) g^2) / b2,
+        p0 = (p1 + lr mhat1 / (sqrt(vhat1) + eps)) / (1 - lr wd).
+    Exact in real arithmetic; v0 is clamped at 0 against rounding (reading R31)."""
+    g = grad_scale * g
+    mhat = m1 / (1.0 - cfg.beta1 ** step)
+    vhat = v1 / (1.0 - cfg.beta2 ** step)
+    wd = cfg.weight_decay if decay else 0.0
+    p0 = (p1 + cfg.lr * mhat / (np.sqrt(vhat) + cfg.eps)) / (1.0 - cfg.lr * wd)
+    m0 = (m1 - (1.0 - cfg.beta1) * g) / cfg.beta1
+    v0 = np.maximum((v1 - (1.0 - cfg.beta2) * g * g) / cfg.beta2, 0.0)
+    return p0, m0, v0

@@ -56,7 +56,7 @@ class Costs:
 
 @dataclass(frozen=True)
 class Opts:
-    decoupled: bool = True
+    decoupled: int = True  # True / False, or 2 = selective (the better of both)
     staggered: bool = True
     horizon: int = 3
 
@@ -135,6 +135,12 @@ def comm_edges(ex, N, DP, m):
 
 # ---------------------------------------------------------------- step 3-6
 def schedule(live, m, costs: Costs, opts: Opts) -> Plan:
+    if opts.decoupled == 2:
+        # selective decoupling (§3.2; R32): both plans,
+        # the shorter steady-state period wins, ties to Decoupled BackProp
+        pd = schedule(live, m, costs, Opts(True, opts.staggered, opts.horizon))
+        pc = schedule(live, m, costs, Opts(False, opts.staggered, opts.horizon))
+        return pc if pc.period < pd.period else pd
     N, DP = len(live), len(live[0])
     H = max(1, int(opts.horizon))
     ex = assign(live, m)

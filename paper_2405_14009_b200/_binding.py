@@ -81,7 +81,7 @@ class slip_report(C.Structure):
     _fields_ = [("period_ms", C.c_double), ("total_ms", C.c_double), ("predicted_period", C.c_int64),
                 ("n_ops", C.c_int64), ("n_kernels", C.c_int64), ("plan_hash", C.c_uint64),
                 ("last_loss", C.c_float), ("nonfinite", C.c_int32), ("phase_ms", C.c_double * 6),
-                ("phase_ops", C.c_int64 * 6), ("w_gemm_launches", C.c_int64)]
+                ("phase_ops", C.c_int64 * 6), ("w_gemm_launches", C.c_int64), ("rollbacks", C.c_int64)]
 
 
 P = C.c_void_p
@@ -129,6 +129,9 @@ SIGNATURES = {
     "slip_grad_allreduce": (C.c_int, [P, P, P]),
     "slip_comm_set_role": (C.c_int, [P, I32]),
     "slip_set_sm_reserve": (C.c_int, [I32]),
+    "slip_set_validation": (C.c_int, [P, I32]),
+    "slip_inject_fault": (C.c_int, [P, I32]),
+    "slip_optimizer_rollback": (C.c_int, [P, C.POINTER(slip_adam), I64, F32, P]),
     "slip_attention": (C.c_int, [I32, I32, I32, I32, P, P, P, P, P, P, I32, P]),
     "slip_set_trace": (C.c_int, [P, I32]),
     "slip_get_trace": (C.c_int, [P, C.POINTER(slip_trace_rec), I64, C.POINTER(I64)]),

@@ -36,6 +36,8 @@ void destroy_setup(slip_comm* c) {
   c->pair_stream.clear();
   if (c->stage_comm) ncclCommDestroy(c->stage_comm);
   c->stage_comm = nullptr;
+  if (c->live_comm) ncclCommDestroy(c->live_comm);
+  c->live_comm = nullptr;
   if (c->ar_stream) cudaStreamDestroy(c->ar_stream);
   c->ar_stream = nullptr;
   c->ready = false;
@@ -98,6 +100,16 @@ slip_status slip_comm_setup(slip_comm* c, const slip_cluster* cl) {
     sc = nullptr;
   }
   c->stage_comm = sc;
+  // all live ranks (post-step validation flags)
+  int n_all = 0;
+  for (uint8_t v : cc.live) n_all += v;
+  ncclComm_t lc = nullptr;
+  SLIP_NCCL(ncclCommSplit(c->world_comm, c->my_live ? 0 : NCCL_SPLIT_NOCOLOR, c->role, &lc, nullptr));
+  if (lc && n_all <= 1) {
+    ncclCommDestroy(lc);
+    lc = nullptr;
+  }
+  c->live_comm = lc;
   // directed pairs used by the assignment (ACT i -> i+1, GRAD i+1 -> i), in a fixed order
   std::set<std::pair<int, int>> pairs;
   for (int k = 0; k < cc.DP; ++k)

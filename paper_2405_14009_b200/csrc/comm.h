@@ -20,6 +20,7 @@ struct slip_comm {
   int my_stage = 0, my_pipe = 0;
   bool my_live = true;
   ncclComm_t stage_comm = nullptr;  // live peers of my stage (nullptr if singleton / failed)
+  ncclComm_t live_comm = nullptr;   // all live ranks (validation flags; nullptr if failed / alone)
   int stage_size = 1;
   cudaStream_t ar_stream = nullptr;
   // directed pair (src rank, dst rank) -> communicator in which src is rank 0, dst rank 1

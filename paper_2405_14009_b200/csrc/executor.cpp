@@ -99,6 +99,7 @@ extern "C" slip_status slip_execute_schedule(slip_ctx* ctx, slip_comm* comm, con
   const bool tracing = ctx->trace_on;
   int64_t launches0 = ctx->launches;
 
+  if (ctx->validate) SLIP_CUDA(cudaMemsetAsync(ctx->ws.vflags + 4, 0, sizeof(int32_t), cs));
   for (int run = 0; run < 2; ++run) {
     const int H = run == 0 ? warmup : iterations;
     if (H == 0) continue;
@@ -135,8 +136,25 @@ extern "C" slip_status slip_execute_schedule(slip_ctx* ctx, slip_comm* comm, con
       if (r != cudaSuccess) return r;
       return cudaStreamWaitEvent(to, e, 0);
     };
+    // validated mode: the rollback check of iteration t runs before this worker's first W / BC
+    // of a later iteration (the last moment t's gradients are intact) or at the end
+    struct Pending {
+      int iter = -1;
+      int64_t step = 0;
+      cudaEvent_t flag_ready = nullptr;
+    } pend;
+    auto flush_rollback = [&](int before_iter) -> slip_status {
+      if (pend.iter < 0 || pend.iter >= before_iter) return SLIP_OK;
+      SLIP_CUDA(cudaStreamWaitEvent(cs, pend.flag_ready, 0));
+      int32_t* vf = ctx->ws.vflags;
+      SLIP_TRY(rollback_if(ctx, adam, pend.step, grad_scale, vf + 2 + (pend.iter & 1), vf + (pend.iter & 1), vf + 4,
+                           cs));
+      pend.iter = -1;
+      return SLIP_OK;
+    };
     for (const slip_action& a : progs[me]) {
       const int ph = phase_of(a.kind);
+      if (ctx->validate && (a.kind == SLIP_ACT_W || a.kind == SLIP_ACT_BC)) SLIP_TRY(flush_rollback(a.iter));
       // tracing: begin / end events on the stream the action runs on
       cudaStream_t ts = cs;
       if (a.kind == SLIP_ACT_RECV_X || a.kind == SLIP_ACT_RECV_DY) ts = xfer_stream(a.peer, me);
@@ -144,22 +162,27 @@ extern "C" slip_status slip_execute_schedule(slip_ctx* ctx, slip_comm* comm, con
       if (a.kind == SLIP_ACT_AR) ts = comm->ar_stream;
       const bool tr = timed && tracing && !(a.kind == SLIP_ACT_AR && !comm->stage_comm);
       size_t tb_idx = 0;
+      // called by every action after its stream waits: the phase timing (and the trace)
+      // measure the operation itself, not the time it waited for a peer or a free slot
+      bool marked = false;
       auto trace_begin = [&]() -> cudaError_t {
-        if (!tr) return cudaSuccess;
+        cudaError_t r = cudaSuccess;
+        if (timed && ph >= 0) {
+          marked = true;
+          cudaEvent_t tb, te;
+          r = tpool.get(&tb);
+          if (r == cudaSuccess) r = tpool.get(&te);
+          if (r == cudaSuccess) r = cudaEventRecord(tb, ts);
+          marks.push_back({ph, tpool.next - 2});
+        }
+        if (!tr || r != cudaSuccess) return r;
         cudaEvent_t e0, e1;
-        cudaError_t r = tpool.get(&e0);
+        r = tpool.get(&e0);
         if (r == cudaSuccess) r = tpool.get(&e1);
         if (r == cudaSuccess) r = cudaEventRecord(e0, ts);
         tb_idx = tpool.next - 2;
         return r;
       };
-      if (timed && ph >= 0) {
-        cudaEvent_t tb, te;
-        SLIP_CUDA(tpool.get(&tb));
-        SLIP_CUDA(tpool.get(&te));
-        SLIP_CUDA(cudaEventRecord(tb, cs));
-        marks.push_back({ph, tpool.next - 2});
-      }
       SlotBufs* sb = a.slot >= 0 ? &ctx->slots[a.slot] : nullptr;
       SlotEv* se = a.slot >= 0 ? &sev[a.slot] : nullptr;
       switch (a.kind) {
@@ -264,19 +287,44 @@ extern "C" slip_status slip_execute_schedule(slip_ctx* ctx, slip_comm* comm, con
         case SLIP_ACT_OPT:
           ctx->opt_step += 1;
           SLIP_CUDA(trace_begin());
-          SLIP_TRY(slip_optimizer_step(ctx, adam, ctx->opt_step, grad_scale, ctx->ws.nonfinite, stream));
+          if (!ctx->validate) {
+            SLIP_TRY(slip_optimizer_step(ctx, adam, ctx->opt_step, grad_scale, ctx->ws.nonfinite, stream));
+          } else {
+            // local validation, step only if finite (no wait for other stages), then the
+            // live-rank MAX of the flag on the all-reduce stream
+            int32_t* own = ctx->ws.vflags + (a.iter & 1);
+            int32_t* glob = ctx->ws.vflags + 2 + (a.iter & 1);
+            SLIP_TRY(validated_step(ctx, adam, ctx->opt_step, grad_scale, own, ctx->fault_next_opt, cs));
+            ctx->fault_next_opt = 0;
+            cudaEvent_t fe;
+            if (comm->live_comm) {
+              SLIP_CUDA(chain(cs, comm->ar_stream));
+              ncclResult_t r = ncclAllReduce(own, glob, 1, ncclInt32, ncclMax, comm->live_comm, comm->ar_stream);
+              if (r != ncclSuccess) return nccl_status(r, "ncclAllReduce(validation flag)");
+              SLIP_CUDA(pool.get(&fe));
+              SLIP_CUDA(cudaEventRecord(fe, comm->ar_stream));
+            } else {
+              SLIP_CUDA(cudaMemcpyAsync(glob, own, sizeof(int32_t), cudaMemcpyDeviceToDevice, cs));
+              SLIP_CUDA(pool.get(&fe));
+              SLIP_CUDA(cudaEventRecord(fe, cs));
+            }
+            pend.iter = a.iter;
+            pend.step = ctx->opt_step;
+            pend.flag_ready = fe;
+          }
           break;
         default:
           set_error("execute: unknown action");
           return SLIP_EINVAL;
       }
-      if (timed && ph >= 0) SLIP_CUDA(cudaEventRecord(tpool.ev[marks.back().second + 1], cs));
+      if (marked) SLIP_CUDA(cudaEventRecord(tpool.ev[marks.back().second + 1], ts));
       if (tr) {
         SLIP_CUDA(cudaEventRecord(tpool.ev[tb_idx + 1], ts));
         slip_trace_rec rec{a.kind, a.mb, a.origin, a.iter, a.peer, a.slot, 0.f, 0.f};
         tmarks.push_back({rec, tb_idx});
       }
     }
+    if (ctx->validate) SLIP_TRY(flush_rollback(1 << 30));
     // join every side stream back into the compute stream
     for (auto& kv : comm->pair_stream) SLIP_CUDA(chain(kv.second, cs));
     SLIP_CUDA(chain(comm->ar_stream, cs));
@@ -327,13 +375,19 @@ extern "C" slip_status slip_execute_schedule(slip_ctx* ctx, slip_comm* comm, con
   int32_t nf = 0;
   SLIP_CUDA(cudaMemcpy(&nf, ctx->ws.nonfinite, sizeof nf, cudaMemcpyDeviceToHost));
   out->nonfinite = nf;
+  if (ctx->validate) {
+    int32_t rb = 0;
+    SLIP_CUDA(cudaMemcpy(&rb, ctx->ws.vflags + 4, sizeof rb, cudaMemcpyDeviceToHost));
+    out->rollbacks = rb;
+    // a rolled-back or skipped step does not count towards AdamW's bias correction next call
+    ctx->opt_step -= rb;
+  }
   return SLIP_OK;
 }
 
 extern "C" slip_status slip_set_trace(slip_ctx* ctx, int32_t enable) {
   SLIP_CHECK(ctx, SLIP_EINVAL, "set_trace: ctx is NULL");
-  ctx->trace_on = enable != 0;
-  if (!ctx->trace_on) ctx->trace.clear();
+  ctx->trace_on = enable != 0;  // the last traced run's records stay readable
   return SLIP_OK;
 }
 

@@ -64,110 +64,125 @@ __device__ __forceinline__ uint2 pack4(float a, float b, float c, float d) {
 }
 
 // ------------------------------------------------------------------ LayerNorm fwd
-// One block per row; thread i owns 16-byte vectors i, i + blockDim, ... (VPT of them).
-template <int VPT>
-__global__ void __launch_bounds__(512) ln_fwd_kernel(const bf16* __restrict__ x, const bf16* __restrict__ gamma,
+// One warp per row (8 rows per 256-thread block): lane l owns the 16-byte vectors
+// l, l + 32, ... (VPL of them), all loads issued before any reduction, shuffles only —
+// many rows in flight per SM, no block barriers.  Two-pass statistics in fp32 (R24).
+constexpr int LN_ROWS = 8;
+template <int VPL>
+__global__ void __launch_bounds__(256) ln_fwd_kernel(const bf16* __restrict__ x, const bf16* __restrict__ gamma,
                                                      const bf16* __restrict__ beta, bf16* __restrict__ y,
-                                                     float* __restrict__ mean, float* __restrict__ rstd, int h,
+                                                     float* __restrict__ mean, float* __restrict__ rstd, int T, int h,
                                                      float eps) {
-  __shared__ float2 red[33];
   ptx::grid_dep_wait();
-  const int row = blockIdx.x;
+  const int lane = threadIdx.x & 31;
+  const int row = blockIdx.x * LN_ROWS + (threadIdx.x >> 5);
+  if (row >= T) return;
   const int nv = h >> 3;
   const uint4* xr = reinterpret_cast<const uint4*>(x + static_cast<size_t>(row) * h);
-  float v[VPT][8];
+  uint4 raw[VPL];
+#pragma unroll
+  for (int i = 0; i < VPL; ++i) {
+    const int idx = lane + 32 * i;
+    raw[i] = idx < nv ? xr[idx] : make_uint4(0, 0, 0, 0);
+  }
   float sum = 0.f;
 #pragma unroll
-  for (int i = 0; i < VPT; ++i) {
-    const int idx = threadIdx.x + i * blockDim.x;
-    if (idx < nv) {
-      unpack8(xr[idx], v[i]);
+  for (int i = 0; i < VPL; ++i) {
+    float v[8];
+    unpack8(raw[i], v);
 #pragma unroll
-      for (int e = 0; e < 8; ++e) sum += v[i][e];
-    }
+    for (int e = 0; e < 8; ++e) sum += v[e];
   }
-  const float mu = block_sum2(sum, 0.f, red).x / h;
+  const float mu = warp_sum(sum) / h;
   float sq = 0.f;
 #pragma unroll
-  for (int i = 0; i < VPT; ++i) {
-    if (threadIdx.x + i * blockDim.x < nv) {
+  for (int i = 0; i < VPL; ++i) {
+    if (lane + 32 * i < nv) {
+      float v[8];
+      unpack8(raw[i], v);
 #pragma unroll
-      for (int e = 0; e < 8; ++e) {
-        const float d = v[i][e] - mu;
-        sq += d * d;
-      }
+      for (int e = 0; e < 8; ++e) sq += (v[e] - mu) * (v[e] - mu);
     }
   }
-  const float rs = rsqrtf(block_sum2(sq, 0.f, red).x / h + eps);
+  const float rs = rsqrtf(warp_sum(sq) / h + eps);
   uint4* yr = reinterpret_cast<uint4*>(y + static_cast<size_t>(row) * h);
 #pragma unroll
-  for (int i = 0; i < VPT; ++i) {
-    const int idx = threadIdx.x + i * blockDim.x;
+  for (int i = 0; i < VPL; ++i) {
+    const int idx = lane + 32 * i;
     if (idx < nv) {
-      float g[8], b[8], o[8];
+      float v[8], g[8], b[8], o[8];
+      unpack8(raw[i], v);
       unpack8(reinterpret_cast<const uint4*>(gamma)[idx], g);
       unpack8(reinterpret_cast<const uint4*>(beta)[idx], b);
 #pragma unroll
-      for (int e = 0; e < 8; ++e) o[e] = (v[i][e] - mu) * rs * g[e] + b[e];
+      for (int e = 0; e < 8; ++e) o[e] = (v[e] - mu) * rs * g[e] + b[e];
       yr[idx] = pack8(o);
     }
   }
-  if (threadIdx.x == 0) {
+  if (lane == 0) {
     mean[row] = mu;
     rstd[row] = rs;
   }
 }
 
 // ------------------------------------------------------------------ LayerNorm bwd (rows)
-template <int VPT>
-__global__ void __launch_bounds__(512) ln_bwd_rows_kernel(const bf16* __restrict__ dy, const bf16* x,
+// One warp per row.  Pass 1 forms g = dy * gamma and the two row sums from registers
+// (dy, x kept as raw 16-byte vectors); pass 2 writes dx = resid + rstd (g - mean(g) -
+// xhat mean(g xhat)).  x is fully read before dx is written (dx must not alias x).
+template <int VPL>
+__global__ void __launch_bounds__(256) ln_bwd_rows_kernel(const bf16* __restrict__ dy, const bf16* x,
                                                           const float* __restrict__ mean,
                                                           const float* __restrict__ rstd,
                                                           const bf16* __restrict__ gamma,
-                                                          const bf16* __restrict__ resid, bf16* dx, int h) {
-  __shared__ float2 red[33];
+                                                          const bf16* __restrict__ resid, bf16* dx, int T, int h) {
   ptx::grid_dep_wait();
-  const int row = blockIdx.x;
+  const int lane = threadIdx.x & 31;
+  const int row = blockIdx.x * LN_ROWS + (threadIdx.x >> 5);
+  if (row >= T) return;
   const int nv = h >> 3;
   const float mu = mean[row], rs = rstd[row];
   const uint4* xr = reinterpret_cast<const uint4*>(x + static_cast<size_t>(row) * h);
   const uint4* dyr = reinterpret_cast<const uint4*>(dy + static_cast<size_t>(row) * h);
-  float g[VPT][8], xh[VPT][8];
+  const uint4* rr = resid ? reinterpret_cast<const uint4*>(resid + static_cast<size_t>(row) * h) : nullptr;
+  uint4 xv[VPL], dv[VPL], rv[VPL];
+#pragma unroll
+  for (int i = 0; i < VPL; ++i) {
+    const int idx = lane + 32 * i;
+    const bool ok = idx < nv;
+    xv[i] = ok ? xr[idx] : make_uint4(0, 0, 0, 0);
+    dv[i] = ok ? dyr[idx] : make_uint4(0, 0, 0, 0);
+    rv[i] = (ok && rr) ? rr[idx] : make_uint4(0, 0, 0, 0);
+  }
   float s1 = 0.f, s2 = 0.f;
 #pragma unroll
-  for (int i = 0; i < VPT; ++i) {
-    const int idx = threadIdx.x + i * blockDim.x;
+  for (int i = 0; i < VPL; ++i) {
+    const int idx = lane + 32 * i;
     if (idx < nv) {
-      float xv[8], dv[8], gm[8];
-      unpack8(xr[idx], xv);
-      unpack8(dyr[idx], dv);
+      float a[8], d[8], gm[8];
+      unpack8(xv[i], a);
+      unpack8(dv[i], d);
       unpack8(reinterpret_cast<const uint4*>(gamma)[idx], gm);
 #pragma unroll
       for (int e = 0; e < 8; ++e) {
-        xh[i][e] = (xv[e] - mu) * rs;
-        g[i][e] = dv[e] * gm[e];
-        s1 += g[i][e];
-        s2 += g[i][e] * xh[i][e];
+        const float g = d[e] * gm[e];
+        s1 += g;
+        s2 += g * ((a[e] - mu) * rs);
       }
     }
   }
-  const float2 s = block_sum2(s1, s2, red);  // every x read completes before any dx write below
-  const float mg = s.x / h, mgx = s.y / h;
+  const float mg = warp_sum(s1) / h, mgx = warp_sum(s2) / h;
   uint4* dxr = reinterpret_cast<uint4*>(dx + static_cast<size_t>(row) * h);
-  const uint4* rr = resid ? reinterpret_cast<const uint4*>(resid + static_cast<size_t>(row) * h) : nullptr;
 #pragma unroll
-  for (int i = 0; i < VPT; ++i) {
-    const int idx = threadIdx.x + i * blockDim.x;
+  for (int i = 0; i < VPL; ++i) {
+    const int idx = lane + 32 * i;
     if (idx < nv) {
-      float o[8], rv[8];
-      if (rr) {
-        unpack8(rr[idx], rv);
-      } else {
+      float a[8], d[8], gm[8], r[8], o[8];
+      unpack8(xv[i], a);
+      unpack8(dv[i], d);
+      unpack8(rv[i], r);
+      unpack8(reinterpret_cast<const uint4*>(gamma)[idx], gm);
 #pragma unroll
-        for (int e = 0; e < 8; ++e) rv[e] = 0.f;
-      }
-#pragma unroll
-      for (int e = 0; e < 8; ++e) o[e] = rv[e] + rs * (g[i][e] - mg - xh[i][e] * mgx);
+      for (int e = 0; e < 8; ++e) o[e] = r[e] + rs * (d[e] * gm[e] - mg - (a[e] - mu) * rs * mgx);
       dxr[idx] = pack8(o);
     }
   }
@@ -312,8 +327,10 @@ __global__ void __launch_bounds__(256) adamw_kernel(float* __restrict__ p, float
                                                     float* __restrict__ v, const float* __restrict__ g,
                                                     bf16* __restrict__ w, int64_t n4, int64_t per_layer, WdRanges wr,
                                                     float lr, float b1, float b2, float eps, float wd, float inv_bc1,
-                                                    float inv_bc2, float grad_scale, int32_t* __restrict__ nonfinite) {
+                                                    float inv_bc2, float grad_scale, int32_t* __restrict__ nonfinite,
+                                                    const int32_t* __restrict__ skip) {
   ptx::grid_dep_wait();
+  if (skip && *skip) return;  // validated mode: this stage's gradients failed (no step)
   bool bad = false;
   for (int64_t i = blockIdx.x * 256LL + threadIdx.x; i < n4; i += static_cast<int64_t>(gridDim.x) * 256) {
     const int64_t e0 = 4 * i;
@@ -345,6 +362,65 @@ __global__ void __launch_bounds__(256) adamw_kernel(float* __restrict__ p, float
     reinterpret_cast<uint2*>(w)[i] = pack4(pa[0], pa[1], pa[2], pa[3]);
   }
   if (nonfinite && __any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicOr(nonfinite, 1);
+}
+
+// Arithmetic reversal of adamw_kernel (oracle adamw_inverse): given
+// the post-step state and the same gradient, restore p, m, v and the bf16 copy.  Acts only
+// if *global_bad (some stage failed validation) and not *own_bad (this stage stepped);
+// the first acting block counts the rollback.
+__global__ void __launch_bounds__(256) adamw_rollback_kernel(
+    float* __restrict__ p, float* __restrict__ m, float* __restrict__ v, const float* __restrict__ g,
+    bf16* __restrict__ w, int64_t n4, int64_t per_layer, WdRanges wr, float lr, float b1, float b2, float eps, float wd,
+    float inv_bc1, float inv_bc2, float grad_scale, const int32_t* __restrict__ global_bad,
+    const int32_t* __restrict__ own_bad, int32_t* __restrict__ count) {
+  ptx::grid_dep_wait();
+  if ((global_bad && !*global_bad) || (own_bad && *own_bad)) return;
+  if (count && blockIdx.x == 0 && threadIdx.x == 0) atomicAdd(count, 1);
+  const float ib1 = 1.f / b1, ib2 = 1.f / b2;
+  for (int64_t i = blockIdx.x * 256LL + threadIdx.x; i < n4; i += static_cast<int64_t>(gridDim.x) * 256) {
+    const int64_t e0 = 4 * i;
+    const int64_t o = e0 % per_layer;
+    const bool decay = (o >= wr.a0 && o < wr.a1) || (o >= wr.b0 && o < wr.b1) || (o >= wr.c0 && o < wr.c1) ||
+                       (o >= wr.d0 && o < wr.d1);
+    const float wdl = decay ? wd : 0.f;
+    float4 pp = reinterpret_cast<float4*>(p)[i];
+    float4 mm = reinterpret_cast<float4*>(m)[i];
+    float4 vv = reinterpret_cast<float4*>(v)[i];
+    const float4 gg = reinterpret_cast<const float4*>(g)[i];
+    float* pa = &pp.x;
+    float* ma = &mm.x;
+    float* va = &vv.x;
+    const float* ga = &gg.x;
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const float gr = grad_scale * ga[e];
+      const float mh = ma[e] * inv_bc1;
+      const float vh = va[e] * inv_bc2;
+      pa[e] = (pa[e] + lr * mh / (sqrtf(vh) + eps)) / (1.f - lr * wdl);
+      ma[e] = (ma[e] - (1.f - b1) * gr) * ib1;
+      va[e] = fmaxf((va[e] - (1.f - b2) * gr * gr) * ib2, 0.f);
+    }
+    reinterpret_cast<float4*>(p)[i] = pp;
+    reinterpret_cast<float4*>(m)[i] = mm;
+    reinterpret_cast<float4*>(v)[i] = vv;
+    reinterpret_cast<uint2*>(w)[i] = pack4(pa[0], pa[1], pa[2], pa[3]);
+  }
+}
+
+// Local validation: OR of "some gradient element is not finite" into
+// *bad (and into *nonfinite for the report).
+__global__ void __launch_bounds__(256) grad_check_kernel(const float* __restrict__ g, int64_t n4,
+                                                         int32_t* __restrict__ bad, int32_t* __restrict__ nonfinite) {
+  ptx::grid_dep_wait();
+  bool b = false;
+  for (int64_t i = blockIdx.x * 256LL + threadIdx.x; i < n4; i += static_cast<int64_t>(gridDim.x) * 256) {
+    const float4 x = reinterpret_cast<const float4*>(g)[i];
+    b |= !isfinite(x.x) || !isfinite(x.y) || !isfinite(x.z) || !isfinite(x.w);
+  }
+  if (__any_sync(0xffffffffu, b) && (threadIdx.x & 31) == 0) {
+    atomicOr(bad, 1);
+    if (nonfinite) atomicOr(nonfinite, 1);
+  }
 }
 
 __global__ void f32_to_bf16_kernel(const float* __restrict__ src, bf16* __restrict__ dst, int64_t n4) {
@@ -396,24 +472,22 @@ int grid_for(int64_t work, int per_block = 256) {
   return g < 1 ? 1 : static_cast<int>(g);
 }
 
-// threads per row for the LayerNorm kernels and vectors per thread
-void ln_shape(int h, int* threads, int* vpt) {
-  const int nv = h / 8;
-  int t = nv <= 512 ? nv : 512;
-  t = (t + 31) / 32 * 32;
-  *threads = t;
-  *vpt = (nv + t - 1) / t;
-}
+// 16-byte vectors per lane for a row of h bf16 (one warp per row)
+int ln_vpl(int h) { return (h / 8 + 31) / 32; }
 
 }  // namespace
 
+#define SLIP_LN_VPL_CASES(X) X(1) X(2) X(4) X(8) X(10) X(16) X(32)
 cudaError_t ln_fwd(const bf16* x, const bf16* gamma, const bf16* beta, bf16* y, float* mean, float* rstd, int T, int h,
                    float eps, cudaStream_t s) {
   if (h % 8 || h > 8192) return cudaErrorInvalidValue;
-  int nt, vpt;
-  ln_shape(h, &nt, &vpt);
-  return launch_pdl(vpt == 1 ? ln_fwd_kernel<1> : ln_fwd_kernel<2>, dim3(T), dim3(nt), 0, s, 1, x, gamma, beta, y,
-                    mean, rstd, h, eps);
+  const int v = ln_vpl(h);
+  const dim3 grid((T + LN_ROWS - 1) / LN_ROWS);
+#define X(n) \
+  if (v <= n) return launch_pdl(ln_fwd_kernel<n>, grid, dim3(256), 0, s, 1, x, gamma, beta, y, mean, rstd, T, h, eps);
+  SLIP_LN_VPL_CASES(X)
+#undef X
+  return cudaErrorInvalidValue;
 }
 
 cudaError_t ln_bwd(const bf16* dy, const bf16* x, const float* mean, const float* rstd, const bf16* gamma,
@@ -422,10 +496,15 @@ cudaError_t ln_bwd(const bf16* dy, const bf16* x, const float* mean, const float
   if (h % 8 || h > 8192) return cudaErrorInvalidValue;
   if ((h + 255) / 256 > kTickets || dx == x) return cudaErrorInvalidValue;
   if (dx) {
-    int nt, vpt;
-    ln_shape(h, &nt, &vpt);
-    cudaError_t e = launch_pdl(vpt == 1 ? ln_bwd_rows_kernel<1> : ln_bwd_rows_kernel<2>, dim3(T), dim3(nt), 0, s, 1,
-                               dy, x, mean, rstd, gamma, resid, dx, h);
+    const int v = ln_vpl(h);
+    const dim3 grid((T + LN_ROWS - 1) / LN_ROWS);
+    cudaError_t e = cudaErrorInvalidValue;
+#define X(n)                                                                                                      \
+  if (e == cudaErrorInvalidValue && v <= n)                                                                       \
+    e = launch_pdl(ln_bwd_rows_kernel<n>, grid, dim3(256), 0, s, 1, dy, x, mean, rstd, gamma, resid, dx, T, h); \
+  else
+    SLIP_LN_VPL_CASES(X) {}
+#undef X
     if (e != cudaSuccess) return e;
   }
   dim3 grid((h + 255) / 256, kRedChunks);
@@ -457,9 +536,40 @@ cudaError_t mse_loss(const bf16* y, const bf16* r, bf16* dy, float* part, int np
                     0.5f / static_cast<float>(n));
 }
 
+namespace {
+WdRanges wd_ranges(int h, int f) {
+  const int64_t H = h, F = f;
+  WdRanges wr;
+  wr.a0 = 0;
+  wr.a1 = 3 * H * H;
+  wr.b0 = 3 * H * H + 3 * H;
+  wr.b1 = wr.b0 + H * H;
+  wr.c0 = 4 * H * H + 8 * H;
+  wr.c1 = wr.c0 + F * H;
+  wr.d0 = wr.c1 + F;
+  wr.d1 = wr.d0 + H * F;
+  return wr;
+}
+}  // namespace
+
+cudaError_t adamw_rollback(float* p, float* m, float* v, const float* g, bf16* w, int64_t n, int64_t per_layer, int h,
+                           int f, float lr, float b1, float b2, float eps, float wd, float bc1, float bc2,
+                           float grad_scale, const int32_t* global_bad, const int32_t* own_bad, int32_t* count,
+                           cudaStream_t s) {
+  if (n % 4 || per_layer % 4) return cudaErrorInvalidValue;
+  return launch_pdl(adamw_rollback_kernel, dim3(grid_for(n / 4)), dim3(256), 0, s, 1, p, m, v, g, w, n / 4, per_layer,
+                    wd_ranges(h, f), lr, b1, b2, eps, wd, 1.0f / bc1, 1.0f / bc2, grad_scale, global_bad, own_bad,
+                    count);
+}
+
+cudaError_t grad_check(const float* g, int64_t n, int32_t* bad, int32_t* nonfinite, cudaStream_t s) {
+  if (n % 4) return cudaErrorInvalidValue;
+  return launch_pdl(grad_check_kernel, dim3(grid_for(n / 4)), dim3(256), 0, s, 1, g, n / 4, bad, nonfinite);
+}
+
 cudaError_t adamw(float* p, float* m, float* v, const float* g, bf16* w, int64_t n, int64_t per_layer, int h, int f,
                   float lr, float b1, float b2, float eps, float wd, float bc1, float bc2, float grad_scale,
-                  int32_t* nonfinite, cudaStream_t s) {
+                  int32_t* nonfinite, cudaStream_t s, const int32_t* skip) {
   if (n % 4 || per_layer % 4) return cudaErrorInvalidValue;
   const int64_t H = h, F = f;
   WdRanges wr;
@@ -472,7 +582,7 @@ cudaError_t adamw(float* p, float* m, float* v, const float* g, bf16* w, int64_t
   wr.d0 = wr.c1 + F;
   wr.d1 = wr.d0 + H * F;
   return launch_pdl(adamw_kernel, dim3(grid_for(n / 4)), dim3(256), 0, s, 1, p, m, v, g, w, n / 4, per_layer, wr, lr,
-                    b1, b2, eps, wd, 1.0f / bc1, 1.0f / bc2, grad_scale, nonfinite);
+                    b1, b2, eps, wd, 1.0f / bc1, 1.0f / bc2, grad_scale, nonfinite, skip);
 }
 
 cudaError_t f32_to_bf16(const float* src, bf16* dst, int64_t n, cudaStream_t s) {

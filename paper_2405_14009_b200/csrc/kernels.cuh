@@ -11,7 +11,7 @@ namespace slip {
 
 using bf16 = __nv_bfloat16;
 
-constexpr int kRedChunks = 16;  // row chunks of the deterministic column reductions
+constexpr int kRedChunks = 64;  // row chunks of the deterministic column reductions
 constexpr int kTickets = 256;   // column strips (256 columns each) a reduction may use
 
 // LayerNorm forward over rows of x [T, h]: y = xhat*gamma + beta; mean, rstd fp32 [T].
@@ -37,9 +37,19 @@ cudaError_t mse_loss(const bf16* y, const bf16* r, bf16* dy, float* part, int np
 // AdamW over flat fp32 arrays (reading R11).  Weight decay applies
 // to the 2-D weights: layer-local offsets in [0, 3h^2), [3h^2+3h, 4h^2+3h),
 // [4h^2+8h, 4h^2+8h+fh), [4h^2+8h+fh+f, 4h^2+8h+2fh+f).
+// skip (device, may be NULL): if *skip != 0 the step is not taken (validated mode).
 cudaError_t adamw(float* p, float* m, float* v, const float* g, bf16* w, int64_t n, int64_t per_layer, int h, int f,
                   float lr, float b1, float b2, float eps, float wd, float bc1, float bc2, float grad_scale,
-                  int32_t* nonfinite, cudaStream_t s);
+                  int32_t* nonfinite, cudaStream_t s, const int32_t* skip = nullptr);
+// Arithmetic reversal of one adamw step with the same gradient;
+// acts only if (global_bad == NULL || *global_bad) and (own_bad == NULL || !*own_bad);
+// count (may be NULL) is incremented when it acts.
+cudaError_t adamw_rollback(float* p, float* m, float* v, const float* g, bf16* w, int64_t n, int64_t per_layer, int h,
+                           int f, float lr, float b1, float b2, float eps, float wd, float bc1, float bc2,
+                           float grad_scale, const int32_t* global_bad, const int32_t* own_bad, int32_t* count,
+                           cudaStream_t s);
+// *bad |= any element of g not finite (and *nonfinite, if not NULL)
+cudaError_t grad_check(const float* g, int64_t n, int32_t* bad, int32_t* nonfinite, cudaStream_t s);
 
 // bf16 <- RNE(fp32)
 cudaError_t f32_to_bf16(const float* src, bf16* dst, int64_t n, cudaStream_t s);

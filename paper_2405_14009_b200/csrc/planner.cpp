@@ -352,6 +352,18 @@ slip_status plan(const Cluster& c, const slip_costs& costs, const slip_plan_opts
     set_error("planner: some stage has no live worker (unrecoverable, PAPER.md §3.4)");
     return SLIP_EUNRECOVERABLE;
   }
+  if (opts.decoupled == 2) {
+    // selective decoupling (§3.2, reading R32): plan with and
+    // without Decoupled BackProp, keep the shorter steady-state period (ties: decoupled)
+    slip_plan_opts od = opts, oc = opts;
+    od.decoupled = 1;
+    oc.decoupled = 0;
+    Plan pd, pc;
+    SLIP_TRY(plan(c, costs, od, pd));
+    SLIP_TRY(plan(c, costs, oc, pc));
+    out = pc.period < pd.period ? std::move(pc) : std::move(pd);
+    return SLIP_OK;
+  }
   Scheduler sch(c, costs, opts, out.exec);
   return sch.run(out.ops, out.makespans, out.period);
 }

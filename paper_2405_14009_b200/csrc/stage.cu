@@ -125,6 +125,7 @@ void carve_ws(Carver& cv, const Dims& d, Workspace* out) {
   w.loss_part = cv.take<float>(256);
   w.losses = cv.take<float>(1024);
   w.nonfinite = cv.take<int32_t>(64);
+  w.vflags = cv.take<int32_t>(64);
   if (out) *out = w;
 }
 
@@ -575,6 +576,63 @@ slip_status slip_synth_normal(void* out_bf16, int64_t n, uint64_t seed, uint64_t
   SLIP_CHECK(out_bf16 && n > 0, SLIP_EINVAL, "synth_normal: bad arguments");
   SLIP_CUDA(synth_normal(static_cast<bf16*>(out_bf16), n, seed, k, j, reinterpret_cast<cudaStream_t>(st)));
   return SLIP_OK;
+}
+
+}  // extern "C"
+
+namespace slip {
+// Validated OPT (executor): own = fault injected ? 1 : any non-finite gradient; step only if !own.
+slip_status validated_step(slip_ctx* c, const slip_adam* a, int64_t step, float grad_scale, int32_t* own, int fault,
+                           cudaStream_t s) {
+  const double bc1 = 1.0 - std::pow(static_cast<double>(a->beta1), static_cast<double>(step));
+  const double bc2 = 1.0 - std::pow(static_cast<double>(a->beta2), static_cast<double>(step));
+  SLIP_CUDA(cudaMemsetAsync(own, 0, sizeof(int32_t), s));
+  if (fault) SLIP_CUDA(cudaMemsetAsync(own, 1, 1, s));
+  SLIP_TRY(kcheck(c, grad_check(c->grad, c->n_params, own, c->ws.nonfinite, s), "grad_check"));
+  return kcheck(c,
+                adamw(c->master, c->adam_m, c->adam_v, c->grad, c->w, c->n_params, c->po.per_layer, c->dm.h, c->dm.f,
+                      a->lr, a->beta1, a->beta2, a->eps, a->weight_decay, static_cast<float>(bc1),
+                      static_cast<float>(bc2), grad_scale, c->ws.nonfinite, s, own),
+                "adamw");
+}
+// Conditional reversal of the step taken with (step, grad_scale): acts iff *glob && !*own.
+slip_status rollback_if(slip_ctx* c, const slip_adam* a, int64_t step, float grad_scale, const int32_t* glob,
+                        const int32_t* own, int32_t* count, cudaStream_t s) {
+  const double bc1 = 1.0 - std::pow(static_cast<double>(a->beta1), static_cast<double>(step));
+  const double bc2 = 1.0 - std::pow(static_cast<double>(a->beta2), static_cast<double>(step));
+  return kcheck(c,
+                adamw_rollback(c->master, c->adam_m, c->adam_v, c->grad, c->w, c->n_params, c->po.per_layer, c->dm.h,
+                               c->dm.f, a->lr, a->beta1, a->beta2, a->eps, a->weight_decay, static_cast<float>(bc1),
+                               static_cast<float>(bc2), grad_scale, glob, own, count, s),
+                "adamw_rollback");
+}
+}  // namespace slip
+
+extern "C" {
+
+slip_status slip_set_validation(slip_ctx* c, int32_t enable) {
+  SLIP_CHECK(c, SLIP_EINVAL, "set_validation: ctx is NULL");
+  c->validate = enable != 0;
+  return SLIP_OK;
+}
+
+slip_status slip_inject_fault(slip_ctx* c, int32_t kind) {
+  SLIP_CHECK(c && (kind == 0 || kind == 1), SLIP_EINVAL, "inject_fault: kind must be 0 or 1");
+  c->fault_next_opt = kind;
+  return SLIP_OK;
+}
+
+slip_status slip_optimizer_rollback(slip_ctx* c, const slip_adam* a, int64_t step, float grad_scale, slip_stream st) {
+  SLIP_CHECK(c && c->bound && a, SLIP_EINVAL, "optimizer_rollback: bad arguments");
+  SLIP_CHECK(step >= 1, SLIP_EINVAL, "optimizer_rollback: step must be >= 1");
+  const double bc1 = 1.0 - std::pow(static_cast<double>(a->beta1), static_cast<double>(step));
+  const double bc2 = 1.0 - std::pow(static_cast<double>(a->beta2), static_cast<double>(step));
+  return kcheck(c,
+                adamw_rollback(c->master, c->adam_m, c->adam_v, c->grad, c->w, c->n_params, c->po.per_layer, c->dm.h,
+                               c->dm.f, a->lr, a->beta1, a->beta2, a->eps, a->weight_decay, static_cast<float>(bc1),
+                               static_cast<float>(bc2), grad_scale, nullptr, nullptr, nullptr,
+                               reinterpret_cast<cudaStream_t>(st)),
+                "adamw_rollback");
 }
 
 slip_status slip_set_sm_reserve(int32_t n) {

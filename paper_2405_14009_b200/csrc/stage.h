@@ -46,6 +46,7 @@ struct Workspace {
   float* loss_part;  // [256] MSE partials
   float* losses;     // [1024] per-micro-batch losses (executor)
   int32_t* nonfinite;  // [1] post-step validation flag (executor)
+  int32_t* vflags;     // [8] validated mode: own_bad[2], global_bad[2] (per iteration parity), rollbacks
 };
 
 enum SlotState : int { SLOT_FREE = 0, SLOT_F_DONE = 1, SLOT_B_DONE = 2 };
@@ -77,6 +78,8 @@ struct slip_ctx {
   int64_t launches = 0;  // kernels enqueued through this context
   int64_t opt_step = 0;  // AdamW steps taken by the executor
   bool trace_on = false;
+  bool validate = false;   // post-step validation + cross-stage rollback (slip_set_validation)
+  int fault_next_opt = 0;  // slip_inject_fault: the next validation reports non-finite gradients
   std::vector<slip_trace_rec> trace;  // timeline of the last traced executor run
 };
 
@@ -85,4 +88,8 @@ slip_status check_model(const slip_model* m);
 Dims make_dims(const slip_model& m);
 size_t stash_bytes_per_slot(const Dims& d, int L);
 size_t workspace_bytes(const Dims& d);
+slip_status validated_step(slip_ctx* c, const slip_adam* a, int64_t step, float grad_scale, int32_t* own, int fault,
+                           cudaStream_t s);
+slip_status rollback_if(slip_ctx* c, const slip_adam* a, int64_t step, float grad_scale, const int32_t* glob,
+                        const int32_t* own, int32_t* count, cudaStream_t s);
 }  // namespace slip

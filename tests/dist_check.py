@@ -143,6 +143,70 @@ def migrate_scenario(a, cfg, L, comm, costs, rank, world, holder):
     return flag.item() == 1.0
 
 
+def validate_scenario(a, cfg, L, comm, costs, rank, world, holder):
+    """Post-step validation with cross-stage rollback (§4.3,
+    reading R31).  Iteration 1 trains normally.  In iteration 2 stage 0 reports
+    non-finite gradients (slip_inject_fault): it must skip its step (weights bit-equal
+    to after iteration 1) while the other stages, which stepped on their own
+    validation, must roll the step back (weights equal to after iteration 1 within the
+    fp32 reversal error) and report one rollback each.  Iteration 3 then trains
+    normally again and all live peers of a stage stay bit-identical."""
+    DP, PP, m = a.dp, a.pp, a.m
+    g = torch.Generator().manual_seed(5)
+    xs = [torch.randn(cfg.tokens, cfg.hidden, generator=g).to(torch.bfloat16).pin_memory() for _ in range(DP * m)]
+    rs = [torch.randn(cfg.tokens, cfg.hidden, generator=g).to(torch.bfloat16).pin_memory() for _ in range(DP * m)]
+    adam = (1e-3, 0.9, 0.95, 1e-8, 0.1)
+    full = [[1] * DP for _ in range(PP)]
+    me_i = rank % PP
+    st = holder["stage"] = rt.Stage(cfg, L, n_slots=2 * m * DP)
+    rt.init_master_(st.master, cfg, L, cfg.layers, seed=100 + me_i)
+    rt.call("slip_weights_from_master", st.ctx, rt._stream())
+    rt.call("slip_set_validation", st.ctx, 1)
+    comm.setup(PP, DP, m, full)
+
+    def iterate():
+        losses = torch.zeros(DP * m, dtype=torch.float32).pin_memory()
+        rep = rt.execute_schedule(st, comm, PP, DP, m, full, costs, True, True, adam=adam, iterations=1,
+                                  io=rt.make_io(xs, rs, losses))
+        torch.cuda.synchronize()
+        return rep
+
+    r1 = iterate()
+    p1, m1, v1, w1 = st.master.clone(), st.adam_m.clone(), st.adam_v.clone(), st.w.clone()
+    if me_i == 0:
+        rt.call("slip_inject_fault", st.ctx, 1)
+    r2 = iterate()
+    p2, w2 = st.master.clone(), st.w.clone()
+    res = {"rank": rank, "stage": me_i, "rollbacks": [r1.rollbacks, r2.rollbacks], "nonfinite": r2.nonfinite}
+    ok = r1.rollbacks == 0
+    if me_i == 0:
+        ok &= bool(torch.equal(p2, p1)) and bool(torch.equal(w2, w1)) and r2.rollbacks == 0
+        res["skipped_bit_equal"] = bool(torch.equal(p2, p1))
+    else:
+        e = ((p2 - p1).abs().max() / p1.abs().max()).item()
+        em = ((st.adam_m - m1).abs().max() / m1.abs().max()).item()
+        res["rollback_relerr_master"] = e
+        res["rollback_relerr_m"] = em
+        res["bf16_mismatch_frac"] = (w2 != w1).float().mean().item()
+        ok &= e <= 1e-6 and em <= 1e-4 and r2.rollbacks == 1
+    r3 = iterate()
+    res["rollbacks3"] = r3.rollbacks
+    ok &= r3.rollbacks == 0
+    ck = torch.tensor([float(st.master.double().sum().item()), float(me_i)], dtype=torch.float64, device="cuda")
+    allck = [torch.zeros_like(ck) for _ in range(world)]
+    dist.all_gather(allck, ck)
+    for r2_ in range(world):
+        if int(allck[r2_][1].item()) == me_i:
+            ok &= allck[r2_][0].item() == ck[0].item()
+    flag = torch.tensor([1.0 if ok else 0.0], device="cuda")
+    dist.all_reduce(flag, op=dist.ReduceOp.MIN)
+    outs = [None] * world
+    dist.all_gather_object(outs, res)
+    if rank == 0:
+        print(json.dumps({"scenario": "validate", "ok": flag.item() == 1.0, "ranks": outs}), flush=True)
+    return flag.item() == 1.0
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--dp", type=int, default=2)
@@ -150,6 +214,7 @@ def main():
     ap.add_argument("--m", type=int, default=3)
     ap.add_argument("--failures", default="auto")
     ap.add_argument("--migrate", action="store_true", help="normalization swap scenario (PP >= 2)")
+    ap.add_argument("--validate", action="store_true", help="post-step validation / rollback scenario (PP >= 2)")
     a = ap.parse_args()
     rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
     local = int(os.environ.get("LOCAL_RANK", rank))
@@ -188,8 +253,8 @@ def main():
         torch.cuda.synchronize()
         return rep, stage.grad.clone(), stage.master.clone(), losses.clone()
 
-    if a.migrate:
-        ok = migrate_scenario(a, cfg, L, comm, costs, rank, world, holder)
+    if a.migrate or a.validate:
+        ok = (migrate_scenario if a.migrate else validate_scenario)(a, cfg, L, comm, costs, rank, world, holder)
         comm.close()
         holder["stage"].close()
         dist.destroy_process_group()

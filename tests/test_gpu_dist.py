@@ -44,3 +44,11 @@ def test_dp2_pp2_normalization_swap():
     that takes over the role continues training identically (dist_check --migrate)."""
     out = _run(4, 2, 2, "--migrate")
     assert '"scenario": "migrate", "ok": true' in out
+
+
+@pytest.mark.skipif(torch.cuda.device_count() < 4, reason="needs 4 GPUs")
+def test_dp2_pp2_validation_rollback():
+    """Stage 0 fails validation in iteration 2: it skips its step, stage 1 (which
+    stepped on its own validation) rolls back (dist_check --validate)."""
+    out = _run(4, 2, 2, "--validate")
+    assert '"scenario": "validate", "ok": true' in out

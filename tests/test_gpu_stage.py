@@ -167,6 +167,30 @@ def test_adamw_matches_oracle():
     assert int(flag.item()) == 1
 
 
+def test_adamw_rollback_reverses_the_step():
+    """slip_optimizer_rollback (reading R31) against the oracle's
+    inverse: after 3 steps, reversing step 3 on the GPU restores master / m / v to the
+    state after step 2 within fp32 reversal error, and the bf16 copy is RNE(master)."""
+    from paper_2405_14009_b200._binding import slip_adam
+    import ctypes as C
+    rt = _rt()
+    cfg = sd.C1_TINY
+    st, layers, x, r, y, dx = run_stage(cfg, 1)
+    for step in (1, 2):
+        st.optimizer_step(step, grad_scale=0.25)
+    torch.cuda.synchronize()
+    p2, m2, v2 = st.master.clone(), st.adam_m.clone(), st.adam_v.clone()
+    st.optimizer_step(3, grad_scale=0.25)
+    a = slip_adam(1e-3, 0.9, 0.95, 1e-8, 0.1)
+    rt.call("slip_optimizer_rollback", st.ctx, C.byref(a), 3, 0.25, rt._stream())
+    torch.cuda.synchronize()
+    assert ((st.master - p2).abs().max() / p2.abs().max()).item() <= 1e-6
+    assert ((st.adam_m - m2).abs().max() / m2.abs().max()).item() <= 1e-5
+    assert ((st.adam_v - v2).abs().max() / v2.abs().max()).item() <= 1e-4
+    w = st.w.float().cpu().numpy().astype(np.float64)
+    assert np.array_equal(w, sd.bf16_round(st.master.cpu().numpy().astype(np.float64)))
+
+
 def test_mse_head_and_synth():
     rt = _rt()
     cfg = sd.C1_TINY

@@ -49,3 +49,31 @@ def test_nonfinite_flag():
     assert not nonfinite({"a": np.ones(3)})
     assert nonfinite({"a": np.array([1.0, np.inf])})
     assert nonfinite({"a": np.array([np.nan])})
+
+
+def test_adamw_inverse_round_trip_and_step1_closed_form():
+    """Rollback pins (reading R31): the inverse undoes a step to
+    fp64 rounding for random states and steps; at step 1 from m = v = 0 it recovers
+    exactly zero moments and the closed form p0 = (p1 + lr sign(g)) / (1 - lr wd)
+    (|g| >> eps)."""
+    import numpy as np
+    from oracle import adam as A
+    rng = np.random.default_rng(31)
+    cfg = A.AdamCfg()
+    for t in (1, 2, 7, 100):
+        p0 = rng.standard_normal(1000)
+        m0 = rng.standard_normal(1000) * 1e-2 if t > 1 else np.zeros(1000)
+        v0 = rng.random(1000) * 1e-3 if t > 1 else np.zeros(1000)
+        g = rng.standard_normal(1000)
+        for decay in (True, False):
+            p1, m1, v1 = A.adamw_step(p0, m0, v0, g, t, cfg, grad_scale=0.25, decay=decay)
+            q0, n0, w0 = A.adamw_inverse(p1, m1, v1, g, t, cfg, grad_scale=0.25, decay=decay)
+            assert np.allclose(q0, p0, rtol=1e-12, atol=1e-14)
+            assert np.allclose(n0, m0, rtol=1e-10, atol=1e-16)
+            assert np.allclose(w0, v0, rtol=1e-8, atol=1e-16)
+    g = rng.standard_normal(100)
+    p0 = rng.standard_normal(100)
+    p1, m1, v1 = A.adamw_step(p0, np.zeros(100), np.zeros(100), g, 1, cfg)
+    assert np.allclose(p1, p0 - cfg.lr * cfg.weight_decay * p0 - cfg.lr * np.sign(g), atol=1e-9)
+    q0, n0, w0 = A.adamw_inverse(p1, m1, v1, g, 1, cfg)
+    assert np.allclose(n0, 0.0, atol=1e-15) and np.allclose(w0, 0.0, atol=1e-15)

@@ -38,7 +38,7 @@ def instances(n, seed=5):
         lim = 0 if rng.integers(0, 2) else int(af * (N + 1) * 2)
         costs = PL.Costs(*(int(rng.integers(1, 9)) for _ in range(3)), int(rng.integers(0, 4)),
                          int(rng.integers(0, 4)), int(rng.integers(0, 4)), af, aw, lim)
-        out.append((N, DP, m, sorted(failed), costs, bool(rng.integers(0, 2)), bool(rng.integers(0, 2)),
+        out.append((N, DP, m, sorted(failed), costs, int(rng.integers(0, 3)), bool(rng.integers(0, 2)),
                     int(rng.integers(1, 4))))
     return out
 
@@ -70,3 +70,23 @@ def test_cpp_recoverable_and_unrecoverable():
     with pytest.raises(rt.SlipError) as e:
         rt.plan_schedule(2, 2, 2, live_grid(2, 2, [(1, 0), (1, 1)]), rt.make_costs())
     assert e.value.code == 2  # SLIP_EUNRECOVERABLE
+
+
+def test_selective_decoupling_is_the_better_of_both():
+    """decoupled = 2 (reading R32) returns exactly the plan with the shorter period of
+    decoupled / coupled (ties: decoupled), in C++ and in the oracle.  (With the list
+    scheduler the decoupled plan is never longer on these instances.)"""
+    rt = _rt()
+    rng = np.random.default_rng(9)
+    for _ in range(40):
+        N, DP, m = int(rng.integers(2, 5)), int(rng.integers(2, 4)), int(rng.integers(2, 9))
+        failed = [(N - 1, 1)] if rng.integers(0, 2) else []
+        lv = live_grid(N, DP, failed)
+        c = PL.Costs(*(int(rng.integers(1, 9)) for _ in range(3)), 1, 1, 1)
+        pd = PL.schedule(lv, m, c, PL.Opts(True, True, 3))
+        pc = PL.schedule(lv, m, c, PL.Opts(False, True, 3))
+        pa = PL.schedule(lv, m, c, PL.Opts(2, True, 3))
+        assert pa.period == min(pd.period, pc.period)
+        assert [o.key() for o in pa.ops] == [o.key() for o in (pc if pc.period < pd.period else pd).ops]
+        costs = rt.make_costs(c.t_f, c.t_b, c.t_w, c.t_comm, c.t_ar, c.t_opt)
+        assert rt.plan_schedule(N, DP, m, lv, costs, 2, True, 3).period == pa.period
