@@ -58,6 +58,7 @@ def parse():
                     help="Algorithm 1 + P2P migration swaps before the timed steps (needs --failed-at)")
     ap.add_argument("--sm-reserve", type=int, default=-1,
                     help="SMs kept free of persistent GEMM CTAs for NCCL kernels (default: 0 at N=1, 8 at N>1)")
+    ap.add_argument("--p2p-ctas", type=int, default=2, help="CTAs per NCCL P2P kernel (0: NCCL default)")
     ap.add_argument("--trace", default="", help="directory: dump one traced 2-iteration run per rank (JSON)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -269,6 +270,7 @@ def main():
     rt.init_master_(stage.master, cfg, L, args.layers, seed=rank % PP)
     rt.call("slip_weights_from_master", stage.ctx, rt._stream())
     comm = rt.Comm(rank, world)
+    comm.set_p2p_ctas(args.p2p_ctas)
     comm.setup(PP, DP, m, live)
     stream = torch.cuda.current_stream()
 
@@ -459,6 +461,7 @@ def main():
                                    len(failed)),
                    "model": "gpt-%s-shape" % MODEL, "global_batch": DP * m * MB, "seq_len": SEQ,
                    "parallelism": "dp%dxpp%d" % (DP, PP), "failed_workers": failed, "sm_reserve": sm_reserve,
+                   "p2p_ctas": args.p2p_ctas,
                    "l2": "inputs larger than L2 (2.4 GB bf16 weights + GBs of stash per step)"},
         "clocks": clk,
         "e2e": e2e,

@@ -305,6 +305,12 @@ slip_status slip_comm_create(slip_comm** out, int32_t rank, int32_t world, const
 slip_status slip_comm_setup(slip_comm* comm, const slip_cluster* c);
 slip_status slip_comm_destroy(slip_comm* comm);
 
+/* CTAs (SMs) each activation / gradient transfer kernel may use (the pair
+ * communicators' NCCL maxCTAs; 0 = NCCL's default; default 2).  Those kernels run
+ * concurrently with the persistent compute kernels, which lose the SMs they hold
+ * for as long as a transfer waits for its peer.  Call before slip_comm_setup. */
+slip_status slip_comm_set_p2p_ctas(slip_comm* comm, int32_t n);
+
 /* Worker position this process plays, as the role rank k*N + i of worker
  * (stage i, pipeline k); default = its world rank.  After a normalization
  * swap (slip_migration_plan) the GPU that sat at the target position plays the

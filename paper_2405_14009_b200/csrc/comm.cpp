@@ -120,12 +120,21 @@ slip_status slip_comm_setup(slip_comm* c, const slip_cluster* cl) {
         pairs.insert({a, b});
         pairs.insert({b, a});
       }
+  // Pair communicators carry one [T, h] activation / gradient at a time and their kernels
+  // run concurrently with the persistent compute kernels: cap each at c->p2p_ctas CTAs
+  // (SMs) so that the transfers a worker has outstanding fit in the SM reserve
+  // (slip_set_sm_reserve) instead of starving the GEMM grids.
+  ncclConfig_t pcfg = NCCL_CONFIG_INITIALIZER;
+  if (c->p2p_ctas > 0) {
+    pcfg.minCTAs = 1;
+    pcfg.maxCTAs = c->p2p_ctas;
+  }
   int color = 0;
   for (const auto& pr : pairs) {
     const bool member = c->role == pr.first || c->role == pr.second;
     ncclComm_t pc = nullptr;
     SLIP_NCCL(ncclCommSplit(c->world_comm, member ? color : NCCL_SPLIT_NOCOLOR, c->role == pr.first ? 0 : 1, &pc,
-                            nullptr));
+                            c->p2p_ctas > 0 ? &pcfg : nullptr));
     if (member) {
       c->pair_comm[pr] = pc;
       cudaStream_t st;
@@ -143,6 +152,13 @@ slip_status slip_comm_destroy(slip_comm* c) {
   destroy_setup(c);
   if (c->world_comm) ncclCommDestroy(c->world_comm);
   delete c;
+  return SLIP_OK;
+}
+
+slip_status slip_comm_set_p2p_ctas(slip_comm* c, int32_t n) {
+  SLIP_CHECK(c && n >= 0 && n <= 64, SLIP_EINVAL, "comm_set_p2p_ctas: n must be in [0, 64]");
+  destroy_setup(c);
+  c->p2p_ctas = n;
   return SLIP_OK;
 }
 

@@ -14,6 +14,7 @@
 struct slip_comm {
   int rank = 0, world = 1;
   int role = 0;  // worker position k*N + i this process plays (default: its world rank)
+  int p2p_ctas = 2;  // CTAs per pair-communicator kernel (0: NCCL's default)
   ncclComm_t world_comm = nullptr;
   bool ready = false;
   slip::Cluster cl;

@@ -303,6 +303,10 @@ class Comm:
         self.h, self.rank, self.world = h, rank, world
         self._cluster = None
 
+    def set_p2p_ctas(self, n: int):
+        """CTAs per activation / gradient transfer kernel (0: NCCL default)."""
+        call("slip_comm_set_p2p_ctas", self.h, int(n))
+
     def set_role(self, role: int):
         """Play worker position `role` = k*N + i (after a normalization swap)."""
         call("slip_comm_set_role", self.h, int(role))
