@@ -73,6 +73,12 @@ typedef enum { SLIP_F = 0, SLIP_B = 1, SLIP_W = 2, SLIP_BC = 3, SLIP_OPT = 4, SL
 typedef struct {
   int32_t hidden, heads, ffn, seq, micro_batch;
   float ln_eps;
+  /* GPT model ends hosted by this stage (reading R33):
+   * ends bit 0 = token + position embedding (first stage: the stage input is T
+   * int32 token ids), bit 1 = final LayerNorm + LM head + cross-entropy (last
+   * stage: slip_loss_ce replaces the MSE head).  vocab = padded vocabulary
+   * (multiple of 128, e.g. 50257 -> 50304); ignored when ends == 0. */
+  int32_t vocab, ends;
 } slip_model;
 
 /* Cluster (SPEC core_model.ClusterConfig): N stages x DP pipelines, m
@@ -190,7 +196,10 @@ slip_status slip_migration_plan(const slip_cluster* c, const int32_t* R, slip_sw
  *   Wqkv[3h,h] bqkv[3h] Wo[h,h] bo[h] g1[h] b1n[h] g2[h] b2n[h]
  *   W1[f,h] b1[f] W2[h,f] b2[h]                        (12h^2+13h for f = 4h)
  * QKV rows are the [Q; K; V] blocks; head n uses rows n*d .. (n+1)*d - 1 of
- * each block.  Linear weights are [out, in]. */
+ * each block.  Linear weights are [out, in].  After the layers, the ends:
+ *   embedding (ends bit 0):  E[vocab,h] P[seq,h]
+ *   LM head   (ends bit 1):  gf[h] bf[h] Wout[vocab,h]
+ * AdamW decays the 2-D tensors (E, P, Wout included), not gf / bf. */
 slip_status slip_param_count(const slip_model* m, int32_t n_layers, int64_t* out);
 
 /* Bytes of the stash arena for n_slots in-flight micro-batches (F-stash +
@@ -222,7 +231,12 @@ slip_status slip_slot_ptr(slip_ctx* ctx, int32_t slot, int32_t which, void** out
 
 /* F (§4.2 c = F): x_in [T,h] bf16 device -> y_out [T,h] bf16
  * device, through all layers of the stage; writes the slot's F-stash.  x_in
- * is copied into the slot unless it already is the slot's input buffer. */
+ * is copied into the slot unless it already is the slot's input buffer.  With
+ * the embedding end (model.ends bit 0) x_in is T int32 token ids and the stage
+ * input is E[tok] + P[t mod seq].  B then always writes the embedding-output
+ * gradient into the slot (dx may be NULL) and W adds the embedding scatter
+ * dE[v] += sum_{t: tok_t = v} dX_t, dP[p] += sum_{t mod seq = p} dX_t
+ * (deterministic: one CTA per distinct token, rows summed in t order). */
 slip_status slip_stage_forward(slip_ctx* ctx, int32_t slot, const void* x_in, void* y_out, slip_stream s);
 
 /* B = B_input (§3.2): dy [T,h] bf16 = dL/d(stage
@@ -261,6 +275,19 @@ slip_status slip_loss_mse(slip_ctx* ctx, const void* y, const void* target, void
  * counter-based generator keyed by (seed, k, j), so a re-routed micro-batch
  * sees the same data on whichever peer runs it. */
 slip_status slip_synth_normal(void* out_bf16, int64_t n, uint64_t seed, uint64_t k, uint64_t j, slip_stream s);
+
+/* Last stage with the LM head (model.ends bit 1): y = stage output [T, h], labels
+ * = T int32 class ids (device) < vocab.  Final LayerNorm, logits = Y Wout^T, loss
+ * = mean_t (lse_t - logits_t[label_t]) into *d_loss (device fp32), and the head's
+ * input gradients: dy = d loss / d y (may alias y), gf / bf gradients (B); dLogits
+ * and Y stay in the slot's stash for W (dWout += dLogits^T Y in the slot's grouped
+ * W launch).  The slot must hold a forward (F done).  accumulate as in B. */
+slip_status slip_loss_ce(slip_ctx* ctx, int32_t slot, const void* y, const int32_t* labels, void* dy, float* d_loss,
+                         int32_t accumulate, slip_stream s);
+
+/* Uniform synthetic token ids in [0, n_classes): out[t] = Philox(seed, k, j, t). */
+slip_status slip_synth_tokens(int32_t* out, int64_t n, int32_t n_classes, uint64_t seed, uint64_t k, uint64_t j,
+                              slip_stream s);
 
 /* w_bf16 <- RNE(master) (after loading master weights). */
 slip_status slip_weights_from_master(slip_ctx* ctx, slip_stream s);
@@ -372,7 +399,9 @@ slip_status slip_rank_program(const slip_cluster* c, const slip_costs* costs, co
  * Host buffers for an end-to-end run (may be NULL: inputs are then generated
  * on the device by slip_synth_normal with (seed, k, j) and targets with
  * (seed + 1, k, j)).  x_host[k*m + j] / target_host[k*m + j]: pinned host
- * [T,h] bf16; loss_host[k*m + j] receives each micro-batch's loss. */
+ * [T,h] bf16 — or T int32 token ids / labels when the first / last stage hosts
+ * the embedding / LM-head end (slip_synth_tokens when NULL); loss_host[k*m + j]
+ * receives each micro-batch's loss. */
 typedef struct {
   const void* const* x_host;
   const void* const* target_host;

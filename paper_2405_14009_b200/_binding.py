@@ -23,7 +23,7 @@ class SlipError(RuntimeError):
 
 class slip_model(C.Structure):
     _fields_ = [("hidden", C.c_int32), ("heads", C.c_int32), ("ffn", C.c_int32), ("seq", C.c_int32),
-                ("micro_batch", C.c_int32), ("ln_eps", C.c_float)]
+                ("micro_batch", C.c_int32), ("ln_eps", C.c_float), ("vocab", C.c_int32), ("ends", C.c_int32)]
 
 
 class slip_cluster(C.Structure):
@@ -130,6 +130,8 @@ SIGNATURES = {
     "slip_comm_set_role": (C.c_int, [P, I32]),
     "slip_comm_set_p2p_ctas": (C.c_int, [P, I32]),
     "slip_set_sm_reserve": (C.c_int, [I32]),
+    "slip_loss_ce": (C.c_int, [P, I32, P, P, P, P, I32, P]),
+    "slip_synth_tokens": (C.c_int, [P, I64, I32, U64, U64, U64, P]),
     "slip_set_validation": (C.c_int, [P, I32]),
     "slip_inject_fault": (C.c_int, [P, I32]),
     "slip_optimizer_rollback": (C.c_int, [P, C.POINTER(slip_adam), I64, F32, P]),

@@ -189,7 +189,16 @@ extern "C" slip_status slip_execute_schedule(slip_ctx* ctx, slip_comm* comm, con
         case SLIP_ACT_LOAD_X: {
           if (se->freed) SLIP_CUDA(cudaStreamWaitEvent(cs, se->freed, 0));
           SLIP_CUDA(trace_begin());
-          if (io && io->x_host) {
+          if (ctx->dm.ends & 1) {  // the stage input is T token ids (embedding end)
+            int32_t* tok = sb->end.tokens;
+            if (io && io->x_host) {
+              SLIP_CUDA(cudaMemcpyAsync(tok, io->x_host[a.origin * m + a.mb], D.T * sizeof(int32_t),
+                                        cudaMemcpyHostToDevice, cs));
+            } else {
+              SLIP_CUDA(synth_tokens(tok, D.T, D.V, seed, a.origin, a.mb, cs));
+              ctx->launches += 1;
+            }
+          } else if (io && io->x_host) {
             SLIP_CUDA(cudaMemcpyAsync(sb->x, io->x_host[a.origin * m + a.mb], bytes, cudaMemcpyHostToDevice, cs));
           } else {
             SLIP_CUDA(synth_normal(sb->x, static_cast<int64_t>(Th), seed, a.origin, a.mb, cs));
@@ -209,7 +218,8 @@ extern "C" slip_status slip_execute_schedule(slip_ctx* ctx, slip_comm* comm, con
         case SLIP_ACT_F:
           if (se->sent_y) SLIP_CUDA(cudaStreamWaitEvent(cs, se->sent_y, 0));
           SLIP_CUDA(trace_begin());
-          SLIP_TRY(slip_stage_forward(ctx, a.slot, sb->x, sb->dy, stream));
+          SLIP_TRY(slip_stage_forward(ctx, a.slot, (ctx->dm.ends & 1) ? static_cast<void*>(sb->end.tokens) : sb->x,
+                                      sb->dy, stream));
           break;
         case SLIP_ACT_SEND_Y: {
           cudaStream_t ps = xfer_stream(me, a.peer);
@@ -224,6 +234,19 @@ extern "C" slip_status slip_execute_schedule(slip_ctx* ctx, slip_comm* comm, con
         case SLIP_ACT_LOSS: {
           bf16* target = ctx->ws.dy1;  // B's temporaries are free before the head runs
           SLIP_CUDA(trace_begin());
+          if (ctx->dm.ends & 2) {  // LM head + cross-entropy on T int32 labels
+            int32_t* labels = reinterpret_cast<int32_t*>(target);
+            if (io && io->target_host) {
+              SLIP_CUDA(cudaMemcpyAsync(labels, io->target_host[a.origin * m + a.mb], D.T * sizeof(int32_t),
+                                        cudaMemcpyHostToDevice, cs));
+            } else {
+              SLIP_CUDA(synth_tokens(labels, D.T, D.V, seed + 1, a.origin, a.mb, cs));
+              ctx->launches += 1;
+            }
+            SLIP_TRY(slip_loss_ce(ctx, a.slot, sb->dy, labels, sb->dy, d_losses + a.origin * m + a.mb, a.accumulate & 1,
+                                  stream));
+            break;
+          }
           if (io && io->target_host) {
             SLIP_CUDA(
                 cudaMemcpyAsync(target, io->target_host[a.origin * m + a.mb], bytes, cudaMemcpyHostToDevice, cs));

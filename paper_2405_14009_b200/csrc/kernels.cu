@@ -321,7 +321,14 @@ __global__ void mse_finalize_kernel(const float* __restrict__ part, int nparts, 
 // ------------------------------------------------------------------ AdamW
 struct WdRanges {
   int64_t a0, a1, b0, b1, c0, c1, d0, d1;
+  TailDecay tail;
 };
+__device__ __forceinline__ bool decays(const WdRanges& wr, int64_t e0, int64_t per_layer) {
+  if (e0 >= wr.tail.start) return (e0 >= wr.tail.a0 && e0 < wr.tail.a1) || (e0 >= wr.tail.b0 && e0 < wr.tail.b1);
+  const int64_t o = e0 % per_layer;
+  return (o >= wr.a0 && o < wr.a1) || (o >= wr.b0 && o < wr.b1) || (o >= wr.c0 && o < wr.c1) ||
+         (o >= wr.d0 && o < wr.d1);
+}
 
 __global__ void __launch_bounds__(256) adamw_kernel(float* __restrict__ p, float* __restrict__ m,
                                                     float* __restrict__ v, const float* __restrict__ g,
@@ -334,9 +341,7 @@ __global__ void __launch_bounds__(256) adamw_kernel(float* __restrict__ p, float
   bool bad = false;
   for (int64_t i = blockIdx.x * 256LL + threadIdx.x; i < n4; i += static_cast<int64_t>(gridDim.x) * 256) {
     const int64_t e0 = 4 * i;
-    const int64_t o = e0 % per_layer;
-    const bool decay = (o >= wr.a0 && o < wr.a1) || (o >= wr.b0 && o < wr.b1) || (o >= wr.c0 && o < wr.c1) ||
-                       (o >= wr.d0 && o < wr.d1);
+    const bool decay = decays(wr, e0, per_layer);
     const float wdl = decay ? wd : 0.f;
     float4 pp = reinterpret_cast<float4*>(p)[i];
     float4 mm = reinterpret_cast<float4*>(m)[i];
@@ -379,9 +384,7 @@ __global__ void __launch_bounds__(256) adamw_rollback_kernel(
   const float ib1 = 1.f / b1, ib2 = 1.f / b2;
   for (int64_t i = blockIdx.x * 256LL + threadIdx.x; i < n4; i += static_cast<int64_t>(gridDim.x) * 256) {
     const int64_t e0 = 4 * i;
-    const int64_t o = e0 % per_layer;
-    const bool decay = (o >= wr.a0 && o < wr.a1) || (o >= wr.b0 && o < wr.b1) || (o >= wr.c0 && o < wr.c1) ||
-                       (o >= wr.d0 && o < wr.d1);
+    const bool decay = decays(wr, e0, per_layer);
     const float wdl = decay ? wd : 0.f;
     float4 pp = reinterpret_cast<float4*>(p)[i];
     float4 mm = reinterpret_cast<float4*>(m)[i];
@@ -463,6 +466,139 @@ __global__ void synth_normal_kernel(bf16* __restrict__ out, int64_t n, uint2 key
 #pragma unroll
     for (int e = 0; e < 4; ++e)
       if (4 * i + e < n) out[4 * i + e] = __float2bfloat16_rn(z[e]);
+  }
+}
+
+// ------------------------------------------------------------------ GPT ends (reading R33)
+// X[t] = E[tok[t]] + P[t mod seq]: one warp per token row, 16-byte vectors.
+__global__ void __launch_bounds__(256) embed_fwd_kernel(const bf16* __restrict__ E, const bf16* __restrict__ P,
+                                                        const int32_t* __restrict__ tok, bf16* __restrict__ X, int T,
+                                                        int h, int seq) {
+  ptx::grid_dep_wait();
+  const int t = blockIdx.x * 8 + (threadIdx.x >> 5), lane = threadIdx.x & 31;
+  if (t >= T) return;
+  const uint4* er = reinterpret_cast<const uint4*>(E + static_cast<int64_t>(tok[t]) * h);
+  const uint4* pr = reinterpret_cast<const uint4*>(P + static_cast<int64_t>(t % seq) * h);
+  uint4* xr = reinterpret_cast<uint4*>(X + static_cast<int64_t>(t) * h);
+  for (int i = lane; i < h / 8; i += 32) {
+    float a[8], b[8];
+    unpack8(er[i], a);
+    unpack8(pr[i], b);
+#pragma unroll
+    for (int e = 0; e < 8; ++e) a[e] += b[e];
+    xr[i] = pack8(a);
+  }
+}
+
+// Embedding scatter, deterministic without atomics: block t owns token tok[t] iff t is
+// its first occurrence, and sums the rows of every occurrence in t order.  Blocks
+// T .. T+seq-1 own the position rows (sum over the micro-batch's sequences in order).
+__global__ void __launch_bounds__(256) embed_bwd_kernel(const bf16* __restrict__ dX, const int32_t* __restrict__ tok,
+                                                        float* __restrict__ dE, float* __restrict__ dP, int T, int h,
+                                                        int seq, int accumulate) {
+  ptx::grid_dep_wait();
+  __shared__ int first;
+  const int b = blockIdx.x;
+  if (b < T) {
+    const int v = tok[b];
+    if (threadIdx.x == 0) first = 1;
+    __syncthreads();
+    for (int u = threadIdx.x; u < b; u += blockDim.x)
+      if (tok[u] == v) first = 0;
+    __syncthreads();
+    if (!first) return;
+    float* out = dE + static_cast<int64_t>(v) * h;
+    for (int c = threadIdx.x; c < h; c += blockDim.x) {
+      float acc = 0.f;
+      for (int u = b; u < T; ++u)
+        if (tok[u] == v) acc += __bfloat162float(dX[static_cast<int64_t>(u) * h + c]);
+      out[c] = accumulate ? out[c] + acc : acc;
+    }
+  } else {
+    const int p = b - T;
+    float* out = dP + static_cast<int64_t>(p) * h;
+    for (int c = threadIdx.x; c < h; c += blockDim.x) {
+      float acc = 0.f;
+      for (int u = p; u < T; u += seq) acc += __bfloat162float(dX[static_cast<int64_t>(u) * h + c]);
+      out[c] = accumulate ? out[c] + acc : acc;
+    }
+  }
+}
+
+// Cross-entropy over one logits row per block (V bf16, read three times from L1/L2):
+// max, sum of exp, then dLogits in place and the row's loss.
+__global__ void __launch_bounds__(512) ce_rows_kernel(bf16* __restrict__ logits, const int32_t* __restrict__ labels,
+                                                      float* __restrict__ row_loss, int V, float inv_T) {
+  __shared__ float2 red[33];
+  ptx::grid_dep_wait();
+  const int t = blockIdx.x;
+  bf16* row = logits + static_cast<int64_t>(t) * V;
+  const uint4* r4 = reinterpret_cast<const uint4*>(row);
+  const int nv = V / 8;
+  float mx = -INFINITY;
+  for (int i = threadIdx.x; i < nv; i += blockDim.x) {
+    float a[8];
+    unpack8(r4[i], a);
+#pragma unroll
+    for (int e = 0; e < 8; ++e) mx = fmaxf(mx, a[e]);
+  }
+  // block max through the pair reduction (second slot unused)
+  {
+    float v = mx;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
+    const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+    if (l == 0) red[w].x = v;
+    __syncthreads();
+    if (w == 0) {
+      float u = l < static_cast<int>(blockDim.x >> 5) ? red[l].x : -INFINITY;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) u = fmaxf(u, __shfl_xor_sync(0xffffffffu, u, o));
+      if (l == 0) red[32].x = u;
+    }
+    __syncthreads();
+    mx = red[32].x;
+    __syncthreads();
+  }
+  float se = 0.f;
+  for (int i = threadIdx.x; i < nv; i += blockDim.x) {
+    float a[8];
+    unpack8(r4[i], a);
+#pragma unroll
+    for (int e = 0; e < 8; ++e) se += __expf(a[e] - mx);
+  }
+  se = block_sum2(se, 0.f, red).x;
+  const float lse = mx + logf(se);
+  const int lab = labels[t];
+  const float zl = __bfloat162float(row[lab]);
+  __syncthreads();  // every thread has read row[lab] before any dLogits write
+  const float inv_se = 1.f / se;
+  uint4* w4 = reinterpret_cast<uint4*>(row);
+  for (int i = threadIdx.x; i < nv; i += blockDim.x) {
+    float a[8];
+    unpack8(r4[i], a);
+#pragma unroll
+    for (int e = 0; e < 8; ++e) a[e] = (__expf(a[e] - mx) * inv_se - (8 * i + e == lab ? 1.f : 0.f)) * inv_T;
+    w4[i] = pack8(a);
+  }
+  if (threadIdx.x == 0) row_loss[t] = lse - zl;
+}
+
+__global__ void mean_kernel(const float* __restrict__ x, int n, float* __restrict__ out) {
+  ptx::grid_dep_wait();
+  __shared__ float2 red[33];
+  float acc = 0.f;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) acc += x[i];  // fixed per-thread order
+  const float s = block_sum2(acc, 0.f, red).x;
+  if (threadIdx.x == 0) *out = s / n;
+}
+
+__global__ void synth_tokens_kernel(int32_t* __restrict__ out, int64_t n, int32_t classes, uint2 key, uint32_t kk,
+                                    uint32_t jj) {
+  ptx::grid_dep_wait();
+  for (int64_t i = blockIdx.x * 256LL + threadIdx.x; i < n; i += static_cast<int64_t>(gridDim.x) * 256) {
+    const uint4 r = philox(make_uint4(static_cast<uint32_t>(i), static_cast<uint32_t>(i >> 32), jj, kk), key);
+    out[i] = static_cast<int32_t>((static_cast<uint64_t>(r.x) * static_cast<uint64_t>(classes)) >> 32);
   }
 }
 
@@ -555,10 +691,12 @@ WdRanges wd_ranges(int h, int f) {
 cudaError_t adamw_rollback(float* p, float* m, float* v, const float* g, bf16* w, int64_t n, int64_t per_layer, int h,
                            int f, float lr, float b1, float b2, float eps, float wd, float bc1, float bc2,
                            float grad_scale, const int32_t* global_bad, const int32_t* own_bad, int32_t* count,
-                           cudaStream_t s) {
+                           cudaStream_t s, TailDecay tail) {
   if (n % 4 || per_layer % 4) return cudaErrorInvalidValue;
+  WdRanges wr = wd_ranges(h, f);
+  wr.tail = tail;
   return launch_pdl(adamw_rollback_kernel, dim3(grid_for(n / 4)), dim3(256), 0, s, 1, p, m, v, g, w, n / 4, per_layer,
-                    wd_ranges(h, f), lr, b1, b2, eps, wd, 1.0f / bc1, 1.0f / bc2, grad_scale, global_bad, own_bad,
+                    wr, lr, b1, b2, eps, wd, 1.0f / bc1, 1.0f / bc2, grad_scale, global_bad, own_bad,
                     count);
 }
 
@@ -569,10 +707,11 @@ cudaError_t grad_check(const float* g, int64_t n, int32_t* bad, int32_t* nonfini
 
 cudaError_t adamw(float* p, float* m, float* v, const float* g, bf16* w, int64_t n, int64_t per_layer, int h, int f,
                   float lr, float b1, float b2, float eps, float wd, float bc1, float bc2, float grad_scale,
-                  int32_t* nonfinite, cudaStream_t s, const int32_t* skip) {
+                  int32_t* nonfinite, cudaStream_t s, const int32_t* skip, TailDecay tail) {
   if (n % 4 || per_layer % 4) return cudaErrorInvalidValue;
   const int64_t H = h, F = f;
   WdRanges wr;
+  wr.tail = tail;
   wr.a0 = 0;
   wr.a1 = 3 * H * H;
   wr.b0 = 3 * H * H + 3 * H;
@@ -593,6 +732,32 @@ cudaError_t f32_to_bf16(const float* src, bf16* dst, int64_t n, cudaStream_t s) 
 cudaError_t synth_normal(bf16* out, int64_t n, uint64_t seed, uint64_t k, uint64_t j, cudaStream_t s) {
   uint2 key = make_uint2(static_cast<uint32_t>(seed), static_cast<uint32_t>(seed >> 32));
   return launch_pdl(synth_normal_kernel, dim3(grid_for((n + 3) / 4)), dim3(256), 0, s, 1, out, n, key,
+                    static_cast<uint32_t>(k), static_cast<uint32_t>(j));
+}
+
+cudaError_t embed_fwd(const bf16* E, const bf16* P, const int32_t* tok, bf16* X, int T, int h, int seq, cudaStream_t s) {
+  if (h % 8) return cudaErrorInvalidValue;
+  return launch_pdl(embed_fwd_kernel, dim3((T + 7) / 8), dim3(256), 0, s, 1, E, P, tok, X, T, h, seq);
+}
+
+cudaError_t embed_bwd(const bf16* dX, const int32_t* tok, float* dE, float* dP, int T, int h, int seq, int accumulate,
+                      cudaStream_t s) {
+  return launch_pdl(embed_bwd_kernel, dim3(T + seq), dim3(256), 0, s, 1, dX, tok, dE, dP, T, h, seq, accumulate);
+}
+
+cudaError_t cross_entropy(bf16* logits, const int32_t* labels, float* row_loss, float* loss, int T, int V,
+                          cudaStream_t s) {
+  if (V % 8) return cudaErrorInvalidValue;
+  cudaError_t e = launch_pdl(ce_rows_kernel, dim3(T), dim3(512), 0, s, 1, logits, labels, row_loss, V,
+                             1.0f / static_cast<float>(T));
+  if (e != cudaSuccess) return e;
+  return launch_pdl(mean_kernel, dim3(1), dim3(1024), 0, s, 1, static_cast<const float*>(row_loss), T, loss);
+}
+
+cudaError_t synth_tokens(int32_t* out, int64_t n, int32_t n_classes, uint64_t seed, uint64_t k, uint64_t j,
+                         cudaStream_t s) {
+  uint2 key = make_uint2(static_cast<uint32_t>(seed), static_cast<uint32_t>(seed >> 32));
+  return launch_pdl(synth_tokens_kernel, dim3(grid_for(n)), dim3(256), 0, s, 1, out, n, n_classes, key,
                     static_cast<uint32_t>(k), static_cast<uint32_t>(j));
 }
 

@@ -37,17 +37,35 @@ cudaError_t mse_loss(const bf16* y, const bf16* r, bf16* dy, float* part, int np
 // AdamW over flat fp32 arrays (reading R11).  Weight decay applies
 // to the 2-D weights: layer-local offsets in [0, 3h^2), [3h^2+3h, 4h^2+3h),
 // [4h^2+8h, 4h^2+8h+fh), [4h^2+8h+fh+f, 4h^2+8h+2fh+f).
+// Parameters from `start` on (the model ends) are not layers: decayed iff in [a0, a1)
+// (E, P) or [b0, b1) (Wout).
+struct TailDecay {
+  int64_t start = INT64_MAX, a0 = 0, a1 = 0, b0 = 0, b1 = 0;
+};
 // skip (device, may be NULL): if *skip != 0 the step is not taken (validated mode).
 cudaError_t adamw(float* p, float* m, float* v, const float* g, bf16* w, int64_t n, int64_t per_layer, int h, int f,
                   float lr, float b1, float b2, float eps, float wd, float bc1, float bc2, float grad_scale,
-                  int32_t* nonfinite, cudaStream_t s, const int32_t* skip = nullptr);
+                  int32_t* nonfinite, cudaStream_t s, const int32_t* skip = nullptr, TailDecay tail = TailDecay());
 // Arithmetic reversal of one adamw step with the same gradient;
 // acts only if (global_bad == NULL || *global_bad) and (own_bad == NULL || !*own_bad);
 // count (may be NULL) is incremented when it acts.
 cudaError_t adamw_rollback(float* p, float* m, float* v, const float* g, bf16* w, int64_t n, int64_t per_layer, int h,
                            int f, float lr, float b1, float b2, float eps, float wd, float bc1, float bc2,
                            float grad_scale, const int32_t* global_bad, const int32_t* own_bad, int32_t* count,
-                           cudaStream_t s);
+                           cudaStream_t s, TailDecay tail = TailDecay());
+
+// ---- GPT model ends (reading R33)
+// X[t] = E[tok[t]] + P[t mod seq]   (bf16, [T, h])
+cudaError_t embed_fwd(const bf16* E, const bf16* P, const int32_t* tok, bf16* X, int T, int h, int seq, cudaStream_t s);
+// dE[v] (+)= sum_{t: tok_t = v} dX_t (one CTA per distinct token, t order), dP[p] (+)= sum_{t mod seq = p} dX_t
+cudaError_t embed_bwd(const bf16* dX, const int32_t* tok, float* dE, float* dP, int T, int h, int seq, int accumulate,
+                      cudaStream_t s);
+// in place: logits [T, V] bf16 -> dLogits = (softmax - onehot(label)) / T; row_loss[t] = lse_t - logit_t[label_t];
+// then *loss = mean_t row_loss (fixed order)
+cudaError_t cross_entropy(bf16* logits, const int32_t* labels, float* row_loss, float* loss, int T, int V,
+                          cudaStream_t s);
+cudaError_t synth_tokens(int32_t* out, int64_t n, int32_t n_classes, uint64_t seed, uint64_t k, uint64_t j,
+                         cudaStream_t s);
 // *bad |= any element of g not finite (and *nonfinite, if not NULL)
 cudaError_t grad_check(const float* g, int64_t n, int32_t* bad, int32_t* nonfinite, cudaStream_t s);
 

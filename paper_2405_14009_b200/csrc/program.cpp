@@ -63,9 +63,10 @@ slip_status build_program(const Cluster& cl, const Plan& plan, int H, int rank, 
         return SLIP_ESTATE;
       }
       const int slot = it->second;
-      if (me_i + 1 == N) act(SLIP_ACT_LOSS, o, -1, slot, 0);
-      else act(SLIP_ACT_RECV_DY, o, rank_of_worker(N, me_i + 1, exec_of(me_i + 1, o.mb, o.origin)), slot, 0);
       int acc = first_b[o.iter] ? 0 : 1;
+      // the LOSS head's B-side gradients (final LayerNorm) accumulate like B's
+      if (me_i + 1 == N) act(SLIP_ACT_LOSS, o, -1, slot, acc);
+      else act(SLIP_ACT_RECV_DY, o, rank_of_worker(N, me_i + 1, exec_of(me_i + 1, o.mb, o.origin)), slot, 0);
       first_b[o.iter] = 0;
       if (o.phase == SLIP_BC) {
         acc |= (first_w[o.iter] ? 0 : 2);

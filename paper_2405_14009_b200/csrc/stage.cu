@@ -45,7 +45,48 @@ slip_status check_model(const slip_model* m) {
   SLIP_CHECK(m->hidden <= 4096, SLIP_EUNSUPPORTED, "model: hidden > 4096");
   SLIP_CHECK(m->seq % 8 == 0 && m->seq <= 2048, SLIP_EUNSUPPORTED, "model: seq must be a multiple of 8 and <= 2048");
   SLIP_CHECK(m->ln_eps > 0.f, SLIP_EINVAL, "model: ln_eps must be > 0");
+  SLIP_CHECK(m->ends >= 0 && m->ends <= 3, SLIP_EINVAL, "model: ends must be 0..3");
+  SLIP_CHECK(m->ends == 0 || (m->vocab > 0 && m->vocab % 128 == 0), SLIP_EUNSUPPORTED,
+             "model: vocab must be a positive multiple of 128 (padded) when the stage hosts a model end");
   return SLIP_OK;
+}
+
+EndOffsets end_offsets(const Dims& d, int64_t base) {
+  EndOffsets e;
+  int64_t o = base;
+  const int64_t V = d.V, H = d.h, S = d.s;
+  if (d.ends & 1) {
+    e.E = o;
+    o += V * H;
+    e.P = o;
+    o += S * H;
+  }
+  if (d.ends & 2) {
+    e.gf = o;
+    o += H;
+    e.bf = o;
+    o += H;
+    e.Wout = o;
+    o += V * H;
+  }
+  e.total = o - base;
+  return e;
+}
+
+// AdamW decay of the model-end tensors: E and P (contiguous), Wout; not gf / bf
+TailDecay tail_decay(const slip_ctx* c) {
+  TailDecay t;
+  if (!c->dm.ends) return t;
+  t.start = c->po.per_layer * c->L;
+  if (c->eo.E >= 0) {
+    t.a0 = c->eo.E;
+    t.a1 = c->eo.P + static_cast<int64_t>(c->dm.s) * c->dm.h;
+  }
+  if (c->eo.Wout >= 0) {
+    t.b0 = c->eo.Wout;
+    t.b1 = c->eo.Wout + static_cast<int64_t>(c->dm.V) * c->dm.h;
+  }
+  return t;
 }
 
 Dims make_dims(const slip_model& m) {
@@ -58,6 +99,8 @@ Dims make_dims(const slip_model& m) {
   d.b = m.micro_batch;
   d.T = m.seq * m.micro_batch;
   d.z = m.heads * m.micro_batch;
+  d.ends = m.ends;
+  d.V = m.ends ? m.vocab : 0;
   d.eps = m.ln_eps;
   return d;
 }
@@ -107,7 +150,17 @@ void carve_slot(Carver& cv, const Dims& d, int L, SlotBufs* out) {
     ls.dx2 = cv.take<bf16>(Th);
     ls.dqkv = cv.take<bf16>(3 * Th);
   }
-  sb.wtab = cv.take<GroupEntry>(4 * static_cast<size_t>(L));
+  sb.end = EndStash{};
+  if (d.ends & 1) sb.end.tokens = cv.take<int32_t>(d.T);
+  if (d.ends & 2) {
+    sb.end.xf = cv.take<bf16>(Th);
+    sb.end.yf = cv.take<bf16>(Th);
+    sb.end.mean_f = cv.take<float>(d.T);
+    sb.end.rstd_f = cv.take<float>(d.T);
+    sb.end.dlogits = cv.take<bf16>(static_cast<size_t>(d.T) * d.V);
+    sb.end.row_loss = cv.take<float>(d.T);
+  }
+  sb.wtab = cv.take<GroupEntry>(4 * static_cast<size_t>(L) + 1);
   sb.wtab_tiles = 0;
   if (out) *out = sb;
 }
@@ -338,6 +391,7 @@ std::vector<GemmDesc> w_problems(slip_ctx* c, int slot) {
     add(ls.dx2, ls.o, D.h, D.h, G.wo);
     add(ls.dqkv, ls.y1, 3 * D.h, D.h, G.wqkv);
   }
+  if (D.ends & 2) add(sb.end.dlogits, sb.end.yf, D.V, D.h, c->grad + c->eo.Wout);  // dWout += dLogits^T Y
   return v;
 }
 
@@ -349,12 +403,18 @@ slip_status backward_weight_impl(slip_ctx* c, int slot, int accumulate, cudaStre
   proto.a.mn_major = proto.b.mn_major = true;
   proto.mode = EPI_F32_ACC;
   proto.accumulate = accumulate;
-  cudaError_t e = gemm_group_launch(sb.wtab, 4 * c->L, sb.wtab_tiles, proto, s);
+  const int n_probs = 4 * c->L + ((c->dm.ends & 2) ? 1 : 0);
+  cudaError_t e = gemm_group_launch(sb.wtab, n_probs, sb.wtab_tiles, proto, s);
   if (e != cudaSuccess) {
     set_error(std::string("W grouped launch: ") + cudaGetErrorString(e) + " " + gemm_last_message());
     return SLIP_ECUDA;
   }
   c->launches += 1;
+  if (c->dm.ends & 1)  // embedding scatter of the stage-input gradient B left in the slot
+    SLIP_TRY(kcheck(c,
+                    embed_bwd(sb.dx, sb.end.tokens, c->grad + c->eo.E, c->grad + c->eo.P, c->dm.T, c->dm.h, c->dm.s,
+                              accumulate, s),
+                    "embed_bwd"));
   return SLIP_OK;
 }
 
@@ -386,13 +446,16 @@ slip_status backward_input_impl(slip_ctx* c, int slot, const void* dy, void* dx,
     // dY1 = dQKV Wqkv
     SLIP_TRY(linear_dx(c, ls.dqkv, Wt.wqkv, 3 * D.h, D.h, c->ws.dy1, EPI_BF16, nullptr, s));
     // LN1 backward + residual: dX = dX2 + LN1'(dY1); db2 of the layer below = colsum(dX)
-    bf16* dxl = l > 0 ? sb.layer[l - 1].dout : static_cast<bf16*>(dx);
+    // with the embedding end the input gradient always lands in the slot (W's scatter reads it)
+    bf16* dxl = l > 0 ? sb.layer[l - 1].dout : ((D.ends & 1) ? sb.dx : static_cast<bf16*>(dx));
     float* dxsum = l > 0 ? layer_g(c, l - 1).b2 : nullptr;
     SLIP_TRY(kcheck(c,
                     ln_bwd(c->ws.dy1, ls.xin, ls.mean1, ls.rstd1, Wt.g1, ls.dx2, dxl, G.g1, G.b1n, dxl ? dxsum : nullptr,
                            accumulate, c->ws.part, c->ws.tickets, D.T, D.h, s),
                     "ln_bwd 1", dxl ? 2 : 1));
   }
+  if ((D.ends & 1) && dx && dx != sb.dx)
+    SLIP_CUDA(cudaMemcpyAsync(dx, sb.dx, Th * sizeof(bf16), cudaMemcpyDeviceToDevice, s));
   return SLIP_OK;
 }
 
@@ -403,7 +466,8 @@ extern "C" {
 slip_status slip_param_count(const slip_model* m, int32_t n_layers, int64_t* out) {
   SLIP_TRY(check_model(m));
   SLIP_CHECK(n_layers > 0 && out, SLIP_EINVAL, "param_count: bad arguments");
-  *out = param_offsets(m->hidden, m->ffn).per_layer * n_layers;
+  const int64_t layers = param_offsets(m->hidden, m->ffn).per_layer * n_layers;
+  *out = layers + end_offsets(make_dims(*m), layers).total;
   return SLIP_OK;
 }
 
@@ -437,7 +501,8 @@ slip_status slip_ctx_create(slip_ctx** out, const slip_model* m, int32_t n_layer
   c->L = n_layers;
   c->n_slots = n_slots;
   c->po = param_offsets(m->hidden, m->ffn);
-  c->n_params = c->po.per_layer * n_layers;
+  c->eo = end_offsets(c->dm, c->po.per_layer * n_layers);
+  c->n_params = c->po.per_layer * n_layers + c->eo.total;
   c->state.assign(n_slots, SLOT_FREE);
   *out = c;
   return SLIP_OK;
@@ -480,7 +545,7 @@ slip_status slip_stage_bind(slip_ctx* c, void* w_bf16, float* master, float* gra
   SLIP_CUDA(cudaMemset(c->ws.tickets, 0, kTickets * sizeof(unsigned)));
   SLIP_CUDA(cudaMemset(c->ws.nonfinite, 0, sizeof(int32_t)));
   // W problem tables (tensor maps of the 4L weight-gradient GEMMs) per slot
-  std::vector<GroupEntry> host(4 * static_cast<size_t>(c->L));
+  std::vector<GroupEntry> host(4 * static_cast<size_t>(c->L) + ((c->dm.ends & 2) ? 1 : 0));
   for (int i = 0; i < c->n_slots; ++i) {
     std::vector<GemmDesc> probs = w_problems(c, i);
     int tiles = 0;
@@ -511,7 +576,13 @@ slip_status slip_stage_forward(slip_ctx* c, int32_t slot, const void* x_in, void
   const Dims& D = c->dm;
   SlotBufs& sb = c->slots[slot];
   const size_t Th = static_cast<size_t>(D.T) * D.h;
-  if (x_in != sb.x) SLIP_CUDA(cudaMemcpyAsync(sb.x, x_in, Th * sizeof(bf16), cudaMemcpyDeviceToDevice, s));
+  if (D.ends & 1) {  // x_in = T token ids: X = E[tok] + P[t mod seq]
+    if (x_in != sb.end.tokens)
+      SLIP_CUDA(cudaMemcpyAsync(sb.end.tokens, x_in, D.T * sizeof(int32_t), cudaMemcpyDeviceToDevice, s));
+    SLIP_TRY(kcheck(c, embed_fwd(c->w + c->eo.E, c->w + c->eo.P, sb.end.tokens, sb.x, D.T, D.h, D.s, s), "embed_fwd"));
+  } else if (x_in != sb.x) {
+    SLIP_CUDA(cudaMemcpyAsync(sb.x, x_in, Th * sizeof(bf16), cudaMemcpyDeviceToDevice, s));
+  }
   for (int l = 0; l < c->L; ++l) {
     LayerStash& ls = sb.layer[l];
     LayerW Wt = layer_w(c, l);
@@ -559,7 +630,8 @@ slip_status slip_optimizer_step(slip_ctx* c, const slip_adam* a, int64_t step, f
   return kcheck(c,
                 adamw(c->master, c->adam_m, c->adam_v, c->grad, c->w, c->n_params, c->po.per_layer, c->dm.h, c->dm.f,
                       a->lr, a->beta1, a->beta2, a->eps, a->weight_decay, static_cast<float>(bc1),
-                      static_cast<float>(bc2), grad_scale, d_nonfinite, reinterpret_cast<cudaStream_t>(st)),
+                      static_cast<float>(bc2), grad_scale, d_nonfinite, reinterpret_cast<cudaStream_t>(st), nullptr,
+                      tail_decay(c)),
                 "adamw");
 }
 
@@ -570,6 +642,36 @@ slip_status slip_loss_mse(slip_ctx* c, const void* y, const void* target, void* 
                 mse_loss(static_cast<const bf16*>(y), static_cast<const bf16*>(target), static_cast<bf16*>(dy),
                          c->ws.loss_part, 256, d_loss, n, reinterpret_cast<cudaStream_t>(st)),
                 "mse_loss", 2);
+}
+
+slip_status slip_loss_ce(slip_ctx* c, int32_t slot, const void* y, const int32_t* labels, void* dy, float* d_loss,
+                         int32_t accumulate, slip_stream st) {
+  SLIP_TRY(slot_check(c, slot, SLOT_F_DONE));
+  SLIP_CHECK(c->dm.ends & 2, SLIP_EINVAL, "loss_ce: the stage hosts no LM head (model.ends bit 1)");
+  SLIP_CHECK(y && labels && dy && d_loss, SLIP_EINVAL, "loss_ce: NULL argument");
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(st);
+  const Dims& D = c->dm;
+  EndStash& e = c->slots[slot].end;
+  const size_t Th = static_cast<size_t>(D.T) * D.h;
+  const bf16* gf = c->w + c->eo.gf;
+  const bf16* bfp = c->w + c->eo.bf;
+  const bf16* Wout = c->w + c->eo.Wout;
+  if (y != e.xf) SLIP_CUDA(cudaMemcpyAsync(e.xf, y, Th * sizeof(bf16), cudaMemcpyDeviceToDevice, s));
+  SLIP_TRY(kcheck(c, ln_fwd(e.xf, gf, bfp, e.yf, e.mean_f, e.rstd_f, D.T, D.h, D.eps, s), "ln_fwd f"));
+  SLIP_TRY(linear_fwd(c, e.yf, Wout, D.V, D.h, e.dlogits, nullptr, nullptr, EPI_BF16, nullptr, s));  // logits
+  SLIP_TRY(kcheck(c, cross_entropy(e.dlogits, labels, e.row_loss, d_loss, D.T, D.V, s), "cross_entropy", 2));
+  SLIP_TRY(linear_dx(c, e.dlogits, Wout, D.V, D.h, c->ws.dy2, EPI_BF16, nullptr, s));  // dY = dLogits Wout
+  return kcheck(c,
+                ln_bwd(c->ws.dy2, e.xf, e.mean_f, e.rstd_f, gf, nullptr, static_cast<bf16*>(dy), c->grad + c->eo.gf,
+                       c->grad + c->eo.bf, nullptr, accumulate, c->ws.part, c->ws.tickets, D.T, D.h, s),
+                "ln_bwd f", 2);
+}
+
+slip_status slip_synth_tokens(int32_t* out, int64_t n, int32_t n_classes, uint64_t seed, uint64_t k, uint64_t j,
+                              slip_stream st) {
+  SLIP_CHECK(out && n > 0 && n_classes > 0, SLIP_EINVAL, "synth_tokens: bad arguments");
+  SLIP_CUDA(synth_tokens(out, n, n_classes, seed, k, j, reinterpret_cast<cudaStream_t>(st)));
+  return SLIP_OK;
 }
 
 slip_status slip_synth_normal(void* out_bf16, int64_t n, uint64_t seed, uint64_t k, uint64_t j, slip_stream st) {
@@ -592,7 +694,7 @@ slip_status validated_step(slip_ctx* c, const slip_adam* a, int64_t step, float 
   return kcheck(c,
                 adamw(c->master, c->adam_m, c->adam_v, c->grad, c->w, c->n_params, c->po.per_layer, c->dm.h, c->dm.f,
                       a->lr, a->beta1, a->beta2, a->eps, a->weight_decay, static_cast<float>(bc1),
-                      static_cast<float>(bc2), grad_scale, c->ws.nonfinite, s, own),
+                      static_cast<float>(bc2), grad_scale, c->ws.nonfinite, s, own, tail_decay(c)),
                 "adamw");
 }
 // Conditional reversal of the step taken with (step, grad_scale): acts iff *glob && !*own.
@@ -603,7 +705,7 @@ slip_status rollback_if(slip_ctx* c, const slip_adam* a, int64_t step, float gra
   return kcheck(c,
                 adamw_rollback(c->master, c->adam_m, c->adam_v, c->grad, c->w, c->n_params, c->po.per_layer, c->dm.h,
                                c->dm.f, a->lr, a->beta1, a->beta2, a->eps, a->weight_decay, static_cast<float>(bc1),
-                               static_cast<float>(bc2), grad_scale, glob, own, count, s),
+                               static_cast<float>(bc2), grad_scale, glob, own, count, s, tail_decay(c)),
                 "adamw_rollback");
 }
 }  // namespace slip
@@ -631,7 +733,7 @@ slip_status slip_optimizer_rollback(slip_ctx* c, const slip_adam* a, int64_t ste
                 adamw_rollback(c->master, c->adam_m, c->adam_v, c->grad, c->w, c->n_params, c->po.per_layer, c->dm.h,
                                c->dm.f, a->lr, a->beta1, a->beta2, a->eps, a->weight_decay, static_cast<float>(bc1),
                                static_cast<float>(bc2), grad_scale, nullptr, nullptr, nullptr,
-                               reinterpret_cast<cudaStream_t>(st)),
+                               reinterpret_cast<cudaStream_t>(st), tail_decay(c)),
                 "adamw_rollback");
 }
 

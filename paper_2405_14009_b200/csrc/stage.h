@@ -29,12 +29,21 @@ struct LayerStash {
 
 struct GroupEntry;
 
+struct EndStash {                // GPT ends of a slot (reading R33); null when absent
+  int32_t* tokens;               // [T] token ids (embedding end)
+  bf16 *xf, *yf;                 // [T, h] last-layer output, final-LN output (LM-head end)
+  float *mean_f, *rstd_f;        // [T]
+  bf16* dlogits;                 // [T, V] logits, then dLogits in place (W-stash of dWout)
+  float* row_loss;               // [T]
+};
+
 struct SlotBufs {
   bf16* x;   // stage input   [T, h]
   bf16* dy;  // stage output gradient [T, h]
   bf16* dx;  // stage input gradient produced by B (executor send buffer) [T, h]
   std::vector<LayerStash> layer;
-  GroupEntry* wtab;  // device table of the slot's 4L W problems (grouped launch)
+  EndStash end;
+  GroupEntry* wtab;  // device table of the slot's W problems (4L, + dWout with the LM head)
   int wtab_tiles;
 };
 
@@ -54,6 +63,12 @@ enum SlotState : int { SLOT_FREE = 0, SLOT_F_DONE = 1, SLOT_B_DONE = 2 };
 struct Dims {
   int h, a, d, f, s, b, T, z;
   float eps;
+  int V, ends;  // padded vocabulary, ends bits (0 when the stage hosts no model end)
+};
+
+// Element offsets of the model-end tensors after the L layers (-1 when absent).
+struct EndOffsets {
+  int64_t E = -1, P = -1, gf = -1, bf = -1, Wout = -1, total = 0;
 };
 
 }  // namespace slip
@@ -64,6 +79,7 @@ struct slip_ctx {
   int L = 0;
   int n_slots = 0;
   slip::ParamOffsets po;
+  slip::EndOffsets eo;
   int64_t n_params = 0;
   slip::bf16* w = nullptr;
   float *master = nullptr, *grad = nullptr, *adam_m = nullptr, *adam_v = nullptr;
@@ -87,6 +103,7 @@ namespace slip {
 slip_status check_model(const slip_model* m);
 Dims make_dims(const slip_model& m);
 size_t stash_bytes_per_slot(const Dims& d, int L);
+EndOffsets end_offsets(const Dims& d, int64_t base);
 size_t workspace_bytes(const Dims& d);
 slip_status validated_step(slip_ctx* c, const slip_adam* a, int64_t step, float grad_scale, int32_t* own, int fault,
                            cudaStream_t s);

@@ -21,7 +21,8 @@ def _stream(stream=None) -> C.c_void_p:
 
 
 def make_model(cfg) -> slip_model:
-    return slip_model(cfg.hidden, cfg.heads, cfg.ffn, cfg.seq, cfg.micro_batch, cfg.ln_eps)
+    return slip_model(cfg.hidden, cfg.heads, cfg.ffn, cfg.seq, cfg.micro_batch, cfg.ln_eps,
+                      getattr(cfg, "vocab", 0), getattr(cfg, "ends", 0))
 
 
 def make_cluster(N: int, DP: int, m: int, live=None):
@@ -65,6 +66,16 @@ def init_master_(master, cfg, n_layers, total_layers, seed=0):
         for n in ("g1", "g2"):
             off, sz = po[n]
             master[base + off: base + off + sz].fill_(1.0)
+    # GPT ends after the layers (reading R33): E, P, Wout ~ N(0, 0.02^2), gf = 1, bf = 0
+    off = n_layers * P
+    ends, V, h = getattr(cfg, "ends", 0), getattr(cfg, "vocab", 0), cfg.hidden
+    if ends & 1:
+        master[off: off + (V + cfg.seq) * h].normal_(0.0, 0.02, generator=g)
+        off += (V + cfg.seq) * h
+    if ends & 2:
+        master[off: off + h].fill_(1.0)
+        off += 2 * h
+        master[off: off + V * h].normal_(0.0, 0.02, generator=g)
 
 
 def make_costs(t_f=1, t_b=1, t_w=1, t_comm=0, t_ar=0, t_opt=0, a_f=0, a_w=0, m_limit=0) -> slip_costs:
@@ -267,6 +278,10 @@ class Stage:
         a = slip_adam(lr, beta1, beta2, eps, weight_decay)
         call("slip_optimizer_step", self.ctx, C.byref(a), int(step), float(grad_scale),
              _ptr(nonfinite) if nonfinite is not None else None, _stream(stream))
+
+    def loss_ce(self, slot, y, labels, dy, d_loss, accumulate=0, stream=None):
+        call("slip_loss_ce", self.ctx, slot, _ptr(y), _ptr(labels), _ptr(dy), _ptr(d_loss), int(accumulate),
+             _stream(stream))
 
     def loss_mse(self, y, target, dy, d_loss, stream=None):
         call("slip_loss_mse", self.ctx, _ptr(y), _ptr(target), _ptr(dy), _ptr(d_loss), _stream(stream))

@@ -35,6 +35,8 @@ class ModelCfg:
     micro_batch: int
     layers: int
     ln_eps: float = 1e-5
+    vocab: int = 0  # padded vocabulary of the GPT ends (reading R33); 0 = no ends
+    ends: int = 0   # bit 0: this stage hosts the embedding, bit 1: the LM head
 
     @property
     def head_dim(self) -> int:
@@ -154,3 +156,58 @@ def unpack_stage(flat: np.ndarray, cfg: ModelCfg, n_layers: int) -> list:
     P = cfg.params_per_layer
     return [unpack_layer(flat[l * P:(l + 1) * P], cfg) for l in range(n_layers)]
 
+
+
+# ---------------------------------------------------------------- GPT ends (R33)
+END_ORDER = ("E", "P", "gf", "bf", "Wout")
+
+
+def end_shapes(cfg: ModelCfg) -> dict:
+    out = {}
+    if cfg.ends & 1:
+        out["E"] = (cfg.vocab, cfg.hidden)
+        out["P"] = (cfg.seq, cfg.hidden)
+    if cfg.ends & 2:
+        out["gf"] = (cfg.hidden,)
+        out["bf"] = (cfg.hidden,)
+        out["Wout"] = (cfg.vocab, cfg.hidden)
+    return out
+
+
+def end_params(cfg: ModelCfg, stage: int) -> dict:
+    """fp64 arrays of bf16 values: E, P, Wout ~ N(0, 0.02^2), gf = 1 + N(0, 0.1^2), bf ~ N(0, 0.1^2)."""
+    g = rng(4, stage)
+    out = {}
+    for n, shp in end_shapes(cfg).items():
+        if n in ("E", "P", "Wout"):
+            v = g.normal(0.0, 0.02, shp)
+        elif n == "gf":
+            v = 1.0 + g.normal(0.0, 0.1, shp)
+        else:
+            v = g.normal(0.0, 0.1, shp)
+        out[n] = bf16_round(v)
+    return out
+
+
+def pack_ends(params: dict) -> np.ndarray:
+    return np.concatenate([np.asarray(params[n], dtype=np.float64).reshape(-1) for n in END_ORDER if n in params]
+                          or [np.zeros(0)])
+
+
+def unpack_ends(flat: np.ndarray, cfg: ModelCfg) -> dict:
+    out, off = {}, 0
+    for n, shp in end_shapes(cfg).items():
+        sz = int(np.prod(shp))
+        out[n] = np.asarray(flat[off:off + sz]).reshape(shp)
+        off += sz
+    return out
+
+
+def stage_tokens(cfg: ModelCfg, k: int, j: int, classes: int | None = None) -> np.ndarray:
+    """Token ids of micro-batch (k, j): T int32 uniform over the (padded) vocabulary."""
+    return rng(5, k, j).integers(0, classes or cfg.vocab, cfg.tokens).astype(np.int32)
+
+
+def stage_labels(cfg: ModelCfg, k: int, j: int, classes: int | None = None) -> np.ndarray:
+    """Labels of micro-batch (k, j): T int32 uniform over the (padded) vocabulary."""
+    return rng(6, k, j).integers(0, classes or cfg.vocab, cfg.tokens).astype(np.int32)

@@ -225,3 +225,71 @@ def test_one_layer_c2_full_size():
     g = sd.unpack_stage(st.grad.cpu().numpy().astype(np.float64), cfg, 1)
     for n in sd.PARAM_ORDER:
         assert relerr(g[0][n], grads[0][n]) <= GATE_A, n
+
+
+ENDS_CFGS = {
+    "tiny_both": (sd.ModelCfg(hidden=64, heads=2, ffn=256, seq=32, micro_batch=2, layers=1, vocab=256, ends=3), 1),
+    "d128_both": (sd.ModelCfg(hidden=256, heads=2, ffn=1024, seq=128, micro_batch=2, layers=2, vocab=384, ends=3), 2),
+    "emb_only": (sd.ModelCfg(hidden=128, heads=2, ffn=512, seq=64, micro_batch=1, layers=1, vocab=256, ends=1), 1),
+    "head_only": (sd.ModelCfg(hidden=128, heads=2, ffn=512, seq=64, micro_batch=1, layers=1, vocab=256, ends=2), 1),
+}
+
+
+@pytest.mark.parametrize("name", list(ENDS_CFGS))
+def test_stage_with_gpt_ends_matches_oracle(name):
+    """GPT ends (reading R33): embedding (tokens in), layers,
+    final LayerNorm + LM head + cross-entropy (labels in), B, W (with dWout in the
+    grouped launch and the embedding scatter) against oracle/ends.py + oracle/layer.py."""
+    from oracle import ends as OE
+    rt = _rt()
+    cfg, L = ENDS_CFGS[name]
+    layers = sd.stage_params(cfg, 0, L, total_layers=max(L, 2))
+    ends = sd.end_params(cfg, 0)
+    flat = np.concatenate([sd.pack_stage(layers), sd.pack_ends(ends)])
+    st = rt.Stage(cfg, L, n_slots=1)
+    assert st.n_params == flat.size
+    st.load_master(torch.from_numpy(flat).float().cuda())
+    T, h = cfg.tokens, cfg.hidden
+    tok = sd.stage_tokens(cfg, 0, 0)
+    tok[5] = tok[9] = tok[17]  # repeated tokens in the scatter
+    lab = sd.stage_labels(cfg, 0, 0)
+    x_in = torch.from_numpy(tok).cuda() if cfg.ends & 1 else to_dev_bf16(sd.stage_input(cfg, 0, 0))
+    y = torch.empty(T, h, dtype=torch.bfloat16, device="cuda")
+    dy = torch.empty_like(y)
+    dx = torch.empty_like(y)
+    loss = torch.zeros(1, device="cuda")
+    st.forward(0, x_in, y)
+    if cfg.ends & 2:
+        st.loss_ce(0, y, torch.from_numpy(lab).cuda(), dy, loss)
+    else:
+        dy.copy_(to_dev_bf16(sd.stage_target(cfg, 0, 0)))
+    st.backward_input(0, dy, dx, accumulate=False)
+    st.backward_weight(0, accumulate=False)
+    torch.cuda.synchronize()
+    # oracle
+    x0 = OE.embed_fwd(ends["E"], ends["P"], tok, cfg.seq) if cfg.ends & 1 else sd.stage_input(cfg, 0, 0)
+    out, caches = OL.stage_forward(layers, x0, cfg)
+    assert relerr(to_np(y), out) <= GATE_A
+    if cfg.ends & 2:
+        lref, hc = OE.head_forward(out, ends["gf"], ends["bf"], ends["Wout"], lab, cfg.ln_eps)
+        assert abs(loss.item() - lref) <= 1e-2 * abs(lref)
+        dout, hb, hws = OE.head_backward_input(hc)
+        assert relerr(to_np(dy), dout) <= GATE_A
+    else:
+        dout = sd.stage_target(cfg, 0, 0)
+    dxr, grads = OL.stage_backward_coupled(layers, caches, dout, cfg)
+    assert relerr(to_np(dx), dxr) <= GATE_A
+    gflat = st.grad.cpu().numpy().astype(np.float64)
+    P = cfg.params_per_layer
+    g = sd.unpack_stage(gflat[:L * P], cfg, L)
+    for l in range(L):
+        for n in sd.PARAM_ORDER:
+            assert relerr(g[l][n], grads[l][n]) <= GATE_A, (l, n)
+    ge = sd.unpack_ends(gflat[L * P:], cfg)
+    if cfg.ends & 1:
+        dE, dP = OE.embed_bwd(dxr, tok, cfg.seq, cfg.vocab)
+        assert relerr(ge["E"], dE) <= GATE_A and relerr(ge["P"], dP) <= GATE_A
+        assert np.all(ge["E"][np.setdiff1d(np.arange(cfg.vocab), tok)] == 0.0)  # untouched rows stay 0
+    if cfg.ends & 2:
+        assert relerr(ge["gf"], hb["gf"]) <= GATE_A and relerr(ge["bf"], hb["bf"]) <= GATE_A
+        assert relerr(ge["Wout"], OE.head_backward_weight(hws)["Wout"]) <= GATE_A
