@@ -39,6 +39,7 @@ H, HEADS, FFN, SEQ, MB, LAYERS = 2048, 16, 8192, 2048, 1, 24
 # GPT shapes of SURVEY.md §8(a) (reading R2); the default is BASELINE.json configs[1]
 MODELS = {"1.3b": (2048, 16, 8192, 24), "2.7b": (2560, 32, 10240, 32), "6.7b": (4096, 32, 16384, 32)}
 MODEL = "1.3b"
+VOCAB = 50304  # GPT-2/3 BPE vocabulary 50257 padded to a multiple of 128 (reading R33)
 
 
 def parse():
@@ -60,6 +61,9 @@ def parse():
                     help="SMs kept free of persistent GEMM CTAs for NCCL kernels (default: 0 at N=1, 8 at N>1)")
     ap.add_argument("--p2p-ctas", type=int, default=2, help="CTAs per NCCL P2P kernel (0: NCCL default)")
     ap.add_argument("--trace", default="", help="directory: dump one traced 2-iteration run per rank (JSON)")
+    ap.add_argument("--gpt-ends", action="store_true",
+                    help="GPT model ends: token + position embedding on the first stage, final LN + LM head "
+                         "(vocab 50304) + cross-entropy on the last stage (SURVEY §8(f) NEXT-3)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--model", default="1.3b", choices=sorted(MODELS), help="GPT shape (default: BASELINE configs[1])")
@@ -213,7 +217,12 @@ def main():
     assert DP * PP == world and args.layers % PP == 0
     L = args.layers // PP
     m = args.m or 4 * PP
-    cfg = sd.ModelCfg(hidden=H, heads=HEADS, ffn=FFN, seq=SEQ, micro_batch=MB, layers=args.layers)
+    me_stage = rank % PP
+    ends = 0
+    if args.gpt_ends:
+        ends = (1 if me_stage == 0 else 0) | (2 if me_stage == PP - 1 else 0)
+    cfg = sd.ModelCfg(hidden=H, heads=HEADS, ffn=FFN, seq=SEQ, micro_batch=MB, layers=args.layers,
+                      vocab=VOCAB if args.gpt_ends else 0, ends=ends)
     T = cfg.tokens
     # failures at normalized positions: last stages, distinct peer groups (R20),
     # or the actual (un-normalized) set given by --failed-at
@@ -361,7 +370,7 @@ def main():
     # slot in one persistent tcgen05 launch, fp32 accumulation fused in the epilogue).
     # achieved = algorithmic FLOP per launch (24 T h^2 L for ffn = 4h) x launches / their
     # CUDA-event time on the compute stream inside the timed region.
-    flops_w_op = 2.0 * T * (4 * H * H + 2 * FFN * H) * L
+    flops_w_op = 2.0 * T * (4 * H * H + 2 * FFN * H) * L + (2.0 * T * VOCAB * H if ends & 2 else 0.0)
     ach_local = flops_w_op * rep.phase_ops[2] / (rep.phase_ms[2] / 1e3) / 1e12 if rep.phase_ops[2] else 0.0
     # masked ranks run nothing: take the per-phase numbers of the busiest live rank
     stats = torch.tensor([ach_local, float(rep.w_gemm_launches), rep.phase_ms[2]] + list(rep.phase_ms[:5]),
@@ -419,11 +428,15 @@ def main():
     # reads the losses back D2H (one executor call per step)
     e2e = None
     if not args.no_e2e:
-        xs = [torch.empty(T, H, dtype=torch.bfloat16).pin_memory() for _ in range(DP * m)]
-        rs = [torch.empty(T, H, dtype=torch.bfloat16).pin_memory() for _ in range(DP * m)]
         g = torch.Generator().manual_seed(7)
-        for a in xs + rs:
-            a.copy_(torch.randn(T, H, generator=g).to(torch.bfloat16))
+        if ends & 1:  # token ids in
+            xs = [torch.randint(0, VOCAB, (T,), generator=g, dtype=torch.int32).pin_memory() for _ in range(DP * m)]
+        else:
+            xs = [torch.randn(T, H, generator=g).to(torch.bfloat16).pin_memory() for _ in range(DP * m)]
+        if ends & 2:  # labels in
+            rs = [torch.randint(0, VOCAB, (T,), generator=g, dtype=torch.int32).pin_memory() for _ in range(DP * m)]
+        else:
+            rs = [torch.randn(T, H, generator=g).to(torch.bfloat16).pin_memory() for _ in range(DP * m)]
         loss_host = torch.zeros(DP * m, dtype=torch.float32).pin_memory()
         io = rt.make_io(xs, rs, loss_host)
         execute(1, io)
@@ -436,7 +449,8 @@ def main():
         barrier()
         e2e_ms = allreduce_max(f0.elapsed_time(f1))
         # bytes per step over the whole job: X for every stage-0 F, targets for every last-stage B
-        h2d = 2 * DP * m * T * H * 2
+        in_b = T * 4 if args.gpt_ends else T * H * 2  # token ids / labels, or [T, h] bf16
+        h2d = 2 * DP * m * in_b
         e2e = {"value": tokens_per_step * args.steps / (e2e_ms / 1000.0), "unit": "tokens/s",
                "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": 4 * DP * m,
                "last_loss": float(r.last_loss) if (rank % PP) == PP - 1 else None}
@@ -457,7 +471,8 @@ def main():
                                "%d layers, DP%dxPP%d, "
                                "m=%d micro-batches/pipeline, %s, failures=%d" % (
                                    args.layers, DP, PP, m,
-                                   plan_name,
+                                   plan_name + (", GPT ends (embedding + LM head V=50304 + CE)"
+                                                if args.gpt_ends else ", MSE head on a synthetic stage-0 input"),
                                    len(failed)),
                    "model": "gpt-%s-shape" % MODEL, "global_batch": DP * m * MB, "seq_len": SEQ,
                    "parallelism": "dp%dxpp%d" % (DP, PP), "failed_workers": failed, "sm_reserve": sm_reserve,

@@ -491,27 +491,42 @@ __global__ void __launch_bounds__(256) embed_fwd_kernel(const bf16* __restrict__
 }
 
 // Embedding scatter, deterministic without atomics: block t owns token tok[t] iff t is
-// its first occurrence, and sums the rows of every occurrence in t order.  Blocks
-// T .. T+seq-1 own the position rows (sum over the micro-batch's sequences in order).
+// its first occurrence; warp 0 lists the occurrences in t order (ballots over 32-token
+// chunks) and the block sums their rows in that order.  Blocks T .. T+seq-1 own the
+// position rows (sum over the micro-batch's sequences in order).
 __global__ void __launch_bounds__(256) embed_bwd_kernel(const bf16* __restrict__ dX, const int32_t* __restrict__ tok,
                                                         float* __restrict__ dE, float* __restrict__ dP, int T, int h,
                                                         int seq, int accumulate) {
   ptx::grid_dep_wait();
-  __shared__ int first;
+  extern __shared__ int occ[];  // [T] occurrence list
+  __shared__ int n_occ;
   const int b = blockIdx.x;
   if (b < T) {
     const int v = tok[b];
-    if (threadIdx.x == 0) first = 1;
+    if (threadIdx.x < 32) {
+      const int lane = threadIdx.x;
+      bool earlier = false;
+      int n = 0;
+      for (int u0 = 0; u0 < T; u0 += 32) {
+        const int u = u0 + lane;
+        const bool hit = u < T && tok[u] == v;
+        const unsigned m = __ballot_sync(0xffffffffu, hit);
+        if (u0 < b) {  // hits at positions u < b mean an earlier occurrence of v
+          const unsigned below = b - u0 >= 32 ? 0xffffffffu : ((1u << (b - u0)) - 1u);
+          earlier = earlier || (m & below) != 0u;
+        }
+        if (hit) occ[n + __popc(m & ((1u << lane) - 1u))] = u;
+        n += __popc(m);
+      }
+      if (lane == 0) n_occ = earlier ? 0 : n;  // not the first occurrence: another block owns v
+    }
     __syncthreads();
-    for (int u = threadIdx.x; u < b; u += blockDim.x)
-      if (tok[u] == v) first = 0;
-    __syncthreads();
-    if (!first) return;
+    const int n = n_occ;
+    if (n == 0) return;
     float* out = dE + static_cast<int64_t>(v) * h;
     for (int c = threadIdx.x; c < h; c += blockDim.x) {
       float acc = 0.f;
-      for (int u = b; u < T; ++u)
-        if (tok[u] == v) acc += __bfloat162float(dX[static_cast<int64_t>(u) * h + c]);
+      for (int q = 0; q < n; ++q) acc += __bfloat162float(dX[static_cast<int64_t>(occ[q]) * h + c]);
       out[c] = accumulate ? out[c] + acc : acc;
     }
   } else {
@@ -742,7 +757,9 @@ cudaError_t embed_fwd(const bf16* E, const bf16* P, const int32_t* tok, bf16* X,
 
 cudaError_t embed_bwd(const bf16* dX, const int32_t* tok, float* dE, float* dP, int T, int h, int seq, int accumulate,
                       cudaStream_t s) {
-  return launch_pdl(embed_bwd_kernel, dim3(T + seq), dim3(256), 0, s, 1, dX, tok, dE, dP, T, h, seq, accumulate);
+  if (T > 12288) return cudaErrorInvalidValue;  // occurrence list in shared memory
+  return launch_pdl(embed_bwd_kernel, dim3(T + seq), dim3(256), static_cast<size_t>(T) * sizeof(int), s, 1, dX, tok,
+                    dE, dP, T, h, seq, accumulate);
 }
 
 cudaError_t cross_entropy(bf16* logits, const int32_t* labels, float* row_loss, float* loss, int T, int V,
