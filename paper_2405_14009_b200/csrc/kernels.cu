@@ -189,12 +189,14 @@ __global__ void __launch_bounds__(256) ln_bwd_rows_kernel(const bf16* __restrict
 }
 
 // ------------------------------------------------------------------ column reductions
-// grid (ceil(N/256), kRedChunks), block 256 = 32 column-vectors x 8 row groups.
+// One block per 64-column strip covering ALL T rows: 256 threads = 8 column vectors
+// (16 bytes each) x 32 row groups; thread (cv, rg) sums rows rg, rg+32, ... of its 8
+// columns, then the 32 row-group partials of each column are added in a fixed order —
+// deterministic, no partial buffers, no tickets, one launch.
 // MODE 0: out0 (+)= sum_t a.
 // MODE 1 (LayerNorm): out0 (+)= sum dy*xhat, out1 (+)= sum dy       (a = dy)
 // MODE 2 (LayerNorm + producer bias): MODE 1 and out2 (+)= sum_t dx (dx = the LN input grad)
-// Each block writes its chunk's partials; the last block of a column strip (atomic
-// ticket) sums the kRedChunks partials in chunk order and resets the ticket.
+constexpr int CR_COLS = 64;
 template <int MODE>
 __global__ void __launch_bounds__(256) colred_kernel(const bf16* __restrict__ a, int64_t ld, const bf16* __restrict__ x,
                                                      const float* __restrict__ mean, const float* __restrict__ rstd,
@@ -203,16 +205,15 @@ __global__ void __launch_bounds__(256) colred_kernel(const bf16* __restrict__ a,
                                                      float* __restrict__ out2, int accumulate,
                                                      unsigned* __restrict__ tickets) {
   constexpr int NO = MODE == 0 ? 1 : (MODE == 1 ? 2 : 3);  // outputs
-  __shared__ float red[NO][8][257];
-  __shared__ bool last;
+  __shared__ float red[NO][32][CR_COLS + 1];
+  (void)tickets;
   ptx::grid_dep_wait();
-  const int cv = threadIdx.x & 31;
-  const int rg = threadIdx.x >> 5;
-  const int col = (blockIdx.x * 32 + cv) * 8;
-  const int chunk = blockIdx.y;
-  const int rows_per = (T + kRedChunks - 1) / kRedChunks;
-  const int r0 = chunk * rows_per;
-  const int r1 = min(T, r0 + rows_per);
+  const int cv = threadIdx.x & 7;
+  const int rg = threadIdx.x >> 3;
+  const int col = blockIdx.x * CR_COLS + cv * 8;
+  // row chunk of this block (gridDim.y chunks; one chunk writes the outputs directly)
+  const int R = gridDim.y, rows_per = (T + R - 1) / R;
+  const int r0 = blockIdx.y * rows_per, r1 = min(T, r0 + rows_per);
   float acc[NO][8];
 #pragma unroll
   for (int o = 0; o < NO; ++o)
@@ -220,7 +221,7 @@ __global__ void __launch_bounds__(256) colred_kernel(const bf16* __restrict__ a,
     for (int e = 0; e < 8; ++e) acc[o][e] = 0.f;
   if (col < N) {
 #pragma unroll 4
-    for (int r = r0 + rg; r < r1; r += 8) {
+    for (int r = r0 + rg; r < r1; r += 32) {
       float v[8];
       unpack8(*reinterpret_cast<const uint4*>(a + static_cast<size_t>(r) * ld + col), v);
       if (MODE == 0) {
@@ -249,35 +250,44 @@ __global__ void __launch_bounds__(256) colred_kernel(const bf16* __restrict__ a,
 #pragma unroll
     for (int e = 0; e < 8; ++e) red[o][rg][cv * 8 + e] = acc[o][e];
   __syncthreads();
-  const int c = threadIdx.x;  // 256 columns of this strip
-  const int gcol = blockIdx.x * 256 + c;
-  const size_t plane = static_cast<size_t>(kRedChunks) * N;
-  if (gcol < N) {
+  if (threadIdx.x < CR_COLS * NO) {
+    const int o = threadIdx.x / CR_COLS, c = threadIdx.x % CR_COLS;
+    const int gcol = blockIdx.x * CR_COLS + c;
+    if (gcol < N) {
+      float s4[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
-    for (int o = 0; o < NO; ++o) {
-      float s = 0.f;
-#pragma unroll
-      for (int g = 0; g < 8; ++g) s += red[o][g][c];
-      part[o * plane + static_cast<size_t>(chunk) * N + gcol] = s;
+      for (int g = 0; g < 32; ++g) s4[g & 3] += red[o][g][c];
+      const float s = (s4[0] + s4[1]) + (s4[2] + s4[3]);
+      if (R == 1) {
+        float* out = o == 0 ? out0 : (o == 1 ? out1 : out2);
+        out[gcol] = accumulate ? out[gcol] + s : s;
+      } else {
+        part[(static_cast<size_t>(o) * R + blockIdx.y) * N + gcol] = s;
+      }
     }
   }
-  __threadfence();
-  __syncthreads();
-  if (threadIdx.x == 0) last = atomicAdd(&tickets[blockIdx.x], 1u) == static_cast<unsigned>(kRedChunks - 1);
-  __syncthreads();
-  if (!last) return;
-  __threadfence();
-  if (gcol < N) {
-    float* outs[3] = {out0, out1, out2};
-#pragma unroll
-    for (int o = 0; o < NO; ++o) {
-      float s = 0.f;
-      for (int k = 0; k < kRedChunks; ++k) s += __ldcg(part + o * plane + static_cast<size_t>(k) * N + gcol);
-      float* out = outs[o];
-      out[gcol] = accumulate ? out[gcol] + s : s;
-    }
-  }
-  if (threadIdx.x == 0) tickets[blockIdx.x] = 0u;
+}
+
+// Sum of the R row-chunk partials of each column in chunk order (deterministic).
+__global__ void __launch_bounds__(256) colred_finalize_kernel(const float* __restrict__ part, int R, int N, int NO,
+                                                              float* __restrict__ out0, float* __restrict__ out1,
+                                                              float* __restrict__ out2, int accumulate) {
+  ptx::grid_dep_wait();
+  const int i = blockIdx.x * 256 + threadIdx.x;
+  if (i >= N * NO) return;
+  const int o = i / N, c = i % N;
+  float s = 0.f;
+  for (int k = 0; k < R; ++k) s += part[(static_cast<size_t>(o) * R + k) * N + c];
+  float* out = o == 0 ? out0 : (o == 1 ? out1 : out2);
+  out[c] = accumulate ? out[c] + s : s;
+}
+
+// Row chunks so that a reduction fills the GPU: about 2 blocks per SM.
+int colred_chunks(int N) {
+  const int strips = (N + CR_COLS - 1) / CR_COLS;
+  int R = (2 * 148 + strips - 1) / strips;
+  if (R > kRedChunks) R = kRedChunks;
+  return R < 1 ? 1 : R;
 }
 
 // ------------------------------------------------------------------ MSE head
@@ -658,23 +668,36 @@ cudaError_t ln_bwd(const bf16* dy, const bf16* x, const float* mean, const float
 #undef X
     if (e != cudaSuccess) return e;
   }
-  dim3 grid((h + 255) / 256, kRedChunks);
-  if (dx && dxsum)
-    return launch_pdl(colred_kernel<2>, grid, dim3(256), 0, s, 1, dy, static_cast<int64_t>(h), x, mean, rstd,
-                      static_cast<const bf16*>(dx), T, h, part, dgamma, dbeta, dxsum, accumulate, tickets);
-  return launch_pdl(colred_kernel<1>, grid, dim3(256), 0, s, 1, dy, static_cast<int64_t>(h), x, mean, rstd,
-                    static_cast<const bf16*>(nullptr), T, h, part, dgamma, dbeta, static_cast<float*>(nullptr),
-                    accumulate, tickets);
+  const int R = colred_chunks(h);
+  dim3 grid((h + CR_COLS - 1) / CR_COLS, R);
+  const bool three = dx && dxsum;
+  cudaError_t e = three ? launch_pdl(colred_kernel<2>, grid, dim3(256), 0, s, 1, dy, static_cast<int64_t>(h), x, mean,
+                                     rstd, static_cast<const bf16*>(dx), T, h, part, dgamma, dbeta, dxsum, accumulate,
+                                     tickets)
+                        : launch_pdl(colred_kernel<1>, grid, dim3(256), 0, s, 1, dy, static_cast<int64_t>(h), x, mean,
+                                     rstd, static_cast<const bf16*>(nullptr), T, h, part, dgamma, dbeta,
+                                     static_cast<float*>(nullptr), accumulate, tickets);
+  if (e != cudaSuccess || R == 1) return e;
+  const int NO = three ? 3 : 2;
+  return launch_pdl(colred_finalize_kernel, dim3((h * NO + 255) / 256), dim3(256), 0, s, 1,
+                    static_cast<const float*>(part), R, h, NO, dgamma, dbeta, three ? dxsum : static_cast<float*>(nullptr),
+                    accumulate);
 }
+
+int colred_launches(int N) { return colred_chunks(N) > 1 ? 2 : 1; }
 
 cudaError_t colsum(const bf16* a, int T, int N, int64_t ld, float* out, int accumulate, float* part,
                    unsigned* tickets, cudaStream_t s) {
   if (N % 8 || ld % 8 || (N + 255) / 256 > kTickets) return cudaErrorInvalidValue;
-  dim3 grid((N + 255) / 256, kRedChunks);
-  return launch_pdl(colred_kernel<0>, grid, dim3(256), 0, s, 1, a, ld, static_cast<const bf16*>(nullptr),
-                    static_cast<const float*>(nullptr), static_cast<const float*>(nullptr),
-                    static_cast<const bf16*>(nullptr), T, N, part, out, static_cast<float*>(nullptr),
-                    static_cast<float*>(nullptr), accumulate, tickets);
+  const int R = colred_chunks(N);
+  dim3 grid((N + CR_COLS - 1) / CR_COLS, R);
+  cudaError_t e = launch_pdl(colred_kernel<0>, grid, dim3(256), 0, s, 1, a, ld, static_cast<const bf16*>(nullptr),
+                             static_cast<const float*>(nullptr), static_cast<const float*>(nullptr),
+                             static_cast<const bf16*>(nullptr), T, N, part, out, static_cast<float*>(nullptr),
+                             static_cast<float*>(nullptr), accumulate, tickets);
+  if (e != cudaSuccess || R == 1) return e;
+  return launch_pdl(colred_finalize_kernel, dim3((N + 255) / 256), dim3(256), 0, s, 1, static_cast<const float*>(part),
+                    R, N, 1, out, static_cast<float*>(nullptr), static_cast<float*>(nullptr), accumulate);
 }
 
 cudaError_t mse_loss(const bf16* y, const bf16* r, bf16* dy, float* part, int nparts, float* loss, int64_t n,

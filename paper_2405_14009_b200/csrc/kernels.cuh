@@ -22,6 +22,8 @@ cudaError_t ln_fwd(const bf16* x, const bf16* gamma, const bf16* beta, bf16* y, 
 // (dx may be null; it must not alias x).  dgamma (+)= sum_t dy*xhat, dbeta (+)= sum_t dy and,
 // if dxsum != null, dxsum (+)= sum_t dx, all three in ONE column-reduction launch.
 // part: 3*kRedChunks*h floats of scratch; tickets: kTickets zero-initialised counters.
+// Column reductions over N columns take 1 launch, or 2 when they need a finalize pass.
+int colred_launches(int N);
 cudaError_t ln_bwd(const bf16* dy, const bf16* x, const float* mean, const float* rstd, const bf16* gamma,
                    const bf16* resid, bf16* dx, float* dgamma, float* dbeta, float* dxsum, int accumulate, float* part,
                    unsigned* tickets, int T, int h, cudaStream_t s);

@@ -348,7 +348,8 @@ slip_status attention_bwd(slip_ctx* c, LayerStash& ls, cudaStream_t s) {
 
 // colsum(a[T, N]) -> out (fp32, overwrite or accumulate), one launch
 slip_status bias_grad(slip_ctx* c, const bf16* a, int N, int64_t ld, float* out, int accumulate, cudaStream_t s) {
-  return kcheck(c, colsum(a, c->dm.T, N, ld, out, accumulate, c->ws.part, c->ws.tickets, s), "colsum");
+  return kcheck(c, colsum(a, c->dm.T, N, ld, out, accumulate, c->ws.part, c->ws.tickets, s), "colsum",
+                colred_launches(N));
 }
 
 slip_status slot_check(slip_ctx* c, int slot, int want) {
@@ -438,7 +439,7 @@ slip_status backward_input_impl(slip_ctx* c, int slot, const void* dy, void* dx,
     SLIP_TRY(kcheck(c,
                     ln_bwd(c->ws.dy2, ls.x2, ls.mean2, ls.rstd2, Wt.g2, ls.dout, ls.dx2, G.g2, G.b2n, G.bo, accumulate,
                            c->ws.part, c->ws.tickets, D.T, D.h, s),
-                    "ln_bwd 2", 2));
+                    "ln_bwd 2", 1 + colred_launches(D.h)));
     // dO = dX2 Wo
     SLIP_TRY(linear_dx(c, ls.dx2, Wt.wo, D.h, D.h, c->ws.dO, EPI_BF16, nullptr, s));
     SLIP_TRY(attention_bwd(c, ls, s));
@@ -452,7 +453,7 @@ slip_status backward_input_impl(slip_ctx* c, int slot, const void* dy, void* dx,
     SLIP_TRY(kcheck(c,
                     ln_bwd(c->ws.dy1, ls.xin, ls.mean1, ls.rstd1, Wt.g1, ls.dx2, dxl, G.g1, G.b1n, dxl ? dxsum : nullptr,
                            accumulate, c->ws.part, c->ws.tickets, D.T, D.h, s),
-                    "ln_bwd 1", dxl ? 2 : 1));
+                    "ln_bwd 1", (dxl ? 1 : 0) + colred_launches(D.h)));
   }
   if ((D.ends & 1) && dx && dx != sb.dx)
     SLIP_CUDA(cudaMemcpyAsync(dx, sb.dx, Th * sizeof(bf16), cudaMemcpyDeviceToDevice, s));
@@ -664,7 +665,7 @@ slip_status slip_loss_ce(slip_ctx* c, int32_t slot, const void* y, const int32_t
   return kcheck(c,
                 ln_bwd(c->ws.dy2, e.xf, e.mean_f, e.rstd_f, gf, nullptr, static_cast<bf16*>(dy), c->grad + c->eo.gf,
                        c->grad + c->eo.bf, nullptr, accumulate, c->ws.part, c->ws.tickets, D.T, D.h, s),
-                "ln_bwd f", 2);
+                "ln_bwd f", 1 + colred_launches(D.h));
 }
 
 slip_status slip_synth_tokens(int32_t* out, int64_t n, int32_t n_classes, uint64_t seed, uint64_t k, uint64_t j,
