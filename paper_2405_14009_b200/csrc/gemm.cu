@@ -74,16 +74,36 @@ struct KParams {
   int accumulate;
   const GroupEntry* groups;  // grouped mode: problem table in device memory (nullptr otherwise)
   int n_groups;
+  // stream-K (see GemmDesc)
+  int sk;              // 1: stream-K decomposition over sk_units CTA pairs
+  int sk_units;
+  int64_t sk_iters;    // total * nkb
+  float* sk_ws;        // [2 * sk_units][BM][BN] fp32 partials (slot = pair * 2 + cta)
+  unsigned* sk_flags;  // [2 * sk_units] = sk_epoch once the slot's partial is written
+  unsigned sk_epoch;
 };
+
+// Work items of one CTA (pair): tiles round-robin, or a stream-K share of the tile x
+// k-block iterations.  kind: 0 = whole tile, 1 = first part (finishes the tile with the
+// other parts' partials), 2 = later part (writes a partial).
+struct ItemIter {
+  int64_t it, end;  // stream-K iteration range
+  int t;            // round-robin tile
+};
+__device__ __forceinline__ int64_t sk_start(const KParams& p, int u) {
+  return static_cast<int64_t>(u) * p.sk_iters / p.sk_units;
+}
 
 struct Tile {
   int zi, zo, m0, n0, kb0, kb1;
   int g, M, N;  // problem (grouped mode) and its extent
+  int t;        // tile index
 };
 
 template <int BN, int TM = BM>
 __device__ __forceinline__ Tile decode_tile(int t, const KParams& p) {
   Tile r;
+  r.t = t;
   if (p.groups) {
     int lo = 0, hi = p.n_groups - 1;
     while (lo < hi) {  // first problem whose tile range ends after t
@@ -133,6 +153,35 @@ __device__ __forceinline__ Tile decode_tile(int t, const KParams& p) {
   return r;
 }
 
+template <int BN, int TM>
+__device__ __forceinline__ bool next_item(const KParams& p, int u, int tstep, ItemIter& st, Tile& tl, int& kind) {
+  if (!p.sk) {
+    if (st.t >= p.total) return false;
+    tl = decode_tile<BN, TM>(st.t, p);
+    kind = 0;
+    st.t += tstep;
+    return true;
+  }
+  if (st.it >= st.end) return false;
+  const int t = static_cast<int>(st.it / p.nkb);
+  const int kb0 = static_cast<int>(st.it - static_cast<int64_t>(t) * p.nkb);
+  const int64_t rem = st.end - st.it;
+  const int kb1 = rem < p.nkb - kb0 ? kb0 + static_cast<int>(rem) : p.nkb;
+  tl = decode_tile<BN, TM>(t, p);
+  tl.kb0 = kb0;
+  tl.kb1 = kb1;
+  kind = (kb0 == 0 && kb1 == p.nkb) ? 0 : (kb0 == 0 ? 1 : 2);
+  st.it += kb1 - kb0;
+  return true;
+}
+__device__ __forceinline__ ItemIter item_begin(const KParams& p, int u) {
+  ItemIter st;
+  st.t = u;
+  st.it = p.sk ? sk_start(p, u) : 0;
+  st.end = p.sk ? sk_start(p, u + 1) : 0;
+  return st;
+}
+
 __device__ __forceinline__ float gelu_f(float x) {
   const float c = 0.7978845608028654f, a = 0.044715f;
   return 0.5f * x * (1.0f + ptx::tanh_fast(c * (x + a * x * x * x)));
@@ -160,10 +209,29 @@ __device__ __forceinline__ uint4 pack8(const float (&f)[8]) {
   return u;
 }
 
+#ifdef SLIP_GEMM_PROBE
+__device__ long long g_gprobe[4096];
+#define GPROBE(idx)                                                                      \
+  do {                                                                                   \
+    if (blockIdx.x == SLIP_GEMM_PROBE) g_gprobe[idx] = clock64();                        \
+  } while (0)
+__device__ __forceinline__ void g_gprobe_kind(int i, int k) {
+  if (blockIdx.x == SLIP_GEMM_PROBE) g_gprobe[200 + i] = k;
+}
+#else
+#define GPROBE(idx) \
+  do {              \
+  } while (0)
+#define g_gprobe_kind(i, k) \
+  do {                      \
+  } while (0)
+#endif
+
 template <int BN, bool A_MN, bool B_MN, bool PAIR>
 __global__ void __launch_bounds__(NUM_THREADS, 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-                   const __grid_constant__ CUtensorMap tmC, const KParams p) {
+                   const __grid_constant__ CUtensorMap tmC, const __grid_constant__ CUtensorMap tmX,
+                   const KParams p) {
   using C = Cfg<BN, A_MN, B_MN, PAIR>;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -198,7 +266,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   if (warp == 0 && lane == 0 && !p.groups) {
     ptx::prefetch_tmap(&tmA);
     ptx::prefetch_tmap(&tmB);
-    if (p.mode >= EPI_F32_STORE) ptx::prefetch_tmap(&tmC);
+    ptx::prefetch_tmap(&tmC);
+    if (p.mode == EPI_BF16_GELU) ptx::prefetch_tmap(&tmX);
   }
   if (warp == 2) {
     if (PAIR) ptx::tmem_alloc_pair<C::TMEM_COLS>(tmem_holder);
@@ -210,14 +279,17 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   ptx::tc_fence_after();
   const uint32_t tmem_base = *tmem_holder;
   ptx::grid_dep_wait();  // prologue above overlapped the previous kernel (PDL)
+  if (threadIdx.x == 0) GPROBE(0);
 
   if (warp == 0) {
     if (lane == 0) {
       // ---------------------------------------------------------------- TMA producer
       int stage = 0;
       uint32_t phase = 0;
-      for (int t = t0; t < p.total; t += tstep) {
-        const Tile tl = decode_tile<BN, C::TILE_M>(t, p);
+      ItemIter st = item_begin(p, t0);
+      Tile tl;
+      int kind;
+      while (next_item<BN, C::TILE_M>(p, t0, tstep, st, tl, kind)) {
         const CUtensorMap* mA = tl.g >= 0 ? &p.groups[tl.g].ta : &tmA;
         const CUtensorMap* mB = tl.g >= 0 ? &p.groups[tl.g].tb : &tmB;
         const int am0 = tl.m0 + cta * BM;          // this CTA's rows of A
@@ -272,9 +344,14 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       uint32_t phase = 0;
       int acc = 0;
       uint32_t acc_phase = 0;
-      for (int t = t0; t < p.total; t += tstep) {
-        const Tile tl = decode_tile<BN, C::TILE_M>(t, p);
+      ItemIter st = item_begin(p, t0);
+      Tile tl;
+      int kind;
+      int gi = 0;
+      while (next_item<BN, C::TILE_M>(p, t0, tstep, st, tl, kind)) {
+        GPROBE(10 + gi);
         ptx::mbar_wait(&tempty[acc], acc_phase ^ 1);
+        GPROBE(20 + gi);
         ptx::tc_fence_after();
         const uint32_t d_tmem = tmem_base + acc * C::ACC_COLS;
         for (int kb = tl.kb0; kb < tl.kb1; ++kb) {
@@ -298,6 +375,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         }
         if (PAIR) ptx::tc_commit_pair_mc(&tfull[acc], 0x3);
         else ptx::tc_commit(&tfull[acc]);
+        GPROBE(30 + gi);
+        ++gi;
         if (++acc == 2) {
           acc = 0;
           acc_phase ^= 1;
@@ -316,19 +395,22 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     const int qd = lane & 3;  // bf16 path: 8-column group of this lane after the transpose
     const bool ext_res = p.mode < EPI_F32_STORE && p.resid != nullptr;
     const bool ext_aux = p.mode == EPI_BF16_DGELU;
-    for (int t = t0; t < p.total; t += tstep) {
-      const Tile tl = decode_tile<BN, C::TILE_M>(t, p);
+    ItemIter st = item_begin(p, t0);
+    Tile tl;
+    int kind;
+    int gie = 0;
+    while (next_item<BN, C::TILE_M>(p, t0, tstep, st, tl, kind)) {
       const CUtensorMap* mC = tl.g >= 0 ? &p.groups[tl.g].tc : &tmC;
       const int row0 = tl.m0 + cta * BM + lq * 32;
       // residual / GeLU-input operands of a chunk are read-only: their loads are issued one
       // chunk ahead (the first before the accumulator is ready) so DRAM latency overlaps the
       // MMA mainloop and the previous chunk instead of stalling each row group.
       uint4 rn[4], hn[4];
-      auto prefetch = [&](int ch_) {
-        const int cc_ = tl.n0 + ch_ * 32 + 8 * qd;
+      auto prefetch = [&](int ch_) {  // this lane's row, 32 columns of chunk ch_: 4 x 16 bytes
+        const int mm = row0 + lane;
 #pragma unroll
         for (int it = 0; it < 4; ++it) {
-          const int mm = row0 + 8 * it + (lane >> 2);
+          const int cc_ = tl.n0 + ch_ * 32 + 8 * it;
           const bool ok = mm < tl.M && cc_ < tl.N;
           const int64_t off = tl.zo * p.c_zo + tl.zi * p.c_zi + static_cast<int64_t>(mm) * p.ldc + cc_;
           rn[it] = (ext_res && ok) ? __ldg(reinterpret_cast<const uint4*>(p.resid + off)) : make_uint4(0, 0, 0, 0);
@@ -337,8 +419,26 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       };
       if (ext_res || ext_aux) prefetch(half);
       ptx::mbar_wait(&tfull[acc], acc_phase);
+      if (ew == 0 && lane == 0) GPROBE(40 + 4 * gie + 0);
       ptx::tc_fence_after();
       const int m = row0 + lane;
+      // stream-K: the later parts of this tile (at the start of the next pairs' shares)
+      int q_end = t0 + 1;
+      if (kind == 1) {
+        while (q_end < p.sk_units && sk_start(p, q_end) < static_cast<int64_t>(tl.t + 1) * p.nkb) ++q_end;
+        if (ew == 0 && lane == 0)
+          for (int q = t0 + 1; q < q_end; ++q) {
+            if (sk_start(p, q) == sk_start(p, q + 1)) continue;  // empty share: no partial
+            const unsigned* f = p.sk_flags + q * (PAIR ? 2 : 1) + cta;
+            unsigned v;
+            do {
+              asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(f) : "memory");
+            } while (v != p.sk_epoch);
+          }
+        ptx::named_bar_sync(1, 32 * EPI_WARPS);
+      }
+      if (ew == 0 && lane == 0) GPROBE(40 + 4 * gie + 1);
+      const int slot_row = lq * 32 + lane;  // this thread's row of the CTA's 128
 #pragma unroll 1
       for (int ch = half; ch < NCH; ch += 2) {
         uint4 rc[4], hc[4];
@@ -349,8 +449,34 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         }
         if ((ext_res || ext_aux) && ch + 2 < NCH) prefetch(ch + 2);
         uint32_t r[32];
+        if (ew == 0 && lane == 0 && gie == 0) GPROBE(100 + 10 * (ch >> 1) + 0);
         ptx::tmem_ld_32x32b_x32(tmem_base + (static_cast<uint32_t>(lq * 32) << 16) + acc * C::ACC_COLS + ch * 32, r);
         ptx::tmem_ld_wait();
+        if (ew == 0 && lane == 0 && gie == 0) GPROBE(100 + 10 * (ch >> 1) + 1);
+        if (kind == 2) {  // a later part of a split tile: leave the fp32 partial, no epilogue
+          float4* dst = reinterpret_cast<float4*>(
+              p.sk_ws + (static_cast<size_t>(t0 * (PAIR ? 2 : 1) + cta) * BM + slot_row) * BN + ch * 32);
+#pragma unroll
+          for (int j = 0; j < 8; ++j)
+            dst[j] = make_float4(__uint_as_float(r[4 * j]), __uint_as_float(r[4 * j + 1]),
+                                 __uint_as_float(r[4 * j + 2]), __uint_as_float(r[4 * j + 3]));
+          continue;
+        }
+        if (kind == 1) {  // first part: add the later parts' partials in pair order
+          for (int q = t0 + 1; q < q_end; ++q) {
+            if (sk_start(p, q) == sk_start(p, q + 1)) continue;
+            const float4* src = reinterpret_cast<const float4*>(
+                p.sk_ws + (static_cast<size_t>(q * (PAIR ? 2 : 1) + cta) * BM + slot_row) * BN + ch * 32);
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+              const float4 v = __ldcg(src + j);
+              r[4 * j] = __float_as_uint(__uint_as_float(r[4 * j]) + v.x);
+              r[4 * j + 1] = __float_as_uint(__uint_as_float(r[4 * j + 1]) + v.y);
+              r[4 * j + 2] = __float_as_uint(__uint_as_float(r[4 * j + 2]) + v.z);
+              r[4 * j + 3] = __float_as_uint(__uint_as_float(r[4 * j + 3]) + v.w);
+            }
+          }
+        }
         const int n = tl.n0 + ch * 32;
         if (n >= tl.N || row0 >= tl.M) continue;
         if (p.mode >= EPI_F32_STORE) {
@@ -373,36 +499,32 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             ptx::bulk_commit();
           }
         } else {
-          // Transpose the 32x32 chunk through shared memory (16-byte chunks XOR-swizzled,
-          // conflict-free both ways) so that 4 lanes cover 64 contiguous bytes of a row:
-          // bias / residual / aux reads and the bf16 stores are coalesced per row.
+          // Row per lane (TMEM lane = output row, 32 consecutive columns in registers): bias
+          // (broadcast), GeLU / GeLU' / residual in registers, then the bf16 row is written to
+          // this warp's 2 KB staging tile with the 64-byte swizzle (16-byte chunk c of row r at
+          // r * 64 + ((c ^ (r >> 1 & 3)) << 4): conflict-free) and one TMA store writes the
+          // 32 x 32 tile (the GeLU pre-activation through a second tile and map).
           (void)m;
+          if (ew == 0 && lane == 0 && gie == 0) GPROBE(100 + 10 * (ch >> 1) + 2);
+          if (lane == 0) ptx::bulk_wait_read0();  // the previous store has read the staging tiles
           __syncwarp();
-          float4* rowp = reinterpret_cast<float4*>(buf + lane * 32);
-#pragma unroll
-          for (int j = 0; j < 8; ++j)
-            rowp[j ^ (lane & 7)] =
-                make_float4(p.alpha * __uint_as_float(r[4 * j]), p.alpha * __uint_as_float(r[4 * j + 1]),
-                            p.alpha * __uint_as_float(r[4 * j + 2]), p.alpha * __uint_as_float(r[4 * j + 3]));
-          __syncwarp();
-          const int cc = n + 8 * qd;     // first output column of this lane
-          float bv[8];
-#pragma unroll
-          for (int e = 0; e < 8; ++e) bv[e] = 0.f;
-          if (p.bias && cc < tl.N) unpack8(*reinterpret_cast<const uint4*>(p.bias + cc), bv);
-          const float4* sb = reinterpret_cast<const float4*>(buf);
+          uint8_t* so = reinterpret_cast<uint8_t*>(buf);
+          uint8_t* sx = so + 2048;
 #pragma unroll
           for (int it = 0; it < 4; ++it) {
-            const int rr = 8 * it + (lane >> 2);
-            const int mm = row0 + rr;
-            const float4 u0 = sb[rr * 8 + ((2 * qd) ^ (rr & 7))];
-            const float4 u1 = sb[rr * 8 + ((2 * qd + 1) ^ (rr & 7))];
-            if (mm >= tl.M || cc >= tl.N) continue;
-            float x[8] = {u0.x + bv[0], u0.y + bv[1], u0.z + bv[2], u0.w + bv[3],
-                          u1.x + bv[4], u1.y + bv[5], u1.z + bv[6], u1.w + bv[7]};
-            const int64_t off = tl.zo * p.c_zo + tl.zi * p.c_zi + static_cast<int64_t>(mm) * p.ldc + cc;
+            const int cc = n + 8 * it;
+            float x[8];
+#pragma unroll
+            for (int e = 0; e < 8; ++e) x[e] = p.alpha * __uint_as_float(r[8 * it + e]);
+            if (p.bias && cc < tl.N) {
+              float bv[8];
+              unpack8(__ldg(reinterpret_cast<const uint4*>(p.bias + cc)), bv);
+#pragma unroll
+              for (int e = 0; e < 8; ++e) x[e] += bv[e];
+            }
+            const uint32_t soff = lane * 64 + ((it ^ ((lane >> 1) & 3)) << 4);
             if (p.mode == EPI_BF16_GELU) {
-              *reinterpret_cast<uint4*>(p.aux + off) = pack8(x);
+              *reinterpret_cast<uint4*>(sx + soff) = pack8(x);
 #pragma unroll
               for (int e = 0; e < 8; ++e) x[e] = gelu_f(x[e]);
             } else if (p.mode == EPI_BF16_DGELU) {
@@ -417,8 +539,16 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 #pragma unroll
               for (int e = 0; e < 8; ++e) x[e] += rv[e];
             }
-            *reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(p.c) + off) = pack8(x);
+            *reinterpret_cast<uint4*>(so + soff) = pack8(x);
           }
+          ptx::fence_proxy_async_smem();
+          __syncwarp();
+          if (lane == 0) {
+            ptx::tma_store_4d(&tmC, so, n, row0, tl.zi, tl.zo);
+            if (p.mode == EPI_BF16_GELU) ptx::tma_store_4d(&tmX, sx, n, row0, tl.zi, tl.zo);
+            ptx::bulk_commit();
+          }
+          if (ew == 0 && lane == 0 && gie == 0) GPROBE(100 + 10 * (ch >> 1) + 3);
         }
       }
       ptx::tc_fence_before();
@@ -426,6 +556,17 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       if (lane == 0) {
         if (PAIR) ptx::mbar_arrive_leader(&tempty[acc]);
         else ptx::mbar_arrive(&tempty[acc]);
+      }
+      if (ew == 0 && lane == 0) GPROBE(40 + 4 * gie + 2);
+      if (ew == 0 && lane == 0) g_gprobe_kind(gie, kind);
+      ++gie;
+      if (kind == 2) {  // publish the partial: every writer fences, then one release store
+        __threadfence();
+        ptx::named_bar_sync(1, 32 * EPI_WARPS);
+        if (ew == 0 && lane == 0) {
+          unsigned* f = p.sk_flags + t0 * (PAIR ? 2 : 1) + cta;
+          asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(f), "r"(p.sk_epoch) : "memory");
+        }
       }
       if (++acc == 2) {
         acc = 0;
@@ -462,7 +603,8 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
 
 // 4-D view: dims (inner, outer, zi, zo); strides in elements for dims 1..3.
 bool encode4d(CUtensorMap* map, CUtensorMapDataType dt, int esize, const void* base, uint64_t d0, uint64_t d1,
-              uint64_t d2, uint64_t d3, int64_t s1, int64_t s2, int64_t s3, uint32_t b0, uint32_t b1) {
+              uint64_t d2, uint64_t d3, int64_t s1, int64_t s2, int64_t s3, uint32_t b0, uint32_t b1,
+              CUtensorMapSwizzle swz = CU_TENSOR_MAP_SWIZZLE_128B) {
   auto fn = encode_fn();
   if (!fn) {
     g_msg = "cuTensorMapEncodeTiled unavailable (driver entry point)";
@@ -493,7 +635,7 @@ bool encode4d(CUtensorMap* map, CUtensorMapDataType dt, int esize, const void* b
   cuuint32_t box[4] = {b0, b1, 1, 1};
   cuuint32_t est[4] = {1, 1, 1, 1};
   CUresult r = fn(map, dt, 4, const_cast<void*>(base), dims, strides, box, est, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                  CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+                  swz, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) {
     char b[200];
     snprintf(b, sizeof b, "cuTensorMapEncodeTiled failed (%d): dims %llu %llu %llu %llu box %u %u", static_cast<int>(r),
@@ -516,8 +658,8 @@ bool encode_operand(CUtensorMap* map, const Operand& o, int rows, int K, int zi,
 
 // Persistent launch: one CTA (or CTA pair, cluster 2x1x1) per SM, at most one per tile.
 template <int BN, bool A_MN, bool B_MN, bool PAIR>
-cudaError_t launch_kernel(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& tc, const KParams& p,
-                          cudaStream_t s) {
+cudaError_t launch_kernel(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& tc, const CUtensorMap& tx,
+                          const KParams& p, cudaStream_t s) {
   using C = Cfg<BN, A_MN, B_MN, PAIR>;
   auto kern = gemm_tc_kernel<BN, A_MN, B_MN, PAIR>;
   static std::once_flag once;
@@ -529,7 +671,7 @@ cudaError_t launch_kernel(const CUtensorMap& ta, const CUtensorMap& tb, const CU
   if (p.total == 0) return cudaSuccess;
   const int units = PAIR ? sm_budget() / 2 : sm_budget();
   const int grid = (p.total < units ? p.total : units) * (PAIR ? 2 : 1);
-  return launch_pdl(kern, dim3(grid), dim3(NUM_THREADS), C::SMEM_BYTES, s, PAIR ? 2 : 1, ta, tb, tc, p);
+  return launch_pdl(kern, dim3(grid), dim3(NUM_THREADS), C::SMEM_BYTES, s, PAIR ? 2 : 1, ta, tb, tc, tx, p);
 }
 
 template <int BN, bool A_MN, bool B_MN, bool PAIR = false>
@@ -549,13 +691,25 @@ cudaError_t launch_t(const GemmDesc& d, cudaStream_t s, const GroupEntry* groups
     p.groups = groups;
     p.n_groups = n_groups;
     p.total = group_tiles;
-    return launch_kernel<BN, A_MN, B_MN, PAIR>(ta, tb, tc, p, s);
+    return launch_kernel<BN, A_MN, B_MN, PAIR>(ta, tb, tc, tc, p, s);
   }
   if (!encode_operand(&ta, d.a, d.M, d.K, d.zi_count, d.zo_count, BM)) return cudaErrorInvalidValue;
   if (!encode_operand(&tb, d.b, d.N, d.K, d.zi_count, d.zo_count, C::B_ROWS)) return cudaErrorInvalidValue;
+  CUtensorMap tx;
+  std::memset(&tx, 0, sizeof tx);
   if (d.mode >= EPI_F32_STORE) {
     if (!encode4d(&tc, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, d.c, d.N, d.M, d.zi_count, d.zo_count, d.ldc, d.c_zi,
                   d.c_zo, 32, 32))
+      return cudaErrorInvalidValue;
+  } else {
+    // bf16 outputs (and the GeLU pre-activation) leave through TMA stores of 32 x 32 tiles
+    // staged in shared memory with the 64-byte swizzle (conflict-free row writes)
+    if (!encode4d(&tc, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, d.c, d.N, d.M, d.zi_count, d.zo_count, d.ldc, d.c_zi,
+                  d.c_zo, 32, 32, CU_TENSOR_MAP_SWIZZLE_64B))
+      return cudaErrorInvalidValue;
+    if (d.mode == EPI_BF16_GELU &&
+        !encode4d(&tx, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, d.aux, d.N, d.M, d.zi_count, d.zo_count, d.ldc, d.c_zi,
+                  d.c_zo, 32, 32, CU_TENSOR_MAP_SWIZZLE_64B))
       return cudaErrorInvalidValue;
   }
   KParams p{};
@@ -579,7 +733,21 @@ cudaError_t launch_t(const GemmDesc& d, cudaStream_t s, const GroupEntry* groups
   p.aux = static_cast<__nv_bfloat16*>(d.aux);
   p.alpha = d.alpha;
   p.accumulate = d.accumulate;
-  return launch_kernel<BN, A_MN, B_MN, PAIR>(ta, tb, tc, p, s);
+  // stream-K when the tiles leave a partial last wave of CTA pairs (see GemmDesc)
+  const int units = PAIR ? sm_budget() / 2 : sm_budget();
+  if (PAIR && d.sk_ws && d.sk_flags && d.mode < EPI_F32_STORE && d.causal == CAUSAL_NONE && d.zi_count == 1 &&
+      d.zo_count == 1 && p.total % units != 0 && p.total < 4 * units && p.nkb >= 8) {
+    static std::atomic<unsigned> epoch{0};
+    p.sk = 1;
+    p.sk_units = units;
+    p.sk_iters = static_cast<int64_t>(p.total) * p.nkb;
+    p.sk_ws = d.sk_ws;
+    p.sk_flags = d.sk_flags;
+    p.sk_epoch = epoch.fetch_add(1) + 1;
+    if (p.sk_epoch == 0) p.sk_epoch = epoch.fetch_add(1) + 1;  // 0 = never written
+    p.total = units;  // every pair takes a share
+  }
+  return launch_kernel<BN, A_MN, B_MN, PAIR>(ta, tb, tc, tx, p, s);
 }
 
 template <int BN>
@@ -623,6 +791,12 @@ int sm_budget() {
 }
 
 const char* gemm_last_message() { return g_msg.c_str(); }
+
+#ifdef SLIP_GEMM_PROBE
+void gemm_probe_read(long long* out, int n) { cudaMemcpyFromSymbol(out, g_gprobe, n * sizeof(long long)); }
+#endif
+
+size_t gemm_sk_bytes() { return static_cast<size_t>(num_sms()) * BM * 256 * sizeof(float); }
 
 bool encode_bf16_4d(CUtensorMap* map, const void* base, uint64_t d0, uint64_t d1, uint64_t d2, uint64_t d3,
                     int64_t s1, int64_t s2, int64_t s3, uint32_t b0, uint32_t b1) {

@@ -52,7 +52,15 @@ struct GemmDesc {
   float alpha = 1.0f;
   int accumulate = 0;
   bool pair = true;  // bn == 256, no causal mode: use CTA-pair (cta_group::2) 256 x 256 tiles
+  // Stream-K (bf16 epilogues, pair tiles, no batching): when the tiles do not fill whole
+  // waves of CTA pairs, every pair takes an equal share of the tile x k-block iterations;
+  // a tile split between pairs is finished by the pair holding its first k-block, which
+  // adds the fp32 partials the others left in sk_ws (fixed order: deterministic).
+  // sk_ws: gemm_sk_bytes() bytes, sk_flags: num_sms() zero-initialised words; NULL: off.
+  float* sk_ws = nullptr;
+  unsigned* sk_flags = nullptr;
 };
+size_t gemm_sk_bytes();
 
 // Enqueue on `s`.  Returns cudaSuccess or the launch / encode error; shape errors
 // return cudaErrorInvalidValue with a message retrievable by gemm_last_message().

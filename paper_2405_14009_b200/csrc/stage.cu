@@ -179,6 +179,8 @@ void carve_ws(Carver& cv, const Dims& d, Workspace* out) {
   w.losses = cv.take<float>(1024);
   w.nonfinite = cv.take<int32_t>(64);
   w.vflags = cv.take<int32_t>(64);
+  w.sk_flags = cv.take<unsigned>(static_cast<size_t>(num_sms()));
+  w.sk_ws = cv.take<float>(gemm_sk_bytes() / sizeof(float));
   if (out) *out = w;
 }
 
@@ -203,7 +205,12 @@ using namespace slip;
 namespace {
 
 // ---------------------------------------------------------------- GEMM helpers
-slip_status run_gemm(slip_ctx* c, const GemmDesc& d, cudaStream_t s, const char* what) {
+slip_status run_gemm(slip_ctx* c, const GemmDesc& d0, cudaStream_t s, const char* what) {
+  GemmDesc d = d0;
+  if (c->stream_k) {  // stream-K workspace of the ctx (partial last waves of the F / B linears)
+    d.sk_ws = c->ws.sk_ws;
+    d.sk_flags = c->ws.sk_flags;
+  }
   cudaError_t e = gemm_launch(d, s);
   if (e != cudaSuccess) {
     std::string m = std::string(what) + ": " + cudaGetErrorString(e);
@@ -545,6 +552,7 @@ slip_status slip_stage_bind(slip_ctx* c, void* w_bf16, float* master, float* gra
   carve_ws(wv, c->dm, &c->ws);
   SLIP_CUDA(cudaMemset(c->ws.tickets, 0, kTickets * sizeof(unsigned)));
   SLIP_CUDA(cudaMemset(c->ws.nonfinite, 0, sizeof(int32_t)));
+  SLIP_CUDA(cudaMemset(c->ws.sk_flags, 0, static_cast<size_t>(num_sms()) * sizeof(unsigned)));
   // W problem tables (tensor maps of the 4L weight-gradient GEMMs) per slot
   std::vector<GroupEntry> host(4 * static_cast<size_t>(c->L) + ((c->dm.ends & 2) ? 1 : 0));
   for (int i = 0; i < c->n_slots; ++i) {
@@ -712,6 +720,12 @@ slip_status rollback_if(slip_ctx* c, const slip_adam* a, int64_t step, float gra
 }  // namespace slip
 
 extern "C" {
+
+slip_status slip_set_stream_k(slip_ctx* c, int32_t enable) {
+  SLIP_CHECK(c, SLIP_EINVAL, "set_stream_k: ctx is NULL");
+  c->stream_k = enable != 0;
+  return SLIP_OK;
+}
 
 slip_status slip_set_validation(slip_ctx* c, int32_t enable) {
   SLIP_CHECK(c, SLIP_EINVAL, "set_validation: ctx is NULL");

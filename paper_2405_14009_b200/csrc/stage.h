@@ -56,6 +56,8 @@ struct Workspace {
   float* losses;     // [1024] per-micro-batch losses (executor)
   int32_t* nonfinite;  // [1] post-step validation flag (executor)
   int32_t* vflags;     // [8] validated mode: own_bad[2], global_bad[2] (per iteration parity), rollbacks
+  float* sk_ws;        // stream-K fp32 partials of the F / B linears (gemm_sk_bytes)
+  unsigned* sk_flags;  // [num_sms] stream-K partial epochs
 };
 
 enum SlotState : int { SLOT_FREE = 0, SLOT_F_DONE = 1, SLOT_B_DONE = 2 };
@@ -95,6 +97,7 @@ struct slip_ctx {
   int64_t opt_step = 0;  // AdamW steps taken by the executor
   bool trace_on = false;
   bool validate = false;   // post-step validation + cross-stage rollback (slip_set_validation)
+  bool stream_k = false;   // stream-K for F / B linears (slip_set_stream_k; measured slower, off)
   int fault_next_opt = 0;  // slip_inject_fault: the next validation reports non-finite gradients
   std::vector<slip_trace_rec> trace;  // timeline of the last traced executor run
 };

@@ -26,10 +26,13 @@ def main():
     ap.add_argument("--layers", type=int, default=1)
     ap.add_argument("--reps", type=int, default=10)
     ap.add_argument("--once", action="store_true")
+    ap.add_argument("--no-sk", action="store_true", help="disable stream-K for the F / B linears")
     a = ap.parse_args()
     cfg = CFGS[a.cfg]
     L = a.layers
     st = rt.Stage(cfg, L, n_slots=1)
+    if a.no_sk:
+        rt.call("slip_set_stream_k", st.ctx, 0)
     rt.init_master_(st.master, cfg, L, cfg.layers)
     rt.call("slip_weights_from_master", st.ctx, rt._stream())
     T, h, f = cfg.tokens, cfg.hidden, cfg.ffn
