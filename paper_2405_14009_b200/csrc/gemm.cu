@@ -508,6 +508,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           if (ew == 0 && lane == 0 && gie == 0) GPROBE(100 + 10 * (ch >> 1) + 2);
           if (lane == 0) ptx::bulk_wait_read0();  // the previous store has read the staging tiles
           __syncwarp();
+          if (ew == 0 && lane == 0 && gie == 0) GPROBE(100 + 10 * (ch >> 1) + 6);
           uint8_t* so = reinterpret_cast<uint8_t*>(buf);
           uint8_t* sx = so + 2048;
 #pragma unroll
@@ -541,7 +542,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             }
             *reinterpret_cast<uint4*>(so + soff) = pack8(x);
           }
+          if (ew == 0 && lane == 0 && gie == 0) GPROBE(100 + 10 * (ch >> 1) + 4);
           ptx::fence_proxy_async_smem();
+          if (ew == 0 && lane == 0 && gie == 0) GPROBE(100 + 10 * (ch >> 1) + 5);
           __syncwarp();
           if (lane == 0) {
             ptx::tma_store_4d(&tmC, so, n, row0, tl.zi, tl.zo);

@@ -61,8 +61,12 @@ int main(int argc, char** argv) {
     printf("\n  epi acc ready / waited / done (kind):");
     for (int i = 0; i < 4; ++i)
       if (p[40 + 4 * i]) printf(" [%lld %lld %lld k%lld]", p[40 + 4 * i] - t0, p[41 + 4 * i] - t0, p[42 + 4 * i] - t0, p[200 + i]);
-    printf("\n  chunk (before ld, after ld, after transpose, after stores):");
-    for (int c = 0; c < 4; ++c) printf(" [%lld %lld %lld %lld]", p[100 + 10 * c] - t0, p[101 + 10 * c] - t0, p[102 + 10 * c] - t0, p[103 + 10 * c] - t0);
+    printf("\n  chunk (ld, ld done, bf16 start, wait done, computed, fenced, issued):");
+    for (int c = 0; c < 4; ++c) {
+      const long long b = p[100 + 10 * c];
+      printf(" [%lld: +%lld +%lld +%lld +%lld +%lld +%lld]", b - t0, p[101 + 10 * c] - b, p[102 + 10 * c] - b,
+             p[106 + 10 * c] - b, p[104 + 10 * c] - b, p[105 + 10 * c] - b, p[103 + 10 * c] - b);
+    }
     printf("\n");
     cudaMemset(flags, 0, 4096);
   }
