@@ -279,7 +279,8 @@ def main():
     rt.init_master_(stage.master, cfg, L, args.layers, seed=rank % PP)
     rt.call("slip_weights_from_master", stage.ctx, rt._stream())
     comm = rt.Comm(rank, world)
-    comm.set_p2p_ctas(args.p2p_ctas)
+    if world > 1:
+        comm.set_p2p_ctas(args.p2p_ctas)
     comm.setup(PP, DP, m, live)
     stream = torch.cuda.current_stream()
 

@@ -8,7 +8,8 @@ import ctypes as C
 import os
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_PKG, "libslip.so")
+# SLIP_LIB: an alternative build of the same library (A/B measurements of kernel changes)
+LIB_PATH = os.environ.get("SLIP_LIB") or os.path.join(_PKG, "libslip.so")
 
 SLIP_F, SLIP_B, SLIP_W, SLIP_BC, SLIP_OPT, SLIP_AR = range(6)
 STATUS = {0: "SLIP_OK", 1: "SLIP_EINVAL", 2: "SLIP_EUNRECOVERABLE", 3: "SLIP_EINFEASIBLE_MEMORY", 4: "SLIP_ESTATE",

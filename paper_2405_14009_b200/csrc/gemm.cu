@@ -192,6 +192,10 @@ __device__ __forceinline__ float gelu_grad_f(float x) {
   return 0.5f * (1.0f + t) + 0.5f * x * (1.0f - t * t) * c * (1.0f + 3.0f * a * x * x);
 }
 
+__device__ __forceinline__ void st_shared_u4(uint32_t addr, const uint4& v) {
+  asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w)
+               : "memory");
+}
 __device__ __forceinline__ void unpack8(const uint4& u, float (&f)[8]) {
   const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&u);
 #pragma unroll
@@ -393,8 +397,15 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     uint32_t acc_phase = 0;
     constexpr int NCH = C::ACC_COLS / 32;
     const int qd = lane & 3;  // bf16 path: 8-column group of this lane after the transpose
-    const bool ext_res = p.mode < EPI_F32_STORE && p.resid != nullptr;
-    const bool ext_aux = p.mode == EPI_BF16_DGELU;
+    // kernel parameters the chunk loop uses, held in registers: the loop's asm statements
+    // clobber "memory", which would otherwise re-read each of them per use
+    const int e_mode = p.mode;
+    const float e_alpha = p.alpha;
+    const __nv_bfloat16* const e_bias = p.bias;
+    const __nv_bfloat16* const e_resid = p.resid;
+    const int e_accum = p.accumulate;
+    const bool ext_res = e_mode < EPI_F32_STORE && e_resid != nullptr;
+    const bool ext_aux = e_mode == EPI_BF16_DGELU;
     ItemIter st = item_begin(p, t0);
     Tile tl;
     int kind;
@@ -479,11 +490,11 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         }
         const int n = tl.n0 + ch * 32;
         if (n >= tl.N || row0 >= tl.M) continue;
-        if (p.mode >= EPI_F32_STORE) {
+        if (e_mode >= EPI_F32_STORE) {
           if (lane == 0) ptx::bulk_wait_read0();
           __syncwarp();
           float4* rowp = reinterpret_cast<float4*>(buf + lane * 32);
-          const float al = (p.mode == EPI_F32_STORE) ? p.alpha : 1.0f;
+          const float al = (e_mode == EPI_F32_STORE) ? e_alpha : 1.0f;
 #pragma unroll
           for (int j = 0; j < 8; ++j) {
             rowp[j ^ (lane & 7)] = make_float4(al * __uint_as_float(r[4 * j]), al * __uint_as_float(r[4 * j + 1]),
@@ -492,7 +503,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           ptx::fence_proxy_async_smem();
           __syncwarp();
           if (lane == 0) {
-            if (p.mode == EPI_F32_ACC && p.accumulate)
+            if (e_mode == EPI_F32_ACC && e_accum)
               ptx::tma_reduce_add_4d(mC, buf, n, row0, tl.zi, tl.zo);
             else
               ptx::tma_store_4d(mC, buf, n, row0, tl.zi, tl.zo);
@@ -511,36 +522,37 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           if (ew == 0 && lane == 0 && gie == 0) GPROBE(100 + 10 * (ch >> 1) + 6);
           uint8_t* so = reinterpret_cast<uint8_t*>(buf);
           uint8_t* sx = so + 2048;
+          const uint32_t so_s = ptx::smem_u32(so), sx_s = so_s + 2048;  // shared-window addresses
 #pragma unroll
           for (int it = 0; it < 4; ++it) {
             const int cc = n + 8 * it;
             float x[8];
 #pragma unroll
-            for (int e = 0; e < 8; ++e) x[e] = p.alpha * __uint_as_float(r[8 * it + e]);
-            if (p.bias && cc < tl.N) {
+            for (int e = 0; e < 8; ++e) x[e] = e_alpha * __uint_as_float(r[8 * it + e]);
+            if (e_bias && cc < tl.N) {
               float bv[8];
-              unpack8(__ldg(reinterpret_cast<const uint4*>(p.bias + cc)), bv);
+              unpack8(__ldg(reinterpret_cast<const uint4*>(e_bias + cc)), bv);
 #pragma unroll
               for (int e = 0; e < 8; ++e) x[e] += bv[e];
             }
             const uint32_t soff = lane * 64 + ((it ^ ((lane >> 1) & 3)) << 4);
-            if (p.mode == EPI_BF16_GELU) {
-              *reinterpret_cast<uint4*>(sx + soff) = pack8(x);
+            if (e_mode == EPI_BF16_GELU) {
+              st_shared_u4(sx_s + soff, pack8(x));
 #pragma unroll
               for (int e = 0; e < 8; ++e) x[e] = gelu_f(x[e]);
-            } else if (p.mode == EPI_BF16_DGELU) {
+            } else if (e_mode == EPI_BF16_DGELU) {
               float hv[8];
               unpack8(hc[it], hv);
 #pragma unroll
               for (int e = 0; e < 8; ++e) x[e] *= gelu_grad_f(hv[e]);
             }
-            if (p.resid) {
+            if (e_resid) {
               float rv[8];
               unpack8(rc[it], rv);
 #pragma unroll
               for (int e = 0; e < 8; ++e) x[e] += rv[e];
             }
-            *reinterpret_cast<uint4*>(so + soff) = pack8(x);
+            st_shared_u4(so_s + soff, pack8(x));
           }
           if (ew == 0 && lane == 0 && gie == 0) GPROBE(100 + 10 * (ch >> 1) + 4);
           ptx::fence_proxy_async_smem();
@@ -548,7 +560,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           __syncwarp();
           if (lane == 0) {
             ptx::tma_store_4d(&tmC, so, n, row0, tl.zi, tl.zo);
-            if (p.mode == EPI_BF16_GELU) ptx::tma_store_4d(&tmX, sx, n, row0, tl.zi, tl.zo);
+            if (e_mode == EPI_BF16_GELU) ptx::tma_store_4d(&tmX, sx, n, row0, tl.zi, tl.zo);
             ptx::bulk_commit();
           }
           if (ew == 0 && lane == 0 && gie == 0) GPROBE(100 + 10 * (ch >> 1) + 3);
