@@ -64,6 +64,15 @@ struct KArgs {
   float* dsum_w;            // DQ: D written here for the dK / dV kernel
 };
 
+// Descriptor of a 128B-swizzled operand at base; the UMMA_K steps below are constant
+// offsets added to it (start-address field, 16-byte units), so that the MMA issue loop
+// does not rebuild descriptors per instruction.
+__device__ __forceinline__ uint64_t kdesc(uint32_t base) { return ptx::smem_desc_sw128(base, 16, 1024); }
+__device__ __forceinline__ uint64_t mdesc(uint32_t base, uint32_t lbo) { return ptx::smem_desc_sw128(base, lbo, 1024); }
+__host__ __device__ constexpr uint64_t dk_off(int kk) { return static_cast<uint64_t>((kk >> 2) * (16384 >> 4) + (kk & 3) * 2); }
+__host__ __device__ constexpr uint64_t hk_off(int kk) { return static_cast<uint64_t>((kk >> 2) * (8192 >> 4) + (kk & 3) * 2); }
+__host__ __device__ constexpr uint64_t m_off(int kk) { return static_cast<uint64_t>(kk * (2048 >> 4)); }
+
 // tile [128 rows][D] as a K-major operand (contraction over d), UMMA_K step kk
 __device__ __forceinline__ uint64_t dk(uint32_t base, int kk) {
   return ptx::smem_desc_sw128(base + (kk >> 2) * ATOM + (kk & 3) * 32, 16, 1024);
@@ -208,9 +217,10 @@ __global__ void __launch_bounds__(FWD_NT, 1)
         ptx::mbar_wait(&k_full[st], (j / KST) & 1);
         ptx::tc_fence_after();
         const uint32_t kb = kb0 + st * C::TB;
+        const uint64_t dq = kdesc(qb), dkk = kdesc(kb);
 #pragma unroll
         for (int kk = 0; kk < C::KS; ++kk)
-          ptx::tc_mma_f16_w(tmem + (j % NSB) * 128, dk(qb, kk), dk(kb, kk), C::IDESC_S, kk > 0);
+          ptx::tc_mma_f16_w(tmem + (j % NSB) * 128, dq + dk_off(kk), dkk + dk_off(kk), C::IDESC_S, kk > 0);
         ptx::tc_commit_w(&s_full[j % NSB]);
         ptx::tc_commit_w(&k_empty[st]);
       };
@@ -222,9 +232,10 @@ __global__ void __launch_bounds__(FWD_NT, 1)
         PROBE(100 + j);
         ptx::tc_fence_after();
         const uint32_t vb = vb0 + st * C::TB;
+        const uint64_t dvb = mdesc(vb, ATOM);
 #pragma unroll
         for (int kk = 0; kk < TILE / 16; ++kk)  // O += P V_j, P (bf16 pairs) from TMEM
-          ptx::tc_mma_f16_ts_w(tmem + NSB * 128, tmem + (j % NSB) * 128 + kk * 8, dm(vb, kk), C::IDESC_O,
+          ptx::tc_mma_f16_ts_w(tmem + NSB * 128, tmem + (j % NSB) * 128 + kk * 8, dvb + m_off(kk), C::IDESC_O,
                              (j > 0 || kk > 0) ? 1u : 0u);
         ptx::tc_commit_w(&o_done[j % NSB]);
         ptx::tc_commit_w(&v_empty[st]);
@@ -456,10 +467,13 @@ __global__ void __launch_bounds__(BWD_NT, 1)
         ptx::mbar_wait(&kv_full[st], (h / NST) & 1);
         ptx::tc_fence_after();
         const uint32_t kb = rb + st * STG, vb = kb + H::HB, tS = tmem + (h % NSB) * 128;
+        const uint64_t dqq = kdesc(qb), dkh = kdesc(kb), doo = kdesc(ob), dvh = kdesc(vb);
 #pragma unroll
-        for (int kk = 0; kk < C::KS; ++kk) ptx::tc_mma_f16_w(tS, dk(qb, kk), hk(kb, kk), H::IDESC_S, kk > 0);
+        for (int kk = 0; kk < C::KS; ++kk)
+          ptx::tc_mma_f16_w(tS, dqq + dk_off(kk), dkh + hk_off(kk), H::IDESC_S, kk > 0);
 #pragma unroll
-        for (int kk = 0; kk < C::KS; ++kk) ptx::tc_mma_f16_w(tS + 64, dk(ob, kk), hk(vb, kk), H::IDESC_S, kk > 0);
+        for (int kk = 0; kk < C::KS; ++kk)
+          ptx::tc_mma_f16_w(tS + 64, doo + dk_off(kk), dvh + hk_off(kk), H::IDESC_S, kk > 0);
         ptx::tc_commit_w(&s_full[h % NSB]);
       };
       for (int h = 0; h < NSB && h < nh; ++h) mma_sd(h);
@@ -469,9 +483,10 @@ __global__ void __launch_bounds__(BWD_NT, 1)
         PROBE(2000 + h);
         ptx::tc_fence_after();
         const uint32_t kb = rb + st * STG, tX = tmem + (h % NSB) * 128;
+        const uint64_t dkm = mdesc(kb, HATOM);
 #pragma unroll
         for (int kk = 0; kk < HT / 16; ++kk)  // dQ += dS K_h, dS (bf16 pairs) from TMEM
-          ptx::tc_mma_f16_ts_w(tmem + NSB * 128, tX + acol(kk), hm(kb, kk), H::IDESC_ACC, (h > 0 || kk > 0) ? 1u : 0u);
+          ptx::tc_mma_f16_ts_w(tmem + NSB * 128, tX + acol(kk), dkm + m_off(kk), H::IDESC_ACC, (h > 0 || kk > 0) ? 1u : 0u);
         ptx::tc_commit_w(&kv_empty[st]);
         if (h + NSB < nh) mma_sd(h + NSB);  // into the buffer dQ_h reads dS from (MMAs execute in order)
       }
@@ -640,10 +655,13 @@ __global__ void __launch_bounds__(BWD_NT, 1)
         ptx::mbar_wait(&qd_full[st], (h / NST) & 1);
         ptx::tc_fence_after();
         const uint32_t qb = rb + st * STG, ob = qb + H::HB, tS = tmem + (h & 1) * 128;
+        const uint64_t dkk = kdesc(kb), dqh = kdesc(qb), dvv = kdesc(vb), doh = kdesc(ob);
 #pragma unroll
-        for (int kk = 0; kk < C::KS; ++kk) ptx::tc_mma_f16_w(tS, dk(kb, kk), hk(qb, kk), H::IDESC_S, kk > 0);
+        for (int kk = 0; kk < C::KS; ++kk)
+          ptx::tc_mma_f16_w(tS, dkk + dk_off(kk), dqh + hk_off(kk), H::IDESC_S, kk > 0);
 #pragma unroll
-        for (int kk = 0; kk < C::KS; ++kk) ptx::tc_mma_f16_w(tS + 64, dk(vb, kk), hk(ob, kk), H::IDESC_S, kk > 0);
+        for (int kk = 0; kk < C::KS; ++kk)
+          ptx::tc_mma_f16_w(tS + 64, dvv + dk_off(kk), doh + hk_off(kk), H::IDESC_S, kk > 0);
         ptx::tc_commit_w(&s_full[h & 1]);
       };
       mma_sd(0);
@@ -653,12 +671,13 @@ __global__ void __launch_bounds__(BWD_NT, 1)
         ptx::mbar_wait(&x_full[h & 1], (h >> 1) & 1);
         ptx::tc_fence_after();
         const uint32_t qb = rb + st * STG, ob = qb + H::HB, tX = tmem + (h & 1) * 128;
+        const uint64_t dom = mdesc(ob, HATOM), dqm = mdesc(qb, HATOM);
 #pragma unroll
         for (int kk = 0; kk < HT / 16; ++kk)  // dV += P^T dO_h
-          ptx::tc_mma_f16_ts_w(tmem + 256, tX + acol(kk), hm(ob, kk), H::IDESC_ACC, (h > 0 || kk > 0) ? 1u : 0u);
+          ptx::tc_mma_f16_ts_w(tmem + 256, tX + acol(kk), dom + m_off(kk), H::IDESC_ACC, (h > 0 || kk > 0) ? 1u : 0u);
 #pragma unroll
         for (int kk = 0; kk < HT / 16; ++kk)  // dK += dS^T Q_h
-          ptx::tc_mma_f16_ts_w(tmem + 384, tX + 64 + acol(kk), hm(qb, kk), H::IDESC_ACC,
+          ptx::tc_mma_f16_ts_w(tmem + 384, tX + 64 + acol(kk), dqm + m_off(kk), H::IDESC_ACC,
                              (h > 0 || kk > 0) ? 1u : 0u);
         ptx::tc_commit_w(&qd_empty[st]);
         if (h + 2 < nh) mma_sd(h + 2);  // into the buffer dV_h / dK_h read from (in order)
