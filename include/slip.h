@@ -303,6 +303,14 @@ slip_status slip_weights_from_master(slip_ctx* ctx, slip_stream s);
 slip_status slip_attention(int32_t s, int32_t heads, int32_t batch, int32_t d, const void* qkv, const void* o,
                            const void* d_o, void* out, float* lse, float* dsum, int32_t backward, slip_stream st);
 
+/* Stream-K for the F / B linears of this ctx (default OFF: on B200 the split tiles
+ * expose one epilogue per part and measured slower): a GEMM whose CTA-pair
+ * tiles leave a partial last wave (e.g. 64 tiles of a [2048 x 2048] output on 74
+ * pairs) gives every pair an equal share of the tile x k-block iterations; a split
+ * tile is finished by the pair holding its first k-block, which adds the other
+ * parts' fp32 partials in pair order (deterministic). */
+slip_status slip_set_stream_k(slip_ctx* ctx, int32_t enable);
+
 /* Process-wide: persistent GEMM grids fill at most (#SMs - n) SMs, leaving n
  * SMs to kernels of other streams (the executor's NCCL transfers and stage
  * all-reduce run concurrently with compute; a persistent CTA that finds no free
