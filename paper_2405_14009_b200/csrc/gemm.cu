@@ -406,6 +406,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     const int e_accum = p.accumulate;
     const bool ext_res = e_mode < EPI_F32_STORE && e_resid != nullptr;
     const bool ext_aux = e_mode == EPI_BF16_DGELU;
+    const bool ext_bias = e_mode < EPI_F32_STORE && e_bias != nullptr;
     ItemIter st = item_begin(p, t0);
     Tile tl;
     int kind;
@@ -416,7 +417,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       // residual / GeLU-input operands of a chunk are read-only: their loads are issued one
       // chunk ahead (the first before the accumulator is ready) so DRAM latency overlaps the
       // MMA mainloop and the previous chunk instead of stalling each row group.
-      uint4 rn[4], hn[4];
+      // The bias (8 columns per 16-byte load, the same for every row) is prefetched the same
+      // way: loaded at its point of use, its L2 latency serialised the chunk loop.
+      uint4 rn[4], hn[4], bn[4];
       auto prefetch = [&](int ch_) {  // this lane's row, 32 columns of chunk ch_: 4 x 16 bytes
         const int mm = row0 + lane;
 #pragma unroll
@@ -426,9 +429,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           const int64_t off = tl.zo * p.c_zo + tl.zi * p.c_zi + static_cast<int64_t>(mm) * p.ldc + cc_;
           rn[it] = (ext_res && ok) ? __ldg(reinterpret_cast<const uint4*>(p.resid + off)) : make_uint4(0, 0, 0, 0);
           hn[it] = (ext_aux && ok) ? __ldg(reinterpret_cast<const uint4*>(p.aux + off)) : make_uint4(0, 0, 0, 0);
+          bn[it] = (ext_bias && cc_ < tl.N) ? __ldg(reinterpret_cast<const uint4*>(e_bias + cc_)) : make_uint4(0, 0, 0, 0);
         }
       };
-      if (ext_res || ext_aux) prefetch(half);
+      if (ext_res || ext_aux || ext_bias) prefetch(half);
       ptx::mbar_wait(&tfull[acc], acc_phase);
       if (ew == 0 && lane == 0) GPROBE(40 + 4 * gie + 0);
       ptx::tc_fence_after();
@@ -452,19 +456,16 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       const int slot_row = lq * 32 + lane;  // this thread's row of the CTA's 128
 #pragma unroll 1
       for (int ch = half; ch < NCH; ch += 2) {
-        uint4 rc[4], hc[4];
-#pragma unroll
-        for (int it = 0; it < 4; ++it) {
-          rc[it] = rn[it];
-          hc[it] = hn[it];
-        }
-        if ((ext_res || ext_aux) && ch + 2 < NCH) prefetch(ch + 2);
+        // rn / hn / bn hold this chunk's operands; the next chunk's are loaded into the same
+        // registers right after their last use below (no copies: register budget)
+        const bool pf_next = (ext_res || ext_aux || ext_bias) && ch + 2 < NCH;
         uint32_t r[32];
         if (ew == 0 && lane == 0 && gie == 0) GPROBE(100 + 10 * (ch >> 1) + 0);
         ptx::tmem_ld_32x32b_x32(tmem_base + (static_cast<uint32_t>(lq * 32) << 16) + acc * C::ACC_COLS + ch * 32, r);
         ptx::tmem_ld_wait();
         if (ew == 0 && lane == 0 && gie == 0) GPROBE(100 + 10 * (ch >> 1) + 1);
         if (kind == 2) {  // a later part of a split tile: leave the fp32 partial, no epilogue
+          if (pf_next) prefetch(ch + 2);
           float4* dst = reinterpret_cast<float4*>(
               p.sk_ws + (static_cast<size_t>(t0 * (PAIR ? 2 : 1) + cta) * BM + slot_row) * BN + ch * 32);
 #pragma unroll
@@ -489,7 +490,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           }
         }
         const int n = tl.n0 + ch * 32;
-        if (n >= tl.N || row0 >= tl.M) continue;
+        if (n >= tl.N || row0 >= tl.M) {
+          if (pf_next) prefetch(ch + 2);
+          continue;
+        }
         if (e_mode >= EPI_F32_STORE) {
           if (lane == 0) ptx::bulk_wait_read0();
           __syncwarp();
@@ -525,13 +529,12 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           const uint32_t so_s = ptx::smem_u32(so), sx_s = so_s + 2048;  // shared-window addresses
 #pragma unroll
           for (int it = 0; it < 4; ++it) {
-            const int cc = n + 8 * it;
             float x[8];
 #pragma unroll
             for (int e = 0; e < 8; ++e) x[e] = e_alpha * __uint_as_float(r[8 * it + e]);
-            if (e_bias && cc < tl.N) {
+            if (ext_bias) {  // zero beyond N (prefetch)
               float bv[8];
-              unpack8(__ldg(reinterpret_cast<const uint4*>(e_bias + cc)), bv);
+              unpack8(bn[it], bv);
 #pragma unroll
               for (int e = 0; e < 8; ++e) x[e] += bv[e];
             }
@@ -542,18 +545,19 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
               for (int e = 0; e < 8; ++e) x[e] = gelu_f(x[e]);
             } else if (e_mode == EPI_BF16_DGELU) {
               float hv[8];
-              unpack8(hc[it], hv);
+              unpack8(hn[it], hv);
 #pragma unroll
               for (int e = 0; e < 8; ++e) x[e] *= gelu_grad_f(hv[e]);
             }
             if (e_resid) {
               float rv[8];
-              unpack8(rc[it], rv);
+              unpack8(rn[it], rv);
 #pragma unroll
               for (int e = 0; e < 8; ++e) x[e] += rv[e];
             }
             st_shared_u4(so_s + soff, pack8(x));
           }
+          if (pf_next) prefetch(ch + 2);
           if (ew == 0 && lane == 0 && gie == 0) GPROBE(100 + 10 * (ch >> 1) + 4);
           ptx::fence_proxy_async_smem();
           if (ew == 0 && lane == 0 && gie == 0) GPROBE(100 + 10 * (ch >> 1) + 5);

@@ -258,7 +258,7 @@ __global__ void __launch_bounds__(256) colred_kernel(const bf16* __restrict__ a,
 #pragma unroll
       for (int g = 0; g < 32; ++g) s4[g & 3] += red[o][g][c];
       const float s = (s4[0] + s4[1]) + (s4[2] + s4[3]);
-      if (R == 1) {
+      if (part == nullptr) {  // one row chunk, not deferred: the outputs directly
         float* out = o == 0 ? out0 : (o == 1 ? out1 : out2);
         out[gcol] = accumulate ? out[gcol] + s : s;
       } else {
@@ -279,6 +279,26 @@ __global__ void __launch_bounds__(256) colred_finalize_kernel(const float* __res
   float s = 0.f;
   for (int k = 0; k < R; ++k) s += part[(static_cast<size_t>(o) * R + k) * N + c];
   float* out = o == 0 ? out0 : (o == 1 ? out1 : out2);
+  out[c] = accumulate ? out[c] + s : s;
+}
+
+// The finalize of many reductions in one launch (a whole B call's bias / LayerNorm
+// reductions, see RedBatch): thread i of the concatenated [entry][output][column] space
+// sums its column's R partials in chunk order (deterministic, as the per-reduction pass).
+__global__ void __launch_bounds__(256) colred_finalize_batch_kernel(const RedBatch b, int first, int last,
+                                                                    int accumulate) {
+  ptx::grid_dep_wait();
+  const int64_t i = b.start[first] + static_cast<int64_t>(blockIdx.x) * 256 + threadIdx.x;
+  if (i >= b.start[last]) return;
+  int e = first;
+  while (i >= b.start[e + 1]) ++e;
+  const RedEntry& r = b.e[e];
+  const int k = static_cast<int>(i - b.start[e]);
+  const int o = k / r.N, c = k % r.N;
+  const float* p = r.part + static_cast<size_t>(o) * r.R * r.N + c;
+  float s = 0.f;
+  for (int q = 0; q < r.R; ++q) s += p[static_cast<size_t>(q) * r.N];
+  float* out = r.out[o];
   out[c] = accumulate ? out[c] + s : s;
 }
 
@@ -653,7 +673,7 @@ cudaError_t ln_fwd(const bf16* x, const bf16* gamma, const bf16* beta, bf16* y, 
 
 cudaError_t ln_bwd(const bf16* dy, const bf16* x, const float* mean, const float* rstd, const bf16* gamma,
                    const bf16* resid, bf16* dx, float* dgamma, float* dbeta, float* dxsum, int accumulate, float* part,
-                   unsigned* tickets, int T, int h, cudaStream_t s) {
+                   unsigned* tickets, int T, int h, cudaStream_t s, RedBatch* defer) {
   if (h % 8 || h > 8192) return cudaErrorInvalidValue;
   if ((h + 255) / 256 > kTickets || dx == x) return cudaErrorInvalidValue;
   if (dx) {
@@ -671,14 +691,20 @@ cudaError_t ln_bwd(const bf16* dy, const bf16* x, const float* mean, const float
   const int R = colred_chunks(h);
   dim3 grid((h + CR_COLS - 1) / CR_COLS, R);
   const bool three = dx && dxsum;
+  const int NO = three ? 3 : 2;
+  if (defer) {
+    part = defer->add(R, h, NO, dgamma, dbeta, three ? dxsum : nullptr);
+    if (!part) return cudaErrorInvalidValue;
+  } else if (R == 1) {
+    part = nullptr;
+  }
   cudaError_t e = three ? launch_pdl(colred_kernel<2>, grid, dim3(256), 0, s, 1, dy, static_cast<int64_t>(h), x, mean,
                                      rstd, static_cast<const bf16*>(dx), T, h, part, dgamma, dbeta, dxsum, accumulate,
                                      tickets)
                         : launch_pdl(colred_kernel<1>, grid, dim3(256), 0, s, 1, dy, static_cast<int64_t>(h), x, mean,
                                      rstd, static_cast<const bf16*>(nullptr), T, h, part, dgamma, dbeta,
                                      static_cast<float*>(nullptr), accumulate, tickets);
-  if (e != cudaSuccess || R == 1) return e;
-  const int NO = three ? 3 : 2;
+  if (e != cudaSuccess || R == 1 || defer) return e;
   return launch_pdl(colred_finalize_kernel, dim3((h * NO + 255) / 256), dim3(256), 0, s, 1,
                     static_cast<const float*>(part), R, h, NO, dgamma, dbeta, three ? dxsum : static_cast<float*>(nullptr),
                     accumulate);
@@ -686,16 +712,50 @@ cudaError_t ln_bwd(const bf16* dy, const bf16* x, const float* mean, const float
 
 int colred_launches(int N) { return colred_chunks(N) > 1 ? 2 : 1; }
 
+size_t colred_part_floats(int N, int NO) { return static_cast<size_t>(colred_chunks(N)) * N * NO; }
+
+float* RedBatch::add(int R, int N, int NO, float* o0, float* o1, float* o2) {
+  if (n == kMaxRed) return nullptr;
+  const size_t need = static_cast<size_t>(R) * N * NO;
+  if (used + need > cap) return nullptr;
+  RedEntry& r = e[n];
+  r.part = arena + used;
+  r.out[0] = o0;
+  r.out[1] = o1;
+  r.out[2] = o2;
+  r.R = R;
+  r.N = N;
+  start[n + 1] = start[n] + static_cast<int64_t>(N) * NO;
+  used += need;
+  ++n;
+  return r.part;
+}
+
+cudaError_t colred_finalize_batch(const RedBatch& b, int accumulate, cudaStream_t s, int* launches) {
+  *launches = 0;
+  if (b.n == 0) return cudaSuccess;
+  const int64_t total = b.start[b.n];
+  const int blocks = static_cast<int>((total + 255) / 256);
+  *launches = 1;
+  return launch_pdl(colred_finalize_batch_kernel, dim3(blocks), dim3(256), 0, s, 1, b, 0, b.n, accumulate);
+}
+
 cudaError_t colsum(const bf16* a, int T, int N, int64_t ld, float* out, int accumulate, float* part,
-                   unsigned* tickets, cudaStream_t s) {
+                   unsigned* tickets, cudaStream_t s, RedBatch* defer) {
   if (N % 8 || ld % 8 || (N + 255) / 256 > kTickets) return cudaErrorInvalidValue;
   const int R = colred_chunks(N);
   dim3 grid((N + CR_COLS - 1) / CR_COLS, R);
+  if (defer) {
+    part = defer->add(R, N, 1, out, nullptr, nullptr);
+    if (!part) return cudaErrorInvalidValue;
+  } else if (R == 1) {
+    part = nullptr;
+  }
   cudaError_t e = launch_pdl(colred_kernel<0>, grid, dim3(256), 0, s, 1, a, ld, static_cast<const bf16*>(nullptr),
                              static_cast<const float*>(nullptr), static_cast<const float*>(nullptr),
                              static_cast<const bf16*>(nullptr), T, N, part, out, static_cast<float*>(nullptr),
                              static_cast<float*>(nullptr), accumulate, tickets);
-  if (e != cudaSuccess || R == 1) return e;
+  if (e != cudaSuccess || R == 1 || defer) return e;
   return launch_pdl(colred_finalize_kernel, dim3((N + 255) / 256), dim3(256), 0, s, 1, static_cast<const float*>(part),
                     R, N, 1, out, static_cast<float*>(nullptr), static_cast<float*>(nullptr), accumulate);
 }

@@ -14,6 +14,33 @@ using bf16 = __nv_bfloat16;
 constexpr int kRedChunks = 64;  // row chunks of the deterministic column reductions
 constexpr int kTickets = 256;   // column strips (256 columns each) a reduction may use
 
+// Deferred finalize of column reductions: the reductions of one B call write their
+// row-chunk partials into consecutive regions of an arena and ONE launch at the end of
+// the call adds them up (colred_finalize_batch), instead of a finalize launch each.
+constexpr int kMaxRed = 128;
+struct RedEntry {
+  float* part;    // [NO][R][N] partials
+  float* out[3];  // NO outputs (fp32 [N], overwrite or accumulate)
+  int R, N;
+};
+struct RedBatch {
+  RedEntry e[kMaxRed];
+  int64_t start[kMaxRed + 1];  // prefix of NO*N over the entries
+  int n = 0;
+  float* arena = nullptr;
+  size_t cap = 0, used = 0;  // floats
+  void reset(float* a, size_t c) {
+    arena = a;
+    cap = c;
+    used = 0;
+    n = 0;
+    start[0] = 0;
+  }
+  float* add(int R, int N, int NO, float* o0, float* o1, float* o2);  // partial region, or null if full
+};
+size_t colred_part_floats(int N, int NO);  // arena floats one reduction takes
+cudaError_t colred_finalize_batch(const RedBatch& b, int accumulate, cudaStream_t s, int* launches);
+
 // LayerNorm forward over rows of x [T, h]: y = xhat*gamma + beta; mean, rstd fp32 [T].
 cudaError_t ln_fwd(const bf16* x, const bf16* gamma, const bf16* beta, bf16* y, float* mean, float* rstd, int T,
                    int h, float eps, cudaStream_t s);
@@ -26,11 +53,11 @@ cudaError_t ln_fwd(const bf16* x, const bf16* gamma, const bf16* beta, bf16* y, 
 int colred_launches(int N);
 cudaError_t ln_bwd(const bf16* dy, const bf16* x, const float* mean, const float* rstd, const bf16* gamma,
                    const bf16* resid, bf16* dx, float* dgamma, float* dbeta, float* dxsum, int accumulate, float* part,
-                   unsigned* tickets, int T, int h, cudaStream_t s);
+                   unsigned* tickets, int T, int h, cudaStream_t s, RedBatch* defer = nullptr);
 
 // out[n] (+)= sum_t a[t, n] for a bf16 [T, N] matrix with row stride ld (bias gradients).
 cudaError_t colsum(const bf16* a, int T, int N, int64_t ld, float* out, int accumulate, float* part,
-                   unsigned* tickets, cudaStream_t s);
+                   unsigned* tickets, cudaStream_t s, RedBatch* defer = nullptr);
 
 // MSE head: dy = (y - r)/n (bf16), loss partials per block; loss = 0.5*sum/n.
 cudaError_t mse_loss(const bf16* y, const bf16* r, bf16* dy, float* part, int nparts, float* loss, int64_t n,

@@ -174,6 +174,12 @@ void carve_ws(Carver& cv, const Dims& d, Workspace* out) {
   w.dO = cv.take<bf16>(Th);
   w.dy1 = cv.take<bf16>(Th);
   w.part = cv.take<float>(3 * red);
+  // deferred reductions: the four of a layer (b1, LN2 + bo, bqkv, LN1 + b2 below) for
+  // kMaxRed / 4 layers before a flush
+  w.red_cap = (kMaxRed / 4) * (colred_part_floats(d.f, 1) + colred_part_floats(3 * d.h, 1) +
+                               2 * colred_part_floats(d.h, 3)) +
+              colred_part_floats(d.h, 1);
+  w.red = cv.take<float>(w.red_cap);
   w.tickets = cv.take<unsigned>(kTickets);
   w.loss_part = cv.take<float>(256);
   w.losses = cv.take<float>(1024);
@@ -353,10 +359,25 @@ slip_status attention_bwd(slip_ctx* c, LayerStash& ls, cudaStream_t s) {
   return attn_status(c, attn_backward(a, s), "attention backward", 2);
 }
 
-// colsum(a[T, N]) -> out (fp32, overwrite or accumulate), one launch
+// Finalize the deferred reductions of the current B call (one launch) and start a new batch.
+slip_status red_flush(slip_ctx* c, int accumulate, cudaStream_t s) {
+  int n = 0;
+  const cudaError_t e = colred_finalize_batch(c->red, accumulate, s, &n);
+  c->red.reset(c->ws.red, c->ws.red_cap);
+  return kcheck(c, e, "colred_finalize_batch", n);
+}
+
+// Make room in the batch for one reduction of NO outputs over N columns.
+slip_status red_reserve(slip_ctx* c, int N, int NO, int accumulate, cudaStream_t s) {
+  if (c->red.n < kMaxRed && c->red.used + colred_part_floats(N, NO) <= c->red.cap) return SLIP_OK;
+  return red_flush(c, accumulate, s);
+}
+
+// colsum(a[T, N]) -> out (fp32, overwrite or accumulate); the finalize is deferred to
+// the end of the B call (red_flush)
 slip_status bias_grad(slip_ctx* c, const bf16* a, int N, int64_t ld, float* out, int accumulate, cudaStream_t s) {
-  return kcheck(c, colsum(a, c->dm.T, N, ld, out, accumulate, c->ws.part, c->ws.tickets, s), "colsum",
-                colred_launches(N));
+  SLIP_TRY(red_reserve(c, N, 1, accumulate, s));
+  return kcheck(c, colsum(a, c->dm.T, N, ld, out, accumulate, c->ws.part, c->ws.tickets, s, &c->red), "colsum", 1);
 }
 
 slip_status slot_check(slip_ctx* c, int slot, int want) {
@@ -431,6 +452,7 @@ slip_status backward_input_impl(slip_ctx* c, int slot, const void* dy, void* dx,
   SlotBufs& sb = c->slots[slot];
   const size_t Th = static_cast<size_t>(D.T) * D.h;
   if (dy != sb.dy) SLIP_CUDA(cudaMemcpyAsync(sb.dy, dy, Th * sizeof(bf16), cudaMemcpyDeviceToDevice, s));
+  c->red.reset(c->ws.red, c->ws.red_cap);
   // db2 of the top layer = colsum(dy)
   SLIP_TRY(bias_grad(c, sb.dy, D.h, D.h, layer_g(c, c->L - 1).b2, accumulate, s));
   for (int l = c->L - 1; l >= 0; --l) {
@@ -443,10 +465,11 @@ slip_status backward_input_impl(slip_ctx* c, int slot, const void* dy, void* dx,
     // dY2 = dH W1
     SLIP_TRY(linear_dx(c, ls.dh, Wt.w1, D.f, D.h, c->ws.dy2, EPI_BF16, nullptr, s));
     // LN2 backward + residual: dX2 = dOut + LN2'(dY2); dgamma2, dbeta2, dbo = colsum(dX2)
+    SLIP_TRY(red_reserve(c, D.h, 3, accumulate, s));
     SLIP_TRY(kcheck(c,
                     ln_bwd(c->ws.dy2, ls.x2, ls.mean2, ls.rstd2, Wt.g2, ls.dout, ls.dx2, G.g2, G.b2n, G.bo, accumulate,
-                           c->ws.part, c->ws.tickets, D.T, D.h, s),
-                    "ln_bwd 2", 1 + colred_launches(D.h)));
+                           c->ws.part, c->ws.tickets, D.T, D.h, s, &c->red),
+                    "ln_bwd 2", 2));
     // dO = dX2 Wo
     SLIP_TRY(linear_dx(c, ls.dx2, Wt.wo, D.h, D.h, c->ws.dO, EPI_BF16, nullptr, s));
     SLIP_TRY(attention_bwd(c, ls, s));
@@ -457,11 +480,13 @@ slip_status backward_input_impl(slip_ctx* c, int slot, const void* dy, void* dx,
     // with the embedding end the input gradient always lands in the slot (W's scatter reads it)
     bf16* dxl = l > 0 ? sb.layer[l - 1].dout : ((D.ends & 1) ? sb.dx : static_cast<bf16*>(dx));
     float* dxsum = l > 0 ? layer_g(c, l - 1).b2 : nullptr;
+    SLIP_TRY(red_reserve(c, D.h, 3, accumulate, s));
     SLIP_TRY(kcheck(c,
                     ln_bwd(c->ws.dy1, ls.xin, ls.mean1, ls.rstd1, Wt.g1, ls.dx2, dxl, G.g1, G.b1n, dxl ? dxsum : nullptr,
-                           accumulate, c->ws.part, c->ws.tickets, D.T, D.h, s),
-                    "ln_bwd 1", (dxl ? 1 : 0) + colred_launches(D.h)));
+                           accumulate, c->ws.part, c->ws.tickets, D.T, D.h, s, &c->red),
+                    "ln_bwd 1", (dxl ? 1 : 0) + 1));
   }
+  SLIP_TRY(red_flush(c, accumulate, s));
   if ((D.ends & 1) && dx && dx != sb.dx)
     SLIP_CUDA(cudaMemcpyAsync(dx, sb.dx, Th * sizeof(bf16), cudaMemcpyDeviceToDevice, s));
   return SLIP_OK;

@@ -8,6 +8,7 @@
 #include <vector>
 
 #include "../../include/slip.h"
+#include "kernels.cuh"
 
 namespace slip {
 
@@ -56,6 +57,8 @@ struct Workspace {
   float* losses;     // [1024] per-micro-batch losses (executor)
   int32_t* nonfinite;  // [1] post-step validation flag (executor)
   int32_t* vflags;     // [8] validated mode: own_bad[2], global_bad[2] (per iteration parity), rollbacks
+  float* red;          // deferred column-reduction partials of a B call (RedBatch arena)
+  size_t red_cap;      // floats
   float* sk_ws;        // stream-K fp32 partials of the F / B linears (gemm_sk_bytes)
   unsigned* sk_flags;  // [num_sms] stream-K partial epochs
 };
@@ -92,6 +95,7 @@ struct slip_ctx {
   bool bound = false;
   std::vector<slip::SlotBufs> slots;
   slip::Workspace ws{};
+  slip::RedBatch red;  // B's bias / LayerNorm reductions, finalized in one launch
   std::vector<int> state;
   int64_t launches = 0;  // kernels enqueued through this context
   int64_t opt_step = 0;  // AdamW steps taken by the executor

@@ -11,20 +11,43 @@ namespace slip {
 void gemm_probe_read(long long* out, int n);
 }
 
+__global__ void fill(__nv_bfloat16* p, size_t n, unsigned seed) {
+  for (size_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += size_t(gridDim.x) * blockDim.x) {
+    unsigned h = (unsigned)i * 2654435761u ^ seed;
+    h ^= h >> 13;
+    h *= 0x5bd1e995u;
+    h ^= h >> 15;
+    p[i] = __float2bfloat16(((h & 0xFFFF) / 65536.0f - 0.5f) * 0.1f);
+  }
+}
+
+// usage: gemm_probe [K] [random 0/1] [resid+bias 0/1] [b_mn_major 0/1] [N]
 int main(int argc, char** argv) {
-  const int M = 2048, N = 2048, K = argc > 1 ? atoi(argv[1]) : 2048;
+  const int M = 2048, K = argc > 1 ? atoi(argv[1]) : 2048;
+  const int rnd = argc > 2 ? atoi(argv[2]) : 0, res = argc > 3 ? atoi(argv[3]) : 0;
+  const int bmn = argc > 4 ? atoi(argv[4]) : 0, N = argc > 5 ? atoi(argv[5]) : 2048;
   __nv_bfloat16 *a, *b, *c;
   cudaMalloc(&a, size_t(M) * K * 2);
   cudaMalloc(&b, size_t(N) * K * 2);
   cudaMalloc(&c, size_t(M) * N * 2);
   cudaMemset(a, 0, size_t(M) * K * 2);
   cudaMemset(b, 0, size_t(N) * K * 2);
+  __nv_bfloat16 *r, *bias;
+  cudaMalloc(&r, size_t(M) * N * 2);
+  cudaMalloc(&bias, size_t(N) * 2);
+  cudaMemset(r, 0, size_t(M) * N * 2);
+  cudaMemset(bias, 0, size_t(N) * 2);
+  if (rnd) {
+    fill<<<1184, 256>>>(a, size_t(M) * K, 1);
+    fill<<<1184, 256>>>(b, size_t(N) * K, 2);
+    fill<<<1184, 256>>>(r, size_t(M) * N, 3);
+  }
   float* ws;
   unsigned* flags;
   cudaMalloc(&ws, slip::gemm_sk_bytes());
   cudaMalloc(&flags, 4096);
   cudaMemset(flags, 0, 4096);
-  for (int sk = 0; sk < 2; ++sk) {
+  for (int sk = 0; sk < 1; ++sk) {
     slip::GemmDesc d;
     d.M = M;
     d.N = N;
@@ -33,7 +56,12 @@ int main(int argc, char** argv) {
     d.a.ptr = a;
     d.a.ld = K;
     d.b.ptr = b;
-    d.b.ld = K;
+    d.b.ld = bmn ? N : K;
+    d.b.mn_major = bmn != 0;
+    if (res) {
+      d.resid = r;
+      d.bias = bias;
+    }
     d.c = c;
     d.ldc = N;
     d.mode = slip::EPI_BF16;
@@ -51,10 +79,14 @@ int main(int argc, char** argv) {
     cudaEventSynchronize(e1);
     float ms;
     cudaEventElapsedTime(&ms, e0, e1);
-    printf("K=%d sk=%d: %.2f us (%s)\n", K, sk, ms * 1000 / 50, cudaGetErrorString(cudaGetLastError()));
     std::vector<long long> p(4096);
     slip::gemm_probe_read(p.data(), 4096);
     const long long t0 = p[0];
+    long long tend = 0;
+    for (int i = 0; i < 4; ++i)
+      if (p[42 + 4 * i] > tend) tend = p[42 + 4 * i];
+    printf("M=%d N=%d K=%d rnd=%d res=%d bmn=%d sk=%d: %.2f us, CTA0 %lld cycles (%s)\n", M, N, K, rnd, res, bmn, sk,
+           ms * 1000 / 50, tend - t0, cudaGetErrorString(cudaGetLastError()));
     printf("  mma item start / acc free / committed:");
     for (int i = 0; i < 4; ++i)
       if (p[10 + i]) printf(" [%lld %lld %lld]", p[10 + i] - t0, p[20 + i] - t0, p[30 + i] - t0);

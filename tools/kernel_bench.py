@@ -27,6 +27,8 @@ def main():
     ap.add_argument("--reps", type=int, default=10)
     ap.add_argument("--once", action="store_true")
     ap.add_argument("--no-sk", action="store_true", help="disable stream-K for the F / B linears")
+    ap.add_argument("--profile", action="store_true",
+                    help="per-kernel live durations (torch.profiler / CUPTI, warm caches) of --reps steps")
     a = ap.parse_args()
     cfg = CFGS[a.cfg]
     L = a.layers
@@ -51,6 +53,28 @@ def main():
     if a.once:
         step()
         torch.cuda.synchronize()
+        return
+    if a.profile:
+        from torch.profiler import ProfilerActivity, profile
+        with profile(activities=[ProfilerActivity.CUDA]) as prof:
+            for _ in range(a.reps):
+                step()
+            torch.cuda.synchronize()
+        ev = [e for e in prof.events() if e.device_type.name == "CUDA"]
+        seq = []  # kernels of the last step in launch order
+        per = len(ev) // a.reps
+        for e in ev[-per:]:
+            seq.append((e.name, e.device_time if hasattr(e, "device_time") else e.cuda_time))
+        tot = {}
+        for e in ev:
+            d = e.device_time if hasattr(e, "device_time") else e.cuda_time
+            k = e.name.split("(")[0][:60]
+            tot[k] = tot.get(k, 0.0) + d
+        import re
+        for name, d in seq:
+            short = re.sub(r"^void |slip::|\(anonymous namespace\)::|<unnamed>::", "", name).split("(")[0]
+            print(f"{d:9.1f} us  {short[:90]}")
+        print("total per step (us):", round(sum(tot.values()) / a.reps, 1))
         return
     ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
     tf = tb = tw = 0.0
