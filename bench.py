@@ -390,6 +390,46 @@ def main():
             traffic = json.load(f).get("dram_bytes_per_launch")
     except Exception:
         pass
+    if os.environ.get("SLIP_BENCH_PROFILE") and rank == 0:
+        # diagnostic (outside the timed region): per-kernel CUPTI durations of one step
+        import re
+        from torch.profiler import ProfilerActivity, profile
+        with profile(activities=[ProfilerActivity.CUDA]) as prof:
+            execute(1)
+            torch.cuda.synchronize()
+        tot, cnt = {}, {}
+        for e in prof.events():
+            if e.device_type.name != "CUDA":
+                continue
+            k = re.sub(r"^void |slip::|\(anonymous namespace\)::|<unnamed>::", "", e.name).split("(")[0][:60]
+            d = e.device_time if hasattr(e, "device_time") else e.cuda_time
+            tot[k] = tot.get(k, 0.0) + d
+            cnt[k] = cnt.get(k, 0) + 1
+        for k in sorted(tot, key=lambda k: -tot[k]):
+            print(f"PROFILE {tot[k] / 1e3:9.3f} ms {cnt[k]:6d} x {tot[k] / cnt[k]:8.1f} us  {k}", file=sys.stderr)
+        # idle gaps between consecutive device activities, by (previous -> next) kernel
+        kev = []
+        for e in prof.events():
+            if e.device_type.name != "CUDA":
+                continue
+            k = re.sub(r"^void |slip::|\(anonymous namespace\)::|<unnamed>::", "", e.name).split("(")[0][:40]
+            t0 = e.time_range.start
+            kev.append((t0, t0 + (e.device_time if hasattr(e, "device_time") else e.cuda_time), k))
+        kev.sort()
+        gaps, gcnt = {}, {}
+        end = None
+        prev = None
+        for t0, t1, k in kev:
+            if end is not None and t0 > end:
+                key = f"{prev} -> {k}"
+                gaps[key] = gaps.get(key, 0.0) + (t0 - end)
+                gcnt[key] = gcnt.get(key, 0) + 1
+            if end is None or t1 > end:
+                end, prev = t1, k
+        print(f"PROFILE span {(kev[-1][1] - kev[0][0]) / 1e3:.3f} ms, idle {sum(gaps.values()) / 1e3:.3f} ms",
+              file=sys.stderr)
+        for k in sorted(gaps, key=lambda k: -gaps[k])[:15]:
+            print(f"PROFILE gap {gaps[k] / 1e3:8.3f} ms {gcnt[k]:6d} x {gaps[k] / gcnt[k]:7.1f} us  {k}", file=sys.stderr)
     if args.trace:
         # plan-vs-execution timeline (outside the timed region)
         rt.set_trace(stage, True)

@@ -77,6 +77,8 @@ struct KParams {
   // stream-K (see GemmDesc)
   int sk;              // 1: stream-K decomposition over sk_units CTA pairs
   int sk_units;
+  int sk_dp;           // hybrid: tiles [0, sk_dp) whole and round-robin, AFTER each unit's share
+                       // of the stream-K k-space, which covers tiles [sk_dp, sk_dp + sk_iters / nkb)
   int64_t sk_iters;    // total * nkb
   float* sk_ws;        // [2 * sk_units][BM][BN] fp32 partials (slot = pair * 2 + cta)
   unsigned* sk_flags;  // [2 * sk_units] = sk_epoch once the slot's partial is written
@@ -162,12 +164,18 @@ __device__ __forceinline__ bool next_item(const KParams& p, int u, int tstep, It
     st.t += tstep;
     return true;
   }
-  if (st.it >= st.end) return false;
+  if (st.it >= st.end) {  // the share is done: whole tiles of the data-parallel part
+    if (st.t >= p.sk_dp) return false;
+    tl = decode_tile<BN, TM>(st.t, p);
+    kind = 0;
+    st.t += tstep;
+    return true;
+  }
   const int t = static_cast<int>(st.it / p.nkb);
   const int kb0 = static_cast<int>(st.it - static_cast<int64_t>(t) * p.nkb);
   const int64_t rem = st.end - st.it;
   const int kb1 = rem < p.nkb - kb0 ? kb0 + static_cast<int>(rem) : p.nkb;
-  tl = decode_tile<BN, TM>(t, p);
+  tl = decode_tile<BN, TM>(p.sk_dp + t, p);
   tl.kb0 = kb0;
   tl.kb1 = kb1;
   kind = (kb0 == 0 && kb1 == p.nkb) ? 0 : (kb0 == 0 ? 1 : 2);
@@ -440,7 +448,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       // stream-K: the later parts of this tile (at the start of the next pairs' shares)
       int q_end = t0 + 1;
       if (kind == 1) {
-        while (q_end < p.sk_units && sk_start(p, q_end) < static_cast<int64_t>(tl.t + 1) * p.nkb) ++q_end;
+        while (q_end < p.sk_units && sk_start(p, q_end) < static_cast<int64_t>(tl.t - p.sk_dp + 1) * p.nkb) ++q_end;
         if (ew == 0 && lane == 0)
           for (int q = t0 + 1; q < q_end; ++q) {
             if (sk_start(p, q) == sk_start(p, q + 1)) continue;  // empty share: no partial
@@ -453,7 +461,6 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         ptx::named_bar_sync(1, 32 * EPI_WARPS);
       }
       if (ew == 0 && lane == 0) GPROBE(40 + 4 * gie + 1);
-      const int slot_row = lq * 32 + lane;  // this thread's row of the CTA's 128
 #pragma unroll 1
       for (int ch = half; ch < NCH; ch += 2) {
         // rn / hn / bn hold this chunk's operands; the next chunk's are loaded into the same
@@ -466,22 +473,25 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         if (ew == 0 && lane == 0 && gie == 0) GPROBE(100 + 10 * (ch >> 1) + 1);
         if (kind == 2) {  // a later part of a split tile: leave the fp32 partial, no epilogue
           if (pf_next) prefetch(ch + 2);
-          float4* dst = reinterpret_cast<float4*>(
-              p.sk_ws + (static_cast<size_t>(t0 * (PAIR ? 2 : 1) + cta) * BM + slot_row) * BN + ch * 32);
+          // partial layout [lane quarter][chunk][8][lane] float4: each store instruction of
+          // the warp writes 512 contiguous bytes (the fix-up reads it back the same way)
+          float4* dst = reinterpret_cast<float4*>(p.sk_ws + static_cast<size_t>(t0 * (PAIR ? 2 : 1) + cta) * BM * BN) +
+                        (lq * NCH + ch) * 8 * 32 + lane;
 #pragma unroll
           for (int j = 0; j < 8; ++j)
-            dst[j] = make_float4(__uint_as_float(r[4 * j]), __uint_as_float(r[4 * j + 1]),
+            dst[j * 32] = make_float4(__uint_as_float(r[4 * j]), __uint_as_float(r[4 * j + 1]),
                                  __uint_as_float(r[4 * j + 2]), __uint_as_float(r[4 * j + 3]));
           continue;
         }
         if (kind == 1) {  // first part: add the later parts' partials in pair order
           for (int q = t0 + 1; q < q_end; ++q) {
             if (sk_start(p, q) == sk_start(p, q + 1)) continue;
-            const float4* src = reinterpret_cast<const float4*>(
-                p.sk_ws + (static_cast<size_t>(q * (PAIR ? 2 : 1) + cta) * BM + slot_row) * BN + ch * 32);
+            const float4* src =
+                reinterpret_cast<const float4*>(p.sk_ws + static_cast<size_t>(q * (PAIR ? 2 : 1) + cta) * BM * BN) +
+                (lq * NCH + ch) * 8 * 32 + lane;
 #pragma unroll
             for (int j = 0; j < 8; ++j) {
-              const float4 v = __ldcg(src + j);
+              const float4 v = __ldcg(src + j * 32);
               r[4 * j] = __float_as_uint(__uint_as_float(r[4 * j]) + v.x);
               r[4 * j + 1] = __float_as_uint(__uint_as_float(r[4 * j + 1]) + v.y);
               r[4 * j + 2] = __float_as_uint(__uint_as_float(r[4 * j + 2]) + v.z);
@@ -752,14 +762,19 @@ cudaError_t launch_t(const GemmDesc& d, cudaStream_t s, const GroupEntry* groups
   p.aux = static_cast<__nv_bfloat16*>(d.aux);
   p.alpha = d.alpha;
   p.accumulate = d.accumulate;
-  // stream-K when the tiles leave a partial last wave of CTA pairs (see GemmDesc)
+  // Hybrid stream-K when the tiles leave a partial last wave of CTA pairs (see GemmDesc):
+  // the whole waves stay data-parallel, the remainder's tile x k-block iterations are
+  // shared evenly, and each pair runs its share FIRST so that the split tiles' epilogues
+  // (partials, fix-up) overlap its whole tiles' mainloops; only one-wave-or-more GEMMs.
   const int units = PAIR ? sm_budget() / 2 : sm_budget();
+  const int rem_tiles = p.total % units;
   if (PAIR && d.sk_ws && d.sk_flags && d.mode < EPI_F32_STORE && d.causal == CAUSAL_NONE && d.zi_count == 1 &&
-      d.zo_count == 1 && p.total % units != 0 && p.total < 4 * units && p.nkb >= 8) {
+      d.zo_count == 1 && p.total > units && rem_tiles != 0 && rem_tiles * p.nkb >= 4 * units) {
     static std::atomic<unsigned> epoch{0};
     p.sk = 1;
     p.sk_units = units;
-    p.sk_iters = static_cast<int64_t>(p.total) * p.nkb;
+    p.sk_dp = p.total - rem_tiles;
+    p.sk_iters = static_cast<int64_t>(rem_tiles) * p.nkb;
     p.sk_ws = d.sk_ws;
     p.sk_flags = d.sk_flags;
     p.sk_epoch = epoch.fetch_add(1) + 1;

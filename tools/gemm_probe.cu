@@ -21,7 +21,7 @@ __global__ void fill(__nv_bfloat16* p, size_t n, unsigned seed) {
   }
 }
 
-// usage: gemm_probe [K] [random 0/1] [resid+bias 0/1] [b_mn_major 0/1] [N]
+// usage: gemm_probe [K] [random 0/1] [resid+bias 0/1] [b_mn_major 0/1] [N] [also stream-K 0/1]
 int main(int argc, char** argv) {
   const int M = 2048, K = argc > 1 ? atoi(argv[1]) : 2048;
   const int rnd = argc > 2 ? atoi(argv[2]) : 0, res = argc > 3 ? atoi(argv[3]) : 0;
@@ -47,7 +47,8 @@ int main(int argc, char** argv) {
   cudaMalloc(&ws, slip::gemm_sk_bytes());
   cudaMalloc(&flags, 4096);
   cudaMemset(flags, 0, 4096);
-  for (int sk = 0; sk < 1; ++sk) {
+  const int sk_max = argc > 6 ? atoi(argv[6]) : 0;
+  for (int sk = 0; sk <= sk_max; ++sk) {
     slip::GemmDesc d;
     d.M = M;
     d.N = N;

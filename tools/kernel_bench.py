@@ -27,6 +27,7 @@ def main():
     ap.add_argument("--reps", type=int, default=10)
     ap.add_argument("--once", action="store_true")
     ap.add_argument("--no-sk", action="store_true", help="disable stream-K for the F / B linears")
+    ap.add_argument("--sk", action="store_true", help="enable (hybrid) stream-K for the F / B linears")
     ap.add_argument("--profile", action="store_true",
                     help="per-kernel live durations (torch.profiler / CUPTI, warm caches) of --reps steps")
     a = ap.parse_args()
@@ -35,6 +36,8 @@ def main():
     st = rt.Stage(cfg, L, n_slots=1)
     if a.no_sk:
         rt.call("slip_set_stream_k", st.ctx, 0)
+    if a.sk:
+        rt.call("slip_set_stream_k", st.ctx, 1)
     rt.init_master_(st.master, cfg, L, cfg.layers)
     rt.call("slip_weights_from_master", st.ctx, rt._stream())
     T, h, f = cfg.tokens, cfg.hidden, cfg.ffn
