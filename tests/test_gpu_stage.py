@@ -118,6 +118,32 @@ def test_accumulation_over_microbatches():
         assert relerr(got[0][n], ref[0][n]) <= GATE_A, n
 
 
+def test_stream_k_stage_matches_oracle():
+    """The hybrid stream-K linears (slip_set_stream_k, off by default): a shape whose QKV
+    (96 pair tiles) and FC1 (128) GEMMs leave a partial last wave of the 74 CTA pairs, so
+    split tiles are finished from other pairs' fp32 partials."""
+    rt = _rt()
+    cfg = sd.ModelCfg(hidden=1024, heads=8, ffn=4096, seq=1024, micro_batch=2, layers=1)
+    layers = sd.stage_params(cfg, 0, 1, total_layers=2)
+    st = rt.Stage(cfg, 1, n_slots=1)
+    rt.call("slip_set_stream_k", st.ctx, 1)
+    st.load_master(torch.from_numpy(sd.pack_stage(layers)).float().cuda())
+    x, r = sd.stage_input(cfg, 0, 0), sd.stage_target(cfg, 0, 0)
+    y = torch.empty(cfg.tokens, cfg.hidden, dtype=torch.bfloat16, device="cuda")
+    dx = torch.empty_like(y)
+    st.forward(0, to_dev_bf16(x), y)
+    st.backward_input(0, to_dev_bf16(r), dx, accumulate=False)
+    st.backward_weight(0, accumulate=False)
+    torch.cuda.synchronize()
+    out, caches = OL.stage_forward(layers, x, cfg)
+    dxr, grads = OL.stage_backward_coupled(layers, caches, r, cfg)
+    assert relerr(to_np(y), out) <= GATE_A
+    assert relerr(to_np(dx), dxr) <= GATE_A
+    g = sd.unpack_stage(st.grad.cpu().numpy().astype(np.float64), cfg, 1)
+    for n in sd.PARAM_ORDER:
+        assert relerr(g[0][n], grads[0][n]) <= GATE_A, n
+
+
 def test_slot_state_machine():
     rt = _rt()
     cfg = sd.C1_TINY
