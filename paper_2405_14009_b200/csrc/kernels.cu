@@ -73,18 +73,27 @@ __global__ void __launch_bounds__(256) ln_fwd_kernel(const bf16* __restrict__ x,
                                                      const bf16* __restrict__ beta, bf16* __restrict__ y,
                                                      float* __restrict__ mean, float* __restrict__ rstd, int T, int h,
                                                      float eps) {
+  // gamma / beta staged in smem by the whole block while the rows load (one latency, not
+  // two; the 8 rows of the block share them)
+  __shared__ uint4 gb[2][VPL * 32];
   ptx::grid_dep_wait();
   const int lane = threadIdx.x & 31;
   const int row = blockIdx.x * LN_ROWS + (threadIdx.x >> 5);
-  if (row >= T) return;
   const int nv = h >> 3;
-  const uint4* xr = reinterpret_cast<const uint4*>(x + static_cast<size_t>(row) * h);
+  for (int i = threadIdx.x; i < nv; i += 256) {
+    gb[0][i] = __ldg(reinterpret_cast<const uint4*>(gamma) + i);
+    gb[1][i] = __ldg(reinterpret_cast<const uint4*>(beta) + i);
+  }
   uint4 raw[VPL];
+  const bool live = row < T;
+  const uint4* xr = reinterpret_cast<const uint4*>(x + static_cast<size_t>(live ? row : 0) * h);
 #pragma unroll
   for (int i = 0; i < VPL; ++i) {
     const int idx = lane + 32 * i;
-    raw[i] = idx < nv ? xr[idx] : make_uint4(0, 0, 0, 0);
+    raw[i] = (live && idx < nv) ? xr[idx] : make_uint4(0, 0, 0, 0);
   }
+  __syncthreads();
+  if (!live) return;
   float sum = 0.f;
 #pragma unroll
   for (int i = 0; i < VPL; ++i) {
@@ -112,8 +121,8 @@ __global__ void __launch_bounds__(256) ln_fwd_kernel(const bf16* __restrict__ x,
     if (idx < nv) {
       float v[8], g[8], b[8], o[8];
       unpack8(raw[i], v);
-      unpack8(reinterpret_cast<const uint4*>(gamma)[idx], g);
-      unpack8(reinterpret_cast<const uint4*>(beta)[idx], b);
+      unpack8(gb[0][idx], g);
+      unpack8(gb[1][idx], b);
 #pragma unroll
       for (int e = 0; e < 8; ++e) o[e] = (v[e] - mu) * rs * g[e] + b[e];
       yr[idx] = pack8(o);
@@ -188,6 +197,58 @@ __global__ void __launch_bounds__(256) ln_bwd_rows_kernel(const bf16* __restrict
   }
 }
 
+// ------------------------------------------------------------------ LayerNorm bwd (row statistics)
+// One warp per row: stat[row] = (sum_c g, sum_c g xhat), g = dy gamma — the two row sums
+// the column pass (colred MODE 3 / 4) needs; reads dy and x only.
+template <int VPL>
+__global__ void __launch_bounds__(256) ln_bwd_stats_kernel(const bf16* __restrict__ dy, const bf16* __restrict__ x,
+                                                           const float* __restrict__ mean,
+                                                           const float* __restrict__ rstd,
+                                                           const bf16* __restrict__ gamma, float2* __restrict__ stat,
+                                                           int T, int h) {
+  __shared__ uint4 gs[VPL * 32];  // gamma, staged by the block while the rows load (as ln_fwd)
+  ptx::grid_dep_wait();
+  const int lane = threadIdx.x & 31;
+  const int row = blockIdx.x * LN_ROWS + (threadIdx.x >> 5);
+  const int nv = h >> 3;
+  for (int i = threadIdx.x; i < nv; i += 256) gs[i] = __ldg(reinterpret_cast<const uint4*>(gamma) + i);
+  const bool live = row < T;
+  const int rr = live ? row : 0;
+  const float mu = mean[rr], rs = rstd[rr];
+  const uint4* xr = reinterpret_cast<const uint4*>(x + static_cast<size_t>(rr) * h);
+  const uint4* dyr = reinterpret_cast<const uint4*>(dy + static_cast<size_t>(rr) * h);
+  uint4 xv[VPL], dv[VPL];
+#pragma unroll
+  for (int i = 0; i < VPL; ++i) {
+    const int idx = lane + 32 * i;
+    const bool ok = live && idx < nv;
+    xv[i] = ok ? xr[idx] : make_uint4(0, 0, 0, 0);
+    dv[i] = ok ? dyr[idx] : make_uint4(0, 0, 0, 0);
+  }
+  __syncthreads();
+  if (!live) return;
+  float s1 = 0.f, s2 = 0.f;
+#pragma unroll
+  for (int i = 0; i < VPL; ++i) {
+    const int idx = lane + 32 * i;
+    if (idx < nv) {
+      float a[8], d[8], gm[8];
+      unpack8(xv[i], a);
+      unpack8(dv[i], d);
+      unpack8(gs[idx], gm);
+#pragma unroll
+      for (int e = 0; e < 8; ++e) {
+        const float g = d[e] * gm[e];
+        s1 += g;
+        s2 += g * ((a[e] - mu) * rs);
+      }
+    }
+  }
+  s1 = warp_sum(s1);
+  s2 = warp_sum(s2);
+  if (lane == 0) stat[row] = make_float2(s1, s2);
+}
+
 // ------------------------------------------------------------------ column reductions
 // One block per 64-column strip covering ALL T rows: 256 threads = 8 column vectors
 // (16 bytes each) x 32 row groups; thread (cv, rg) sums rows rg, rg+32, ... of its 8
@@ -196,15 +257,25 @@ __global__ void __launch_bounds__(256) ln_bwd_rows_kernel(const bf16* __restrict
 // MODE 0: out0 (+)= sum_t a.
 // MODE 1 (LayerNorm): out0 (+)= sum dy*xhat, out1 (+)= sum dy       (a = dy)
 // MODE 2 (LayerNorm + producer bias): MODE 1 and out2 (+)= sum_t dx (dx = the LN input grad)
+// MODE 3 / 4 (the whole LayerNorm backward, row statistics from the producing GEMM's
+// epilogue, GemmDesc::ln_stat): writes dx = resid + rstd (dy gamma - mean_h(g) -
+// xhat mean_h(g xhat)) and reduces like MODE 2 (3) or MODE 1 (4).
 constexpr int CR_COLS = 64;
+struct LnCols {
+  const bf16* gamma;
+  const bf16* resid;
+  bf16* dx;
+  const float2* stat;  // [T][nparts] (sum g, sum g xhat)
+  int nparts;
+};
 template <int MODE>
 __global__ void __launch_bounds__(256) colred_kernel(const bf16* __restrict__ a, int64_t ld, const bf16* __restrict__ x,
                                                      const float* __restrict__ mean, const float* __restrict__ rstd,
                                                      const bf16* __restrict__ dx, int T, int N, float* part,
                                                      float* __restrict__ out0, float* __restrict__ out1,
                                                      float* __restrict__ out2, int accumulate,
-                                                     unsigned* __restrict__ tickets) {
-  constexpr int NO = MODE == 0 ? 1 : (MODE == 1 ? 2 : 3);  // outputs
+                                                     unsigned* __restrict__ tickets, const LnCols lc) {
+  constexpr int NO = MODE == 0 ? 1 : ((MODE == 1 || MODE == 4) ? 2 : 3);  // outputs
   __shared__ float red[NO][32][CR_COLS + 1];
   (void)tickets;
   ptx::grid_dep_wait();
@@ -219,7 +290,61 @@ __global__ void __launch_bounds__(256) colred_kernel(const bf16* __restrict__ a,
   for (int o = 0; o < NO; ++o)
 #pragma unroll
     for (int e = 0; e < 8; ++e) acc[o][e] = 0.f;
-  if (col < N) {
+  if (MODE >= 3 && col < N) {
+    // the whole LayerNorm backward: rows in batches of LB per thread, every load of a
+    // batch (dy, x, resid, the row statistics) issued before any of its dx stores
+    constexpr int LB = 4;
+    float gm[8];
+    unpack8(__ldg(reinterpret_cast<const uint4*>(lc.gamma + col)), gm);
+    for (int rb = r0 + rg; rb < r1; rb += 32 * LB) {
+      uint4 dq[LB], xq[LB], rq[LB];
+      float s1[LB], s2[LB];
+#pragma unroll
+      for (int b = 0; b < LB; ++b) {
+        const int r = rb + 32 * b;
+        const bool ok = r < r1;
+        const size_t o = static_cast<size_t>(ok ? r : r0) * N + col;
+        dq[b] = ok ? __ldg(reinterpret_cast<const uint4*>(a + static_cast<size_t>(r) * ld + col)) : make_uint4(0, 0, 0, 0);
+        xq[b] = ok ? __ldg(reinterpret_cast<const uint4*>(x + o)) : make_uint4(0, 0, 0, 0);
+        rq[b] = (ok && lc.resid) ? __ldg(reinterpret_cast<const uint4*>(lc.resid + o)) : make_uint4(0, 0, 0, 0);
+        s1[b] = 0.f;
+        s2[b] = 0.f;
+        if (ok) {  // the row's statistics: parts in index order
+          const float2* st = lc.stat + static_cast<size_t>(r) * lc.nparts;
+          for (int q = 0; q < lc.nparts; ++q) {
+            const float2 w = __ldg(st + q);
+            s1[b] += w.x;
+            s2[b] += w.y;
+          }
+        }
+      }
+#pragma unroll
+      for (int b = 0; b < LB; ++b) {
+        const int r = rb + 32 * b;
+        if (r >= r1) break;
+        float v[8], xv[8], rv[8], o[8];
+        unpack8(dq[b], v);
+        unpack8(xq[b], xv);
+        unpack8(rq[b], rv);
+        const float mg = s1[b] / N, mgx = s2[b] / N, mu = __ldg(mean + r), rs = __ldg(rstd + r);
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+          const float xh = (xv[e] - mu) * rs;
+          o[e] = rv[e] + rs * (v[e] * gm[e] - mg - xh * mgx);
+          acc[0][e] += v[e] * xh;
+          acc[1][e] += v[e];
+        }
+        const uint4 packed = pack8(o);
+        *reinterpret_cast<uint4*>(lc.dx + static_cast<size_t>(r) * N + col) = packed;
+        if (MODE == 3) {
+          float gv[8];
+          unpack8(packed, gv);
+#pragma unroll
+          for (int e = 0; e < 8; ++e) acc[2][e] += gv[e];
+        }
+      }
+    }
+  } else if (col < N) {
 #pragma unroll 4
     for (int r = r0 + rg; r < r1; r += 32) {
       float v[8];
@@ -303,9 +428,9 @@ __global__ void __launch_bounds__(256) colred_finalize_batch_kernel(const RedBat
 }
 
 // Row chunks so that a reduction fills the GPU: about 2 blocks per SM.
-int colred_chunks(int N) {
+int colred_chunks(int N, int per_sm) {
   const int strips = (N + CR_COLS - 1) / CR_COLS;
-  int R = (2 * 148 + strips - 1) / strips;
+  int R = (per_sm * 148) / strips;  // whole blocks fit one wave at per_sm resident blocks per SM
   if (R > kRedChunks) R = kRedChunks;
   return R < 1 ? 1 : R;
 }
@@ -688,7 +813,7 @@ cudaError_t ln_bwd(const bf16* dy, const bf16* x, const float* mean, const float
 #undef X
     if (e != cudaSuccess) return e;
   }
-  const int R = colred_chunks(h);
+  const int R = colred_chunks(h, 4);
   dim3 grid((h + CR_COLS - 1) / CR_COLS, R);
   const bool three = dx && dxsum;
   const int NO = three ? 3 : 2;
@@ -700,19 +825,62 @@ cudaError_t ln_bwd(const bf16* dy, const bf16* x, const float* mean, const float
   }
   cudaError_t e = three ? launch_pdl(colred_kernel<2>, grid, dim3(256), 0, s, 1, dy, static_cast<int64_t>(h), x, mean,
                                      rstd, static_cast<const bf16*>(dx), T, h, part, dgamma, dbeta, dxsum, accumulate,
-                                     tickets)
+                                     tickets, LnCols{})
                         : launch_pdl(colred_kernel<1>, grid, dim3(256), 0, s, 1, dy, static_cast<int64_t>(h), x, mean,
                                      rstd, static_cast<const bf16*>(nullptr), T, h, part, dgamma, dbeta,
-                                     static_cast<float*>(nullptr), accumulate, tickets);
+                                     static_cast<float*>(nullptr), accumulate, tickets, LnCols{});
   if (e != cudaSuccess || R == 1 || defer) return e;
   return launch_pdl(colred_finalize_kernel, dim3((h * NO + 255) / 256), dim3(256), 0, s, 1,
                     static_cast<const float*>(part), R, h, NO, dgamma, dbeta, three ? dxsum : static_cast<float*>(nullptr),
                     accumulate);
 }
 
-int colred_launches(int N) { return colred_chunks(N) > 1 ? 2 : 1; }
+cudaError_t ln_bwd2(const bf16* dy, const bf16* x, const float* mean, const float* rstd, const bf16* gamma,
+                    const bf16* resid, bf16* dx, float* stat, float* dgamma, float* dbeta, float* dxsum, int accumulate,
+                    float* part, int T, int h, cudaStream_t s, RedBatch* defer) {
+  if (h % 8 || h > 8192 || !dx || dx == x || dx == dy || !stat) return cudaErrorInvalidValue;
+  {
+    const int v = ln_vpl(h);
+    const dim3 grid((T + LN_ROWS - 1) / LN_ROWS);
+    cudaError_t e = cudaErrorInvalidValue;
+#define X(n)                                                                                                   \
+  if (e == cudaErrorInvalidValue && v <= n)                                                                    \
+    e = launch_pdl(ln_bwd_stats_kernel<n>, grid, dim3(256), 0, s, 1, dy, x, mean, rstd, gamma,                 \
+                   reinterpret_cast<float2*>(stat), T, h);                                                      \
+  else
+    SLIP_LN_VPL_CASES(X) {}
+#undef X
+    if (e != cudaSuccess) return e;
+  }
+  const int nparts = 1;
+  const int R = colred_chunks(h, 2);  // 128 registers: 2 blocks per SM
+  dim3 grid((h + CR_COLS - 1) / CR_COLS, R);
+  const bool three = dxsum != nullptr;
+  const int NO = three ? 3 : 2;
+  if (defer) {
+    part = defer->add(R, h, NO, dgamma, dbeta, three ? dxsum : nullptr);
+    if (!part) return cudaErrorInvalidValue;
+  } else if (R == 1) {
+    part = nullptr;
+  }
+  const LnCols lc{gamma, resid, dx, reinterpret_cast<const float2*>(stat), nparts};
+  cudaError_t e =
+      three ? launch_pdl(colred_kernel<3>, grid, dim3(256), 0, s, 1, dy, static_cast<int64_t>(h), x, mean, rstd,
+                         static_cast<const bf16*>(nullptr), T, h, part, dgamma, dbeta, dxsum, accumulate,
+                         static_cast<unsigned*>(nullptr), lc)
+            : launch_pdl(colred_kernel<4>, grid, dim3(256), 0, s, 1, dy, static_cast<int64_t>(h), x, mean, rstd,
+                         static_cast<const bf16*>(nullptr), T, h, part, dgamma, dbeta, static_cast<float*>(nullptr),
+                         accumulate, static_cast<unsigned*>(nullptr), lc);
+  if (e != cudaSuccess || R == 1 || defer) return e;
+  return launch_pdl(colred_finalize_kernel, dim3((h * NO + 255) / 256), dim3(256), 0, s, 1,
+                    static_cast<const float*>(part), R, h, NO, dgamma, dbeta, three ? dxsum : static_cast<float*>(nullptr),
+                    accumulate);
+}
 
-size_t colred_part_floats(int N, int NO) { return static_cast<size_t>(colred_chunks(N)) * N * NO; }
+int colred_launches(int N) { return colred_chunks(N, 4) > 1 ? 2 : 1; }
+
+// an upper bound of every variant's partials (the most chunks: 4 blocks per SM)
+size_t colred_part_floats(int N, int NO) { return static_cast<size_t>(colred_chunks(N, 4)) * N * NO; }
 
 float* RedBatch::add(int R, int N, int NO, float* o0, float* o1, float* o2) {
   if (n == kMaxRed) return nullptr;
@@ -743,7 +911,7 @@ cudaError_t colred_finalize_batch(const RedBatch& b, int accumulate, cudaStream_
 cudaError_t colsum(const bf16* a, int T, int N, int64_t ld, float* out, int accumulate, float* part,
                    unsigned* tickets, cudaStream_t s, RedBatch* defer) {
   if (N % 8 || ld % 8 || (N + 255) / 256 > kTickets) return cudaErrorInvalidValue;
-  const int R = colred_chunks(N);
+  const int R = colred_chunks(N, 4);
   dim3 grid((N + CR_COLS - 1) / CR_COLS, R);
   if (defer) {
     part = defer->add(R, N, 1, out, nullptr, nullptr);
@@ -754,7 +922,7 @@ cudaError_t colsum(const bf16* a, int T, int N, int64_t ld, float* out, int accu
   cudaError_t e = launch_pdl(colred_kernel<0>, grid, dim3(256), 0, s, 1, a, ld, static_cast<const bf16*>(nullptr),
                              static_cast<const float*>(nullptr), static_cast<const float*>(nullptr),
                              static_cast<const bf16*>(nullptr), T, N, part, out, static_cast<float*>(nullptr),
-                             static_cast<float*>(nullptr), accumulate, tickets);
+                             static_cast<float*>(nullptr), accumulate, tickets, LnCols{});
   if (e != cudaSuccess || R == 1 || defer) return e;
   return launch_pdl(colred_finalize_kernel, dim3((N + 255) / 256), dim3(256), 0, s, 1, static_cast<const float*>(part),
                     R, N, 1, out, static_cast<float*>(nullptr), static_cast<float*>(nullptr), accumulate);

@@ -55,6 +55,15 @@ cudaError_t ln_bwd(const bf16* dy, const bf16* x, const float* mean, const float
                    const bf16* resid, bf16* dx, float* dgamma, float* dbeta, float* dxsum, int accumulate, float* part,
                    unsigned* tickets, int T, int h, cudaStream_t s, RedBatch* defer = nullptr);
 
+// LayerNorm backward as a row-statistics pass and ONE column-strip pass: stat[t] =
+// (sum g, sum g*xhat) (stat: 2T floats of scratch), then dx = resid + rstd (dy*gamma -
+// mean_h(g) - xhat mean_h(g xhat)) written as bf16 while dgamma, dbeta (and dxsum if
+// non-null, over the stored bf16 dx) are reduced as ln_bwd does.  resid may be null;
+// dx must not alias x or dy.
+cudaError_t ln_bwd2(const bf16* dy, const bf16* x, const float* mean, const float* rstd, const bf16* gamma,
+                    const bf16* resid, bf16* dx, float* stat, float* dgamma, float* dbeta, float* dxsum, int accumulate,
+                    float* part, int T, int h, cudaStream_t s, RedBatch* defer = nullptr);
+
 // out[n] (+)= sum_t a[t, n] for a bf16 [T, N] matrix with row stride ld (bias gradients).
 cudaError_t colsum(const bf16* a, int T, int N, int64_t ld, float* out, int accumulate, float* part,
                    unsigned* tickets, cudaStream_t s, RedBatch* defer = nullptr);

@@ -174,6 +174,7 @@ void carve_ws(Carver& cv, const Dims& d, Workspace* out) {
   w.dO = cv.take<bf16>(Th);
   w.dy1 = cv.take<bf16>(Th);
   w.part = cv.take<float>(3 * red);
+  w.lnstat = cv.take<float>(2 * static_cast<size_t>(d.T));
   // deferred reductions: the four of a layer (b1, LN2 + bo, bqkv, LN1 + b2 below) for
   // kMaxRed / 4 layers before a flush
   w.red_cap = (kMaxRed / 4) * (colred_part_floats(d.f, 1) + colred_part_floats(3 * d.h, 1) +
@@ -273,6 +274,8 @@ slip_status linear_dx(slip_ctx* c, const bf16* dY, const bf16* W, int N, int K, 
   d.aux = aux;
   return run_gemm(c, d, s, "linear_dx");
 }
+
+
 
 // dW[N, K] (+)= dY[T, N]^T X[T, K]   (fp32, fused in the epilogue: TMA store / reduce-add)
 slip_status linear_dw(slip_ctx* c, const bf16* dY, const bf16* X, int N, int K, float* dW, int accumulate,
@@ -467,9 +470,9 @@ slip_status backward_input_impl(slip_ctx* c, int slot, const void* dy, void* dx,
     // LN2 backward + residual: dX2 = dOut + LN2'(dY2); dgamma2, dbeta2, dbo = colsum(dX2)
     SLIP_TRY(red_reserve(c, D.h, 3, accumulate, s));
     SLIP_TRY(kcheck(c,
-                    ln_bwd(c->ws.dy2, ls.x2, ls.mean2, ls.rstd2, Wt.g2, ls.dout, ls.dx2, G.g2, G.b2n, G.bo, accumulate,
-                           c->ws.part, c->ws.tickets, D.T, D.h, s, &c->red),
-                    "ln_bwd 2", 2));
+                    ln_bwd2(c->ws.dy2, ls.x2, ls.mean2, ls.rstd2, Wt.g2, ls.dout, ls.dx2, c->ws.lnstat, G.g2, G.b2n,
+                            G.bo, accumulate, c->ws.part, D.T, D.h, s, &c->red),
+                    "ln_bwd2 2", 2));
     // dO = dX2 Wo
     SLIP_TRY(linear_dx(c, ls.dx2, Wt.wo, D.h, D.h, c->ws.dO, EPI_BF16, nullptr, s));
     SLIP_TRY(attention_bwd(c, ls, s));
@@ -481,10 +484,17 @@ slip_status backward_input_impl(slip_ctx* c, int slot, const void* dy, void* dx,
     bf16* dxl = l > 0 ? sb.layer[l - 1].dout : ((D.ends & 1) ? sb.dx : static_cast<bf16*>(dx));
     float* dxsum = l > 0 ? layer_g(c, l - 1).b2 : nullptr;
     SLIP_TRY(red_reserve(c, D.h, 3, accumulate, s));
-    SLIP_TRY(kcheck(c,
-                    ln_bwd(c->ws.dy1, ls.xin, ls.mean1, ls.rstd1, Wt.g1, ls.dx2, dxl, G.g1, G.b1n, dxl ? dxsum : nullptr,
-                           accumulate, c->ws.part, c->ws.tickets, D.T, D.h, s, &c->red),
-                    "ln_bwd 1", (dxl ? 1 : 0) + 1));
+    if (dxl) {
+      SLIP_TRY(kcheck(c,
+                      ln_bwd2(c->ws.dy1, ls.xin, ls.mean1, ls.rstd1, Wt.g1, ls.dx2, dxl, c->ws.lnstat, G.g1, G.b1n,
+                              dxsum, accumulate, c->ws.part, D.T, D.h, s, &c->red),
+                      "ln_bwd2 1", 2));
+    } else {  // stage 0 without an input gradient: only dgamma1, dbeta1
+      SLIP_TRY(kcheck(c,
+                      ln_bwd(c->ws.dy1, ls.xin, ls.mean1, ls.rstd1, Wt.g1, ls.dx2, nullptr, G.g1, G.b1n, nullptr,
+                             accumulate, c->ws.part, c->ws.tickets, D.T, D.h, s, &c->red),
+                      "ln_bwd 1", 1));
+    }
   }
   SLIP_TRY(red_flush(c, accumulate, s));
   if ((D.ends & 1) && dx && dx != sb.dx)
