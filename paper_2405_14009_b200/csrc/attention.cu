@@ -62,6 +62,7 @@ struct KArgs {
   const __nv_bfloat16* dO;  // DQ: its gradient [T, h]
   int64_t ldh;              // row stride of O / dO
   float* dsum_w;            // DQ: D written here for the dK / dV kernel
+  float* colsum;            // backward: per 32-row-group column sums of the stored output
 };
 
 // Descriptor of a 128B-swizzled operand at base; the UMMA_K steps below are constant
@@ -100,6 +101,20 @@ __device__ __forceinline__ void store_row_chunk(__nv_bfloat16* row, int c0, cons
       *reinterpret_cast<uint4*>(row + c) = u;
     }
   }
+}
+
+// Backward epilogue column sums (the QKV bias gradient, KArgs::colsum): the warp's 32 rows
+// (row-per-lane, rows >= s count 0) of the chunk's 32 columns, of the values as stored
+// (bf16-rounded), summed by ptx::warp_colsum32; lane c writes column c0 + c of its group.
+template <int D>
+__device__ __forceinline__ void colsum_row_chunk(float* dst, int c0, bool row_ok, const uint32_t (&v)[32]) {
+  float cs[32];
+#pragma unroll
+  for (int i = 0; i < 32; ++i)
+    cs[i] = row_ok ? __bfloat162float(__float2bfloat16_rn(__uint_as_float(v[i]))) : 0.f;
+  const float t = ptx::warp_colsum32(cs);
+  const int lane = threadIdx.x & 31;
+  if (c0 + lane < D) dst[c0 + lane] = t;
 }
 
 // ====================================================================== forward kernel
@@ -557,6 +572,11 @@ __global__ void __launch_bounds__(BWD_NT, 1)
     ptx::mbar_wait(acc_full, 0);
     ptx::tc_fence_after();
     __nv_bfloat16* orow = a.out + (static_cast<int64_t>(bi) * a.s + q) * a.ldo + a.col0 + static_cast<int64_t>(hn) * a.d;
+    const int grp0 = q0 + lq * 32;  // this warp's 32-row group
+    float* csrow = (a.colsum && grp0 < a.s)
+                       ? a.colsum + (static_cast<int64_t>(bi) * ((a.s + 31) >> 5) + (grp0 >> 5)) * a.ldo + a.col0 +
+                             static_cast<int64_t>(hn) * a.d
+                       : nullptr;
 #pragma unroll
     for (int c = 0; c < C::OC; ++c) {
       if ((c & 1) != g) continue;
@@ -564,6 +584,7 @@ __global__ void __launch_bounds__(BWD_NT, 1)
       ptx::tmem_ld_32x32b_x32(tmem + NSB * 128 + lane_off + c * 32, v);
       ptx::tmem_ld_wait();
       if (q < a.s) store_row_chunk<D>(orow, c * 32, v);
+      if (csrow) colsum_row_chunk<D>(csrow, c * 32, q < a.s, v);
     }
   }
   ptx::tc_fence_before();
@@ -748,6 +769,11 @@ __global__ void __launch_bounds__(BWD_NT, 1)
     ptx::mbar_wait(acc_full, 0);
     ptx::tc_fence_after();
     const int64_t rowoff = (static_cast<int64_t>(bi) * a.s + key) * a.ldo + static_cast<int64_t>(hn) * a.d;
+    const int grp0 = k0 + lq * 32;  // this warp's 32-row group
+    float* csrow = (a.colsum && grp0 < a.s)
+                       ? a.colsum + (static_cast<int64_t>(bi) * ((a.s + 31) >> 5) + (grp0 >> 5)) * a.ldo +
+                             static_cast<int64_t>(hn) * a.d
+                       : nullptr;
 #pragma unroll
     for (int c = 0; c < C::OC; ++c) {
       if ((c & 1) != g) continue;
@@ -755,9 +781,11 @@ __global__ void __launch_bounds__(BWD_NT, 1)
       ptx::tmem_ld_32x32b_x32(tmem + 384 + lane_off + c * 32, v);
       ptx::tmem_ld_wait();
       if (key < a.s) store_row_chunk<D>(a.out + rowoff + a.col0, c * 32, v);
+      if (csrow) colsum_row_chunk<D>(csrow + a.col0, c * 32, key < a.s, v);
       ptx::tmem_ld_32x32b_x32(tmem + 256 + lane_off + c * 32, v);
       ptx::tmem_ld_wait();
       if (key < a.s) store_row_chunk<D>(a.out + rowoff + a.col1, c * 32, v);
+      if (csrow) colsum_row_chunk<D>(csrow + a.col1, c * 32, key < a.s, v);
     }
   }
   ptx::tc_fence_before();
@@ -851,6 +879,7 @@ cudaError_t backward_d(const AttnArgs& a, cudaStream_t st) {
   k.out = a.out;
   k.ldo = a.qkv_ld;
   k.d = a.d;
+  k.colsum = a.colsum;
   constexpr int s2 = dq_smem<D>(), s3 = dkdv_smem<D>();
   static_assert(dq_smem<D>() <= 232448 && dkdv_smem<D>() <= 232448, "attention smem budget");
   static bool once = false;

@@ -24,6 +24,9 @@ struct AttnArgs {
   __nv_bfloat16* out;        // FWD: O [T, h];  backward: dQKV [T, 3h]
   float* lse;                // [z, s] log2-domain log-sum-exp of S*log2(e)/sqrt(d)
   float* dsum;               // [z, s] D = rowsum(dO * O)
+  // backward, optional: column sums of the stored (bf16) dQKV per (batch, 32-row group) —
+  // the QKV bias gradient's partials: colsum[(b * ceil(s/32) + r / 32) * 3h + col]
+  float* colsum = nullptr;
 };
 
 cudaError_t attn_forward(const AttnArgs& a, cudaStream_t s);   // writes lse, out = O

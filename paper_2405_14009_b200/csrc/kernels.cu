@@ -410,21 +410,34 @@ __global__ void __launch_bounds__(256) colred_finalize_kernel(const float* __res
 // The finalize of many reductions in one launch (a whole B call's bias / LayerNorm
 // reductions, see RedBatch): thread i of the concatenated [entry][output][column] space
 // sums its column's R partials in chunk order (deterministic, as the per-reduction pass).
+// Block = 64 columns x 4 quarters of the R chunks (quarter-major: a warp reads 32
+// consecutive columns); the quarters' sums are added in quarter order through smem.
 __global__ void __launch_bounds__(256) colred_finalize_batch_kernel(const RedBatch b, int first, int last,
                                                                     int accumulate) {
+  __shared__ float qs[4][64];
   ptx::grid_dep_wait();
-  const int64_t i = b.start[first] + static_cast<int64_t>(blockIdx.x) * 256 + threadIdx.x;
-  if (i >= b.start[last]) return;
+  const int cl = threadIdx.x & 63, qr = threadIdx.x >> 6;
+  const int64_t i = b.start[first] + static_cast<int64_t>(blockIdx.x) * 64 + cl;
+  const bool live = i < b.start[last];
   int e = first;
-  while (i >= b.start[e + 1]) ++e;
+  if (live)
+    while (i >= b.start[e + 1]) ++e;
   const RedEntry& r = b.e[e];
-  const int k = static_cast<int>(i - b.start[e]);
+  const int k = live ? static_cast<int>(i - b.start[e]) : 0;
   const int o = k / r.N, c = k % r.N;
-  const float* p = r.part + static_cast<size_t>(o) * r.R * r.N + c;
   float s = 0.f;
-  for (int q = 0; q < r.R; ++q) s += p[static_cast<size_t>(q) * r.N];
-  float* out = r.out[o];
-  out[c] = accumulate ? out[c] + s : s;
+  if (live) {
+    const float* p = r.part + static_cast<size_t>(o) * r.R * r.N + c;
+    const int q0 = (r.R * qr) >> 2, q1 = (r.R * (qr + 1)) >> 2;
+    for (int q = q0; q < q1; ++q) s += p[static_cast<size_t>(q) * r.N];
+  }
+  qs[qr][cl] = s;
+  __syncthreads();
+  if (qr == 0 && live) {
+    const float t = ((qs[0][cl] + qs[1][cl]) + qs[2][cl]) + qs[3][cl];
+    float* out = r.out[o];
+    out[c] = accumulate ? out[c] + t : t;
+  }
 }
 
 // Row chunks so that a reduction fills the GPU: about 2 blocks per SM.
@@ -903,7 +916,7 @@ cudaError_t colred_finalize_batch(const RedBatch& b, int accumulate, cudaStream_
   *launches = 0;
   if (b.n == 0) return cudaSuccess;
   const int64_t total = b.start[b.n];
-  const int blocks = static_cast<int>((total + 255) / 256);
+  const int blocks = static_cast<int>((total + 63) / 64);
   *launches = 1;
   return launch_pdl(colred_finalize_batch_kernel, dim3(blocks), dim3(256), 0, s, 1, b, 0, b.n, accumulate);
 }

@@ -287,5 +287,23 @@ __device__ __forceinline__ float tanh_fast(float x) {
   return y;
 }
 
+// Column sums of a warp's 32 x 32 tile held row-per-lane (lane r holds v[0..31] of row r):
+// returns, in lane c, sum_r v_r[c].  Reduce-scatter by halving: 16 + 8 + 4 + 2 + 1 shuffles,
+// a fixed tree (deterministic).  v is clobbered.
+__device__ __forceinline__ float warp_colsum32(float (&v)[32]) {
+  const int lane = threadIdx.x & 31;
+#pragma unroll
+  for (int w = 16; w >= 1; w >>= 1) {
+    const bool up = (lane & w) != 0;  // this lane keeps the upper half of its columns
+#pragma unroll
+    for (int i = 0; i < w; ++i) {
+      const float send = up ? v[i] : v[i + w];
+      const float keep = up ? v[i + w] : v[i];
+      v[i] = keep + __shfl_xor_sync(0xffffffffu, send, w);
+    }
+  }
+  return v[0];
+}
+
 }  // namespace ptx
 }  // namespace slip

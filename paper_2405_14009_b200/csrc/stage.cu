@@ -175,10 +175,10 @@ void carve_ws(Carver& cv, const Dims& d, Workspace* out) {
   w.dy1 = cv.take<bf16>(Th);
   w.part = cv.take<float>(3 * red);
   w.lnstat = cv.take<float>(2 * static_cast<size_t>(d.T));
-  // deferred reductions: the four of a layer (b1, LN2 + bo, bqkv, LN1 + b2 below) for
-  // kMaxRed / 4 layers before a flush
-  w.red_cap = (kMaxRed / 4) * (colred_part_floats(d.f, 1) + colred_part_floats(3 * d.h, 1) +
-                               2 * colred_part_floats(d.h, 3)) +
+  // deferred reductions: the four of a layer (b1, bqkv per (batch, 32-row group) from the
+  // attention backward, LN2 + bo, LN1 + b2 below) for 8 layers before a flush
+  w.red_cap = 8 * (colred_part_floats(d.f, 1) + static_cast<size_t>(d.b) * ((d.s + 31) / 32) * 3 * d.h +
+                   2 * colred_part_floats(d.h, 3)) +
               colred_part_floats(d.h, 1);
   w.red = cv.take<float>(w.red_cap);
   w.tickets = cv.take<unsigned>(kTickets);
@@ -356,9 +356,10 @@ slip_status attention_fwd(slip_ctx* c, LayerStash& ls, cudaStream_t s) {
   return attn_status(c, attn_forward(a, s), "attention forward", 1);
 }
 
-slip_status attention_bwd(slip_ctx* c, LayerStash& ls, cudaStream_t s) {
+slip_status attention_bwd(slip_ctx* c, LayerStash& ls, cudaStream_t s, float* colsum = nullptr) {
   AttnArgs a = attn_args(c, ls);
   a.out = ls.dqkv;
+  a.colsum = colsum;
   return attn_status(c, attn_backward(a, s), "attention backward", 2);
 }
 
@@ -370,10 +371,22 @@ slip_status red_flush(slip_ctx* c, int accumulate, cudaStream_t s) {
   return kcheck(c, e, "colred_finalize_batch", n);
 }
 
-// Make room in the batch for one reduction of NO outputs over N columns.
-slip_status red_reserve(slip_ctx* c, int N, int NO, int accumulate, cudaStream_t s) {
-  if (c->red.n < kMaxRed && c->red.used + colred_part_floats(N, NO) <= c->red.cap) return SLIP_OK;
+// Make room in the batch for one reduction of `floats` partials.
+slip_status red_reserve_floats(slip_ctx* c, size_t floats, int accumulate, cudaStream_t s) {
+  if (c->red.n < kMaxRed && c->red.used + floats <= c->red.cap) return SLIP_OK;
   return red_flush(c, accumulate, s);
+}
+// ... of NO outputs over N columns by a colred launch
+slip_status red_reserve(slip_ctx* c, int N, int NO, int accumulate, cudaStream_t s) {
+  return red_reserve_floats(c, colred_part_floats(N, NO), accumulate, s);
+}
+// The partial region of a bias gradient whose producer leaves column sums per 32-row
+// group (GEMM epilogue / attention backward): R groups x N columns, finalized with the batch.
+slip_status red_rows(slip_ctx* c, int R, int N, float* out, int accumulate, cudaStream_t s, float** part) {
+  SLIP_TRY(red_reserve_floats(c, static_cast<size_t>(R) * N, accumulate, s));
+  *part = c->red.add(R, N, 1, out, nullptr, nullptr);
+  SLIP_CHECK(*part, SLIP_EINVAL, "reduction arena too small");
+  return SLIP_OK;
 }
 
 // colsum(a[T, N]) -> out (fp32, overwrite or accumulate); the finalize is deferred to
@@ -475,8 +488,10 @@ slip_status backward_input_impl(slip_ctx* c, int slot, const void* dy, void* dx,
                     "ln_bwd2 2", 2));
     // dO = dX2 Wo
     SLIP_TRY(linear_dx(c, ls.dx2, Wt.wo, D.h, D.h, c->ws.dO, EPI_BF16, nullptr, s));
-    SLIP_TRY(attention_bwd(c, ls, s));
-    SLIP_TRY(bias_grad(c, ls.dqkv, 3 * D.h, 3 * D.h, G.bqkv, accumulate, s));
+    // attention backward (dQKV, and dbqkv's column sums per (batch, 32-row group))
+    float* pbq = nullptr;
+    SLIP_TRY(red_rows(c, D.b * ((D.s + 31) / 32), 3 * D.h, G.bqkv, accumulate, s, &pbq));
+    SLIP_TRY(attention_bwd(c, ls, s, pbq));
     // dY1 = dQKV Wqkv
     SLIP_TRY(linear_dx(c, ls.dqkv, Wt.wqkv, 3 * D.h, D.h, c->ws.dy1, EPI_BF16, nullptr, s));
     // LN1 backward + residual: dX = dX2 + LN1'(dY1); db2 of the layer below = colsum(dX)
