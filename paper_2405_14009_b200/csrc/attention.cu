@@ -144,6 +144,31 @@ __device__ long long g_probe[4096];
   do {             \
   } while (0)
 #endif
+// Optional per-CTA schedule record (globaltimer start / end, SM id) of the backward kernels.
+#ifdef SLIP_ATTN_SCHED
+__device__ unsigned long long g_sched[2][4096][3];
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+#define SCHED(k, w)                                                                          \
+  do {                                                                                       \
+    if (threadIdx.x == 0) {                                                                  \
+      const int cta_ = blockIdx.y * gridDim.x + blockIdx.x;                                  \
+      g_sched[k][cta_][w] = gtimer();                                                        \
+      if (w == 0) {                                                                          \
+        unsigned sm_;                                                                        \
+        asm volatile("mov.u32 %0, %%smid;" : "=r"(sm_));                                     \
+        g_sched[k][cta_][2] = sm_;                                                           \
+      }                                                                                      \
+    }                                                                                        \
+  } while (0)
+#else
+#define SCHED(k, w) \
+  do {              \
+  } while (0)
+#endif
 
 template <int D>
 __global__ void __launch_bounds__(FWD_NT, 1)
@@ -406,6 +431,7 @@ __global__ void __launch_bounds__(BWD_NT, 1)
     attn_dq_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK64,
                    const __grid_constant__ CUtensorMap tmV64, const __grid_constant__ CUtensorMap tmdO,
                    const KArgs a) {
+  SCHED(0, 0);
   using C = AC<D>;
   using H = HC<D>;
   constexpr int NST = 3, NSB = 2;  // K/V ring stages, S|dP buffers in TMEM (dQ after them)
@@ -593,6 +619,7 @@ __global__ void __launch_bounds__(BWD_NT, 1)
     ptx::tc_fence_after();
     ptx::tmem_dealloc<512>(tmem);
   }
+  SCHED(0, 1);
 }
 
 // ---------------------------------------------------------------- dK, dV
@@ -604,6 +631,7 @@ __global__ void __launch_bounds__(BWD_NT, 1)
     attn_dkdv_kernel(const __grid_constant__ CUtensorMap tmQ64, const __grid_constant__ CUtensorMap tmK,
                      const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmdO64,
                      const KArgs a) {
+  SCHED(1, 0);
   using C = AC<D>;
   using H = HC<D>;
   constexpr int NST = 3;
@@ -794,6 +822,7 @@ __global__ void __launch_bounds__(BWD_NT, 1)
     ptx::tc_fence_after();
     ptx::tmem_dealloc<512>(tmem);
   }
+  SCHED(1, 1);
 }
 
 thread_local std::string g_amsg;
@@ -903,6 +932,9 @@ const char* attn_last_message() { return g_amsg.c_str(); }
 
 #ifdef SLIP_ATTN_PROBE
 void attn_probe_read(long long* out, int n) { cudaMemcpyFromSymbol(out, g_probe, n * sizeof(long long)); }
+#endif
+#ifdef SLIP_ATTN_SCHED
+void attn_sched_read(unsigned long long* out) { cudaMemcpyFromSymbol(out, g_sched, sizeof(g_sched)); }
 #endif
 
 cudaError_t attn_forward(const AttnArgs& a, cudaStream_t s) {

@@ -21,7 +21,7 @@ __global__ void fill(__nv_bfloat16* p, size_t n, unsigned seed) {
   }
 }
 
-// usage: gemm_probe [K] [random 0/1] [resid+bias 0/1] [b_mn_major 0/1] [N] [also stream-K 0/1]
+// usage: gemm_probe [K] [random 0/1] [resid+bias 0/1] [b_mn_major 0/1] [N] [also stream-K 0/1] [bn] [pair]
 int main(int argc, char** argv) {
   const int M = 2048, K = argc > 1 ? atoi(argv[1]) : 2048;
   const int rnd = argc > 2 ? atoi(argv[2]) : 0, res = argc > 3 ? atoi(argv[3]) : 0;
@@ -48,12 +48,14 @@ int main(int argc, char** argv) {
   cudaMalloc(&flags, 4096);
   cudaMemset(flags, 0, 4096);
   const int sk_max = argc > 6 ? atoi(argv[6]) : 0;
+  const int bnv = argc > 7 ? atoi(argv[7]) : 256, pairv = argc > 8 ? atoi(argv[8]) : 1;
   for (int sk = 0; sk <= sk_max; ++sk) {
     slip::GemmDesc d;
     d.M = M;
     d.N = N;
     d.K = K;
-    d.bn = 256;
+    d.bn = bnv;
+    d.pair = pairv != 0;
     d.a.ptr = a;
     d.a.ld = K;
     d.b.ptr = b;
