@@ -21,7 +21,7 @@ __global__ void fill(__nv_bfloat16* p, size_t n, unsigned seed) {
   }
 }
 
-// usage: gemm_probe [K] [random 0/1] [resid+bias 0/1] [b_mn_major 0/1] [N] [also stream-K 0/1] [bn] [pair]
+// usage: gemm_probe [K] [random 0/1] [resid+bias 0/1] [b_mn_major 0/1] [N] [also stream-K 0/1] [bn] [pair] [mode 0/1/2]
 int main(int argc, char** argv) {
   const int M = 2048, K = argc > 1 ? atoi(argv[1]) : 2048;
   const int rnd = argc > 2 ? atoi(argv[2]) : 0, res = argc > 3 ? atoi(argv[3]) : 0;
@@ -49,6 +49,11 @@ int main(int argc, char** argv) {
   cudaMemset(flags, 0, 4096);
   const int sk_max = argc > 6 ? atoi(argv[6]) : 0;
   const int bnv = argc > 7 ? atoi(argv[7]) : 256, pairv = argc > 8 ? atoi(argv[8]) : 1;
+  const int modev = argc > 9 ? atoi(argv[9]) : 0;  // 0 bf16, 1 GeLU (+aux out), 2 GeLU' (aux in)
+  __nv_bfloat16* auxb;
+  cudaMalloc(&auxb, size_t(M) * N * 2);
+  cudaMemset(auxb, 0, size_t(M) * N * 2);
+  if (rnd) fill<<<1184, 256>>>(auxb, size_t(M) * N, 4);
   for (int sk = 0; sk <= sk_max; ++sk) {
     slip::GemmDesc d;
     d.M = M;
@@ -67,7 +72,8 @@ int main(int argc, char** argv) {
     }
     d.c = c;
     d.ldc = N;
-    d.mode = slip::EPI_BF16;
+    d.mode = modev == 1 ? slip::EPI_BF16_GELU : (modev == 2 ? slip::EPI_BF16_DGELU : slip::EPI_BF16);
+    if (modev) d.aux = auxb;
     if (sk) {
       d.sk_ws = ws;
       d.sk_flags = flags;
