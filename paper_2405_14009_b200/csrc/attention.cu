@@ -74,14 +74,9 @@ __host__ __device__ constexpr uint64_t dk_off(int kk) { return static_cast<uint6
 __host__ __device__ constexpr uint64_t hk_off(int kk) { return static_cast<uint64_t>((kk >> 2) * (8192 >> 4) + (kk & 3) * 2); }
 __host__ __device__ constexpr uint64_t m_off(int kk) { return static_cast<uint64_t>(kk * (2048 >> 4)); }
 
-// tile [128 rows][D] as a K-major operand (contraction over d), UMMA_K step kk
-__device__ __forceinline__ uint64_t dk(uint32_t base, int kk) {
-  return ptx::smem_desc_sw128(base + (kk >> 2) * ATOM + (kk & 3) * 32, 16, 1024);
-}
-// tile [128 rows][D] as an MN-major operand (contraction over the 128 rows), step kk
-__device__ __forceinline__ uint64_t dm(uint32_t base, int kk) {
-  return ptx::smem_desc_sw128(base + kk * 2048, ATOM, 1024);
-}
+// (kdesc(base) + dk_off(kk): a [128 rows][D] tile as a K-major operand, UMMA_K step kk
+//  = 16 d; mdesc(base, ATOM) + m_off(kk): as an MN-major operand, contraction over its
+//  rows; hk_off / HATOM: the same for [64 rows][D] half tiles.)
 __device__ __forceinline__ uint32_t pack2(float a, float b) {
   __nv_bfloat162 v = __floats2bfloat162_rn(a, b);
   return *reinterpret_cast<uint32_t*>(&v);
@@ -410,14 +405,6 @@ struct HC {
   static constexpr uint32_t IDESC_S = ptx::idesc_bf16_f32(128, HT, false, false);  // N = 64, K-major x2
   static constexpr uint32_t IDESC_ACC = ptx::idesc_bf16_f32(128, D, false, true);  // A TMEM, B MN-major
 };
-// [64 rows][D] half tile as a K-major operand (contraction over d), step kk
-__device__ __forceinline__ uint64_t hk(uint32_t base, int kk) {
-  return ptx::smem_desc_sw128(base + (kk >> 2) * HATOM + (kk & 3) * 32, 16, 1024);
-}
-// [64 rows][D] half tile as an MN-major operand (contraction over its 64 rows), step kk
-__device__ __forceinline__ uint64_t hm(uint32_t base, int kk) {
-  return ptx::smem_desc_sw128(base + kk * 2048, HATOM, 1024);
-}
 // TMEM column of the bf16 A operand (64 contraction indices, 2 per column) for step kk:
 // group g = kk / 2 wrote its 32 indices to columns [32 g, 32 g + 16)
 __device__ __forceinline__ uint32_t acol(int kk) { return 32 * (kk >> 1) + (kk & 1) * 8; }

@@ -1,6 +1,7 @@
-// kernels.cuh — memory-bound kernels of the stage step (coalesced, 16-byte vectorised,
-// block-per-row with warp-shuffle reductions; column reductions are deterministic and
-// finish in one launch via a last-block ticket).
+// kernels.cuh — memory-bound kernels of the stage step (coalesced, 16-byte vectorised;
+// LayerNorm rows one warp each with shuffle reductions; column reductions deterministic:
+// 64-column strips x row chunks, then a fixed-order sum of the chunk partials, batched
+// per B call by RedBatch).
 #pragma once
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
