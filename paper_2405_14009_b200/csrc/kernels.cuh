@@ -49,7 +49,7 @@ cudaError_t ln_fwd(const bf16* x, const bf16* gamma, const bf16* beta, bf16* y, 
 // LayerNorm backward.  dx = resid + rstd*(g - mean_h(g) - xhat*mean_h(g*xhat)), g = dy*gamma
 // (dx may be null; it must not alias x).  dgamma (+)= sum_t dy*xhat, dbeta (+)= sum_t dy and,
 // if dxsum != null, dxsum (+)= sum_t dx, all three in ONE column-reduction launch.
-// part: 3*kRedChunks*h floats of scratch; tickets: kTickets zero-initialised counters.
+// part: 3*kRedChunks*h floats of scratch (unless deferred); tickets: unused (no last-block tickets).
 // Column reductions over N columns take 1 launch, or 2 when they need a finalize pass.
 int colred_launches(int N);
 cudaError_t ln_bwd(const bf16* dy, const bf16* x, const float* mean, const float* rstd, const bf16* gamma,
