@@ -30,6 +30,9 @@ int main(int argc, char** argv) {
   cudaMalloc(&a, size_t(M) * K * 2);
   cudaMalloc(&b, size_t(N) * K * 2);
   cudaMalloc(&c, size_t(M) * N * 2);
+  float* cf;
+  cudaMalloc(&cf, size_t(M) * N * 4);
+  cudaMemset(cf, 0, size_t(M) * N * 4);
   cudaMemset(a, 0, size_t(M) * K * 2);
   cudaMemset(b, 0, size_t(N) * K * 2);
   __nv_bfloat16 *r, *bias;
@@ -73,7 +76,18 @@ int main(int argc, char** argv) {
     d.c = c;
     d.ldc = N;
     d.mode = modev == 1 ? slip::EPI_BF16_GELU : (modev == 2 ? slip::EPI_BF16_DGELU : slip::EPI_BF16);
-    if (modev) d.aux = auxb;
+    if (modev == 1 || modev == 2) d.aux = auxb;
+    if (modev == 4) {  // the W GEMM: dW(f32) += A^T B, both operands MN-major [K rows]
+      d.mode = slip::EPI_F32_ACC;
+      d.accumulate = 1;
+      d.c = cf;
+      d.a.mn_major = true;
+      d.a.ld = M;
+      d.b.mn_major = true;
+      d.b.ld = N;
+      d.bias = nullptr;
+      d.resid = nullptr;
+    }
     if (sk) {
       d.sk_ws = ws;
       d.sk_flags = flags;
