@@ -100,6 +100,10 @@ extern "C" slip_status slip_execute_schedule(slip_ctx* ctx, slip_comm* comm, con
   int64_t launches0 = ctx->launches;
 
   if (ctx->validate) SLIP_CUDA(cudaMemsetAsync(ctx->ws.vflags + 4, 0, sizeof(int32_t), cs));
+  // host inputs (slip_io): copied on their own stream as soon as the slot is free, so the
+  // copies of later micro-batches overlap the compute of earlier ones
+  if (io && !ctx->h2d) SLIP_CUDA(cudaStreamCreateWithFlags(&ctx->h2d, cudaStreamNonBlocking));
+  cudaStream_t hs = ctx->h2d;
   for (int run = 0; run < 2; ++run) {
     const int H = run == 0 ? warmup : iterations;
     if (H == 0) continue;
@@ -160,6 +164,7 @@ extern "C" slip_status slip_execute_schedule(slip_ctx* ctx, slip_comm* comm, con
       if (a.kind == SLIP_ACT_RECV_X || a.kind == SLIP_ACT_RECV_DY) ts = xfer_stream(a.peer, me);
       if (a.kind == SLIP_ACT_SEND_Y || a.kind == SLIP_ACT_SEND_DX) ts = xfer_stream(me, a.peer);
       if (a.kind == SLIP_ACT_AR) ts = comm->ar_stream;
+      if (io && io->x_host && a.kind == SLIP_ACT_LOAD_X) ts = hs;
       const bool tr = timed && tracing && !(a.kind == SLIP_ACT_AR && !comm->stage_comm);
       size_t tb_idx = 0;
       // called by every action after its stream waits: the phase timing (and the trace)
@@ -187,19 +192,22 @@ extern "C" slip_status slip_execute_schedule(slip_ctx* ctx, slip_comm* comm, con
       SlotEv* se = a.slot >= 0 ? &sev[a.slot] : nullptr;
       switch (a.kind) {
         case SLIP_ACT_LOAD_X: {
+          if (io && io->x_host) {  // H2D on the copy stream once the slot is free, then join
+            if (se->freed) SLIP_CUDA(cudaStreamWaitEvent(hs, se->freed, 0));
+            SLIP_CUDA(trace_begin());
+            if (ctx->dm.ends & 1)  // the stage input is T token ids (embedding end)
+              SLIP_CUDA(cudaMemcpyAsync(sb->end.tokens, io->x_host[a.origin * m + a.mb], D.T * sizeof(int32_t),
+                                        cudaMemcpyHostToDevice, hs));
+            else
+              SLIP_CUDA(cudaMemcpyAsync(sb->x, io->x_host[a.origin * m + a.mb], bytes, cudaMemcpyHostToDevice, hs));
+            SLIP_CUDA(chain(hs, cs));
+            break;
+          }
           if (se->freed) SLIP_CUDA(cudaStreamWaitEvent(cs, se->freed, 0));
           SLIP_CUDA(trace_begin());
           if (ctx->dm.ends & 1) {  // the stage input is T token ids (embedding end)
-            int32_t* tok = sb->end.tokens;
-            if (io && io->x_host) {
-              SLIP_CUDA(cudaMemcpyAsync(tok, io->x_host[a.origin * m + a.mb], D.T * sizeof(int32_t),
-                                        cudaMemcpyHostToDevice, cs));
-            } else {
-              SLIP_CUDA(synth_tokens(tok, D.T, D.V, seed, a.origin, a.mb, cs));
-              ctx->launches += 1;
-            }
-          } else if (io && io->x_host) {
-            SLIP_CUDA(cudaMemcpyAsync(sb->x, io->x_host[a.origin * m + a.mb], bytes, cudaMemcpyHostToDevice, cs));
+            SLIP_CUDA(synth_tokens(sb->end.tokens, D.T, D.V, seed, a.origin, a.mb, cs));
+            ctx->launches += 1;
           } else {
             SLIP_CUDA(synth_normal(sb->x, static_cast<int64_t>(Th), seed, a.origin, a.mb, cs));
             ctx->launches += 1;
@@ -248,8 +256,14 @@ extern "C" slip_status slip_execute_schedule(slip_ctx* ctx, slip_comm* comm, con
             break;
           }
           if (io && io->target_host) {
+            // the target goes to slot.dx (free until this micro-batch's B writes its input
+            // gradient there, after the head), copied on the copy stream ahead of time
+            target = sb->dx;
+            if (se->freed) SLIP_CUDA(cudaStreamWaitEvent(hs, se->freed, 0));
+            if (se->sent_dx) SLIP_CUDA(cudaStreamWaitEvent(hs, se->sent_dx, 0));
             SLIP_CUDA(
-                cudaMemcpyAsync(target, io->target_host[a.origin * m + a.mb], bytes, cudaMemcpyHostToDevice, cs));
+                cudaMemcpyAsync(target, io->target_host[a.origin * m + a.mb], bytes, cudaMemcpyHostToDevice, hs));
+            SLIP_CUDA(chain(hs, cs));
           } else {
             SLIP_CUDA(synth_normal(target, static_cast<int64_t>(Th), seed + 1, a.origin, a.mb, cs));
             ctx->launches += 1;
@@ -351,6 +365,7 @@ extern "C" slip_status slip_execute_schedule(slip_ctx* ctx, slip_comm* comm, con
     // join every side stream back into the compute stream
     for (auto& kv : comm->pair_stream) SLIP_CUDA(chain(kv.second, cs));
     SLIP_CUDA(chain(comm->ar_stream, cs));
+    if (hs) SLIP_CUDA(chain(hs, cs));
     if (timed) {
       SLIP_CUDA(cudaEventRecord(t1, cs));
       out->predicted_period = plan.period;

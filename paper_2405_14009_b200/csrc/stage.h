@@ -99,6 +99,7 @@ struct slip_ctx {
   slip::RedBatch red;  // B's bias / LayerNorm reductions, finalized in one launch
   std::vector<int> state;
   int64_t launches = 0;  // kernels enqueued through this context
+  cudaStream_t h2d = nullptr;  // executor: host-to-device copies of the e2e inputs (lazily created)
   int64_t opt_step = 0;  // AdamW steps taken by the executor
   bool trace_on = false;
   bool validate = false;   // post-step validation + cross-stage rollback (slip_set_validation)
