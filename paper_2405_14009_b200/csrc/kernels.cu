@@ -344,6 +344,25 @@ __global__ void __launch_bounds__(256) colred_kernel(const bf16* __restrict__ a,
         }
       }
     }
+  } else if (MODE == 0 && col < N) {
+    // bias gradients: batches of 8 rows per thread, all 8 loads in flight before the adds
+    constexpr int RB = 8;
+    for (int rb = r0 + rg; rb < r1; rb += 32 * RB) {
+      uint4 q[RB];
+#pragma unroll
+      for (int b = 0; b < RB; ++b) {
+        const int r = rb + 32 * b;
+        q[b] = r < r1 ? __ldg(reinterpret_cast<const uint4*>(a + static_cast<size_t>(r) * ld + col))
+                      : make_uint4(0, 0, 0, 0);
+      }
+#pragma unroll
+      for (int b = 0; b < RB; ++b) {
+        float v[8];
+        unpack8(q[b], v);
+#pragma unroll
+        for (int e = 0; e < 8; ++e) acc[0][e] += v[e];
+      }
+    }
   } else if (col < N) {
 #pragma unroll 4
     for (int r = r0 + rg; r < r1; r += 32) {
