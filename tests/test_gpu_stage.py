@@ -253,6 +253,22 @@ def test_one_layer_c2_full_size():
         assert relerr(g[0][n], grads[0][n]) <= GATE_A, n
 
 
+@pytest.mark.slow
+@pytest.mark.parametrize("name", ["c3_2p7b", "c5_6p7b"])
+def test_one_layer_full_size_larger_models(name):
+    """One layer of the GPT-2.7B (h 2560, 32 heads of d = 80) and GPT-6.7B (h 4096, 32 heads
+    of d = 128) shapes of BASELINE.json configs at full size (s 2048), fp64 oracle."""
+    cfg = {"c3_2p7b": sd.C3_2P7B, "c5_6p7b": sd.C5_6P7B}[name]
+    st, layers, x, r, y, dx = run_stage(cfg, 1)
+    out, caches = OL.stage_forward(layers, x, cfg)
+    dxr, grads = OL.stage_backward_coupled(layers, caches, r, cfg)
+    assert relerr(to_np(y), out) <= GATE_A
+    assert relerr(to_np(dx), dxr) <= GATE_A
+    g = sd.unpack_stage(st.grad.cpu().numpy().astype(np.float64), cfg, 1)
+    for n in sd.PARAM_ORDER:
+        assert relerr(g[0][n], grads[0][n]) <= GATE_A, (name, n)
+
+
 ENDS_CFGS = {
     "tiny_both": (sd.ModelCfg(hidden=64, heads=2, ffn=256, seq=32, micro_batch=2, layers=1, vocab=256, ends=3), 1),
     "d128_both": (sd.ModelCfg(hidden=256, heads=2, ffn=1024, seq=128, micro_batch=2, layers=2, vocab=384, ends=3), 2),
