@@ -374,8 +374,8 @@ def main():
     flops_w_op = 2.0 * T * (4 * H * H + 2 * FFN * H) * L + (2.0 * T * VOCAB * H if ends & 2 else 0.0)
     ach_local = flops_w_op * rep.phase_ops[2] / (rep.phase_ms[2] / 1e3) / 1e12 if rep.phase_ops[2] else 0.0
     # masked ranks run nothing: take the per-phase numbers of the busiest live rank
-    stats = torch.tensor([ach_local, float(rep.w_gemm_launches), rep.phase_ms[2]] + list(rep.phase_ms[:5]),
-                         dtype=torch.float64, device="cuda")
+    stats = torch.tensor([ach_local, float(rep.w_gemm_launches), rep.phase_ms[2]] + list(rep.phase_ms[:5]) +
+                         [float(rep.phase_ops[2])], dtype=torch.float64, device="cuda")
     if world > 1:
         dist.all_reduce(stats, op=dist.ReduceOp.MAX)
     stats = stats.tolist()
@@ -383,6 +383,7 @@ def main():
     w_launches = int(stats[1])
     w_ms_total = stats[2]
     phase_ms = stats[3:8]
+    w_ops = stats[8]  # micro-batch W's: back-to-back W's run as one launch (K = n T)
     p_burst, p_sus, hbm, peak_src = peaks()
     traffic = None
     try:
@@ -522,10 +523,13 @@ def main():
         "clocks": clk,
         "e2e": e2e,
         "gpu_launches": gpu_launches,
-        "roofline": {"bound": "tensor", "kernel": "W GEMMs (tcgen05, dW += dY^T X fused fp32 TMA reduce-add)",
+        "roofline": {"bound": "tensor",
+                     "kernel": "W GEMMs (tcgen05, dW (+)= sum over the launch's micro-batches dY^T X, fp32 TMA store)",
                      "achieved": ach, "peak": p_sus, "peak_kind": "bf16_tflops_sustained (%s)" % peak_src,
                      "unit": "TFLOP/s", "frac": (ach / p_sus) if ach else None, "traffic": traffic,
-                     "flops_per_launch": flops_w_op, "launches": w_launches,
+                     "flops_per_launch": flops_w_op * w_ops / w_launches if w_launches else None,
+                     "microbatch_w_per_launch": w_ops / w_launches if w_launches else None,
+                     "launches": w_launches,
                      "avg_launch_ms": (w_ms_total / w_launches) if w_launches else None},
         "phases_ms_per_step_busiest_rank": {n: phase_ms[i] / args.steps
                                             for i, n in enumerate(("F", "B", "W", "BC", "OPT"))},

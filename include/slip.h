@@ -253,6 +253,14 @@ slip_status slip_backward_input(slip_ctx* ctx, int32_t slot, const void* dy, voi
  * slot. */
 slip_status slip_backward_weight(slip_ctx* ctx, int32_t slot, int32_t accumulate, slip_stream s);
 
+/* W of n (2..8) micro-batches in ONE grouped launch (the deferred W's the schedule puts
+ * back to back, §3.2): the contraction of every dW runs over the n slots' stashes
+ * (K = n*T), accumulated in TMEM, and dW is written (accumulate = 0) or added once.
+ * slots: host array of n distinct B-done slots; all are freed.  Needs n_slots >= 2.
+ * Equal to n slip_backward_weight calls up to fp32 summation order. */
+slip_status slip_backward_weight_multi(slip_ctx* ctx, const int32_t* slots, int32_t n, int32_t accumulate,
+                                       slip_stream s);
+
 /* Coupled backward (the conventional baseline): B then W
  * of the same slot back to back. */
 slip_status slip_backward_coupled(slip_ctx* ctx, int32_t slot, const void* dy, void* dx, int32_t accumulate,

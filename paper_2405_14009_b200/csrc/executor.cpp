@@ -10,6 +10,7 @@
 // slot.dx holds the input gradient B produces and SEND_DX ships.  Events: `freed` (W
 // done) guards slot.x, `sent_y` guards slot.dy, `sent_dx` guards slot.dx.
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -71,6 +72,11 @@ extern "C" slip_status slip_execute_schedule(slip_ctx* ctx, slip_comm* comm, con
                                              slip_report* out) {
   SLIP_CHECK(ctx && ctx->bound, SLIP_EINVAL, "execute: ctx not bound");
   SLIP_CHECK(comm && comm->ready, SLIP_EINVAL, "execute: comm not set up (slip_comm_setup)");
+  // SLIP_NO_MERGE_W=1: one launch per W action (A/B measurements)
+  static const bool merge_w_ = [] {
+    const char* e = std::getenv("SLIP_NO_MERGE_W");
+    return !(e && e[0] == '1');
+  }();
   SLIP_CHECK(costs && opts && adam && out, SLIP_EINVAL, "execute: NULL argument");
   SLIP_CHECK(warmup >= 0 && iterations >= 1, SLIP_EINVAL, "execute: iterations must be >= 1");
   Cluster cl;
@@ -95,6 +101,8 @@ extern "C" slip_status slip_execute_schedule(slip_ctx* ctx, slip_comm* comm, con
   SLIP_CUDA(tpool.get(&t0));
   SLIP_CUDA(tpool.get(&t1));
   std::vector<std::pair<int, size_t>> marks;  // (phase, index of the begin event in tpool)
+  std::vector<std::pair<size_t, int>> mark_extra;  // (mark, extra ops it covers): merged W's
+  int w_extra = 0;
   std::vector<std::pair<slip_trace_rec, size_t>> tmarks;  // trace records, begin event index
   const bool tracing = ctx->trace_on;
   int64_t launches0 = ctx->launches;
@@ -156,7 +164,11 @@ extern "C" slip_status slip_execute_schedule(slip_ctx* ctx, slip_comm* comm, con
       pend.iter = -1;
       return SLIP_OK;
     };
-    for (const slip_action& a : progs[me]) {
+    const std::vector<slip_action>& prog = progs[me];
+    size_t skip_to = 0;  // W actions already run by a merged W launch
+    for (size_t ai = 0; ai < prog.size(); ++ai) {
+      if (ai < skip_to) continue;
+      const slip_action& a = prog[ai];
       const int ph = phase_of(a.kind);
       if (ctx->validate && (a.kind == SLIP_ACT_W || a.kind == SLIP_ACT_BC)) SLIP_TRY(flush_rollback(a.iter));
       // tracing: begin / end events on the stream the action runs on
@@ -306,13 +318,35 @@ extern "C" slip_status slip_execute_schedule(slip_ctx* ctx, slip_comm* comm, con
           SLIP_CUDA(cudaEventRecord(se->sent_dx, ps));
           break;
         }
-        case SLIP_ACT_W:
+        case SLIP_ACT_W: {
+          // W actions the program puts back to back (same iteration; e.g. the deferred W's of
+          // the cool-down) run as ONE grouped launch over their slots (K = n T): each dW is
+          // accumulated in TMEM and written once instead of read-modified-written per W
+          size_t run = 1;
+          if (merge_w_ && !ctx->validate && ctx->n_slots >= 2)
+            while (ai + run < prog.size() && run < 8 && prog[ai + run].kind == SLIP_ACT_W &&
+                   prog[ai + run].iter == a.iter)
+              ++run;
           SLIP_CUDA(trace_begin());
-          SLIP_TRY(slip_backward_weight(ctx, a.slot, a.accumulate, stream));
-          SLIP_CUDA(pool.get(&se->freed));
-          SLIP_CUDA(cudaEventRecord(se->freed, cs));
-          if (timed) out->w_gemm_launches += 1;  // one grouped launch of all 4L products
+          if (run == 1) {
+            SLIP_TRY(slip_backward_weight(ctx, a.slot, a.accumulate, stream));
+          } else {
+            int slots[8];
+            for (size_t j = 0; j < run; ++j) slots[j] = prog[ai + j].slot;
+            SLIP_TRY(weight_multi(ctx, slots, static_cast<int>(run), a.accumulate, cs));
+          }
+          for (size_t j = 0; j < run; ++j) {
+            SlotEv& sj = sev[prog[ai + j].slot];
+            SLIP_CUDA(pool.get(&sj.freed));
+            SLIP_CUDA(cudaEventRecord(sj.freed, cs));
+          }
+          if (timed) {
+            out->w_gemm_launches += 1;  // one grouped launch of all 4L products (of `run` slots)
+            w_extra = static_cast<int>(run) - 1;  // the phase mark stands for `run` W's
+          }
+          skip_to = ai + run;
           break;
+        }
         case SLIP_ACT_AR:
           if (comm->stage_comm) {
             SLIP_CUDA(chain(cs, comm->ar_stream));
@@ -355,6 +389,8 @@ extern "C" slip_status slip_execute_schedule(slip_ctx* ctx, slip_comm* comm, con
           return SLIP_EINVAL;
       }
       if (marked) SLIP_CUDA(cudaEventRecord(tpool.ev[marks.back().second + 1], ts));
+      if (marked && w_extra > 0) mark_extra.push_back({marks.size() - 1, w_extra});
+      w_extra = 0;
       if (tr) {
         SLIP_CUDA(cudaEventRecord(tpool.ev[tb_idx + 1], ts));
         slip_trace_rec rec{a.kind, a.mb, a.origin, a.iter, a.peer, a.slot, 0.f, 0.f};
@@ -387,6 +423,7 @@ extern "C" slip_status slip_execute_schedule(slip_ctx* ctx, slip_comm* comm, con
       ctx->trace.push_back(tm.first);
     }
   }
+  for (const auto& me : mark_extra) out->phase_ops[marks[me.first].first] += me.second;
   for (const auto& mk : marks) {
     float e = 0.f;
     SLIP_CUDA(cudaEventElapsedTime(&e, tpool.ev[mk.second], tpool.ev[mk.second + 1]));

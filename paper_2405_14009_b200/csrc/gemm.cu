@@ -14,6 +14,7 @@
 #include <atomic>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <string>
@@ -72,6 +73,11 @@ struct KParams {
   __nv_bfloat16* aux;
   float alpha;
   int accumulate;
+  // grouped mode: the contraction runs over kz_n operand batches (zi = kz_list[j], each
+  // kz_nkb k-blocks) into ONE accumulator — the W of several micro-batches in one launch
+  int kz_n, kz_nkb;
+  int kz_list[8];
+  int band;  // grouped tile order: m-tile band width
   const GroupEntry* groups;  // grouped mode: problem table in device memory (nullptr otherwise)
   int n_groups;
   // stream-K (see GemmDesc)
@@ -119,10 +125,27 @@ __device__ __forceinline__ Tile decode_tile(int t, const KParams& p) {
     r.M = ge.M;
     r.N = ge.N;
     r.zi = r.zo = 0;
-    r.m0 = (q % ge.mt) * TM;
-    r.n0 = (q / ge.mt) * BN;
+    // tiles in bands of GM m-tiles, n-major inside a band: the ~74 tiles in flight touch
+    // ~GM A slabs and ~74/GM B slabs, which stay in L2 while the pairs walk K together
+    // (plain m-fastest order spread them over every A slab of the problem: with K = 4T
+    // the W launch re-read its operands ~4x from DRAM)
+    const int GM = p.band;
+    const int nt = (ge.N + BN - 1) / BN;
+    const int whole = ge.mt / GM * GM;  // m tiles in full bands
+    int mb, nb;
+    if (q < whole * nt) {
+      const int band = q / (GM * nt), l = q - band * (GM * nt);
+      mb = band * GM + l % GM;
+      nb = l / GM;
+    } else {
+      const int l = q - whole * nt, gm = ge.mt - whole;
+      mb = whole + l % gm;
+      nb = l / gm;
+    }
+    r.m0 = mb * TM;
+    r.n0 = nb * BN;
     r.kb0 = 0;
-    r.kb1 = ge.nkb;
+    r.kb1 = ge.nkb * (p.kz_n > 1 ? p.kz_n : 1);
     return r;
   }
   r.g = -1;
@@ -310,36 +333,39 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           ptx::mbar_wait(&empty[stage], phase ^ 1);
           uint8_t* sa = ring + stage * C::STAGE_BYTES;
           uint8_t* sb = sa + C::A_BYTES;
+          const int kzj = p.kz_n > 1 ? kb / p.kz_nkb : 0;
+          const int kc = (p.kz_n > 1 ? kb - kzj * p.kz_nkb : kb) * BK;  // k coordinate
+          const int zc = p.kz_n > 1 ? p.kz_list[kzj] : tl.zi;          // operand batch
           if (PAIR) {
             if (cta == 0) ptx::mbar_arrive_expect_tx(&full[stage], 2 * C::STAGE_BYTES);
             else ptx::mbar_arrive_leader(&full[stage]);
             if (!A_MN) {
-              ptx::tma_load_4d_pair(mA, sa, &full[stage], kb * BK, am0, tl.zi, tl.zo);
+              ptx::tma_load_4d_pair(mA, sa, &full[stage], kc, am0, zc, tl.zo);
             } else {
-              ptx::tma_load_4d_pair(mA, sa, &full[stage], am0, kb * BK, tl.zi, tl.zo);
-              ptx::tma_load_4d_pair(mA, sa + 8192, &full[stage], am0 + 64, kb * BK, tl.zi, tl.zo);
+              ptx::tma_load_4d_pair(mA, sa, &full[stage], am0, kc, zc, tl.zo);
+              ptx::tma_load_4d_pair(mA, sa + 8192, &full[stage], am0 + 64, kc, zc, tl.zo);
             }
             if (!B_MN) {
-              ptx::tma_load_4d_pair(mB, sb, &full[stage], kb * BK, bn0, tl.zi, tl.zo);
+              ptx::tma_load_4d_pair(mB, sb, &full[stage], kc, bn0, zc, tl.zo);
             } else {
 #pragma unroll
               for (int a = 0; a < C::B_ATOMS; ++a)
-                ptx::tma_load_4d_pair(mB, sb + a * 8192, &full[stage], bn0 + a * 64, kb * BK, tl.zi, tl.zo);
+                ptx::tma_load_4d_pair(mB, sb + a * 8192, &full[stage], bn0 + a * 64, kc, zc, tl.zo);
             }
           } else {
             ptx::mbar_arrive_expect_tx(&full[stage], C::STAGE_BYTES);
             if (!A_MN) {
-              ptx::tma_load_4d(mA, sa, &full[stage], kb * BK, am0, tl.zi, tl.zo);
+              ptx::tma_load_4d(mA, sa, &full[stage], kc, am0, zc, tl.zo);
             } else {
-              ptx::tma_load_4d(mA, sa, &full[stage], am0, kb * BK, tl.zi, tl.zo);
-              ptx::tma_load_4d(mA, sa + 8192, &full[stage], am0 + 64, kb * BK, tl.zi, tl.zo);
+              ptx::tma_load_4d(mA, sa, &full[stage], am0, kc, zc, tl.zo);
+              ptx::tma_load_4d(mA, sa + 8192, &full[stage], am0 + 64, kc, zc, tl.zo);
             }
             if (!B_MN) {
-              ptx::tma_load_4d(mB, sb, &full[stage], kb * BK, bn0, tl.zi, tl.zo);
+              ptx::tma_load_4d(mB, sb, &full[stage], kc, bn0, zc, tl.zo);
             } else {
 #pragma unroll
               for (int a = 0; a < C::B_ATOMS; ++a)
-                ptx::tma_load_4d(mB, sb + a * 8192, &full[stage], bn0 + a * 64, kb * BK, tl.zi, tl.zo);
+                ptx::tma_load_4d(mB, sb + a * 8192, &full[stage], bn0 + a * 64, kc, zc, tl.zo);
             }
           }
           if (++stage == C::STAGES) {
@@ -720,6 +746,16 @@ cudaError_t launch_t(const GemmDesc& d, cudaStream_t s, const GroupEntry* groups
     p.groups = groups;
     p.n_groups = n_groups;
     p.total = group_tiles;
+    p.band = 8;  // measured: 2 / 4 / 8 / 16 / 32 -> W 15.03 / 14.93 / 14.74 / 14.84 / 15.06 ms
+    if (d.kz_n > 1) {
+      if (d.kz_n > 8 || d.kz_nkb <= 0) {
+        g_msg = "gemm_group: kz_n must be in [2, 8] with kz_nkb > 0";
+        return cudaErrorInvalidValue;
+      }
+      p.kz_n = d.kz_n;
+      p.kz_nkb = d.kz_nkb;
+      for (int j = 0; j < d.kz_n; ++j) p.kz_list[j] = d.kz_list[j];
+    }
     return launch_kernel<BN, A_MN, B_MN, PAIR>(ta, tb, tc, tc, p, s);
   }
   if (!encode_operand(&ta, d.a, d.M, d.K, d.zi_count, d.zo_count, BM)) return cudaErrorInvalidValue;
@@ -869,16 +905,18 @@ cudaError_t gemm_group_encode(const GemmDesc* probs, int n, GroupEntry* out, int
   for (int i = 0; i < n; ++i) {
     const GemmDesc& d = probs[i];
     if (d.bn != probs[0].bn || d.a.mn_major != probs[0].a.mn_major || d.b.mn_major != probs[0].b.mn_major ||
-        d.mode != probs[0].mode || d.mode < EPI_F32_STORE || d.zi_count != 1 || d.zo_count != 1 ||
+        d.mode != probs[0].mode || d.mode < EPI_F32_STORE || d.zi_count < 1 || d.zo_count != 1 ||
         d.causal != CAUSAL_NONE) {
-      g_msg = "gemm_group: problems must share BN, majorness and an fp32 epilogue, without batching";
+      g_msg = "gemm_group: problems must share BN, majorness and an fp32 epilogue, without output batching";
       return cudaErrorInvalidValue;
     }
     GroupEntry& g = out[i];
     std::memset(&g, 0, sizeof g);
-    if (!encode_operand(&g.ta, d.a, d.M, d.K, 1, 1, BM)) return cudaErrorInvalidValue;
+    // zi_count > 1: operand batches the contraction may run over (GemmDesc::kz_*); the
+    // output has none
+    if (!encode_operand(&g.ta, d.a, d.M, d.K, d.zi_count, 1, BM)) return cudaErrorInvalidValue;
     const uint32_t b_rows = (probs[0].pair && probs[0].bn == 256) ? 128u : static_cast<uint32_t>(d.bn);
-    if (!encode_operand(&g.tb, d.b, d.N, d.K, 1, 1, b_rows)) return cudaErrorInvalidValue;
+    if (!encode_operand(&g.tb, d.b, d.N, d.K, d.zi_count, 1, b_rows)) return cudaErrorInvalidValue;
     if (!encode4d(&g.tc, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, d.c, d.N, d.M, 1, 1, d.ldc, 0, 0, 32, 32))
       return cudaErrorInvalidValue;
     const int tile_m = (probs[0].pair && probs[0].bn == 256) ? 2 * BM : BM;

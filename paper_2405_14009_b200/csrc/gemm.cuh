@@ -59,6 +59,11 @@ struct GemmDesc {
   // sk_ws: gemm_sk_bytes() bytes, sk_flags: num_sms() zero-initialised words; NULL: off.
   float* sk_ws = nullptr;
   unsigned* sk_flags = nullptr;
+  // Grouped launches (gemm_group_launch proto): the contraction runs over kz_n operand
+  // batches — zi = kz_list[j] of the A / B maps (encoded with zi_count > 1), kz_nkb
+  // k-blocks each — into one accumulator (the W of several micro-batches, slot = zi).
+  int kz_n = 0, kz_nkb = 0;
+  int kz_list[8] = {};
 };
 size_t gemm_sk_bytes();
 

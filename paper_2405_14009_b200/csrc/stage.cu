@@ -162,6 +162,7 @@ void carve_slot(Carver& cv, const Dims& d, int L, SlotBufs* out) {
   }
   sb.wtab = cv.take<GroupEntry>(4 * static_cast<size_t>(L) + 1);
   sb.wtab_tiles = 0;
+  sb.wtab_all = cv.take<GroupEntry>(4 * static_cast<size_t>(L) + 1);
   if (out) *out = sb;
 }
 
@@ -617,6 +618,22 @@ slip_status slip_stage_bind(slip_ctx* c, void* w_bf16, float* master, float* gra
     SLIP_CUDA(cudaMemcpy(c->slots[i].wtab, host.data(), host.size() * sizeof(GroupEntry), cudaMemcpyHostToDevice));
     c->slots[i].wtab_tiles = tiles;
   }
+  if (c->n_slots >= 2) {  // slot 0's problems with the slot as the operands' zi dimension
+    std::vector<GemmDesc> probs = w_problems(c, 0);
+    const int64_t zs = static_cast<int64_t>(per / sizeof(bf16));
+    for (GemmDesc& d : probs) {
+      d.zi_count = c->n_slots;
+      d.a.zi_stride = zs;
+      d.b.zi_stride = zs;
+    }
+    int tiles = 0;
+    cudaError_t e = gemm_group_encode(probs.data(), static_cast<int>(probs.size()), host.data(), &tiles);
+    if (e != cudaSuccess) {
+      set_error(std::string("stage_bind: W all-slot table: ") + gemm_last_message());
+      return SLIP_EUNSUPPORTED;
+    }
+    SLIP_CUDA(cudaMemcpy(c->slots[0].wtab_all, host.data(), host.size() * sizeof(GroupEntry), cudaMemcpyHostToDevice));
+  }
   c->state.assign(c->n_slots, SLOT_FREE);
   c->bound = true;
   return SLIP_OK;
@@ -666,6 +683,51 @@ slip_status slip_backward_input(slip_ctx* c, int32_t slot, const void* dy, void*
   SLIP_TRY(backward_input_impl(c, slot, dy, dx, accumulate, reinterpret_cast<cudaStream_t>(st)));
   c->state[slot] = SLOT_B_DONE;
   return SLIP_OK;
+}
+
+}  // extern "C"
+
+namespace slip {
+slip_status weight_multi(slip_ctx* c, const int* slots, int n, int accumulate, cudaStream_t s) {
+  SLIP_CHECK(c && slots && n >= 2 && n <= 8 && c->n_slots >= 2, SLIP_EINVAL, "weight_multi: bad arguments");
+  for (int j = 0; j < n; ++j) SLIP_TRY(slot_check(c, slots[j], SLOT_B_DONE));
+  GemmDesc proto;
+  proto.bn = 256;
+  proto.a.mn_major = proto.b.mn_major = true;
+  proto.mode = EPI_F32_ACC;
+  proto.accumulate = accumulate;
+  proto.kz_n = n;
+  proto.kz_nkb = (c->dm.T + 63) / 64;
+  for (int j = 0; j < n; ++j) proto.kz_list[j] = slots[j];
+  const int n_probs = 4 * c->L + ((c->dm.ends & 2) ? 1 : 0);
+  cudaError_t e = gemm_group_launch(c->slots[0].wtab_all, n_probs, c->slots[0].wtab_tiles, proto, s);
+  if (e != cudaSuccess) {
+    set_error(std::string("W multi launch: ") + cudaGetErrorString(e) + " " + gemm_last_message());
+    return SLIP_ECUDA;
+  }
+  c->launches += 1;
+  for (int j = 0; j < n; ++j) {
+    SlotBufs& sb = c->slots[slots[j]];
+    if (c->dm.ends & 1)  // embedding scatter of each slot's stage-input gradient
+      SLIP_TRY(kcheck(c,
+                      embed_bwd(sb.dx, sb.end.tokens, c->grad + c->eo.E, c->grad + c->eo.P, c->dm.T, c->dm.h, c->dm.s,
+                                accumulate || j > 0, s),
+                      "embed_bwd"));
+    c->state[slots[j]] = SLOT_FREE;
+  }
+  return SLIP_OK;
+}
+}  // namespace slip
+
+extern "C" {
+
+slip_status slip_backward_weight_multi(slip_ctx* c, const int32_t* slots, int32_t n, int32_t accumulate,
+                                       slip_stream st) {
+  SLIP_CHECK(c && c->bound && slots, SLIP_EINVAL, "backward_weight_multi: bad arguments");
+  std::vector<int> v(slots, slots + (n > 0 ? n : 0));
+  for (int j = 0; j < n; ++j)
+    for (int k = 0; k < j; ++k) SLIP_CHECK(v[j] != v[k], SLIP_EINVAL, "backward_weight_multi: repeated slot");
+  return weight_multi(c, v.data(), n, accumulate, reinterpret_cast<cudaStream_t>(st));
 }
 
 slip_status slip_backward_weight(slip_ctx* c, int32_t slot, int32_t accumulate, slip_stream st) {

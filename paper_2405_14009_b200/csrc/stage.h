@@ -46,6 +46,8 @@ struct SlotBufs {
   EndStash end;
   GroupEntry* wtab;  // device table of the slot's W problems (4L, + dWout with the LM head)
   int wtab_tiles;
+  GroupEntry* wtab_all;  // (slot 0 only) the same problems over ALL slots (zi = slot) for a
+                         // W of several micro-batches in one launch (weight_multi)
 };
 
 struct Workspace {
@@ -114,6 +116,11 @@ Dims make_dims(const slip_model& m);
 size_t stash_bytes_per_slot(const Dims& d, int L);
 EndOffsets end_offsets(const Dims& d, int64_t base);
 size_t workspace_bytes(const Dims& d);
+
+// The W of n (2..8) B-done slots in ONE grouped launch: every dW accumulates the n
+// micro-batches' products in TMEM (K = n*T) and is written (or added) once.  Releases
+// the slots.
+slip_status weight_multi(slip_ctx* c, const int* slots, int n, int accumulate, cudaStream_t s);
 slip_status validated_step(slip_ctx* c, const slip_adam* a, int64_t step, float grad_scale, int32_t* own, int fault,
                            cudaStream_t s);
 slip_status rollback_if(slip_ctx* c, const slip_adam* a, int64_t step, float grad_scale, const int32_t* glob,

@@ -269,6 +269,11 @@ class Stage:
     def backward_weight(self, slot, accumulate=False, stream=None):
         call("slip_backward_weight", self.ctx, slot, int(accumulate), _stream(stream))
 
+    def backward_weight_multi(self, slots, accumulate=False, stream=None):
+        arr = (C.c_int32 * len(slots))(*slots)
+        call("slip_backward_weight_multi", self.ctx, C.cast(arr, C.c_void_p), len(slots), int(accumulate),
+             _stream(stream))
+
     def backward_coupled(self, slot, dy, dx=None, accumulate=False, stream=None):
         call("slip_backward_coupled", self.ctx, slot, _ptr(dy), _ptr(dx) if dx is not None else None,
              int(accumulate), _stream(stream))

@@ -144,6 +144,37 @@ def test_stream_k_stage_matches_oracle():
         assert relerr(g[0][n], grads[0][n]) <= GATE_A, n
 
 
+@pytest.mark.parametrize("name", ["c1", "d80_ragged"])
+def test_weight_multi_matches_oracle(name):
+    """slip_backward_weight_multi: the W of 3 micro-batches in one launch (K = 3T over the
+    slots) equals the oracle's summed weight gradients; biases / LayerNorm come from B."""
+    cfg, L = CFGS[name]
+    rt = _rt()
+    layers = sd.stage_params(cfg, 0, L, total_layers=max(L, 2))
+    st = rt.Stage(cfg, L, n_slots=4)
+    st.load_master(torch.from_numpy(sd.pack_stage(layers)).float().cuda())
+    ref = None
+    order = [2, 0, 3]  # slots used out of order
+    for j, slot in enumerate(order):
+        x, r = sd.stage_input(cfg, 0, j), sd.stage_target(cfg, 0, j)
+        y = torch.empty(cfg.tokens, cfg.hidden, dtype=torch.bfloat16, device="cuda")
+        st.forward(slot, to_dev_bf16(x), y)
+        st.backward_input(slot, to_dev_bf16(r), None, accumulate=j > 0)
+        out, c = OL.stage_forward(layers, x, cfg)
+        _, g = OL.stage_backward_coupled(layers, c, r, cfg)
+        ref = g if ref is None else [{n: a[n] + b[n] for n in a} for a, b in zip(ref, g)]
+    st.backward_weight_multi(order, accumulate=False)
+    torch.cuda.synchronize()
+    got = sd.unpack_stage(st.grad.cpu().numpy().astype(np.float64), cfg, L)
+    for l in range(L):
+        for n in sd.PARAM_ORDER:
+            assert relerr(got[l][n], ref[l][n]) <= GATE_A, (name, l, n)
+    # the slots are free again
+    x = sd.stage_input(cfg, 0, 0)
+    y = torch.empty(cfg.tokens, cfg.hidden, dtype=torch.bfloat16, device="cuda")
+    st.forward(2, to_dev_bf16(x), y)
+
+
 def test_slot_state_machine():
     rt = _rt()
     cfg = sd.C1_TINY
