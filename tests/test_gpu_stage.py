@@ -366,3 +366,37 @@ def test_stage_with_gpt_ends_matches_oracle(name):
     if cfg.ends & 2:
         assert relerr(ge["gf"], hb["gf"]) <= GATE_A and relerr(ge["bf"], hb["bf"]) <= GATE_A
         assert relerr(ge["Wout"], OE.head_backward_weight(hws)["Wout"]) <= GATE_A
+
+
+def test_weight_multi_with_gpt_ends_equals_separate_w():
+    """The merged W (slip_backward_weight_multi) with both model ends — dWout in the grouped
+    launch, embedding scatter per slot — equals separate per-slot W calls up to fp32
+    summation order (the separate path is pinned to the oracle above)."""
+    rt = _rt()
+    cfg, L = ENDS_CFGS["d128_both"]
+    layers = sd.stage_params(cfg, 0, L, total_layers=max(L, 2))
+    flat = np.concatenate([sd.pack_stage(layers), sd.pack_ends(sd.end_params(cfg, 0))])
+    T, h = cfg.tokens, cfg.hidden
+    grads = []
+    for merged in (False, True):
+        st = rt.Stage(cfg, L, n_slots=3)
+        st.load_master(torch.from_numpy(flat).float().cuda())
+        for j, slot in enumerate((1, 2)):
+            tok = torch.from_numpy(sd.stage_tokens(cfg, 0, j)).cuda()
+            lab = torch.from_numpy(sd.stage_labels(cfg, 0, j)).cuda()
+            y = torch.empty(T, h, dtype=torch.bfloat16, device="cuda")
+            dy, dx = torch.empty_like(y), torch.empty_like(y)
+            loss = torch.zeros(1, device="cuda")
+            st.forward(slot, tok, y)
+            st.loss_ce(slot, y, lab, dy, loss)
+            st.backward_input(slot, dy, dx, accumulate=j > 0)
+        if merged:
+            st.backward_weight_multi([2, 1], accumulate=False)
+        else:
+            st.backward_weight(1, accumulate=False)
+            st.backward_weight(2, accumulate=True)
+        torch.cuda.synchronize()
+        grads.append(st.grad.clone())
+    a, b = grads
+    assert torch.isfinite(b).all()
+    assert ((a - b).abs().max() / a.abs().max()).item() <= 1e-5
