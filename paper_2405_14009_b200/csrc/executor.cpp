@@ -12,6 +12,7 @@
 #include <algorithm>
 #include <cstdlib>
 #include <cstring>
+#include <map>
 #include <string>
 #include <vector>
 
@@ -62,6 +63,19 @@ int phase_of(int kind) {
     default: return -1;
   }
 }
+
+// last plan + rank programs per context and horizon slot (warm-up / timed)
+struct ExecCache {
+  bool valid = false;
+  int N = 0, DP = 0, m = 0, me = -1;
+  std::vector<uint8_t> live;
+  slip_costs costs{};
+  slip_plan_opts opts{};
+  Plan plan;
+  std::vector<std::vector<slip_action>> progs;
+  int need = 0;
+};
+std::map<std::pair<const slip_ctx*, int>, ExecCache> exec_cache_;
 
 }  // namespace
 
@@ -118,17 +132,38 @@ extern "C" slip_status slip_execute_schedule(slip_ctx* ctx, slip_comm* comm, con
     const bool timed = run == 1;
     slip_plan_opts po = *opts;
     po.horizon = H;
-    Plan plan;
-    SLIP_TRY(slip::plan(cl, *costs, po, plan));
-    // programs of every rank (cheap): mine to run, all of them to check pair FIFO order
-    std::vector<std::vector<slip_action>> progs(N * DP);
-    int need = 0;
-    for (int r = 0; r < N * DP; ++r) {
-      int ns = 0;
-      SLIP_TRY(build_program(cl, plan, H, r, progs[r], ns));
-      if (r == me) need = ns;
+    // The plan and the rank programs depend only on (cluster, costs, options, horizon):
+    // a repeated call (one call per step in e2e use) reuses them instead of re-planning
+    // on the host while the GPU idles (~1 ms per rank program at N = 8).
+    ExecCache& ec = exec_cache_[{ctx, run}];
+    const bool hit = ec.valid && ec.N == cl.N && ec.DP == cl.DP && ec.m == cl.m && ec.live == cl.live &&
+                     ec.me == me && std::memcmp(&ec.costs, costs, sizeof(slip_costs)) == 0 &&
+                     std::memcmp(&ec.opts, &po, sizeof(slip_plan_opts)) == 0;
+    if (!hit) {
+      ec.valid = false;
+      ec.plan = Plan();
+      SLIP_TRY(slip::plan(cl, *costs, po, ec.plan));
+      // programs of every rank (cheap): mine to run, all of them to check pair FIFO order
+      ec.progs.assign(N * DP, {});
+      ec.need = 0;
+      for (int r = 0; r < N * DP; ++r) {
+        int ns = 0;
+        SLIP_TRY(build_program(cl, ec.plan, H, r, ec.progs[r], ns));
+        if (r == me) ec.need = ns;
+      }
+      SLIP_CHECK(check_fifo(cl, ec.progs, me), SLIP_ESTATE, "execute: plan violates per-pair FIFO order");
+      ec.N = cl.N;
+      ec.DP = cl.DP;
+      ec.m = cl.m;
+      ec.live = cl.live;
+      ec.me = me;
+      ec.costs = *costs;
+      ec.opts = po;
+      ec.valid = true;
     }
-    SLIP_CHECK(check_fifo(cl, progs, me), SLIP_ESTATE, "execute: plan violates per-pair FIFO order");
+    const Plan& plan = ec.plan;
+    const std::vector<std::vector<slip_action>>& progs = ec.progs;
+    const int need = ec.need;
     SLIP_CHECK(need <= ctx->n_slots, SLIP_EINVAL,
                ("execute: the plan needs " + std::to_string(need) + " slots, ctx has " +
                 std::to_string(ctx->n_slots))
