@@ -213,14 +213,14 @@ __device__ __forceinline__ ItemIter item_begin(const KParams& p, int u) {
   return st;
 }
 
-__device__ __forceinline__ float gelu_f(float x) {
-  const float c = 0.7978845608028654f, a = 0.044715f;
-  return 0.5f * x * (1.0f + ptx::tanh_fast(c * (x + a * x * x * x)));
-}
-__device__ __forceinline__ float gelu_grad_f(float x) {
+// gelu(x) and gelu'(x) from one tanh: the forward stores gelu'(H) as the F-stash, so the
+// backward epilogue (dH = dG * gelu'(H)) is a multiply instead of a tanh + polynomial
+// that paced the FC2 input-gradient GEMM
+__device__ __forceinline__ void gelu_and_grad(float x, float& g, float& dg) {
   const float c = 0.7978845608028654f, a = 0.044715f;
   const float t = ptx::tanh_fast(c * (x + a * x * x * x));
-  return 0.5f * (1.0f + t) + 0.5f * x * (1.0f - t * t) * c * (1.0f + 3.0f * a * x * x);
+  g = 0.5f * x * (1.0f + t);
+  dg = 0.5f * (1.0f + t) + 0.5f * x * (1.0f - t * t) * c * (1.0f + 3.0f * a * x * x);
 }
 
 __device__ __forceinline__ void st_shared_u4(uint32_t addr, const uint4& v) {
@@ -576,14 +576,15 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             }
             const uint32_t soff = lane * 64 + ((it ^ ((lane >> 1) & 3)) << 4);
             if (e_mode == EPI_BF16_GELU) {
-              st_shared_u4(sx_s + soff, pack8(x));
+              float dg[8];
 #pragma unroll
-              for (int e = 0; e < 8; ++e) x[e] = gelu_f(x[e]);
+              for (int e = 0; e < 8; ++e) gelu_and_grad(x[e], x[e], dg[e]);
+              st_shared_u4(sx_s + soff, pack8(dg));
             } else if (e_mode == EPI_BF16_DGELU) {
               float hv[8];
               unpack8(hn[it], hv);
 #pragma unroll
-              for (int e = 0; e < 8; ++e) x[e] *= gelu_grad_f(hv[e]);
+              for (int e = 0; e < 8; ++e) x[e] *= hv[e];
             }
             if (e_resid) {
               float rv[8];

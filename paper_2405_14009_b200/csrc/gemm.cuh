@@ -15,8 +15,8 @@ namespace slip {
 
 enum EpiMode : int {
   EPI_BF16 = 0,        // C = bf16(alpha*acc + bias[n] + resid[m,n])
-  EPI_BF16_GELU = 1,   // H = alpha*acc + bias[n]; aux = bf16(H); C = bf16(gelu(H))
-  EPI_BF16_DGELU = 2,  // C = bf16(acc * gelu'(aux[m,n]))
+  EPI_BF16_GELU = 1,   // H = alpha*acc + bias[n]; aux = bf16(gelu'(H)); C = bf16(gelu(H))
+  EPI_BF16_DGELU = 2,  // C = bf16(acc * aux[m,n])   (aux = gelu'(H) from EPI_BF16_GELU)
   EPI_F32_STORE = 3,   // C(f32) = alpha*acc                  (TMA store)
   EPI_F32_ACC = 4      // C(f32) += acc, or = acc if !accumulate (TMA reduce-add / store)
 };

@@ -259,7 +259,7 @@ slip_status linear_fwd(slip_ctx* c, const bf16* X, const bf16* W, int N, int K, 
   return run_gemm(c, d, s, "linear_fwd");
 }
 
-// dX[T, K] = dY[T, N] W[N, K]   (mode: EPI_BF16 or EPI_BF16_DGELU with aux = H)
+// dX[T, K] = dY[T, N] W[N, K]   (mode: EPI_BF16 or EPI_BF16_DGELU with aux = gelu'(H))
 slip_status linear_dx(slip_ctx* c, const bf16* dY, const bf16* W, int N, int K, bf16* dX, int mode, bf16* aux,
                       cudaStream_t s) {
   GemmDesc d;

@@ -22,7 +22,7 @@ struct ParamOffsets {
 ParamOffsets param_offsets(int h, int f);
 
 struct LayerStash {
-  bf16 *xin, *y1, *qkv, *o, *x2, *y2, *hpre, *g;  // F-stash
+  bf16 *xin, *y1, *qkv, *o, *x2, *y2, *hpre, *g;  // F-stash (hpre = gelu'(H), B's GeLU derivative)
   float* lse;                                       // [z, s] attention log-sum-exp (replaces P)
   float *mean1, *rstd1, *mean2, *rstd2;
   bf16 *dout, *dh, *dx2, *dqkv;                          // W-stash (with y1, o, y2, g)
