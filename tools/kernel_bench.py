@@ -1,7 +1,7 @@
 """Per-op timing of one GPT-shaped stage on one B200 (CUDA events), and a short
 fixed launch sequence for ncu captures.
 
-    python tools/kernel_bench.py [--cfg c2|c3|c5] [--layers 1] [--reps 10] [--once]
+    python tools/kernel_bench.py [--cfg c2|c3|c5] [--layers 1] [--reps 10] [--once | --phases]
 
 --once runs F, B, W exactly once each after one warm-up (for `ncu -k regex:... -s/-c`).
 Prints one JSON line: ms per op and TFLOP/s of the W GEMMs (4 per layer)."""
@@ -26,6 +26,9 @@ def main():
     ap.add_argument("--layers", type=int, default=1)
     ap.add_argument("--reps", type=int, default=10)
     ap.add_argument("--once", action="store_true")
+    ap.add_argument("--phases", action="store_true",
+                    help="F, B, W, AdamW once each between marker kernels, inside cudaProfilerStart/Stop "
+                         "(ncu --profile-from-start off; summarise with tools/ncu_summary.py phases)")
     ap.add_argument("--no-sk", action="store_true", help="disable stream-K for the F / B linears")
     ap.add_argument("--sk", action="store_true", help="enable (hybrid) stream-K for the F / B linears")
     ap.add_argument("--profile", action="store_true",
@@ -56,6 +59,25 @@ def main():
     if a.once:
         step()
         torch.cuda.synchronize()
+        return
+    if a.phases:
+        # F, B, W and one AdamW step once each, separated by one torch fill kernel per
+        # boundary so tools/ncu_summary.py phases can attribute every launch to its phase.
+        st.optimizer_step(1)
+        marker = torch.zeros(1, device="cuda")
+        torch.cuda.synchronize()
+        torch.cuda.profiler.start()
+        marker.fill_(1.0)
+        st.forward(0, x, y)
+        marker.fill_(2.0)
+        st.backward_input(0, dy, dx)
+        marker.fill_(3.0)
+        st.backward_weight(0)
+        marker.fill_(4.0)
+        st.optimizer_step(2)
+        marker.fill_(5.0)
+        torch.cuda.synchronize()
+        torch.cuda.profiler.stop()
         return
     if a.profile:
         from torch.profiler import ProfilerActivity, profile

@@ -2,6 +2,12 @@
 
     python tools/ncu_summary.py launches <launches.csv> [--last-fraction 0.333]
     python tools/ncu_summary.py full <report.ncu-rep>
+    python tools/ncu_summary.py phases <metrics.csv> [hbm_peak_gbs]
+
+`phases` reads the per-launch metric CSV of `ncu --profile-from-start off --csv --metrics PHASE_METRICS
+python tools/kernel_bench.py --phases` and splits it at the torch fill kernels that kernel_bench puts
+between F, B, W and AdamW: per kernel the duration, tensor-pipe % and DRAM bytes; per
+phase the time-weighted tensor-pipe % of the tensor-core kernels and the HBM GB/s of the others.
 """
 import collections
 import csv
@@ -76,7 +82,77 @@ def full(path):
     return out.getvalue()
 
 
+PHASE_METRICS = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum",
+                 "sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_active",
+                 "sm__cycles_elapsed.avg.per_second"]
+PHASES = ["F", "B", "W", "AdamW"]
+
+
+def _scale(v, unit):
+    unit = unit.lower()
+    mult = {"byte": 1, "kbyte": 1e3, "mbyte": 1e6, "gbyte": 1e9, "nsecond": 1e-9, "usecond": 1e-6,
+            "msecond": 1e-3, "second": 1, "hz": 1, "khz": 1e3, "mhz": 1e6, "ghz": 1e9, "%": 1, "": 1}
+    return v * mult.get(unit, 1)
+
+
+def phases(path, hbm_peak=6546.6):
+    rows = list(csv.reader(open(path)))
+    hdr, launches = None, collections.OrderedDict()
+    for r in rows:
+        if r and r[0] == "ID":
+            hdr = r
+            continue
+        if not hdr or len(r) != len(hdr):
+            continue
+        d = dict(zip(hdr, r))
+        k = launches.setdefault(d["ID"], {"name": d["Kernel Name"], "m": {}})
+        k["m"][d["Metric Name"]] = _scale(float(d["Metric Value"].replace(",", "")), d["Metric Unit"])
+    out = io.StringIO()
+    out.write(f"# {path}: one F / B / W / AdamW pass, ncu --clock-control none (cold caches, serialised);\n"
+              f"# tensor = sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_active; "
+              f"HBM GB/s against {hbm_peak} (MEASURED_PEAKS.json)\n")
+    phase = -1
+    per = collections.defaultdict(list)
+    for k in launches.values():
+        if "slip" not in k["name"]:  # torch fill marker between phases
+            phase += 1
+            continue
+        if 0 <= phase < len(PHASES):
+            per[PHASES[phase]].append(k)
+    for ph in PHASES:
+        ks = per.get(ph, [])
+        if not ks:
+            continue
+        out.write(f"\n## {ph}\n{'kernel':44s} {'us':>9s} {'tensor%':>8s} {'DRAM MB':>9s} {'GB/s':>8s} {'MHz':>6s}\n")
+        t_all = t_tc = w_tc = t_mem = b_mem = 0.0
+        for k in ks:
+            m = k["m"]
+            t = m.get("gpu__time_duration.sum", 0.0)
+            b = m.get("dram__bytes_read.sum", 0.0) + m.get("dram__bytes_write.sum", 0.0)
+            tp = m.get("sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_active", 0.0)
+            mhz = m.get("sm__cycles_elapsed.avg.per_second", 0.0) / 1e6
+            nm = re.sub(r"^void |slip::|<unnamed>::|\(anonymous namespace\)::", "", k["name"]).split("(")[0]
+            out.write(f"{nm[:44]:44s} {t * 1e6:9.1f} {tp:8.1f} {b / 1e6:9.1f} {b / t / 1e9 if t else 0:8.0f} "
+                      f"{mhz:6.0f}\n")
+            t_all += t
+            if "gemm_tc" in nm or "attn_" in nm:
+                t_tc += t
+                w_tc += t * tp
+            else:
+                t_mem += t
+                b_mem += b
+        out.write(f"{ph}: {t_all * 1e6:.1f} us; tensor-core kernels {t_tc * 1e6:.1f} us at "
+                  f"{w_tc / t_tc if t_tc else 0:.1f} % tensor pipe (time-weighted); other kernels "
+                  f"{t_mem * 1e6:.1f} us, {b_mem / 1e6:.1f} MB, "
+                  f"{b_mem / t_mem / 1e9 if t_mem else 0:.0f} GB/s = "
+                  f"{b_mem / t_mem / 1e9 / hbm_peak if t_mem else 0:.3f} of peak\n")
+    return out.getvalue()
+
+
 if __name__ == "__main__":
+    if sys.argv[1] == "phases":
+        print(phases(sys.argv[2], float(sys.argv[3]) if len(sys.argv) > 3 else 6546.6))
+        sys.exit(0)
     if sys.argv[1] == "launches":
         fr = float(sys.argv[3]) if len(sys.argv) > 3 else 1 / 3
         print(launches(sys.argv[2], fr))
