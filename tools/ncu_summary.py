@@ -90,7 +90,8 @@ PHASES = ["F", "B", "W", "AdamW"]
 
 def _scale(v, unit):
     unit = unit.lower()
-    mult = {"byte": 1, "kbyte": 1e3, "mbyte": 1e6, "gbyte": 1e9, "nsecond": 1e-9, "usecond": 1e-6,
+    mult = {"byte": 1, "kbyte": 1e3, "mbyte": 1e6, "gbyte": 1e9, "nsecond": 1e-9, "usecond": 1e-6, "ns": 1e-9,
+            "us": 1e-6, "ms": 1e-3,
             "msecond": 1e-3, "second": 1, "hz": 1, "khz": 1e3, "mhz": 1e6, "ghz": 1e9, "%": 1, "": 1}
     return v * mult.get(unit, 1)
 
