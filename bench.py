@@ -60,6 +60,8 @@ def parse():
     ap.add_argument("--sm-reserve", type=int, default=-1,
                     help="SMs kept free of persistent GEMM CTAs for NCCL kernels (default: 0 at N=1, 8 at N>1)")
     ap.add_argument("--p2p-ctas", type=int, default=2, help="CTAs per NCCL P2P kernel (0: NCCL default)")
+    ap.add_argument("--no-fused-ar", action="store_true",
+                    help="NCCL all-reduce + AdamW instead of the DP=2 all-reduce fused into AdamW over NVLink")
     ap.add_argument("--trace", default="", help="directory: dump one traced 2-iteration run per rank (JSON)")
     ap.add_argument("--gpt-ends", action="store_true",
                     help="GPT model ends: token + position embedding on the first stage, final LN + LM head "
@@ -282,6 +284,9 @@ def main():
     if world > 1:
         comm.set_p2p_ctas(args.p2p_ctas)
     comm.setup(PP, DP, m, live)
+    fused_ar = world > 1 and DP == 2 and not args.no_fused_ar
+    if fused_ar:
+        rt.fuse_ar_adam(stage, comm)
     stream = torch.cuda.current_stream()
 
     def allreduce_max(v):
@@ -308,7 +313,7 @@ def main():
         per.append(allreduce_max(rep.phase_ms[ph] / n if n else 0.0))
     q = lambda ms: max(1, int(round(ms * 100)))  # noqa: E731
     costs = rt.make_costs(t_f=q(per[0]), t_b=q(per[1] or per[3]), t_w=q(per[2] or 0.01), t_comm=1,
-                          t_ar=q(per[4] * 0.5 if per[4] else 0.01), t_opt=q(per[4] or 0.01))
+                          t_ar=1 if fused_ar else q(per[4] * 0.5 if per[4] else 0.01), t_opt=q(per[4] or 0.01))
     norm = None
     my_role = rank
     if args.normalize and failed:
@@ -344,6 +349,8 @@ def main():
         my_role = role[rank]
         live = after
         comm.setup(PP, DP, m, live)
+        if fused_ar:
+            rt.fuse_ar_adam(stage, comm)
         norm = {"actual_failed": failed, "R": R, "swaps": swaps, "migration_ms": mig_ms,
                 "migration_warm_ms": mig_warm_ms, "state_bytes_per_swap": 12 * stage.n_params,
                 "migration_GBps": (12 * stage.n_params / (mig_warm_ms * 1e6)) if swaps and mig_warm_ms else None,
@@ -518,7 +525,7 @@ def main():
                                    len(failed)),
                    "model": "gpt-%s-shape" % MODEL, "global_batch": DP * m * MB, "seq_len": SEQ,
                    "parallelism": "dp%dxpp%d" % (DP, PP), "failed_workers": failed, "sm_reserve": sm_reserve,
-                   "p2p_ctas": args.p2p_ctas,
+                   "p2p_ctas": args.p2p_ctas, "fused_ar_adam": fused_ar,
                    "l2": "inputs larger than L2 (2.4 GB bf16 weights + GBs of stash per step)"},
         "clocks": clk,
         "e2e": e2e,

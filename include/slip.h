@@ -378,6 +378,23 @@ slip_status slip_migrate_state(slip_ctx* ctx, slip_comm* comm, int32_t peer, int
  * singleton group returns without communicating. */
 slip_status slip_grad_allreduce(slip_ctx* ctx, slip_comm* comm, slip_stream s);
 
+/* The DP = 2 stage all-reduce fused into AdamW over NVLink (SURVEY.md §8(e)
+ * option (i); the all-reduce of PAPER.md line 561 followed by the optimizer step
+ * of line 583).  Collective over the caller's stage group; call on both live
+ * peers after slip_stage_bind and slip_comm_setup.  It maps the peer's fp32
+ * gradient buffer and a flag word into this process with CUDA IPC; afterwards
+ * slip_execute_schedule skips the NCCL all-reduce and its OPT step is a two-GPU
+ * flag barrier, ONE AdamW pass that reads g_own + g_peer (the same fp32 sum on
+ * both replicas: IEEE addition is commutative, so the result equals the NCCL
+ * all-reduce's bit for bit), and a second barrier before either peer may
+ * overwrite its gradient.  The own gradient is left un-summed.
+ * enable = 0 (or a singleton / failed group) unmaps and returns SLIP_OK;
+ * SLIP_EUNSUPPORTED for a live group of more than 2; SLIP_ECUDA if the gradient
+ * buffer is not IPC-exportable (e.g. a VMM allocation).  Validated steps
+ * (slip_set_validation) keep the NCCL all-reduce.  Re-call after re-binding the
+ * stage or re-running slip_comm_setup (which unmaps). */
+slip_status slip_comm_fuse_ar_adam(slip_ctx* ctx, slip_comm* comm, int32_t enable);
+
 /* ------------------------------------------------------------- rank programs
  * The executor interprets a per-rank program derived from the plan (host
  * logic only, no GPU): for every op of worker (i, k) in planned order, the

@@ -3,6 +3,7 @@
 #include "comm.h"
 
 #include <cstring>
+#include <cuda.h>
 #include <set>
 #include <string>
 
@@ -27,7 +28,19 @@ using namespace slip;
 
 namespace {
 
+void close_fused(slip_comm* c) {
+  if (c->ipc_grad_base) cudaIpcCloseMemHandle(c->ipc_grad_base);
+  if (c->ipc_flag_base) cudaIpcCloseMemHandle(c->ipc_flag_base);
+  if (c->flags) cudaFree(c->flags);
+  c->ipc_grad_base = c->ipc_flag_base = nullptr;
+  c->flags = c->peer_flags = nullptr;
+  c->peer_grad = c->fused_local = nullptr;
+  c->fused_ar = false;
+  c->epoch = 0;
+}
+
 void destroy_setup(slip_comm* c) {
+  close_fused(c);
   for (auto& kv : c->pair_comm)
     if (kv.second) ncclCommDestroy(kv.second);
   for (auto& kv : c->pair_stream)
@@ -190,6 +203,62 @@ slip_status slip_migrate_state(slip_ctx* ctx, slip_comm* c, int32_t peer, int32_
     ctx->opt_step = opt_step;
     SLIP_TRY(slip_weights_from_master(ctx, s));
   }
+  return SLIP_OK;
+}
+
+slip_status slip_comm_fuse_ar_adam(slip_ctx* ctx, slip_comm* c, int32_t enable) {
+  SLIP_CHECK(ctx && ctx->bound && c && c->ready, SLIP_EINVAL, "comm_fuse_ar_adam: ctx not bound or comm not set up");
+  close_fused(c);
+  if (!enable || !c->my_live || !c->stage_comm) return SLIP_OK;  // nothing to fuse (singleton group)
+  if (c->stage_size != 2) {
+    set_error("comm_fuse_ar_adam: only a stage group of 2 live peers can fuse its all-reduce");
+    return SLIP_EUNSUPPORTED;
+  }
+  // base of the allocation holding the caller's gradient buffer (torch sub-allocates)
+  using AddrRange = CUresult (*)(CUdeviceptr*, size_t*, CUdeviceptr);
+  static AddrRange range = nullptr;
+  if (!range) {
+    void* f = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    SLIP_CUDA(cudaGetDriverEntryPoint("cuMemGetAddressRange", &f, cudaEnableDefault, &q));
+    SLIP_CHECK(q == cudaDriverEntryPointSuccess && f, SLIP_ECUDA, "comm_fuse_ar_adam: no cuMemGetAddressRange");
+    range = reinterpret_cast<AddrRange>(f);
+  }
+  CUdeviceptr base = 0;
+  size_t bytes = 0;
+  SLIP_CHECK(range(&base, &bytes, reinterpret_cast<CUdeviceptr>(ctx->grad)) == CUDA_SUCCESS, SLIP_ECUDA,
+             "comm_fuse_ar_adam: cuMemGetAddressRange(grad) failed");
+  SLIP_CUDA(cudaMalloc(&c->flags, 256));
+  SLIP_CUDA(cudaMemset(c->flags, 0, 256));
+  struct Rec {
+    cudaIpcMemHandle_t grad, flag;
+    int64_t grad_off, n_params;
+  } mine{}, both[2];
+  SLIP_CUDA(cudaIpcGetMemHandle(&mine.grad, reinterpret_cast<void*>(base)));
+  SLIP_CUDA(cudaIpcGetMemHandle(&mine.flag, c->flags));
+  mine.grad_off = static_cast<int64_t>(reinterpret_cast<CUdeviceptr>(ctx->grad) - base);
+  mine.n_params = ctx->n_params;
+  void* dbuf = nullptr;
+  SLIP_CUDA(cudaMalloc(&dbuf, 3 * sizeof(Rec)));
+  SLIP_CUDA(cudaMemcpy(dbuf, &mine, sizeof(Rec), cudaMemcpyHostToDevice));
+  ncclResult_t r = ncclAllGather(dbuf, static_cast<char*>(dbuf) + sizeof(Rec), sizeof(Rec), ncclUint8, c->stage_comm,
+                                 c->ar_stream);
+  cudaError_t e = r == ncclSuccess ? cudaStreamSynchronize(c->ar_stream) : cudaSuccess;
+  if (e == cudaSuccess && r == ncclSuccess)
+    e = cudaMemcpy(both, static_cast<char*>(dbuf) + sizeof(Rec), 2 * sizeof(Rec), cudaMemcpyDeviceToHost);
+  cudaFree(dbuf);
+  if (r != ncclSuccess) return nccl_status(r, "ncclAllGather(ipc handles)");
+  SLIP_CUDA(e);
+  int me = 0;
+  SLIP_NCCL(ncclCommUserRank(c->stage_comm, &me));
+  const Rec& peer = both[1 - me];
+  SLIP_CHECK(peer.n_params == ctx->n_params, SLIP_EINVAL, "comm_fuse_ar_adam: peer holds a different stage size");
+  SLIP_CUDA(cudaIpcOpenMemHandle(&c->ipc_grad_base, peer.grad, cudaIpcMemLazyEnablePeerAccess));
+  SLIP_CUDA(cudaIpcOpenMemHandle(&c->ipc_flag_base, peer.flag, cudaIpcMemLazyEnablePeerAccess));
+  c->peer_grad = reinterpret_cast<const float*>(static_cast<char*>(c->ipc_grad_base) + peer.grad_off);
+  c->peer_flags = static_cast<unsigned*>(c->ipc_flag_base);
+  c->fused_local = ctx->grad;
+  c->fused_ar = true;
   return SLIP_OK;
 }
 

@@ -27,6 +27,16 @@ struct slip_comm {
   // directed pair (src rank, dst rank) -> communicator in which src is rank 0, dst rank 1
   std::map<std::pair<int, int>, ncclComm_t> pair_comm;
   std::map<std::pair<int, int>, cudaStream_t> pair_stream;
+  // DP = 2 all-reduce fused into AdamW (slip_comm_fuse_ar_adam): the peer's fp32
+  // gradient and barrier flag, mapped over NVLink with CUDA IPC
+  bool fused_ar = false;
+  const float* peer_grad = nullptr;
+  const float* fused_local = nullptr;  // ctx->grad when the mapping was made
+  unsigned* flags = nullptr;       // own flag word (cudaMalloc, exported to the peer)
+  unsigned* peer_flags = nullptr;  // the peer's flag word
+  void* ipc_grad_base = nullptr;   // opened IPC mappings (closed by destroy_setup)
+  void* ipc_flag_base = nullptr;
+  unsigned epoch = 0;
 };
 
 namespace slip {

@@ -108,6 +108,11 @@ extern "C" slip_status slip_execute_schedule(slip_ctx* ctx, slip_comm* comm, con
   const size_t bytes = Th * sizeof(bf16);
   const float grad_scale = 1.0f / static_cast<float>(DP * m);
   float* d_losses = ctx->ws.losses;
+  // DP = 2 all-reduce fused into AdamW (slip_comm_fuse_ar_adam); validated steps keep the
+  // NCCL all-reduce (their rollback needs the summed gradient in place)
+  const bool fused_ar = comm->fused_ar && comm->stage_comm && !ctx->validate;
+  SLIP_CHECK(!fused_ar || comm->fused_local == ctx->grad, SLIP_ESTATE,
+             "execute: gradient buffer re-bound since slip_comm_fuse_ar_adam");
 
   EventPool<false> pool;
   EventPool<true> tpool;
@@ -383,7 +388,7 @@ extern "C" slip_status slip_execute_schedule(slip_ctx* ctx, slip_comm* comm, con
           break;
         }
         case SLIP_ACT_AR:
-          if (comm->stage_comm) {
+          if (comm->stage_comm && !fused_ar) {
             SLIP_CUDA(chain(cs, comm->ar_stream));
             SLIP_CUDA(trace_begin());
             SLIP_TRY(slip_grad_allreduce(ctx, comm, reinterpret_cast<slip_stream>(comm->ar_stream)));
@@ -392,8 +397,17 @@ extern "C" slip_status slip_execute_schedule(slip_ctx* ctx, slip_comm* comm, con
           break;
         case SLIP_ACT_OPT:
           ctx->opt_step += 1;
+          // the stage all-reduce fused into AdamW over NVLink (DP = 2): both peers' W are
+          // done before either reads (this barrier's wait for the peer stays outside the
+          // OPT phase mark, as the NCCL all-reduce's does), and neither overwrites its
+          // gradient (next iteration's first W) before the other has read it
+          if (fused_ar) SLIP_CUDA(peer_barrier(comm->peer_flags, comm->flags, ++comm->epoch, cs));
           SLIP_CUDA(trace_begin());
-          if (!ctx->validate) {
+          if (fused_ar) {
+            SLIP_TRY(slip::optimizer_step_peer(ctx, adam, ctx->opt_step, grad_scale, ctx->ws.nonfinite, stream,
+                                               comm->peer_grad));
+            SLIP_CUDA(peer_barrier(comm->peer_flags, comm->flags, ++comm->epoch, cs));
+          } else if (!ctx->validate) {
             SLIP_TRY(slip_optimizer_step(ctx, adam, ctx->opt_step, grad_scale, ctx->ws.nonfinite, stream));
           } else {
             // local validation, step only if finite (no wait for other stages), then the

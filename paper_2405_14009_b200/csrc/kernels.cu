@@ -522,18 +522,34 @@ __global__ void __launch_bounds__(256) adamw_kernel(float* __restrict__ p, float
                                                     bf16* __restrict__ w, int64_t n4, int64_t per_layer, WdRanges wr,
                                                     float lr, float b1, float b2, float eps, float wd, float inv_bc1,
                                                     float inv_bc2, float grad_scale, int32_t* __restrict__ nonfinite,
-                                                    const int32_t* __restrict__ skip) {
+                                                    const int32_t* __restrict__ skip,
+                                                    const float* __restrict__ g_peer) {
   ptx::grid_dep_wait();
   if (skip && *skip) return;  // validated mode: this stage's gradients failed (no step)
   bool bad = false;
-  for (int64_t i = blockIdx.x * 256LL + threadIdx.x; i < n4; i += static_cast<int64_t>(gridDim.x) * 256) {
+  const int64_t stride = static_cast<int64_t>(gridDim.x) * 256;
+  // the peer's gradient crosses NVLink at a few us of latency: its load for the next
+  // iteration is issued before this one's local loads, two remote loads in flight
+  float4 gp = make_float4(0.f, 0.f, 0.f, 0.f);
+  if (g_peer && blockIdx.x * 256LL + threadIdx.x < n4)
+    gp = __ldcs(reinterpret_cast<const float4*>(g_peer) + blockIdx.x * 256LL + threadIdx.x);
+  for (int64_t i = blockIdx.x * 256LL + threadIdx.x; i < n4; i += stride) {
+    float4 gp_next = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (g_peer && i + stride < n4) gp_next = __ldcs(reinterpret_cast<const float4*>(g_peer) + i + stride);
     const int64_t e0 = 4 * i;
     const bool decay = decays(wr, e0, per_layer);
     const float wdl = decay ? wd : 0.f;
     float4 pp = reinterpret_cast<float4*>(p)[i];
     float4 mm = reinterpret_cast<float4*>(m)[i];
     float4 vv = reinterpret_cast<float4*>(v)[i];
-    const float4 gg = __ldcs(reinterpret_cast<const float4*>(g) + i);
+    float4 gg = __ldcs(reinterpret_cast<const float4*>(g) + i);
+    if (g_peer) {  // DP = 2 all-reduce fused in: the peer's gradient over NVLink; a + b is
+                   // commutative in IEEE fp32, so both replicas form the same sum
+      gg.x += gp.x;
+      gg.y += gp.y;
+      gg.z += gp.z;
+      gg.w += gp.w;
+    }
     float* pa = &pp.x;
     float* ma = &mm.x;
     float* va = &vv.x;
@@ -552,6 +568,7 @@ __global__ void __launch_bounds__(256) adamw_kernel(float* __restrict__ p, float
     reinterpret_cast<float4*>(m)[i] = mm;
     reinterpret_cast<float4*>(v)[i] = vv;
     reinterpret_cast<uint2*>(w)[i] = pack4(pa[0], pa[1], pa[2], pa[3]);
+    gp = gp_next;
   }
   if (nonfinite && __any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicOr(nonfinite, 1);
 }
@@ -1005,7 +1022,7 @@ cudaError_t grad_check(const float* g, int64_t n, int32_t* bad, int32_t* nonfini
 
 cudaError_t adamw(float* p, float* m, float* v, const float* g, bf16* w, int64_t n, int64_t per_layer, int h, int f,
                   float lr, float b1, float b2, float eps, float wd, float bc1, float bc2, float grad_scale,
-                  int32_t* nonfinite, cudaStream_t s, const int32_t* skip, TailDecay tail) {
+                  int32_t* nonfinite, cudaStream_t s, const int32_t* skip, TailDecay tail, const float* g_peer) {
   if (n % 4 || per_layer % 4) return cudaErrorInvalidValue;
   const int64_t H = h, F = f;
   WdRanges wr;
@@ -1019,7 +1036,34 @@ cudaError_t adamw(float* p, float* m, float* v, const float* g, bf16* w, int64_t
   wr.d0 = wr.c1 + F;
   wr.d1 = wr.d0 + H * F;
   return launch_pdl(adamw_kernel, dim3(grid_for(n / 4)), dim3(256), 0, s, 1, p, m, v, g, w, n / 4, per_layer, wr, lr,
-                    b1, b2, eps, wd, 1.0f / bc1, 1.0f / bc2, grad_scale, nonfinite, skip);
+                    b1, b2, eps, wd, 1.0f / bc1, 1.0f / bc2, grad_scale, nonfinite, skip, g_peer);
+}
+
+// Two-GPU barrier through peer-mapped flags (the fused DP = 2 all-reduce, comm.cpp):
+// publish `epoch` into the peer's flag with a system-scope release (after a system
+// fence, so every earlier kernel's writes on this GPU are visible to the peer), then
+// spin on the own flag with acquire loads.  A peer that never arrives is a bug, not a
+// failure mode (failed ranks have no stage group): trap after 30 s rather than hang.
+__global__ void peer_barrier_kernel(unsigned* peer_flag, const unsigned* my_flag, unsigned epoch) {
+  if (threadIdx.x != 0) return;
+  __threadfence_system();
+  asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(peer_flag), "r"(epoch) : "memory");
+  uint64_t t0;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+  for (;;) {
+    unsigned v;
+    asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(my_flag) : "memory");
+    if (static_cast<int>(v - epoch) >= 0) break;
+    uint64_t t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    if (t - t0 > 30000000000ull) __trap();
+    __nanosleep(256);
+  }
+}
+
+cudaError_t peer_barrier(unsigned* peer_flag, const unsigned* my_flag, unsigned epoch, cudaStream_t s) {
+  peer_barrier_kernel<<<1, 32, 0, s>>>(peer_flag, my_flag, epoch);
+  return cudaGetLastError();
 }
 
 cudaError_t f32_to_bf16(const float* src, bf16* dst, int64_t n, cudaStream_t s) {

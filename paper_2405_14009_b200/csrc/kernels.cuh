@@ -84,7 +84,11 @@ struct TailDecay {
 // skip (device, may be NULL): if *skip != 0 the step is not taken (validated mode).
 cudaError_t adamw(float* p, float* m, float* v, const float* g, bf16* w, int64_t n, int64_t per_layer, int h, int f,
                   float lr, float b1, float b2, float eps, float wd, float bc1, float bc2, float grad_scale,
-                  int32_t* nonfinite, cudaStream_t s, const int32_t* skip = nullptr, TailDecay tail = TailDecay());
+                  int32_t* nonfinite, cudaStream_t s, const int32_t* skip = nullptr, TailDecay tail = TailDecay(),
+                  const float* g_peer = nullptr);
+// g_peer (peer-mapped, may be NULL): the DP peer's gradient; the step uses g + g_peer.
+// Two-GPU barrier on peer-mapped flags (fused DP = 2 all-reduce); epochs increase per call.
+cudaError_t peer_barrier(unsigned* peer_flag, const unsigned* my_flag, unsigned epoch, cudaStream_t s);
 // Arithmetic reversal of one adamw step with the same gradient;
 // acts only if (global_bad == NULL || *global_bad) and (own_bad == NULL || !*own_bad);
 // count (may be NULL) is incremented when it acts.

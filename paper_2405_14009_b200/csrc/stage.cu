@@ -745,6 +745,13 @@ slip_status slip_backward_coupled(slip_ctx* c, int32_t slot, const void* dy, voi
 
 slip_status slip_optimizer_step(slip_ctx* c, const slip_adam* a, int64_t step, float grad_scale, int32_t* d_nonfinite,
                                 slip_stream st) {
+  return slip::optimizer_step_peer(c, a, step, grad_scale, d_nonfinite, st, nullptr);
+}
+
+}  // extern "C"
+
+slip_status slip::optimizer_step_peer(slip_ctx* c, const slip_adam* a, int64_t step, float grad_scale,
+                                      int32_t* d_nonfinite, slip_stream st, const float* peer_grad) {
   SLIP_CHECK(c && c->bound && a, SLIP_EINVAL, "optimizer_step: bad arguments");
   SLIP_CHECK(step >= 1, SLIP_EINVAL, "optimizer_step: step must be >= 1");
   const double bc1 = 1.0 - std::pow(static_cast<double>(a->beta1), static_cast<double>(step));
@@ -753,9 +760,11 @@ slip_status slip_optimizer_step(slip_ctx* c, const slip_adam* a, int64_t step, f
                 adamw(c->master, c->adam_m, c->adam_v, c->grad, c->w, c->n_params, c->po.per_layer, c->dm.h, c->dm.f,
                       a->lr, a->beta1, a->beta2, a->eps, a->weight_decay, static_cast<float>(bc1),
                       static_cast<float>(bc2), grad_scale, d_nonfinite, reinterpret_cast<cudaStream_t>(st), nullptr,
-                      tail_decay(c)),
+                      tail_decay(c), peer_grad),
                 "adamw");
 }
+
+extern "C" {
 
 slip_status slip_loss_mse(slip_ctx* c, const void* y, const void* target, void* dy, float* d_loss, slip_stream st) {
   SLIP_CHECK(c && c->bound && y && target && dy && d_loss, SLIP_EINVAL, "loss_mse: bad arguments");

@@ -123,6 +123,10 @@ size_t workspace_bytes(const Dims& d);
 slip_status weight_multi(slip_ctx* c, const int* slots, int n, int accumulate, cudaStream_t s);
 slip_status validated_step(slip_ctx* c, const slip_adam* a, int64_t step, float grad_scale, int32_t* own, int fault,
                            cudaStream_t s);
+// slip_optimizer_step with the DP peer's gradient added in (peer_grad peer-mapped, or
+// NULL): the DP = 2 all-reduce fused into AdamW (slip_comm_fuse_ar_adam).
+slip_status optimizer_step_peer(slip_ctx* c, const slip_adam* a, int64_t step, float grad_scale, int32_t* d_nonfinite,
+                                slip_stream st, const float* peer_grad);
 slip_status rollback_if(slip_ctx* c, const slip_adam* a, int64_t step, float grad_scale, const int32_t* glob,
                         const int32_t* own, int32_t* count, cudaStream_t s);
 }  // namespace slip

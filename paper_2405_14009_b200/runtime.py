@@ -350,6 +350,11 @@ def grad_allreduce(stage: Stage, comm: Comm, stream=None):
     call("slip_grad_allreduce", stage.ctx, comm.h, _stream(stream))
 
 
+def fuse_ar_adam(stage: Stage, comm: Comm, enable=True):
+    """DP = 2 all-reduce fused into AdamW over NVLink (collective over the stage pair)."""
+    call("slip_comm_fuse_ar_adam", stage.ctx, comm.h, int(bool(enable)))
+
+
 def execute_schedule(stage: Stage, comm: Comm, N, DP, m, live, costs: slip_costs, decoupled=True, staggered=True,
                      adam=(1e-4, 0.9, 0.95, 1e-8, 0.1), warmup=0, iterations=1, seed=1234, io=None,
                      stream=None) -> slip_report:

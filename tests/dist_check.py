@@ -207,6 +207,46 @@ def validate_scenario(a, cfg, L, comm, costs, rank, world, holder):
     return flag.item() == 1.0
 
 
+def fused_scenario(a, cfg, L, comm, costs, rank, world, holder):
+    """The DP = 2 stage all-reduce fused into AdamW over NVLink (slip_comm_fuse_ar_adam,
+    SURVEY §8(e) option (i)): two fault-free iterations with the fused step must leave
+    fp32 master, m, v and the bf16 weights bit-identical to the NCCL all-reduce + AdamW
+    path (g_a + g_b is the same fp32 sum on both peers and in NCCL's 2-rank reduction)."""
+    DP, PP, m = a.dp, a.pp, a.m
+    full = [[1] * DP for _ in range(PP)]
+    me_i = rank % PP
+    g = torch.Generator().manual_seed(7)
+    xs = [torch.randn(cfg.tokens, cfg.hidden, generator=g).to(torch.bfloat16).pin_memory() for _ in range(DP * m)]
+    rs = [torch.randn(cfg.tokens, cfg.hidden, generator=g).to(torch.bfloat16).pin_memory() for _ in range(DP * m)]
+
+    def train(fused):
+        if "stage" in holder:
+            holder["stage"].close()
+        st = holder["stage"] = rt.Stage(cfg, L, n_slots=2 * m * DP)
+        rt.init_master_(st.master, cfg, L, cfg.layers, seed=100 + me_i)
+        rt.call("slip_weights_from_master", st.ctx, rt._stream())
+        comm.setup(PP, DP, m, full)
+        if fused:
+            rt.fuse_ar_adam(st, comm)
+        losses = torch.zeros(DP * m, dtype=torch.float32).pin_memory()
+        rt.execute_schedule(st, comm, PP, DP, m, full, costs, True, True, adam=(1e-3, 0.9, 0.95, 1e-8, 0.1),
+                            iterations=2, io=rt.make_io(xs, rs, losses))
+        torch.cuda.synchronize()
+        return [st.master.clone(), st.adam_m.clone(), st.adam_v.clone(), st.w.clone(), losses.clone()]
+
+    ref = train(False)
+    fus = train(True)
+    eq = [bool(torch.equal(x, y)) for x, y in zip(ref, fus)]
+    ok = all(eq)
+    flag = torch.tensor([1.0 if ok else 0.0], device="cuda")
+    dist.all_reduce(flag, op=dist.ReduceOp.MIN)
+    outs = [None] * world
+    dist.all_gather_object(outs, {"rank": rank, "equal[master,m,v,w,losses]": eq})
+    if rank == 0:
+        print(json.dumps({"scenario": "fused_ar", "ok": flag.item() == 1.0, "ranks": outs}), flush=True)
+    return flag.item() == 1.0
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--dp", type=int, default=2)
@@ -215,6 +255,7 @@ def main():
     ap.add_argument("--failures", default="auto")
     ap.add_argument("--migrate", action="store_true", help="normalization swap scenario (PP >= 2)")
     ap.add_argument("--validate", action="store_true", help="post-step validation / rollback scenario (PP >= 2)")
+    ap.add_argument("--fused-ar", action="store_true", help="DP=2 all-reduce fused into AdamW vs NCCL, bit-exact")
     a = ap.parse_args()
     rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
     local = int(os.environ.get("LOCAL_RANK", rank))
@@ -253,8 +294,9 @@ def main():
         torch.cuda.synchronize()
         return rep, stage.grad.clone(), stage.master.clone(), losses.clone()
 
-    if a.migrate or a.validate:
-        ok = (migrate_scenario if a.migrate else validate_scenario)(a, cfg, L, comm, costs, rank, world, holder)
+    if a.migrate or a.validate or a.fused_ar:
+        fn = migrate_scenario if a.migrate else (validate_scenario if a.validate else fused_scenario)
+        ok = fn(a, cfg, L, comm, costs, rank, world, holder)
         comm.close()
         holder["stage"].close()
         dist.destroy_process_group()
