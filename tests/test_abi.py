@@ -83,3 +83,12 @@ def test_runtime_has_no_cpu_fallback_or_oracle_import():
             s = open(os.path.join(pkg, f)).read()
             assert "oracle" not in s.replace("oracle/", ""), f
             assert "import numpy" not in s, f
+
+
+def test_fused_allreduce_adam_rejects_unbound_arguments():
+    """slip_comm_fuse_ar_adam validates before touching CUDA or NCCL: NULL ctx / comm
+    is SLIP_EINVAL with a message (no GPU needed)."""
+    b = _binding()
+    lib = b.lib()
+    assert lib.slip_comm_fuse_ar_adam(None, None, 1) == 1
+    assert b"comm_fuse_ar_adam" in lib.slip_last_error()
