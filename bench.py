@@ -11,8 +11,9 @@ micro-batches per step.  N > 1: DP 2 x PP N/2, 24/PP layers per stage and
 m = 4*PP micro-batches per pipeline, so the per-GPU work is fixed (weak
 scaling).  A step is one training iteration of the plan: F, B (input grads),
 deferred W (weight grads), the per-stage DP all-reduce and the staggered AdamW.
---failures F masks F ranks at the normalized positions (last stages, distinct
-peer groups); their micro-batches are re-routed to the DP peer.
+--failures F masks F ranks at the positions Algorithm 1
+normalizes them to over the profiled cost table; their micro-batches are re-routed
+to the DP peer.
 
 One JSON line on rank 0 (contract in the task statement): value = whole-job
 tokens/s over exactly K timed steps (CUDA events, max over ranks), plus e2e
@@ -226,26 +227,47 @@ def main():
     cfg = sd.ModelCfg(hidden=H, heads=HEADS, ffn=FFN, seq=SEQ, micro_batch=MB, layers=args.layers,
                       vocab=VOCAB if args.gpt_ends else 0, ends=ends)
     T = cfg.tokens
-    # failures at normalized positions: last stages, distinct peer groups (R20),
-    # or the actual (un-normalized) set given by --failed-at
-    failed = [(PP - 1 - q, (q + 1) % DP) for q in range(args.failures)]
+    decoupled = not args.coupled
+    staggered = not (args.coupled or args.no_stagger)
+    # nominal integer costs ~ FLOP ratios of F : B : W (SURVEY §8(d.4)), refined by profiling below
+    costs = rt.make_costs(t_f=108, t_b=117, t_w=100, t_comm=1, t_ar=10, t_opt=10)
+
+    def alg1_live(cs):
+        """--failures F: the failures sit where Phase 1 of the Planner puts them (PAPER.md
+        lines 374-424): R = A[N-1][F] of Algorithm 1 over the heuristic cost table of this
+        plan variant (slip_normalize_costs -> slip_normalize), placed by
+        slip_normalized_live — the steady state after the migration swaps."""
+        if args.failures > PP * (DP - 1):
+            return None, None
+        R, _ = rt.normalize(PP, DP, args.failures,
+                            rt.normalize_costs(PP, DP, m, cs, args.failures, decoupled, staggered))
+        return R, rt.normalized_live(PP, DP, R)
+
+    # the actual (un-normalized) set given by --failed-at, else Algorithm 1's placement
+    alg1_R = None
     if args.failed_at:
         failed = [tuple(int(v) for v in f.split(",")) for f in args.failed_at.split(";")]
-    live = [[1] * DP for _ in range(PP)]
-    for (i, k) in failed:
-        live[i][k] = 0
+        live = [[1] * DP for _ in range(PP)]
+        for (i, k) in failed:
+            live[i][k] = 0
+    elif args.failures:
+        alg1_R, live = alg1_live(costs)
+        if live is None:
+            if rank == 0:
+                print(json.dumps({"metric": METRIC, "value": None, "unit": "tokens/s", "n_gpus": world,
+                                  "error": "unrecoverable: %d failures > N (DP - 1)" % args.failures}))
+            return
+        failed = [(i, k) for i in range(PP) for k in range(DP) if not live[i][k]]
+    else:
+        failed, live = [], [[1] * DP for _ in range(PP)]
     if not rt.recoverable(PP, DP, live):
         if rank == 0:
             print(json.dumps({"metric": METRIC, "value": None, "unit": "tokens/s", "n_gpus": world,
                               "error": "unrecoverable failure set %s (a stage lost every worker)" % failed}))
         return
-    decoupled = not args.coupled
-    staggered = not (args.coupled or args.no_stagger)
     plan_name = ("coupled 1F1B" if args.coupled else
                  "decoupled B/W, global optimizer barrier" if args.no_stagger else
                  "decoupled B/W + staggered AdamW")
-    # nominal integer costs ~ FLOP ratios of F : B : W (SURVEY §8(d.4)), refined by profiling below
-    costs = rt.make_costs(t_f=108, t_b=117, t_w=100, t_comm=1, t_ar=10, t_opt=10)
     def inflight(lv, cs):
         """{(i, k): max in-flight micro-batches (F started, W / BC not finished)} of the plan"""
         plan = rt.plan_schedule(PP, DP, m, lv, cs, decoupled, staggered, horizon=2)
@@ -318,6 +340,22 @@ def main():
                           t_ar=1 if fused_ar else q(per[4] * 0.5 if per[4] else 0.01), t_opt=q(per[4] or 0.01))
     norm = None
     my_role = rank
+    if alg1_R is not None:
+        # Algorithm 1 again with the profiled costs; a different placement re-forms the groups
+        R2, live2 = alg1_live(costs)
+        if live2 != live:
+            if slots_for(live2, costs) > n_slots:
+                n_slots = slots_for(live2, costs)
+                stage.close()
+                stage = rt.Stage(cfg, L, n_slots)
+                rt.init_master_(stage.master, cfg, L, args.layers, seed=rank % PP)
+                rt.call("slip_weights_from_master", stage.ctx, rt._stream())
+            live = live2
+            comm.setup(PP, DP, m, live)
+            if fused_ar:
+                rt.fuse_ar_adam(stage, comm)
+        alg1_R = R2
+        failed = [(i, k) for i in range(PP) for k in range(DP) if not live[i][k]]
     if args.normalize and failed:
         # Normalization with the profiled costs, then one P2P state copy per swap (PAPER.md
         # lines 377-379): the GPU at the target position takes over the failed worker's role
@@ -341,7 +379,7 @@ def main():
                 if rank == p_s:
                     rt.migrate_state(stage, comm, p_t, True)
                 elif rank == p_t:
-                    rt.migrate_state(stage, comm, p_s, False, opt_step=0)
+                    rt.migrate_state(stage, comm, p_s, False)
             g1.record(stream)
             barrier()
             return allreduce_max(g0.elapsed_time(g1))
@@ -370,10 +408,10 @@ def main():
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(stream)
     rep = execute(args.steps)
-    # the plan is identical on every rank; a masked rank (possibly rank 0) reports none
-    predicted_period = int(allreduce_max(float(rep.predicted_period)))
     e1.record(stream)
     barrier()
+    # the plan is identical on every rank; a masked rank (possibly rank 0) reports none
+    predicted_period = int(allreduce_max(float(rep.predicted_period)))
     ms_total = allreduce_max(e0.elapsed_time(e1))
     clk = clocks.stop() if clocks else None
     tokens_per_step = DP * m * T
@@ -550,6 +588,10 @@ def main():
     line["memory"] = memory
     if norm:
         line["normalization"] = norm
+    elif alg1_R is not None:
+        line["normalization"] = {"R": alg1_R, "placement": "Algorithm 1 over the profiled heuristic cost table "
+                                                            "(slip_normalize), placed by slip_normalized_live",
+                                 "normalized_failed": failed}
     if cpu:
         line["cpu_baseline"] = cpu
     print(json.dumps(line), flush=True)

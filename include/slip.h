@@ -367,9 +367,11 @@ slip_status slip_comm_set_role(slip_comm* comm, int32_t role);
  * receiver needs to take over a role — fp32 master weights, AdamW m and v
  * (3 x 4 B per parameter) — over the world communicator between WORLD ranks
  * (send = 1 on the live peer of the failed worker's stage, send = 0 on the
- * GPU taking over).  The receiver then rebuilds its bf16 weights from the
- * master copy and sets its AdamW step count to opt_step (the coordinator's
- * iteration count).  Both sides must call it; stream-ordered on s. */
+ * GPU taking over).  The sender's AdamW step count travels with the state: the
+ * receiver rebuilds its bf16 weights from the master copy and sets its step count
+ * to the sender's (opt_step < 0) or to opt_step (>= 0, an explicit override).  Both
+ * sides must call it; it synchronizes s before returning (migration is not on the
+ * per-step path). */
 slip_status slip_migrate_state(slip_ctx* ctx, slip_comm* comm, int32_t peer, int32_t send, int64_t opt_step,
                                slip_stream s);
 

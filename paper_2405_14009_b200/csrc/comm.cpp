@@ -189,6 +189,11 @@ slip_status slip_migrate_state(slip_ctx* ctx, slip_comm* c, int32_t peer, int32_
   cudaStream_t st = reinterpret_cast<cudaStream_t>(s);
   const size_t n = static_cast<size_t>(ctx->n_params);
   float* bufs[3] = {ctx->master, ctx->adam_m, ctx->adam_v};
+  // the sender's AdamW step count travels with the state, so the receiver continues
+  // with the same bias correction as the peer it replicates
+  int64_t* d_step = nullptr;
+  SLIP_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&d_step), sizeof(int64_t), st));
+  if (send) SLIP_CUDA(cudaMemcpyAsync(d_step, &ctx->opt_step, sizeof(int64_t), cudaMemcpyHostToDevice, st));
   SLIP_NCCL(ncclGroupStart());
   for (float* b : bufs) {
     ncclResult_t r = send ? ncclSend(b, n, ncclFloat32, peer, c->world_comm, st)
@@ -198,9 +203,21 @@ slip_status slip_migrate_state(slip_ctx* ctx, slip_comm* c, int32_t peer, int32_
       return nccl_status(r, send ? "ncclSend(state)" : "ncclRecv(state)");
     }
   }
+  {
+    ncclResult_t r = send ? ncclSend(d_step, 1, ncclInt64, peer, c->world_comm, st)
+                          : ncclRecv(d_step, 1, ncclInt64, peer, c->world_comm, st);
+    if (r != ncclSuccess) {
+      ncclGroupEnd();
+      return nccl_status(r, "migrate_state: step count");
+    }
+  }
   SLIP_NCCL(ncclGroupEnd());
+  int64_t sender_step = 0;
+  SLIP_CUDA(cudaMemcpyAsync(&sender_step, d_step, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+  SLIP_CUDA(cudaFreeAsync(d_step, st));
+  SLIP_CUDA(cudaStreamSynchronize(st));
   if (!send) {
-    ctx->opt_step = opt_step;
+    ctx->opt_step = opt_step >= 0 ? opt_step : sender_step;
     SLIP_TRY(slip_weights_from_master(ctx, s));
   }
   return SLIP_OK;
@@ -240,7 +257,9 @@ slip_status slip_comm_fuse_ar_adam(slip_ctx* ctx, slip_comm* c, int32_t enable) 
   mine.n_params = ctx->n_params;
   void* dbuf = nullptr;
   SLIP_CUDA(cudaMalloc(&dbuf, 3 * sizeof(Rec)));
-  SLIP_CUDA(cudaMemcpy(dbuf, &mine, sizeof(Rec), cudaMemcpyHostToDevice));
+  // ordered before the all-gather on the same stream (a pageable cudaMemcpy on the legacy
+  // stream has no ordering with the non-blocking ar_stream)
+  SLIP_CUDA(cudaMemcpyAsync(dbuf, &mine, sizeof(Rec), cudaMemcpyHostToDevice, c->ar_stream));
   ncclResult_t r = ncclAllGather(dbuf, static_cast<char*>(dbuf) + sizeof(Rec), sizeof(Rec), ncclUint8, c->stage_comm,
                                  c->ar_stream);
   cudaError_t e = r == ncclSuccess ? cudaStreamSynchronize(c->ar_stream) : cudaSuccess;
@@ -252,9 +271,41 @@ slip_status slip_comm_fuse_ar_adam(slip_ctx* ctx, slip_comm* c, int32_t enable) 
   int me = 0;
   SLIP_NCCL(ncclCommUserRank(c->stage_comm, &me));
   const Rec& peer = both[1 - me];
-  SLIP_CHECK(peer.n_params == ctx->n_params, SLIP_EINVAL, "comm_fuse_ar_adam: peer holds a different stage size");
-  SLIP_CUDA(cudaIpcOpenMemHandle(&c->ipc_grad_base, peer.grad, cudaIpcMemLazyEnablePeerAccess));
-  SLIP_CUDA(cudaIpcOpenMemHandle(&c->ipc_flag_base, peer.flag, cudaIpcMemLazyEnablePeerAccess));
+  // both peers fuse or neither: a one-sided failure would leave the other side spinning in
+  // peer_barrier until its trap, so the local outcome is MIN-reduced over the pair first
+  int32_t ok = peer.n_params == ctx->n_params ? 1 : 0;
+  cudaError_t oe = cudaSuccess;
+  if (ok) oe = cudaIpcOpenMemHandle(&c->ipc_grad_base, peer.grad, cudaIpcMemLazyEnablePeerAccess);
+  if (oe != cudaSuccess) c->ipc_grad_base = nullptr;
+  if (ok && oe == cudaSuccess) {
+    oe = cudaIpcOpenMemHandle(&c->ipc_flag_base, peer.flag, cudaIpcMemLazyEnablePeerAccess);
+    if (oe != cudaSuccess) c->ipc_flag_base = nullptr;
+  }
+  if (oe != cudaSuccess) {
+    ok = 0;
+    cudaGetLastError();
+  }
+  int32_t* dok = nullptr;
+  SLIP_CUDA(cudaMalloc(&dok, sizeof(int32_t)));
+  SLIP_CUDA(cudaMemcpyAsync(dok, &ok, sizeof(int32_t), cudaMemcpyHostToDevice, c->ar_stream));
+  r = ncclAllReduce(dok, dok, 1, ncclInt32, ncclMin, c->stage_comm, c->ar_stream);
+  int32_t all_ok = 0;
+  e = r == ncclSuccess ? cudaMemcpyAsync(&all_ok, dok, sizeof(int32_t), cudaMemcpyDeviceToHost, c->ar_stream)
+                       : cudaSuccess;
+  if (e == cudaSuccess && r == ncclSuccess) e = cudaStreamSynchronize(c->ar_stream);
+  cudaFree(dok);
+  if (r != ncclSuccess || e != cudaSuccess || !all_ok) {
+    close_fused(c);
+    if (r != ncclSuccess) return nccl_status(r, "ncclAllReduce(fuse agreement)");
+    SLIP_CUDA(e);
+    if (peer.n_params != ctx->n_params) {
+      set_error("comm_fuse_ar_adam: peer holds a different stage size");
+      return SLIP_EINVAL;
+    }
+    set_error(oe != cudaSuccess ? "comm_fuse_ar_adam: cudaIpcOpenMemHandle failed here"
+                                : "comm_fuse_ar_adam: the peer could not map this rank's buffers");
+    return SLIP_ECUDA;
+  }
   c->peer_grad = reinterpret_cast<const float*>(static_cast<char*>(c->ipc_grad_base) + peer.grad_off);
   c->peer_flags = static_cast<unsigned*>(c->ipc_flag_base);
   c->fused_local = ctx->grad;

@@ -221,7 +221,7 @@ extern "C" slip_status slip_execute_schedule(slip_ctx* ctx, slip_comm* comm, con
       size_t tb_idx = 0;
       // called by every action after its stream waits: the phase timing (and the trace)
       // measure the operation itself, not the time it waited for a peer or a free slot
-      bool marked = false;
+      bool marked = false, mark_done = false;
       auto trace_begin = [&]() -> cudaError_t {
         cudaError_t r = cudaSuccess;
         if (timed && ph >= 0) {
@@ -406,6 +406,12 @@ extern "C" slip_status slip_execute_schedule(slip_ctx* ctx, slip_comm* comm, con
           if (fused_ar) {
             SLIP_TRY(slip::optimizer_step_peer(ctx, adam, ctx->opt_step, grad_scale, ctx->ws.nonfinite, stream,
                                                comm->peer_grad));
+            // the OPT phase (a planner cost) ends with AdamW; the wait for the peer's AdamW
+            // below is peer skew, not optimizer time
+            if (marked) {
+              SLIP_CUDA(cudaEventRecord(tpool.ev[marks.back().second + 1], ts));
+              mark_done = true;
+            }
             SLIP_CUDA(peer_barrier(comm->peer_flags, comm->flags, ++comm->epoch, cs));
           } else if (!ctx->validate) {
             SLIP_TRY(slip_optimizer_step(ctx, adam, ctx->opt_step, grad_scale, ctx->ws.nonfinite, stream));
@@ -437,7 +443,7 @@ extern "C" slip_status slip_execute_schedule(slip_ctx* ctx, slip_comm* comm, con
           set_error("execute: unknown action");
           return SLIP_EINVAL;
       }
-      if (marked) SLIP_CUDA(cudaEventRecord(tpool.ev[marks.back().second + 1], ts));
+      if (marked && !mark_done) SLIP_CUDA(cudaEventRecord(tpool.ev[marks.back().second + 1], ts));
       if (marked && w_extra > 0) mark_extra.push_back({marks.size() - 1, w_extra});
       w_extra = 0;
       if (tr) {

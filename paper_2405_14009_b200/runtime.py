@@ -341,7 +341,7 @@ class Comm:
             self.h = None
 
 
-def migrate_state(stage: Stage, comm: Comm, peer: int, send: bool, opt_step: int = 0, stream=None):
+def migrate_state(stage: Stage, comm: Comm, peer: int, send: bool, opt_step: int = -1, stream=None):
     """P2P copy of the stage state of one normalization swap (world ranks)."""
     call("slip_migrate_state", stage.ctx, comm.h, int(peer), int(bool(send)), int(opt_step), _stream(stream))
 

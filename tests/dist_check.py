@@ -11,7 +11,8 @@ checks, on every live rank:
     changes no numbers, PAPER.md line 215);
   * the all-reduced stage gradient equals the fault-free one within 1e-4
     normwise (only the fp32 summation order of micro-batch contributions moves);
-  * after the AdamW step, all live peers of a stage hold bit-identical weights.
+  * after the AdamW step, all live peers of a stage hold bit-identical weights
+    (raw bytes all-gathered and compared with torch.equal).
 Prints one JSON line per scenario on rank 0 and exits non-zero on failure."""
 import argparse
 import json
@@ -25,6 +26,21 @@ import torch.distributed as dist  # noqa: E402
 
 import slipdata as sd  # noqa: E402
 from paper_2405_14009_b200 import runtime as rt  # noqa: E402
+
+def peers_equal(t, me_live, me_stage, world):
+    """Bitwise comparison of `t` across the live ranks of my stage: every rank's raw
+    bytes are all-gathered (as int32 words) and compared with torch.equal.  Returns
+    the list of comparisons made on this rank (empty when masked)."""
+    words = t.contiguous().view(torch.int32)
+    allw = [torch.empty_like(words) for _ in range(world)]
+    dist.all_gather(allw, words)
+    meta = torch.tensor([float(me_live), float(me_stage)], dtype=torch.float64, device="cuda")
+    allm = [torch.zeros_like(meta) for _ in range(world)]
+    dist.all_gather(allm, meta)
+    if not me_live:
+        return []
+    return [bool(torch.equal(allw[r], words)) for r in range(world)
+            if allm[r][0].item() == 1.0 and int(allm[r][1].item()) == me_stage]
 
 
 def migrate_scenario(a, cfg, L, comm, costs, rank, world, holder):
@@ -91,7 +107,7 @@ def migrate_scenario(a, cfg, L, comm, costs, rank, world, holder):
     if rank == w_src:
         rt.migrate_state(st, comm, w_target, True)
     elif rank == w_target:
-        rt.migrate_state(st, comm, w_src, False, opt_step=1)
+        rt.migrate_state(st, comm, w_src, False)  # the step count (1) comes with the state
     t1.record()
     torch.cuda.synchronize()
     mig_ms = t0.elapsed_time(t1)
@@ -124,14 +140,9 @@ def migrate_scenario(a, cfg, L, comm, costs, rank, world, holder):
     # last-stage losses: every micro-batch's loss is written once in both runs
     res["losses_equal"] = bool(torch.equal(lA, lB))
     ok &= res["losses_equal"]
-    ck = torch.tensor([float(pB.double().sum().item()) if me_live else float("nan"), float(me_live), float(me_i)],
-                      dtype=torch.float64, device="cuda")
-    allck = [torch.zeros_like(ck) for _ in range(world)]
-    dist.all_gather(allck, ck)
-    if me_live:
-        for r2 in range(world):
-            if allck[r2][1].item() == 1.0 and int(allck[r2][2].item()) == me_i:
-                ok &= allck[r2][0].item() == ck[0].item()
+    eq = peers_equal(pB, me_live, me_i, world)
+    res["peer_master_bit_identical"] = eq
+    ok &= all(eq)
     flag = torch.tensor([1.0 if ok else 0.0], device="cuda")
     dist.all_reduce(flag, op=dist.ReduceOp.MIN)
     outs = [None] * world
@@ -192,12 +203,9 @@ def validate_scenario(a, cfg, L, comm, costs, rank, world, holder):
     r3 = iterate()
     res["rollbacks3"] = r3.rollbacks
     ok &= r3.rollbacks == 0
-    ck = torch.tensor([float(st.master.double().sum().item()), float(me_i)], dtype=torch.float64, device="cuda")
-    allck = [torch.zeros_like(ck) for _ in range(world)]
-    dist.all_gather(allck, ck)
-    for r2_ in range(world):
-        if int(allck[r2_][1].item()) == me_i:
-            ok &= allck[r2_][0].item() == ck[0].item()
+    eq = peers_equal(st.master, True, me_i, world) + peers_equal(st.w, True, me_i, world)
+    res["peer_master_w_bit_identical"] = eq
+    ok &= all(eq)
     flag = torch.tensor([1.0 if ok else 0.0], device="cuda")
     dist.all_reduce(flag, op=dist.ReduceOp.MIN)
     outs = [None] * world
@@ -213,38 +221,50 @@ def fused_scenario(a, cfg, L, comm, costs, rank, world, holder):
     fp32 master, m, v and the bf16 weights bit-identical to the NCCL all-reduce + AdamW
     path (g_a + g_b is the same fp32 sum on both peers and in NCCL's 2-rank reduction)."""
     DP, PP, m = a.dp, a.pp, a.m
-    full = [[1] * DP for _ in range(PP)]
-    me_i = rank % PP
+    me_i, me_k = rank % PP, rank // PP
     g = torch.Generator().manual_seed(7)
     xs = [torch.randn(cfg.tokens, cfg.hidden, generator=g).to(torch.bfloat16).pin_memory() for _ in range(DP * m)]
     rs = [torch.randn(cfg.tokens, cfg.hidden, generator=g).to(torch.bfloat16).pin_memory() for _ in range(DP * m)]
+    # fault-free, and (PP >= 2) one failed worker: its stage is a singleton (plain AdamW)
+    # while the other stages stay fused — the mixed case of the executor's protocol
+    cases = [[]] + ([[(PP - 1, 1)]] if PP >= 2 else [])
+    all_ok = True
+    for failed in cases:
+        live = [[1] * DP for _ in range(PP)]
+        for (i, k) in failed:
+            live[i][k] = 0
 
-    def train(fused):
-        if "stage" in holder:
-            holder["stage"].close()
-        st = holder["stage"] = rt.Stage(cfg, L, n_slots=2 * m * DP)
-        rt.init_master_(st.master, cfg, L, cfg.layers, seed=100 + me_i)
-        rt.call("slip_weights_from_master", st.ctx, rt._stream())
-        comm.setup(PP, DP, m, full)
-        if fused:
-            rt.fuse_ar_adam(st, comm)
-        losses = torch.zeros(DP * m, dtype=torch.float32).pin_memory()
-        rt.execute_schedule(st, comm, PP, DP, m, full, costs, True, True, adam=(1e-3, 0.9, 0.95, 1e-8, 0.1),
-                            iterations=2, io=rt.make_io(xs, rs, losses))
-        torch.cuda.synchronize()
-        return [st.master.clone(), st.adam_m.clone(), st.adam_v.clone(), st.w.clone(), losses.clone()]
+        def train(fused):
+            if "stage" in holder:
+                holder["stage"].close()
+            st = holder["stage"] = rt.Stage(cfg, L, n_slots=2 * m * DP)
+            rt.init_master_(st.master, cfg, L, cfg.layers, seed=100 + me_i)
+            rt.call("slip_weights_from_master", st.ctx, rt._stream())
+            comm.setup(PP, DP, m, live)
+            if fused:
+                rt.fuse_ar_adam(st, comm)
+            losses = torch.zeros(DP * m, dtype=torch.float32).pin_memory()
+            rt.execute_schedule(st, comm, PP, DP, m, live, costs, True, True, adam=(1e-3, 0.9, 0.95, 1e-8, 0.1),
+                                iterations=2, io=rt.make_io(xs, rs, losses))
+            torch.cuda.synchronize()
+            return [st.master.clone(), st.adam_m.clone(), st.adam_v.clone(), st.w.clone(), losses.clone()]
 
-    ref = train(False)
-    fus = train(True)
-    eq = [bool(torch.equal(x, y)) for x, y in zip(ref, fus)]
-    ok = all(eq)
-    flag = torch.tensor([1.0 if ok else 0.0], device="cuda")
-    dist.all_reduce(flag, op=dist.ReduceOp.MIN)
-    outs = [None] * world
-    dist.all_gather_object(outs, {"rank": rank, "equal[master,m,v,w,losses]": eq})
-    if rank == 0:
-        print(json.dumps({"scenario": "fused_ar", "ok": flag.item() == 1.0, "ranks": outs}), flush=True)
-    return flag.item() == 1.0
+        ref = train(False)
+        fus = train(True)
+        me_live = live[me_i][me_k] == 1
+        eq = [bool(torch.equal(x, y)) for x, y in zip(ref, fus)] if me_live else []
+        peq = peers_equal(fus[0], me_live, me_i, world)
+        ok = all(eq) and all(peq)
+        flag = torch.tensor([1.0 if ok else 0.0], device="cuda")
+        dist.all_reduce(flag, op=dist.ReduceOp.MIN)
+        outs = [None] * world
+        dist.all_gather_object(outs, {"rank": rank, "live": me_live, "equal[master,m,v,w,losses]": eq,
+                                      "peer_master_bit_identical": peq})
+        if rank == 0:
+            print(json.dumps({"scenario": "fused_ar", "failed": failed, "ok": flag.item() == 1.0, "ranks": outs}),
+                  flush=True)
+        all_ok = all_ok and flag.item() == 1.0
+    return all_ok
 
 
 def main():
@@ -335,16 +355,10 @@ def main():
                         if ex[(PP - 1, j, k)] == me_k:
                             ok &= bool(l1[k * m + j] == l0[k * m + j])
                             res.setdefault("loss_equal", []).append(bool(l1[k * m + j] == l0[k * m + j]))
-        # peers of a stage hold identical weights: compare checksums across ranks
-        ck = torch.tensor([float(p1.double().sum().item()) if me_live else float("nan"), float(me_live)],
-                          dtype=torch.float64, device="cuda")
-        allck = [torch.zeros_like(ck) for _ in range(world)]
-        dist.all_gather(allck, ck)
-        for r2 in range(world):
-            if r2 % PP == me_i and allck[r2][1].item() == 1.0 and me_live:
-                same = allck[r2][0].item() == ck[0].item()
-                ok &= same
-                res.setdefault("peer_weights_equal", []).append(same)
+        # peers of a stage hold bit-identical fp32 master weights after the step
+        eq = peers_equal(p1, me_live, me_i, world)
+        res["peer_weights_equal"] = eq
+        ok &= all(eq)
         flag = torch.tensor([1.0 if ok else 0.0], device="cuda")
         dist.all_reduce(flag, op=dist.ReduceOp.MIN)
         outs = [None] * world

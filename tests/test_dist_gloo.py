@@ -8,7 +8,10 @@ with all_gather_object, and each process checks
   * the ops executed by the live ranks partition all (stage, micro-batch) work,
   * a model of the executor's stream / event protocol (compute stream, one stream
     per directed pair with rendezvous send/recv, the stage all-reduce as a
-    collective over live peers) runs to completion: no deadlock.
+    collective over live peers) runs to completion: no deadlock — both with the
+    NCCL all-reduce and with the DP = 2 all-reduce fused into AdamW
+    (slip_comm_fuse_ar_adam), whose OPT is a flag barrier with the peer, AdamW, and
+    a second barrier, all on the compute stream.
 """
 import os
 import socket
@@ -20,6 +23,7 @@ import torch.multiprocessing as mp
 CASES = [
     (2, 2, 3, []), (2, 2, 3, [(1, 1)]), (2, 2, 3, [(0, 0)]),
     (4, 2, 3, []), (4, 2, 3, [(3, 1)]), (4, 2, 3, [(3, 1), (2, 0)]), (4, 2, 3, [(0, 1)]),
+    (4, 2, 2, [(1, 0)]), (4, 2, 1, [(2, 1)]), (2, 2, 8, [(1, 0)]), (4, 2, 16, [(3, 1)]),
     (4, 3, 6, [(2, 1)]), (3, 3, 4, [(1, 0), (2, 2), (0, 1)]), (4, 2, 8, [(1, 1)]),
 ]
 KINDS = ("LOAD_X", "RECV_X", "F", "SEND_Y", "LOSS", "RECV_DY", "B", "SEND_DX", "W", "BC", "AR", "OPT")
@@ -33,8 +37,10 @@ def _free_port():
     return p
 
 
-def simulate(progs, N, DP, live):
-    """Executor stream/event model; returns True if every action completes."""
+def simulate(progs, N, DP, live, fused=False):
+    """Executor stream/event model; returns True if every action completes.  fused:
+    stages with exactly 2 live workers skip the AR collective and run OPT as
+    barrier -> AdamW -> barrier with the peer on the compute stream."""
     nodes = []  # dict(deps=set, rv=key or None)
     rv_groups = {}
 
@@ -48,6 +54,8 @@ def simulate(progs, N, DP, live):
         tail = {}  # stream -> last node
         chan = {}  # (src, dst, kind) -> count
         ar_count = 0
+        opt_count = 0
+        pair_fused = fused and sum(1 for k in range(DP) if live[r % N][k]) == 2
         slot = {}  # slot -> dict(freed, sent_y, sent_dx)
         pending_cs_dep = None
         for a in prog:
@@ -74,6 +82,16 @@ def simulate(progs, N, DP, live):
                 n = add([tail.get(st), cs], rv=(r, peer, "act" if k == "SEND_Y" else "grad", q))
                 tail[st] = n
                 sv["sent_y" if k == "SEND_Y" else "sent_dx"] = n
+            elif k == "AR" and pair_fused:
+                continue  # the exchange happens inside OPT
+            elif k == "OPT" and pair_fused:
+                stage = r % N
+                b1 = add([cs, pending_cs_dep], rv=("bar", stage, opt_count, 0))
+                adam = add([b1])
+                b2 = add([adam], rv=("bar", stage, opt_count, 1))
+                opt_count += 1
+                pending_cs_dep = None
+                tail["cs"] = b2
             elif k == "AR":
                 stage = r % N
                 n = add([tail.get("ar"), cs], rv=("ar", stage, ar_count))
@@ -152,7 +170,8 @@ def _worker(rank, world, port, results):
         want = sorted((i, t, j, k, ph) for i in range(N) for t in range(H) for j in range(m) for k in range(DP)
                       for ph in ("F", "B", "W"))
         dead_idle = all(not progs[k * N + i] for i in range(N) for k in range(DP) if not live[i][k])
-        ok.append((len(hashes) == 1, snd == rcv, work == want, dead_idle, simulate(progs, N, DP, live)))
+        ok.append((len(hashes) == 1, snd == rcv, work == want, dead_idle, simulate(progs, N, DP, live),
+                   simulate(progs, N, DP, live, fused=True)))
     results[rank] = ok
     dist.destroy_process_group()
 

@@ -1,0 +1,295 @@
+"""Executor and re-route numerics on ONE GPU against the fp64 oracle (SURVEY §8(a)
+rows a3, a5, a7, a10; §3.1, ReRouteAct / ReRouteGrad /
+InputBackwardPass / WeightBackwardPass line 554-558).
+
+(i)  slip_execute_schedule at N = 1 (the bench's own call: program interpretation,
+     merged W launches over the slots, accumulate flags, grad_scale, the AdamW step
+     counter): after each of two iterations the fp32 stage gradient equals the
+     oracle's sum over the micro-batches of Delta_j (Gate A), and master / m / v after
+     AdamW equal oracle/adam.py applied to the GPU's own gradient (Gate B).
+(ii) DP = 2 re-routing on one GPU: one Stage context per live worker, each driven
+     through ITS rank program (slip_rank_program: LOAD_X / RECV_X / F / SEND_Y /
+     LOSS / RECV_DY / B / SEND_DX / W / BC, with the executor's merging of back-to-back
+     W's), messages passed between the contexts in per-pair FIFO order.  The live
+     peers' fp32 gradients summed in ascending k (the stage all-reduce) equal
+     oracle/pipeline.py per_worker_sum (form ii) within Gate A, and equal the
+     fault-free GPU run within 1e-5 (only the fp32 summation order moves).
+"""
+import numpy as np
+import pytest
+import torch
+
+import slipdata as sd
+from oracle import adam as OA
+from oracle import pipeline as PPL
+from oracle import planner as PL
+
+pytestmark = pytest.mark.gpu
+
+GATE_A = 2e-2
+GATE_B = 1e-4
+ADAM = OA.AdamCfg(lr=1e-3, beta1=0.9, beta2=0.95, eps=1e-8, weight_decay=0.1)
+ACT = dict(LOAD_X=0, RECV_X=1, F=2, SEND_Y=3, LOSS=4, RECV_DY=5, B=6, SEND_DX=7, W=8, BC=9, AR=10, OPT=11)
+
+
+def _rt():
+    from paper_2405_14009_b200 import runtime
+    return runtime
+
+
+def relerr(g, r):
+    g = np.asarray(g, dtype=np.float64)
+    return float(np.max(np.abs(g - r)) / max(np.max(np.abs(r)), 1e-300))
+
+
+def host_bf16(x):
+    return torch.from_numpy(sd.to_bf16_bits(x).view(np.int16).copy()).view(torch.bfloat16)
+
+
+def dev_bf16(x):
+    return host_bf16(x).cuda()
+
+
+def as_np(t):
+    return t.float().cpu().numpy().astype(np.float64)
+
+
+def oracle_grad_sum(stages, cfg, keys):
+    """Sum over the micro-batches `keys` = [(k, j)] (ascending) of the oracle's
+    per-micro-batch stage gradients; returns (per stage a list of per-layer dicts,
+    the per-micro-batch losses)."""
+    tot, losses = None, []
+    for (k, j) in keys:
+        lo, g = PPL.microbatch_pass(stages, cfg, sd.stage_input(cfg, k, j), sd.stage_target(cfg, k, j))
+        losses.append(lo)
+        if tot is None:
+            tot = g
+        else:
+            for ts, gs in zip(tot, g):
+                for a, b in zip(ts, gs):
+                    for n in a:
+                        a[n] = a[n] + b[n]
+    return tot, losses
+
+
+EXEC_CFGS = {
+    "c1": (sd.C1_TINY, 1),
+    "d80_ragged": (sd.ModelCfg(hidden=640, heads=8, ffn=2560, seq=200, micro_batch=1, layers=2), 2),
+}
+
+
+def exec_vs_oracle(cfg, L, m, iters, total_layers=None):
+    """Run `iters` single-iteration slip_execute_schedule calls at N = 1 with the seeded
+    inputs; check Gate A on the gradient and Gate B on AdamW after each.  Returns the
+    per-iteration, per-layer worst relative error over the layer's tensors."""
+    rt = _rt()
+    layers = sd.stage_params(cfg, 0, L, total_layers=total_layers or max(L, 2))
+    costs = rt.make_costs(t_f=1, t_b=1, t_w=1, t_comm=0, t_ar=1, t_opt=1)
+    prog, need = rt.rank_program(1, 1, m, None, costs, 0)
+    kinds = [p[0] for p in prog]
+    # the N = 1 plan defers all W's to the end of the iteration: one merged launch over m slots
+    assert kinds.count(ACT["W"]) == m and kinds[-2 - m:-2] == [ACT["W"]] * m, kinds
+    st = rt.Stage(cfg, L, n_slots=need)
+    st.load_master(torch.from_numpy(sd.pack_stage(layers)).float().cuda())
+    comm = rt.Comm(0, 1)
+    comm.setup(1, 1, m, None)
+    xs = [host_bf16(sd.stage_input(cfg, 0, j)) for j in range(m)]
+    rs = [host_bf16(sd.stage_target(cfg, 0, j)) for j in range(m)]
+    losses = torch.zeros(m, dtype=torch.float32)
+    io = rt.make_io(xs, rs, losses)
+    adam = (ADAM.lr, ADAM.beta1, ADAM.beta2, ADAM.eps, ADAM.weight_decay)
+    m_ref = v_ref = None
+    growth = []
+    for it in range(1, iters + 1):
+        # the weights this iteration's F / B use: RNE(master) = the bf16 copy
+        params = sd.unpack_stage(as_np(st.w), cfg, L)
+        p_before = st.master.cpu().numpy().astype(np.float64)
+        rep = rt.execute_schedule(st, comm, 1, 1, m, None, costs, True, True, adam=adam, iterations=1, io=io)
+        torch.cuda.synchronize()
+        assert rep.w_gemm_launches == 1 and rep.phase_ops[2] == m  # merged W: 1 launch, m micro-batch W's
+        ref, lref = oracle_grad_sum([params], cfg, [(0, j) for j in range(m)])
+        ref = ref[0]
+        gflat = st.grad.cpu().numpy().astype(np.float64)
+        got = sd.unpack_stage(gflat, cfg, L)
+        per_layer = []
+        for l in range(L):
+            errs = {n: relerr(got[l][n], ref[l][n]) for n in sd.PARAM_ORDER}
+            per_layer.append(max(errs.values()))
+            for n, e in errs.items():
+                assert e <= GATE_A, (it, l, n, e)
+        growth.append(per_layer)
+        # losses (device MSE of the bf16 output) vs the oracle's
+        for j in range(m):
+            assert abs(losses[j].item() - lref[j]) <= 1e-2 * lref[j]
+        # Gate B: AdamW step `it` on the GPU's own gradient (grad_scale = 1 / (DP m))
+        Pm = sd.unpack_stage(p_before, cfg, L)
+        G = sd.unpack_stage(gflat, cfg, L)
+        if m_ref is None:
+            m_ref = [{n: np.zeros_like(a) for n, a in d.items()} for d in Pm]
+            v_ref = [{n: np.zeros_like(a) for n, a in d.items()} for d in Pm]
+        new_p, new_m, new_v = [], [], []
+        for l in range(L):
+            p1, m1, v1 = OA.adamw_step_layer(Pm[l], m_ref[l], v_ref[l], G[l], it, ADAM, grad_scale=1.0 / m)
+            new_p.append(p1), new_m.append(m1), new_v.append(v1)
+        p_got = st.master.cpu().numpy().astype(np.float64)
+        assert relerr(p_got - p_before, sd.pack_stage(new_p) - p_before) <= GATE_B
+        assert relerr(st.adam_m.cpu().numpy().astype(np.float64), sd.pack_stage(new_m)) <= GATE_B
+        assert relerr(st.adam_v.cpu().numpy().astype(np.float64), sd.pack_stage(new_v)) <= GATE_B
+        assert np.array_equal(as_np(st.w), sd.bf16_round(p_got))
+        # continue from the GPU's own optimizer state (identical fp32 inputs for the next Gate B)
+        m_ref = sd.unpack_stage(st.adam_m.cpu().numpy().astype(np.float64), cfg, L)
+        v_ref = sd.unpack_stage(st.adam_v.cpu().numpy().astype(np.float64), cfg, L)
+    comm.close()
+    st.close()
+    return growth
+
+
+@pytest.mark.parametrize("name", list(EXEC_CFGS))
+def test_execute_schedule_n1_matches_oracle(name):
+    cfg, L = EXEC_CFGS[name]
+    exec_vs_oracle(cfg, L, m=4, iters=2)
+
+
+@pytest.mark.slow
+def test_execute_schedule_c2_six_layer_stage_full_size():
+    """The C2 stage of SURVEY §8(d.2) at full size: 6 GPT-1.3B layers (h 2048, 16 heads,
+    s 2048), m = 4, through slip_execute_schedule — the bench's launch configuration,
+    including the merged W launch with K = 4T over 4 slots.  Gate A per tensor and per
+    layer; the per-layer error growth is printed and written to
+    gpurun_out/c2_six_layer_growth.json when that directory exists."""
+    import json
+    import os
+    growth = exec_vs_oracle(sd.C2_1P3B, 6, m=4, iters=1, total_layers=24)
+    line = {"config": "gpt-1.3b 6-layer stage, s 2048, m 4, merged W K=4T",
+            "worst_relerr_per_layer_input_to_output": growth[0]}
+    print(json.dumps(line))
+    if os.path.isdir("gpurun_out"):
+        with open("gpurun_out/c2_six_layer_growth.json", "w") as f:
+            json.dump(line, f)
+
+
+# ------------------------------------------------------------------ (ii) re-route on one GPU
+def run_programs(cfg, L, N, DP, m, live, costs, stages_params):
+    """Drive one Stage context per live worker through its rank program; returns
+    {(i, k): fp32 grad tensor} and the per-micro-batch losses."""
+    rt = _rt()
+    progs, ctxs, bufs = {}, {}, {}
+    T, h = cfg.tokens, cfg.hidden
+    for i in range(N):
+        for k in range(DP):
+            if not live[i][k]:
+                continue
+            r = rt.rank_of(N, i, k)
+            prog, need = rt.rank_program(N, DP, m, live, costs, r)
+            progs[r] = prog
+            st = rt.Stage(cfg, L, n_slots=max(1, need))
+            st.load_master(torch.from_numpy(sd.pack_stage(stages_params[i])).float().cuda())
+            ctxs[r] = st
+            mk = lambda: [torch.zeros(T, h, dtype=torch.bfloat16, device="cuda") for _ in range(max(1, need))]  # noqa
+            bufs[r] = {"x": mk(), "y": mk(), "dy": mk(), "dx": mk()}
+    queues = {}  # (src, dst, kind) -> list of ((iter, mb, origin), tensor)
+    pc = {r: 0 for r in progs}
+    losses = {}
+    loss_d = torch.zeros(1, device="cuda")
+    while any(pc[r] < len(progs[r]) for r in progs):
+        progressed = False
+        for r in progs:
+            st, b, prog = ctxs[r], bufs[r], progs[r]
+            i = r % N
+            while pc[r] < len(prog):
+                kind, it, mb, origin, peer, slot, acc = prog[pc[r]]
+                ident = (it, mb, origin)
+                if kind in (ACT["RECV_X"], ACT["RECV_DY"]):
+                    q = queues.get((peer, r, kind))
+                    if not q:
+                        break  # blocked on the sender
+                    got_id, t = q.pop(0)
+                    assert got_id == ident, ("per-pair FIFO violated", got_id, ident)
+                    (b["x"] if kind == ACT["RECV_X"] else b["dy"])[slot].copy_(t)
+                elif kind == ACT["LOAD_X"]:
+                    b["x"][slot].copy_(dev_bf16(sd.stage_input(cfg, origin, mb)))
+                elif kind == ACT["F"]:
+                    st.forward(slot, b["x"][slot], b["y"][slot])
+                elif kind == ACT["SEND_Y"]:
+                    queues.setdefault((r, peer, ACT["RECV_X"]), []).append((ident, b["y"][slot].clone()))
+                elif kind == ACT["LOSS"]:
+                    st.loss_mse(b["y"][slot], dev_bf16(sd.stage_target(cfg, origin, mb)), b["dy"][slot], loss_d)
+                    losses[(origin, mb)] = loss_d.item()
+                elif kind == ACT["B"]:
+                    st.backward_input(slot, b["dy"][slot], b["dx"][slot] if i > 0 else None, accumulate=bool(acc & 1))
+                elif kind == ACT["BC"]:
+                    st.backward_coupled(slot, b["dy"][slot], b["dx"][slot] if i > 0 else None,
+                                        accumulate=bool(acc & 1))
+                elif kind == ACT["SEND_DX"]:
+                    queues.setdefault((r, peer, ACT["RECV_DY"]), []).append((ident, b["dx"][slot].clone()))
+                elif kind == ACT["W"]:
+                    # the executor's merging: back-to-back W's of one iteration -> one launch
+                    run = 1
+                    while (pc[r] + run < len(prog) and run < 8 and prog[pc[r] + run][0] == ACT["W"]
+                           and prog[pc[r] + run][1] == it):
+                        run += 1
+                    if run == 1:
+                        st.backward_weight(slot, accumulate=bool(acc))
+                    else:
+                        st.backward_weight_multi([prog[pc[r] + q][5] for q in range(run)], accumulate=bool(acc))
+                    pc[r] += run - 1
+                # AR / OPT: the all-reduce is formed below (sum over live peers, ascending k)
+                pc[r] += 1
+                progressed = True
+        assert progressed, "deadlock: every rank blocked on a receive"
+    torch.cuda.synchronize()
+    assert all(not q for q in queues.values()), "unconsumed messages"
+    grads = {(r % N, r // N): ctxs[r].grad.clone() for r in progs}
+    for st in ctxs.values():
+        st.close()
+    return grads, losses
+
+
+REROUTE = [
+    # (N, DP, m, failed workers (i, k))
+    (1, 2, 3, [(0, 1)]),
+    (1, 2, 3, [(0, 0)]),
+    (2, 2, 2, [(1, 1)]),
+    (2, 2, 3, [(0, 0)]),
+]
+
+
+@pytest.mark.parametrize("N,DP,m,failed", REROUTE)
+def test_reroute_dp2_on_one_gpu_matches_oracle(N, DP, m, failed):
+    rt = _rt()
+    cfg, L = sd.ModelCfg(hidden=128, heads=2, ffn=512, seq=96, micro_batch=1, layers=2 * N), 1
+    stages = [sd.stage_params(cfg, i, L, total_layers=2 * N) for i in range(N)]
+    costs = rt.make_costs(t_f=2, t_b=2, t_w=1, t_comm=1, t_ar=1, t_opt=1)
+    live_ff = [[1] * DP for _ in range(N)]
+    live = [[1] * DP for _ in range(N)]
+    for (i, k) in failed:
+        live[i][k] = 0
+    g_ff, l_ff = run_programs(cfg, L, N, DP, m, live_ff, costs, stages)
+    g_rr, l_rr = run_programs(cfg, L, N, DP, m, live, costs, stages)
+    # re-routing changes which worker computes a micro-batch, never its numbers
+    assert l_rr == l_ff
+    # oracle form (ii): per-worker accumulation in the plan's W order, live-peer sum
+    delta, _ = PPL.contributions(stages, cfg, DP, m, {(k, j): sd.stage_input(cfg, k, j)
+                                                       for k in range(DP) for j in range(m)},
+                                 {(k, j): sd.stage_target(cfg, k, j) for k in range(DP) for j in range(m)})
+    plan = PL.schedule(live, m, PL.Costs(t_f=2, t_b=2, t_w=1, t_comm=1, t_ar=1, t_opt=1),
+                       PL.Opts(decoupled=True, staggered=True, horizon=1))
+    for i in range(N):
+        peers = [k for k in range(DP) if live[i][k]]
+        summed = g_rr[(i, peers[0])].clone()
+        for k in peers[1:]:
+            summed += g_rr[(i, k)]
+        ff = g_ff[(i, 0)].clone()
+        for k in range(1, DP):
+            ff += g_ff[(i, k)]
+        # against the fault-free GPU run: fp32 summation order only
+        assert ((summed - ff).abs().max() / ff.abs().max()).item() <= 1e-5, i
+        ref = PPL.per_worker_sum(delta, plan, live, i)
+        got = sd.unpack_stage(summed.cpu().numpy().astype(np.float64), cfg, L)
+        for l in range(L):
+            for n in sd.PARAM_ORDER:
+                e = relerr(got[l][n], ref[l][n])
+                assert e <= GATE_A, (i, l, n, e)
+    # the failed worker ran nothing; its peer ran every micro-batch of the stage
+    for (i, k) in failed:
+        assert (i, k) not in g_rr

@@ -8,7 +8,9 @@ B200 (tools/kernel_bench.py), Adam = A ms per million parameters (measured), P2P
 [T, h] bf16 activation over NVLink at 700 GB/s, the stage all-reduce at the measured
 NCCL bus bandwidth.  The C++ planner (the one the executor runs) produces the period for
 coupled 1F1B (the paper's baseline) and decoupled + staggered plans with 0 / 1 / 2
-masked workers at the normalized positions (reading R20).  Prints one JSON line per case.
+masked workers placed by Algorithm 1 (R = A[N-1][F] over the
+heuristic cost table of the same plan variant, slip_normalize_costs -> slip_normalize ->
+slip_normalized_live).  Prints one JSON line per case with R.
 """
 import argparse
 import json
@@ -48,22 +50,26 @@ def main():
     for m in a.m:
         base = None
         for nf in (0, 1, 2):
-            failed = [(a.pp - 1 - i, (i + 1) % a.dp) for i in range(nf)]
-            live = [[1] * a.dp for _ in range(a.pp)]
-            for (i, k) in failed:
-                live[i][k] = 0
-            if not rt.recoverable(a.pp, a.dp, live):
+            if nf > a.pp * (a.dp - 1):
                 continue
             row = {}
             for name, dec, stag in (("coupled_1f1b", False, False), ("decoupled_staggered", True, True)):
+                # Algorithm 1 over this plan variant's own cost table places the failures
+                R = [0] * a.pp
+                if nf:
+                    R, _ = rt.normalize(a.pp, a.dp, nf, rt.normalize_costs(a.pp, a.dp, m, costs, nf, dec, stag))
+                live = rt.normalized_live(a.pp, a.dp, R)
                 r = rt.plan_schedule(a.pp, a.dp, m, live, costs, dec, stag, horizon=3)
                 period_ms = r.period * unit
-                row[name] = {"period_ms": period_ms, "tokens_per_s": a.dp * m * T / (period_ms / 1e3)}
+                row[name] = {"period_ms": period_ms, "tokens_per_s": a.dp * m * T / (period_ms / 1e3), "R": R,
+                             "failed": [(i, k) for i in range(a.pp) for k in range(a.dp) if not live[i][k]]}
             if nf == 0:
                 base = row["coupled_1f1b"]["tokens_per_s"]
-            out = {"cfg": a.cfg, "dp": a.dp, "pp": a.pp, "layers_per_stage": L, "m": m, "failed": failed,
+                base_dec = row["decoupled_staggered"]["tokens_per_s"]
+            out = {"cfg": a.cfg, "dp": a.dp, "pp": a.pp, "layers_per_stage": L, "m": m, "failures": nf,
                    "costs_ms": {"F": f_ms, "B": b_ms, "W": w_ms, "OPT": opt_ms, "AR": ar_ms, "P2P": comm_ms}, **row,
-                   "slipstream_vs_faultfree_1f1b": row["decoupled_staggered"]["tokens_per_s"] / base}
+                   "slipstream_vs_faultfree_1f1b": row["decoupled_staggered"]["tokens_per_s"] / base,
+                   "slipstream_vs_faultfree_decoupled": row["decoupled_staggered"]["tokens_per_s"] / base_dec}
             print(json.dumps(out))
 
 
