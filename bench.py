@@ -183,7 +183,13 @@ def run_reference(args, rank, world):
     cores = cpu_cores()
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": args.gpus,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+        # each step times a bounded sample; the full step is extrapolated from it
+        "ms_per_step_kind": "extrapolated from the per-step sample (%d layers x %d micro-batches); "
+                            "measured sample time per step %.0f ms" % (args.layers, m,
+                                                                      1000.0 * statistics.median(samples)),
+        "sample_ms_per_step": 1000.0 * statistics.median(samples),
+        "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": "gpt-%s-shape (h%d s%d %d heads ffn%d) %d layers, m=%d, DP1xPP1" % (
             MODEL, H, SEQ, HEADS, FFN, args.layers, m), "model": "gpt-%s-shape" % MODEL, "global_batch": m * MB, "seq_len": SEQ,

@@ -31,8 +31,8 @@
  *
  * Numerics (readings R1, R10, R23): bf16 storage (RNE), fp32
  * accumulation in tensor memory (tcgen05), fp32 LayerNorm statistics, fp32
- * softmax, attention scores S and dP as fp32 transients, fp32 master weights,
- * gradients and Adam moments.
+ * softmax, attention scores S and dP as fp32 tensor-memory tiles inside the fused
+ * attention kernels (never stored), fp32 master weights, gradients and Adam moments.
  */
 #ifndef SLIP_H
 #define SLIP_H
@@ -204,7 +204,8 @@ slip_status slip_param_count(const slip_model* m, int32_t n_layers, int64_t* out
 
 /* Bytes of the stash arena for n_slots in-flight micro-batches (F-stash +
  * W-stash, the WeightGradStore of PAPER.md line 558), and of the shared
- * workspace (attention score / dP transients, reduction partials). */
+ * workspace (attention row sums D, [T, h] temporaries of B, reduction partials,
+ * loss scratch, the non-finite / validation flags). */
 slip_status slip_stash_bytes(const slip_model* m, int32_t n_layers, int32_t n_slots, size_t* out);
 slip_status slip_workspace_bytes(const slip_model* m, size_t* out);
 
