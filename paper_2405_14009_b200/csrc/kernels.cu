@@ -9,6 +9,7 @@
 #include <cmath>
 
 #include "kernels.cuh"
+#include "gemm.cuh"
 #include "launch.cuh"
 #include "ptx.cuh"
 
@@ -45,6 +46,18 @@ __device__ __forceinline__ void unpack8(const uint4& u, float (&f)[8]) {
     float2 v = __bfloat1622float2(h[i]);
     f[2 * i] = v.x;
     f[2 * i + 1] = v.y;
+  }
+}
+// bf16 -> f32 of 8 packed values by shifts / masks in inline asm (see ln_bwd_fused_kernel)
+__device__ __forceinline__ void unpack8_asm(const uint4& u, float (&f)[8]) {
+  const uint32_t w[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    uint32_t lo, hi;
+    asm("shl.b32 %0, %1, 16;" : "=r"(lo) : "r"(w[i]));
+    asm("and.b32 %0, %1, 0xffff0000;" : "=r"(hi) : "r"(w[i]));
+    f[2 * i] = __uint_as_float(lo);
+    f[2 * i + 1] = __uint_as_float(hi);
   }
 }
 __device__ __forceinline__ uint4 pack8(const float (&f)[8]) {
@@ -197,58 +210,6 @@ __global__ void __launch_bounds__(256) ln_bwd_rows_kernel(const bf16* __restrict
   }
 }
 
-// ------------------------------------------------------------------ LayerNorm bwd (row statistics)
-// One warp per row: stat[row] = (sum_c g, sum_c g xhat), g = dy gamma — the two row sums
-// the column pass (colred MODE 3 / 4) needs; reads dy and x only.
-template <int VPL>
-__global__ void __launch_bounds__(256) ln_bwd_stats_kernel(const bf16* __restrict__ dy, const bf16* __restrict__ x,
-                                                           const float* __restrict__ mean,
-                                                           const float* __restrict__ rstd,
-                                                           const bf16* __restrict__ gamma, float2* __restrict__ stat,
-                                                           int T, int h) {
-  __shared__ uint4 gs[VPL * 32];  // gamma, staged by the block while the rows load (as ln_fwd)
-  ptx::grid_dep_wait();
-  const int lane = threadIdx.x & 31;
-  const int row = blockIdx.x * LN_ROWS + (threadIdx.x >> 5);
-  const int nv = h >> 3;
-  for (int i = threadIdx.x; i < nv; i += 256) gs[i] = __ldg(reinterpret_cast<const uint4*>(gamma) + i);
-  const bool live = row < T;
-  const int rr = live ? row : 0;
-  const float mu = mean[rr], rs = rstd[rr];
-  const uint4* xr = reinterpret_cast<const uint4*>(x + static_cast<size_t>(rr) * h);
-  const uint4* dyr = reinterpret_cast<const uint4*>(dy + static_cast<size_t>(rr) * h);
-  uint4 xv[VPL], dv[VPL];
-#pragma unroll
-  for (int i = 0; i < VPL; ++i) {
-    const int idx = lane + 32 * i;
-    const bool ok = live && idx < nv;
-    xv[i] = ok ? xr[idx] : make_uint4(0, 0, 0, 0);
-    dv[i] = ok ? dyr[idx] : make_uint4(0, 0, 0, 0);
-  }
-  __syncthreads();
-  if (!live) return;
-  float s1 = 0.f, s2 = 0.f;
-#pragma unroll
-  for (int i = 0; i < VPL; ++i) {
-    const int idx = lane + 32 * i;
-    if (idx < nv) {
-      float a[8], d[8], gm[8];
-      unpack8(xv[i], a);
-      unpack8(dv[i], d);
-      unpack8(gs[idx], gm);
-#pragma unroll
-      for (int e = 0; e < 8; ++e) {
-        const float g = d[e] * gm[e];
-        s1 += g;
-        s2 += g * ((a[e] - mu) * rs);
-      }
-    }
-  }
-  s1 = warp_sum(s1);
-  s2 = warp_sum(s2);
-  if (lane == 0) stat[row] = make_float2(s1, s2);
-}
-
 // ------------------------------------------------------------------ column reductions
 // One block per 64-column strip covering ALL T rows: 256 threads = 8 column vectors
 // (16 bytes each) x 32 row groups; thread (cv, rg) sums rows rg, rg+32, ... of its 8
@@ -257,25 +218,15 @@ __global__ void __launch_bounds__(256) ln_bwd_stats_kernel(const bf16* __restric
 // MODE 0: out0 (+)= sum_t a.
 // MODE 1 (LayerNorm): out0 (+)= sum dy*xhat, out1 (+)= sum dy       (a = dy)
 // MODE 2 (LayerNorm + producer bias): MODE 1 and out2 (+)= sum_t dx (dx = the LN input grad)
-// MODE 3 / 4 (the whole LayerNorm backward, row statistics from the producing GEMM's
-// epilogue, GemmDesc::ln_stat): writes dx = resid + rstd (dy gamma - mean_h(g) -
-// xhat mean_h(g xhat)) and reduces like MODE 2 (3) or MODE 1 (4).
 constexpr int CR_COLS = 64;
-struct LnCols {
-  const bf16* gamma;
-  const bf16* resid;
-  bf16* dx;
-  const float2* stat;  // [T][nparts] (sum g, sum g xhat)
-  int nparts;
-};
 template <int MODE>
 __global__ void __launch_bounds__(256) colred_kernel(const bf16* __restrict__ a, int64_t ld, const bf16* __restrict__ x,
                                                      const float* __restrict__ mean, const float* __restrict__ rstd,
                                                      const bf16* __restrict__ dx, int T, int N, float* part,
                                                      float* __restrict__ out0, float* __restrict__ out1,
                                                      float* __restrict__ out2, int accumulate,
-                                                     unsigned* __restrict__ tickets, const LnCols lc) {
-  constexpr int NO = MODE == 0 ? 1 : ((MODE == 1 || MODE == 4) ? 2 : 3);  // outputs
+                                                     unsigned* __restrict__ tickets) {
+  constexpr int NO = MODE == 0 ? 1 : (MODE == 1 ? 2 : 3);  // outputs
   __shared__ float red[NO][32][CR_COLS + 1];
   (void)tickets;
   ptx::grid_dep_wait();
@@ -290,61 +241,7 @@ __global__ void __launch_bounds__(256) colred_kernel(const bf16* __restrict__ a,
   for (int o = 0; o < NO; ++o)
 #pragma unroll
     for (int e = 0; e < 8; ++e) acc[o][e] = 0.f;
-  if (MODE >= 3 && col < N) {
-    // the whole LayerNorm backward: rows in batches of LB per thread, every load of a
-    // batch (dy, x, resid, the row statistics) issued before any of its dx stores
-    constexpr int LB = 4;
-    float gm[8];
-    unpack8(__ldg(reinterpret_cast<const uint4*>(lc.gamma + col)), gm);
-    for (int rb = r0 + rg; rb < r1; rb += 32 * LB) {
-      uint4 dq[LB], xq[LB], rq[LB];
-      float s1[LB], s2[LB];
-#pragma unroll
-      for (int b = 0; b < LB; ++b) {
-        const int r = rb + 32 * b;
-        const bool ok = r < r1;
-        const size_t o = static_cast<size_t>(ok ? r : r0) * N + col;
-        dq[b] = ok ? __ldg(reinterpret_cast<const uint4*>(a + static_cast<size_t>(r) * ld + col)) : make_uint4(0, 0, 0, 0);
-        xq[b] = ok ? __ldg(reinterpret_cast<const uint4*>(x + o)) : make_uint4(0, 0, 0, 0);
-        rq[b] = (ok && lc.resid) ? __ldg(reinterpret_cast<const uint4*>(lc.resid + o)) : make_uint4(0, 0, 0, 0);
-        s1[b] = 0.f;
-        s2[b] = 0.f;
-        if (ok) {  // the row's statistics: parts in index order
-          const float2* st = lc.stat + static_cast<size_t>(r) * lc.nparts;
-          for (int q = 0; q < lc.nparts; ++q) {
-            const float2 w = __ldg(st + q);
-            s1[b] += w.x;
-            s2[b] += w.y;
-          }
-        }
-      }
-#pragma unroll
-      for (int b = 0; b < LB; ++b) {
-        const int r = rb + 32 * b;
-        if (r >= r1) break;
-        float v[8], xv[8], rv[8], o[8];
-        unpack8(dq[b], v);
-        unpack8(xq[b], xv);
-        unpack8(rq[b], rv);
-        const float mg = s1[b] / N, mgx = s2[b] / N, mu = __ldg(mean + r), rs = __ldg(rstd + r);
-#pragma unroll
-        for (int e = 0; e < 8; ++e) {
-          const float xh = (xv[e] - mu) * rs;
-          o[e] = rv[e] + rs * (v[e] * gm[e] - mg - xh * mgx);
-          acc[0][e] += v[e] * xh;
-          acc[1][e] += v[e];
-        }
-        const uint4 packed = pack8(o);
-        *reinterpret_cast<uint4*>(lc.dx + static_cast<size_t>(r) * N + col) = packed;
-        if (MODE == 3) {
-          float gv[8];
-          unpack8(packed, gv);
-#pragma unroll
-          for (int e = 0; e < 8; ++e) acc[2][e] += gv[e];
-        }
-      }
-    }
-  } else if (MODE == 0 && col < N) {
+  if (MODE == 0 && col < N) {
     // bias gradients: batches of 8 rows per thread, all 8 loads in flight before the adds
     constexpr int RB = 8;
     for (int rb = r0 + rg; rb < r1; rb += 32 * RB) {
@@ -409,6 +306,174 @@ __global__ void __launch_bounds__(256) colred_kernel(const bf16* __restrict__ a,
         part[(static_cast<size_t>(o) * R + blockIdx.y) * N + gcol] = s;
       }
     }
+  }
+}
+
+// ------------------------------------------------------------------ LayerNorm bwd (fused, row blocks)
+// The whole LayerNorm backward in ONE pass over the rows (replaces a row-statistics pass +
+// a column-strip pass): block b owns rows [b*rpb, (b+1)*rpb) — one block of 512 threads per
+// SM; each half of the block (256 threads) takes RB rows per pass, thread t of a half owns
+// the 16-byte column vectors t, t + 256, ... (VPT of them) of its rows.
+//   loads:  dy, x, resid, mean, rstd of the pass's rows, all in flight before any use;
+//   stats:  per row (sum g, sum g xhat), g = dy gamma, over the half's 8 warps (shuffles,
+//           then the warps in index order);
+//   output: dx = resid + rstd (g - mean_h(g) - xhat mean_h(g xhat)) (bf16), and the column
+//           partials dgamma += dy xhat, dbeta += dy (NO = 3: + sum dx as stored) kept in
+//           registers across the block's rows;
+// at the end the two halves' column partials are added (half 0 + half 1) through shared
+// memory and the block writes one partial row per output (part[(o * R + b) * h + c]),
+// summed in block order by the deferred finalize (deterministic).  dx == NULL: only
+// dgamma, dbeta (NO = 2).
+template <int VPT, int NO>
+__global__ void __launch_bounds__(512, 1) ln_bwd_fused_kernel(const bf16* __restrict__ dy, const bf16* __restrict__ x,
+                                                              const float* __restrict__ mean,
+                                                              const float* __restrict__ rstd,
+                                                              const bf16* __restrict__ gamma,
+                                                              const bf16* __restrict__ resid, bf16* __restrict__ dx,
+                                                              int T, int h, int rpb, float* __restrict__ part) {
+  constexpr int RB = 4 / VPT;  // rows per half per pass: RB x VPT x 3 x 16 B in flight per thread
+  __shared__ float2 red[2][2][8][RB];
+  extern __shared__ float comb[];  // [NO][VPT][8][256] half 1's column partials
+  ptx::grid_dep_wait();
+  const int nv = h >> 3;
+  const int hv = threadIdx.x >> 8, tid = threadIdx.x & 255;
+  const int warp = tid >> 5, lane = tid & 31;
+  const float inv_h = 1.0f / static_cast<float>(h);
+  float gm[VPT][8];
+  float acc[NO][VPT][8];
+#pragma unroll
+  for (int v = 0; v < VPT; ++v) {
+    const int c = tid + 256 * v;
+    unpack8(c < nv ? __ldg(reinterpret_cast<const uint4*>(gamma) + c) : make_uint4(0, 0, 0, 0), gm[v]);
+#pragma unroll
+    for (int o = 0; o < NO; ++o)
+#pragma unroll
+      for (int e = 0; e < 8; ++e) acc[o][v][e] = 0.f;
+  }
+  const int rb0 = blockIdx.x * rpb, rb1 = min(T, rb0 + rpb);
+  int buf = 0;
+  for (int p0 = rb0; p0 < rb1; p0 += 2 * RB, buf ^= 1) {
+    const int r0 = p0 + hv * RB;
+    uint4 dq[RB][VPT], xq[RB][VPT], rq[RB][VPT];
+    float mu[RB], rs[RB];
+#pragma unroll
+    for (int b = 0; b < RB; ++b) {
+      const int r = r0 + b;
+      const bool rok = r < rb1;
+      mu[b] = rok ? __ldg(mean + r) : 0.f;
+      rs[b] = rok ? __ldg(rstd + r) : 0.f;
+#pragma unroll
+      for (int v = 0; v < VPT; ++v) {
+        const int c = tid + 256 * v;
+        const bool ok = rok && c < nv;
+        const size_t o = static_cast<size_t>(ok ? r : 0) * nv + c;
+        dq[b][v] = ok ? __ldg(reinterpret_cast<const uint4*>(dy) + o) : make_uint4(0, 0, 0, 0);
+        xq[b][v] = ok ? __ldg(reinterpret_cast<const uint4*>(x) + o) : make_uint4(0, 0, 0, 0);
+        rq[b][v] = (ok && dx && resid) ? __ldg(reinterpret_cast<const uint4*>(resid) + o) : make_uint4(0, 0, 0, 0);
+      }
+    }
+    float s1[RB], s2[RB];
+#pragma unroll
+    for (int b = 0; b < RB; ++b) {
+      s1[b] = 0.f;
+      s2[b] = 0.f;
+#pragma unroll
+      for (int v = 0; v < VPT; ++v) {
+        // (a second unpack instruction sequence: with the same one the compiler keeps the
+        // unpacked rows alive from here to the output pass instead of the packed vectors)
+        float d[8], a[8];
+        unpack8_asm(dq[b][v], d);
+        unpack8_asm(xq[b][v], a);
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+          const float g = d[e] * gm[v][e];
+          s1[b] += g;
+          s2[b] += g * ((a[e] - mu[b]) * rs[b]);
+        }
+      }
+      s1[b] = warp_sum(s1[b]);
+      s2[b] = warp_sum(s2[b]);
+    }
+    if (lane == 0) {
+#pragma unroll
+      for (int b = 0; b < RB; ++b) red[buf][hv][warp][b] = make_float2(s1[b], s2[b]);
+    }
+    __syncthreads();  // (red is double-buffered: one barrier per pass)
+#pragma unroll
+    for (int b = 0; b < RB; ++b) {
+      float t1 = 0.f, t2 = 0.f;
+#pragma unroll
+      for (int w = 0; w < 8; ++w) {
+        const float2 q = red[buf][hv][w][b];
+        t1 += q.x;
+        t2 += q.y;
+      }
+      s1[b] = t1 * inv_h;  // mean_h(g)
+      s2[b] = t2 * inv_h;  // mean_h(g xhat)
+    }
+#pragma unroll
+    for (int b = 0; b < RB; ++b) {
+      const int r = r0 + b;
+#pragma unroll
+      for (int v = 0; v < VPT; ++v) {
+        const int c = tid + 256 * v;
+        if (r >= rb1 || c >= nv) continue;  // (no break: the row arrays must stay in registers)
+        float d[8], a[8];
+        unpack8(dq[b][v], d);
+        unpack8(xq[b][v], a);
+        if (dx) {
+          float rv[8], o[8];
+          unpack8(rq[b][v], rv);
+#pragma unroll
+          for (int e = 0; e < 8; ++e) {
+            const float xh = (a[e] - mu[b]) * rs[b];
+            acc[0][v][e] += d[e] * xh;
+            acc[1][v][e] += d[e];
+            o[e] = rv[e] + rs[b] * (d[e] * gm[v][e] - s1[b] - xh * s2[b]);
+          }
+          const uint4 packed = pack8(o);
+          reinterpret_cast<uint4*>(dx)[static_cast<size_t>(r) * nv + c] = packed;
+          if (NO == 3) {
+            float gv[8];
+            unpack8(packed, gv);
+#pragma unroll
+            for (int e = 0; e < 8; ++e) acc[NO - 1][v][e] += gv[e];
+          }
+        } else {
+#pragma unroll
+          for (int e = 0; e < 8; ++e) {
+            acc[0][v][e] += d[e] * ((a[e] - mu[b]) * rs[b]);
+            acc[1][v][e] += d[e];
+          }
+        }
+      }
+    }
+  }
+  // half 0 + half 1, then one partial row of each output per block
+  if (hv == 1) {
+#pragma unroll
+    for (int o = 0; o < NO; ++o)
+#pragma unroll
+      for (int v = 0; v < VPT; ++v)
+#pragma unroll
+        for (int e = 0; e < 8; ++e) comb[((o * VPT + v) * 8 + e) * 256 + tid] = acc[o][v][e];
+  }
+  __syncthreads();
+  if (hv == 0) {
+#pragma unroll
+    for (int o = 0; o < NO; ++o)
+#pragma unroll
+      for (int v = 0; v < VPT; ++v) {
+        const int c = tid + 256 * v;
+        if (c < nv) {
+          float t[8];
+#pragma unroll
+          for (int e = 0; e < 8; ++e) t[e] = acc[o][v][e] + comb[((o * VPT + v) * 8 + e) * 256 + tid];
+          float4* dst = reinterpret_cast<float4*>(part + (static_cast<size_t>(o) * gridDim.x + blockIdx.x) * h + 8 * c);
+          dst[0] = make_float4(t[0], t[1], t[2], t[3]);
+          dst[1] = make_float4(t[4], t[5], t[6], t[7]);
+        }
+      }
   }
 }
 
@@ -874,56 +939,51 @@ cudaError_t ln_bwd(const bf16* dy, const bf16* x, const float* mean, const float
   }
   cudaError_t e = three ? launch_pdl(colred_kernel<2>, grid, dim3(256), 0, s, 1, dy, static_cast<int64_t>(h), x, mean,
                                      rstd, static_cast<const bf16*>(dx), T, h, part, dgamma, dbeta, dxsum, accumulate,
-                                     tickets, LnCols{})
+                                     tickets)
                         : launch_pdl(colred_kernel<1>, grid, dim3(256), 0, s, 1, dy, static_cast<int64_t>(h), x, mean,
                                      rstd, static_cast<const bf16*>(nullptr), T, h, part, dgamma, dbeta,
-                                     static_cast<float*>(nullptr), accumulate, tickets, LnCols{});
+                                     static_cast<float*>(nullptr), accumulate, tickets);
   if (e != cudaSuccess || R == 1 || defer) return e;
   return launch_pdl(colred_finalize_kernel, dim3((h * NO + 255) / 256), dim3(256), 0, s, 1,
                     static_cast<const float*>(part), R, h, NO, dgamma, dbeta, three ? dxsum : static_cast<float*>(nullptr),
                     accumulate);
 }
 
-cudaError_t ln_bwd2(const bf16* dy, const bf16* x, const float* mean, const float* rstd, const bf16* gamma,
-                    const bf16* resid, bf16* dx, float* stat, float* dgamma, float* dbeta, float* dxsum, int accumulate,
-                    float* part, int T, int h, cudaStream_t s, RedBatch* defer) {
-  if (h % 8 || h > 8192 || !dx || dx == x || dx == dy || !stat) return cudaErrorInvalidValue;
-  {
-    const int v = ln_vpl(h);
-    const dim3 grid((T + LN_ROWS - 1) / LN_ROWS);
-    cudaError_t e = cudaErrorInvalidValue;
-#define X(n)                                                                                                   \
-  if (e == cudaErrorInvalidValue && v <= n)                                                                    \
-    e = launch_pdl(ln_bwd_stats_kernel<n>, grid, dim3(256), 0, s, 1, dy, x, mean, rstd, gamma,                 \
-                   reinterpret_cast<float2*>(stat), T, h);                                                      \
-  else
-    SLIP_LN_VPL_CASES(X) {}
-#undef X
-    if (e != cudaSuccess) return e;
-  }
-  const int nparts = 1;
-  const int R = colred_chunks(h, 2);  // 128 registers: 2 blocks per SM
-  dim3 grid((h + CR_COLS - 1) / CR_COLS, R);
+cudaError_t ln_bwd_fused(const bf16* dy, const bf16* x, const float* mean, const float* rstd, const bf16* gamma,
+                         const bf16* resid, bf16* dx, float* dgamma, float* dbeta, float* dxsum, int T, int h,
+                         cudaStream_t s, RedBatch* defer) {
+  const int nv = h / 8;
+  const int vpt = (nv + 255) / 256;
+  if (h % 8 || vpt > 4 || !defer || (dx && (dx == x || dx == dy)) || (dxsum && !dx)) return cudaErrorInvalidValue;
+  const int vp = vpt <= 1 ? 1 : (vpt <= 2 ? 2 : 4);
+  // one block of 16 warps per SM: the partial rows (one per block) stay few
+  const int rpb = (T + num_sms() - 1) / num_sms();
+  const int nb = (T + rpb - 1) / rpb;
   const bool three = dxsum != nullptr;
   const int NO = three ? 3 : 2;
-  if (defer) {
-    part = defer->add(R, h, NO, dgamma, dbeta, three ? dxsum : nullptr);
-    if (!part) return cudaErrorInvalidValue;
-  } else if (R == 1) {
-    part = nullptr;
-  }
-  const LnCols lc{gamma, resid, dx, reinterpret_cast<const float2*>(stat), nparts};
-  cudaError_t e =
-      three ? launch_pdl(colred_kernel<3>, grid, dim3(256), 0, s, 1, dy, static_cast<int64_t>(h), x, mean, rstd,
-                         static_cast<const bf16*>(nullptr), T, h, part, dgamma, dbeta, dxsum, accumulate,
-                         static_cast<unsigned*>(nullptr), lc)
-            : launch_pdl(colred_kernel<4>, grid, dim3(256), 0, s, 1, dy, static_cast<int64_t>(h), x, mean, rstd,
-                         static_cast<const bf16*>(nullptr), T, h, part, dgamma, dbeta, static_cast<float*>(nullptr),
-                         accumulate, static_cast<unsigned*>(nullptr), lc);
-  if (e != cudaSuccess || R == 1 || defer) return e;
-  return launch_pdl(colred_finalize_kernel, dim3((h * NO + 255) / 256), dim3(256), 0, s, 1,
-                    static_cast<const float*>(part), R, h, NO, dgamma, dbeta, three ? dxsum : static_cast<float*>(nullptr),
-                    accumulate);
+  float* part = defer->add(nb, h, NO, dgamma, dbeta, three ? dxsum : nullptr);
+  if (!part) return cudaErrorInvalidValue;
+  const int smem = NO * vp * 8 * 256 * static_cast<int>(sizeof(float));
+#define L(V, N)                                                                                                    \
+  [&]() -> cudaError_t {                                                                                           \
+    static bool attr_ = false;                                                                                     \
+    if (!attr_) {                                                                                                  \
+      cudaFuncSetAttribute(ln_bwd_fused_kernel<V, N>, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024);     \
+      attr_ = true;                                                                                                \
+    }                                                                                                              \
+    return launch_pdl(ln_bwd_fused_kernel<V, N>, dim3(nb), dim3(512), smem, s, 1, dy, x, mean, rstd, gamma, resid, \
+                      dx, T, h, rpb, part);                                                                        \
+  }()
+  if (vp == 1) return three ? L(1, 3) : L(1, 2);
+  if (vp == 2) return three ? L(2, 3) : L(2, 2);
+  return three ? L(4, 3) : L(4, 2);
+#undef L
+}
+
+int ln_bwd_fused_parts(int T, int h) {
+  (void)h;
+  const int rpb = (T + num_sms() - 1) / num_sms();
+  return (T + rpb - 1) / rpb;
 }
 
 int colred_launches(int N) { return colred_chunks(N, 4) > 1 ? 2 : 1; }
@@ -971,7 +1031,7 @@ cudaError_t colsum(const bf16* a, int T, int N, int64_t ld, float* out, int accu
   cudaError_t e = launch_pdl(colred_kernel<0>, grid, dim3(256), 0, s, 1, a, ld, static_cast<const bf16*>(nullptr),
                              static_cast<const float*>(nullptr), static_cast<const float*>(nullptr),
                              static_cast<const bf16*>(nullptr), T, N, part, out, static_cast<float*>(nullptr),
-                             static_cast<float*>(nullptr), accumulate, tickets, LnCols{});
+                             static_cast<float*>(nullptr), accumulate, tickets);
   if (e != cudaSuccess || R == 1 || defer) return e;
   return launch_pdl(colred_finalize_kernel, dim3((N + 255) / 256), dim3(256), 0, s, 1, static_cast<const float*>(part),
                     R, N, 1, out, static_cast<float*>(nullptr), static_cast<float*>(nullptr), accumulate);

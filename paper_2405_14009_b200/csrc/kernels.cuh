@@ -56,14 +56,15 @@ cudaError_t ln_bwd(const bf16* dy, const bf16* x, const float* mean, const float
                    const bf16* resid, bf16* dx, float* dgamma, float* dbeta, float* dxsum, int accumulate, float* part,
                    unsigned* tickets, int T, int h, cudaStream_t s, RedBatch* defer = nullptr);
 
-// LayerNorm backward as a row-statistics pass and ONE column-strip pass: stat[t] =
-// (sum g, sum g*xhat) (stat: 2T floats of scratch), then dx = resid + rstd (dy*gamma -
-// mean_h(g) - xhat mean_h(g xhat)) written as bf16 while dgamma, dbeta (and dxsum if
-// non-null, over the stored bf16 dx) are reduced as ln_bwd does.  resid may be null;
-// dx must not alias x or dy.
-cudaError_t ln_bwd2(const bf16* dy, const bf16* x, const float* mean, const float* rstd, const bf16* gamma,
-                    const bf16* resid, bf16* dx, float* stat, float* dgamma, float* dbeta, float* dxsum, int accumulate,
-                    float* part, int T, int h, cudaStream_t s, RedBatch* defer = nullptr);
+// The whole LayerNorm backward in one pass over row blocks (ln_bwd_fused_kernel): dx =
+// resid + rstd (dy*gamma - mean_h(g) - xhat mean_h(g*xhat)) (dx may be NULL: reductions
+// only), and the deferred column reductions dgamma, dbeta and (dxsum != NULL, needs dx)
+// sum_t dx over the stored bf16 dx; one partial row per block (ln_bwd_fused_parts).
+// h % 8 == 0, h <= 8192; dx must not alias x or dy.
+cudaError_t ln_bwd_fused(const bf16* dy, const bf16* x, const float* mean, const float* rstd, const bf16* gamma,
+                         const bf16* resid, bf16* dx, float* dgamma, float* dbeta, float* dxsum, int T, int h,
+                         cudaStream_t s, RedBatch* defer);
+int ln_bwd_fused_parts(int T, int h);
 
 // out[n] (+)= sum_t a[t, n] for a bf16 [T, N] matrix with row stride ld (bias gradients).
 cudaError_t colsum(const bf16* a, int T, int N, int64_t ld, float* out, int accumulate, float* part,

@@ -175,11 +175,10 @@ void carve_ws(Carver& cv, const Dims& d, Workspace* out) {
   w.dO = cv.take<bf16>(Th);
   w.dy1 = cv.take<bf16>(Th);
   w.part = cv.take<float>(3 * red);
-  w.lnstat = cv.take<float>(2 * static_cast<size_t>(d.T));
   // deferred reductions: the four of a layer (b1, bqkv per (batch, 32-row group) from the
   // attention backward, LN2 + bo, LN1 + b2 below) for 8 layers before a flush
   w.red_cap = 8 * (colred_part_floats(d.f, 1) + static_cast<size_t>(d.b) * ((d.s + 31) / 32) * 3 * d.h +
-                   2 * colred_part_floats(d.h, 3)) +
+                   2 * static_cast<size_t>(ln_bwd_fused_parts(d.T, d.h)) * d.h * 3) +
               colred_part_floats(d.h, 1);
   w.red = cv.take<float>(w.red_cap);
   w.tickets = cv.take<unsigned>(kTickets);
@@ -482,11 +481,11 @@ slip_status backward_input_impl(slip_ctx* c, int slot, const void* dy, void* dx,
     // dY2 = dH W1
     SLIP_TRY(linear_dx(c, ls.dh, Wt.w1, D.f, D.h, c->ws.dy2, EPI_BF16, nullptr, s));
     // LN2 backward + residual: dX2 = dOut + LN2'(dY2); dgamma2, dbeta2, dbo = colsum(dX2)
-    SLIP_TRY(red_reserve(c, D.h, 3, accumulate, s));
+    SLIP_TRY(red_reserve_floats(c, static_cast<size_t>(ln_bwd_fused_parts(D.T, D.h)) * D.h * 3, accumulate, s));
     SLIP_TRY(kcheck(c,
-                    ln_bwd2(c->ws.dy2, ls.x2, ls.mean2, ls.rstd2, Wt.g2, ls.dout, ls.dx2, c->ws.lnstat, G.g2, G.b2n,
-                            G.bo, accumulate, c->ws.part, D.T, D.h, s, &c->red),
-                    "ln_bwd2 2", 2));
+                    ln_bwd_fused(c->ws.dy2, ls.x2, ls.mean2, ls.rstd2, Wt.g2, ls.dout, ls.dx2, G.g2, G.b2n, G.bo, D.T,
+                                 D.h, s, &c->red),
+                    "ln_bwd_fused 2", 1));
     // dO = dX2 Wo
     SLIP_TRY(linear_dx(c, ls.dx2, Wt.wo, D.h, D.h, c->ws.dO, EPI_BF16, nullptr, s));
     // attention backward (dQKV, and dbqkv's column sums per (batch, 32-row group))
@@ -499,18 +498,12 @@ slip_status backward_input_impl(slip_ctx* c, int slot, const void* dy, void* dx,
     // with the embedding end the input gradient always lands in the slot (W's scatter reads it)
     bf16* dxl = l > 0 ? sb.layer[l - 1].dout : ((D.ends & 1) ? sb.dx : static_cast<bf16*>(dx));
     float* dxsum = l > 0 ? layer_g(c, l - 1).b2 : nullptr;
-    SLIP_TRY(red_reserve(c, D.h, 3, accumulate, s));
-    if (dxl) {
-      SLIP_TRY(kcheck(c,
-                      ln_bwd2(c->ws.dy1, ls.xin, ls.mean1, ls.rstd1, Wt.g1, ls.dx2, dxl, c->ws.lnstat, G.g1, G.b1n,
-                              dxsum, accumulate, c->ws.part, D.T, D.h, s, &c->red),
-                      "ln_bwd2 1", 2));
-    } else {  // stage 0 without an input gradient: only dgamma1, dbeta1
-      SLIP_TRY(kcheck(c,
-                      ln_bwd(c->ws.dy1, ls.xin, ls.mean1, ls.rstd1, Wt.g1, ls.dx2, nullptr, G.g1, G.b1n, nullptr,
-                             accumulate, c->ws.part, c->ws.tickets, D.T, D.h, s, &c->red),
-                      "ln_bwd 1", 1));
-    }
+    // (stage 0 without an input gradient: dx = NULL, only dgamma1, dbeta1)
+    SLIP_TRY(red_reserve_floats(c, static_cast<size_t>(ln_bwd_fused_parts(D.T, D.h)) * D.h * 3, accumulate, s));
+    SLIP_TRY(kcheck(c,
+                    ln_bwd_fused(c->ws.dy1, ls.xin, ls.mean1, ls.rstd1, Wt.g1, ls.dx2, dxl, G.g1, G.b1n,
+                                 dxl ? dxsum : nullptr, D.T, D.h, s, &c->red),
+                    "ln_bwd_fused 1", 1));
   }
   SLIP_TRY(red_flush(c, accumulate, s));
   if ((D.ends & 1) && dx && dx != sb.dx)

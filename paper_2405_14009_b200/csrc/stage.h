@@ -59,7 +59,6 @@ struct Workspace {
   float* losses;     // [1024] per-micro-batch losses (executor)
   int32_t* nonfinite;  // [1] post-step validation flag (executor)
   int32_t* vflags;     // [8] validated mode: own_bad[2], global_bad[2] (per iteration parity), rollbacks
-  float* lnstat;       // [T][2] LayerNorm-backward row statistics (sum g, sum g xhat)
   float* red;          // deferred column-reduction partials of a B call (RedBatch arena)
   size_t red_cap;      // floats
   float* sk_ws;        // stream-K fp32 partials of the F / B linears (gemm_sk_bytes)
