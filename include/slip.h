@@ -460,6 +460,7 @@ typedef struct {
   int64_t phase_ops[6];
   int64_t w_gemm_launches;   /* tcgen05 GEMM launches issued by the W / BC ops */
   int64_t rollbacks;         /* validated mode: optimizer steps this rank rolled back */
+  int64_t skipped;           /* validated mode: steps this rank skipped on its own failed validation */
 } slip_report;
 
 /* Runs `iterations` training iterations of the plan on this rank (worker

@@ -82,7 +82,8 @@ class slip_report(C.Structure):
     _fields_ = [("period_ms", C.c_double), ("total_ms", C.c_double), ("predicted_period", C.c_int64),
                 ("n_ops", C.c_int64), ("n_kernels", C.c_int64), ("plan_hash", C.c_uint64),
                 ("last_loss", C.c_float), ("nonfinite", C.c_int32), ("phase_ms", C.c_double * 6),
-                ("phase_ops", C.c_int64 * 6), ("w_gemm_launches", C.c_int64), ("rollbacks", C.c_int64)]
+                ("phase_ops", C.c_int64 * 6), ("w_gemm_launches", C.c_int64), ("rollbacks", C.c_int64),
+                ("skipped", C.c_int64)]
 
 
 P = C.c_void_p

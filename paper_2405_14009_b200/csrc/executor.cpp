@@ -126,7 +126,7 @@ extern "C" slip_status slip_execute_schedule(slip_ctx* ctx, slip_comm* comm, con
   const bool tracing = ctx->trace_on;
   int64_t launches0 = ctx->launches;
 
-  if (ctx->validate) SLIP_CUDA(cudaMemsetAsync(ctx->ws.vflags + 4, 0, sizeof(int32_t), cs));
+  if (ctx->validate) SLIP_CUDA(cudaMemsetAsync(ctx->ws.vflags + 4, 0, 2 * sizeof(int32_t), cs));
   // host inputs (slip_io): copied on their own stream as soon as the slot is free, so the
   // copies of later micro-batches overlap the compute of earlier ones
   if (io && !ctx->h2d) SLIP_CUDA(cudaStreamCreateWithFlags(&ctx->h2d, cudaStreamNonBlocking));
@@ -506,11 +506,12 @@ extern "C" slip_status slip_execute_schedule(slip_ctx* ctx, slip_comm* comm, con
   SLIP_CUDA(cudaMemcpy(&nf, ctx->ws.nonfinite, sizeof nf, cudaMemcpyDeviceToHost));
   out->nonfinite = nf;
   if (ctx->validate) {
-    int32_t rb = 0;
-    SLIP_CUDA(cudaMemcpy(&rb, ctx->ws.vflags + 4, sizeof rb, cudaMemcpyDeviceToHost));
-    out->rollbacks = rb;
+    int32_t rs[2] = {0, 0};  // rollbacks, skipped steps
+    SLIP_CUDA(cudaMemcpy(rs, ctx->ws.vflags + 4, sizeof rs, cudaMemcpyDeviceToHost));
+    out->rollbacks = rs[0];
+    out->skipped = rs[1];
     // a rolled-back or skipped step does not count towards AdamW's bias correction next call
-    ctx->opt_step -= rb;
+    ctx->opt_step -= rs[0] + rs[1];
   }
   return SLIP_OK;
 }

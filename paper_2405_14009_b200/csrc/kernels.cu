@@ -1075,6 +1075,15 @@ cudaError_t adamw_rollback(float* p, float* m, float* v, const float* g, bf16* w
                     count);
 }
 
+__global__ void count_flag_kernel(const int32_t* __restrict__ flag, int32_t* __restrict__ count) {
+  ptx::grid_dep_wait();
+  if (threadIdx.x == 0 && *flag) *count += 1;
+}
+
+cudaError_t count_flag(const int32_t* flag, int32_t* count, cudaStream_t s) {
+  return launch_pdl(count_flag_kernel, dim3(1), dim3(32), 0, s, 1, flag, count);
+}
+
 cudaError_t grad_check(const float* g, int64_t n, int32_t* bad, int32_t* nonfinite, cudaStream_t s) {
   if (n % 4) return cudaErrorInvalidValue;
   return launch_pdl(grad_check_kernel, dim3(grid_for(n / 4)), dim3(256), 0, s, 1, g, n / 4, bad, nonfinite);

@@ -113,6 +113,9 @@ cudaError_t synth_tokens(int32_t* out, int64_t n, int32_t n_classes, uint64_t se
 // *bad |= any element of g not finite (and *nonfinite, if not NULL)
 cudaError_t grad_check(const float* g, int64_t n, int32_t* bad, int32_t* nonfinite, cudaStream_t s);
 
+// *count += (*flag != 0) (one thread; validated mode's count of skipped steps)
+cudaError_t count_flag(const int32_t* flag, int32_t* count, cudaStream_t s);
+
 // bf16 <- RNE(fp32)
 cudaError_t f32_to_bf16(const float* src, bf16* dst, int64_t n, cudaStream_t s);
 

@@ -815,11 +815,13 @@ slip_status validated_step(slip_ctx* c, const slip_adam* a, int64_t step, float 
   SLIP_CUDA(cudaMemsetAsync(own, 0, sizeof(int32_t), s));
   if (fault) SLIP_CUDA(cudaMemsetAsync(own, 1, 1, s));
   SLIP_TRY(kcheck(c, grad_check(c->grad, c->n_params, own, c->ws.nonfinite, s), "grad_check"));
-  return kcheck(c,
-                adamw(c->master, c->adam_m, c->adam_v, c->grad, c->w, c->n_params, c->po.per_layer, c->dm.h, c->dm.f,
-                      a->lr, a->beta1, a->beta2, a->eps, a->weight_decay, static_cast<float>(bc1),
-                      static_cast<float>(bc2), grad_scale, c->ws.nonfinite, s, own, tail_decay(c)),
-                "adamw");
+  SLIP_TRY(kcheck(c,
+                  adamw(c->master, c->adam_m, c->adam_v, c->grad, c->w, c->n_params, c->po.per_layer, c->dm.h,
+                        c->dm.f, a->lr, a->beta1, a->beta2, a->eps, a->weight_decay, static_cast<float>(bc1),
+                        static_cast<float>(bc2), grad_scale, c->ws.nonfinite, s, own, tail_decay(c)),
+                  "adamw"));
+  // a skipped step does not count towards AdamW's bias correction (the executor subtracts it)
+  return kcheck(c, count_flag(own, c->ws.vflags + 5, s), "count_flag");
 }
 // Conditional reversal of the step taken with (step, grad_scale): acts iff *glob && !*own.
 slip_status rollback_if(slip_ctx* c, const slip_adam* a, int64_t step, float grad_scale, const int32_t* glob,

@@ -58,7 +58,7 @@ struct Workspace {
   float* loss_part;  // [256] MSE partials
   float* losses;     // [1024] per-micro-batch losses (executor)
   int32_t* nonfinite;  // [1] post-step validation flag (executor)
-  int32_t* vflags;     // [8] validated mode: own_bad[2], global_bad[2] (per iteration parity), rollbacks
+  int32_t* vflags;     // [8] validated mode: own_bad[2], global_bad[2] (per iteration parity), rollbacks, skips
   float* red;          // deferred column-reduction partials of a B call (RedBatch arena)
   size_t red_cap;      // floats
   float* sk_ws;        // stream-K fp32 partials of the F / B linears (gemm_sk_bytes)

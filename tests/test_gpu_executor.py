@@ -293,3 +293,99 @@ def test_reroute_dp2_on_one_gpu_matches_oracle(N, DP, m, failed):
     # the failed worker ran nothing; its peer ran every micro-batch of the stage
     for (i, k) in failed:
         assert (i, k) not in g_rr
+
+
+def test_execute_schedule_validation_skips_a_nonfinite_step():
+    """Post-step validation at N = 1 (reading R31): with a fault
+    injected the stage's own validation fails, so the step is skipped — master, m, v and
+    the bf16 weights bit-identical to before it, no rollback needed — and the skipped
+    step does not advance AdamW's bias-correction count: the next iteration equals, bit
+    for bit, the second iteration of a run that never saw the fault."""
+    rt = _rt()
+    cfg, L, m = sd.C1_TINY, 1, 2
+    layers = sd.stage_params(cfg, 0, L, total_layers=2)
+    costs = rt.make_costs(t_f=1, t_b=1, t_w=1, t_comm=0, t_ar=1, t_opt=1)
+    adam = (1e-3, 0.9, 0.95, 1e-8, 0.1)
+
+    def make():
+        _, need = rt.rank_program(1, 1, m, None, costs, 0)
+        st = rt.Stage(cfg, L, n_slots=need)
+        st.load_master(torch.from_numpy(sd.pack_stage(layers)).float().cuda())
+        rt.call("slip_set_validation", st.ctx, 1)
+        comm = rt.Comm(0, 1)
+        comm.setup(1, 1, m, None)
+        io = rt.make_io([host_bf16(sd.stage_input(cfg, 0, j)) for j in range(m)],
+                        [host_bf16(sd.stage_target(cfg, 0, j)) for j in range(m)], torch.zeros(m))
+        return st, comm, io
+
+    def state(st):
+        return [st.master.clone(), st.adam_m.clone(), st.adam_v.clone(), st.w.clone()]
+
+    st, comm, io = make()
+    r1 = rt.execute_schedule(st, comm, 1, 1, m, None, costs, adam=adam, iterations=1, io=io)
+    torch.cuda.synchronize()
+    s1 = state(st)
+    rt.call("slip_inject_fault", st.ctx, 1)
+    r2 = rt.execute_schedule(st, comm, 1, 1, m, None, costs, adam=adam, iterations=1, io=io)
+    torch.cuda.synchronize()
+    assert r1.rollbacks == 0 and r2.rollbacks == 0 and r1.skipped == 0 and r2.skipped == 1
+    assert all(torch.equal(a, b) for a, b in zip(s1, state(st)))
+    rt.execute_schedule(st, comm, 1, 1, m, None, costs, adam=adam, iterations=1, io=io)
+    torch.cuda.synchronize()
+    ref, rcomm, rio = make()
+    for _ in range(2):
+        rt.execute_schedule(ref, rcomm, 1, 1, m, None, costs, adam=adam, iterations=1, io=rio)
+    torch.cuda.synchronize()
+    assert all(torch.equal(a, b) for a, b in zip(state(ref), state(st)))
+    for c in (comm, rcomm):
+        c.close()
+
+
+def test_execute_schedule_gpt_ends_n1_matches_oracle():
+    """The executor with both GPT ends on one stage (reading R33): token ids and labels
+    from host buffers, embedding, layers, final LN + LM head + cross-entropy, B, the merged
+    W (dW_out in the grouped launch, the embedding scatter) over m = 3 micro-batches:
+    summed gradients per tensor vs oracle/ends.py + oracle/layer.py (Gate A), losses to 1e-2."""
+    from oracle import ends as OE
+    from oracle import layer as OL
+    rt = _rt()
+    cfg = sd.ModelCfg(hidden=128, heads=2, ffn=512, seq=64, micro_batch=2, layers=1, vocab=384, ends=3)
+    L, m = 1, 3
+    layers = sd.stage_params(cfg, 0, L, total_layers=2)
+    ends = sd.end_params(cfg, 0)
+    flat = np.concatenate([sd.pack_stage(layers), sd.pack_ends(ends)])
+    costs = rt.make_costs(t_f=1, t_b=1, t_w=1, t_comm=0, t_ar=1, t_opt=1)
+    _, need = rt.rank_program(1, 1, m, None, costs, 0)
+    st = rt.Stage(cfg, L, n_slots=need)
+    st.load_master(torch.from_numpy(flat).float().cuda())
+    comm = rt.Comm(0, 1)
+    comm.setup(1, 1, m, None)
+    toks = [sd.stage_tokens(cfg, 0, j) for j in range(m)]
+    labs = [sd.stage_labels(cfg, 0, j) for j in range(m)]
+    losses = torch.zeros(m)
+    io = rt.make_io([torch.from_numpy(t.copy()) for t in toks], [torch.from_numpy(x.copy()) for x in labs], losses)
+    rt.execute_schedule(st, comm, 1, 1, m, None, costs, adam=(1e-3, 0.9, 0.95, 1e-8, 0.1), iterations=1, io=io)
+    torch.cuda.synchronize()
+    ref_l, ref_e = None, None
+    for j in range(m):
+        x0 = OE.embed_fwd(ends["E"], ends["P"], toks[j], cfg.seq)
+        out, caches = OL.stage_forward(layers, x0, cfg)
+        lref, hc = OE.head_forward(out, ends["gf"], ends["bf"], ends["Wout"], labs[j], cfg.ln_eps)
+        assert abs(losses[j].item() - lref) <= 1e-2 * abs(lref)
+        dout, hb, hws = OE.head_backward_input(hc)
+        dxr, grads = OL.stage_backward_coupled(layers, caches, dout, cfg)
+        dE, dP = OE.embed_bwd(dxr, toks[j], cfg.seq, cfg.vocab)
+        e = {"E": dE, "P": dP, "gf": hb["gf"], "bf": hb["bf"], "Wout": OE.head_backward_weight(hws)["Wout"]}
+        ref_l = grads if ref_l is None else [{n: a[n] + b[n] for n in a} for a, b in zip(ref_l, grads)]
+        ref_e = e if ref_e is None else {n: ref_e[n] + e[n] for n in e}
+    gflat = st.grad.cpu().numpy().astype(np.float64)
+    P = cfg.params_per_layer
+    got = sd.unpack_stage(gflat[:L * P], cfg, L)
+    for l in range(L):
+        for n in sd.PARAM_ORDER:
+            assert relerr(got[l][n], ref_l[l][n]) <= GATE_A, (l, n)
+    ge = sd.unpack_ends(gflat[L * P:], cfg)
+    for n in ("E", "P", "gf", "bf", "Wout"):
+        assert relerr(ge[n], ref_e[n]) <= GATE_A, n
+    comm.close()
+    st.close()
