@@ -18,12 +18,6 @@ slip_status nccl_status(ncclResult_t r, const char* where) {
 }
 }  // namespace slip
 
-#define SLIP_NCCL(expr)                                        \
-  do {                                                         \
-    ncclResult_t _r = (expr);                                  \
-    if (_r != ncclSuccess) return ::slip::nccl_status(_r, #expr); \
-  } while (0)
-
 using namespace slip;
 
 namespace {
@@ -51,6 +45,11 @@ void destroy_setup(slip_comm* c) {
   c->stage_comm = nullptr;
   if (c->live_comm) ncclCommDestroy(c->live_comm);
   c->live_comm = nullptr;
+  if (c->val_comm) ncclCommDestroy(c->val_comm);
+  c->val_comm = nullptr;
+  if (c->val_stream) cudaStreamDestroy(c->val_stream);
+  c->val_stream = nullptr;
+  c->val_rank.clear();
   if (c->ar_stream) cudaStreamDestroy(c->ar_stream);
   c->ar_stream = nullptr;
   c->ready = false;
@@ -123,6 +122,18 @@ slip_status slip_comm_setup(slip_comm* c, const slip_cluster* cl) {
     lc = nullptr;
   }
   c->live_comm = lc;
+  // the same group again for the validation-flag P2P of preceding stages
+  ncclComm_t vc = nullptr;
+  SLIP_NCCL(ncclCommSplit(c->world_comm, c->my_live ? 0 : NCCL_SPLIT_NOCOLOR, c->role, &vc, nullptr));
+  if (vc && n_all <= 1) {
+    ncclCommDestroy(vc);
+    vc = nullptr;
+  }
+  c->val_comm = vc;
+  c->val_rank.assign(static_cast<size_t>(cc.N) * cc.DP, -1);
+  for (int r = 0, q = 0; r < cc.N * cc.DP; ++r)  // split ranks follow the key (role) order
+    if (cc.is_live(r % cc.N, r / cc.N)) c->val_rank[r] = q++;
+  if (vc) SLIP_CUDA(cudaStreamCreateWithFlags(&c->val_stream, cudaStreamNonBlocking));
   // directed pairs used by the assignment (ACT i -> i+1, GRAD i+1 -> i), in a fixed order
   std::set<std::pair<int, int>> pairs;
   for (int k = 0; k < cc.DP; ++k)

@@ -22,6 +22,11 @@ struct slip_comm {
   bool my_live = true;
   ncclComm_t stage_comm = nullptr;  // live peers of my stage (nullptr if singleton / failed)
   ncclComm_t live_comm = nullptr;   // all live ranks (validation flags; nullptr if failed / alone)
+  // validated mode: point-to-point validation flags of preceding stages,
+  // a communicator of its own (the flag all-reduce uses live_comm on another stream)
+  ncclComm_t val_comm = nullptr;
+  cudaStream_t val_stream = nullptr;
+  std::vector<int> val_rank;  // role -> rank in val_comm (-1: failed)
   int stage_size = 1;
   cudaStream_t ar_stream = nullptr;
   // directed pair (src rank, dst rank) -> communicator in which src is rank 0, dst rank 1
@@ -38,6 +43,12 @@ struct slip_comm {
   void* ipc_flag_base = nullptr;
   unsigned epoch = 0;
 };
+
+#define SLIP_NCCL(expr)                                          \
+  do {                                                           \
+    ncclResult_t _r = (expr);                                    \
+    if (_r != ncclSuccess) return ::slip::nccl_status(_r, #expr); \
+  } while (0)
 
 namespace slip {
 // worker (stage i, pipeline k) <-> rank k*N + i

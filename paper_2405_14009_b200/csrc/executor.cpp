@@ -10,6 +10,7 @@
 // slot.dx holds the input gradient B produces and SEND_DX ships.  Events: `freed` (W
 // done) guards slot.x, `sent_y` guards slot.dy, `sent_dx` guards slot.dx.
 #include <algorithm>
+#include <cstdint>
 #include <cstdlib>
 #include <cstring>
 #include <map>
@@ -204,6 +205,36 @@ extern "C" slip_status slip_execute_schedule(slip_ctx* ctx, slip_comm* comm, con
       pend.iter = -1;
       return SLIP_OK;
     };
+    // validated mode: the stages whose OPT the plan finishes before this stage's OPT starts
+    // ("preceding stages") send their validation flag point to point
+    // (designated sender: the lowest live pipeline of the stage); this stage steps only if
+    // its own validation and theirs pass, the later stages' failures are rolled back
+    const bool val_p2p = ctx->validate && comm->val_comm;
+    std::vector<std::vector<std::vector<int>>> pre;  // [iter][stage] -> preceding stages
+    auto sender_of = [&](int j) {
+      for (int k = 0; k < DP; ++k)
+        if (cl.is_live(j, k)) return rank_of(N, j, k);
+      return -1;
+    };
+    if (val_p2p) {
+      pre.assign(H, std::vector<std::vector<int>>(N));
+      std::vector<int64_t> s0(static_cast<size_t>(H) * N, INT64_MAX), e1(static_cast<size_t>(H) * N, INT64_MIN);
+      for (const slip_op& o : plan.ops)
+        if (o.phase == SLIP_OPT && o.iter < H) {
+          int64_t& a0 = s0[static_cast<size_t>(o.iter) * N + o.stage];
+          int64_t& a1 = e1[static_cast<size_t>(o.iter) * N + o.stage];
+          a0 = std::min(a0, o.start);
+          a1 = std::max(a1, o.end);
+        }
+      for (int t = 0; t < H; ++t)
+        for (int i = 0; i < N; ++i)
+          for (int j = 0; j < N; ++j)
+            if (j != i && e1[static_cast<size_t>(t) * N + j] != INT64_MIN &&
+                s0[static_cast<size_t>(t) * N + i] != INT64_MAX &&
+                e1[static_cast<size_t>(t) * N + j] <= s0[static_cast<size_t>(t) * N + i])
+              pre[t][i].push_back(j);
+    }
+    int send_pos = kValSend, recv_pos = kValRecv;
     const std::vector<slip_action>& prog = progs[me];
     size_t skip_to = 0;  // W actions already run by a merged W launch
     for (size_t ai = 0; ai < prog.size(); ++ai) {
@@ -420,8 +451,59 @@ extern "C" slip_status slip_execute_schedule(slip_ctx* ctx, slip_comm* comm, con
             // live-rank MAX of the flag on the all-reduce stream
             int32_t* own = ctx->ws.vflags + (a.iter & 1);
             int32_t* glob = ctx->ws.vflags + 2 + (a.iter & 1);
-            SLIP_TRY(validated_step(ctx, adam, ctx->opt_step, grad_scale, own, ctx->fault_next_opt, cs));
+            int n_pre = 0;
+            int32_t* pre_buf = nullptr;
+            if (val_p2p && !pre[a.iter][me_i].empty()) {
+              const std::vector<int>& P = pre[a.iter][me_i];
+              n_pre = static_cast<int>(P.size());
+              if (recv_pos + n_pre > kVflags) {  // ring wrap: the earlier readers (cs) first
+                recv_pos = kValRecv;
+                SLIP_CUDA(chain(cs, comm->val_stream));
+              }
+              pre_buf = ctx->ws.vflags + recv_pos;
+              recv_pos += n_pre;
+              SLIP_NCCL(ncclGroupStart());
+              for (int q = 0; q < n_pre; ++q) {
+                ncclResult_t r = ncclRecv(pre_buf + q, 1, ncclInt32, comm->val_rank[sender_of(P[q])], comm->val_comm,
+                                          comm->val_stream);
+                if (r != ncclSuccess) {
+                  ncclGroupEnd();
+                  return nccl_status(r, "ncclRecv(validation flag)");
+                }
+              }
+              SLIP_NCCL(ncclGroupEnd());
+              SLIP_CUDA(chain(comm->val_stream, cs));
+            }
+            SLIP_TRY(validated_step(ctx, adam, ctx->opt_step, grad_scale, own, ctx->fault_next_opt, cs, pre_buf,
+                                    n_pre));
             ctx->fault_next_opt = 0;
+            if (val_p2p && sender_of(me_i) == me) {  // my stage's flag to the stages it precedes
+              std::vector<int> dst;
+              for (int i = 0; i < N; ++i) {
+                const std::vector<int>& P = pre[a.iter][i];
+                if (i != me_i && std::find(P.begin(), P.end(), me_i) != P.end())
+                  for (int k = 0; k < DP; ++k)
+                    if (cl.is_live(i, k)) dst.push_back(rank_of(N, i, k));
+              }
+              if (!dst.empty()) {
+                if (send_pos + 1 > kValRecv) {  // ring wrap: the earlier sends first
+                  send_pos = kValSend;
+                  SLIP_CUDA(chain(comm->val_stream, cs));
+                }
+                int32_t* sb = ctx->ws.vflags + send_pos++;
+                SLIP_CUDA(cudaMemcpyAsync(sb, own, sizeof(int32_t), cudaMemcpyDeviceToDevice, cs));
+                SLIP_CUDA(chain(cs, comm->val_stream));
+                SLIP_NCCL(ncclGroupStart());
+                for (int r : dst) {
+                  ncclResult_t e = ncclSend(sb, 1, ncclInt32, comm->val_rank[r], comm->val_comm, comm->val_stream);
+                  if (e != ncclSuccess) {
+                    ncclGroupEnd();
+                    return nccl_status(e, "ncclSend(validation flag)");
+                  }
+                }
+                SLIP_NCCL(ncclGroupEnd());
+              }
+            }
             cudaEvent_t fe;
             if (comm->live_comm) {
               SLIP_CUDA(chain(cs, comm->ar_stream));
@@ -456,6 +538,7 @@ extern "C" slip_status slip_execute_schedule(slip_ctx* ctx, slip_comm* comm, con
     // join every side stream back into the compute stream
     for (auto& kv : comm->pair_stream) SLIP_CUDA(chain(kv.second, cs));
     SLIP_CUDA(chain(comm->ar_stream, cs));
+    if (comm->val_stream) SLIP_CUDA(chain(comm->val_stream, cs));
     if (hs) SLIP_CUDA(chain(hs, cs));
     if (timed) {
       SLIP_CUDA(cudaEventRecord(t1, cs));

@@ -1080,6 +1080,18 @@ __global__ void count_flag_kernel(const int32_t* __restrict__ flag, int32_t* __r
   if (threadIdx.x == 0 && *flag) *count += 1;
 }
 
+__global__ void or_flags_kernel(int32_t* __restrict__ own, const int32_t* __restrict__ flags, int n) {
+  ptx::grid_dep_wait();
+  if (threadIdx.x != 0) return;
+  int32_t v = *own;
+  for (int i = 0; i < n; ++i) v |= flags[i] != 0;
+  *own = v;
+}
+
+cudaError_t or_flags(int32_t* own, const int32_t* flags, int n, cudaStream_t s) {
+  return launch_pdl(or_flags_kernel, dim3(1), dim3(32), 0, s, 1, own, flags, n);
+}
+
 cudaError_t count_flag(const int32_t* flag, int32_t* count, cudaStream_t s) {
   return launch_pdl(count_flag_kernel, dim3(1), dim3(32), 0, s, 1, flag, count);
 }

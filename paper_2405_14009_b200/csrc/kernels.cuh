@@ -113,6 +113,8 @@ cudaError_t synth_tokens(int32_t* out, int64_t n, int32_t n_classes, uint64_t se
 // *bad |= any element of g not finite (and *nonfinite, if not NULL)
 cudaError_t grad_check(const float* g, int64_t n, int32_t* bad, int32_t* nonfinite, cudaStream_t s);
 
+// *own |= any(flags[0 .. n) != 0) (one thread; validation flags of preceding stages)
+cudaError_t or_flags(int32_t* own, const int32_t* flags, int n, cudaStream_t s);
 // *count += (*flag != 0) (one thread; validated mode's count of skipped steps)
 cudaError_t count_flag(const int32_t* flag, int32_t* count, cudaStream_t s);
 

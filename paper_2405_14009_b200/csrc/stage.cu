@@ -185,7 +185,7 @@ void carve_ws(Carver& cv, const Dims& d, Workspace* out) {
   w.loss_part = cv.take<float>(256);
   w.losses = cv.take<float>(1024);
   w.nonfinite = cv.take<int32_t>(64);
-  w.vflags = cv.take<int32_t>(64);
+  w.vflags = cv.take<int32_t>(kVflags);
   w.sk_flags = cv.take<unsigned>(static_cast<size_t>(num_sms()));
   w.sk_ws = cv.take<float>(gemm_sk_bytes() / sizeof(float));
   if (out) *out = w;
@@ -809,12 +809,14 @@ slip_status slip_synth_normal(void* out_bf16, int64_t n, uint64_t seed, uint64_t
 namespace slip {
 // Validated OPT (executor): own = fault injected ? 1 : any non-finite gradient; step only if !own.
 slip_status validated_step(slip_ctx* c, const slip_adam* a, int64_t step, float grad_scale, int32_t* own, int fault,
-                           cudaStream_t s) {
+                           cudaStream_t s, const int32_t* pre_flags, int n_pre) {
   const double bc1 = 1.0 - std::pow(static_cast<double>(a->beta1), static_cast<double>(step));
   const double bc2 = 1.0 - std::pow(static_cast<double>(a->beta2), static_cast<double>(step));
   SLIP_CUDA(cudaMemsetAsync(own, 0, sizeof(int32_t), s));
   if (fault) SLIP_CUDA(cudaMemsetAsync(own, 1, 1, s));
   SLIP_TRY(kcheck(c, grad_check(c->grad, c->n_params, own, c->ws.nonfinite, s), "grad_check"));
+  // "based on its individual validation results and those of preceding stages"
+  if (n_pre > 0) SLIP_TRY(kcheck(c, or_flags(own, pre_flags, n_pre, s), "or_flags"));
   SLIP_TRY(kcheck(c,
                   adamw(c->master, c->adam_m, c->adam_v, c->grad, c->w, c->n_params, c->po.per_layer, c->dm.h,
                         c->dm.f, a->lr, a->beta1, a->beta2, a->eps, a->weight_decay, static_cast<float>(bc1),

@@ -12,6 +12,9 @@
 
 namespace slip {
 
+// validated mode's flag words in the workspace (Workspace::vflags)
+constexpr int kValSend = 64, kValRecv = 256, kVflags = 512;
+
 using bf16 = __nv_bfloat16;
 
 // Offsets (elements) of one layer's tensors inside the flat parameter vector
@@ -58,7 +61,8 @@ struct Workspace {
   float* loss_part;  // [256] MSE partials
   float* losses;     // [1024] per-micro-batch losses (executor)
   int32_t* nonfinite;  // [1] post-step validation flag (executor)
-  int32_t* vflags;     // [8] validated mode: own_bad[2], global_bad[2] (per iteration parity), rollbacks, skips
+  int32_t* vflags;     // [kVflags] validated mode: own_bad[2], global_bad[2] (per iteration parity), rollbacks,
+                       // skips; [kValSend, kValRecv): ring of sent flags; [kValRecv, kVflags): received flags
   float* red;          // deferred column-reduction partials of a B call (RedBatch arena)
   size_t red_cap;      // floats
   float* sk_ws;        // stream-K fp32 partials of the F / B linears (gemm_sk_bytes)
@@ -120,8 +124,11 @@ size_t workspace_bytes(const Dims& d);
 // micro-batches' products in TMEM (K = n*T) and is written (or added) once.  Releases
 // the slots.
 slip_status weight_multi(slip_ctx* c, const int* slots, int n, int accumulate, cudaStream_t s);
+// Local validation and the step if valid: own = non-finite gradient | injected fault | any
+// of the n_pre preceding stages' flags (device int32 each); AdamW skips when own is set,
+// and vflags[5] counts the skip.
 slip_status validated_step(slip_ctx* c, const slip_adam* a, int64_t step, float grad_scale, int32_t* own, int fault,
-                           cudaStream_t s);
+                           cudaStream_t s, const int32_t* pre_flags = nullptr, int n_pre = 0);
 // slip_optimizer_step with the DP peer's gradient added in (peer_grad peer-mapped, or
 // NULL): the DP = 2 all-reduce fused into AdamW (slip_comm_fuse_ar_adam).
 slip_status optimizer_step_peer(slip_ctx* c, const slip_adam* a, int64_t step, float grad_scale, int32_t* d_nonfinite,

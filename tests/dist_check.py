@@ -154,14 +154,28 @@ def migrate_scenario(a, cfg, L, comm, costs, rank, world, holder):
     return flag.item() == 1.0
 
 
+def preceding_stages(PP, DP, m, live, costs):
+    """{stage i: stages whose planned OPT (iteration 0) ends before stage i's starts} — the
+    "preceding stages" whose validation flags stage i waits for."""
+    plan = rt.plan_schedule(PP, DP, m, live, costs, True, True, horizon=1)
+    s0, e1 = {}, {}
+    for (i, _mb, _o, ph, _ex, it, st, en) in plan.ops:
+        if ph == 4 and it == 0:
+            s0[i] = min(s0.get(i, st), st)
+            e1[i] = max(e1.get(i, en), en)
+    return {i: {j for j in range(PP) if j != i and j in e1 and i in s0 and e1[j] <= s0[i]} for i in range(PP)}
+
+
 def validate_scenario(a, cfg, L, comm, costs, rank, world, holder):
-    """Post-step validation with cross-stage rollback (§4.3,
-    reading R31).  Iteration 1 trains normally.  In iteration 2 stage 0 reports
-    non-finite gradients (slip_inject_fault): it must skip its step (weights bit-equal
-    to after iteration 1) while the other stages, which stepped on their own
-    validation, must roll the step back (weights equal to after iteration 1 within the
-    fp32 reversal error) and report one rollback each.  Iteration 3 then trains
-    normally again and all live peers of a stage stay bit-identical."""
+    """Post-step validation (§4.3, reading R31).  Iteration 1
+    trains normally.  In iteration 2 one stage reports non-finite gradients
+    (slip_inject_fault) — stage 0 (the last to step), then, in a second run, the last
+    stage (the first to step).  The faulty stage skips its step (weights bit-equal to
+    after iteration 1, one skip); a stage that the plan steps after it (it is a
+    "preceding stage") received its flag point to point and skips too (bit-equal, one
+    skip, no rollback); every other stage stepped on its own validation and rolls the
+    step back (weights equal to after iteration 1 within the fp32 reversal error, one
+    rollback).  Iteration 3 trains normally and all live peers stay bit-identical."""
     DP, PP, m = a.dp, a.pp, a.m
     g = torch.Generator().manual_seed(5)
     xs = [torch.randn(cfg.tokens, cfg.hidden, generator=g).to(torch.bfloat16).pin_memory() for _ in range(DP * m)]
@@ -169,50 +183,60 @@ def validate_scenario(a, cfg, L, comm, costs, rank, world, holder):
     adam = (1e-3, 0.9, 0.95, 1e-8, 0.1)
     full = [[1] * DP for _ in range(PP)]
     me_i = rank % PP
-    st = holder["stage"] = rt.Stage(cfg, L, n_slots=2 * m * DP)
-    rt.init_master_(st.master, cfg, L, cfg.layers, seed=100 + me_i)
-    rt.call("slip_weights_from_master", st.ctx, rt._stream())
-    rt.call("slip_set_validation", st.ctx, 1)
-    comm.setup(PP, DP, m, full)
+    pre = preceding_stages(PP, DP, m, full, costs)
+    all_ok = True
+    for bad in (0, PP - 1):
+        if "stage" in holder:
+            holder["stage"].close()
+        st = holder["stage"] = rt.Stage(cfg, L, n_slots=2 * m * DP)
+        rt.init_master_(st.master, cfg, L, cfg.layers, seed=100 + me_i)
+        rt.call("slip_weights_from_master", st.ctx, rt._stream())
+        rt.call("slip_set_validation", st.ctx, 1)
+        comm.setup(PP, DP, m, full)
 
-    def iterate():
-        losses = torch.zeros(DP * m, dtype=torch.float32).pin_memory()
-        rep = rt.execute_schedule(st, comm, PP, DP, m, full, costs, True, True, adam=adam, iterations=1,
-                                  io=rt.make_io(xs, rs, losses))
-        torch.cuda.synchronize()
-        return rep
+        def iterate():
+            losses = torch.zeros(DP * m, dtype=torch.float32).pin_memory()
+            rep = rt.execute_schedule(st, comm, PP, DP, m, full, costs, True, True, adam=adam, iterations=1,
+                                      io=rt.make_io(xs, rs, losses))
+            torch.cuda.synchronize()
+            return rep
 
-    r1 = iterate()
-    p1, m1, v1, w1 = st.master.clone(), st.adam_m.clone(), st.adam_v.clone(), st.w.clone()
-    if me_i == 0:
-        rt.call("slip_inject_fault", st.ctx, 1)
-    r2 = iterate()
-    p2, w2 = st.master.clone(), st.w.clone()
-    res = {"rank": rank, "stage": me_i, "rollbacks": [r1.rollbacks, r2.rollbacks], "nonfinite": r2.nonfinite}
-    ok = r1.rollbacks == 0
-    if me_i == 0:
-        ok &= bool(torch.equal(p2, p1)) and bool(torch.equal(w2, w1)) and r2.rollbacks == 0
-        res["skipped_bit_equal"] = bool(torch.equal(p2, p1))
-    else:
-        e = ((p2 - p1).abs().max() / p1.abs().max()).item()
-        em = ((st.adam_m - m1).abs().max() / m1.abs().max()).item()
-        res["rollback_relerr_master"] = e
-        res["rollback_relerr_m"] = em
-        res["bf16_mismatch_frac"] = (w2 != w1).float().mean().item()
-        ok &= e <= 1e-6 and em <= 1e-4 and r2.rollbacks == 1
-    r3 = iterate()
-    res["rollbacks3"] = r3.rollbacks
-    ok &= r3.rollbacks == 0
-    eq = peers_equal(st.master, True, me_i, world) + peers_equal(st.w, True, me_i, world)
-    res["peer_master_w_bit_identical"] = eq
-    ok &= all(eq)
-    flag = torch.tensor([1.0 if ok else 0.0], device="cuda")
-    dist.all_reduce(flag, op=dist.ReduceOp.MIN)
-    outs = [None] * world
-    dist.all_gather_object(outs, res)
-    if rank == 0:
-        print(json.dumps({"scenario": "validate", "ok": flag.item() == 1.0, "ranks": outs}), flush=True)
-    return flag.item() == 1.0
+        r1 = iterate()
+        p1, m1, v1, w1 = st.master.clone(), st.adam_m.clone(), st.adam_v.clone(), st.w.clone()
+        if me_i == bad:
+            rt.call("slip_inject_fault", st.ctx, 1)
+        r2 = iterate()
+        p2, w2 = st.master.clone(), st.w.clone()
+        skips = me_i == bad or bad in pre[me_i]
+        res = {"rank": rank, "stage": me_i, "faulty_stage": bad, "preceding": sorted(pre[me_i]),
+               "rollbacks": [r1.rollbacks, r2.rollbacks], "skipped": [r1.skipped, r2.skipped],
+               "nonfinite": r2.nonfinite}
+        ok = r1.rollbacks == 0 and r1.skipped == 0
+        if skips:
+            ok &= bool(torch.equal(p2, p1)) and bool(torch.equal(w2, w1)) and r2.rollbacks == 0 and r2.skipped == 1
+            res["skipped_bit_equal"] = bool(torch.equal(p2, p1))
+        else:
+            e = ((p2 - p1).abs().max() / p1.abs().max()).item()
+            em = ((st.adam_m - m1).abs().max() / m1.abs().max()).item()
+            res["rollback_relerr_master"] = e
+            res["rollback_relerr_m"] = em
+            res["bf16_mismatch_frac"] = (w2 != w1).float().mean().item()
+            ok &= e <= 1e-6 and em <= 1e-4 and r2.rollbacks == 1 and r2.skipped == 0
+        r3 = iterate()
+        res["rollbacks3"] = r3.rollbacks
+        ok &= r3.rollbacks == 0 and r3.skipped == 0
+        eq = peers_equal(st.master, True, me_i, world) + peers_equal(st.w, True, me_i, world)
+        res["peer_master_w_bit_identical"] = eq
+        ok &= all(eq)
+        flag = torch.tensor([1.0 if ok else 0.0], device="cuda")
+        dist.all_reduce(flag, op=dist.ReduceOp.MIN)
+        outs = [None] * world
+        dist.all_gather_object(outs, res)
+        if rank == 0:
+            print(json.dumps({"scenario": "validate", "faulty_stage": bad, "ok": flag.item() == 1.0, "ranks": outs}),
+                  flush=True)
+        all_ok = all_ok and flag.item() == 1.0
+    return all_ok
 
 
 def fused_scenario(a, cfg, L, comm, costs, rank, world, holder):

