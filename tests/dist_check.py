@@ -209,6 +209,7 @@ def validate_scenario(a, cfg, L, comm, costs, rank, world, holder):
         p2, w2 = st.master.clone(), st.w.clone()
         skips = me_i == bad or bad in pre[me_i]
         res = {"rank": rank, "stage": me_i, "faulty_stage": bad, "preceding": sorted(pre[me_i]),
+               "via_preceding": me_i != bad and bad in pre[me_i],
                "rollbacks": [r1.rollbacks, r2.rollbacks], "skipped": [r1.skipped, r2.skipped],
                "nonfinite": r2.nonfinite}
         ok = r1.rollbacks == 0 and r1.skipped == 0

@@ -60,6 +60,7 @@ def test_dp1_pp2_validation_preceding_stage():
     stage through the point-to-point validation flag (it skips instead of rolling back)."""
     out = _run(2, 1, 2, "--validate")
     assert '"scenario": "validate"' in out and '"ok": false' not in out
+    assert '"via_preceding": true' in out  # the point-to-point flag path was exercised
 
 
 @pytest.mark.skipif(torch.cuda.device_count() < 2, reason="needs 2 GPUs")
