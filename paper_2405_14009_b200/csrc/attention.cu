@@ -63,6 +63,8 @@ struct KArgs {
   int64_t ldh;              // row stride of O / dO
   float* dsum_w;            // DQ: D written here for the dK / dV kernel
   float* colsum;            // backward: per 32-row-group column sums of the stored output
+  const __nv_bfloat16* q;   // DQ: Q block of the QKV activation (row stride ldq)
+  int64_t ldq;
 };
 
 // Descriptor of a 128B-swizzled operand at base; the UMMA_K steps below are constant
@@ -396,6 +398,7 @@ __global__ void __launch_bounds__(FWD_NT, 1)
 // columns of a half tile).  A group's bf16 pairs go to the first 16 of its own 32
 // columns, so no warp overwrites columns another warp has not read yet.
 constexpr int HT = 64;          // rows of a half tile
+constexpr int kDqStages = 4;    // K / V half-tile ring of the dQ kernel
 constexpr int HATOM = 8192;     // 64 rows x 128 B
 constexpr int BWD_NT = 32 * 12;
 
@@ -413,6 +416,10 @@ __device__ __forceinline__ uint32_t acol(int kk) { return 32 * (kk >> 1) + (kk &
 // One CTA per (q-tile i, z), longest first.  S_h = Q K_h^T, dP_h = dO V_h^T over the 64-key
 // half tiles h, dS = P (dP - D) / sqrt(d) with P = exp2(S log2e/sqrt(d) - lse), dQ += dS K_h.
 // D of the tile's rows is computed here first (and stored for the dK / dV kernel).
+// Q and dO — the A operands of every S / dP MMA of the CTA — live in TMEM (written once by
+// the softmax warps from their rows, bf16 pairs), so those MMAs read only the 64-key K / V
+// half tile from shared memory: with both operands in shared memory the N = 64 MMAs alone
+// use the whole shared-memory bandwidth and the K / V TMA writes queue behind them.
 template <int D>
 __global__ void __launch_bounds__(BWD_NT, 1)
     attn_dq_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK64,
@@ -421,16 +428,15 @@ __global__ void __launch_bounds__(BWD_NT, 1)
   SCHED(0, 0);
   using C = AC<D>;
   using H = HC<D>;
-  constexpr int NST = 3, NSB = 2;  // K/V ring stages, S|dP buffers in TMEM (dQ after them)
+  constexpr int NST = kDqStages, NSB = 2;  // K/V ring stages, S|dP buffers in TMEM (dQ after them)
   constexpr int STG = 2 * H::HB;  // K_h | V_h
+  constexpr uint32_t QCOL = 384, DOCOL = 448;  // TMEM columns of Q and dO (bf16 pairs, D / 2 each)
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint8_t* Qs = sm;
-  uint8_t* dOs = Qs + C::TB;
-  uint8_t* ring = dOs + C::TB;  // [NST][STG]
+  uint8_t* ring = sm;  // [NST][STG]
   float* red = reinterpret_cast<float*>(ring + NST * STG);  // [2][128]
   uint64_t* bar = reinterpret_cast<uint64_t*>(red + 2 * TILE);
-  uint64_t* q_full = bar;
+  uint64_t* q_full = bar;              // Q, dO written to TMEM (8 warps)
   uint64_t* kv_full = bar + 1;         // [NST]
   uint64_t* kv_empty = kv_full + NST;  // [NST]
   uint64_t* s_full = kv_empty + NST;   // [NSB]
@@ -448,7 +454,7 @@ __global__ void __launch_bounds__(BWD_NT, 1)
   const int nh = (kend + HT - 1) / HT;
 
   if (threadIdx.x == 0) {
-    ptx::mbar_init(q_full, 1);
+    ptx::mbar_init(q_full, 8);
     for (int t = 0; t < NST; ++t) {
       ptx::mbar_init(&kv_full[t], 1);
       ptx::mbar_init(&kv_empty[t], 1);
@@ -470,11 +476,6 @@ __global__ void __launch_bounds__(BWD_NT, 1)
 
   if (warp == 0) {
     if (lane == 0) {  // ------------------------------------------------ TMA producer
-      ptx::mbar_arrive_expect_tx(q_full, 2 * C::TB);
-      for (int t = 0; t < C::NA; ++t) {
-        ptx::tma_load_4d(&tmQ, Qs + t * ATOM, q_full, t * 64, q0, hn, bi);
-        ptx::tma_load_4d(&tmdO, dOs + t * ATOM, q_full, t * 64, q0, hn, bi);
-      }
       for (int h = 0; h < nh; ++h) {
         const int st = h % NST;
         ptx::mbar_wait(&kv_empty[st], ((h / NST) & 1) ^ 1);
@@ -489,19 +490,20 @@ __global__ void __launch_bounds__(BWD_NT, 1)
   } else if (warp == 1) {
     {  // ------------------------------------------------ MMA issuer (warp-wide, elected lane issues)
       ptx::mbar_wait(q_full, 0);
-      const uint32_t qb = ptx::smem_u32(Qs), ob = ptx::smem_u32(dOs), rb = ptx::smem_u32(ring);
-      auto mma_sd = [&](int h) {  // S_b = Q K_h^T, dP_b = dO V_h^T  (b = h % NSB)
+      ptx::tc_fence_after();
+      const uint32_t rb = ptx::smem_u32(ring);
+      auto mma_sd = [&](int h) {  // S_b = Q K_h^T, dP_b = dO V_h^T  (b = h % NSB), A from TMEM
         const int st = h % NST;
         ptx::mbar_wait(&kv_full[st], (h / NST) & 1);
         ptx::tc_fence_after();
         const uint32_t kb = rb + st * STG, vb = kb + H::HB, tS = tmem + (h % NSB) * 128;
-        const uint64_t dqq = kdesc(qb), dkh = kdesc(kb), doo = kdesc(ob), dvh = kdesc(vb);
+        const uint64_t dkh = kdesc(kb), dvh = kdesc(vb);
 #pragma unroll
         for (int kk = 0; kk < C::KS; ++kk)
-          ptx::tc_mma_f16_w(tS, dqq + dk_off(kk), dkh + hk_off(kk), H::IDESC_S, kk > 0);
+          ptx::tc_mma_f16_ts_w(tS, tmem + QCOL + kk * 8, dkh + hk_off(kk), H::IDESC_S, kk > 0);
 #pragma unroll
         for (int kk = 0; kk < C::KS; ++kk)
-          ptx::tc_mma_f16_w(tS + 64, doo + dk_off(kk), dvh + hk_off(kk), H::IDESC_S, kk > 0);
+          ptx::tc_mma_f16_ts_w(tS + 64, tmem + DOCOL + kk * 8, dvh + hk_off(kk), H::IDESC_S, kk > 0);
         ptx::tc_commit_w(&s_full[h % NSB]);
       };
       for (int h = 0; h < NSB && h < nh; ++h) mma_sd(h);
@@ -526,25 +528,45 @@ __global__ void __launch_bounds__(BWD_NT, 1)
     const int q = q0 + r;
     const size_t zs = static_cast<size_t>(z) * a.s;
     const uint32_t lane_off = static_cast<uint32_t>(lq * 32) << 16;
-    // D = rowsum(dO * O) over this head's d columns: half of them per column group
+    // Q and dO rows into TMEM (the S / dP MMAs' A operands: row = lane, bf16 pairs along d;
+    // column group g writes the UMMA_K steps kk = g, g + 2, ...; rows past s are zero) and
+    // D = rowsum(dO * O) over this head's d columns from the same loads
     float dpart = 0.f;
-    if (q < a.s) {
-      const __nv_bfloat16* orow = a.o + (static_cast<int64_t>(bi) * a.s + q) * a.ldh + static_cast<int64_t>(hn) * a.d;
-      const __nv_bfloat16* grow = a.dO + (static_cast<int64_t>(bi) * a.s + q) * a.ldh + static_cast<int64_t>(hn) * a.d;
-      for (int c = g * 8; c < D; c += 16) {
-        float ov[8], gv[8];
-        const uint4 ou = *reinterpret_cast<const uint4*>(orow + c);
-        const uint4 gu = *reinterpret_cast<const uint4*>(grow + c);
-        const __nv_bfloat162* o2 = reinterpret_cast<const __nv_bfloat162*>(&ou);
-        const __nv_bfloat162* g2 = reinterpret_cast<const __nv_bfloat162*>(&gu);
+    {
+      const bool rok = q < a.s;
+      const int64_t ro = (static_cast<int64_t>(bi) * a.s + (rok ? q : 0));
+      const __nv_bfloat16* qrow = a.q + ro * a.ldq + static_cast<int64_t>(hn) * a.d;
+      const __nv_bfloat16* orow = a.o + ro * a.ldh + static_cast<int64_t>(hn) * a.d;
+      const __nv_bfloat16* grow = a.dO + ro * a.ldh + static_cast<int64_t>(hn) * a.d;
+      for (int kk = g; kk < C::KS; kk += 2) {
+        uint4 qu[2], gu[2], ou[2];
 #pragma unroll
-        for (int e = 0; e < 4; ++e) {
-          const float2 x = __bfloat1622float2(o2[e]), y = __bfloat1622float2(g2[e]);
-          ov[2 * e] = x.x, ov[2 * e + 1] = x.y, gv[2 * e] = y.x, gv[2 * e + 1] = y.y;
+        for (int u = 0; u < 2; ++u) {
+          const int c = kk * 16 + u * 8;
+          qu[u] = rok ? *reinterpret_cast<const uint4*>(qrow + c) : make_uint4(0, 0, 0, 0);
+          gu[u] = rok ? *reinterpret_cast<const uint4*>(grow + c) : make_uint4(0, 0, 0, 0);
+          ou[u] = rok ? *reinterpret_cast<const uint4*>(orow + c) : make_uint4(0, 0, 0, 0);
         }
+        const uint32_t qw[8] = {qu[0].x, qu[0].y, qu[0].z, qu[0].w, qu[1].x, qu[1].y, qu[1].z, qu[1].w};
+        const uint32_t gw[8] = {gu[0].x, gu[0].y, gu[0].z, gu[0].w, gu[1].x, gu[1].y, gu[1].z, gu[1].w};
+        ptx::tmem_st_32x32b_x8(tmem + lane_off + QCOL + kk * 8, qw);
+        ptx::tmem_st_32x32b_x8(tmem + lane_off + DOCOL + kk * 8, gw);
 #pragma unroll
-        for (int e = 0; e < 8; ++e) dpart = fmaf(ov[e], gv[e], dpart);
+        for (int u = 0; u < 2; ++u) {
+          const __nv_bfloat162* o2 = reinterpret_cast<const __nv_bfloat162*>(&ou[u]);
+          const __nv_bfloat162* g2 = reinterpret_cast<const __nv_bfloat162*>(&gu[u]);
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            const float2 x = __bfloat1622float2(o2[e]), y = __bfloat1622float2(g2[e]);
+            dpart = fmaf(x.x, y.x, dpart);
+            dpart = fmaf(x.y, y.y, dpart);
+          }
+        }
       }
+      ptx::tmem_st_wait();
+      ptx::tc_fence_before();
+      __syncwarp();
+      if (lane == 0) ptx::mbar_arrive(q_full);
     }
     red[g * TILE + r] = dpart;
     ptx::named_bar_sync(1 + lq, 64);
@@ -820,7 +842,7 @@ constexpr int fwd_smem() {
 }
 template <int D>
 constexpr int dq_smem() {
-  return 2 * AC<D>::TB + 3 * 2 * HC<D>::HB + 2 * TILE * 4 + 1024 + 1024;
+  return kDqStages * 2 * HC<D>::HB + 2 * TILE * 4 + 1024 + 1024;
 }
 template <int D>
 constexpr int dkdv_smem() {
@@ -896,6 +918,8 @@ cudaError_t backward_d(const AttnArgs& a, cudaStream_t st) {
   k.ldo = a.qkv_ld;
   k.d = a.d;
   k.colsum = a.colsum;
+  k.q = a.qkv;
+  k.ldq = a.qkv_ld;
   constexpr int s2 = dq_smem<D>(), s3 = dkdv_smem<D>();
   static_assert(dq_smem<D>() <= 232448 && dkdv_smem<D>() <= 232448, "attention smem budget");
   static bool once = false;
