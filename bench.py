@@ -67,6 +67,8 @@ def parse():
     ap.add_argument("--gpt-ends", action="store_true",
                     help="GPT model ends: token + position embedding on the first stage, final LN + LM head "
                          "(vocab 50304) + cross-entropy on the last stage (SURVEY §8(f) NEXT-3)")
+    ap.add_argument("--no-dual-stream", action="store_true",
+                    help="forward actions on the compute stream (default: their own stream after profiling)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--model", default="1.3b", choices=sorted(MODELS), help="GPT shape (default: BASELINE configs[1])")
@@ -403,6 +405,13 @@ def main():
                 "cost_table_10us": {"%d,%d" % ix: v for ix, v in tab.items()},
                 "normalized_failed": [(i, k) for i in range(PP) for k in range(DP) if not live[i][k]]}
         failed = norm["normalized_failed"]
+    # the profiled costs above came from single-stream execution; with one pipeline stage
+    # (PP = 1) the timed steps run the forward actions on their own stream
+    # (slip_set_dual_stream: same plan, same results; measured +1-2.8 % at N = 1).  With
+    # PP > 1 the overlapping forward competes with the backward chain across the stages,
+    # which is the critical path at small m (DP2xPP2 m = 2: 321k -> 301k), so it stays off.
+    dual = not args.no_dual_stream and PP == 1
+    rt.call("slip_set_dual_stream", stage.ctx, int(dual))
     # warm-up steps with the profiled plan
     execute(args.warmup)
     barrier()
@@ -573,7 +582,7 @@ def main():
                                    len(failed)),
                    "model": "gpt-%s-shape" % MODEL, "global_batch": DP * m * MB, "seq_len": SEQ,
                    "parallelism": "dp%dxpp%d" % (DP, PP), "failed_workers": failed, "sm_reserve": sm_reserve,
-                   "p2p_ctas": args.p2p_ctas, "fused_ar_adam": fused_ar,
+                   "p2p_ctas": args.p2p_ctas, "fused_ar_adam": fused_ar, "dual_stream": dual,
                    "l2": "inputs larger than L2 (2.4 GB bf16 weights + GBs of stash per step)"},
         "clocks": clk,
         "e2e": e2e,
@@ -586,6 +595,7 @@ def main():
                      "microbatch_w_per_launch": w_ops / w_launches if w_launches else None,
                      "launches": w_launches,
                      "avg_launch_ms": (w_ms_total / w_launches) if w_launches else None},
+        # (with the dual stream the F and B phase times overlap each other)
         "phases_ms_per_step_busiest_rank": {n: phase_ms[i] / args.steps
                                             for i, n in enumerate(("F", "B", "W", "BC", "OPT"))},
         "predicted_period_units": predicted_period,

@@ -494,6 +494,16 @@ slip_status slip_inject_fault(slip_ctx* ctx, int32_t kind);
  * 0), bf16 weights refreshed. */
 slip_status slip_optimizer_rollback(slip_ctx* ctx, const slip_adam* a, int64_t step, float grad_scale, slip_stream s);
 
+/* Execution option of slip_execute_schedule (default off; SLIP_DUAL_STREAM=1 in the
+ * environment turns the default on): the forward actions (LOAD_X / RECV_X, F, and the
+ * SEND_Y that follows) run on a second compute stream of the context, ordered by events
+ * after the slot's previous W and the latest OPT; B / LOSS of a slot wait for its F.  The
+ * plan and every result are unchanged; the forward of a later micro-batch fills the SMs
+ * the backward kernels of an earlier one leave idle.  Ignored in validated mode (a
+ * rollback rewrites weights the overlapping forward may read).  Phase times of
+ * slip_report then overlap (profile planner costs with it off). */
+slip_status slip_set_dual_stream(slip_ctx* ctx, int32_t enable);
+
 /* ------------------------------------------------------------------ tracing
  * Per-action timeline of the timed iterations of the last slip_execute_schedule
  * on this ctx (off by default; costs two CUDA events per action).  Each record

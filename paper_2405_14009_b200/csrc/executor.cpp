@@ -50,6 +50,7 @@ struct SlotEv {
   cudaEvent_t freed = nullptr;
   cudaEvent_t sent_y = nullptr;
   cudaEvent_t sent_dx = nullptr;
+  cudaEvent_t f_done = nullptr;  // dual stream: the slot's forward finished
 };
 
 // map action kinds onto the report's phase slots
@@ -92,6 +93,14 @@ extern "C" slip_status slip_execute_schedule(slip_ctx* ctx, slip_comm* comm, con
     const char* e = std::getenv("SLIP_NO_MERGE_W");
     return !(e && e[0] == '1');
   }();
+  // forward actions on a second compute stream (slip_set_dual_stream; SLIP_DUAL_STREAM=1
+  // sets the default), so the F of a later micro-batch fills the SMs the B / W kernels of
+  // an earlier one leave idle (one-wave GEMMs, wave tails, small kernels)
+  static const bool dual_env_ = [] {
+    const char* e = std::getenv("SLIP_DUAL_STREAM");
+    return e && e[0] == '1';
+  }();
+  const bool dual_ = ctx->dual_stream < 0 ? dual_env_ : ctx->dual_stream != 0;
   SLIP_CHECK(costs && opts && adam && out, SLIP_EINVAL, "execute: NULL argument");
   SLIP_CHECK(warmup >= 0 && iterations >= 1, SLIP_EINVAL, "execute: iterations must be >= 1");
   Cluster cl;
@@ -132,6 +141,11 @@ extern "C" slip_status slip_execute_schedule(slip_ctx* ctx, slip_comm* comm, con
   // copies of later micro-batches overlap the compute of earlier ones
   if (io && !ctx->h2d) SLIP_CUDA(cudaStreamCreateWithFlags(&ctx->h2d, cudaStreamNonBlocking));
   cudaStream_t hs = ctx->h2d;
+  // (not in validated mode: a rollback rewrites the weights the forward of the next
+  // iteration may be reading on the other stream)
+  const bool dual = dual_ && !ctx->validate;
+  if (dual && !ctx->fwd) SLIP_CUDA(cudaStreamCreateWithFlags(&ctx->fwd, cudaStreamNonBlocking));
+  cudaStream_t fs = dual ? ctx->fwd : cs;  // stream of the forward actions
   for (int run = 0; run < 2; ++run) {
     const int H = run == 0 ? warmup : iterations;
     if (H == 0) continue;
@@ -175,9 +189,16 @@ extern "C" slip_status slip_execute_schedule(slip_ctx* ctx, slip_comm* comm, con
                 std::to_string(ctx->n_slots))
                    .c_str());
     std::vector<SlotEv> sev(ctx->n_slots);
+    cudaEvent_t opt_done = nullptr;  // dual stream: the last OPT (the weights F reads)
     if (timed) {
       SLIP_CUDA(cudaEventRecord(t0, cs));
       launches0 = ctx->launches;
+    }
+    if (fs != cs) {  // the forward stream starts with the compute stream
+      cudaEvent_t e;
+      SLIP_CUDA(pool.get(&e));
+      SLIP_CUDA(cudaEventRecord(e, cs));
+      SLIP_CUDA(cudaStreamWaitEvent(fs, e, 0));
     }
     auto xfer_stream = [&](int src, int dst) { return comm->pair_stream.at({src, dst}); };
     auto xfer_comm = [&](int src, int dst) { return comm->pair_comm.at({src, dst}); };
@@ -248,6 +269,7 @@ extern "C" slip_status slip_execute_schedule(slip_ctx* ctx, slip_comm* comm, con
       if (a.kind == SLIP_ACT_SEND_Y || a.kind == SLIP_ACT_SEND_DX) ts = xfer_stream(me, a.peer);
       if (a.kind == SLIP_ACT_AR) ts = comm->ar_stream;
       if (io && io->x_host && a.kind == SLIP_ACT_LOAD_X) ts = hs;
+      else if (a.kind == SLIP_ACT_LOAD_X || a.kind == SLIP_ACT_F) ts = fs;
       const bool tr = timed && tracing && !(a.kind == SLIP_ACT_AR && !comm->stage_comm);
       size_t tb_idx = 0;
       // called by every action after its stream waits: the phase timing (and the trace)
@@ -283,16 +305,16 @@ extern "C" slip_status slip_execute_schedule(slip_ctx* ctx, slip_comm* comm, con
                                         cudaMemcpyHostToDevice, hs));
             else
               SLIP_CUDA(cudaMemcpyAsync(sb->x, io->x_host[a.origin * m + a.mb], bytes, cudaMemcpyHostToDevice, hs));
-            SLIP_CUDA(chain(hs, cs));
+            SLIP_CUDA(chain(hs, fs));
             break;
           }
-          if (se->freed) SLIP_CUDA(cudaStreamWaitEvent(cs, se->freed, 0));
+          if (se->freed) SLIP_CUDA(cudaStreamWaitEvent(fs, se->freed, 0));
           SLIP_CUDA(trace_begin());
           if (ctx->dm.ends & 1) {  // the stage input is T token ids (embedding end)
-            SLIP_CUDA(synth_tokens(sb->end.tokens, D.T, D.V, seed, a.origin, a.mb, cs));
+            SLIP_CUDA(synth_tokens(sb->end.tokens, D.T, D.V, seed, a.origin, a.mb, fs));
             ctx->launches += 1;
           } else {
-            SLIP_CUDA(synth_normal(sb->x, static_cast<int64_t>(Th), seed, a.origin, a.mb, cs));
+            SLIP_CUDA(synth_normal(sb->x, static_cast<int64_t>(Th), seed, a.origin, a.mb, fs));
             ctx->launches += 1;
           }
           break;
@@ -303,18 +325,26 @@ extern "C" slip_status slip_execute_schedule(slip_ctx* ctx, slip_comm* comm, con
           SLIP_CUDA(trace_begin());
           ncclResult_t r = ncclRecv(sb->x, Th, ncclBfloat16, 0, xfer_comm(a.peer, me), ps);
           if (r != ncclSuccess) return nccl_status(r, "ncclRecv activation");
-          SLIP_CUDA(chain(ps, cs));
+          SLIP_CUDA(chain(ps, fs));
           break;
         }
         case SLIP_ACT_F:
-          if (se->sent_y) SLIP_CUDA(cudaStreamWaitEvent(cs, se->sent_y, 0));
+          if (se->sent_y) SLIP_CUDA(cudaStreamWaitEvent(fs, se->sent_y, 0));
+          if (dual) {  // the slot's stash is free (W done) and the weights are this iteration's
+            if (se->freed) SLIP_CUDA(cudaStreamWaitEvent(fs, se->freed, 0));
+            if (opt_done) SLIP_CUDA(cudaStreamWaitEvent(fs, opt_done, 0));
+          }
           SLIP_CUDA(trace_begin());
           SLIP_TRY(slip_stage_forward(ctx, a.slot, (ctx->dm.ends & 1) ? static_cast<void*>(sb->end.tokens) : sb->x,
-                                      sb->dy, stream));
+                                      sb->dy, reinterpret_cast<slip_stream>(fs)));
+          if (dual) {  // B / LOSS of this slot (on cs) read the F-stash and the output
+            SLIP_CUDA(pool.get(&se->f_done));
+            SLIP_CUDA(cudaEventRecord(se->f_done, fs));
+          }
           break;
         case SLIP_ACT_SEND_Y: {
           cudaStream_t ps = xfer_stream(me, a.peer);
-          SLIP_CUDA(chain(cs, ps));
+          SLIP_CUDA(chain(fs, ps));
           SLIP_CUDA(trace_begin());
           ncclResult_t r = ncclSend(sb->dy, Th, ncclBfloat16, 1, xfer_comm(me, a.peer), ps);
           if (r != ncclSuccess) return nccl_status(r, "ncclSend activation");
@@ -324,6 +354,7 @@ extern "C" slip_status slip_execute_schedule(slip_ctx* ctx, slip_comm* comm, con
         }
         case SLIP_ACT_LOSS: {
           bf16* target = ctx->ws.dy1;  // B's temporaries are free before the head runs
+          if (dual && se->f_done) SLIP_CUDA(cudaStreamWaitEvent(cs, se->f_done, 0));
           SLIP_CUDA(trace_begin());
           if (ctx->dm.ends & 2) {  // LM head + cross-entropy on T int32 labels
             int32_t* labels = reinterpret_cast<int32_t*>(target);
@@ -368,6 +399,7 @@ extern "C" slip_status slip_execute_schedule(slip_ctx* ctx, slip_comm* comm, con
         case SLIP_ACT_BC: {
           // slot.dx is the send buffer of the input gradient: the previous occupant's send must be done
           if (se->sent_dx) SLIP_CUDA(cudaStreamWaitEvent(cs, se->sent_dx, 0));
+          if (dual && se->f_done) SLIP_CUDA(cudaStreamWaitEvent(cs, se->f_done, 0));
           SLIP_CUDA(trace_begin());
           void* dx = me_i > 0 ? static_cast<void*>(sb->dx) : nullptr;
           SLIP_TRY(slip_backward_input(ctx, a.slot, sb->dy, dx, a.accumulate & 1, stream));
@@ -520,6 +552,10 @@ extern "C" slip_status slip_execute_schedule(slip_ctx* ctx, slip_comm* comm, con
             pend.step = ctx->opt_step;
             pend.flag_ready = fe;
           }
+          if (dual) {
+            SLIP_CUDA(pool.get(&opt_done));
+            SLIP_CUDA(cudaEventRecord(opt_done, cs));
+          }
           break;
         default:
           set_error("execute: unknown action");
@@ -536,6 +572,7 @@ extern "C" slip_status slip_execute_schedule(slip_ctx* ctx, slip_comm* comm, con
     }
     if (ctx->validate) SLIP_TRY(flush_rollback(1 << 30));
     // join every side stream back into the compute stream
+    if (fs != cs) SLIP_CUDA(chain(fs, cs));
     for (auto& kv : comm->pair_stream) SLIP_CUDA(chain(kv.second, cs));
     SLIP_CUDA(chain(comm->ar_stream, cs));
     if (comm->val_stream) SLIP_CUDA(chain(comm->val_stream, cs));
@@ -596,6 +633,12 @@ extern "C" slip_status slip_execute_schedule(slip_ctx* ctx, slip_comm* comm, con
     // a rolled-back or skipped step does not count towards AdamW's bias correction next call
     ctx->opt_step -= rs[0] + rs[1];
   }
+  return SLIP_OK;
+}
+
+extern "C" slip_status slip_set_dual_stream(slip_ctx* ctx, int32_t enable) {
+  SLIP_CHECK(ctx, SLIP_EINVAL, "set_dual_stream: ctx is NULL");
+  ctx->dual_stream = enable != 0 ? 1 : 0;
   return SLIP_OK;
 }
 
