@@ -67,8 +67,8 @@ def parse():
     ap.add_argument("--gpt-ends", action="store_true",
                     help="GPT model ends: token + position embedding on the first stage, final LN + LM head "
                          "(vocab 50304) + cross-entropy on the last stage (SURVEY §8(f) NEXT-3)")
-    ap.add_argument("--no-dual-stream", action="store_true",
-                    help="forward actions on the compute stream (default: their own stream after profiling)")
+    ap.add_argument("--dual-stream", default="auto", choices=["auto", "on", "off"],
+                    help="forward actions on their own stream after profiling (auto: when PP = 1)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--model", default="1.3b", choices=sorted(MODELS), help="GPT shape (default: BASELINE configs[1])")
@@ -410,7 +410,7 @@ def main():
     # (slip_set_dual_stream: same plan, same results; measured +1-2.8 % at N = 1).  With
     # PP > 1 the overlapping forward competes with the backward chain across the stages,
     # which is the critical path at small m (DP2xPP2 m = 2: 321k -> 301k), so it stays off.
-    dual = not args.no_dual_stream and PP == 1
+    dual = args.dual_stream == "on" or (args.dual_stream == "auto" and PP == 1)
     rt.call("slip_set_dual_stream", stage.ctx, int(dual))
     # warm-up steps with the profiled plan
     execute(args.warmup)

@@ -144,7 +144,25 @@ extern "C" slip_status slip_execute_schedule(slip_ctx* ctx, slip_comm* comm, con
   // (not in validated mode: a rollback rewrites the weights the forward of the next
   // iteration may be reading on the other stream)
   const bool dual = dual_ && !ctx->validate;
-  if (dual && !ctx->fwd) SLIP_CUDA(cudaStreamCreateWithFlags(&ctx->fwd, cudaStreamNonBlocking));
+  // the backward-side actions then run on a high-priority stream of the context (the block
+  // scheduler places their CTAs first: the backward chain is the pipeline's critical path),
+  // the forward ones on a low-priority one; the caller's stream brackets both
+  cudaStream_t cs_call = cs;
+  if (dual) {
+    if (!ctx->fwd || !ctx->bwd) {
+      int least = 0, greatest = 0;
+      SLIP_CUDA(cudaDeviceGetStreamPriorityRange(&least, &greatest));
+      if (!ctx->fwd) SLIP_CUDA(cudaStreamCreateWithPriority(&ctx->fwd, cudaStreamNonBlocking, least));
+      if (!ctx->bwd) SLIP_CUDA(cudaStreamCreateWithPriority(&ctx->bwd, cudaStreamNonBlocking, greatest));
+    }
+    cudaEvent_t e;
+    SLIP_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    SLIP_CUDA(cudaEventRecord(e, cs_call));
+    SLIP_CUDA(cudaStreamWaitEvent(ctx->bwd, e, 0));
+    SLIP_CUDA(cudaEventDestroy(e));
+    cs = ctx->bwd;
+    stream = reinterpret_cast<slip_stream>(cs);
+  }
   cudaStream_t fs = dual ? ctx->fwd : cs;  // stream of the forward actions
   for (int run = 0; run < 2; ++run) {
     const int H = run == 0 ? warmup : iterations;
@@ -583,6 +601,13 @@ extern "C" slip_status slip_execute_schedule(slip_ctx* ctx, slip_comm* comm, con
       out->n_ops = static_cast<int64_t>(progs[me].size());
       out->plan_hash = plan_hash(plan.ops.data(), static_cast<int64_t>(plan.ops.size()));
     }
+  }
+  if (cs != cs_call) {  // the caller's stream resumes after the backward-side stream
+    cudaEvent_t e;
+    SLIP_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    SLIP_CUDA(cudaEventRecord(e, cs));
+    SLIP_CUDA(cudaStreamWaitEvent(cs_call, e, 0));
+    SLIP_CUDA(cudaEventDestroy(e));
   }
   SLIP_CUDA(cudaEventSynchronize(t1));
   float ms = 0.f;

@@ -105,7 +105,8 @@ struct slip_ctx {
   std::vector<int> state;
   int64_t launches = 0;  // kernels enqueued through this context
   cudaStream_t h2d = nullptr;  // executor: host-to-device copies of the e2e inputs (lazily created)
-  cudaStream_t fwd = nullptr;  // executor, dual stream: the forward actions' stream (lazily created)
+  cudaStream_t fwd = nullptr;  // executor, dual stream: the forward actions' stream (lowest priority)
+  cudaStream_t bwd = nullptr;  // executor, dual stream: every other compute action (highest priority)
   int dual_stream = -1;        // slip_set_dual_stream (-1: the SLIP_DUAL_STREAM environment default)
   int64_t opt_step = 0;  // AdamW steps taken by the executor
   bool trace_on = false;
