@@ -602,6 +602,17 @@ def main():
         "planner_costs_10us": [costs.t_f, costs.t_b, costs.t_w, costs.t_opt],
     }
     line["memory"] = memory
+    # the metric's second half (BASELINE.json: "B/W tensor-pipe % of peak") from the committed
+    # per-phase ncu capture of this model's layer (a profiler number: context, not timed here)
+    try:
+        with open(os.path.join(ROOT, "profiles", "r02_tensor_pipe.json")) as f:
+            tp = json.load(f).get("gpt-%s" % MODEL)
+        if tp:
+            line["tensor_pipe_ncu"] = {ph: tp[ph]["tensor_pipe_pct"] for ph in ("F", "B", "W") if ph in tp}
+            line["tensor_pipe_ncu"]["source"] = "profiles/r02_tensor_pipe.json (ncu, one layer-micro-batch)"
+            line["hbm_frac_ncu"] = {"adamw": tp["AdamW"]["other_frac_hbm"], "b_elementwise": tp["B"]["other_frac_hbm"]}
+    except Exception:
+        pass
     if norm:
         line["normalization"] = norm
     elif alg1_R is not None:
