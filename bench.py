@@ -67,6 +67,9 @@ def parse():
     ap.add_argument("--gpt-ends", action="store_true",
                     help="GPT model ends: token + position embedding on the first stage, final LN + LM head "
                          "(vocab 50304) + cross-entropy on the last stage (SURVEY §8(f) NEXT-3)")
+    ap.add_argument("--fused-adamw", action="store_true",
+                    help="AdamW of the 2-D weights in the last W's epilogue where no all-reduce follows "
+                         "(measured slower under the 1 kW power cap: off by default)")
     ap.add_argument("--dual-stream", default="auto", choices=["auto", "on", "off"],
                     help="forward actions on their own stream after profiling (auto: when PP = 1)")
     ap.add_argument("--no-e2e", action="store_true")
@@ -412,6 +415,10 @@ def main():
     # which is the critical path at small m (DP2xPP2 m = 2: 321k -> 301k), so it stays off.
     dual = args.dual_stream == "on" or (args.dual_stream == "auto" and PP == 1)
     rt.call("slip_set_dual_stream", stage.ctx, int(dual))
+    # AdamW of the 2-D weights in the epilogue of the iteration's last W where no all-reduce
+    # follows (N = 1; the survivor of a failed DP = 2 group) — slip_set_fused_adamw
+    fused_adamw = args.fused_adamw
+    rt.call("slip_set_fused_adamw", stage.ctx, int(fused_adamw))
     # warm-up steps with the profiled plan
     execute(args.warmup)
     barrier()
@@ -583,12 +590,16 @@ def main():
                    "model": "gpt-%s-shape" % MODEL, "global_batch": DP * m * MB, "seq_len": SEQ,
                    "parallelism": "dp%dxpp%d" % (DP, PP), "failed_workers": failed, "sm_reserve": sm_reserve,
                    "p2p_ctas": args.p2p_ctas, "fused_ar_adam": fused_ar, "dual_stream": dual,
+                   "adamw_in_w_epilogue": fused_adamw,
                    "l2": "inputs larger than L2 (2.4 GB bf16 weights + GBs of stash per step)"},
         "clocks": clk,
         "e2e": e2e,
         "gpu_launches": gpu_launches,
         "roofline": {"bound": "tensor",
-                     "kernel": "W GEMMs (tcgen05, dW (+)= sum over the launch's micro-batches dY^T X, fp32 TMA store)",
+                     "kernel": "W GEMMs (tcgen05, dW (+)= sum over the launch's micro-batches dY^T X, fp32 TMA store" +
+                               ("; where no all-reduce follows, the iteration's last W applies AdamW to the 2-D "
+                                "weights in its epilogue instead of storing dW: achieved counts the GEMM FLOPs only)"
+                                if fused_adamw else ")"),
                      "achieved": ach, "peak": p_sus, "peak_kind": "bf16_tflops_sustained (%s)" % peak_src,
                      "unit": "TFLOP/s", "frac": (ach / p_sus) if ach else None, "traffic": traffic,
                      "flops_per_launch": flops_w_op * w_ops / w_launches if w_launches else None,

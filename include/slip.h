@@ -494,6 +494,17 @@ slip_status slip_inject_fault(slip_ctx* ctx, int32_t kind);
  * 0), bf16 weights refreshed. */
 slip_status slip_optimizer_rollback(slip_ctx* ctx, const slip_adam* a, int64_t step, float grad_scale, slip_stream s);
 
+/* Execution option of slip_execute_schedule (default off): where the iteration's last W
+ * already yields the final stage gradient — no DP all-reduce (DP = 1, or a stage whose
+ * peer failed), no validation, no GPT ends — that W's grouped GEMM applies AdamW to the
+ * 2-D weights in its epilogue (EPI_ADAMW: dW from the accumulator straight into master /
+ * m / v and the bf16 copy, with the step and grad_scale of the OPT that follows) instead
+ * of storing dW, and that OPT steps only the 1-D parameters.  Same arithmetic as
+ * slip_optimizer_step; the gradient buffer then holds no W gradients for those weights.
+ * The optimizer's traffic for the weights (26 B each) moves under the W GEMM's
+ * compute-bound mainloop, and dW's 4-byte store and re-read disappear. */
+slip_status slip_set_fused_adamw(slip_ctx* ctx, int32_t enable);
+
 /* Execution option of slip_execute_schedule (default off; SLIP_DUAL_STREAM=1 in the
  * environment turns the default on): the forward actions (LOAD_X / RECV_X, F, and the
  * SEND_Y that follows) run on a second compute stream of the context, ordered by events

@@ -138,6 +138,7 @@ SIGNATURES = {
     "slip_synth_tokens": (C.c_int, [P, I64, I32, U64, U64, U64, P]),
     "slip_set_validation": (C.c_int, [P, I32]),
     "slip_set_dual_stream": (C.c_int, [P, I32]),
+    "slip_set_fused_adamw": (C.c_int, [P, I32]),
     "slip_set_stream_k": (C.c_int, [P, I32]),
     "slip_inject_fault": (C.c_int, [P, I32]),
     "slip_optimizer_rollback": (C.c_int, [P, C.POINTER(slip_adam), I64, F32, P]),

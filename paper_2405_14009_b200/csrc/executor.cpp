@@ -121,6 +121,11 @@ extern "C" slip_status slip_execute_schedule(slip_ctx* ctx, slip_comm* comm, con
   // DP = 2 all-reduce fused into AdamW (slip_comm_fuse_ar_adam); validated steps keep the
   // NCCL all-reduce (their rollback needs the summed gradient in place)
   const bool fused_ar = comm->fused_ar && comm->stage_comm && !ctx->validate;
+  // AdamW of the 2-D weights in the epilogue of the iteration's last W (slip_set_fused_adamw):
+  // only where that W's dW is already the final gradient — no all-reduce (DP = 1 or a
+  // singleton group whose peer failed), no validation, no model ends
+  const bool adamw_in_w = ctx->fuse_adamw && !comm->stage_comm && !ctx->validate && ctx->dm.ends == 0 &&
+                          ctx->n_slots >= 2;
   SLIP_CHECK(!fused_ar || comm->fused_local == ctx->grad, SLIP_ESTATE,
              "execute: gradient buffer re-bound since slip_comm_fuse_ar_adam");
 
@@ -274,6 +279,7 @@ extern "C" slip_status slip_execute_schedule(slip_ctx* ctx, slip_comm* comm, con
               pre[t][i].push_back(j);
     }
     int send_pos = kValSend, recv_pos = kValRecv;
+    int w_adamw_iter = -1;  // iteration whose 2-D weights the last W's epilogue stepped
     const std::vector<slip_action>& prog = progs[me];
     size_t skip_to = 0;  // W actions already run by a merged W launch
     for (size_t ai = 0; ai < prog.size(); ++ai) {
@@ -449,7 +455,14 @@ extern "C" slip_status slip_execute_schedule(slip_ctx* ctx, slip_comm* comm, con
                    prog[ai + run].iter == a.iter)
               ++run;
           SLIP_CUDA(trace_begin());
-          if (run == 1) {
+          const bool last_w = ai + run < prog.size() && prog[ai + run].kind == SLIP_ACT_AR && prog[ai + run].iter == a.iter;
+          if (adamw_in_w && last_w) {  // dW straight into AdamW (step = the coming OPT's)
+            int slots[8];
+            for (size_t j = 0; j < run; ++j) slots[j] = prog[ai + j].slot;
+            const AdamEpi ad = adam_epilogue_args(ctx, adam, ctx->opt_step + 1, grad_scale);
+            SLIP_TRY(weight_multi(ctx, slots, static_cast<int>(run), a.accumulate, cs, &ad));
+            w_adamw_iter = a.iter;
+          } else if (run == 1) {
             SLIP_TRY(slip_backward_weight(ctx, a.slot, a.accumulate, stream));
           } else {
             int slots[8];
@@ -494,6 +507,8 @@ extern "C" slip_status slip_execute_schedule(slip_ctx* ctx, slip_comm* comm, con
               mark_done = true;
             }
             SLIP_CUDA(peer_barrier(comm->peer_flags, comm->flags, ++comm->epoch, cs));
+          } else if (!ctx->validate && w_adamw_iter == a.iter) {  // the 2-D weights stepped in W
+            SLIP_TRY(optimizer_step_vectors(ctx, adam, ctx->opt_step, grad_scale, ctx->ws.nonfinite, cs));
           } else if (!ctx->validate) {
             SLIP_TRY(slip_optimizer_step(ctx, adam, ctx->opt_step, grad_scale, ctx->ws.nonfinite, stream));
           } else {

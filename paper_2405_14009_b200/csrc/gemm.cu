@@ -22,6 +22,7 @@
 #include "gemm.cuh"
 #include "launch.cuh"
 #include "ptx.cuh"
+#include "adamw_math.cuh"
 
 namespace slip {
 namespace {
@@ -73,6 +74,7 @@ struct KParams {
   __nv_bfloat16* aux;
   float alpha;
   int accumulate;
+  AdamEpi adam;  // EPI_ADAMW
   // grouped mode: the contraction runs over kz_n operand batches (zi = kz_list[j], each
   // kz_nkb k-blocks) into ONE accumulator — the W of several micro-batches in one launch
   int kz_n, kz_nkb;
@@ -262,7 +264,9 @@ __device__ __forceinline__ void g_gprobe_kind(int i, int k) {
   } while (0)
 #endif
 
-template <int BN, bool A_MN, bool B_MN, bool PAIR>
+// ADAMW (compile time): the instantiation of the W launch whose epilogue applies AdamW
+// (EPI_ADAMW) — none of the other epilogues are compiled into it, and it into no other
+template <int BN, bool A_MN, bool B_MN, bool PAIR, bool ADAMW = false>
 __global__ void __launch_bounds__(NUM_THREADS, 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                    const __grid_constant__ CUtensorMap tmC, const __grid_constant__ CUtensorMap tmX,
@@ -495,7 +499,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         uint32_t r[32];
         if (ew == 0 && lane == 0 && gie == 0) GPROBE(100 + 10 * (ch >> 1) + 0);
         ptx::tmem_ld_32x32b_x32(tmem_base + (static_cast<uint32_t>(lq * 32) << 16) + acc * C::ACC_COLS + ch * 32, r);
-        ptx::tmem_ld_wait();
+        ptx::tmem_ld_wait_dep(r);  // (orders every use of r after the wait)
         if (ew == 0 && lane == 0 && gie == 0) GPROBE(100 + 10 * (ch >> 1) + 1);
         if (kind == 2) {  // a later part of a split tile: leave the fp32 partial, no epilogue
           if (pf_next) prefetch(ch + 2);
@@ -530,6 +534,55 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           if (pf_next) prefetch(ch + 2);
           continue;
         }
+        if constexpr (ADAMW) {
+          // the W GEMM's final dW tile goes straight into AdamW.  The warp's 32 x 32 block is
+          // transposed through its staging tile (XOR swizzle: conflict-free both ways) so
+          // that lane = column: every p / m / v / g load and p / m / v / w store of the warp
+          // is one coalesced 128-byte (bf16: 64-byte) row segment; rows go 8 at a time with
+          // all their loads in flight before any use, the optimizer state streamed
+          // (evict-first) so it does not push the W operand slabs out of L2
+          const AdamEpi& ad = p.adam;
+#pragma unroll
+          for (int j = 0; j < 32; ++j) buf[lane * 32 + (j ^ lane)] = __uint_as_float(r[j]);
+          __syncwarp();
+          const int col = n + lane;
+          const bool cok = col < tl.N;
+          const int64_t base = (tl.g >= 0 ? p.groups[tl.g].poff : 0) + static_cast<int64_t>(row0) * tl.N + col;
+          const int rows = min(32, tl.M - row0);
+          bool bad = false;
+#pragma unroll 1
+          for (int i0 = 0; i0 < rows; i0 += 8) {
+            float pp[8], mm[8], vv[8], gg[8];
+#pragma unroll
+            for (int k = 0; k < 8; ++k) {
+              const int i = i0 + k;
+              const bool ok = cok && i < rows;
+              const int64_t e = base + static_cast<int64_t>(i) * tl.N;
+              pp[k] = ok ? __ldcs(ad.p + e) : 0.f;
+              mm[k] = ok ? __ldcs(ad.m + e) : 0.f;
+              vv[k] = ok ? __ldcs(ad.v + e) : 0.f;
+              gg[k] = (ok && e_accum) ? __ldcs(ad.g + e) : 0.f;
+            }
+#pragma unroll
+            for (int k = 0; k < 8; ++k) {
+              const int i = i0 + k;
+              if (!cok || i >= rows) continue;
+              const float a = buf[i * 32 + (lane ^ i)];
+              const float ge = e_accum ? a + gg[k] : a;
+              bad |= !isfinite(ge);
+              adamw_update(pp[k], mm[k], vv[k], ge, ad.lr, ad.b1, ad.b2, ad.eps, ad.wd, ad.inv_bc1, ad.inv_bc2,
+                           ad.grad_scale);
+              const int64_t e = base + static_cast<int64_t>(i) * tl.N;
+              __stcs(ad.p + e, pp[k]);
+              __stcs(ad.m + e, mm[k]);
+              __stcs(ad.v + e, vv[k]);
+              ad.w[e] = __float2bfloat16_rn(pp[k]);
+            }
+          }
+          __syncwarp();  // the staging tile is rewritten by the next chunk
+          if (__any_sync(0xffffffffu, bad) && lane == 0 && ad.nonfinite) atomicOr(ad.nonfinite, 1);
+          continue;
+        } else {
         if (e_mode >= EPI_F32_STORE) {
           if (lane == 0) ptx::bulk_wait_read0();
           __syncwarp();
@@ -606,6 +659,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           }
           if (ew == 0 && lane == 0 && gie == 0) GPROBE(100 + 10 * (ch >> 1) + 3);
         }
+        }  // !ADAMW
       }
       ptx::tc_fence_before();
       __syncwarp();
@@ -713,11 +767,11 @@ bool encode_operand(CUtensorMap* map, const Operand& o, int rows, int K, int zi,
 }
 
 // Persistent launch: one CTA (or CTA pair, cluster 2x1x1) per SM, at most one per tile.
-template <int BN, bool A_MN, bool B_MN, bool PAIR>
+template <int BN, bool A_MN, bool B_MN, bool PAIR, bool ADAMW = false>
 cudaError_t launch_kernel(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& tc, const CUtensorMap& tx,
                           const KParams& p, cudaStream_t s) {
   using C = Cfg<BN, A_MN, B_MN, PAIR>;
-  auto kern = gemm_tc_kernel<BN, A_MN, B_MN, PAIR>;
+  auto kern = gemm_tc_kernel<BN, A_MN, B_MN, PAIR, ADAMW>;
   static std::once_flag once;
   static cudaError_t attr_err = cudaSuccess;
   std::call_once(once, [&] {
@@ -748,6 +802,13 @@ cudaError_t launch_t(const GemmDesc& d, cudaStream_t s, const GroupEntry* groups
     p.n_groups = n_groups;
     p.total = group_tiles;
     p.band = 8;  // measured: 2 / 4 / 8 / 16 / 32 -> W 15.03 / 14.93 / 14.74 / 14.84 / 15.06 ms
+    if (d.mode == EPI_ADAMW) {
+      if (!d.adam || !d.adam->p || !d.adam->m || !d.adam->v || !d.adam->w || (d.accumulate && !d.adam->g)) {
+        g_msg = "gemm_group: EPI_ADAMW needs the AdamW state (GemmDesc::adam)";
+        return cudaErrorInvalidValue;
+      }
+      p.adam = *d.adam;
+    }
     if (d.kz_n > 1) {
       if (d.kz_n > 8 || d.kz_nkb <= 0) {
         g_msg = "gemm_group: kz_n must be in [2, 8] with kz_nkb > 0";
@@ -757,6 +818,8 @@ cudaError_t launch_t(const GemmDesc& d, cudaStream_t s, const GroupEntry* groups
       p.kz_nkb = d.kz_nkb;
       for (int j = 0; j < d.kz_n; ++j) p.kz_list[j] = d.kz_list[j];
     }
+    if constexpr (A_MN && B_MN)
+      if (d.mode == EPI_ADAMW) return launch_kernel<BN, A_MN, B_MN, PAIR, true>(ta, tb, tc, tc, p, s);
     return launch_kernel<BN, A_MN, B_MN, PAIR>(ta, tb, tc, tc, p, s);
   }
   if (!encode_operand(&ta, d.a, d.M, d.K, d.zi_count, d.zo_count, BM)) return cudaErrorInvalidValue;
@@ -923,6 +986,7 @@ cudaError_t gemm_group_encode(const GemmDesc* probs, int n, GroupEntry* out, int
     const int tile_m = (probs[0].pair && probs[0].bn == 256) ? 2 * BM : BM;
     g.M = d.M;
     g.N = d.N;
+    g.poff = d.poff;
     g.mt = (d.M + tile_m - 1) / tile_m;
     g.nkb = (d.K + BK - 1) / BK;
     g.tile_begin = tiles;

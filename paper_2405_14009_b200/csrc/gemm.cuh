@@ -7,6 +7,7 @@
 // (zi, zo) offsets, which covers per-(batch, head) attention views of the QKV buffer.
 #pragma once
 #include <cuda.h>
+#include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
 #include <cstdint>
@@ -18,7 +19,20 @@ enum EpiMode : int {
   EPI_BF16_GELU = 1,   // H = alpha*acc + bias[n]; aux = bf16(gelu'(H)); C = bf16(gelu(H))
   EPI_BF16_DGELU = 2,  // C = bf16(acc * aux[m,n])   (aux = gelu'(H) from EPI_BF16_GELU)
   EPI_F32_STORE = 3,   // C(f32) = alpha*acc                  (TMA store)
-  EPI_F32_ACC = 4      // C(f32) += acc, or = acc if !accumulate (TMA reduce-add / store)
+  EPI_F32_ACC = 4,     // C(f32) += acc, or = acc if !accumulate (TMA reduce-add / store)
+  EPI_ADAMW = 5        // g = acc (+ C if accumulate): AdamW on the parameters of C's elements
+                       // (GemmDesc::adam), dW itself is not stored (grouped W launches)
+};
+
+// EPI_ADAMW: flat fp32 master / m / v, the bf16 weight copy and the gradient buffer the
+// problem's C indexes into (element (r, c) of problem g is flat index poff_g + r*ldc + c);
+// every element is a 2-D weight (decayed).  inv_bc = 1 / (1 - beta^step).
+struct AdamEpi {
+  float *p = nullptr, *m = nullptr, *v = nullptr;
+  const float* g = nullptr;  // read when accumulate (earlier W's partial sum)
+  __nv_bfloat16* w = nullptr;
+  float lr = 0.f, b1 = 0.f, b2 = 0.f, eps = 0.f, wd = 0.f, inv_bc1 = 1.f, inv_bc2 = 1.f, grad_scale = 1.f;
+  int32_t* nonfinite = nullptr;
 };
 
 enum Causal : int {
@@ -64,6 +78,8 @@ struct GemmDesc {
   // k-blocks each — into one accumulator (the W of several micro-batches, slot = zi).
   int kz_n = 0, kz_nkb = 0;
   int kz_list[8] = {};
+  int64_t poff = -1;               // EPI_ADAMW: flat element offset of C (set per problem)
+  const AdamEpi* adam = nullptr;   // EPI_ADAMW (grouped launch proto)
 };
 size_t gemm_sk_bytes();
 
@@ -78,6 +94,7 @@ cudaError_t gemm_launch(const GemmDesc& d, cudaStream_t s);
 struct alignas(128) GroupEntry {
   CUtensorMap ta, tb, tc;
   int M, N, mt, nkb, tile_begin, tile_end;
+  int64_t poff;  // EPI_ADAMW: flat element offset of the problem's C (GemmDesc::poff)
 };
 cudaError_t gemm_group_encode(const GemmDesc* probs, int n, GroupEntry* host_out, int* total_tiles);
 cudaError_t gemm_group_launch(const GroupEntry* dev_table, int n, int total_tiles, const GemmDesc& proto,

@@ -9,6 +9,7 @@
 #include <cmath>
 
 #include "kernels.cuh"
+#include "adamw_math.cuh"
 #include "gemm.cuh"
 #include "launch.cuh"
 #include "ptx.cuh"
@@ -622,18 +623,45 @@ __global__ void __launch_bounds__(256) adamw_kernel(float* __restrict__ p, float
 #pragma unroll
     for (int e = 0; e < 4; ++e) {
       bad |= !isfinite(ga[e]);
-      const float gr = grad_scale * ga[e];
-      ma[e] = b1 * ma[e] + (1.f - b1) * gr;
-      va[e] = b2 * va[e] + (1.f - b2) * gr * gr;
-      const float mh = ma[e] * inv_bc1;
-      const float vh = va[e] * inv_bc2;
-      pa[e] = pa[e] - lr * wdl * pa[e] - lr * mh / (sqrtf(vh) + eps);
+      adamw_update(pa[e], ma[e], va[e], ga[e], lr, b1, b2, eps, wdl, inv_bc1, inv_bc2, grad_scale);
     }
     reinterpret_cast<float4*>(p)[i] = pp;
     reinterpret_cast<float4*>(m)[i] = mm;
     reinterpret_cast<float4*>(v)[i] = vv;
     reinterpret_cast<uint2*>(w)[i] = pack4(pa[0], pa[1], pa[2], pa[3]);
     gp = gp_next;
+  }
+  if (nonfinite && __any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicOr(nonfinite, 1);
+}
+
+// AdamW over the 1-D parameters of every layer only (bqkv | bo g1 b1n g2 b2n | b1 | b2:
+// 9h + f per layer, never decayed): the OPT of a stage whose 2-D weights were already
+// stepped in the W GEMM's epilogue (EPI_ADAMW).
+__global__ void __launch_bounds__(256) adamw_vectors_kernel(float* __restrict__ p, float* __restrict__ m,
+                                                            float* __restrict__ v, const float* __restrict__ g,
+                                                            bf16* __restrict__ w, int64_t total, int64_t per_layer,
+                                                            int h, int f, float lr, float b1, float b2, float eps,
+                                                            float inv_bc1, float inv_bc2, float grad_scale,
+                                                            int32_t* __restrict__ nonfinite) {
+  ptx::grid_dep_wait();
+  const int64_t H = h, F = f, per = 9 * H + F;
+  bool bad = false;
+  for (int64_t i = blockIdx.x * 256LL + threadIdx.x; i < total; i += static_cast<int64_t>(gridDim.x) * 256) {
+    const int64_t layer = i / per, r = i - layer * per;
+    int64_t o;
+    if (r < 3 * H) o = 3 * H * H + r;                              // bqkv
+    else if (r < 8 * H) o = 4 * H * H + 3 * H + (r - 3 * H);       // bo g1 b1n g2 b2n
+    else if (r < 8 * H + F) o = 4 * H * H + 8 * H + F * H + (r - 8 * H);  // b1
+    else o = 4 * H * H + 8 * H + 2 * F * H + F + (r - 8 * H - F);   // b2
+    const int64_t e = layer * per_layer + o;
+    float pp = p[e], mm = m[e], vv = v[e];
+    const float gg = g[e];
+    bad |= !isfinite(gg);
+    adamw_update(pp, mm, vv, gg, lr, b1, b2, eps, 0.f, inv_bc1, inv_bc2, grad_scale);
+    p[e] = pp;
+    m[e] = mm;
+    v[e] = vv;
+    w[e] = __float2bfloat16_rn(pp);
   }
   if (nonfinite && __any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicOr(nonfinite, 1);
 }
@@ -1118,6 +1146,14 @@ cudaError_t adamw(float* p, float* m, float* v, const float* g, bf16* w, int64_t
   wr.d1 = wr.d0 + H * F;
   return launch_pdl(adamw_kernel, dim3(grid_for(n / 4)), dim3(256), 0, s, 1, p, m, v, g, w, n / 4, per_layer, wr, lr,
                     b1, b2, eps, wd, 1.0f / bc1, 1.0f / bc2, grad_scale, nonfinite, skip, g_peer);
+}
+
+cudaError_t adamw_vectors(float* p, float* m, float* v, const float* g, bf16* w, int layers, int64_t per_layer, int h,
+                          int f, float lr, float b1, float b2, float eps, float bc1, float bc2, float grad_scale,
+                          int32_t* nonfinite, cudaStream_t s) {
+  const int64_t total = static_cast<int64_t>(layers) * (9LL * h + f);
+  return launch_pdl(adamw_vectors_kernel, dim3(grid_for(total)), dim3(256), 0, s, 1, p, m, v, g, w, total, per_layer, h,
+                    f, lr, b1, b2, eps, 1.0f / bc1, 1.0f / bc2, grad_scale, nonfinite);
 }
 
 // Two-GPU barrier through peer-mapped flags (the fused DP = 2 all-reduce, comm.cpp):

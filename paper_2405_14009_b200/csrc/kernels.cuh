@@ -88,6 +88,11 @@ cudaError_t adamw(float* p, float* m, float* v, const float* g, bf16* w, int64_t
                   int32_t* nonfinite, cudaStream_t s, const int32_t* skip = nullptr, TailDecay tail = TailDecay(),
                   const float* g_peer = nullptr);
 // g_peer (peer-mapped, may be NULL): the DP peer's gradient; the step uses g + g_peer.
+// AdamW over the layers' 1-D parameters only (the 2-D weights were stepped in the W GEMM
+// epilogue, gemm.cuh EPI_ADAMW); same per-element arithmetic (adamw_math.cuh).
+cudaError_t adamw_vectors(float* p, float* m, float* v, const float* g, bf16* w, int layers, int64_t per_layer, int h,
+                          int f, float lr, float b1, float b2, float eps, float bc1, float bc2, float grad_scale,
+                          int32_t* nonfinite, cudaStream_t s);
 // Two-GPU barrier on peer-mapped flags (fused DP = 2 all-reduce); epochs increase per call.
 cudaError_t peer_barrier(unsigned* peer_flag, const unsigned* my_flag, unsigned epoch, cudaStream_t s);
 // Arithmetic reversal of one adamw step with the same gradient;

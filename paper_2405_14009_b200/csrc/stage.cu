@@ -426,6 +426,7 @@ std::vector<GemmDesc> w_problems(slip_ctx* c, int slot) {
     d.mode = EPI_F32_ACC;
     d.c = dW;
     d.ldc = K;
+    d.poff = dW - c->grad;  // (the fused-AdamW epilogue indexes the flat state with it)
     v.push_back(d);
   };
   for (int l = c->L - 1; l >= 0; --l) {
@@ -683,13 +684,15 @@ slip_status slip_backward_input(slip_ctx* c, int32_t slot, const void* dy, void*
 }  // extern "C"
 
 namespace slip {
-slip_status weight_multi(slip_ctx* c, const int* slots, int n, int accumulate, cudaStream_t s) {
-  SLIP_CHECK(c && slots && n >= 2 && n <= 8 && c->n_slots >= 2, SLIP_EINVAL, "weight_multi: bad arguments");
+slip_status weight_multi(slip_ctx* c, const int* slots, int n, int accumulate, cudaStream_t s, const AdamEpi* adam) {
+  SLIP_CHECK(c && slots && n >= 1 && n <= 8 && c->n_slots >= 2, SLIP_EINVAL, "weight_multi: bad arguments");
+  SLIP_CHECK(!adam || !c->dm.ends, SLIP_EINVAL, "weight_multi: the fused AdamW epilogue excludes the GPT ends");
   for (int j = 0; j < n; ++j) SLIP_TRY(slot_check(c, slots[j], SLOT_B_DONE));
   GemmDesc proto;
   proto.bn = 256;
   proto.a.mn_major = proto.b.mn_major = true;
-  proto.mode = EPI_F32_ACC;
+  proto.mode = adam ? EPI_ADAMW : EPI_F32_ACC;
+  proto.adam = adam;
   proto.accumulate = accumulate;
   proto.kz_n = n;
   proto.kz_nkb = (c->dm.T + 63) / 64;
@@ -744,6 +747,38 @@ slip_status slip_optimizer_step(slip_ctx* c, const slip_adam* a, int64_t step, f
 }
 
 }  // extern "C"
+
+AdamEpi slip::adam_epilogue_args(slip_ctx* c, const slip_adam* a, int64_t step, float grad_scale) {
+  AdamEpi e;
+  e.p = c->master;
+  e.m = c->adam_m;
+  e.v = c->adam_v;
+  e.g = c->grad;
+  e.w = c->w;
+  e.lr = a->lr;
+  e.b1 = a->beta1;
+  e.b2 = a->beta2;
+  e.eps = a->eps;
+  e.wd = a->weight_decay;
+  // the same float constants the flat kernel receives (adamw(): 1.0f / float(bc))
+  e.inv_bc1 = 1.0f / static_cast<float>(1.0 - std::pow(static_cast<double>(a->beta1), static_cast<double>(step)));
+  e.inv_bc2 = 1.0f / static_cast<float>(1.0 - std::pow(static_cast<double>(a->beta2), static_cast<double>(step)));
+  e.grad_scale = grad_scale;
+  e.nonfinite = c->ws.nonfinite;
+  return e;
+}
+
+slip_status slip::optimizer_step_vectors(slip_ctx* c, const slip_adam* a, int64_t step, float grad_scale,
+                                         int32_t* d_nonfinite, cudaStream_t st) {
+  SLIP_CHECK(c && c->bound && a && step >= 1 && !c->dm.ends, SLIP_EINVAL, "optimizer_step_vectors: bad arguments");
+  const double bc1 = 1.0 - std::pow(static_cast<double>(a->beta1), static_cast<double>(step));
+  const double bc2 = 1.0 - std::pow(static_cast<double>(a->beta2), static_cast<double>(step));
+  return kcheck(c,
+                adamw_vectors(c->master, c->adam_m, c->adam_v, c->grad, c->w, c->L, c->po.per_layer, c->dm.h, c->dm.f,
+                              a->lr, a->beta1, a->beta2, a->eps, static_cast<float>(bc1), static_cast<float>(bc2),
+                              grad_scale, d_nonfinite, st),
+                "adamw_vectors");
+}
 
 slip_status slip::optimizer_step_peer(slip_ctx* c, const slip_adam* a, int64_t step, float grad_scale,
                                       int32_t* d_nonfinite, slip_stream st, const float* peer_grad) {
@@ -845,6 +880,12 @@ extern "C" {
 slip_status slip_set_stream_k(slip_ctx* c, int32_t enable) {
   SLIP_CHECK(c, SLIP_EINVAL, "set_stream_k: ctx is NULL");
   c->stream_k = enable != 0;
+  return SLIP_OK;
+}
+
+slip_status slip_set_fused_adamw(slip_ctx* c, int32_t enable) {
+  SLIP_CHECK(c, SLIP_EINVAL, "set_fused_adamw: ctx is NULL");
+  c->fuse_adamw = enable != 0;
   return SLIP_OK;
 }
 

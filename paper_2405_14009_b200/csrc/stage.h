@@ -8,6 +8,7 @@
 #include <vector>
 
 #include "../../include/slip.h"
+#include "gemm.cuh"
 #include "kernels.cuh"
 
 namespace slip {
@@ -108,6 +109,7 @@ struct slip_ctx {
   cudaStream_t fwd = nullptr;  // executor, dual stream: the forward actions' stream (lowest priority)
   cudaStream_t bwd = nullptr;  // executor, dual stream: every other compute action (highest priority)
   int dual_stream = -1;        // slip_set_dual_stream (-1: the SLIP_DUAL_STREAM environment default)
+  bool fuse_adamw = false;     // slip_set_fused_adamw: AdamW of the 2-D weights in the last W's epilogue
   int64_t opt_step = 0;  // AdamW steps taken by the executor
   bool trace_on = false;
   bool validate = false;   // post-step validation + cross-stage rollback (slip_set_validation)
@@ -123,15 +125,23 @@ size_t stash_bytes_per_slot(const Dims& d, int L);
 EndOffsets end_offsets(const Dims& d, int64_t base);
 size_t workspace_bytes(const Dims& d);
 
-// The W of n (2..8) B-done slots in ONE grouped launch: every dW accumulates the n
-// micro-batches' products in TMEM (K = n*T) and is written (or added) once.  Releases
-// the slots.
-slip_status weight_multi(slip_ctx* c, const int* slots, int n, int accumulate, cudaStream_t s);
+// The W of n (1..8) B-done slots in ONE grouped launch: every dW accumulates the n
+// micro-batches' products in TMEM (K = n*T) and is written (or added) once — or, with
+// `adam` (the iteration's last W of a stage without an all-reduce), goes straight into
+// AdamW in the epilogue (EPI_ADAMW; the 2-D weights only, the rest is left to the OPT).
+// Releases the slots.
+slip_status weight_multi(slip_ctx* c, const int* slots, int n, int accumulate, cudaStream_t s,
+                         const AdamEpi* adam = nullptr);
 // Local validation and the step if valid: own = non-finite gradient | injected fault | any
 // of the n_pre preceding stages' flags (device int32 each); AdamW skips when own is set,
 // and vflags[5] counts the skip.
 slip_status validated_step(slip_ctx* c, const slip_adam* a, int64_t step, float grad_scale, int32_t* own, int fault,
                            cudaStream_t s, const int32_t* pre_flags = nullptr, int n_pre = 0);
+// The AdamW state / constants for the fused W epilogue (EPI_ADAMW) of step `step`, and
+// the OPT that then remains: AdamW over the layers' 1-D parameters only.
+AdamEpi adam_epilogue_args(slip_ctx* c, const slip_adam* a, int64_t step, float grad_scale);
+slip_status optimizer_step_vectors(slip_ctx* c, const slip_adam* a, int64_t step, float grad_scale,
+                                   int32_t* d_nonfinite, cudaStream_t st);
 // slip_optimizer_step with the DP peer's gradient added in (peer_grad peer-mapped, or
 // NULL): the DP = 2 all-reduce fused into AdamW (slip_comm_fuse_ar_adam).
 slip_status optimizer_step_peer(slip_ctx* c, const slip_adam* a, int64_t step, float grad_scale, int32_t* d_nonfinite,

@@ -389,3 +389,36 @@ def test_execute_schedule_gpt_ends_n1_matches_oracle():
         assert relerr(ge[n], ref_e[n]) <= GATE_A, n
     comm.close()
     st.close()
+
+
+@pytest.mark.parametrize("name", list(EXEC_CFGS))
+def test_fused_adamw_in_w_epilogue_equals_separate_step(name):
+    """slip_set_fused_adamw: the iteration's last W applies AdamW to the 2-D weights in its
+    epilogue (the OPT then steps the 1-D parameters only).  Two iterations at N = 1 must
+    leave master, m, v and the bf16 weights identical to the separate optimizer pass (the
+    same per-element arithmetic, adamw_math.cuh, on the same fp32 gradient values)."""
+    rt = _rt()
+    cfg, L = EXEC_CFGS[name]
+    m = 4
+    layers = sd.stage_params(cfg, 0, L, total_layers=max(L, 2))
+    costs = rt.make_costs(t_f=1, t_b=1, t_w=1, t_comm=0, t_ar=1, t_opt=1)
+    _, need = rt.rank_program(1, 1, m, None, costs, 0)
+    out = []
+    for fused in (False, True):
+        st = rt.Stage(cfg, L, n_slots=need)
+        st.load_master(torch.from_numpy(sd.pack_stage(layers)).float().cuda())
+        rt.call("slip_set_fused_adamw", st.ctx, int(fused))
+        comm = rt.Comm(0, 1)
+        comm.setup(1, 1, m, None)
+        io = rt.make_io([host_bf16(sd.stage_input(cfg, 0, j)) for j in range(m)],
+                        [host_bf16(sd.stage_target(cfg, 0, j)) for j in range(m)], torch.zeros(m))
+        for _ in range(2):
+            rep = rt.execute_schedule(st, comm, 1, 1, m, None, costs, adam=(1e-3, 0.9, 0.95, 1e-8, 0.1),
+                                      iterations=1, io=io)
+            assert rep.nonfinite == 0
+        torch.cuda.synchronize()
+        out.append([st.master.clone(), st.adam_m.clone(), st.adam_v.clone(), st.w.clone()])
+        comm.close()
+        st.close()
+    for a, b, what in zip(out[0], out[1], ("master", "m", "v", "w")):
+        assert torch.equal(a, b), (what, ((a.float() - b.float()).abs().max() / a.float().abs().max()).item())
