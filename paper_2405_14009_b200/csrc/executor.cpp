@@ -79,6 +79,15 @@ struct ExecCache {
 };
 std::map<std::pair<const slip_ctx*, int>, ExecCache> exec_cache_;
 
+// CUDA events of a context's calls, reused from call to call (every call ends synchronized,
+// so all of them have completed): creating ~1000 events per call cost host time at the
+// start of every step of the end-to-end loop, while the GPU idled
+struct CallEvents {
+  EventPool<false> pool;
+  EventPool<true> tpool;
+};
+std::map<const slip_ctx*, CallEvents> call_events_;
+
 }  // namespace
 
 extern "C" slip_status slip_execute_schedule(slip_ctx* ctx, slip_comm* comm, const slip_cluster* cluster,
@@ -129,8 +138,11 @@ extern "C" slip_status slip_execute_schedule(slip_ctx* ctx, slip_comm* comm, con
   SLIP_CHECK(!fused_ar || comm->fused_local == ctx->grad, SLIP_ESTATE,
              "execute: gradient buffer re-bound since slip_comm_fuse_ar_adam");
 
-  EventPool<false> pool;
-  EventPool<true> tpool;
+  CallEvents& ce = call_events_[ctx];
+  EventPool<false>& pool = ce.pool;
+  EventPool<true>& tpool = ce.tpool;
+  pool.next = 0;
+  tpool.next = 0;
   cudaEvent_t t0 = nullptr, t1 = nullptr;
   SLIP_CUDA(tpool.get(&t0));
   SLIP_CUDA(tpool.get(&t1));
@@ -675,6 +687,14 @@ extern "C" slip_status slip_execute_schedule(slip_ctx* ctx, slip_comm* comm, con
   }
   return SLIP_OK;
 }
+
+namespace slip {
+// the executor's per-context caches (plans, rank programs, events), dropped with the context
+void executor_forget(const slip_ctx* ctx) {
+  call_events_.erase(ctx);
+  for (int run = 0; run < 2; ++run) exec_cache_.erase({ctx, run});
+}
+}  // namespace slip
 
 extern "C" slip_status slip_set_dual_stream(slip_ctx* ctx, int32_t enable) {
   SLIP_CHECK(ctx, SLIP_EINVAL, "set_dual_stream: ctx is NULL");

@@ -562,6 +562,7 @@ slip_status slip_ctx_create(slip_ctx** out, const slip_model* m, int32_t n_layer
 }
 
 slip_status slip_ctx_destroy(slip_ctx* ctx) {
+  slip::executor_forget(ctx);
   if (ctx && ctx->h2d) cudaStreamDestroy(ctx->h2d);
   if (ctx && ctx->fwd) cudaStreamDestroy(ctx->fwd);
   if (ctx && ctx->bwd) cudaStreamDestroy(ctx->bwd);

@@ -139,6 +139,8 @@ slip_status validated_step(slip_ctx* c, const slip_adam* a, int64_t step, float 
                            cudaStream_t s, const int32_t* pre_flags = nullptr, int n_pre = 0);
 // The AdamW state / constants for the fused W epilogue (EPI_ADAMW) of step `step`, and
 // the OPT that then remains: AdamW over the layers' 1-D parameters only.
+// drop the executor's caches of a context (slip_ctx_destroy)
+void executor_forget(const slip_ctx* ctx);
 AdamEpi adam_epilogue_args(slip_ctx* c, const slip_adam* a, int64_t step, float grad_scale);
 slip_status optimizer_step_vectors(slip_ctx* c, const slip_adam* a, int64_t step, float grad_scale,
                                    int32_t* d_nonfinite, cudaStream_t st);
