@@ -320,7 +320,7 @@ def main():
     ok = True
     holder = {}
 
-    def run(live):
+    def run(live, fused_adamw=False):
         # a fresh stage per scenario: the AdamW step count is part of the training state,
         # and a rank masked in an earlier scenario skipped that scenario's OPT
         if "stage" in holder:
@@ -328,6 +328,7 @@ def main():
         stage = holder["stage"] = rt.Stage(cfg, L, n_slots=2 * m * DP)
         rt.init_master_(stage.master, cfg, L, cfg.layers, seed=100 + me_i)
         rt.call("slip_weights_from_master", stage.ctx, rt._stream())
+        rt.call("slip_set_fused_adamw", stage.ctx, int(fused_adamw))
         comm.setup(PP, DP, m, live)
         losses = torch.zeros(DP * m, dtype=torch.float32).pin_memory()
         g = torch.Generator().manual_seed(5)
@@ -366,9 +367,14 @@ def main():
         if not rt.recoverable(PP, DP, live):
             continue
         rep, g1, p1, l1 = run(live)
+        # AdamW in the last W's epilogue where no all-reduce follows (the survivor of a
+        # failed DP = 2 group, DP = 1 stages): the same weights, bit for bit
+        _, _, p1f, _ = run(live, fused_adamw=True)
         me_live = live[me_i][me_k] == 1
         res = {"failed": failed, "rank": rank}
         if me_live:
+            res["fused_adamw_bit_identical"] = bool(torch.equal(p1, p1f))
+            ok &= res["fused_adamw_bit_identical"]
             gerr = ((g1 - g0).abs().max() / g0.abs().max()).item()
             res["grad_relerr"] = gerr
             ok &= gerr <= 1e-4
