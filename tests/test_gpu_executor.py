@@ -422,3 +422,37 @@ def test_fused_adamw_in_w_epilogue_equals_separate_step(name):
         st.close()
     for a, b, what in zip(out[0], out[1], ("master", "m", "v", "w")):
         assert torch.equal(a, b), (what, ((a.float() - b.float()).abs().max() / a.float().abs().max()).item())
+
+
+@pytest.mark.parametrize("name", list(EXEC_CFGS))
+def test_dual_stream_equals_single_stream(name):
+    """slip_set_dual_stream at N = 1: the forwards run on their own (low-priority) stream,
+    ordered by events after the W that frees their slot and the OPT that wrote their
+    weights.  Three iterations in ONE call (the streams overlap across iterations) must
+    leave the gradient, master, m, v and the bf16 weights identical to the single-stream
+    run: a forward that read weights before the optimizer step finished, or a slot's stash
+    before its W had consumed it, would change them."""
+    rt = _rt()
+    cfg, L = EXEC_CFGS[name]
+    m = 4
+    layers = sd.stage_params(cfg, 0, L, total_layers=max(L, 2))
+    costs = rt.make_costs(t_f=1, t_b=1, t_w=1, t_comm=0, t_ar=1, t_opt=1)
+    _, need = rt.rank_program(1, 1, m, None, costs, 0)
+    out = []
+    for dual in (False, True):
+        st = rt.Stage(cfg, L, n_slots=need)
+        st.load_master(torch.from_numpy(sd.pack_stage(layers)).float().cuda())
+        rt.call("slip_set_dual_stream", st.ctx, int(dual))
+        comm = rt.Comm(0, 1)
+        comm.setup(1, 1, m, None)
+        io = rt.make_io([host_bf16(sd.stage_input(cfg, 0, j)) for j in range(m)],
+                        [host_bf16(sd.stage_target(cfg, 0, j)) for j in range(m)], torch.zeros(m))
+        rep = rt.execute_schedule(st, comm, 1, 1, m, None, costs, adam=(1e-3, 0.9, 0.95, 1e-8, 0.1),
+                                  iterations=3, io=io)
+        torch.cuda.synchronize()
+        assert rep.nonfinite == 0
+        out.append([st.grad.clone(), st.master.clone(), st.adam_m.clone(), st.adam_v.clone(), st.w.clone()])
+        comm.close()
+        st.close()
+    for a, b, what in zip(out[0], out[1], ("grad", "master", "m", "v", "w")):
+        assert torch.equal(a, b), (what, ((a.float() - b.float()).abs().max() / a.float().abs().max()).item())
