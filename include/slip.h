@@ -398,6 +398,16 @@ slip_status slip_grad_allreduce(slip_ctx* ctx, slip_comm* comm, slip_stream s);
  * stage or re-running slip_comm_setup (which unmaps). */
 slip_status slip_comm_fuse_ar_adam(slip_ctx* ctx, slip_comm* comm, int32_t enable);
 
+/* The compute half of slip_comm_fuse_ar_adam for a caller that maps the peer's
+ * gradient itself (e.g. one process driving both GPUs of a DP = 2 group with peer
+ * access enabled): slip_optimizer_step on g_own + peer_grad[i] (the same fp32 sum
+ * on both replicas), peer_grad a device pointer readable from this GPU (peer or
+ * IPC mapping, the peer's whole n_params fp32 gradient; NULL = plain
+ * slip_optimizer_step).  No barrier: the caller orders the peer's gradient before
+ * and its next write after (as the executor's two flag barriers do). */
+slip_status slip_optimizer_step_peer(slip_ctx* ctx, const slip_adam* a, int64_t step, float grad_scale,
+                                     int32_t* d_nonfinite, const float* peer_grad, slip_stream s);
+
 /* ------------------------------------------------------------- rank programs
  * The executor interprets a per-rank program derived from the plan (host
  * logic only, no GPU): for every op of worker (i, k) in planned order, the

@@ -121,6 +121,7 @@ SIGNATURES = {
     "slip_backward_weight_multi": (C.c_int, [P, P, I32, I32, P]),
     "slip_backward_coupled": (C.c_int, [P, I32, P, P, I32, P]),
     "slip_optimizer_step": (C.c_int, [P, C.POINTER(slip_adam), I64, F32, P, P]),
+    "slip_optimizer_step_peer": (C.c_int, [P, C.POINTER(slip_adam), I64, F32, P, P, P]),
     "slip_loss_mse": (C.c_int, [P, P, P, P, P, P]),
     "slip_synth_normal": (C.c_int, [P, I64, U64, U64, U64, P]),
     "slip_weights_from_master": (C.c_int, [P, P]),

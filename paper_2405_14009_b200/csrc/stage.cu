@@ -747,6 +747,11 @@ slip_status slip_optimizer_step(slip_ctx* c, const slip_adam* a, int64_t step, f
   return slip::optimizer_step_peer(c, a, step, grad_scale, d_nonfinite, st, nullptr);
 }
 
+slip_status slip_optimizer_step_peer(slip_ctx* c, const slip_adam* a, int64_t step, float grad_scale,
+                                     int32_t* d_nonfinite, const float* peer_grad, slip_stream st) {
+  return slip::optimizer_step_peer(c, a, step, grad_scale, d_nonfinite, st, peer_grad);
+}
+
 }  // extern "C"
 
 AdamEpi slip::adam_epilogue_args(slip_ctx* c, const slip_adam* a, int64_t step, float grad_scale) {
