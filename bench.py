@@ -50,6 +50,8 @@ def parse():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="slip", choices=["slip", "reference"])
     ap.add_argument("--failures", type=int, default=0)
+    ap.add_argument("--dp", type=int, default=0,
+                    help="data-parallel pipelines (default: 1 on one GPU, else 2; PP = world / DP)")
     ap.add_argument("--microbatches", "--m", dest="m", type=int, default=0, help="micro-batches per pipeline (default 4*PP)")
     ap.add_argument("--layers", type=int, default=None, help="total layers (default: the model's)")
     ap.add_argument("--coupled", action="store_true", help="coupled backward, no staggering (1F1B baseline)")
@@ -226,9 +228,10 @@ def main():
     torch.cuda.set_device(local)
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    DP = 1 if world == 1 else 2
+    DP = args.dp or (1 if world == 1 else 2)
     PP = world // DP
-    assert DP * PP == world and args.layers % PP == 0
+    if DP * PP != world or args.layers % PP:
+        raise SystemExit(f"--dp {DP}: WORLD_SIZE {world} must be DP x PP with PP dividing {args.layers} layers")
     L = args.layers // PP
     m = args.m or 4 * PP
     me_stage = rank % PP
