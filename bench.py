@@ -73,7 +73,7 @@ def parse():
                     help="AdamW of the 2-D weights in the last W's epilogue where no all-reduce follows "
                          "(measured slower under the 1 kW power cap: off by default)")
     ap.add_argument("--dual-stream", default="auto", choices=["auto", "on", "off"],
-                    help="forward actions on their own stream after profiling (auto: when PP = 1)")
+                    help="forward actions on their own stream after profiling (auto: PP = 1 or m >= 4 PP)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--model", default="1.3b", choices=sorted(MODELS), help="GPT shape (default: BASELINE configs[1])")
@@ -411,12 +411,13 @@ def main():
                 "cost_table_10us": {"%d,%d" % ix: v for ix, v in tab.items()},
                 "normalized_failed": [(i, k) for i in range(PP) for k in range(DP) if not live[i][k]]}
         failed = norm["normalized_failed"]
-    # the profiled costs above came from single-stream execution; with one pipeline stage
-    # (PP = 1) the timed steps run the forward actions on their own stream
-    # (slip_set_dual_stream: same plan, same results; measured +1-2.8 % at N = 1).  With
-    # PP > 1 the overlapping forward competes with the backward chain across the stages,
-    # which is the critical path at small m (DP2xPP2 m = 2: 321k -> 301k), so it stays off.
-    dual = args.dual_stream == "on" or (args.dual_stream == "auto" and PP == 1)
+    # the profiled costs above came from single-stream execution; the timed steps run the
+    # forward actions on their own stream (slip_set_dual_stream: same plan, same results)
+    # with one pipeline stage (measured +1-2.8 % at N = 1) and with PP > 1 at m >= 4 PP
+    # (the default: DP2xPP2 m = 8 399.0k -> 407.8k, DP1xPP4 m = 16 384.0k -> 389.1k).  At
+    # small m the overlapping forward competes with the backward chain across the stages,
+    # the critical path there (DP2xPP2 m = 2: 321k -> 301k), so it stays off.
+    dual = args.dual_stream == "on" or (args.dual_stream == "auto" and (PP == 1 or m >= 4 * PP))
     rt.call("slip_set_dual_stream", stage.ctx, int(dual))
     # AdamW of the 2-D weights in the epilogue of the iteration's last W where no all-reduce
     # follows (N = 1; the survivor of a failed DP = 2 group) — slip_set_fused_adamw
