@@ -139,9 +139,10 @@ class ClockSampler:
 
 
 # ---------------------------------------------------------------- oracle (CPU baseline)
-def oracle_sample(layers_total, m):
+def oracle_sample(layers_total, m, dp=1):
     """fp64 oracle on the host: one GPT-1.3B-shaped layer x one micro-batch of F + B + W
-    plus AdamW over one layer's parameters; extrapolated to layers_total x m."""
+    plus AdamW over one layer's parameters; extrapolated to the job: dp pipelines of
+    layers_total layers x m micro-batches, each replica taking its AdamW step."""
     import numpy as np
 
     import slipdata as sd
@@ -161,8 +162,8 @@ def oracle_sample(layers_total, m):
     OA.adamw_step_layer(P, z, z, grads, 1, OA.AdamCfg(), grad_scale=1.0 / m)
     t2 = time.perf_counter()
     t_layer, t_adam = t1 - t0, t2 - t1
-    step_s = layers_total * (m * t_layer + t_adam)
-    tokens = m * MB * SEQ
+    step_s = dp * layers_total * (m * t_layer + t_adam)
+    tokens = dp * m * MB * SEQ
     return tokens / step_s, t_layer, t_adam
 
 
@@ -177,33 +178,38 @@ def run_reference(args, rank, world):
     """--impl reference: the fp64 oracle, as it stands, on the host cores (rank 0 only)."""
     if rank != 0:
         return
-    m = args.m or 4
+    # the GPU arm's workload at this N (same DP x PP split and micro-batch count)
+    DP = args.dp or (1 if args.gpus == 1 else 2)
+    PP = max(1, args.gpus // DP)
+    m = args.m or 4 * PP
     vals = []
     samples = []
     for step in range(args.warmup + args.steps):
-        v, tl, ta = oracle_sample(args.layers, m)
+        v, tl, ta = oracle_sample(args.layers, m, DP)
         if step >= args.warmup:
             vals.append(v)
             samples.append(tl + ta)
     value = statistics.median(vals)
-    ms = 1000.0 * (m * MB * SEQ) / value
+    ms = 1000.0 * (DP * m * MB * SEQ) / value
     cores = cpu_cores()
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
         # each step times a bounded sample; the full step is extrapolated from it
-        "ms_per_step_kind": "extrapolated from the per-step sample (%d layers x %d micro-batches); "
-                            "measured sample time per step %.0f ms" % (args.layers, m,
-                                                                      1000.0 * statistics.median(samples)),
+        "ms_per_step_kind": "extrapolated from the per-step sample (%d pipeline(s) x %d layers x %d micro-batches);"
+                            " measured sample time per step %.0f ms" % (DP, args.layers, m,
+                                                                       1000.0 * statistics.median(samples)),
         "sample_ms_per_step": 1000.0 * statistics.median(samples),
         "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": "gpt-%s-shape (h%d s%d %d heads ffn%d) %d layers, m=%d, DP1xPP1" % (
-            MODEL, H, SEQ, HEADS, FFN, args.layers, m), "model": "gpt-%s-shape" % MODEL, "global_batch": m * MB, "seq_len": SEQ,
-            "parallelism": "host"},
+        "config": {"workload": "gpt-%s-shape (h%d s%d %d heads ffn%d) %d layers, DP%dxPP%d, m=%d micro-batches/pipeline,"
+                               " failures=0" % (MODEL, H, SEQ, HEADS, FFN, args.layers, DP, PP, m),
+                   "model": "gpt-%s-shape" % MODEL, "global_batch": DP * m * MB, "seq_len": SEQ,
+                   "parallelism": "dp%dxpp%d (the fp64 oracle on the host cores)" % (DP, PP)},
         "cpu_baseline": {"value": value, "unit": "tokens/s", "cores": cores, "kind": "oracle",
                          "sample": "per step: 1 layer x 1 micro-batch F+B+W (T=2048, h=2048) + AdamW over 1 layer,"
-                                   " fp64 numpy, extrapolated to %d layers x %d micro-batches" % (args.layers, m)},
+                                   " fp64 numpy, extrapolated to %d pipeline(s) x %d layers x %d micro-batches"
+                                   % (DP, args.layers, m)},
         "e2e": {"value": value, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
