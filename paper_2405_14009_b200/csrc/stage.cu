@@ -442,6 +442,19 @@ std::vector<GemmDesc> w_problems(slip_ctx* c, int slot) {
 }
 
 // W as ONE persistent grouped launch over all 4L products of the slot (tables encoded at bind).
+
+// dE, dP of the embedding end from the stage-input gradient of one slot.  The scatter
+// writes only the rows of the tokens present, so the first W of an iteration (accumulate
+// = 0, overwrite) clears dE and dP first: rows of tokens absent from this micro-batch must
+// not keep the previous iteration's (all-reduced) gradient.
+slip_status embedding_grad(slip_ctx* c, SlotBufs& sb, int accumulate, cudaStream_t s) {
+  const Dims& D = c->dm;
+  if (!accumulate)
+    SLIP_CUDA(cudaMemsetAsync(c->grad + c->eo.E, 0, (static_cast<size_t>(D.V) + D.s) * D.h * sizeof(float), s));
+  return kcheck(c, embed_bwd(sb.dx, sb.end.tokens, c->grad + c->eo.E, c->grad + c->eo.P, D.T, D.h, D.s, 1, s),
+                "embed_bwd");
+}
+
 slip_status backward_weight_impl(slip_ctx* c, int slot, int accumulate, cudaStream_t s) {
   SlotBufs& sb = c->slots[slot];
   GemmDesc proto;
@@ -457,10 +470,7 @@ slip_status backward_weight_impl(slip_ctx* c, int slot, int accumulate, cudaStre
   }
   c->launches += 1;
   if (c->dm.ends & 1)  // embedding scatter of the stage-input gradient B left in the slot
-    SLIP_TRY(kcheck(c,
-                    embed_bwd(sb.dx, sb.end.tokens, c->grad + c->eo.E, c->grad + c->eo.P, c->dm.T, c->dm.h, c->dm.s,
-                              accumulate, s),
-                    "embed_bwd"));
+    SLIP_TRY(embedding_grad(c, sb, accumulate, s));
   return SLIP_OK;
 }
 
@@ -708,10 +718,7 @@ slip_status weight_multi(slip_ctx* c, const int* slots, int n, int accumulate, c
   for (int j = 0; j < n; ++j) {
     SlotBufs& sb = c->slots[slots[j]];
     if (c->dm.ends & 1)  // embedding scatter of each slot's stage-input gradient
-      SLIP_TRY(kcheck(c,
-                      embed_bwd(sb.dx, sb.end.tokens, c->grad + c->eo.E, c->grad + c->eo.P, c->dm.T, c->dm.h, c->dm.s,
-                                accumulate || j > 0, s),
-                      "embed_bwd"));
+      SLIP_TRY(embedding_grad(c, sb, accumulate || j > 0, s));
     c->state[slots[j]] = SLOT_FREE;
   }
   return SLIP_OK;

@@ -1,7 +1,7 @@
 """Multi-GPU correctness of the executor (run under torchrun, one rank per GPU).
 
     torchrun --nproc-per-node 2 tests/dist_check.py --dp 2 --pp 1
-    torchrun --nproc-per-node 4 tests/dist_check.py --dp 2 --pp 2
+    torchrun --nproc-per-node 4 tests/dist_check.py --dp 2 --pp 2 [--gpt-ends]
 
 For a fault-free run and for every recoverable failure set given by --failures
 (masked ranks at the listed (stage, pipeline) positions) it runs one training
@@ -32,8 +32,16 @@ def peers_equal(t, me_live, me_stage, world):
     bytes are all-gathered (as int32 words) and compared with torch.equal.  Returns
     the list of comparisons made on this rank (empty when masked)."""
     words = t.contiguous().view(torch.int32)
-    allw = [torch.empty_like(words) for _ in range(world)]
-    dist.all_gather(allw, words)
+    # stages may differ in size (GPT ends): gather the sizes, then padded words
+    n = torch.tensor([float(words.numel())], dtype=torch.float64, device="cuda")
+    alln = [torch.zeros_like(n) for _ in range(world)]
+    dist.all_gather(alln, n)
+    nmax = int(max(x.item() for x in alln))
+    padded = torch.zeros(nmax, dtype=torch.int32, device="cuda")
+    padded[:words.numel()] = words
+    allp = [torch.empty_like(padded) for _ in range(world)]
+    dist.all_gather(allp, padded)
+    allw = [allp[r][:int(alln[r].item())] for r in range(world)]
     meta = torch.tensor([float(me_live), float(me_stage)], dtype=torch.float64, device="cuda")
     allm = [torch.zeros_like(meta) for _ in range(world)]
     dist.all_gather(allm, meta)
@@ -301,6 +309,8 @@ def main():
     ap.add_argument("--migrate", action="store_true", help="normalization swap scenario (PP >= 2)")
     ap.add_argument("--validate", action="store_true", help="post-step validation / rollback scenario (PP >= 2)")
     ap.add_argument("--fused-ar", action="store_true", help="DP=2 all-reduce fused into AdamW vs NCCL, bit-exact")
+    ap.add_argument("--gpt-ends", action="store_true",
+                    help="GPT ends: token + position embedding on stage 0, final LN + LM head + CE on the last stage")
     a = ap.parse_args()
     rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
     local = int(os.environ.get("LOCAL_RANK", rank))
@@ -308,9 +318,11 @@ def main():
     dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     DP, PP, m = a.dp, a.pp, a.m
     assert DP * PP == world
-    cfg = sd.ModelCfg(hidden=256, heads=4, ffn=1024, seq=256, micro_batch=1, layers=2 * PP)
-    L = 2
     me_i, me_k = rank % PP, rank // PP
+    vocab = 1024 if a.gpt_ends else 0
+    ends = ((1 if me_i == 0 else 0) | (2 if me_i == PP - 1 else 0)) if a.gpt_ends else 0
+    cfg = sd.ModelCfg(hidden=256, heads=4, ffn=1024, seq=256, micro_batch=1, layers=2 * PP, vocab=vocab, ends=ends)
+    L = 2
     if a.failures == "auto":
         scenarios = [[(PP - 1, 1)], [(0, 0)]] + ([[(PP - 1, 1), (0, 0)]] if PP > 1 else [])
     else:
@@ -332,8 +344,16 @@ def main():
         comm.setup(PP, DP, m, live)
         losses = torch.zeros(DP * m, dtype=torch.float32).pin_memory()
         g = torch.Generator().manual_seed(5)
-        xs = [torch.randn(cfg.tokens, cfg.hidden, generator=g).to(torch.bfloat16).pin_memory() for _ in range(DP * m)]
-        rs = [torch.randn(cfg.tokens, cfg.hidden, generator=g).to(torch.bfloat16).pin_memory() for _ in range(DP * m)]
+        if a.gpt_ends:  # token ids in, labels out (the same lists on every rank)
+            xs = [torch.randint(0, vocab, (cfg.tokens,), generator=g, dtype=torch.int32).pin_memory()
+                  for _ in range(DP * m)]
+            rs = [torch.randint(0, vocab, (cfg.tokens,), generator=g, dtype=torch.int32).pin_memory()
+                  for _ in range(DP * m)]
+        else:
+            xs = [torch.randn(cfg.tokens, cfg.hidden, generator=g).to(torch.bfloat16).pin_memory()
+                  for _ in range(DP * m)]
+            rs = [torch.randn(cfg.tokens, cfg.hidden, generator=g).to(torch.bfloat16).pin_memory()
+                  for _ in range(DP * m)]
         io = rt.make_io(xs, rs, losses)
         rep = rt.execute_schedule(stage, comm, PP, DP, m, live, costs, True, True, adam=(1e-3, 0.9, 0.95, 1e-8, 0.1),
                                   iterations=1, io=io)
@@ -390,6 +410,12 @@ def main():
         eq = peers_equal(p1, me_live, me_i, world)
         res["peer_weights_equal"] = eq
         ok &= all(eq)
+        bad = torch.tensor([0.0 if all(eq) else 1.0], device="cuda")
+        dist.all_reduce(bad)
+        if bad.item() > 0:  # diagnosis (collective on every rank): the summed gradient, the layers
+            res["peer_grads_equal"] = peers_equal(g1, me_live, me_i, world)
+            nl = rt.param_offsets(cfg.hidden, cfg.ffn)["per_layer"] * L
+            res["peer_layers_equal"] = peers_equal(p1[:nl].contiguous(), me_live, me_i, world)
         flag = torch.tensor([1.0 if ok else 0.0], device="cuda")
         dist.all_reduce(flag, op=dist.ReduceOp.MIN)
         outs = [None] * world

@@ -74,3 +74,18 @@ def test_dp2_fused_allreduce_adam():
 def test_dp2_pp2_fused_allreduce_adam():
     out = _run(4, 2, 2, "--fused-ar")
     assert '"scenario": "fused_ar"' in out and '"ok": false' not in out
+
+
+@pytest.mark.skipif(torch.cuda.device_count() < 2, reason="needs 2 GPUs")
+def test_dp2_pp1_reroute_gpt_ends():
+    """GPT ends (token + position embedding, final LN + LM head + cross-entropy) on the
+    single stage, DP = 2: re-routing leaves the CE losses bit-identical."""
+    out = _run(2, 2, 1, "--gpt-ends")
+    assert '"ok": true' in out and '"ok": false' not in out
+
+
+@pytest.mark.skipif(torch.cuda.device_count() < 4, reason="needs 4 GPUs")
+def test_dp2_pp2_reroute_gpt_ends():
+    """Embedding on stage 0, LM head + CE on stage 1, DP2 x PP2 with re-routing."""
+    out = _run(4, 2, 2, "--gpt-ends")
+    assert '"ok": true' in out and '"ok": false' not in out

@@ -345,9 +345,9 @@ def test_execute_schedule_gpt_ends_n1_matches_oracle():
     """The executor with both GPT ends on one stage (reading R33): token ids and labels
     from host buffers, embedding, layers, final LN + LM head + cross-entropy, B, the merged
     W (dW_out in the grouped launch, the embedding scatter) over m = 3 micro-batches:
-    summed gradients per tensor vs oracle/ends.py + oracle/layer.py (Gate A), losses to 1e-2."""
-    from oracle import ends as OE
-    from oracle import layer as OL
+    summed gradients per tensor vs oracle/ends.py + oracle/layer.py (Gate A), losses to 1e-2,
+    after each of two calls (the second starts from the first's gradient buffer: rows of
+    the embedding gradient that no micro-batch of the iteration touches must be zero)."""
     rt = _rt()
     cfg = sd.ModelCfg(hidden=128, heads=2, ffn=512, seq=64, micro_batch=2, layers=1, vocab=384, ends=3)
     L, m = 1, 3
@@ -364,8 +364,22 @@ def test_execute_schedule_gpt_ends_n1_matches_oracle():
     labs = [sd.stage_labels(cfg, 0, j) for j in range(m)]
     losses = torch.zeros(m)
     io = rt.make_io([torch.from_numpy(t.copy()) for t in toks], [torch.from_numpy(x.copy()) for x in labs], losses)
-    rt.execute_schedule(st, comm, 1, 1, m, None, costs, adam=(1e-3, 0.9, 0.95, 1e-8, 0.1), iterations=1, io=io)
-    torch.cuda.synchronize()
+    P = cfg.params_per_layer
+    for it in range(2):
+        # the weights this call's F / B use: RNE(master) = the bf16 copy
+        wflat = as_np(st.w)
+        layers = sd.unpack_stage(wflat[:L * P], cfg, L)
+        ends = sd.unpack_ends(wflat[L * P:], cfg)
+        rt.execute_schedule(st, comm, 1, 1, m, None, costs, adam=(1e-3, 0.9, 0.95, 1e-8, 0.1), iterations=1, io=io)
+        torch.cuda.synchronize()
+        _check_gpt_ends_grads(st, cfg, L, m, layers, ends, toks, labs, losses, it)
+    comm.close()
+    st.close()
+
+
+def _check_gpt_ends_grads(st, cfg, L, m, layers, ends, toks, labs, losses, it):
+    from oracle import ends as OE
+    from oracle import layer as OL
     ref_l, ref_e = None, None
     for j in range(m):
         x0 = OE.embed_fwd(ends["E"], ends["P"], toks[j], cfg.seq)
@@ -383,12 +397,15 @@ def test_execute_schedule_gpt_ends_n1_matches_oracle():
     got = sd.unpack_stage(gflat[:L * P], cfg, L)
     for l in range(L):
         for n in sd.PARAM_ORDER:
-            assert relerr(got[l][n], ref_l[l][n]) <= GATE_A, (l, n)
+            assert relerr(got[l][n], ref_l[l][n]) <= GATE_A, (it, l, n)
     ge = sd.unpack_ends(gflat[L * P:], cfg)
     for n in ("E", "P", "gf", "bf", "Wout"):
-        assert relerr(ge[n], ref_e[n]) <= GATE_A, n
-    comm.close()
-    st.close()
+        assert relerr(ge[n], ref_e[n]) <= GATE_A, (it, n)
+    # rows of E no micro-batch of the iteration used: exactly zero
+    used = np.zeros(cfg.vocab, dtype=bool)
+    for t in toks:
+        used[np.asarray(t).reshape(-1)] = True
+    assert not np.any(ge["E"][~used]), it
 
 
 @pytest.mark.parametrize("name", list(EXEC_CFGS))
