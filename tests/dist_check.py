@@ -51,6 +51,27 @@ def peers_equal(t, me_live, me_stage, world):
             if allm[r][0].item() == 1.0 and int(allm[r][1].item()) == me_stage]
 
 
+def stage_sum(t, me_live, me_stage, world):
+    """Sum of `t` over the live ranks of my stage (rank order): with the fused DP = 2
+    all-reduce each peer keeps its own un-summed gradient, so the stage gradient is the
+    sum over the peers (a singleton's own gradient already is it)."""
+    n = torch.tensor([float(t.numel()), float(me_live), float(me_stage)], dtype=torch.float64, device="cuda")
+    alln = [torch.zeros_like(n) for _ in range(world)]
+    dist.all_gather(alln, n)
+    nmax = int(max(x[0].item() for x in alln))
+    padded = torch.zeros(nmax, dtype=t.dtype, device="cuda")
+    padded[:t.numel()] = t.reshape(-1)
+    allp = [torch.empty_like(padded) for _ in range(world)]
+    dist.all_gather(allp, padded)
+    if not me_live:
+        return t
+    tot = torch.zeros_like(t.reshape(-1))
+    for r in range(world):
+        if alln[r][1].item() == 1.0 and int(alln[r][2].item()) == me_stage:
+            tot += allp[r][:t.numel()]
+    return tot.reshape(t.shape)
+
+
 def migrate_scenario(a, cfg, L, comm, costs, rank, world, holder):
     """Normalization swap on real GPUs (§4.2.1): one fault-free
     iteration; then worker (0, 0) fails; the planner's Algorithm 1 target is taken as
@@ -309,6 +330,11 @@ def main():
     ap.add_argument("--migrate", action="store_true", help="normalization swap scenario (PP >= 2)")
     ap.add_argument("--validate", action="store_true", help="post-step validation / rollback scenario (PP >= 2)")
     ap.add_argument("--fused-ar", action="store_true", help="DP=2 all-reduce fused into AdamW vs NCCL, bit-exact")
+    ap.add_argument("--iters", type=int, default=1,
+                    help="iterations per run: > 1 checks the replicas stay byte-identical over the steps "
+                         "(losses then compared to the fault-free run within 1e-3, gradients within 1e-2)")
+    ap.add_argument("--fuse-ar-main", action="store_true",
+                    help="the re-route scenarios with the DP = 2 all-reduce fused into AdamW (the bench default)")
     ap.add_argument("--gpt-ends", action="store_true",
                     help="GPT ends: token + position embedding on stage 0, final LN + LM head + CE on the last stage")
     a = ap.parse_args()
@@ -342,6 +368,8 @@ def main():
         rt.call("slip_weights_from_master", stage.ctx, rt._stream())
         rt.call("slip_set_fused_adamw", stage.ctx, int(fused_adamw))
         comm.setup(PP, DP, m, live)
+        if a.fuse_ar_main:
+            rt.fuse_ar_adam(stage, comm)
         losses = torch.zeros(DP * m, dtype=torch.float32).pin_memory()
         g = torch.Generator().manual_seed(5)
         if a.gpt_ends:  # token ids in, labels out (the same lists on every rank)
@@ -356,7 +384,7 @@ def main():
                   for _ in range(DP * m)]
         io = rt.make_io(xs, rs, losses)
         rep = rt.execute_schedule(stage, comm, PP, DP, m, live, costs, True, True, adam=(1e-3, 0.9, 0.95, 1e-8, 0.1),
-                                  iterations=1, io=io)
+                                  iterations=a.iters, io=io)
         torch.cuda.synchronize()
         return rep, stage.grad.clone(), stage.master.clone(), losses.clone()
 
@@ -370,6 +398,8 @@ def main():
 
     live0 = [[1] * DP for _ in range(PP)]
     rep0, g0, p0, l0 = run(live0)
+    if a.fuse_ar_main:  # the fused all-reduce leaves each peer's own gradient un-summed
+        g0 = stage_sum(g0, True, me_i, world)
     # every micro-batch's fault-free loss (each entry is written by exactly one last-stage rank)
     l0c = l0.cuda()
     dist.all_reduce(l0c)
@@ -387,6 +417,8 @@ def main():
         if not rt.recoverable(PP, DP, live):
             continue
         rep, g1, p1, l1 = run(live)
+        if a.fuse_ar_main:
+            g1 = stage_sum(g1, live[me_i][me_k] == 1, me_i, world)
         # AdamW in the last W's epilogue where no all-reduce follows (the survivor of a
         # failed DP = 2 group, DP = 1 stages): the same weights, bit for bit
         _, _, p1f, _ = run(live, fused_adamw=True)
@@ -397,15 +429,19 @@ def main():
             ok &= res["fused_adamw_bit_identical"]
             gerr = ((g1 - g0).abs().max() / g0.abs().max()).item()
             res["grad_relerr"] = gerr
-            ok &= gerr <= 1e-4
+            # one iteration: only the fp32 summation order moves; more: the (equally valid)
+            # weights the re-routed run reached after the earlier steps differ slightly
+            ok &= gerr <= (1e-4 if a.iters == 1 else 1e-2)
             if me_i == PP - 1:
                 # losses of micro-batches whose last stage ran here; compare bitwise
                 ex = rt.assign(PP, DP, m, live)
                 for k in range(DP):
                     for j in range(m):
                         if ex[(PP - 1, j, k)] == me_k:
-                            ok &= bool(l1[k * m + j] == l0[k * m + j])
-                            res.setdefault("loss_equal", []).append(bool(l1[k * m + j] == l0[k * m + j]))
+                            same = bool(l1[k * m + j] == l0[k * m + j]) if a.iters == 1 else \
+                                abs(float(l1[k * m + j]) - float(l0[k * m + j])) <= 1e-3 * abs(float(l0[k * m + j]))
+                            ok &= same
+                            res.setdefault("loss_equal", []).append(same)
         # peers of a stage hold bit-identical fp32 master weights after the step
         eq = peers_equal(p1, me_live, me_i, world)
         res["peer_weights_equal"] = eq

@@ -89,3 +89,20 @@ def test_dp2_pp2_reroute_gpt_ends():
     """Embedding on stage 0, LM head + CE on stage 1, DP2 x PP2 with re-routing."""
     out = _run(4, 2, 2, "--gpt-ends")
     assert '"ok": true' in out and '"ok": false' not in out
+
+
+@pytest.mark.skipif(torch.cuda.device_count() < 2, reason="needs 2 GPUs")
+def test_dp2_pp1_reroute_three_iterations_fused_allreduce():
+    """Three iterations per run with the fused DP = 2 all-reduce + AdamW (the bench's
+    default): the replicas stay byte-identical step after step, fault-free and re-routed."""
+    out = _run(2, 2, 1, "--iters", "3", "--fuse-ar-main")
+    assert '"ok": true' in out and '"ok": false' not in out
+
+
+@pytest.mark.skipif(torch.cuda.device_count() < 4, reason="needs 4 GPUs")
+def test_dp2_pp2_reroute_three_iterations_fused_allreduce():
+    """DP2 x PP2, three iterations per run, fused all-reduce where a stage has two live
+    peers and plain AdamW where its peer failed: replicas byte-identical after the steps,
+    losses within 1e-3 and the stage gradient within 1e-2 of the fault-free run."""
+    out = _run(4, 2, 2, "--iters", "3", "--fuse-ar-main")
+    assert '"ok": true' in out and '"ok": false' not in out
