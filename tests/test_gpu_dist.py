@@ -106,3 +106,18 @@ def test_dp2_pp2_reroute_three_iterations_fused_allreduce():
     losses within 1e-3 and the stage gradient within 1e-2 of the fault-free run."""
     out = _run(4, 2, 2, "--iters", "3", "--fuse-ar-main")
     assert '"ok": true' in out and '"ok": false' not in out
+
+
+@pytest.mark.skipif(torch.cuda.device_count() < 4, reason="needs 4 GPUs")
+def test_dp4_pp1_reroute_three_iterations():
+    """Four data-parallel replicas of one stage (NCCL all-reduce over the live peers),
+    one and two failed workers re-routed to the survivors, three iterations per run."""
+    out = _run(4, 4, 1, "--iters", "3")
+    assert '"ok": true' in out and '"ok": false' not in out
+
+
+@pytest.mark.skipif(torch.cuda.device_count() < 4, reason="needs 4 GPUs")
+def test_dp1_pp4_pipeline_gpt_ends_three_iterations():
+    """A four-stage pipeline (the N = 8 default's depth) with the GPT ends, three iterations."""
+    out = _run(4, 1, 4, "--gpt-ends", "--iters", "3")
+    assert '"ok": true' in out and '"ok": false' not in out
