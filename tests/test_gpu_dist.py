@@ -111,7 +111,7 @@ def test_dp2_pp2_reroute_three_iterations_fused_allreduce():
 @pytest.mark.skipif(torch.cuda.device_count() < 4, reason="needs 4 GPUs")
 def test_dp4_pp1_reroute_three_iterations():
     """Four data-parallel replicas of one stage (NCCL all-reduce over the live peers),
-    one and two failed workers re-routed to the survivors, three iterations per run."""
+    a failed worker (two placements) re-routed to the three survivors, three iterations per run."""
     out = _run(4, 4, 1, "--iters", "3")
     assert '"ok": true' in out and '"ok": false' not in out
 
