@@ -473,3 +473,35 @@ def test_dual_stream_equals_single_stream(name):
         st.close()
     for a, b, what in zip(out[0], out[1], ("grad", "master", "m", "v", "w")):
         assert torch.equal(a, b), (what, ((a.float() - b.float()).abs().max() / a.float().abs().max()).item())
+
+
+def test_dual_stream_with_gpt_ends_equals_single_stream():
+    """The dual compute stream with both GPT ends on the stage (embedding in F on the
+    forward stream; final LN + LM head + CE in LOSS on the backward stream): three
+    iterations in one call, gradient / master / m / v / weights / losses identical to the
+    single-stream run."""
+    rt = _rt()
+    cfg = sd.ModelCfg(hidden=128, heads=2, ffn=512, seq=64, micro_batch=2, layers=2, vocab=384, ends=3)
+    L, m = 2, 4
+    flat = np.concatenate([sd.pack_stage(sd.stage_params(cfg, 0, L, total_layers=2)), sd.pack_ends(sd.end_params(cfg, 0))])
+    costs = rt.make_costs(t_f=1, t_b=1, t_w=1, t_comm=0, t_ar=1, t_opt=1)
+    _, need = rt.rank_program(1, 1, m, None, costs, 0)
+    toks = [torch.from_numpy(sd.stage_tokens(cfg, 0, j).copy()) for j in range(m)]
+    labs = [torch.from_numpy(sd.stage_labels(cfg, 0, j).copy()) for j in range(m)]
+    out = []
+    for dual in (False, True):
+        st = rt.Stage(cfg, L, n_slots=need)
+        st.load_master(torch.from_numpy(flat).float().cuda())
+        rt.call("slip_set_dual_stream", st.ctx, int(dual))
+        comm = rt.Comm(0, 1)
+        comm.setup(1, 1, m, None)
+        losses = torch.zeros(m)
+        io = rt.make_io(toks, labs, losses)
+        rt.execute_schedule(st, comm, 1, 1, m, None, costs, adam=(1e-3, 0.9, 0.95, 1e-8, 0.1), iterations=3, io=io)
+        torch.cuda.synchronize()
+        out.append([st.grad.clone(), st.master.clone(), st.adam_m.clone(), st.adam_v.clone(), st.w.clone(),
+                    losses.clone()])
+        comm.close()
+        st.close()
+    for a, b, what in zip(out[0], out[1], ("grad", "master", "m", "v", "w", "losses")):
+        assert torch.equal(a, b), what
