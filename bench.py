@@ -391,6 +391,19 @@ def main():
             pairs.append((p_s, p_t))
             role[p_t], role[p_f] = w_f, w_t
 
+        # a process whose role moves to a stage of a different model (the GPT ends) binds
+        # that model first; the state copy then fills it (slip_migrate_state checks sizes)
+        new_stage = role[rank] % PP
+        new_ends = ((1 if new_stage == 0 else 0) | (2 if new_stage == PP - 1 else 0)) if args.gpt_ends else 0
+        if new_ends != ends:
+            ends = new_ends
+            cfg = sd.ModelCfg(hidden=H, heads=HEADS, ffn=FFN, seq=SEQ, micro_batch=MB, layers=args.layers,
+                              vocab=VOCAB if args.gpt_ends else 0, ends=ends)
+            stage.close()
+            stage = rt.Stage(cfg, L, n_slots)
+            rt.init_master_(stage.master, cfg, L, args.layers, seed=new_stage)
+            rt.call("slip_weights_from_master", stage.ctx, rt._stream())
+
         def migrate():
             barrier()
             g0, g1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)

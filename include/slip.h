@@ -77,7 +77,9 @@ typedef struct {
    * ends bit 0 = token + position embedding (first stage: the stage input is T
    * int32 token ids), bit 1 = final LayerNorm + LM head + cross-entropy (last
    * stage: slip_loss_ce replaces the MSE head).  vocab = padded vocabulary
-   * (multiple of 128, e.g. 50257 -> 50304); ignored when ends == 0. */
+   * (multiple of 128, e.g. 50257 -> 50304); ignored when ends == 0.  A token id
+   * outside [0, vocab) reads a zero token-embedding row and receives no gradient
+   * (no out-of-bounds access). */
   int32_t vocab, ends;
 } slip_model;
 
@@ -286,8 +288,10 @@ slip_status slip_loss_mse(slip_ctx* ctx, const void* y, const void* target, void
 slip_status slip_synth_normal(void* out_bf16, int64_t n, uint64_t seed, uint64_t k, uint64_t j, slip_stream s);
 
 /* Last stage with the LM head (model.ends bit 1): y = stage output [T, h], labels
- * = T int32 class ids (device) < vocab.  Final LayerNorm, logits = Y Wout^T, loss
- * = mean_t (lse_t - logits_t[label_t]) into *d_loss (device fp32), and the head's
+ * = T int32 class ids (device) < vocab; a label outside [0, vocab) marks an ignored
+ * token (loss term 0, no gradient; the mean still divides by T).  Final LayerNorm,
+ * logits = Y Wout^T, loss = mean_t (lse_t - logits_t[label_t]) into *d_loss (device
+ * fp32), and the head's
  * input gradients: dy = d loss / d y (may alias y), gf / bf gradients (B); dLogits
  * and Y stay in the slot's stash for W (dWout += dLogits^T Y in the slot's grouped
  * W launch).  The slot must hold a forward (F done).  accumulate as in B. */
@@ -371,8 +375,10 @@ slip_status slip_comm_set_role(slip_comm* comm, int32_t role);
  * GPU taking over).  The sender's AdamW step count travels with the state: the
  * receiver rebuilds its bf16 weights from the master copy and sets its step count
  * to the sender's (opt_step < 0) or to opt_step (>= 0, an explicit override).  Both
- * sides must call it; it synchronizes s before returning (migration is not on the
- * per-step path). */
+ * sides must call it, with contexts holding the same stage model (with GPT ends the
+ * receiver first binds the model of the role it takes over): the parameter counts
+ * are exchanged first and a mismatch returns SLIP_EINVAL on both sides.  It
+ * synchronizes s before returning (migration is not on the per-step path). */
 slip_status slip_migrate_state(slip_ctx* ctx, slip_comm* comm, int32_t peer, int32_t send, int64_t opt_step,
                                slip_stream s);
 

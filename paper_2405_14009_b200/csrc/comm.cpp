@@ -199,6 +199,28 @@ slip_status slip_migrate_state(slip_ctx* ctx, slip_comm* c, int32_t peer, int32_
   SLIP_CHECK(peer >= 0 && peer < c->world && peer != c->rank, SLIP_EINVAL, "migrate_state: bad peer rank");
   cudaStream_t st = reinterpret_cast<cudaStream_t>(s);
   const size_t n = static_cast<size_t>(ctx->n_params);
+  // both sides first exchange their parameter counts: a receiver whose context holds a
+  // different stage model (e.g. one without the sender's GPT end) fails on both sides
+  // instead of leaving mismatched transfers in flight
+  {
+    int64_t* d_n = nullptr;
+    SLIP_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&d_n), 2 * sizeof(int64_t), st));
+    const int64_t mine = ctx->n_params;
+    SLIP_CUDA(cudaMemcpyAsync(d_n, &mine, sizeof(int64_t), cudaMemcpyHostToDevice, st));
+    SLIP_NCCL(ncclGroupStart());
+    ncclResult_t r1 = ncclSend(d_n, 1, ncclInt64, peer, c->world_comm, st);
+    ncclResult_t r2 = ncclRecv(d_n + 1, 1, ncclInt64, peer, c->world_comm, st);
+    SLIP_NCCL(ncclGroupEnd());
+    if (r1 != ncclSuccess || r2 != ncclSuccess) return nccl_status(r1 != ncclSuccess ? r1 : r2, "migrate_state: sizes");
+    int64_t theirs = -1;
+    SLIP_CUDA(cudaMemcpyAsync(&theirs, d_n + 1, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+    SLIP_CUDA(cudaFreeAsync(d_n, st));
+    SLIP_CUDA(cudaStreamSynchronize(st));
+    SLIP_CHECK(theirs == mine, SLIP_EINVAL,
+               ("migrate_state: the peer's stage holds " + std::to_string(theirs) + " parameters, this one " +
+                std::to_string(mine) + " (bind the stage model of the role taken over first)")
+                   .c_str());
+  }
   float* bufs[3] = {ctx->master, ctx->adam_m, ctx->adam_v};
   // the sender's AdamW step count travels with the state, so the receiver continues
   // with the same bias correction as the peer it replicates

@@ -770,16 +770,18 @@ __global__ void synth_normal_kernel(bf16* __restrict__ out, int64_t n, uint2 key
 // X[t] = E[tok[t]] + P[t mod seq]: one warp per token row, 16-byte vectors.
 __global__ void __launch_bounds__(256) embed_fwd_kernel(const bf16* __restrict__ E, const bf16* __restrict__ P,
                                                         const int32_t* __restrict__ tok, bf16* __restrict__ X, int T,
-                                                        int h, int seq) {
+                                                        int h, int seq, int V) {
   ptx::grid_dep_wait();
   const int t = blockIdx.x * 8 + (threadIdx.x >> 5), lane = threadIdx.x & 31;
   if (t >= T) return;
-  const uint4* er = reinterpret_cast<const uint4*>(E + static_cast<int64_t>(tok[t]) * h);
+  const int v = tok[t];
+  const bool ok = v >= 0 && v < V;  // an id outside the vocabulary reads a zero embedding row
+  const uint4* er = reinterpret_cast<const uint4*>(E + static_cast<int64_t>(ok ? v : 0) * h);
   const uint4* pr = reinterpret_cast<const uint4*>(P + static_cast<int64_t>(t % seq) * h);
   uint4* xr = reinterpret_cast<uint4*>(X + static_cast<int64_t>(t) * h);
   for (int i = lane; i < h / 8; i += 32) {
     float a[8], b[8];
-    unpack8(er[i], a);
+    unpack8(ok ? er[i] : make_uint4(0, 0, 0, 0), a);
     unpack8(pr[i], b);
 #pragma unroll
     for (int e = 0; e < 8; ++e) a[e] += b[e];
@@ -793,13 +795,14 @@ __global__ void __launch_bounds__(256) embed_fwd_kernel(const bf16* __restrict__
 // position rows (sum over the micro-batch's sequences in order).
 __global__ void __launch_bounds__(256) embed_bwd_kernel(const bf16* __restrict__ dX, const int32_t* __restrict__ tok,
                                                         float* __restrict__ dE, float* __restrict__ dP, int T, int h,
-                                                        int seq, int accumulate) {
+                                                        int seq, int accumulate, int V) {
   ptx::grid_dep_wait();
   extern __shared__ int occ[];  // [T] occurrence list
   __shared__ int n_occ;
   const int b = blockIdx.x;
   if (b < T) {
     const int v = tok[b];
+    if (v < 0 || v >= V) return;  // an id outside the vocabulary has no embedding row
     if (threadIdx.x < 32) {
       const int lane = threadIdx.x;
       bool earlier = false;
@@ -882,7 +885,9 @@ __global__ void __launch_bounds__(512) ce_rows_kernel(bf16* __restrict__ logits,
   se = block_sum2(se, 0.f, red).x;
   const float lse = mx + logf(se);
   const int lab = labels[t];
-  const float zl = __bfloat162float(row[lab]);
+  // a label outside the vocabulary marks an ignored row: loss 0, dLogits 0
+  const bool ok = lab >= 0 && lab < V;
+  const float zl = ok ? __bfloat162float(row[lab]) : 0.f;
   __syncthreads();  // every thread has read row[lab] before any dLogits write
   const float inv_se = 1.f / se;
   uint4* w4 = reinterpret_cast<uint4*>(row);
@@ -890,10 +895,11 @@ __global__ void __launch_bounds__(512) ce_rows_kernel(bf16* __restrict__ logits,
     float a[8];
     unpack8(r4[i], a);
 #pragma unroll
-    for (int e = 0; e < 8; ++e) a[e] = (__expf(a[e] - mx) * inv_se - (8 * i + e == lab ? 1.f : 0.f)) * inv_T;
+    for (int e = 0; e < 8; ++e)
+      a[e] = ok ? (__expf(a[e] - mx) * inv_se - (8 * i + e == lab ? 1.f : 0.f)) * inv_T : 0.f;
     w4[i] = pack8(a);
   }
-  if (threadIdx.x == 0) row_loss[t] = lse - zl;
+  if (threadIdx.x == 0) row_loss[t] = ok ? lse - zl : 0.f;
 }
 
 __global__ void mean_kernel(const float* __restrict__ x, int n, float* __restrict__ out) {
@@ -1194,16 +1200,17 @@ cudaError_t synth_normal(bf16* out, int64_t n, uint64_t seed, uint64_t k, uint64
                     static_cast<uint32_t>(k), static_cast<uint32_t>(j));
 }
 
-cudaError_t embed_fwd(const bf16* E, const bf16* P, const int32_t* tok, bf16* X, int T, int h, int seq, cudaStream_t s) {
+cudaError_t embed_fwd(const bf16* E, const bf16* P, const int32_t* tok, bf16* X, int T, int h, int seq, int V,
+                      cudaStream_t s) {
   if (h % 8) return cudaErrorInvalidValue;
-  return launch_pdl(embed_fwd_kernel, dim3((T + 7) / 8), dim3(256), 0, s, 1, E, P, tok, X, T, h, seq);
+  return launch_pdl(embed_fwd_kernel, dim3((T + 7) / 8), dim3(256), 0, s, 1, E, P, tok, X, T, h, seq, V);
 }
 
-cudaError_t embed_bwd(const bf16* dX, const int32_t* tok, float* dE, float* dP, int T, int h, int seq, int accumulate,
-                      cudaStream_t s) {
+cudaError_t embed_bwd(const bf16* dX, const int32_t* tok, float* dE, float* dP, int T, int h, int seq, int V,
+                      int accumulate, cudaStream_t s) {
   if (T > 12288) return cudaErrorInvalidValue;  // occurrence list in shared memory
   return launch_pdl(embed_bwd_kernel, dim3(T + seq), dim3(256), static_cast<size_t>(T) * sizeof(int), s, 1, dX, tok,
-                    dE, dP, T, h, seq, accumulate);
+                    dE, dP, T, h, seq, accumulate, V);
 }
 
 cudaError_t cross_entropy(bf16* logits, const int32_t* labels, float* row_loss, float* loss, int T, int V,

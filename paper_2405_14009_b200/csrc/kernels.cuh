@@ -104,13 +104,15 @@ cudaError_t adamw_rollback(float* p, float* m, float* v, const float* g, bf16* w
                            cudaStream_t s, TailDecay tail = TailDecay());
 
 // ---- GPT model ends (reading R33)
-// X[t] = E[tok[t]] + P[t mod seq]   (bf16, [T, h])
-cudaError_t embed_fwd(const bf16* E, const bf16* P, const int32_t* tok, bf16* X, int T, int h, int seq, cudaStream_t s);
-// dE[v] (+)= sum_{t: tok_t = v} dX_t (one CTA per distinct token, t order), dP[p] (+)= sum_{t mod seq = p} dX_t
-cudaError_t embed_bwd(const bf16* dX, const int32_t* tok, float* dE, float* dP, int T, int h, int seq, int accumulate,
+// X[t] = E[tok[t]] + P[t mod seq]   (bf16, [T, h]); an id outside [0, V) reads a zero E row
+cudaError_t embed_fwd(const bf16* E, const bf16* P, const int32_t* tok, bf16* X, int T, int h, int seq, int V,
                       cudaStream_t s);
+// dE[v] (+)= sum_{t: tok_t = v} dX_t (one CTA per distinct token, t order; ids outside [0, V) skipped),
+// dP[p] (+)= sum_{t mod seq = p} dX_t
+cudaError_t embed_bwd(const bf16* dX, const int32_t* tok, float* dE, float* dP, int T, int h, int seq, int V,
+                      int accumulate, cudaStream_t s);
 // in place: logits [T, V] bf16 -> dLogits = (softmax - onehot(label)) / T; row_loss[t] = lse_t - logit_t[label_t];
-// then *loss = mean_t row_loss (fixed order)
+// then *loss = mean_t row_loss (fixed order).  A label outside [0, V) marks an ignored row (loss 0, dLogits 0).
 cudaError_t cross_entropy(bf16* logits, const int32_t* labels, float* row_loss, float* loss, int T, int V,
                           cudaStream_t s);
 cudaError_t synth_tokens(int32_t* out, int64_t n, int32_t n_classes, uint64_t seed, uint64_t k, uint64_t j,

@@ -451,7 +451,7 @@ slip_status embedding_grad(slip_ctx* c, SlotBufs& sb, int accumulate, cudaStream
   const Dims& D = c->dm;
   if (!accumulate)
     SLIP_CUDA(cudaMemsetAsync(c->grad + c->eo.E, 0, (static_cast<size_t>(D.V) + D.s) * D.h * sizeof(float), s));
-  return kcheck(c, embed_bwd(sb.dx, sb.end.tokens, c->grad + c->eo.E, c->grad + c->eo.P, D.T, D.h, D.s, 1, s),
+  return kcheck(c, embed_bwd(sb.dx, sb.end.tokens, c->grad + c->eo.E, c->grad + c->eo.P, D.T, D.h, D.s, D.V, 1, s),
                 "embed_bwd");
 }
 
@@ -663,7 +663,7 @@ slip_status slip_stage_forward(slip_ctx* c, int32_t slot, const void* x_in, void
   if (D.ends & 1) {  // x_in = T token ids: X = E[tok] + P[t mod seq]
     if (x_in != sb.end.tokens)
       SLIP_CUDA(cudaMemcpyAsync(sb.end.tokens, x_in, D.T * sizeof(int32_t), cudaMemcpyDeviceToDevice, s));
-    SLIP_TRY(kcheck(c, embed_fwd(c->w + c->eo.E, c->w + c->eo.P, sb.end.tokens, sb.x, D.T, D.h, D.s, s), "embed_fwd"));
+    SLIP_TRY(kcheck(c, embed_fwd(c->w + c->eo.E, c->w + c->eo.P, sb.end.tokens, sb.x, D.T, D.h, D.s, D.V, s), "embed_fwd"));
   } else if (x_in != sb.x) {
     SLIP_CUDA(cudaMemcpyAsync(sb.x, x_in, Th * sizeof(bf16), cudaMemcpyDeviceToDevice, s));
   }

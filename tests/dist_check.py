@@ -72,6 +72,19 @@ def stage_sum(t, me_live, me_stage, world):
     return tot.reshape(t.shape)
 
 
+def host_inputs(cfg, n, seed, gpt_ends):
+    """n micro-batches of pinned host inputs and targets: [T, h] bf16, or T int32 token
+    ids / labels with the GPT ends (the same lists on every rank)."""
+    g = torch.Generator().manual_seed(seed)
+    if gpt_ends:
+        mk = lambda: torch.randint(0, cfg.vocab, (cfg.tokens,), generator=g, dtype=torch.int32).pin_memory()  # noqa
+    else:
+        mk = lambda: torch.randn(cfg.tokens, cfg.hidden, generator=g).to(torch.bfloat16).pin_memory()  # noqa
+    xs = [mk() for _ in range(n)]
+    rs = [mk() for _ in range(n)]
+    return xs, rs
+
+
 def migrate_scenario(a, cfg, L, comm, costs, rank, world, holder):
     """Normalization swap on real GPUs (§4.2.1): one fault-free
     iteration; then worker (0, 0) fails; the planner's Algorithm 1 target is taken as
@@ -84,17 +97,22 @@ def migrate_scenario(a, cfg, L, comm, costs, rank, world, holder):
     moves), and all live peers of a stage bit-identical after the step."""
     DP, PP, m = a.dp, a.pp, a.m
     assert PP >= 2
-    g = torch.Generator().manual_seed(5)
-    xs = [torch.randn(cfg.tokens, cfg.hidden, generator=g).to(torch.bfloat16).pin_memory() for _ in range(DP * m)]
-    rs = [torch.randn(cfg.tokens, cfg.hidden, generator=g).to(torch.bfloat16).pin_memory() for _ in range(DP * m)]
+    xs, rs = host_inputs(cfg, DP * m, 5, a.gpt_ends)
     adam = (1e-3, 0.9, 0.95, 1e-8, 0.1)
     full = [[1] * DP for _ in range(PP)]
+
+    def role_cfg(role):  # the stage model of a role (the GPT ends differ by stage)
+        i = role % PP
+        ends = ((1 if i == 0 else 0) | (2 if i == PP - 1 else 0)) if a.gpt_ends else 0
+        return sd.ModelCfg(hidden=cfg.hidden, heads=cfg.heads, ffn=cfg.ffn, seq=cfg.seq,
+                           micro_batch=cfg.micro_batch, layers=cfg.layers, vocab=cfg.vocab, ends=ends)
 
     def fresh(role):
         if "stage" in holder:
             holder["stage"].close()
-        st = holder["stage"] = rt.Stage(cfg, L, n_slots=2 * m * DP)
-        rt.init_master_(st.master, cfg, L, cfg.layers, seed=100 + role % PP)
+        rc = role_cfg(role)
+        st = holder["stage"] = rt.Stage(rc, L, n_slots=2 * m * DP)
+        rt.init_master_(st.master, rc, L, rc.layers, seed=100 + role % PP)
         rt.call("slip_weights_from_master", st.ctx, rt._stream())
         return st
 
@@ -133,6 +151,8 @@ def migrate_scenario(a, cfg, L, comm, costs, rank, world, holder):
     t0 = torch.cuda.Event(enable_timing=True)
     t1 = torch.cuda.Event(enable_timing=True)
     t0.record()
+    if rank in (w_target, w_failed) and role_cfg(role[rank]).ends != role_cfg(rank).ends:
+        st = fresh(role[rank])  # bind the model of the role taken over (its state arrives next)
     if rank == w_src:
         rt.migrate_state(st, comm, w_target, True)
     elif rank == w_target:
@@ -147,7 +167,7 @@ def migrate_scenario(a, cfg, L, comm, costs, rank, world, holder):
     me_i, me_k = me_role % PP, me_role // PP
     me_live = after[me_i][me_k] == 1
     # the reference tensors of my role live on the process that played it in run A (= rank me_role)
-    refg, refp = torch.empty_like(gA), torch.empty_like(pA)
+    refg, refp = torch.empty_like(gB), torch.empty_like(pB)  # my role's model (may differ from run A's)
     ops = []
     for r in range(world):
         if role[r] != r:  # process r plays role[r]; run A's role[r] data sits on rank role[r]
@@ -206,9 +226,7 @@ def validate_scenario(a, cfg, L, comm, costs, rank, world, holder):
     step back (weights equal to after iteration 1 within the fp32 reversal error, one
     rollback).  Iteration 3 trains normally and all live peers stay bit-identical."""
     DP, PP, m = a.dp, a.pp, a.m
-    g = torch.Generator().manual_seed(5)
-    xs = [torch.randn(cfg.tokens, cfg.hidden, generator=g).to(torch.bfloat16).pin_memory() for _ in range(DP * m)]
-    rs = [torch.randn(cfg.tokens, cfg.hidden, generator=g).to(torch.bfloat16).pin_memory() for _ in range(DP * m)]
+    xs, rs = host_inputs(cfg, DP * m, 5, a.gpt_ends)
     adam = (1e-3, 0.9, 0.95, 1e-8, 0.1)
     full = [[1] * DP for _ in range(PP)]
     me_i = rank % PP
@@ -276,9 +294,7 @@ def fused_scenario(a, cfg, L, comm, costs, rank, world, holder):
     path (g_a + g_b is the same fp32 sum on both peers and in NCCL's 2-rank reduction)."""
     DP, PP, m = a.dp, a.pp, a.m
     me_i, me_k = rank % PP, rank // PP
-    g = torch.Generator().manual_seed(7)
-    xs = [torch.randn(cfg.tokens, cfg.hidden, generator=g).to(torch.bfloat16).pin_memory() for _ in range(DP * m)]
-    rs = [torch.randn(cfg.tokens, cfg.hidden, generator=g).to(torch.bfloat16).pin_memory() for _ in range(DP * m)]
+    xs, rs = host_inputs(cfg, DP * m, 7, a.gpt_ends)
     # fault-free, and (PP >= 2) one failed worker: its stage is a singleton (plain AdamW)
     # while the other stages stay fused — the mixed case of the executor's protocol
     cases = [[]] + ([[(PP - 1, 1)]] if PP >= 2 else [])

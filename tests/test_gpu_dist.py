@@ -121,3 +121,12 @@ def test_dp1_pp4_pipeline_gpt_ends_three_iterations():
     """A four-stage pipeline (the N = 8 default's depth) with the GPT ends, three iterations."""
     out = _run(4, 1, 4, "--gpt-ends", "--iters", "3")
     assert '"ok": true' in out and '"ok": false' not in out
+
+
+@pytest.mark.skipif(torch.cuda.device_count() < 4, reason="needs 4 GPUs")
+def test_dp2_pp2_normalization_swap_gpt_ends():
+    """The normalization swap when the roles moved hold different stage models (embedding
+    on stage 0, LM head on stage 1): the GPU taking over binds its new role's model, then
+    receives the state (slip_migrate_state checks that both sides agree on the size)."""
+    out = _run(4, 2, 2, "--gpt-ends", "--migrate")
+    assert '"ok": true' in out and '"ok": false' not in out

@@ -505,3 +505,52 @@ def test_dual_stream_with_gpt_ends_equals_single_stream():
         st.close()
     for a, b, what in zip(out[0], out[1], ("grad", "master", "m", "v", "w", "losses")):
         assert torch.equal(a, b), what
+
+
+def test_gpt_ends_out_of_range_ids_read_a_zero_row():
+    """Token ids outside [0, vocab) read a zero token-embedding row and receive no
+    gradient; labels outside it mark ignored tokens (include/slip.h).  Run A feeds three
+    invalid ids (-1, V + 7, 2^30) and one ignored label; run B feeds, at those positions,
+    an id v0 used nowhere else whose embedding row is zero in both runs.  Losses, weights
+    and every gradient except dE[v0] (which B fills from those positions) must be
+    bit-identical, and nothing reads or writes out of bounds."""
+    rt = _rt()
+    cfg = sd.ModelCfg(hidden=128, heads=2, ffn=512, seq=64, micro_batch=2, layers=1, vocab=384, ends=3)
+    L, m = 1, 1
+    layers = sd.stage_params(cfg, 0, L, total_layers=2)
+    ends = sd.end_params(cfg, 0)
+    tok = sd.stage_tokens(cfg, 0, 0).copy()
+    pos = [3, 17, 40]
+    v0 = int(next(v for v in range(cfg.vocab) if v not in set(np.delete(tok, pos).tolist())))
+    ends["E"] = ends["E"].copy()
+    ends["E"][v0] = 0.0
+    flat = np.concatenate([sd.pack_stage(layers), sd.pack_ends(ends)])
+    lab = sd.stage_labels(cfg, 0, 0).copy()
+    lab[5] = -100
+    costs = rt.make_costs(t_f=1, t_b=1, t_w=1, t_comm=0, t_ar=1, t_opt=1)
+    _, need = rt.rank_program(1, 1, m, None, costs, 0)
+    out = []
+    for bad in (True, False):
+        t = tok.copy()
+        t[pos] = [-1, cfg.vocab + 7, 2 ** 30] if bad else v0
+        st = rt.Stage(cfg, L, n_slots=need)
+        st.load_master(torch.from_numpy(flat).float().cuda())
+        comm = rt.Comm(0, 1)
+        comm.setup(1, 1, m, None)
+        losses = torch.zeros(m)
+        io = rt.make_io([torch.from_numpy(t)], [torch.from_numpy(lab)], losses)
+        rt.execute_schedule(st, comm, 1, 1, m, None, costs, adam=(1e-3, 0.9, 0.95, 1e-8, 0.1), iterations=1, io=io)
+        torch.cuda.synchronize()
+        out.append([st.grad.clone(), st.master.clone(), losses.clone()])
+        comm.close()
+        st.close()
+    (ga, pa, la), (gb, pb, lb) = out
+    assert torch.isfinite(ga).all() and torch.isfinite(la).all()
+    assert torch.equal(la, lb)
+    row = slice(L * cfg.params_per_layer + v0 * cfg.hidden, L * cfg.params_per_layer + (v0 + 1) * cfg.hidden)
+    assert not ga[row].any() and gb[row].any()
+    ga[row] = 0
+    gb[row] = 0
+    pa[row] = 0
+    pb[row] = 0
+    assert torch.equal(ga, gb) and torch.equal(pa, pb)
