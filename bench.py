@@ -74,6 +74,9 @@ def parse():
                          "(measured slower under the 1 kW power cap: off by default)")
     ap.add_argument("--dual-stream", default="auto", choices=["auto", "on", "off"],
                     help="forward actions on their own stream after profiling (auto: PP = 1 or m >= 4 PP)")
+    ap.add_argument("--validate", action="store_true",
+                    help="post-step validation with cross-stage rollback (slip_set_validation; PAPER.md lines "
+                         "580-583): the NCCL all-reduce and a single compute stream")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--model", default="1.3b", choices=sorted(MODELS), help="GPT shape (default: BASELINE configs[1])")
@@ -437,6 +440,9 @@ def main():
     # small m the overlapping forward competes with the backward chain across the stages,
     # the critical path there (DP2xPP2 m = 2: 321k -> 301k), so it stays off.
     dual = args.dual_stream == "on" or (args.dual_stream == "auto" and (PP == 1 or m >= 4 * PP))
+    if args.validate:  # validated steps keep the NCCL all-reduce (the rollback needs the sum in place)
+        rt.call("slip_set_validation", stage.ctx, 1)
+        dual = False
     rt.call("slip_set_dual_stream", stage.ctx, int(dual))
     # AdamW of the 2-D weights in the epilogue of the iteration's last W where no all-reduce
     # follows (N = 1; the survivor of a failed DP = 2 group) — slip_set_fused_adamw
@@ -612,7 +618,8 @@ def main():
                                    len(failed)),
                    "model": "gpt-%s-shape" % MODEL, "global_batch": DP * m * MB, "seq_len": SEQ,
                    "parallelism": "dp%dxpp%d" % (DP, PP), "failed_workers": failed, "sm_reserve": sm_reserve,
-                   "p2p_ctas": args.p2p_ctas, "fused_ar_adam": fused_ar, "dual_stream": dual,
+                   "p2p_ctas": args.p2p_ctas, "fused_ar_adam": fused_ar and not args.validate, "dual_stream": dual,
+                   "validated": args.validate,
                    "adamw_in_w_epilogue": fused_adamw,
                    "l2": "inputs larger than L2 (2.4 GB bf16 weights + GBs of stash per step)"},
         "clocks": clk,
