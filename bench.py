@@ -63,6 +63,9 @@ def parse():
     ap.add_argument("--sm-reserve", type=int, default=-1,
                     help="SMs kept free of persistent GEMM CTAs for NCCL kernels (default: 0 at N=1, 8 at N>1)")
     ap.add_argument("--p2p-ctas", type=int, default=2, help="CTAs per NCCL P2P kernel (0: NCCL default)")
+    ap.add_argument("--push-ar", action="store_true",
+                    help="fused DP = 2 all-reduce with the exchange in W: each W launch also writes its dW tiles "
+                         "into the peer's receive buffer over NVLink (slip_comm_fuse_ar_push)")
     ap.add_argument("--no-fused-ar", action="store_true",
                     help="NCCL all-reduce + AdamW instead of the DP=2 all-reduce fused into AdamW over NVLink")
     ap.add_argument("--trace", default="", help="directory: dump one traced 2-iteration run per rank (JSON)")
@@ -330,8 +333,11 @@ def main():
         comm.set_p2p_ctas(args.p2p_ctas)
     comm.setup(PP, DP, m, live)
     fused_ar = world > 1 and DP == 2 and not args.no_fused_ar
+
+    def fuse(st, cm):  # the DP = 2 all-reduce fused into AdamW (push: its exchange in W)
+        (rt.fuse_ar_push if (args.push_ar and not args.gpt_ends) else rt.fuse_ar_adam)(st, cm)
     if fused_ar:
-        rt.fuse_ar_adam(stage, comm)
+        fuse(stage, comm)
     stream = torch.cuda.current_stream()
 
     def allreduce_max(v):
@@ -376,7 +382,7 @@ def main():
             live = live2
             comm.setup(PP, DP, m, live)
             if fused_ar:
-                rt.fuse_ar_adam(stage, comm)
+                fuse(stage, comm)
         alg1_R = R2
         failed = [(i, k) for i in range(PP) for k in range(DP) if not live[i][k]]
     if args.normalize and failed:
@@ -426,7 +432,7 @@ def main():
         live = after
         comm.setup(PP, DP, m, live)
         if fused_ar:
-            rt.fuse_ar_adam(stage, comm)
+            fuse(stage, comm)
         norm = {"actual_failed": failed, "R": R, "swaps": swaps, "migration_ms": mig_ms,
                 "migration_warm_ms": mig_warm_ms, "state_bytes_per_swap": 12 * stage.n_params,
                 "migration_GBps": (12 * stage.n_params / (mig_warm_ms * 1e6)) if swaps and mig_warm_ms else None,
@@ -618,7 +624,8 @@ def main():
                                    len(failed)),
                    "model": "gpt-%s-shape" % MODEL, "global_batch": DP * m * MB, "seq_len": SEQ,
                    "parallelism": "dp%dxpp%d" % (DP, PP), "failed_workers": failed, "sm_reserve": sm_reserve,
-                   "p2p_ctas": args.p2p_ctas, "fused_ar_adam": fused_ar and not args.validate, "dual_stream": dual,
+                   "p2p_ctas": args.p2p_ctas, "fused_ar_adam": fused_ar and not args.validate,
+                   "ar_exchange_in_w": bool(fused_ar and args.push_ar and not args.gpt_ends and not args.validate), "dual_stream": dual,
                    "validated": args.validate,
                    "adamw_in_w_epilogue": fused_adamw,
                    "l2": "inputs larger than L2 (2.4 GB bf16 weights + GBs of stash per step)"},

@@ -404,6 +404,17 @@ slip_status slip_grad_allreduce(slip_ctx* ctx, slip_comm* comm, slip_stream s);
  * stage or re-running slip_comm_setup (which unmaps). */
 slip_status slip_comm_fuse_ar_adam(slip_ctx* ctx, slip_comm* comm, int32_t enable);
 
+/* The fused DP = 2 all-reduce + AdamW with the exchange moved into W (push mode): like
+ * slip_comm_fuse_ar_adam, and in addition each peer's W launches write their dW tiles,
+ * with the same TMA store / reduce-add as into its own gradient, into the OTHER peer's
+ * receive buffer over NVLink (a compute step fused with its collective, tile by tile).
+ * AdamW then reads the peer's 2-D weight gradients from its own receive buffer (local
+ * HBM) and only the 1-D parameters' (biases, LayerNorm) over NVLink.  recv: caller-
+ * allocated device buffer of n_params fp32 (torch allocation, IPC-exportable), written
+ * by the peer and read by this rank's AdamW; the results equal slip_comm_fuse_ar_adam's
+ * bit for bit.  Not for stages with a GPT end (SLIP_EUNSUPPORTED).  enable = 0 unmaps. */
+slip_status slip_comm_fuse_ar_push(slip_ctx* ctx, slip_comm* comm, float* recv, int32_t enable);
+
 /* The compute half of slip_comm_fuse_ar_adam for a caller that maps the peer's
  * gradient itself (e.g. one process driving both GPUs of a DP = 2 group with peer
  * access enabled): slip_optimizer_step on g_own + peer_grad[i] (the same fp32 sum

@@ -132,6 +132,7 @@ SIGNATURES = {
     "slip_comm_destroy": (C.c_int, [P]),
     "slip_grad_allreduce": (C.c_int, [P, P, P]),
     "slip_comm_fuse_ar_adam": (C.c_int, [P, P, I32]),
+    "slip_comm_fuse_ar_push": (C.c_int, [P, P, P, I32]),
     "slip_comm_set_role": (C.c_int, [P, I32]),
     "slip_comm_set_p2p_ctas": (C.c_int, [P, I32]),
     "slip_set_sm_reserve": (C.c_int, [I32]),

@@ -25,6 +25,11 @@ namespace {
 void close_fused(slip_comm* c) {
   if (c->ipc_grad_base) cudaIpcCloseMemHandle(c->ipc_grad_base);
   if (c->ipc_flag_base) cudaIpcCloseMemHandle(c->ipc_flag_base);
+  if (c->ipc_recv_base) cudaIpcCloseMemHandle(c->ipc_recv_base);
+  c->ipc_recv_base = nullptr;
+  c->my_recv = nullptr;
+  c->peer_recv = nullptr;
+  c->push = false;
   if (c->flags) cudaFree(c->flags);
   c->ipc_grad_base = c->ipc_flag_base = nullptr;
   c->flags = c->peer_flags = nullptr;
@@ -256,7 +261,24 @@ slip_status slip_migrate_state(slip_ctx* ctx, slip_comm* c, int32_t peer, int32_
   return SLIP_OK;
 }
 
+namespace {
+slip_status fuse_impl(slip_ctx* ctx, slip_comm* c, int32_t enable, float* recv);
+}
+
 slip_status slip_comm_fuse_ar_adam(slip_ctx* ctx, slip_comm* c, int32_t enable) {
+  return fuse_impl(ctx, c, enable, nullptr);
+}
+
+slip_status slip_comm_fuse_ar_push(slip_ctx* ctx, slip_comm* c, float* recv, int32_t enable) {
+  SLIP_CHECK(!enable || recv, SLIP_EINVAL, "comm_fuse_ar_push: recv is NULL");
+  SLIP_CHECK(!enable || !ctx || ctx->dm.ends == 0, SLIP_EUNSUPPORTED,
+             "comm_fuse_ar_push: stages with a GPT end (their embedding gradient is not written by W) use "
+             "slip_comm_fuse_ar_adam");
+  return fuse_impl(ctx, c, enable, enable ? recv : nullptr);
+}
+
+namespace {
+slip_status fuse_impl(slip_ctx* ctx, slip_comm* c, int32_t enable, float* recv) {
   SLIP_CHECK(ctx && ctx->bound && c && c->ready, SLIP_EINVAL, "comm_fuse_ar_adam: ctx not bound or comm not set up");
   close_fused(c);
   if (!enable || !c->my_live || !c->stage_comm) return SLIP_OK;  // nothing to fuse (singleton group)
@@ -281,13 +303,22 @@ slip_status slip_comm_fuse_ar_adam(slip_ctx* ctx, slip_comm* c, int32_t enable) 
   SLIP_CUDA(cudaMalloc(&c->flags, 256));
   SLIP_CUDA(cudaMemset(c->flags, 0, 256));
   struct Rec {
-    cudaIpcMemHandle_t grad, flag;
-    int64_t grad_off, n_params;
+    cudaIpcMemHandle_t grad, flag, recv;
+    int64_t grad_off, n_params, recv_off, has_recv;
   } mine{}, both[2];
   SLIP_CUDA(cudaIpcGetMemHandle(&mine.grad, reinterpret_cast<void*>(base)));
   SLIP_CUDA(cudaIpcGetMemHandle(&mine.flag, c->flags));
   mine.grad_off = static_cast<int64_t>(reinterpret_cast<CUdeviceptr>(ctx->grad) - base);
   mine.n_params = ctx->n_params;
+  if (recv) {  // push mode: the receive buffer the peer's W launches write
+    CUdeviceptr rbase = 0;
+    size_t rbytes = 0;
+    SLIP_CHECK(range(&rbase, &rbytes, reinterpret_cast<CUdeviceptr>(recv)) == CUDA_SUCCESS, SLIP_ECUDA,
+               "comm_fuse_ar_push: cuMemGetAddressRange(recv) failed");
+    SLIP_CUDA(cudaIpcGetMemHandle(&mine.recv, reinterpret_cast<void*>(rbase)));
+    mine.recv_off = static_cast<int64_t>(reinterpret_cast<CUdeviceptr>(recv) - rbase);
+    mine.has_recv = 1;
+  }
   void* dbuf = nullptr;
   SLIP_CUDA(cudaMalloc(&dbuf, 3 * sizeof(Rec)));
   // ordered before the all-gather on the same stream (a pageable cudaMemcpy on the legacy
@@ -313,6 +344,11 @@ slip_status slip_comm_fuse_ar_adam(slip_ctx* ctx, slip_comm* c, int32_t enable) 
   if (ok && oe == cudaSuccess) {
     oe = cudaIpcOpenMemHandle(&c->ipc_flag_base, peer.flag, cudaIpcMemLazyEnablePeerAccess);
     if (oe != cudaSuccess) c->ipc_flag_base = nullptr;
+  }
+  if (ok && recv && !peer.has_recv) ok = 0;  // push mode on one side only
+  if (ok && oe == cudaSuccess && recv) {
+    oe = cudaIpcOpenMemHandle(&c->ipc_recv_base, peer.recv, cudaIpcMemLazyEnablePeerAccess);
+    if (oe != cudaSuccess) c->ipc_recv_base = nullptr;
   }
   if (oe != cudaSuccess) {
     ok = 0;
@@ -343,8 +379,14 @@ slip_status slip_comm_fuse_ar_adam(slip_ctx* ctx, slip_comm* c, int32_t enable) 
   c->peer_flags = static_cast<unsigned*>(c->ipc_flag_base);
   c->fused_local = ctx->grad;
   c->fused_ar = true;
+  if (recv) {
+    c->my_recv = recv;
+    c->peer_recv = reinterpret_cast<float*>(static_cast<char*>(c->ipc_recv_base) + peer.recv_off);
+    c->push = true;
+  }
   return SLIP_OK;
 }
+}  // namespace
 
 slip_status slip_grad_allreduce(slip_ctx* ctx, slip_comm* c, slip_stream s) {
   SLIP_CHECK(ctx && ctx->bound && c && c->ready, SLIP_EINVAL, "grad_allreduce: ctx not bound or comm not set up");

@@ -42,6 +42,12 @@ struct slip_comm {
   void* ipc_grad_base = nullptr;   // opened IPC mappings (closed by destroy_setup)
   void* ipc_flag_base = nullptr;
   unsigned epoch = 0;
+  // push mode (slip_comm_fuse_ar_push): W writes its 2-D weight gradients into the peer's
+  // receive buffer as well (TMA over NVLink); AdamW reads them from this rank's own
+  bool push = false;
+  const float* my_recv = nullptr;  // this rank's receive buffer (the peer writes it)
+  float* peer_recv = nullptr;      // the peer's receive buffer (mapped)
+  void* ipc_recv_base = nullptr;
 };
 
 #define SLIP_NCCL(expr)                                          \

@@ -138,6 +138,14 @@ extern "C" slip_status slip_execute_schedule(slip_ctx* ctx, slip_comm* comm, con
   SLIP_CHECK(!fused_ar || comm->fused_local == ctx->grad, SLIP_ESTATE,
              "execute: gradient buffer re-bound since slip_comm_fuse_ar_adam");
 
+  // push mode (slip_comm_fuse_ar_push): this call's W launches also write the 2-D weight
+  // gradients into the peer's receive buffer (the W tables carry that mirror)
+  if (fused_ar && comm->push && ctx->w_mirror != comm->peer_recv) SLIP_TRY(slip::encode_w_tables(ctx, comm->peer_recv));
+  struct MirrorOn {
+    slip_ctx* c;
+    ~MirrorOn() { c->w_mirror_on = false; }
+  } mirror_guard{ctx};
+  ctx->w_mirror_on = fused_ar && comm->push;
   CallEvents& ce = call_events_[ctx];
   EventPool<false>& pool = ce.pool;
   EventPool<true>& tpool = ce.tpool;
@@ -511,7 +519,7 @@ extern "C" slip_status slip_execute_schedule(slip_ctx* ctx, slip_comm* comm, con
           SLIP_CUDA(trace_begin());
           if (fused_ar) {
             SLIP_TRY(slip::optimizer_step_peer(ctx, adam, ctx->opt_step, grad_scale, ctx->ws.nonfinite, stream,
-                                               comm->peer_grad));
+                                               comm->peer_grad, comm->push ? comm->my_recv : nullptr));
             // the OPT phase (a planner cost) ends with AdamW; the wait for the peer's AdamW
             // below is peer skew, not optimizer time
             if (marked) {

@@ -82,6 +82,7 @@ struct KParams {
   int band;  // grouped tile order: m-tile band width
   const GroupEntry* groups;  // grouped mode: problem table in device memory (nullptr otherwise)
   int n_groups;
+  int mirror;  // grouped fp32 epilogues: also write GroupEntry::tm (GemmDesc::c_mirror)
   // stream-K (see GemmDesc)
   int sk;              // 1: stream-K decomposition over sk_units CTA pairs
   int sk_units;
@@ -600,6 +601,13 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
               ptx::tma_reduce_add_4d(mC, buf, n, row0, tl.zi, tl.zo);
             else
               ptx::tma_store_4d(mC, buf, n, row0, tl.zi, tl.zo);
+            if (p.mirror && tl.g >= 0) {  // the same tile into the mirror (the DP peer's buffer)
+              const CUtensorMap* mM = &p.groups[tl.g].tm;
+              if (e_mode == EPI_F32_ACC && e_accum)
+                ptx::tma_reduce_add_4d(mM, buf, n, row0, tl.zi, tl.zo);
+              else
+                ptx::tma_store_4d(mM, buf, n, row0, tl.zi, tl.zo);
+            }
             ptx::bulk_commit();
           }
         } else {
@@ -800,6 +808,7 @@ cudaError_t launch_t(const GemmDesc& d, cudaStream_t s, const GroupEntry* groups
     p.accumulate = d.accumulate;
     p.groups = groups;
     p.n_groups = n_groups;
+    p.mirror = d.mirror;
     p.total = group_tiles;
     p.band = 8;  // measured: 2 / 4 / 8 / 16 / 32 -> W 15.03 / 14.93 / 14.74 / 14.84 / 15.06 ms
     if (d.mode == EPI_ADAMW) {
@@ -982,6 +991,9 @@ cudaError_t gemm_group_encode(const GemmDesc* probs, int n, GroupEntry* out, int
     const uint32_t b_rows = (probs[0].pair && probs[0].bn == 256) ? 128u : static_cast<uint32_t>(d.bn);
     if (!encode_operand(&g.tb, d.b, d.N, d.K, d.zi_count, 1, b_rows)) return cudaErrorInvalidValue;
     if (!encode4d(&g.tc, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, d.c, d.N, d.M, 1, 1, d.ldc, 0, 0, 32, 32))
+      return cudaErrorInvalidValue;
+    if (d.c_mirror &&
+        !encode4d(&g.tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, d.c_mirror, d.N, d.M, 1, 1, d.ldc, 0, 0, 32, 32))
       return cudaErrorInvalidValue;
     const int tile_m = (probs[0].pair && probs[0].bn == 256) ? 2 * BM : BM;
     g.M = d.M;

@@ -80,6 +80,11 @@ struct GemmDesc {
   int kz_list[8] = {};
   int64_t poff = -1;               // EPI_ADAMW: flat element offset of C (set per problem)
   const AdamEpi* adam = nullptr;   // EPI_ADAMW (grouped launch proto)
+  // Grouped fp32 epilogues: a second copy of C, written with the same TMA store / reduce-add
+  // (e.g. the DP peer's receive buffer over NVLink: the all-reduce's exchange fused into W).
+  // Per problem, encoded into GroupEntry::tm (nullptr: none); the proto's `mirror` enables it.
+  const void* c_mirror = nullptr;
+  int mirror = 0;
 };
 size_t gemm_sk_bytes();
 
@@ -93,6 +98,7 @@ cudaError_t gemm_launch(const GemmDesc& d, cudaStream_t s);
 // device-memory table (encoded once per slot at bind time).
 struct alignas(128) GroupEntry {
   CUtensorMap ta, tb, tc;
+  CUtensorMap tm;  // GemmDesc::c_mirror (zero when absent)
   int M, N, mt, nkb, tile_begin, tile_end;
   int64_t poff;  // EPI_ADAMW: flat element offset of the problem's C (GemmDesc::poff)
 };

@@ -589,19 +589,24 @@ __global__ void __launch_bounds__(256) adamw_kernel(float* __restrict__ p, float
                                                     float lr, float b1, float b2, float eps, float wd, float inv_bc1,
                                                     float inv_bc2, float grad_scale, int32_t* __restrict__ nonfinite,
                                                     const int32_t* __restrict__ skip,
-                                                    const float* __restrict__ g_peer) {
+                                                    const float* __restrict__ g_peer,
+                                                    const float* __restrict__ g_recv) {
   ptx::grid_dep_wait();
   if (skip && *skip) return;  // validated mode: this stage's gradients failed (no step)
   bool bad = false;
   const int64_t stride = static_cast<int64_t>(gridDim.x) * 256;
+  // where the peer's gradient of element group j is read: the 2-D weights from g_recv (the
+  // peer's W launches pushed them into this GPU's memory), the rest over NVLink
+  auto peer_src = [&](int64_t j) {
+    return reinterpret_cast<const float4*>((g_recv && decays(wr, 4 * j, per_layer)) ? g_recv : g_peer) + j;
+  };
   // the peer's gradient crosses NVLink at a few us of latency: its load for the next
   // iteration is issued before this one's local loads, two remote loads in flight
   float4 gp = make_float4(0.f, 0.f, 0.f, 0.f);
-  if (g_peer && blockIdx.x * 256LL + threadIdx.x < n4)
-    gp = __ldcs(reinterpret_cast<const float4*>(g_peer) + blockIdx.x * 256LL + threadIdx.x);
+  if (g_peer && blockIdx.x * 256LL + threadIdx.x < n4) gp = __ldcs(peer_src(blockIdx.x * 256LL + threadIdx.x));
   for (int64_t i = blockIdx.x * 256LL + threadIdx.x; i < n4; i += stride) {
     float4 gp_next = make_float4(0.f, 0.f, 0.f, 0.f);
-    if (g_peer && i + stride < n4) gp_next = __ldcs(reinterpret_cast<const float4*>(g_peer) + i + stride);
+    if (g_peer && i + stride < n4) gp_next = __ldcs(peer_src(i + stride));
     const int64_t e0 = 4 * i;
     const bool decay = decays(wr, e0, per_layer);
     const float wdl = decay ? wd : 0.f;
@@ -1137,7 +1142,8 @@ cudaError_t grad_check(const float* g, int64_t n, int32_t* bad, int32_t* nonfini
 
 cudaError_t adamw(float* p, float* m, float* v, const float* g, bf16* w, int64_t n, int64_t per_layer, int h, int f,
                   float lr, float b1, float b2, float eps, float wd, float bc1, float bc2, float grad_scale,
-                  int32_t* nonfinite, cudaStream_t s, const int32_t* skip, TailDecay tail, const float* g_peer) {
+                  int32_t* nonfinite, cudaStream_t s, const int32_t* skip, TailDecay tail, const float* g_peer,
+                  const float* g_recv) {
   if (n % 4 || per_layer % 4) return cudaErrorInvalidValue;
   const int64_t H = h, F = f;
   WdRanges wr;
@@ -1151,7 +1157,7 @@ cudaError_t adamw(float* p, float* m, float* v, const float* g, bf16* w, int64_t
   wr.d0 = wr.c1 + F;
   wr.d1 = wr.d0 + H * F;
   return launch_pdl(adamw_kernel, dim3(grid_for(n / 4)), dim3(256), 0, s, 1, p, m, v, g, w, n / 4, per_layer, wr, lr,
-                    b1, b2, eps, wd, 1.0f / bc1, 1.0f / bc2, grad_scale, nonfinite, skip, g_peer);
+                    b1, b2, eps, wd, 1.0f / bc1, 1.0f / bc2, grad_scale, nonfinite, skip, g_peer, g_recv);
 }
 
 cudaError_t adamw_vectors(float* p, float* m, float* v, const float* g, bf16* w, int layers, int64_t per_layer, int h,

@@ -86,8 +86,10 @@ struct TailDecay {
 cudaError_t adamw(float* p, float* m, float* v, const float* g, bf16* w, int64_t n, int64_t per_layer, int h, int f,
                   float lr, float b1, float b2, float eps, float wd, float bc1, float bc2, float grad_scale,
                   int32_t* nonfinite, cudaStream_t s, const int32_t* skip = nullptr, TailDecay tail = TailDecay(),
-                  const float* g_peer = nullptr);
+                  const float* g_peer = nullptr, const float* g_recv = nullptr);
 // g_peer (peer-mapped, may be NULL): the DP peer's gradient; the step uses g + g_peer.
+// g_recv (local, may be NULL): the peer's 2-D weight gradients pushed here by its W
+// launches (GemmDesc::c_mirror); read instead of g_peer for those elements.
 // AdamW over the layers' 1-D parameters only (the 2-D weights were stepped in the W GEMM
 // epilogue, gemm.cuh EPI_ADAMW); same per-element arithmetic (adamw_math.cuh).
 cudaError_t adamw_vectors(float* p, float* m, float* v, const float* g, bf16* w, int layers, int64_t per_layer, int h,

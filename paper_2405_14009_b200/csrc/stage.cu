@@ -462,6 +462,7 @@ slip_status backward_weight_impl(slip_ctx* c, int slot, int accumulate, cudaStre
   proto.a.mn_major = proto.b.mn_major = true;
   proto.mode = EPI_F32_ACC;
   proto.accumulate = accumulate;
+  proto.mirror = (c->w_mirror_on && c->w_mirror) ? 1 : 0;
   const int n_probs = 4 * c->L + ((c->dm.ends & 2) ? 1 : 0);
   cudaError_t e = gemm_group_launch(sb.wtab, n_probs, sb.wtab_tiles, proto, s);
   if (e != cudaSuccess) {
@@ -523,6 +524,50 @@ slip_status backward_input_impl(slip_ctx* c, int slot, const void* dy, void* dx,
 }
 
 }  // namespace
+
+
+// The W problem tables (tensor maps of the 4L weight-gradient GEMMs) of every slot, and
+// slot 0's table over all slots; with `mirror` each problem's output is also written to
+// the same offset of that buffer (GemmDesc::c_mirror: the DP peer's receive buffer).
+slip_status slip::encode_w_tables(slip_ctx* c, const float* mirror) {
+  const size_t per = stash_bytes_per_slot(c->dm, c->L);
+  auto with_mirror = [&](std::vector<GemmDesc>& probs) {
+    if (!mirror) return;
+    for (GemmDesc& d : probs) d.c_mirror = mirror + (static_cast<const float*>(d.c) - c->grad);
+  };
+  std::vector<GroupEntry> host(4 * static_cast<size_t>(c->L) + ((c->dm.ends & 2) ? 1 : 0));
+  for (int i = 0; i < c->n_slots; ++i) {
+    std::vector<GemmDesc> probs = w_problems(c, i);
+    with_mirror(probs);
+    int tiles = 0;
+    cudaError_t e = gemm_group_encode(probs.data(), static_cast<int>(probs.size()), host.data(), &tiles);
+    if (e != cudaSuccess) {
+      set_error(std::string("W table: ") + gemm_last_message());
+      return SLIP_EUNSUPPORTED;
+    }
+    SLIP_CUDA(cudaMemcpy(c->slots[i].wtab, host.data(), host.size() * sizeof(GroupEntry), cudaMemcpyHostToDevice));
+    c->slots[i].wtab_tiles = tiles;
+  }
+  if (c->n_slots >= 2) {  // slot 0's problems with the slot as the operands' zi dimension
+    std::vector<GemmDesc> probs = w_problems(c, 0);
+    with_mirror(probs);
+    const int64_t zs = static_cast<int64_t>(per / sizeof(bf16));
+    for (GemmDesc& d : probs) {
+      d.zi_count = c->n_slots;
+      d.a.zi_stride = zs;
+      d.b.zi_stride = zs;
+    }
+    int tiles = 0;
+    cudaError_t e = gemm_group_encode(probs.data(), static_cast<int>(probs.size()), host.data(), &tiles);
+    if (e != cudaSuccess) {
+      set_error(std::string("W all-slot table: ") + gemm_last_message());
+      return SLIP_EUNSUPPORTED;
+    }
+    SLIP_CUDA(cudaMemcpy(c->slots[0].wtab_all, host.data(), host.size() * sizeof(GroupEntry), cudaMemcpyHostToDevice));
+  }
+  c->w_mirror = mirror;
+  return SLIP_OK;
+}
 
 extern "C" {
 
@@ -612,35 +657,8 @@ slip_status slip_stage_bind(slip_ctx* c, void* w_bf16, float* master, float* gra
   SLIP_CUDA(cudaMemset(c->ws.tickets, 0, kTickets * sizeof(unsigned)));
   SLIP_CUDA(cudaMemset(c->ws.nonfinite, 0, sizeof(int32_t)));
   SLIP_CUDA(cudaMemset(c->ws.sk_flags, 0, static_cast<size_t>(num_sms()) * sizeof(unsigned)));
-  // W problem tables (tensor maps of the 4L weight-gradient GEMMs) per slot
-  std::vector<GroupEntry> host(4 * static_cast<size_t>(c->L) + ((c->dm.ends & 2) ? 1 : 0));
-  for (int i = 0; i < c->n_slots; ++i) {
-    std::vector<GemmDesc> probs = w_problems(c, i);
-    int tiles = 0;
-    cudaError_t e = gemm_group_encode(probs.data(), static_cast<int>(probs.size()), host.data(), &tiles);
-    if (e != cudaSuccess) {
-      set_error(std::string("stage_bind: W table: ") + gemm_last_message());
-      return SLIP_EUNSUPPORTED;
-    }
-    SLIP_CUDA(cudaMemcpy(c->slots[i].wtab, host.data(), host.size() * sizeof(GroupEntry), cudaMemcpyHostToDevice));
-    c->slots[i].wtab_tiles = tiles;
-  }
-  if (c->n_slots >= 2) {  // slot 0's problems with the slot as the operands' zi dimension
-    std::vector<GemmDesc> probs = w_problems(c, 0);
-    const int64_t zs = static_cast<int64_t>(per / sizeof(bf16));
-    for (GemmDesc& d : probs) {
-      d.zi_count = c->n_slots;
-      d.a.zi_stride = zs;
-      d.b.zi_stride = zs;
-    }
-    int tiles = 0;
-    cudaError_t e = gemm_group_encode(probs.data(), static_cast<int>(probs.size()), host.data(), &tiles);
-    if (e != cudaSuccess) {
-      set_error(std::string("stage_bind: W all-slot table: ") + gemm_last_message());
-      return SLIP_EUNSUPPORTED;
-    }
-    SLIP_CUDA(cudaMemcpy(c->slots[0].wtab_all, host.data(), host.size() * sizeof(GroupEntry), cudaMemcpyHostToDevice));
-  }
+  c->w_mirror = nullptr;
+  SLIP_TRY(slip::encode_w_tables(c, nullptr));
   c->state.assign(c->n_slots, SLOT_FREE);
   c->bound = true;
   return SLIP_OK;
@@ -705,6 +723,7 @@ slip_status weight_multi(slip_ctx* c, const int* slots, int n, int accumulate, c
   proto.mode = adam ? EPI_ADAMW : EPI_F32_ACC;
   proto.adam = adam;
   proto.accumulate = accumulate;
+  proto.mirror = (!adam && c->w_mirror_on && c->w_mirror) ? 1 : 0;
   proto.kz_n = n;
   proto.kz_nkb = (c->dm.T + 63) / 64;
   for (int j = 0; j < n; ++j) proto.kz_list[j] = slots[j];
@@ -794,7 +813,8 @@ slip_status slip::optimizer_step_vectors(slip_ctx* c, const slip_adam* a, int64_
 }
 
 slip_status slip::optimizer_step_peer(slip_ctx* c, const slip_adam* a, int64_t step, float grad_scale,
-                                      int32_t* d_nonfinite, slip_stream st, const float* peer_grad) {
+                                      int32_t* d_nonfinite, slip_stream st, const float* peer_grad,
+                                      const float* recv) {
   SLIP_CHECK(c && c->bound && a, SLIP_EINVAL, "optimizer_step: bad arguments");
   SLIP_CHECK(step >= 1, SLIP_EINVAL, "optimizer_step: step must be >= 1");
   const double bc1 = 1.0 - std::pow(static_cast<double>(a->beta1), static_cast<double>(step));
@@ -803,7 +823,7 @@ slip_status slip::optimizer_step_peer(slip_ctx* c, const slip_adam* a, int64_t s
                 adamw(c->master, c->adam_m, c->adam_v, c->grad, c->w, c->n_params, c->po.per_layer, c->dm.h, c->dm.f,
                       a->lr, a->beta1, a->beta2, a->eps, a->weight_decay, static_cast<float>(bc1),
                       static_cast<float>(bc2), grad_scale, d_nonfinite, reinterpret_cast<cudaStream_t>(st), nullptr,
-                      tail_decay(c), peer_grad),
+                      tail_decay(c), peer_grad, recv),
                 "adamw");
 }
 

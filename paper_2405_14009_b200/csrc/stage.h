@@ -110,6 +110,10 @@ struct slip_ctx {
   cudaStream_t bwd = nullptr;  // executor, dual stream: every other compute action (highest priority)
   int dual_stream = -1;        // slip_set_dual_stream (-1: the SLIP_DUAL_STREAM environment default)
   bool fuse_adamw = false;     // slip_set_fused_adamw: AdamW of the 2-D weights in the last W's epilogue
+  // W tables' mirror target (the DP peer's receive buffer, slip_comm_fuse_ar_push) and
+  // whether the W launches write it (set by the executor around its calls)
+  const float* w_mirror = nullptr;
+  bool w_mirror_on = false;
   int64_t opt_step = 0;  // AdamW steps taken by the executor
   bool trace_on = false;
   bool validate = false;   // post-step validation + cross-stage rollback (slip_set_validation)
@@ -139,6 +143,8 @@ slip_status validated_step(slip_ctx* c, const slip_adam* a, int64_t step, float 
                            cudaStream_t s, const int32_t* pre_flags = nullptr, int n_pre = 0);
 // The AdamW state / constants for the fused W epilogue (EPI_ADAMW) of step `step`, and
 // the OPT that then remains: AdamW over the layers' 1-D parameters only.
+// (re)encode the W problem tables, each output mirrored into `mirror` (nullptr: none)
+slip_status encode_w_tables(slip_ctx* c, const float* mirror);
 // drop the executor's caches of a context (slip_ctx_destroy)
 void executor_forget(const slip_ctx* ctx);
 AdamEpi adam_epilogue_args(slip_ctx* c, const slip_adam* a, int64_t step, float grad_scale);
@@ -147,7 +153,7 @@ slip_status optimizer_step_vectors(slip_ctx* c, const slip_adam* a, int64_t step
 // slip_optimizer_step with the DP peer's gradient added in (peer_grad peer-mapped, or
 // NULL): the DP = 2 all-reduce fused into AdamW (slip_comm_fuse_ar_adam).
 slip_status optimizer_step_peer(slip_ctx* c, const slip_adam* a, int64_t step, float grad_scale, int32_t* d_nonfinite,
-                                slip_stream st, const float* peer_grad);
+                                slip_stream st, const float* peer_grad, const float* recv = nullptr);
 slip_status rollback_if(slip_ctx* c, const slip_adam* a, int64_t step, float grad_scale, const int32_t* glob,
                         const int32_t* own, int32_t* count, cudaStream_t s);
 }  // namespace slip

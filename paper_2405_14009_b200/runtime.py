@@ -355,6 +355,18 @@ def fuse_ar_adam(stage: Stage, comm: Comm, enable=True):
     call("slip_comm_fuse_ar_adam", stage.ctx, comm.h, int(bool(enable)))
 
 
+def fuse_ar_push(stage: Stage, comm: Comm, enable=True):
+    """The fused DP = 2 all-reduce with the exchange moved into W (slip_comm_fuse_ar_push):
+    the peer's W writes its 2-D weight gradients into this stage's receive buffer (an
+    n_params fp32 tensor allocated here once)."""
+    import torch
+    if enable and getattr(stage, "recv", None) is None:
+        stage.recv = torch.zeros(stage.n_params, dtype=torch.float32, device=stage.grad.device)
+    recv = getattr(stage, "recv", None)
+    call("slip_comm_fuse_ar_push", stage.ctx, comm.h, _ptr(recv) if (enable and recv is not None) else None,
+         int(bool(enable)))
+
+
 def execute_schedule(stage: Stage, comm: Comm, N, DP, m, live, costs: slip_costs, decoupled=True, staggered=True,
                      adam=(1e-4, 0.9, 0.95, 1e-8, 0.1), warmup=0, iterations=1, seed=1234, io=None,
                      stream=None) -> slip_report:

@@ -312,7 +312,7 @@ def fused_scenario(a, cfg, L, comm, costs, rank, world, holder):
             rt.call("slip_weights_from_master", st.ctx, rt._stream())
             comm.setup(PP, DP, m, live)
             if fused:
-                rt.fuse_ar_adam(st, comm)
+                (rt.fuse_ar_push if a.push else rt.fuse_ar_adam)(st, comm)
             losses = torch.zeros(DP * m, dtype=torch.float32).pin_memory()
             rt.execute_schedule(st, comm, PP, DP, m, live, costs, True, True, adam=(1e-3, 0.9, 0.95, 1e-8, 0.1),
                                 iterations=2, io=rt.make_io(xs, rs, losses))
@@ -349,6 +349,8 @@ def main():
     ap.add_argument("--iters", type=int, default=1,
                     help="iterations per run: > 1 checks the replicas stay byte-identical over the steps "
                          "(losses then compared to the fault-free run within 1e-3, gradients within 1e-2)")
+    ap.add_argument("--push", action="store_true",
+                    help="with --fused-ar / --fuse-ar-main: the exchange moved into W (slip_comm_fuse_ar_push)")
     ap.add_argument("--fuse-ar-main", action="store_true",
                     help="the re-route scenarios with the DP = 2 all-reduce fused into AdamW (the bench default)")
     ap.add_argument("--gpt-ends", action="store_true",
@@ -385,7 +387,7 @@ def main():
         rt.call("slip_set_fused_adamw", stage.ctx, int(fused_adamw))
         comm.setup(PP, DP, m, live)
         if a.fuse_ar_main:
-            rt.fuse_ar_adam(stage, comm)
+            (rt.fuse_ar_push if a.push else rt.fuse_ar_adam)(stage, comm)
         losses = torch.zeros(DP * m, dtype=torch.float32).pin_memory()
         g = torch.Generator().manual_seed(5)
         if a.gpt_ends:  # token ids in, labels out (the same lists on every rank)

@@ -130,3 +130,23 @@ def test_dp2_pp2_normalization_swap_gpt_ends():
     receives the state (slip_migrate_state checks that both sides agree on the size)."""
     out = _run(4, 2, 2, "--gpt-ends", "--migrate")
     assert '"ok": true' in out and '"ok": false' not in out
+
+
+@pytest.mark.skipif(torch.cuda.device_count() < 2, reason="needs 2 GPUs")
+def test_dp2_fused_allreduce_push_into_w():
+    """slip_comm_fuse_ar_push: each peer's W launches also write their dW tiles into the
+    other's receive buffer (TMA over NVLink); AdamW reads them locally.  Master, m, v, the
+    bf16 weights and the losses equal the NCCL all-reduce + AdamW bit for bit, and the
+    re-route scenarios keep the replicas byte-identical over three iterations."""
+    out = _run(2, 2, 1, "--fused-ar", "--push")
+    assert '"ok": true' in out and '"ok": false' not in out
+    out = _run(2, 2, 1, "--iters", "3", "--fuse-ar-main", "--push")
+    assert '"ok": true' in out and '"ok": false' not in out
+
+
+@pytest.mark.skipif(torch.cuda.device_count() < 4, reason="needs 4 GPUs")
+def test_dp2_pp2_fused_allreduce_push_into_w():
+    """Push mode with two stages (several W launches per iteration: the mirror adds with
+    TMA reduce-add into the peer's buffer) and a failed worker (a singleton stage)."""
+    out = _run(4, 2, 2, "--fused-ar", "--push")
+    assert '"ok": true' in out and '"ok": false' not in out
