@@ -353,6 +353,8 @@ def main():
                     help="with --fused-ar / --fuse-ar-main: the exchange moved into W (slip_comm_fuse_ar_push)")
     ap.add_argument("--fuse-ar-main", action="store_true",
                     help="the re-route scenarios with the DP = 2 all-reduce fused into AdamW (the bench default)")
+    ap.add_argument("--ragged", action="store_true",
+                    help="a ragged stage shape (h 640, 8 heads of d = 80, s = 200: partial tiles everywhere)")
     ap.add_argument("--gpt-ends", action="store_true",
                     help="GPT ends: token + position embedding on stage 0, final LN + LM head + CE on the last stage")
     a = ap.parse_args()
@@ -365,7 +367,11 @@ def main():
     me_i, me_k = rank % PP, rank // PP
     vocab = 1024 if a.gpt_ends else 0
     ends = ((1 if me_i == 0 else 0) | (2 if me_i == PP - 1 else 0)) if a.gpt_ends else 0
-    cfg = sd.ModelCfg(hidden=256, heads=4, ffn=1024, seq=256, micro_batch=1, layers=2 * PP, vocab=vocab, ends=ends)
+    if a.ragged:
+        cfg = sd.ModelCfg(hidden=640, heads=8, ffn=2560, seq=200, micro_batch=1, layers=2 * PP, vocab=vocab, ends=ends)
+    else:
+        cfg = sd.ModelCfg(hidden=256, heads=4, ffn=1024, seq=256, micro_batch=1, layers=2 * PP, vocab=vocab,
+                          ends=ends)
     L = 2
     if a.failures == "auto":
         scenarios = [[(PP - 1, 1)], [(0, 0)]] + ([[(PP - 1, 1), (0, 0)]] if PP > 1 else [])

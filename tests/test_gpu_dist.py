@@ -150,3 +150,11 @@ def test_dp2_pp2_fused_allreduce_push_into_w():
     TMA reduce-add into the peer's buffer) and a failed worker (a singleton stage)."""
     out = _run(4, 2, 2, "--fused-ar", "--push")
     assert '"ok": true' in out and '"ok": false' not in out
+
+
+@pytest.mark.skipif(torch.cuda.device_count() < 4, reason="needs 4 GPUs")
+def test_dp2_pp2_reroute_ragged_shape():
+    """A ragged stage (h 640, d = 80, s = 200) through re-routing with the fused all-reduce
+    and two iterations: partial GEMM / attention tiles in every P2P-fed stage."""
+    out = _run(4, 2, 2, "--ragged", "--iters", "2", "--fuse-ar-main")
+    assert '"ok": true' in out and '"ok": false' not in out
