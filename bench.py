@@ -223,6 +223,9 @@ def run_reference(args, rank, world):
 
 # ---------------------------------------------------------------- GPU arm
 def main():
+    if os.environ.get("SLIP_BENCH_DUMP_AFTER"):  # debugging aid: Python stacks of a hung run
+        import faulthandler
+        faulthandler.dump_traceback_later(float(os.environ["SLIP_BENCH_DUMP_AFTER"]), exit=True)
     args = parse()
     rank = int(os.environ.get("RANK", 0))
     world = int(os.environ.get("WORLD_SIZE", 1))
